@@ -1,0 +1,322 @@
+"""dSMC smoothing throughput on B200: smoothed particle-timesteps/s (T.N/s).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c2|c1|c3|c5]
+
+A step is one full dSMC smoothing run (leaves -> ceil(log2 K) combine levels
+-> ancestor composition -> per-time mean/cov) over the configuration's
+synthetic trajectory (BASELINE.json configs; default C2: 2-D constant-velocity
+LGSSM, d = 4, K = T+1 = 2^14, N = 1024, multinomial stitching, FP32).
+
+  value  = K.N / device time per step, inputs (prepared model) resident in HBM,
+           CUDA events on the engine's stream, max over ranks.
+  e2e    = the same metric through the public C ABI call dsmc_smooth with host
+           (pinned) model arrays: H2D upload + per-time prep + run + D2H of the
+           moments inside the timed region, host wall clock.
+  roofline = the pair kernel (c32_pair) against the MUFU.EX2 roofline: 1 exp2
+           per pair evaluation; algorithmic work = (combines per level) x N^2
+           pair evaluations per launch.
+  cpu_baseline / --impl reference = the reference's own run_smoother compiled
+           from /root/reference (oracle/_ref/libdsmc_ref.so) on all host
+           threads, on a bounded sample (fewer leaves) of the same workload.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(desc="C1: d=1 LGSSM (experiment.hpp lgssm-check), K=T+1=2^10, N=100, multinomial",
+               model="lgssm", K=1 << 10, N=100, resampler=0),
+    "c2": dict(desc="C2: 2-D constant-velocity LGSSM d=4, K=T+1=2^14, N=1024, multinomial, "
+                    "RTS-marginal proposals", model="cv", K=1 << 14, N=1024, resampler=0),
+    "c3": dict(desc="C3: stochastic volatility, K=T+1=2^16, N=4096, MH-lazy (B=16)",
+               model="sv", K=1 << 16, N=4096, resampler=2),
+    "c5": dict(desc="C5: 2-D constant-velocity LGSSM d=4, K=T+1=2^20, N=1024, multinomial",
+               model="cv", K=1 << 20, N=1024, resampler=0),
+}
+METRIC = "smoothed particle-timesteps/sec (T·N/s)"
+UNIT = "particle-timesteps/s"
+
+
+def build_model(cfg, pinned=False):
+    from paper_2202_02264_b200 import abi, models
+    T = cfg["K"] - 1
+    if cfg["model"] == "cv":
+        m = models.cv_tracking(T)
+    elif cfg["model"] == "lgssm":
+        m = models.lgssm_check(T)
+    else:
+        m = models.sv(T)
+    if pinned:
+        import torch
+        arrays = {}
+        for k, v in m.arrays.items():
+            if v is None:
+                arrays[k] = None
+                continue
+            dt = {np.float64: torch.float64, np.uint8: torch.uint8}[v.dtype.type]
+            t = torch.empty(v.shape, dtype=dt, pin_memory=True)
+            a = t.numpy()
+            a[...] = v
+            arrays[k] = a
+            arrays.setdefault("_hold", []).append(t)
+        hold = arrays.pop("_hold")
+        kw = dict(arrays)
+        if m.kind == abi.MODEL_SV:
+            kw["sv"] = m.sv
+        pm = abi.Model(m.kind, m.horizon, m.d, m.dy, **kw)
+        pm._hold = hold
+        return pm
+    return m
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_reference(cfg, budget_s=8.0):
+    """Reference run_smoother (compiled from /root/reference) on a bounded
+    sample: K' leaves with the same N, d, model family; doubles K' until the
+    run takes >= budget_s / 4. Returns (T.N/s, cores, sample text)."""
+    from oracle.py import Reference
+    if not Reference.available():
+        return None
+    R = Reference()
+    threads = host_threads()
+    Kp = 16
+    while True:
+        sub = dict(cfg, K=Kp)
+        m = build_model(sub)
+        t0 = time.perf_counter()
+        r = R.run_smoother(m, cfg["N"], cfg["resampler"], seed=1, mh_steps=16, threads=threads,
+                           want_paths=False)
+        wall = time.perf_counter() - t0
+        if wall >= budget_s / 4 or Kp >= cfg["K"]:
+            break
+        Kp *= 2
+    val = Kp * cfg["N"] / wall
+    sample = (f"reference run_smoother (oracle/_ref, compiled from /root/reference) on "
+              f"K'={Kp} leaves (T'={Kp - 1}), N={cfg['N']}, same model family, {threads} threads, "
+              f"wall {wall:.2f} s (RunMetadata wall {r['wall_time_ms']:.0f} ms); dense cost is "
+              f"exactly T*N^2 pair evaluations so T*N/s does not depend on T")
+    return val, threads, sample, wall
+
+
+class ClockSampler:
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", q, "--format=csv,noheader,nounits",
+                                      f"--id={self.device}"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 4 + i and s[4 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def sfu_peak_pairs_per_s(sm_max_mhz):
+    """Pair-kernel peak: 1 MUFU.EX2 per pair. Measured ex2 rate if profiled
+    (profiles/sfu_peak.json), else the nominal 16/clk/SM x 148 SMs."""
+    p = os.path.join(ROOT, "profiles", "sfu_peak.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["ex2_per_s"]), "measured (profiles/sfu_peak.json)"
+    mhz = sm_max_mhz or 1965.0
+    return 148 * 16 * mhz * 1e6, "nominal 16 ex2/clk/SM x 148 SMs at sm_max_mhz"
+
+
+def run_ours(args, cfg, rank, world, device):
+    import torch
+    from paper_2202_02264_b200 import abi
+    from paper_2202_02264_b200.dsmc import Engine
+
+    torch.cuda.set_device(device)
+    eng = Engine(device)
+    model = build_model(cfg, pinned=True)
+    K, N, d = cfg["K"], cfg["N"], model.d
+    seed_base = 1 + (1 << 32)
+    # ---- device-resident throughput (value)
+    h = eng.upload(model)
+    eng.sync()
+    for w in range(args.warmup):
+        eng.smooth_resident(h, N, cfg["resampler"], seed=seed_base + w)
+    eng.sync()
+    stream = torch.cuda.ExternalStream(eng.stream_handle())
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = eng.launches
+    with ClockSampler(device) as clocks:
+        start.record(stream)
+        for s in range(args.steps):
+            eng.smooth_resident(h, N, cfg["resampler"], seed=seed_base + 1000 + s)
+        end.record(stream)
+        torch.cuda.synchronize()
+    launches = eng.launches - launches0
+    ms = start.elapsed_time(end) / args.steps
+    timings = eng.timings()
+    mean, cov, lnc = eng.resident_results(K, d)
+    ms_t = torch.tensor([ms], device=f"cuda:{device}")
+    if world > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = world * K * N / (ms_max * 1e-3)
+    # ---- end to end through the public API (host pinned in, host out)
+    h2d = sum(a.nbytes for a in model.arrays.values() if a is not None)
+    d2h = K * d * 8 + K * d * d * 8 + 8
+    e2e_steps = max(3, min(args.steps, 10))
+    eng.smooth(model, N, cfg["resampler"], seed=7)  # warm (pool allocations)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s in range(e2e_steps):
+        eng.smooth(model, N, cfg["resampler"], seed=seed_base + 5000 + s)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_t = torch.tensor([e2e_s], device=f"cuda:{device}")
+    if world > 1:
+        torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
+    e2e_val = world * K * N / float(e2e_t.item())
+    eng.free_model(h)
+    out = None
+    if rank == 0:
+        ck = clocks.summary()
+        pair_ms = timings[3] if len(timings) > 3 else None
+        pairs_total = (K - 1) * N * N
+        peak, peak_src = sfu_peak_pairs_per_s(ck.get("sm_max_mhz"))
+        ach = pairs_total / (pair_ms * 1e-3) if pair_ms else None
+        roof = {"bound": "sfu", "kernel": "c32_pair", "achieved": ach, "peak": peak,
+                "unit": "pair-evals/s (1 MUFU.EX2 each)", "frac": ach / peak if ach else None,
+                "peak_source": peak_src, "traffic": None,
+                "pair_kernel_ms_per_step": pair_ms,
+                "sample_kernel_ms_per_step": timings[4] if len(timings) > 4 else None,
+                "pair_kernel_share_of_step": pair_ms / ms if pair_ms else None,
+                "leaf_ms": timings[0], "levels_ms": timings[1], "compose_gather_ms": timings[2]}
+        prof = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(prof):
+            roof["traffic"] = json.load(open(prof)).get(args.config)
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (simulated trajectory, numpy seed 90210; RTS-marginal proposals)",
+            "config": {"workload": cfg["desc"], "K": K, "T": K - 1, "N": N, "d": d,
+                       "resampler": ["multinomial", "systematic", "mh-lazy",
+                                     "rejection-lazy"][cfg["resampler"]],
+                       "precision": "fp32 throughput path",
+                       "l2": "inputs larger than L2 (leaf slab %.0f MB > 126 MB)" % (K * N * 16 / 1e6),
+                       "parallelism": f"time-sharded x{world}" if world > 1 else "single GPU"},
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "api": "dsmc_smooth (C ABI), host pinned arrays"},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "clocks": ck,
+            "log_norm_const_last": lnc,
+        }
+    eng.close()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=list(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        # the reference's CPU run_smoother on all host threads, bounded sample
+        from oracle.py import Reference
+        if not Reference.available():
+            print(json.dumps({"impl": "reference", "unavailable":
+                              "oracle/_ref/libdsmc_ref.so not built (needs /root/reference)"}))
+            return
+        vals = []
+        for s in range(args.warmup + args.steps):
+            v, cores, sample, wall = cpu_reference(cfg, budget_s=4.0)
+            if s >= args.warmup:
+                vals.append(v)
+        val = float(np.median(vals))
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "K": cfg["K"], "N": cfg["N"]},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }))
+        return
+
+    if world > 1:
+        import torch
+        torch.distributed.init_process_group("nccl")
+    out = run_ours(args, cfg, rank, world, local)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            cb = cpu_reference(cfg)
+            if cb is not None:
+                v, cores, sample, wall = cb
+                out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores,
+                                       "kind": "reference", "sample": sample}
+        print(json.dumps(out))
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

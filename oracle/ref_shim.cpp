@@ -1,0 +1,329 @@
+// ORACLE / TEST INFRASTRUCTURE ONLY.
+//
+// C API over the compiled reference (oracle/_ref/libdsmc_ref.so): the
+// reference's own rng.cpp, kernels/*.cpp, resampling.cpp, fk_model.cpp,
+// smoother.cpp, conditional.cpp compiled unmodified from /root/reference
+// (see oracle/Makefile). Used by tests/ (golden vectors, parity) and by
+// bench.py's CPU baseline leg; never by the product.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dsmc/conditional.hpp"
+#include "dsmc/fk_model.hpp"
+#include "dsmc/kernels.hpp"
+#include "dsmc/metrics.hpp"
+#include "dsmc/resampling.hpp"
+#include "dsmc/rng.hpp"
+#include "dsmc/smoother.hpp"
+#include "dsmc_b200.h"
+#include "ref_models.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    g_err.clear();
+    return DSMC_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return DSMC_E_INVALID_ARGUMENT;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return DSMC_E_DOMAIN;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return DSMC_E_LOGIC;
+  } catch (const std::runtime_error& e) {
+    g_err = e.what();
+    return DSMC_E_RUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return DSMC_E_RUNTIME;
+  }
+}
+
+dsmc::StreamKey key_of(uint64_t seed, uint32_t level, uint64_t node, int role) {
+  return dsmc::StreamKey{seed, level, node, static_cast<dsmc::StreamRole>(role)};
+}
+
+dsmc::PairWeightSource table_source(const double* logw, std::size_t n,
+                                    int has_bound, double bound) {
+  std::vector<double> tab(logw, logw + n * n);
+  dsmc::PairWeightSource src;
+  src.n = n;
+  src.fill_row = [tab, n](std::size_t i, double* out) {
+    std::memcpy(out, tab.data() + i * n, n * sizeof(double));
+  };
+  src.log_weight_at = [tab, n](std::size_t i, std::size_t j) {
+    return tab[i * n + j];
+  };
+  if (has_bound) src.log_upper_bound = bound;
+  return src;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+void ref_philox(const uint64_t ctr[4], const uint64_t key[2], uint64_t out[4]) {
+  auto r = dsmc::rng_detail::philox4x64_10({ctr[0], ctr[1], ctr[2], ctr[3]},
+                                           {key[0], key[1]});
+  for (int i = 0; i < 4; ++i) out[i] = r[i];
+}
+
+// kind: 0 next_u64, 1 uniform, 2 uniform_pos, 3 normal
+void ref_stream(uint64_t seed, uint32_t level, uint64_t node, int role,
+                uint64_t substream, int kind, size_t n, void* out) {
+  dsmc::RngStream s(key_of(seed, level, node, role), substream);
+  for (size_t i = 0; i < n; ++i) {
+    switch (kind) {
+      case 0: static_cast<uint64_t*>(out)[i] = s.next_u64(); break;
+      case 1: static_cast<double*>(out)[i] = s.uniform(); break;
+      case 2: static_cast<double*>(out)[i] = s.uniform_pos(); break;
+      default: static_cast<double*>(out)[i] = s.normal(); break;
+    }
+  }
+}
+
+int ref_set_backend(int b) {
+  return guarded([&] {
+    dsmc::kernels::set_active(static_cast<dsmc::kernels::Backend>(b));
+  });
+}
+int ref_active_backend() { return static_cast<int>(dsmc::kernels::active()); }
+
+double ref_exp_w(double x) { return dsmc::kernels::exp_w(x); }
+void ref_vec_exp(const double* x, size_t n, double* out) {
+  dsmc::kernels::vec_exp(x, n, out);
+}
+double ref_reduce_sum(const double* x, size_t n) {
+  return dsmc::kernels::reduce_sum(x, n);
+}
+int ref_reduce_max(const double* x, size_t n, double* out) {
+  return guarded([&] { *out = dsmc::kernels::reduce_max(x, n); });
+}
+double ref_log_sum_exp(const double* x, size_t n) {
+  return dsmc::kernels::log_sum_exp(x, n);
+}
+double ref_exp_row_store(const double* logw, size_t n, double shift, double* w,
+                         double* sub) {
+  return dsmc::kernels::exp_row_store(logw, n, shift, w, sub);
+}
+void ref_gaussian_row(const double* x, size_t n, double mean, double c,
+                      const double* base, double* out) {
+  dsmc::kernels::gaussian_row(x, n, mean, c, base, out);
+}
+
+void ref_metrics_reset() { dsmc::metrics::reset(); }
+void ref_metrics(uint64_t out[4]) {
+  auto s = dsmc::metrics::snapshot();
+  out[0] = s.weight_evals;
+  out[1] = s.dense_allocs;
+  out[2] = s.dense_max_elems;
+  out[3] = s.lazy_max_elems;
+}
+
+int ref_resample_table(int resampler, const double* logw, size_t n,
+                       size_t n_out, size_t mh_steps, int has_bound,
+                       double bound, uint64_t seed, uint32_t level,
+                       uint64_t node, uint32_t* left, uint32_t* right,
+                       double* lmw, int* has_lmw, uint64_t* evals,
+                       int* biased) {
+  return guarded([&] {
+    auto src = table_source(logw, n, has_bound, bound);
+    auto ps = dsmc::resample_pairs(static_cast<dsmc::Resampler>(resampler), src,
+                                   n_out, mh_steps,
+                                   key_of(seed, level, node,
+                                          DSMC_ROLE_PAIR_RESAMPLE));
+    std::memcpy(left, ps.left.data(), sizeof(uint32_t) * n_out);
+    std::memcpy(right, ps.right.data(), sizeof(uint32_t) * n_out);
+    *has_lmw = ps.log_mean_weight.has_value() ? 1 : 0;
+    *lmw = ps.log_mean_weight.value_or(NAN);
+    *evals = ps.weight_evals;
+    *biased = ps.biased ? 1 : 0;
+  });
+}
+
+// pairs: 5 ints per pair (level, node, left_a, left_b, right_b).
+int ref_build_schedule(int horizon, int* levels, int* pairs) {
+  return guarded([&] {
+    auto s = dsmc::build_schedule(horizon);
+    *levels = s.levels;
+    for (size_t k = 0; k < s.pairs.size(); ++k) {
+      const auto& p = s.pairs[k];
+      int* o = pairs + 5 * k;
+      o[0] = p.level;
+      o[1] = p.node;
+      o[2] = p.left_a;
+      o[3] = p.left_b;
+      o[4] = p.right_b;
+    }
+  });
+}
+int ref_tree_depth(int horizon) { return dsmc::reference_tree_depth(horizon); }
+
+// make_leaf (smoother.cpp:98-130): states, normalized log weights, flags,
+// plus the raw leaf weights (fk_model.cpp:101-112) for injection.
+int ref_make_leaf(const dsmc_model_desc* desc, int t, size_t n, uint64_t seed,
+                  double* x, double* raw_lw, double* norm_lw, int* uniform,
+                  double* lnc) {
+  return guarded([&] {
+    auto model = oracle::build_model(*desc);
+    auto blk = dsmc::make_leaf(model, t, n, seed);
+    std::memcpy(x, blk.paths.data(), sizeof(double) * blk.paths.size());
+    if (norm_lw) std::memcpy(norm_lw, blk.log_w.data(), sizeof(double) * n);
+    if (raw_lw) dsmc::leaf_weights(model, t, blk.paths.data(), n, raw_lw);
+    *uniform = blk.weights_uniform ? 1 : 0;
+    *lnc = blk.log_norm_const.value_or(NAN);
+  });
+}
+
+// Stitch-row fill of the reference model for one combine (the dense table
+// the reference would build), for table-level parity checks.
+int ref_stitch_rows(const dsmc_model_desc* desc, int c, const double* xl,
+                    const double* xr, size_t n, double* out) {
+  return guarded([&] {
+    auto model = oracle::build_model(*desc);
+    auto row = dsmc::make_stitch_row(model, c, xr, n);
+    const int d = model.state_dim;
+    for (size_t i = 0; i < n; ++i) row(xl + i * d, out + i * n);
+  });
+}
+
+// Scalar log_stitch_weight (fk_model.cpp:61-73).
+int ref_stitch_weight(const dsmc_model_desc* desc, int c, const double* xp,
+                      const double* xc, double* out) {
+  return guarded([&] {
+    auto model = oracle::build_model(*desc);
+    *out = dsmc::log_stitch_weight(model, c, xp, xc);
+  });
+}
+
+int ref_stitch_bound(const dsmc_model_desc* desc, int c, double* out) {
+  return guarded([&] {
+    auto model = oracle::build_model(*desc);
+    if (!model.log_stitch_bound)
+      throw std::invalid_argument("model has no stitch bound");
+    *out = model.log_stitch_bound(c);
+  });
+}
+
+// run_smoother (smoother.cpp:226-277) unchanged; root paths + metadata.
+int ref_run_smoother(const dsmc_model_desc* desc, size_t n, int resampler,
+                     size_t mh_steps, uint64_t seed, int threads,
+                     double* root_paths, double* lnc, int* has_lnc,
+                     uint64_t* evals, int* levels, int* biased,
+                     double* wall_ms) {
+  return guarded([&] {
+    auto model = oracle::build_model(*desc);
+    dsmc::SmootherOptions o;
+    o.n_particles = n;
+    o.resampler = static_cast<dsmc::Resampler>(resampler);
+    o.mh_steps = mh_steps;
+    o.seed = seed;
+    o.n_threads = threads;
+    auto res = dsmc::run_smoother(model, o);
+    if (root_paths)
+      std::memcpy(root_paths, res.root.paths.data(),
+                  sizeof(double) * res.root.paths.size());
+    *has_lnc = res.meta.log_norm_const.has_value() ? 1 : 0;
+    *lnc = res.meta.log_norm_const.value_or(NAN);
+    *evals = res.meta.weight_evals;
+    *levels = res.meta.levels;
+    *biased = res.meta.biased ? 1 : 0;
+    *wall_ms = res.meta.wall_time_ms;
+  });
+}
+
+// The same run, level by level through the public pieces (make_leaf,
+// make_pair_source, resample_pairs, combine_blocks), recording every
+// combine's (left, right) pairs and log mean weight in schedule order.
+int ref_trace_smoother(const dsmc_model_desc* desc, size_t n, int resampler,
+                       size_t mh_steps, uint64_t seed, double* root_paths,
+                       uint32_t* pair_left, uint32_t* pair_right,
+                       double* pair_lmw, double* lnc, int* has_lnc) {
+  return guarded([&] {
+    auto model = oracle::build_model(*desc);
+    dsmc::SmootherOptions o;
+    o.n_particles = n;
+    o.resampler = static_cast<dsmc::Resampler>(resampler);
+    o.mh_steps = mh_steps;
+    o.seed = seed;
+    const int T = model.horizon;
+    std::vector<dsmc::BlockEstimate> cur(T + 1);
+    for (int t = 0; t <= T; ++t) cur[t] = dsmc::make_leaf(model, t, n, seed);
+    int level = 0;
+    size_t cursor = 0;
+    while (cur.size() > 1) {
+      ++level;
+      const size_t np = cur.size() / 2;
+      std::vector<dsmc::BlockEstimate> next(np + cur.size() % 2);
+      for (size_t k = 0; k < np; ++k) {
+        const auto& L = cur[2 * k];
+        const auto& R = cur[2 * k + 1];
+        auto bundle = dsmc::make_pair_source(model, L, R);
+        auto ps = dsmc::resample_pairs(
+            o.resampler, bundle.source, n, o.mh_steps,
+            key_of(seed, level, k, DSMC_ROLE_PAIR_RESAMPLE));
+        std::memcpy(pair_left + (cursor + k) * n, ps.left.data(),
+                    sizeof(uint32_t) * n);
+        std::memcpy(pair_right + (cursor + k) * n, ps.right.data(),
+                    sizeof(uint32_t) * n);
+        pair_lmw[cursor + k] = ps.log_mean_weight.value_or(NAN);
+        next[k] = dsmc::combine_blocks(model, L, R, o, level, (int)k);
+      }
+      if (cur.size() % 2) next.back() = std::move(cur.back());
+      cursor += np;
+      cur = std::move(next);
+    }
+    const auto& root = cur.front();
+    std::memcpy(root_paths, root.paths.data(),
+                sizeof(double) * root.paths.size());
+    *has_lnc = root.log_norm_const.has_value() ? 1 : 0;
+    *lnc = root.log_norm_const.value_or(NAN);
+  });
+}
+
+// run_conditional (conditional.cpp:156-216) unchanged.
+int ref_run_conditional(const dsmc_model_desc* desc, const double* ref,
+                        size_t n, int resampler, uint64_t seed, uint32_t sweep,
+                        double* out_path, double* lnc, int* has_lnc,
+                        uint64_t* evals) {
+  return guarded([&] {
+    auto model = oracle::build_model(*desc);
+    dsmc::ConditionalOptions o;
+    o.n_particles = n;
+    o.resampler = static_cast<dsmc::Resampler>(resampler);
+    o.seed = seed;
+    auto res = dsmc::run_conditional(model, ref, o, sweep);
+    std::memcpy(out_path, res.path.data(), sizeof(double) * res.path.size());
+    *has_lnc = res.meta.log_norm_const.has_value() ? 1 : 0;
+    *lnc = res.meta.log_norm_const.value_or(NAN);
+    *evals = res.meta.weight_evals;
+  });
+}
+
+// conditional_leaf (conditional.cpp:52-87): states incl. the reference.
+int ref_conditional_leaf(const dsmc_model_desc* desc, int t, size_t n,
+                         uint64_t seed, uint32_t sweep, const double* star,
+                         double* x, double* raw_lw) {
+  return guarded([&] {
+    auto model = oracle::build_model(*desc);
+    auto blk = dsmc::conditional_leaf(model, t, n, seed, sweep, star);
+    std::memcpy(x, blk.paths.data(), sizeof(double) * blk.paths.size());
+    dsmc::leaf_weights(model, t, blk.paths.data(), n, raw_lw);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,582 @@
+// FP64 parity combine: the reference's dense pair table (build_dense,
+// resampling.cpp:59-104) and inversion sampler (select_sorted,
+// resampling.cpp:109-153) restated per slot, plus the
+// lazy MH / rejection samplers (resampling.cpp:233-324). The N x N table is
+// never stored: pass 1 keeps per-row max, raw total and 64-entry sub-block
+// sums; each sampled slot recomputes the <= 64 weights of its sub-block,
+// which are bit-identical to pass 1 (same fill, same exp_w).
+#pragma once
+
+#include "leaves.cuh"
+
+namespace dsmc_dev {
+
+// Level-wide arguments of one batch of combines.
+struct LevelArgs {
+  int level;      // 1..L
+  int np;         // combines at this level
+  int nb_prev;    // blocks at level-1
+  int k0;         // first combine of this chunk
+  size_t cursor;  // schedule index of combine 0 of this level
+  const uint32_t* first_prev;  // [B][cap][N] (unused at level 1)
+  const uint32_t* last_prev;
+  uint32_t* first_next;
+  uint32_t* last_next;
+  const double* blnc_prev;  // [B][cap]
+  double* blnc_next;
+  double* ws;      // workspace for this chunk
+  size_t ws_comb;  // doubles per combine in ws
+  int n_out;       // slots resampled (N, or N-1 when conditional)
+};
+
+// Block meta derived from the schedule geometry.
+struct Side {
+  int leaf;  // the block is a single leaf
+  int t;     // boundary time (left: last time, right: first time)
+  int idx;   // block index at level-1
+};
+
+__device__ inline void sides(const Bufs& b, const LevelArgs& la, int k,
+                             Side& L, Side& R, CombineGeom& g) {
+  g = combine_geom(la.level, k, b.K);
+  L.leaf = (g.c - 1 == g.a);
+  L.t = g.c - 1;
+  L.idx = 2 * k;
+  R.leaf = (g.b == g.c);
+  R.t = g.c;
+  R.idx = 2 * k + 1;
+}
+
+// slot of block `blk` at boundary -> particle index of that leaf
+__device__ inline uint32_t map_first(const Bufs& b, const LevelArgs& la,
+                                     int ch, const Side& s, uint32_t q) {
+  if (s.leaf) return q;
+  return la.first_prev[((size_t)ch * b.cap + s.idx) * b.N + q];
+}
+__device__ inline uint32_t map_last(const Bufs& b, const LevelArgs& la, int ch,
+                                    const Side& s, uint32_t q) {
+  if (s.leaf) return q;
+  return la.last_prev[((size_t)ch * b.cap + s.idx) * b.N + q];
+}
+__device__ inline double block_lnc(const Bufs& b, const LevelArgs& la, int ch,
+                                   const Side& s, int a) {
+  if (s.leaf) return b.LNC[(size_t)ch * b.K + a];
+  return la.blnc_prev[(size_t)ch * b.cap + s.idx];
+}
+
+// Per-combine column data of the FP64 fill, staged in shared memory.
+struct Col64 {
+  double* x;    // N*d
+  double* base; // N
+  double* lwr;  // N or null
+};
+
+// Column base of the stitch-row factory at cut c (per model class).
+template <int MC>
+__device__ inline double col_base(const DevModel& M, const TimeConst& tc,
+                                  int c, const double* x) {
+  if (MC == kSV) return tc.shift1;
+  if (MC == kLG1) {  // models.cpp:617-627
+    double bs = 0.0;
+    if (tc.obs) {
+      const double h = *at(M.H, M.H_s, c), r = *at(M.R, M.R_s, c);
+      const double tt = DSUB(x[0], DDIV(M.y[c], h));
+      bs = __fma_rn(DDIV(DMUL(-h, h), DMUL(2.0, r)), DMUL(tt, tt), 0.0);
+    }
+    const double var = M.prop_cov[c];
+    const double t2 = DSUB(x[0], M.prop_mean[c]);
+    bs = __fma_rn(DDIV(1.0, DMUL(2.0, var)), DMUL(t2, t2), bs);
+    return DADD(bs, tc.shift1);
+  }
+  // LG d>1 (oracle comb_prepare order)
+  const double lh = cb_log_h(M, tc, c, x);
+  const double lp = DSUB(tc.p_norm, DMUL(0.5, dquad(tc.pW, M.d, x, tc.pm)));
+  return DSUB(DADD(tc.t_norm, lh), lp);
+}
+
+// Row term: the transition mean of a left particle at cut c.
+template <int MC>
+__device__ inline void row_mean(const DevModel& M, const TimeConst& tc, int c, const double* xl,
+                                double* mu) {
+  if (MC == kSV) {
+    mu[0] = DADD(M.sv_mu, DMUL(M.sv_phi, DSUB(xl[0], M.sv_mu)));
+  } else if (MC == kLG1) {
+    mu[0] = DADD(DMUL(*at(M.F, M.F_s, c), xl[0]), *at(M.b, M.b_s, c));
+  } else {  // v = W_Q (F x + b): the row's whitened transition mean
+    double m[4];
+    lg_mean(M, c, xl, m);
+    const double* W = tc.tW;
+    for (int k = 0; k < M.d; ++k) {
+      double v = 0.0;
+      for (int l = 0; l <= k; ++l) v = DADD(v, DMUL(W[k * M.d + l], m[l]));
+      mu[k] = v;
+    }
+  }
+}
+
+// One table entry (fill_row of make_pair_source, smoother.cpp:153-161).
+template <int MC>
+__device__ inline double fill64(const DevModel& M, const TimeConst& tc,
+                                double coef, const double* mu, const Col64& C,
+                                int j, int d, double sl, bool has_l) {
+  double v;
+  if (MC == kLGN) {  // d chained gaussian_row passes (ref_models lgssm_nd)
+    v = C.base[j];
+    for (int k = 0; k < d; ++k) {
+      const double t = DSUB(C.x[(size_t)j * d + k], mu[k]);
+      v = __fma_rn(-0.5, DMUL(t, t), v);
+    }
+  } else {
+    const double t = DSUB(C.x[j], mu[0]);
+    v = __fma_rn(coef, DMUL(t, t), C.base[j]);
+  }
+  if (C.lwr) v = DADD(DADD(v, sl), C.lwr[j]);
+  else if (has_l && sl != 0.0) v = DADD(v, sl);
+  return v;
+}
+
+template <int MC>
+__device__ inline double row_coef(const DevModel& M, int c) {
+  if (MC == kSV) return DDIV(-1.0, DMUL(2.0, M.sv_s2));
+  if (MC == kLG1) return DDIV(-1.0, DMUL(2.0, *at(M.Q, M.Q_s, c)));
+  return 0.0;
+}
+
+// Stage the combine's right boundary slab + column bases in shared memory.
+template <int MC>
+__device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
+                           const Side& R, const DevModel& M,
+                           const TimeConst& tc, double* smem, Col64& C) {
+  const int N = b.N, d = b.d;
+  C.x = smem;
+  C.base = smem + (size_t)N * d;
+  const bool nonuni = R.leaf && !b.UNI[(size_t)ch * b.K + R.t];
+  C.lwr = nonuni ? C.base + N : nullptr;
+  const double* X = b.X64 + ((size_t)ch * b.K + R.t) * N * d;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    const uint32_t p = map_first(b, la, ch, R, j);
+    double x[4];
+    for (int k = 0; k < d; ++k) x[k] = X[(size_t)p * d + k];
+    C.base[j] = col_base<MC>(M, tc, R.t, x);
+    if (MC == kLGN) {  // whitened column w = W_Q x
+      for (int k = 0; k < d; ++k) {
+        double z = 0.0;
+        for (int l = 0; l <= k; ++l) z = DADD(z, DMUL(tc.tW[k * d + l], x[l]));
+        C.x[(size_t)j * d + k] = z;
+      }
+    } else {
+      for (int k = 0; k < d; ++k) C.x[(size_t)j * d + k] = x[k];
+    }
+    if (nonuni) C.lwr[j] = b.LW64[((size_t)ch * b.K + R.t) * N + p];
+  }
+  __syncthreads();
+}
+
+// Pass 1: one warp per row; row max, 64-entry sub-block sums (8-lane
+// contract per sub-block, sequential tail) and the raw row total
+// (sequential over sub-blocks) — exp_row_store (kernels.cpp:93-116).
+// ws layout per combine: m[N] raw[N] scale[N] total[N] prefix[N] sub[N*nsub]
+template <int MC>
+__global__ void __launch_bounds__(256) c64_rows(Bufs b, LevelArgs la) {
+  extern __shared__ double smem[];
+  const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
+  const int N = b.N, d = b.d, nsub = (N + kSub - 1) / kSub;
+  Side L, R;
+  CombineGeom g;
+  sides(b, la, k, L, R, g);
+  const DevModel& M = b.models[ch];
+  const TimeConst& tc = b.tc[(size_t)ch * b.K + g.c];
+  Col64 C;
+  stage_cols<MC>(b, la, ch, R, M, tc, smem, C);
+  double* ws = la.ws + (size_t)blockIdx.y * la.ws_comb;
+  double *wm = ws, *wraw = ws + N, *wsub = ws + 5 * (size_t)N;
+  const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
+  const double coef = row_coef<MC>(M, g.c);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rows_per_cta = 32;
+  const double* XL = b.X64 + ((size_t)ch * b.K + L.t) * N * d;
+  for (int r = warp; r < rows_per_cta; r += 8) {
+    const int i = blockIdx.x * rows_per_cta + r;
+    if (i >= N) break;
+    const uint32_t p = map_last(b, la, ch, L, i);
+    double xl[4], mu[4];
+    for (int q = 0; q < d; ++q) xl[q] = XL[(size_t)p * d + q];
+    row_mean<MC>(M, tc, g.c, xl, mu);
+    const double sl = lnonuni ? b.LW64[((size_t)ch * b.K + L.t) * N + i] : 0.0;
+    // max (reduce_max, kernels.cpp:26-36)
+    double mx = -CUDART_INF;
+    int nan = 0;
+    for (int j = lane; j < N; j += 32) {
+      const double v = fill64<MC>(M, tc, coef, mu, C, j, d, sl, lnonuni);
+      nan |= isnan(v);
+      mx = fmax(mx, v);
+    }
+    for (int o = 16; o; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(~0u, mx, o));
+      nan |= __shfl_xor_sync(~0u, nan, o);
+    }
+    if (nan) {
+      if (lane == 0) raise_err(b.err, DSMC_E_DOMAIN, g.c, la.level, kReasonNaN);
+      mx = -CUDART_INF;
+    }
+    if (lane == 0) wm[i] = mx;
+    double* srow = wsub + (size_t)i * nsub;
+    if (mx == -CUDART_INF) {  // dead row: zero total, never selected
+      for (int s = lane; s < nsub; s += 32) srow[s] = 0.0;
+      if (lane == 0) wraw[i] = 0.0;
+      continue;
+    }
+    const int grp = lane >> 3, l8 = lane & 7;
+    for (int s0 = 0; s0 < nsub; s0 += 4) {
+      const int s = s0 + grp;
+      const bool act = s < nsub;
+      const int j0 = s * kSub;
+      const int len = act ? min(kSub, N - j0) : 0;
+      const int len8 = len & ~7;
+      double acc = 0.0;
+      for (int q = 0; q < len8; q += 8) {
+        const int j = j0 + q + l8;
+        acc = DADD(acc, exp_w(DSUB(fill64<MC>(M, tc, coef, mu, C, j, d, sl, lnonuni), mx)));
+      }
+      double a8[8];
+      for (int l = 0; l < 8; ++l) a8[l] = __shfl_sync(~0u, acc, (lane & ~7) + l);
+      if (act && l8 == 0) {
+        double bs = combine8(a8);
+        for (int j = j0 + len8; j < j0 + len; ++j)
+          bs = DADD(bs, exp_w(DSUB(fill64<MC>(M, tc, coef, mu, C, j, d, sl, lnonuni), mx)));
+        srow[s] = bs;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      double tot = 0.0;
+      for (int s = 0; s < nsub; ++s) tot = DADD(tot, srow[s]);
+      wraw[i] = tot;
+    }
+  }
+}
+
+// Pass 2: one CTA per combine. Cross-row combination (resampling.cpp:92-102),
+// per-slot inversion (Appendix A), ancestor maps, block log Z.
+template <int MC>
+__global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
+                                                  int systematic) {
+  extern __shared__ double smem[];
+  __shared__ double red[32];
+  __shared__ double s_g, s_grand;
+  __shared__ double a8s[8];
+  const int k = la.k0 + blockIdx.x, ch = blockIdx.z;
+  const int N = b.N, d = b.d, nsub = (N + kSub - 1) / kSub;
+  Side L, R;
+  CombineGeom g;
+  sides(b, la, k, L, R, g);
+  const DevModel& M = b.models[ch];
+  const TimeConst& tc = b.tc[(size_t)ch * b.K + g.c];
+  Col64 C;
+  stage_cols<MC>(b, la, ch, R, M, tc, smem, C);
+  double* ws = la.ws + (size_t)blockIdx.x * la.ws_comb;
+  double *wm = ws, *wraw = ws + N, *wscale = ws + 2 * (size_t)N,
+         *wtot = ws + 3 * (size_t)N, *wpre = ws + 4 * (size_t)N,
+         *wsub = ws + 5 * (size_t)N;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // g = max_i m_i
+  double mx = -CUDART_INF;
+  for (int i = tid; i < N; i += blockDim.x) mx = fmax(mx, wm[i]);
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(~0u, mx, o));
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double v = -CUDART_INF;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+    s_g = v;
+  }
+  __syncthreads();
+  const double gmax = s_g;
+  if (gmax == -CUDART_INF) {
+    if (tid == 0) raise_err(b.err, DSMC_E_RUNTIME, g.c, la.level, kReasonZeroTable);
+    return;
+  }
+  for (int i = tid; i < N; i += blockDim.x) {
+    const double sc = exp_w(DSUB(wm[i], gmax));
+    wscale[i] = sc;
+    wtot[i] = DMUL(sc, wraw[i]);
+  }
+  __syncthreads();
+  // grand = reduce_sum(row_total) (8-lane contract)
+  const int n8 = N & ~7;
+  if (tid < 8) {
+    double acc = 0.0;
+    for (int i = tid; i < n8; i += 8) acc = DADD(acc, wtot[i]);
+    a8s[tid] = acc;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a8[8];
+    for (int l = 0; l < 8; ++l) a8[l] = a8s[l];
+    double tot = combine8(a8);
+    for (int i = n8; i < N; ++i) tot = DADD(tot, wtot[i]);
+    s_grand = tot;
+    double cum = 0.0;  // sequential inclusive prefix (the walk's cum)
+    for (int i = 0; i < N; ++i) {
+      cum = DADD(cum, wtot[i]);
+      wpre[i] = cum;
+    }
+    b.LMW[(size_t)ch * b.T + la.cursor + k] = DADD(gmax, log(tot));
+  }
+  __syncthreads();
+  const double grand = s_grand;
+  const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
+  const double coef = row_coef<MC>(M, g.c);
+  const int off = b.conditional ? 1 : 0;
+  const uint64_t node = b.conditional
+                            ? (static_cast<uint64_t>(static_cast<uint32_t>(k)) |
+                               (static_cast<uint64_t>(b.sweep) << 32))
+                            : static_cast<uint64_t>(k);
+  const StreamId id = stream_id(b.seeds[ch], la.level, node,
+                                DSMC_ROLE_PAIR_RESAMPLE, 0);
+  double u0 = 0.0, step = 0.0;
+  if (systematic) {
+    u0 = u64_uniform(stream_u64(id, 0));
+    step = DDIV(grand, (double)la.n_out);
+  }
+  const size_t gidx = (size_t)ch * b.T + la.cursor + k;
+  uint32_t* PL = b.PL + gidx * N;
+  uint32_t* PR = b.PR + gidx * N;
+  const double* XL = b.X64 + ((size_t)ch * b.K + L.t) * N * d;
+  for (int m = tid; m < la.n_out; m += blockDim.x) {
+    const double pt = systematic ? DMUL(DADD(u0, (double)m), step)
+                                 : DMUL(u64_uniform(stream_u64(id, m)), grand);
+    int lo = 0, hi = N;  // first i with pt < S_i
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (pt < wpre[mid]) hi = mid;
+      else lo = mid + 1;
+    }
+    const int i = lo < N ? lo : N - 1;
+    const double before = i > 0 ? wpre[i - 1] : 0.0;
+    int row = i;
+    while (row > 0 && wtot[row] <= 0.0) --row;
+    double local = DDIV(DSUB(pt, before), wscale[row]);
+    if (!(local >= 0.0)) local = 0.0;
+    const double* srow = wsub + (size_t)row * nsub;
+    int s = 0;
+    double c2b = 0.0, c2 = srow[0];
+    while (!(local < c2) && s + 1 < nsub) {
+      c2b = c2;
+      ++s;
+      c2 = DADD(c2, srow[s]);
+    }
+    const uint32_t pl = map_last(b, la, ch, L, row);
+    double xl[4], mu[4];
+    for (int q = 0; q < d; ++q) xl[q] = XL[(size_t)pl * d + q];
+    row_mean<MC>(M, tc, g.c, xl, mu);
+    const double sl = lnonuni ? b.LW64[((size_t)ch * b.K + L.t) * N + row] : 0.0;
+    const double mrow = wm[row];
+    const int j0 = s * kSub, j1 = min(j0 + kSub, N);
+    double c3 = c2b;
+    int j = j0;
+    for (; j < j1; ++j) {
+      c3 = DADD(c3, exp_w(DSUB(fill64<MC>(M, tc, coef, mu, C, j, d, sl, lnonuni), mrow)));
+      if (local < c3) break;
+    }
+    if (j == j1) {  // spill: clamp to the last positive entry
+      j = j1 - 1;
+      while (j > 0 && !(exp_w(DSUB(fill64<MC>(M, tc, coef, mu, C, j, d, sl, lnonuni), mrow)) > 0.0)) --j;
+    }
+    PL[m + off] = (uint32_t)row;
+    PR[m + off] = (uint32_t)j;
+  }
+  if (b.conditional && tid == 0) {
+    PL[0] = 0;
+    PR[0] = 0;
+  }
+  // (the conditional reference-pair check is done by the caller kernel)
+  __syncthreads();
+  // ancestor maps: first'[q] = L.first[l_q], last'[q] = R.last[r_q]
+  const size_t nbase = ((size_t)ch * b.cap + k) * N;
+  for (int q = tid; q < N; q += blockDim.x) {
+    la.first_next[nbase + q] = map_first(b, la, ch, L, PL[q]);
+    la.last_next[nbase + q] = map_last(b, la, ch, R, PR[q]);
+  }
+  if (tid == 0) {
+    const double logn = log((double)N);
+    const bool luni = !L.leaf || b.UNI[(size_t)ch * b.K + L.t];
+    const bool runi = !R.leaf || b.UNI[(size_t)ch * b.K + R.t];
+    const double shift = DADD(luni ? -logn : 0.0, runi ? -logn : 0.0);
+    const double ll = block_lnc(b, la, ch, L, g.a);
+    const double rl = block_lnc(b, la, ch, R, g.c);
+    const double lmw = b.LMW[gidx];
+    la.blnc_next[(size_t)ch * b.cap + k] = DADD(DADD(DADD(ll, rl), lmw), shift);
+  }
+}
+
+// ------------------------------------------------------------- lazy
+// Entry probe (make_pair_source log_weight_at, smoother.cpp:163-169).
+struct Probe64 {
+  const DevModel* M;
+  const TimeConst* tc;
+  const double *XL, *XR, *lwl, *lwr;
+  const Bufs* b;
+  const LevelArgs* la;
+  int ch, c, d;
+  Side L, R;
+  __device__ double operator()(uint32_t i, uint32_t j, int* err) const {
+    const uint32_t pi = map_last(*b, *la, ch, L, i);
+    const uint32_t pj = map_first(*b, *la, ch, R, j);
+    double v = cb_stitch_weight(*M, *tc, c, XL + (size_t)pi * d,
+                                XR + (size_t)pj * d, err);
+    if (lwl) v = DADD(v, lwl[i]);
+    if (lwr) v = DADD(v, lwr[j]);
+    return v;
+  }
+};
+
+// One thread per output slot; substream m+1 (resampling.cpp:253,300).
+__global__ void lazy64_kernel(Bufs b, LevelArgs la, int mh, size_t mh_steps) {
+  const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  const int N = b.N;
+  Side L, R;
+  CombineGeom g;
+  sides(b, la, k, L, R, g);
+  const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
+  const bool rnonuni = R.leaf && !b.UNI[(size_t)ch * b.K + R.t];
+  Probe64 P;
+  P.M = &b.models[ch];
+  P.tc = &b.tc[(size_t)ch * b.K + g.c];
+  P.XL = b.X64 + ((size_t)ch * b.K + L.t) * N * b.d;
+  P.XR = b.X64 + ((size_t)ch * b.K + R.t) * N * b.d;
+  P.lwl = lnonuni ? b.LW64 + ((size_t)ch * b.K + L.t) * N : nullptr;
+  P.lwr = rnonuni ? b.LW64 + ((size_t)ch * b.K + R.t) * N : nullptr;
+  P.b = &b;
+  P.la = &la;
+  P.ch = ch;
+  P.c = g.c;
+  P.d = b.d;
+  P.L = L;
+  P.R = R;
+  const size_t gidx = (size_t)ch * b.T + la.cursor + k;
+  const int off = b.conditional ? 1 : 0;
+  unsigned long long evals = 0;
+  int err = 0, why = 0;
+  if (m < la.n_out) {
+    const uint64_t node = b.conditional
+                              ? (static_cast<uint64_t>(static_cast<uint32_t>(k)) |
+                                 (static_cast<uint64_t>(b.sweep) << 32))
+                              : static_cast<uint64_t>(k);
+    StreamReader s;
+    s.init(stream_id(b.seeds[ch], la.level, node, DSMC_ROLE_PAIR_RESAMPLE, m + 1));
+    uint32_t oi = 0, oj = 0;
+    if (mh) {  // mh_lazy_pairs (resampling.cpp:250-279)
+      uint32_t i = (uint32_t)(m % N), j = i;
+      double cur = 0.0;
+      bool have = false;
+      for (size_t st = 0; st < mh_steps && !err; ++st) {
+        const uint32_t pi = (uint32_t)s.index(N), pj = (uint32_t)s.index(N);
+        const double lu = log(s.uniform_pos());
+        if (!have) {
+          cur = P(i, j, &err);
+          ++evals;
+          have = true;
+        }
+        const double prop = P(pi, pj, &err);
+        ++evals;
+        if (isnan(prop) || isnan(cur)) { err = DSMC_E_INVALID_ARGUMENT; why = kReasonNaN; }
+        if (lu < DSUB(prop, cur)) {
+          i = pi;
+          j = pj;
+          cur = prop;
+        }
+      }
+      oi = i;
+      oj = j;
+    } else {  // rejection_lazy_pairs (resampling.cpp:296-321)
+      if (!(b.bounded[ch] & 1)) { err = DSMC_E_INVALID_ARGUMENT; why = kReasonNoBound; }  // no finite bound
+      double bound = P.tc->bound;
+      if (P.lwl) bound = DADD(bound, b.LWMAX[(size_t)ch * b.K + L.t]);
+      if (P.lwr) bound = DADD(bound, b.LWMAX[(size_t)ch * b.K + R.t]);
+      bool ok = false;
+      for (uint64_t trial = 0; trial < (1u << 24) && !err; ++trial) {
+        const uint32_t i = (uint32_t)s.index(N), j = (uint32_t)s.index(N);
+        const double lw = P(i, j, &err);
+        ++evals;
+        if (isnan(lw)) { err = DSMC_E_INVALID_ARGUMENT; why = kReasonNaN; }
+        if (DSUB(lw, bound) > 1e-9) { err = DSMC_E_INVALID_ARGUMENT; why = kReasonOverBound; }
+        if (err) break;
+        if (log(s.uniform_pos()) <= DSUB(lw, bound)) {
+          oi = i;
+          oj = j;
+          ok = true;
+          break;
+        }
+      }
+      if (!ok && !err) { err = DSMC_E_RUNTIME; why = kReasonTrialCap; }
+    }
+    b.PL[gidx * N + m + off] = oi;
+    b.PR[gidx * N + m + off] = oj;
+    if (err) raise_err(b.err, err, g.c, la.level, why);
+  }
+  // warp-aggregated evaluation count
+  for (int o = 16; o; o >>= 1) evals += __shfl_xor_sync(~0u, evals, o);
+  if ((threadIdx.x & 31) == 0 && evals) atomicAdd(b.evals + ch, evals);
+}
+
+// Ancestor maps + block meta after a lazy combine (no log Z: lazy
+// resamplers never see the whole table, smoother.cpp:220-222).
+__global__ void lazy_finish_kernel(Bufs b, LevelArgs la) {
+  const int k = la.k0 + blockIdx.x, ch = blockIdx.z;
+  const int N = b.N;
+  Side L, R;
+  CombineGeom g;
+  sides(b, la, k, L, R, g);
+  const size_t gidx = (size_t)ch * b.T + la.cursor + k;
+  uint32_t* PL = b.PL + gidx * N;
+  uint32_t* PR = b.PR + gidx * N;
+  if (b.conditional && threadIdx.x == 0) {
+    PL[0] = 0;
+    PR[0] = 0;
+  }
+  __syncthreads();
+  const size_t nbase = ((size_t)ch * b.cap + k) * N;
+  for (int q = threadIdx.x; q < N; q += blockDim.x) {
+    la.first_next[nbase + q] = map_first(b, la, ch, L, PL[q]);
+    la.last_next[nbase + q] = map_last(b, la, ch, R, PR[q]);
+  }
+  if (threadIdx.x == 0) {
+    la.blnc_next[(size_t)ch * b.cap + k] = CUDART_NAN;
+    b.LMW[gidx] = CUDART_NAN;
+  }
+}
+
+// Conditional combines require a finite reference pair (conditional.cpp:
+// 97-103), checked through the scalar entry probe like the reference.
+__global__ void refpair_check_kernel(Bufs b, LevelArgs la) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ch = blockIdx.z;
+  if (k >= la.np) return;
+  Side L, R;
+  CombineGeom g;
+  sides(b, la, k, L, R, g);
+  const int N = b.N;
+  const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
+  const bool rnonuni = R.leaf && !b.UNI[(size_t)ch * b.K + R.t];
+  Probe64 P;
+  P.M = &b.models[ch];
+  P.tc = &b.tc[(size_t)ch * b.K + g.c];
+  P.XL = b.X64 + ((size_t)ch * b.K + L.t) * N * b.d;
+  P.XR = b.X64 + ((size_t)ch * b.K + R.t) * N * b.d;
+  P.lwl = lnonuni ? b.LW64 + ((size_t)ch * b.K + L.t) * N : nullptr;
+  P.lwr = rnonuni ? b.LW64 + ((size_t)ch * b.K + R.t) * N : nullptr;
+  P.b = &b;
+  P.la = &la;
+  P.ch = ch;
+  P.c = g.c;
+  P.d = b.d;
+  P.L = L;
+  P.R = R;
+  int err = 0;
+  const double w = P(0, 0, &err);
+  if (err || !isfinite(w)) raise_err(b.err, DSMC_E_INVALID_ARGUMENT, g.c, la.level, kReasonRefPair);
+}
+
+}  // namespace dsmc_dev

@@ -1,0 +1,1412 @@
+// Host orchestration + C ABI of the B200 dSMC engine (include/dsmc_b200.h).
+//
+// One run = prep (per-time constants) -> leaves -> ceil(log2 K) combine
+// levels (all combines of a level in one launch per kernel; chunked only to
+// bound workspace) -> top-down ancestor composition -> fused gather +
+// moments. Every kernel goes on the context's stream; the host synchronises
+// once at the end to read the device error record (no per-level sync).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "compose.cuh"
+#include "dsmc_b200.h"
+
+using namespace dsmc_dev;
+
+namespace {
+
+struct Arena {
+  std::map<std::string, std::pair<void*, size_t>> bufs;
+  cudaError_t get(const char* name, size_t bytes, void** out) {
+    auto& e = bufs[name];
+    if (e.second < bytes) {
+      if (e.first) cudaFree(e.first);
+      e.first = nullptr;
+      e.second = 0;
+      cudaError_t rc = cudaMalloc(&e.first, std::max<size_t>(bytes, 256));
+      if (rc != cudaSuccess) return rc;
+      e.second = std::max<size_t>(bytes, 256);
+    }
+    *out = e.first;
+    return cudaSuccess;
+  }
+  void release() {
+    for (auto& kv : bufs)
+      if (kv.second.first) cudaFree(kv.second.first);
+    bufs.clear();
+  }
+};
+
+struct Status {
+  int code = DSMC_OK;
+  std::string msg;
+};
+
+}  // namespace
+
+struct dsmc_model_handle {
+  int B = 1;
+  dsmc_model_desc desc{};
+  int K = 0, d = 1, dy = 1;
+  DevModel* models_dev = nullptr;  // [B]
+  TimeConst* tc = nullptr;         // [B][K]
+  int* bounded = nullptr;          // [B]
+  std::vector<void*> owned;
+  cudaStream_t stream = nullptr;  // owned memory is stream-ordered
+};
+
+struct dsmc_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  uint64_t launches = 0;
+  Arena arena;
+  cudaEvent_t ev[4] = {};
+  double timings[3] = {0, 0, 0};
+  // per-launch events around the pair / sample kernels of the last timed run
+  std::vector<cudaEvent_t> kev;
+  int kev_used = 0;
+  bool time_kernels = false;
+  // last resident run
+  int last_K = 0, last_d = 0, last_B = 0;
+  double* d_mean = nullptr;
+  double* d_cov = nullptr;
+  double last_lnc = NAN;
+  int last_has_lnc = 0;
+  uint64_t last_evals = 0;
+  int last_levels = 0;
+  int last_biased = 0;
+  double* h_lnc = nullptr;  // pinned scratch
+};
+
+namespace {
+
+int set_err(dsmc_ctx* ctx, int code, std::string msg) {
+  if (ctx) ctx->err = std::move(msg);
+  return code;
+}
+#define CU(call)                                                          \
+  do {                                                                    \
+    cudaError_t _e = (call);                                              \
+    if (_e != cudaSuccess)                                                \
+      return set_err(ctx, DSMC_E_CUDA, std::string("CUDA: ") +            \
+                                           cudaGetErrorString(_e) + " at " \
+                                           #call);                        \
+  } while (0)
+#define LAUNCHED(ctx) (++(ctx)->launches)
+
+int validate_desc(dsmc_ctx* ctx, const dsmc_model_desc* m) {
+  if (!m) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "model descriptor is null");
+  if (m->horizon < 0)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "model: horizon must be >= 0");
+  if (m->kind == DSMC_MODEL_SV) {
+    if (m->state_dim != 1)
+      return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "sv: state_dim must be 1");
+    if (!(m->sv_sigma2 > 0.0) || !(std::fabs(m->sv_phi) < 1.0))
+      return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                     "sv descriptor: need s2 > 0 and |phi| < 1");
+    if (!m->y) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "sv: y is null");
+    for (int t = 0; t <= m->horizon; ++t)
+      if (!(m->y[t] != 0.0) || !std::isfinite(m->y[t]))
+        return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                       "sv descriptor: observations must be finite and nonzero");
+    return DSMC_OK;
+  }
+  if (m->kind != DSMC_MODEL_LGSSM)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "unknown model kind");
+  if (m->state_dim < 1 || m->state_dim > 4 || m->obs_dim < 1 || m->obs_dim > 4)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "lgssm descriptor: dims must be 1..4");
+  if (!m->m0 || !m->P0 || !m->prop_mean || !m->prop_cov || !m->H || !m->R ||
+      !m->y || (m->horizon >= 1 && (!m->F || !m->b || !m->Q)))
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                   "model: proposal, initial, transition and observation arrays "
+                   "are required");
+  return DSMC_OK;
+}
+
+template <class T>
+int upload(dsmc_ctx* ctx, dsmc_model_handle* h, const T* src, size_t n,
+           const T** dst) {
+  if (!src || n == 0) {
+    *dst = nullptr;
+    return DSMC_OK;
+  }
+  void* p = nullptr;
+  CU(cudaMallocAsync(&p, n * sizeof(T), ctx->stream));
+  h->owned.push_back(p);
+  CU(cudaMemcpyAsync(p, src, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  *dst = static_cast<const T*>(p);
+  return DSMC_OK;
+}
+
+// Upload B descriptors (same K, d) and run the prep kernel.
+int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
+                dsmc_model_handle** out) {
+  for (int c = 0; c < B; ++c) {
+    int rc = validate_desc(ctx, &descs[c]);
+    if (rc) return rc;
+    if (descs[c].horizon != descs[0].horizon || descs[c].state_dim != descs[0].state_dim ||
+        descs[c].kind != descs[0].kind)
+      return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "chains must share kind, horizon and dims");
+  }
+  auto h = std::make_unique<dsmc_model_handle>();
+  h->B = B;
+  h->stream = ctx->stream;
+  h->desc = descs[0];
+  const int K = descs[0].horizon + 1, d = descs[0].state_dim, dy = descs[0].obs_dim;
+  h->K = K;
+  h->d = d;
+  h->dy = dy;
+  std::vector<DevModel> dm(B);
+  for (int c = 0; c < B; ++c) {
+    const dsmc_model_desc& m = descs[c];
+    DevModel& M = dm[c];
+    M.kind = m.kind;
+    M.d = d;
+    M.dy = m.kind == DSMC_MODEL_SV ? 1 : dy;
+    M.T = m.horizon;
+    M.K = K;
+    M.sv_mu = m.sv_mu;
+    M.sv_phi = m.sv_phi;
+    M.sv_s2 = m.sv_sigma2;
+    M.F_s = m.F_stride;
+    M.b_s = m.b_stride;
+    M.Q_s = m.Q_stride;
+    M.H_s = m.H_stride;
+    M.R_s = m.R_stride;
+    int rc = 0;
+    const size_t nT = (size_t)K;
+    if (m.kind == DSMC_MODEL_SV) {
+      rc |= upload(ctx, h.get(), m.y, nT, &M.y);
+      M.has_obs = nullptr;
+      M.prop_mean = M.prop_cov = M.F = M.b = M.Q = M.H = M.R = M.m0 = M.P0 = nullptr;
+    } else {
+      auto span = [&](int64_t stride, size_t per) { return stride ? nT * stride : per; };
+      rc |= upload(ctx, h.get(), m.y, nT * dy, &M.y);
+      rc |= upload(ctx, h.get(), m.has_obs, m.has_obs ? nT : 0, &M.has_obs);
+      rc |= upload(ctx, h.get(), m.prop_mean, nT * d, &M.prop_mean);
+      rc |= upload(ctx, h.get(), m.prop_cov, nT * d * d, &M.prop_cov);
+      rc |= upload(ctx, h.get(), m.m0, (size_t)d, &M.m0);
+      rc |= upload(ctx, h.get(), m.P0, (size_t)d * d, &M.P0);
+      rc |= upload(ctx, h.get(), m.H, span(m.H_stride, (size_t)dy * d), &M.H);
+      rc |= upload(ctx, h.get(), m.R, span(m.R_stride, (size_t)dy * dy), &M.R);
+      if (m.horizon >= 1) {
+        rc |= upload(ctx, h.get(), m.F, span(m.F_stride, (size_t)d * d), &M.F);
+        rc |= upload(ctx, h.get(), m.b, span(m.b_stride, (size_t)d), &M.b);
+        rc |= upload(ctx, h.get(), m.Q, span(m.Q_stride, (size_t)d * d), &M.Q);
+      } else {
+        M.F = M.b = M.Q = nullptr;
+      }
+    }
+    if (rc) return DSMC_E_CUDA;
+  }
+  void* p;
+  CU(cudaMallocAsync(&p, sizeof(DevModel) * B, ctx->stream));
+  h->owned.push_back(p);
+  h->models_dev = static_cast<DevModel*>(p);
+  CU(cudaMemcpyAsync(p, dm.data(), sizeof(DevModel) * B, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMallocAsync(&p, sizeof(TimeConst) * B * (size_t)K, ctx->stream));
+  h->owned.push_back(p);
+  h->tc = static_cast<TimeConst*>(p);
+  CU(cudaMallocAsync(&p, sizeof(int) * B, ctx->stream));
+  h->owned.push_back(p);
+  h->bounded = static_cast<int*>(p);
+  std::vector<int> ones(B, 3);
+  CU(cudaMemcpyAsync(p, ones.data(), sizeof(int) * B, cudaMemcpyHostToDevice, ctx->stream));
+  prep_kernel<<<dim3((K + 127) / 128, B), 128, 0, ctx->stream>>>(h->models_dev, h->tc, K,
+                                                                 h->bounded);
+  LAUNCHED(ctx);
+  CU(cudaGetLastError());
+  *out = h.release();
+  return DSMC_OK;
+}
+
+void free_handle(dsmc_model_handle* h) {
+  if (!h) return;
+  for (void* p : h->owned) cudaFreeAsync(p, h->stream);
+  delete h;
+}
+
+// --------------------------------------------------------------- the run
+struct RunOpts {
+  int precision = DSMC_FP32;
+  int resampler = DSMC_MULTINOMIAL;
+  size_t mh_steps = 16;
+  size_t N = 0;
+  int conditional = 0;
+  uint32_t sweep = 0;
+  const double* inj_x = nullptr;   // host
+  const double* inj_lw = nullptr;  // host
+  const double* star = nullptr;    // device [B][K][d] (conditional)
+  const uint64_t* seeds = nullptr; // device [B]
+  // outputs (device pointers, optional)
+  double* paths = nullptr;
+  double* mean = nullptr;
+  double* cov = nullptr;
+  double* star_out = nullptr;   // device [B][K][d]
+  uint8_t* changed = nullptr;   // device [B][K]
+  bool timing = false;
+};
+
+struct RunResult {
+  int levels = 0;
+  // device pointers valid until the next run on the context
+  uint32_t* PL = nullptr;
+  uint32_t* PR = nullptr;
+  double* LMW = nullptr;
+  double* root_lnc = nullptr;  // [B] (strided by cap)
+  size_t lnc_stride = 0;
+  unsigned long long* evals = nullptr;
+  ErrFlag* err = nullptr;
+  double* LNC = nullptr;
+  double* X64 = nullptr;
+  double* LW64 = nullptr;
+};
+
+size_t smem_cols64(int N, int d) { return sizeof(double) * (size_t)N * (d + 2); }
+
+template <int MC>
+int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
+               int systematic) {
+  const size_t sm = smem_cols64(b.N, b.d);
+  CU(cudaFuncSetAttribute(c64_rows<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CU(cudaFuncSetAttribute(c64_sample<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  c64_rows<MC><<<dim3((b.N + 31) / 32, nk, b.B), 256, sm, ctx->stream>>>(b, la);
+  LAUNCHED(ctx);
+  c64_sample<MC><<<dim3(nk, 1, b.B), 256, sm, ctx->stream>>>(b, la, systematic);
+  LAUNCHED(ctx);
+  return DSMC_OK;
+}
+
+template <int D>
+int launch_c32(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
+               int systematic) {
+  const size_t sm = sizeof(double) * b.N + sizeof(float) * (size_t)b.N * (D + 2);
+  CU(cudaFuncSetAttribute(c32_sample<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  cudaEvent_t* ev = nullptr;
+  if (ctx->time_kernels) {  // 3 events: pair start, pair end = sample start, sample end
+    while ((int)ctx->kev.size() < ctx->kev_used + 3) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      ctx->kev.push_back(e);
+    }
+    ev = &ctx->kev[ctx->kev_used];
+    ctx->kev_used += 3;
+    CU(cudaEventRecord(ev[0], ctx->stream));
+  }
+  c32_pair<D><<<dim3((b.N + kRT - 1) / kRT, nk, b.B), 256, 0, ctx->stream>>>(b, la);
+  LAUNCHED(ctx);
+  if (ev) CU(cudaEventRecord(ev[1], ctx->stream));
+  c32_sample<D><<<dim3(nk, 1, b.B), 512, sm, ctx->stream>>>(b, la, systematic);
+  LAUNCHED(ctx);
+  if (ev) CU(cudaEventRecord(ev[2], ctx->stream));
+  return DSMC_OK;
+}
+
+__global__ void tail_copy_kernel(Bufs b, int idx_prev, int idx_next,
+                                 const uint32_t* fp, const uint32_t* lp,
+                                 uint32_t* fn, uint32_t* ln,
+                                 const double* blp, double* bln) {
+  const int ch = blockIdx.y;
+  const size_t src = ((size_t)ch * b.cap + idx_prev) * b.N;
+  const size_t dst = ((size_t)ch * b.cap + idx_next) * b.N;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < b.N; q += gridDim.x * blockDim.x) {
+    fn[dst + q] = fp[src + q];
+    ln[dst + q] = lp[src + q];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    bln[(size_t)ch * b.cap + idx_next] = blp[(size_t)ch * b.cap + idx_prev];
+}
+
+std::string err_message(const ErrFlag& e, int K) {
+  char buf[512];
+  const int c = e.cut, l = e.level;
+  auto span = [&](int& a, int& bb) {
+    const int s = 1 << (l - 1);
+    const int k = (c / s - 1) / 2;
+    a = 2 * k * s;
+    bb = std::min((2 * k + 2) * s - 1, K - 1);
+  };
+  int a = 0, bb = 0;
+  switch (e.reason) {
+    case kReasonZeroTable:
+      span(a, bb);
+      snprintf(buf, sizeof buf,
+               "combine at cut %d (times %d..%d): all pair weights are zero; the "
+               "blocks share no support under the model", c, a, bb);
+      break;
+    case kReasonTrialCap:
+      span(a, bb);
+      snprintf(buf, sizeof buf,
+               "combine at cut %d (times %d..%d): rejection resampling exceeded "
+               "the trial cap; the bound is far too loose or the weights are "
+               "degenerate", c, a, bb);
+      break;
+    case kReasonOverBound:
+      snprintf(buf, sizeof buf, "pair weight exceeds its stated upper bound (cut %d)", c);
+      break;
+    case kReasonNoBound:
+      snprintf(buf, sizeof buf, "rejection resampling requires a finite log_upper_bound");
+      break;
+    case kReasonNaN:
+      snprintf(buf, sizeof buf, l == 0 ? "leaf %d: weight is NaN" : "NaN pair weight at cut %d", c);
+      break;
+    case kReasonRefPair:
+      snprintf(buf, sizeof buf,
+               "conditional_combine: the reference pair has zero stitch weight at cut %d", c);
+      break;
+    case kReasonLeafZero:
+      snprintf(buf, sizeof buf, "leaf %d: every proposal draw has zero weight", c);
+      break;
+    case kReasonRefLeaf:
+      snprintf(buf, sizeof buf,
+               "conditional_leaf: the reference path has zero weight at time %d", c);
+      break;
+    default:
+      snprintf(buf, sizeof buf, "device error at cut %d level %d", c, l);
+  }
+  return buf;
+}
+
+// Core: leaves + levels (+ composition/gather). B chains share K, N, d.
+int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* res) {
+  const int B = h->B, K = h->K, T = K - 1, d = h->d;
+  const int N = (int)o.N;
+  if (N < 1) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "make_leaf: n must be >= 1");
+  if (o.conditional && N < 2)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "conditional_leaf: need n >= 2 slots");
+  if (o.resampler < 0 || o.resampler > 3)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "unknown resampler");
+  if (o.conditional && o.resampler != DSMC_MULTINOMIAL && o.resampler != DSMC_REJECTION_LAZY)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                   "conditional sweeps need exchangeable unbiased slot draws: use the "
+                   "multinomial or rejection-lazy resampler");
+  const bool fp64 = o.precision == DSMC_FP64_PARITY;
+  if (!fp64 && h->desc.kind == DSMC_MODEL_LGSSM && o.inj_x)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "leaf injection needs FP64 parity precision");
+  const int cap = std::max(1, (K + 1) / 2);
+  Bufs b{};
+  b.K = K;
+  b.T = T;
+  b.N = N;
+  b.d = d;
+  b.B = B;
+  b.cap = cap;
+  b.models = h->models_dev;
+  b.seeds = o.seeds;
+  b.tc = h->tc;
+  b.bounded = h->bounded;
+  b.conditional = o.conditional;
+  b.sweep = o.sweep;
+  b.star = o.star;
+  Arena& A = ctx->arena;
+  void* p;
+  const size_t BK = (size_t)B * K, BKN = BK * N, BT = (size_t)B * std::max(T, 1);
+  if (fp64) {
+    CU(A.get("X64", BKN * d * sizeof(double), &p));
+    b.X64 = (double*)p;
+    CU(A.get("LW64", BKN * sizeof(double), &p));
+    b.LW64 = (double*)p;
+  } else {
+    CU(A.get("X32", BKN * sizeof(float4), &p));
+    b.X32 = (float4*)p;
+    CU(A.get("COL", BKN * sizeof(float), &p));
+    b.COL = (float*)p;
+    CU(A.get("LW32", (size_t)B * N * sizeof(float), &p));
+    b.LW32 = (float*)p;
+  }
+  CU(A.get("LNC", BK * sizeof(double), &p));
+  b.LNC = (double*)p;
+  CU(A.get("LWMAX", BK * sizeof(double), &p));
+  b.LWMAX = (double*)p;
+  CU(A.get("UNI", BK, &p));
+  b.UNI = (uint8_t*)p;
+  CU(A.get("PL", BT * N * sizeof(uint32_t), &p));
+  b.PL = (uint32_t*)p;
+  CU(A.get("PR", BT * N * sizeof(uint32_t), &p));
+  b.PR = (uint32_t*)p;
+  CU(A.get("LMW", BT * sizeof(double), &p));
+  b.LMW = (double*)p;
+  CU(A.get("ERR", sizeof(ErrFlag), &p));
+  b.err = (ErrFlag*)p;
+  CU(A.get("EVALS", B * sizeof(unsigned long long), &p));
+  b.evals = (unsigned long long*)p;
+  CU(cudaMemsetAsync(b.err, 0, sizeof(ErrFlag), ctx->stream));
+  CU(cudaMemsetAsync(b.evals, 0, B * sizeof(unsigned long long), ctx->stream));
+  uint32_t* maps[4];
+  const char* mnames[4] = {"FA", "LA", "FB", "LB"};
+  for (int i = 0; i < 4; ++i) {
+    CU(A.get(mnames[i], (size_t)B * cap * N * sizeof(uint32_t), &p));
+    maps[i] = (uint32_t*)p;
+  }
+  double* blnc[2];
+  CU(A.get("BLNCA", (size_t)B * cap * sizeof(double), &p));
+  blnc[0] = (double*)p;
+  CU(A.get("BLNCB", (size_t)B * cap * sizeof(double), &p));
+  blnc[1] = (double*)p;
+
+  if (o.timing) CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+  // ---------------------------------------------------------------- leaves
+  if (fp64) {
+    const double* dinj_x = nullptr;
+    const double* dinj_lw = nullptr;
+    if (o.inj_x) {
+      CU(A.get("INJX", BKN * d * sizeof(double), &p));
+      CU(cudaMemcpyAsync(p, o.inj_x, BKN * d * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      dinj_x = (const double*)p;
+    }
+    if (o.inj_lw) {
+      CU(A.get("INJW", BKN * sizeof(double), &p));
+      CU(cudaMemcpyAsync(p, o.inj_lw, BKN * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      dinj_lw = (const double*)p;
+    }
+    leaf64_kernel<<<dim3((N + 127) / 128, K, B), 128, 0, ctx->stream>>>(b, dinj_x, dinj_lw);
+    LAUNCHED(ctx);
+    leafnorm64_kernel<<<dim3(K, B), 32, 0, ctx->stream>>>(b);
+    LAUNCHED(ctx);
+  } else {
+    CU(A.get("RAW0", (size_t)B * N * sizeof(double), &p));
+    leaf32_kernel<<<dim3((N + 127) / 128, K, B), 128, 0, ctx->stream>>>(b, (double*)p);
+    LAUNCHED(ctx);
+    leafnorm32_kernel<<<B, 32, 0, ctx->stream>>>(b, (const double*)p);
+    LAUNCHED(ctx);
+  }
+  CU(cudaGetLastError());
+  if (o.timing) CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+
+  // ---------------------------------------------------------------- levels
+  const bool lazy = o.resampler == DSMC_MH_LAZY || o.resampler == DSMC_REJECTION_LAZY;
+  const int nsub = (N + kSub - 1) / kSub;
+  const int nsubp = ((N + kChunk - 1) / kChunk) * (kChunk / kSub);
+  const size_t ws_comb = fp64 ? (size_t)N * (5 + nsub) : ((size_t)N * nsubp + 1) / 2;
+  const size_t ws_budget = (size_t)1 << 30;  // bytes per chunk
+  const int chunk = (int)std::max<size_t>(1, std::min<size_t>(65535, ws_budget / (ws_comb * 8 * B)));
+  double* ws = nullptr;
+  if (!lazy && T > 0) {
+    const int np1 = K / 2;
+    CU(A.get("WS", (size_t)std::min(chunk, np1) * ws_comb * 8 * B, &p));
+    ws = (double*)p;
+  }
+  int cur = 0;  // maps[2*cur], maps[2*cur+1] hold the previous level
+  int nb = K, level = 0;
+  size_t cursor = 0;
+  const int mc = model_class(h->desc.kind, d, h->desc.kind == DSMC_MODEL_SV ? 1 : h->dy);
+  while (nb > 1) {
+    ++level;
+    const int np = nb / 2;
+    LevelArgs la{};
+    la.level = level;
+    la.np = np;
+    la.nb_prev = nb;
+    la.cursor = cursor;
+    la.first_prev = maps[2 * cur];
+    la.last_prev = maps[2 * cur + 1];
+    la.first_next = maps[2 * (1 - cur)];
+    la.last_next = maps[2 * (1 - cur) + 1];
+    la.blnc_prev = blnc[cur];
+    la.blnc_next = blnc[1 - cur];
+    la.n_out = o.conditional ? N - 1 : N;
+    la.ws = ws;
+    la.ws_comb = ws_comb;
+    if (o.conditional) {
+      la.k0 = 0;
+      if (fp64) {
+        refpair_check_kernel<<<dim3((np + 127) / 128, 1, B), 128, 0, ctx->stream>>>(b, la);
+        LAUNCHED(ctx);
+      }
+    }
+    for (int k0 = 0; k0 < np; k0 += chunk) {
+      const int nk = std::min(chunk, np - k0);
+      la.k0 = k0;
+      int rc = 0;
+      if (lazy) {
+        const int mh = o.resampler == DSMC_MH_LAZY;
+        const dim3 grid((la.n_out + 127) / 128, nk, B);
+        if (fp64) {
+          lazy64_kernel<<<grid, 128, 0, ctx->stream>>>(b, la, mh, o.mh_steps);
+        } else {
+          switch (d) {
+            case 1: lazy32_kernel<1><<<grid, 128, 0, ctx->stream>>>(b, la, mh, o.mh_steps); break;
+            case 2: lazy32_kernel<2><<<grid, 128, 0, ctx->stream>>>(b, la, mh, o.mh_steps); break;
+            case 3: lazy32_kernel<3><<<grid, 128, 0, ctx->stream>>>(b, la, mh, o.mh_steps); break;
+            default: lazy32_kernel<4><<<grid, 128, 0, ctx->stream>>>(b, la, mh, o.mh_steps); break;
+          }
+        }
+        LAUNCHED(ctx);
+        lazy_finish_kernel<<<dim3(nk, 1, B), 256, 0, ctx->stream>>>(b, la);
+        LAUNCHED(ctx);
+      } else {
+        const int sys = o.resampler == DSMC_SYSTEMATIC;
+        if (fp64) {
+          rc = mc == kLG1 ? launch_c64<kLG1>(ctx, b, la, nk, sys)
+             : mc == kSV  ? launch_c64<kSV>(ctx, b, la, nk, sys)
+                          : launch_c64<kLGN>(ctx, b, la, nk, sys);
+        } else {
+          rc = d == 1 ? launch_c32<1>(ctx, b, la, nk, sys)
+             : d == 2 ? launch_c32<2>(ctx, b, la, nk, sys)
+             : d == 3 ? launch_c32<3>(ctx, b, la, nk, sys)
+                      : launch_c32<4>(ctx, b, la, nk, sys);
+        }
+      }
+      if (rc) return rc;
+      CU(cudaGetLastError());
+    }
+    if (nb % 2) {  // odd tail carried to the next level
+      const int s = 1 << (level - 1);
+      const bool tail_leaf = (nb - 1) * s == K - 1;
+      if (!tail_leaf) {
+        tail_copy_kernel<<<dim3(4, B), 256, 0, ctx->stream>>>(
+            b, nb - 1, np, la.first_prev, la.last_prev, la.first_next, la.last_next,
+            la.blnc_prev, la.blnc_next);
+        LAUNCHED(ctx);
+      }
+    }
+    cur = 1 - cur;
+    cursor += np;
+    nb = (nb + 1) / 2;
+  }
+  if (o.timing) CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+  res->levels = level;
+  res->PL = b.PL;
+  res->PR = b.PR;
+  res->LMW = b.LMW;
+  res->root_lnc = K == 1 ? b.LNC : blnc[cur];
+  res->lnc_stride = K == 1 ? (size_t)K : (size_t)cap;
+  res->evals = b.evals;
+  res->err = b.err;
+  res->LNC = b.LNC;
+  res->X64 = b.X64;
+  res->LW64 = b.LW64;
+
+  // ----------------------------------------------------------- composition
+  if (o.conditional) {
+    uint32_t* S[2];
+    CU(A.get("SA", (size_t)B * cap * 2 * sizeof(uint32_t), &p));
+    S[0] = (uint32_t*)p;
+    CU(A.get("SB", (size_t)B * cap * 2 * sizeof(uint32_t), &p));
+    S[1] = (uint32_t*)p;
+    star_select_kernel<<<(B + 63) / 64, 64, 0, ctx->stream>>>(b, level, S[0], !fp64);
+    LAUNCHED(ctx);
+    int sc = 0;
+    std::vector<int> nbs{K};
+    while (nbs.back() > 1) nbs.push_back((nbs.back() + 1) / 2);
+    std::vector<size_t> cursors(nbs.size() + 1, 0);
+    for (size_t l = 1; l + 1 <= nbs.size() - 1; ++l) cursors[l + 1] = cursors[l] + nbs[l - 1] / 2;
+    for (int l = level; l >= 2; --l) {
+      td1_kernel<<<dim3((nbs[l] + 127) / 128, B), 128, 0, ctx->stream>>>(
+          b, cursors[l], nbs[l], nbs[l - 1], S[sc], S[1 - sc]);
+      LAUNCHED(ctx);
+      sc = 1 - sc;
+    }
+    star_path_kernel<<<dim3((K + 127) / 128, B), 128, 0, ctx->stream>>>(b, S[sc], !fp64,
+                                                                       o.star_out, o.changed);
+    LAUNCHED(ctx);
+  } else if (o.paths || o.mean || o.cov) {
+    std::vector<int> nbs{K};
+    while (nbs.back() > 1) nbs.push_back((nbs.back() + 1) / 2);
+    std::vector<size_t> cursors(nbs.size() + 1, 0);
+    for (size_t l = 1; l + 1 <= nbs.size() - 1; ++l) cursors[l + 1] = cursors[l] + nbs[l - 1] / 2;
+    // reuse the map buffers (bottom-up maps are dead now)
+    uint32_t* Mb[2] = {maps[0], maps[2]};
+    int mcur = 0;
+    bool root = true;
+    for (int l = level; l >= 2; --l) {
+      td_kernel<<<dim3((N + 255) / 256, nbs[l], B), 256, 0, ctx->stream>>>(
+          b, l, cursors[l], nbs[l], nbs[l - 1], Mb[mcur], Mb[1 - mcur], root ? 1 : 0);
+      LAUNCHED(ctx);
+      root = false;
+      mcur = 1 - mcur;
+    }
+    if (fp64) {
+      gather64_kernel<<<dim3(K, B), 256, 0, ctx->stream>>>(b, Mb[mcur], root ? 1 : 0,
+                                                           o.paths, o.mean, o.cov);
+    } else {
+      const uint32_t* M1 = Mb[mcur];
+      const int r1 = root ? 1 : 0;
+      switch (d) {
+        case 1: gather32_kernel<1><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov); break;
+        case 2: gather32_kernel<2><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov); break;
+        case 3: gather32_kernel<3><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov); break;
+        default: gather32_kernel<4><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov); break;
+      }
+    }
+    LAUNCHED(ctx);
+  }
+  CU(cudaGetLastError());
+  if (o.timing) CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+  return DSMC_OK;
+}
+
+// Read back the device error record (the one host sync of a run).
+int check_device_error(dsmc_ctx* ctx, const RunResult& r, int K) {
+  ErrFlag e;
+  CU(cudaMemcpyAsync(&e, r.err, sizeof e, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (e.code) return set_err(ctx, e.code, err_message(e, K));
+  return DSMC_OK;
+}
+
+struct DevSeeds {
+  uint64_t* p = nullptr;
+};
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+int dsmc_create(int device, dsmc_ctx** out) {
+  if (!out) return DSMC_E_INVALID_ARGUMENT;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0)
+    return DSMC_E_NO_DEVICE;
+  auto* ctx = new dsmc_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return DSMC_E_NO_DEVICE;
+  }
+  for (auto& e : ctx->ev) cudaEventCreate(&e);
+  cudaMallocHost(&ctx->h_lnc, sizeof(double) * 4096);
+  *out = ctx;
+  return DSMC_OK;
+}
+
+void dsmc_destroy(dsmc_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->arena.release();
+  if (ctx->d_mean) cudaFree(ctx->d_mean);
+  if (ctx->d_cov) cudaFree(ctx->d_cov);
+  if (ctx->h_lnc) cudaFreeHost(ctx->h_lnc);
+  for (auto& e : ctx->ev) cudaEventDestroy(e);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* dsmc_last_error(const dsmc_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+uint64_t dsmc_kernel_launches(const dsmc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+void* dsmc_stream(dsmc_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+int dsmc_sync(dsmc_ctx* ctx) {
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DSMC_OK;
+}
+
+int dsmc_model_upload(dsmc_ctx* ctx, const dsmc_model_desc* model,
+                      dsmc_model_handle** out) {
+  if (!ctx || !out) return DSMC_E_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  return make_handle(ctx, model, 1, out);
+}
+
+void dsmc_model_free(dsmc_ctx* ctx, dsmc_model_handle* h) {
+  if (ctx) cudaStreamSynchronize(ctx->stream);
+  free_handle(h);
+}
+
+static int smooth_common(dsmc_ctx* ctx, dsmc_model_handle* h, const dsmc_smooth_opts* opts,
+                         double* d_paths, double* d_mean, double* d_cov, RunResult* res,
+                         bool timing) {
+  if (!opts) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "options are null");
+  RunOpts o;
+  o.precision = opts->precision;
+  o.resampler = opts->resampler;
+  o.mh_steps = opts->mh_steps;
+  o.N = opts->n_particles;
+  o.inj_x = opts->inject_states;
+  o.inj_lw = opts->inject_logw;
+  o.paths = d_paths;
+  o.mean = d_mean;
+  o.cov = d_cov;
+  o.timing = timing;
+  ctx->time_kernels = timing;
+  ctx->kev_used = 0;
+  void* p;
+  CU(ctx->arena.get("SEEDS", sizeof(uint64_t), &p));
+  CU(cudaMemcpyAsync(p, &opts->seed, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+  o.seeds = (const uint64_t*)p;
+  return run_tree(ctx, h, o, res);
+}
+
+int dsmc_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
+                const dsmc_smooth_opts* opts, dsmc_smooth_out* out) {
+  if (!ctx || !out) return DSMC_E_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  const auto t0 = std::chrono::steady_clock::now();
+  dsmc_model_handle* h = nullptr;
+  int rc = make_handle(ctx, model, 1, &h);
+  if (rc) return rc;
+  std::unique_ptr<dsmc_model_handle, void (*)(dsmc_model_handle*)> hold(h, free_handle);
+  const int K = h->K, d = h->d, T = K - 1;
+  const size_t N = opts ? opts->n_particles : 0;
+  void* p;
+  double *dp = nullptr, *dm = nullptr, *dc = nullptr;
+  if (out->paths) {
+    CU(ctx->arena.get("OPATH", (size_t)K * N * d * sizeof(double), &p));
+    dp = (double*)p;
+  }
+  if (out->mean) {
+    CU(ctx->arena.get("OMEAN", (size_t)K * d * sizeof(double), &p));
+    dm = (double*)p;
+  }
+  if (out->cov) {
+    CU(ctx->arena.get("OCOV", (size_t)K * d * d * sizeof(double), &p));
+    dc = (double*)p;
+  }
+  RunResult res;
+  rc = smooth_common(ctx, h, opts, dp, dm, dc, &res, false);
+  if (rc) return rc;
+  rc = check_device_error(ctx, res, K);
+  if (rc) return rc;
+  auto s = ctx->stream;
+  if (dp) CU(cudaMemcpyAsync(out->paths, dp, (size_t)K * N * d * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (dm) CU(cudaMemcpyAsync(out->mean, dm, (size_t)K * d * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (dc) CU(cudaMemcpyAsync(out->cov, dc, (size_t)K * d * d * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (out->pair_left && T > 0) {
+    CU(cudaMemcpyAsync(out->pair_left, res.PL, (size_t)T * N * 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(out->pair_right, res.PR, (size_t)T * N * 4, cudaMemcpyDeviceToHost, s));
+  }
+  if (out->log_mean_weight && T > 0)
+    CU(cudaMemcpyAsync(out->log_mean_weight, res.LMW, (size_t)T * 8, cudaMemcpyDeviceToHost, s));
+  if (out->leaf_states && res.X64 && opts->precision == DSMC_FP64_PARITY)
+    CU(cudaMemcpyAsync(out->leaf_states, res.X64, (size_t)K * N * d * 8, cudaMemcpyDeviceToHost, s));
+  double lnc;
+  unsigned long long evals = 0;
+  CU(cudaMemcpyAsync(&lnc, res.root_lnc, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&evals, res.evals, sizeof evals, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  const bool lazy = opts->resampler == DSMC_MH_LAZY || opts->resampler == DSMC_REJECTION_LAZY;
+  out->log_norm_const = lnc;
+  out->has_log_norm_const = !std::isnan(lnc);
+  out->levels = res.levels;
+  out->weight_evals = lazy ? evals : (uint64_t)T * N * N;
+  out->biased = opts->resampler == DSMC_MH_LAZY && T > 0;
+  out->wall_time_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return DSMC_OK;
+}
+
+int dsmc_smooth_resident(dsmc_ctx* ctx, const dsmc_model_handle* hc,
+                         const dsmc_smooth_opts* opts) {
+  if (!ctx || !hc || !opts) return DSMC_E_INVALID_ARGUMENT;
+  auto* h = const_cast<dsmc_model_handle*>(hc);
+  const int K = h->K, d = h->d;
+  if (ctx->last_K < K || ctx->last_d != d) {
+    if (ctx->d_mean) cudaFree(ctx->d_mean);
+    if (ctx->d_cov) cudaFree(ctx->d_cov);
+    CU(cudaMalloc(&ctx->d_mean, (size_t)K * d * sizeof(double)));
+    CU(cudaMalloc(&ctx->d_cov, (size_t)K * d * d * sizeof(double)));
+    ctx->last_K = K;
+    ctx->last_d = d;
+  }
+  RunResult res;
+  int rc = smooth_common(ctx, h, opts, nullptr, ctx->d_mean, ctx->d_cov, &res, true);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(ctx->h_lnc, res.root_lnc, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->last_levels = res.levels;
+  return DSMC_OK;
+}
+
+int dsmc_resident_results(dsmc_ctx* ctx, double* mean, double* cov,
+                          double* lnc, int* has_lnc) {
+  if (!ctx) return DSMC_E_INVALID_ARGUMENT;
+  const int K = ctx->last_K, d = ctx->last_d;
+  if (mean) CU(cudaMemcpyAsync(mean, ctx->d_mean, (size_t)K * d * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (cov) CU(cudaMemcpyAsync(cov, ctx->d_cov, (size_t)K * d * d * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (lnc) *lnc = ctx->h_lnc[0];
+  if (has_lnc) *has_lnc = !std::isnan(ctx->h_lnc[0]);
+  return DSMC_OK;
+}
+
+int dsmc_last_timings(const dsmc_ctx* ctx, double* ms, int cap) {
+  if (!ctx || cap < 3) return 0;
+  if (cap >= 6) {  // [3] pair-kernel ms, [4] sample-kernel ms, [5] pair launches
+    double pk = 0, sk = 0;
+    for (int i = 0; i + 2 < ctx->kev_used; i += 3) {
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, ctx->kev[i], ctx->kev[i + 1]);
+      cudaEventElapsedTime(&b, ctx->kev[i + 1], ctx->kev[i + 2]);
+      pk += a;
+      sk += b;
+    }
+    ms[3] = pk;
+    ms[4] = sk;
+    ms[5] = ctx->kev_used / 3;
+  }
+  float a = 0, b2 = 0, c = 0;
+  cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+  cudaEventElapsedTime(&b2, ctx->ev[1], ctx->ev[2]);
+  cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
+  ms[0] = a;
+  ms[1] = b2;
+  ms[2] = c;
+  return cap >= 6 ? 6 : 3;
+}
+
+// ------------------------------------------------------------ table path
+__global__ void table_rows_kernel(const double* logw, int n, double* ws, ErrFlag* err) {
+  // one warp per row: max, sub-block sums (8-lane), raw total
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 8 + warp;
+  if (i >= n) return;
+  const int nsub = (n + kSub - 1) / kSub;
+  double *wm = ws, *wraw = ws + n, *wsub = ws + 5 * (size_t)n;
+  const double* row = logw + (size_t)i * n;
+  double mx = -CUDART_INF;
+  int nan = 0;
+  for (int j = lane; j < n; j += 32) {
+    nan |= isnan(row[j]);
+    mx = fmax(mx, row[j]);
+  }
+  for (int o = 16; o; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(~0u, mx, o));
+    nan |= __shfl_xor_sync(~0u, nan, o);
+  }
+  if (nan) {
+    if (lane == 0) raise_err(err, DSMC_E_DOMAIN, 0, 1, kReasonNaN);
+    mx = -CUDART_INF;
+  }
+  if (lane == 0) wm[i] = mx;
+  double* srow = wsub + (size_t)i * nsub;
+  if (mx == -CUDART_INF) {
+    for (int s = lane; s < nsub; s += 32) srow[s] = 0.0;
+    if (lane == 0) wraw[i] = 0.0;
+    return;
+  }
+  const int grp = lane >> 3, l8 = lane & 7;
+  for (int s0 = 0; s0 < nsub; s0 += 4) {
+    const int s = s0 + grp;
+    const bool act = s < nsub;
+    const int j0 = s * kSub;
+    const int len = act ? min(kSub, n - j0) : 0;
+    const int len8 = len & ~7;
+    double acc = 0.0;
+    for (int q = 0; q < len8; q += 8) acc = DADD(acc, exp_w(DSUB(row[j0 + q + l8], mx)));
+    double a8[8];
+    for (int l = 0; l < 8; ++l) a8[l] = __shfl_sync(~0u, acc, (lane & ~7) + l);
+    if (act && l8 == 0) {
+      double bs = combine8(a8);
+      for (int j = j0 + len8; j < j0 + len; ++j) bs = DADD(bs, exp_w(DSUB(row[j], mx)));
+      srow[s] = bs;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double tot = 0.0;
+    for (int s = 0; s < nsub; ++s) tot = DADD(tot, srow[s]);
+    wraw[i] = tot;
+  }
+}
+
+__global__ void table_sample_kernel(const double* logw, int n, int n_out, double* ws,
+                                    uint64_t seed, uint32_t level, uint64_t node,
+                                    int systematic, uint32_t* left, uint32_t* right,
+                                    double* lmw_out, ErrFlag* err) {
+  __shared__ double red[32];
+  __shared__ double s_g, s_grand;
+  __shared__ double a8s[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nsub = (n + kSub - 1) / kSub;
+  double *wm = ws, *wraw = ws + n, *wscale = ws + 2 * (size_t)n, *wtot = ws + 3 * (size_t)n,
+         *wpre = ws + 4 * (size_t)n, *wsub = ws + 5 * (size_t)n;
+  double mx = -CUDART_INF;
+  for (int i = tid; i < n; i += blockDim.x) mx = fmax(mx, wm[i]);
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(~0u, mx, o));
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double v = -CUDART_INF;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+    s_g = v;
+  }
+  __syncthreads();
+  const double gmax = s_g;
+  if (gmax == -CUDART_INF) {
+    if (tid == 0) raise_err(err, DSMC_E_RUNTIME, 0, 1, kReasonZeroTable);
+    return;
+  }
+  for (int i = tid; i < n; i += blockDim.x) {
+    const double sc = exp_w(DSUB(wm[i], gmax));
+    wscale[i] = sc;
+    wtot[i] = DMUL(sc, wraw[i]);
+  }
+  __syncthreads();
+  const int n8 = n & ~7;
+  if (tid < 8) {
+    double acc = 0.0;
+    for (int i = tid; i < n8; i += 8) acc = DADD(acc, wtot[i]);
+    a8s[tid] = acc;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a8[8];
+    for (int l = 0; l < 8; ++l) a8[l] = a8s[l];
+    double tot = combine8(a8);
+    for (int i = n8; i < n; ++i) tot = DADD(tot, wtot[i]);
+    s_grand = tot;
+    double cum = 0.0;
+    for (int i = 0; i < n; ++i) {
+      cum = DADD(cum, wtot[i]);
+      wpre[i] = cum;
+    }
+    *lmw_out = DADD(gmax, log(tot));
+  }
+  __syncthreads();
+  const double grand = s_grand;
+  const StreamId id = stream_id(seed, level, node, DSMC_ROLE_PAIR_RESAMPLE, 0);
+  double u0 = 0.0, step = 0.0;
+  if (systematic) {
+    u0 = u64_uniform(stream_u64(id, 0));
+    step = DDIV(grand, (double)n_out);
+  }
+  for (int m = tid; m < n_out; m += blockDim.x) {
+    const double pt = systematic ? DMUL(DADD(u0, (double)m), step)
+                                 : DMUL(u64_uniform(stream_u64(id, m)), grand);
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (pt < wpre[mid]) hi = mid;
+      else lo = mid + 1;
+    }
+    const int i = lo < n ? lo : n - 1;
+    const double before = i > 0 ? wpre[i - 1] : 0.0;
+    int row = i;
+    while (row > 0 && wtot[row] <= 0.0) --row;
+    double local = DDIV(DSUB(pt, before), wscale[row]);
+    if (!(local >= 0.0)) local = 0.0;
+    const double* srow = wsub + (size_t)row * nsub;
+    int s = 0;
+    double c2b = 0.0, c2 = srow[0];
+    while (!(local < c2) && s + 1 < nsub) {
+      c2b = c2;
+      ++s;
+      c2 = DADD(c2, srow[s]);
+    }
+    const double* lrow = logw + (size_t)row * n;
+    const double mrow = wm[row];
+    const int j0 = s * kSub, j1 = min(j0 + kSub, n);
+    double c3 = c2b;
+    int j = j0;
+    for (; j < j1; ++j) {
+      c3 = DADD(c3, exp_w(DSUB(lrow[j], mrow)));
+      if (local < c3) break;
+    }
+    if (j == j1) {
+      j = j1 - 1;
+      while (j > 0 && !(exp_w(DSUB(lrow[j], mrow)) > 0.0)) --j;
+    }
+    left[m] = (uint32_t)row;
+    right[m] = (uint32_t)j;
+  }
+}
+
+__global__ void table_lazy_kernel(const double* logw, int n, int n_out, int mh,
+                                  size_t mh_steps, double bound, uint64_t seed,
+                                  uint32_t level, uint64_t node, uint32_t* left,
+                                  uint32_t* right, unsigned long long* evals_out,
+                                  ErrFlag* err) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long evals = 0;
+  if (m < n_out) {
+    StreamReader s;
+    s.init(stream_id(seed, level, node, DSMC_ROLE_PAIR_RESAMPLE, m + 1));
+    uint32_t oi = 0, oj = 0;
+    if (mh) {
+      uint32_t i = (uint32_t)(m % n), j = i;
+      double cur = 0.0;
+      bool have = false;
+      for (size_t st = 0; st < mh_steps; ++st) {
+        const uint32_t pi = (uint32_t)s.index(n), pj = (uint32_t)s.index(n);
+        const double lu = log(s.uniform_pos());
+        if (!have) {
+          cur = logw[(size_t)i * n + j];
+          ++evals;
+          have = true;
+        }
+        const double prop = logw[(size_t)pi * n + pj];
+        ++evals;
+        if (isnan(prop) || isnan(cur)) raise_err(err, DSMC_E_INVALID_ARGUMENT, 0, 1, kReasonNaN);
+        if (lu < DSUB(prop, cur)) {
+          i = pi;
+          j = pj;
+          cur = prop;
+        }
+      }
+      oi = i;
+      oj = j;
+    } else {
+      bool ok = false;
+      for (uint64_t trial = 0; trial < (1u << 24); ++trial) {
+        const uint32_t i = (uint32_t)s.index(n), j = (uint32_t)s.index(n);
+        const double lw = logw[(size_t)i * n + j];
+        ++evals;
+        if (isnan(lw)) {
+          raise_err(err, DSMC_E_INVALID_ARGUMENT, 0, 1, kReasonNaN);
+          break;
+        }
+        if (DSUB(lw, bound) > 1e-9) {
+          raise_err(err, DSMC_E_INVALID_ARGUMENT, 0, 1, kReasonOverBound);
+          break;
+        }
+        if (log(s.uniform_pos()) <= DSUB(lw, bound)) {
+          oi = i;
+          oj = j;
+          ok = true;
+          break;
+        }
+      }
+      if (!ok) raise_err(err, DSMC_E_RUNTIME, 0, 1, kReasonTrialCap);
+    }
+    left[m] = oi;
+    right[m] = oj;
+  }
+  for (int o = 16; o; o >>= 1) evals += __shfl_xor_sync(~0u, evals, o);
+  if ((threadIdx.x & 31) == 0 && evals) atomicAdd(evals_out, evals);
+}
+
+int dsmc_resample_table(dsmc_ctx* ctx, int resampler, const double* logw, size_t n,
+                        size_t n_out, size_t mh_steps, int has_bound, double bound,
+                        uint64_t seed, uint32_t level, uint64_t node, uint32_t* left,
+                        uint32_t* right, double* lmw, int* has_lmw,
+                        uint64_t* weight_evals, int* biased) {
+  if (!ctx) return DSMC_E_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (n == 0) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "pair weight source has n == 0");
+  if (resampler < 0 || resampler > 3) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "unknown resampler");
+  const bool lazy = resampler >= 2;
+  if (resampler == DSMC_REJECTION_LAZY && (!has_bound || !std::isfinite(bound)))
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                   "rejection resampling requires a finite log_upper_bound");
+  Arena& A = ctx->arena;
+  void* p;
+  auto s = ctx->stream;
+  CU(A.get("TLOGW", n * n * 8, &p));
+  double* dlw = (double*)p;
+  CU(cudaMemcpyAsync(dlw, logw, n * n * 8, cudaMemcpyHostToDevice, s));
+  CU(A.get("TOUT", std::max<size_t>(1, n_out) * 8, &p));
+  uint32_t* dl = (uint32_t*)p;
+  uint32_t* dr = dl + std::max<size_t>(1, n_out);
+  CU(A.get("TMISC", 64, &p));
+  ErrFlag* derr = (ErrFlag*)p;
+  double* dlmw = (double*)((char*)p + 16);
+  unsigned long long* devals = (unsigned long long*)((char*)p + 24);
+  CU(cudaMemsetAsync(p, 0, 64, s));
+  if (lazy) {
+    if (!(resampler == DSMC_MH_LAZY && mh_steps == 0) && n_out > 0) {
+      table_lazy_kernel<<<(n_out + 127) / 128, 128, 0, s>>>(
+          dlw, (int)n, (int)n_out, resampler == DSMC_MH_LAZY, mh_steps, bound, seed, level,
+          node, dl, dr, devals, derr);
+      LAUNCHED(ctx);
+    }
+  } else {
+    const int nsub = ((int)n + kSub - 1) / kSub;
+    CU(A.get("TWS", n * (5 + nsub) * 8, &p));
+    double* ws = (double*)p;
+    table_rows_kernel<<<(n + 7) / 8, 256, 0, s>>>(dlw, (int)n, ws, derr);
+    LAUNCHED(ctx);
+    table_sample_kernel<<<1, 256, 0, s>>>(dlw, (int)n, (int)n_out, ws, seed, level, node,
+                                          resampler == DSMC_SYSTEMATIC, dl, dr, dlmw, derr);
+    LAUNCHED(ctx);
+  }
+  CU(cudaGetLastError());
+  ErrFlag e;
+  double lm = NAN;
+  unsigned long long ev = 0;
+  CU(cudaMemcpyAsync(&e, derr, sizeof e, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&lm, dlmw, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&ev, devals, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (e.code) {
+    const char* msg = e.reason == kReasonZeroTable
+                          ? "all pair weights are zero; the blocks share no support under the model"
+                      : e.reason == kReasonTrialCap
+                          ? "rejection resampling exceeded the trial cap; the bound is far too "
+                            "loose or the weights are degenerate"
+                      : e.reason == kReasonOverBound ? "pair weight exceeds its stated upper bound"
+                      : e.reason == kReasonNaN ? (lazy ? "pair weight is NaN" : "reduce_max: NaN entry")
+                                               : "device error";
+    return set_err(ctx, e.code, msg);
+  }
+  if (lazy && resampler == DSMC_MH_LAZY && mh_steps == 0) {
+    for (size_t m = 0; m < n_out; ++m) left[m] = right[m] = (uint32_t)(m % n);
+  } else if (n_out) {
+    CU(cudaMemcpy(left, dl, n_out * 4, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(right, dr, n_out * 4, cudaMemcpyDeviceToHost));
+  }
+  *has_lmw = lazy ? 0 : 1;
+  *lmw = lazy ? NAN : lm;
+  *weight_evals = lazy ? ev : (uint64_t)n * n;
+  *biased = resampler == DSMC_MH_LAZY;
+  return DSMC_OK;
+}
+
+// --------------------------------------------------------------- probes
+__global__ void philox_kernel(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3,
+                              uint64_t k0, uint64_t k1, size_t nb, uint64_t* out) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= nb) return;
+  const U64x4 r = philox_k(c0 + i, c1, c2, c3, k0, k1);
+  for (int q = 0; q < 4; ++q) out[4 * i + q] = r.v[q];
+}
+__global__ void expw_kernel(const double* x, size_t n, double* out) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = exp_w(x[i]);
+}
+
+int dsmc_philox_blocks(dsmc_ctx* ctx, const uint64_t ctr[4], const uint64_t key[2],
+                       size_t nb, uint64_t* out) {
+  if (!ctx) return DSMC_E_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  void* p;
+  CU(ctx->arena.get("PHX", nb * 32 + 32, &p));
+  philox_kernel<<<(nb + 127) / 128, 128, 0, ctx->stream>>>(ctr[0], ctr[1], ctr[2], ctr[3],
+                                                           key[0], key[1], nb, (uint64_t*)p);
+  LAUNCHED(ctx);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(out, p, nb * 32, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DSMC_OK;
+}
+
+int dsmc_exp_w(dsmc_ctx* ctx, const double* x, size_t n, double* out) {
+  if (!ctx) return DSMC_E_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  void* p;
+  CU(ctx->arena.get("EXPW", 2 * n * 8 + 16, &p));
+  double* dx = (double*)p;
+  double* dy = dx + n;
+  CU(cudaMemcpyAsync(dx, x, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  expw_kernel<<<(n + 255) / 256, 256, 0, ctx->stream>>>(dx, n, dy);
+  LAUNCHED(ctx);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(out, dy, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DSMC_OK;
+}
+
+// ----------------------------------------------------------- conditional
+int dsmc_conditional_sweep(dsmc_ctx* ctx, const dsmc_model_desc* models, int B,
+                           const double* refs, const uint64_t* seeds,
+                           const dsmc_cond_opts* opts, uint32_t sweep,
+                           double* out_paths, uint8_t* changed, double* lnc_out,
+                           uint64_t* weight_evals) {
+  if (!ctx || !models || B < 1 || !refs || !seeds || !opts || !out_paths)
+    return DSMC_E_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  dsmc_model_handle* h = nullptr;
+  int rc = make_handle(ctx, models, B, &h);
+  if (rc) return rc;
+  std::unique_ptr<dsmc_model_handle, void (*)(dsmc_model_handle*)> hold(h, free_handle);
+  const int K = h->K, d = h->d, T = K - 1;
+  const size_t N = opts->n_particles;
+  Arena& A = ctx->arena;
+  void* p;
+  auto s = ctx->stream;
+  CU(A.get("CSTAR", (size_t)B * K * d * 8, &p));
+  double* dstar = (double*)p;
+  CU(cudaMemcpyAsync(dstar, refs, (size_t)B * K * d * 8, cudaMemcpyHostToDevice, s));
+  CU(A.get("CSEED", (size_t)B * 8, &p));
+  uint64_t* dseeds = (uint64_t*)p;
+  CU(cudaMemcpyAsync(dseeds, seeds, (size_t)B * 8, cudaMemcpyHostToDevice, s));
+  CU(A.get("COUT", (size_t)B * K * d * 8, &p));
+  double* dout = (double*)p;
+  CU(A.get("CCHG", (size_t)B * K, &p));
+  uint8_t* dchg = (uint8_t*)p;
+  RunOpts o;
+  o.precision = opts->precision;
+  o.resampler = opts->resampler;
+  o.N = N;
+  o.conditional = 1;
+  o.sweep = sweep;
+  o.inj_x = opts->inject_states;
+  o.star = dstar;
+  o.seeds = dseeds;
+  o.star_out = dout;
+  o.changed = dchg;
+  RunResult res;
+  rc = run_tree(ctx, h, o, &res);
+  if (rc) return rc;
+  rc = check_device_error(ctx, res, K);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(out_paths, dout, (size_t)B * K * d * 8, cudaMemcpyDeviceToHost, s));
+  if (changed) CU(cudaMemcpyAsync(changed, dchg, (size_t)B * K, cudaMemcpyDeviceToHost, s));
+  std::vector<double> lnc(B);
+  std::vector<unsigned long long> ev(B);
+  for (int c = 0; c < B; ++c)
+    CU(cudaMemcpyAsync(&lnc[c], res.root_lnc + (size_t)c * res.lnc_stride, 8,
+                       cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(ev.data(), res.evals, (size_t)B * 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  const bool lazy = opts->resampler == DSMC_REJECTION_LAZY;
+  for (int c = 0; c < B; ++c) {
+    if (lnc_out) lnc_out[c] = lnc[c];
+    if (weight_evals) weight_evals[c] = lazy ? ev[c] + (uint64_t)T : (uint64_t)T * (N * N + 1);
+  }
+  return DSMC_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ SV pGibbs
+namespace {
+
+// gamma_draw (pgibbs.cpp:80-102), Marsaglia-Tsang with the shape<1 boost.
+__device__ double gamma_draw_dev(double shape, double rate, StreamReader& s) {
+  double boost = 1.0;
+  if (shape < 1.0) {
+    boost = pow(s.uniform_pos(), 1.0 / shape);
+    shape += 1.0;
+  }
+  const double d = shape - 1.0 / 3.0;
+  const double c = 1.0 / sqrt(9.0 * d);
+  for (int guard = 0; guard < 100000; ++guard) {
+    double x, v;
+    do {
+      x = s.normal();
+      v = 1.0 + c * x;
+    } while (v <= 0.0);
+    v = v * v * v;
+    const double u = s.uniform_pos();
+    if (log(u) < 0.5 * x * x + d - d * v + d * log(v)) return boost * d * v / rate;
+  }
+  return CUDART_NAN;
+}
+
+__device__ double sv_loglik(const double* x, int T, double mu, double phi, double s2) {
+  const double v0 = s2 / (1.0 - phi * phi);
+  double ll = dlog_normal_pdf(x[0], mu, v0);
+  for (int t = 1; t <= T; ++t) ll += dlog_normal_pdf(x[t], mu + phi * (x[t - 1] - mu), s2);
+  return ll;
+}
+
+// SV ParamKernel (oracle or_sv_param_update): sigma2 | rest
+// (inverse gamma), mu | rest (normal), random-walk Metropolis on phi. One
+// thread per chain, sequential sums (same order as the oracle).
+__global__ void sv_param_kernel(DevModel* models, double* theta, const double* stars,
+                                const uint64_t* seeds, dsmc_sv_prior pr, int T,
+                                uint32_t sweep, int B, unsigned long long* acc_phi) {
+  const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ch >= B) return;
+  const double* x = stars + (size_t)ch * (T + 1);
+  StreamReader s;
+  s.init(stream_id(seeds[ch], 0, sweep, DSMC_ROLE_GIBBS_PARAM, 0));
+  double mu = theta[3 * ch], phi = theta[3 * ch + 1], s2 = theta[3 * ch + 2];
+  double ss = (1.0 - phi * phi) * (x[0] - mu) * (x[0] - mu);
+  for (int t = 1; t <= T; ++t) {
+    const double e = x[t] - mu - phi * (x[t - 1] - mu);
+    ss += e * e;
+  }
+  const double prec = gamma_draw_dev(pr.s2_shape + 0.5 * (double)(T + 1), pr.s2_rate + 0.5 * ss, s);
+  s2 = 1.0 / prec;
+  const double p = 1.0 / pr.mu_var + (1.0 - phi * phi) / s2 +
+                   (double)T * (1.0 - phi) * (1.0 - phi) / s2;
+  double acc = 0.0;
+  for (int t = 1; t <= T; ++t) acc += x[t] - phi * x[t - 1];
+  const double h = pr.mu_mean / pr.mu_var + (1.0 - phi * phi) * x[0] / s2 + (1.0 - phi) * acc / s2;
+  mu = h / p + sqrt(1.0 / p) * s.normal();
+  const double prop = phi + pr.phi_step * s.normal();
+  const double lu = log(s.uniform_pos());
+  if (fabs(prop) < 1.0) {
+    const double dl = sv_loglik(x, T, mu, prop, s2) - sv_loglik(x, T, mu, phi, s2);
+    if (lu < dl) {
+      phi = prop;
+      atomicAdd(acc_phi, 1ull);
+    }
+  }
+  theta[3 * ch] = mu;
+  theta[3 * ch + 1] = phi;
+  theta[3 * ch + 2] = s2;
+  models[ch].sv_mu = mu;
+  models[ch].sv_phi = phi;
+  models[ch].sv_s2 = s2;
+}
+
+}  // namespace
+
+extern "C" int dsmc_sv_pgibbs_sweep(dsmc_ctx* ctx, int B, int T, const double* ys,
+                                    const dsmc_sv_prior* prior, double* theta,
+                                    double* stars, const uint64_t* seeds, size_t N,
+                                    int resampler, uint32_t sweep, uint8_t* changed,
+                                    uint64_t* accepted_phi) {
+  if (!ctx || B < 1 || T < 0 || !ys || !prior || !theta || !stars || !seeds)
+    return DSMC_E_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  std::vector<dsmc_model_desc> descs(B);
+  for (int c = 0; c < B; ++c) {
+    dsmc_model_desc& m = descs[c];
+    std::memset(&m, 0, sizeof m);
+    m.kind = DSMC_MODEL_SV;
+    m.state_dim = 1;
+    m.obs_dim = 1;
+    m.horizon = T;
+    m.y = ys;
+    m.sv_mu = theta[3 * c];
+    m.sv_phi = theta[3 * c + 1];
+    m.sv_sigma2 = theta[3 * c + 2];
+  }
+  dsmc_model_handle* h = nullptr;
+  int rc = make_handle(ctx, descs.data(), B, &h);  // prep runs again below
+  if (rc) return rc;
+  std::unique_ptr<dsmc_model_handle, void (*)(dsmc_model_handle*)> hold(h, free_handle);
+  const int K = T + 1;
+  Arena& A = ctx->arena;
+  void* p;
+  auto s = ctx->stream;
+  CU(A.get("GSTAR", (size_t)B * K * 8, &p));
+  double* dstar = (double*)p;
+  CU(cudaMemcpyAsync(dstar, stars, (size_t)B * K * 8, cudaMemcpyHostToDevice, s));
+  CU(A.get("GTHETA", (size_t)B * 3 * 8, &p));
+  double* dtheta = (double*)p;
+  CU(cudaMemcpyAsync(dtheta, theta, (size_t)B * 3 * 8, cudaMemcpyHostToDevice, s));
+  CU(A.get("GSEED", (size_t)B * 8, &p));
+  uint64_t* dseeds = (uint64_t*)p;
+  CU(cudaMemcpyAsync(dseeds, seeds, (size_t)B * 8, cudaMemcpyHostToDevice, s));
+  CU(A.get("GACC", 8, &p));
+  unsigned long long* dacc = (unsigned long long*)p;
+  CU(cudaMemsetAsync(dacc, 0, 8, s));
+  CU(A.get("GOUT", (size_t)B * K * 8, &p));
+  double* dout = (double*)p;
+  CU(A.get("GCHG", (size_t)B * K, &p));
+  uint8_t* dchg = (uint8_t*)p;
+  // parameter kernel (pgibbs_sweep: param_kernel then model rebuild)
+  sv_param_kernel<<<(B + 63) / 64, 64, 0, s>>>(h->models_dev, dtheta, dstar, dseeds, *prior, T,
+                                               sweep, B, dacc);
+  LAUNCHED(ctx);
+  std::vector<int> ones(B, 3);
+  CU(cudaMemcpyAsync(h->bounded, ones.data(), sizeof(int) * B, cudaMemcpyHostToDevice, s));
+  prep_kernel<<<dim3((K + 127) / 128, B), 128, 0, s>>>(h->models_dev, h->tc, K, h->bounded);
+  LAUNCHED(ctx);
+  RunOpts o;
+  o.precision = DSMC_FP32;
+  o.resampler = resampler;
+  o.N = N;
+  o.conditional = 1;
+  o.sweep = sweep;
+  o.star = dstar;
+  o.seeds = dseeds;
+  o.star_out = dout;
+  o.changed = dchg;
+  RunResult res;
+  rc = run_tree(ctx, h, o, &res);
+  if (rc) return rc;
+  rc = check_device_error(ctx, res, K);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(stars, dout, (size_t)B * K * 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(theta, dtheta, (size_t)B * 3 * 8, cudaMemcpyDeviceToHost, s));
+  if (changed) CU(cudaMemcpyAsync(changed, dchg, (size_t)B * K, cudaMemcpyDeviceToHost, s));
+  unsigned long long acc = 0;
+  CU(cudaMemcpyAsync(&acc, dacc, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (accepted_phi) *accepted_phi = acc;
+  return DSMC_OK;
+}

@@ -1,0 +1,337 @@
+// Leaf kernels (make_leaf, smoother.cpp:98-130; conditional_leaf,
+// conditional.cpp:52-87). One thread per (particle, time, chain).
+#pragma once
+
+#include <math_constants.h>
+
+#include "kernels64.cuh"
+
+namespace dsmc_dev {
+
+struct Bufs {
+  int K, T, N, d, B, cap;  // cap: map capacity (blocks) per chain
+  const DevModel* models;  // [B]
+  const uint64_t* seeds;   // [B]
+  const TimeConst* tc;     // [B][K]
+  const int* bounded;      // [B] bit0: every cut has a finite bound
+  // FP64 path
+  double* X64;   // [B][K][N][d]
+  double* LW64;  // [B][K][N] normalised
+  // FP32 path
+  float4* X32;   // [B][K][N] centred states
+  float* COL;    // [B][K][N] column terms (log2 units)
+  float* LW32;   // [B][N] leaf-0 normalised weights (log2 units)
+  // leaf meta
+  double* LNC;   // [B][K]
+  uint8_t* UNI;  // [B][K]
+  double* LWMAX; // [B][K] max normalised leaf log weight (rejection bound)
+  // pairs
+  uint32_t* PL;  // [B][T][N]
+  uint32_t* PR;
+  double* LMW;   // [B][T]
+  ErrFlag* err;
+  unsigned long long* evals;  // [B]
+  int conditional;
+  uint32_t sweep;
+  const double* star;  // [B][K][d] (conditional)
+};
+
+// Normal number i of a leaf stream (rng.cpp:74-86 via counter addressing:
+// normal i consumes u64s 2*(i/2) (uniform_pos) and 2*(i/2)+1 (uniform);
+// even i -> r cos(theta), odd i -> r sin(theta)).
+__device__ inline double leaf_normal64(const StreamId& id, uint64_t i) {
+  const uint64_t q = 2 * (i >> 1);
+  const U64x4 blk = stream_block(id, q >> 2);
+  const double u1 = u64_uniform_pos(blk.v[q & 3]);
+  const double u2 = u64_uniform(blk.v[(q & 3) + 1]);
+  const double r = sqrt(DMUL(-2.0, log(u1)));
+  const double th = DMUL(2.0 * 3.14159265358979323846, u2);
+  return (i & 1) ? DMUL(r, sin(th)) : DMUL(r, cos(th));
+}
+
+__device__ inline uint64_t leaf_node(int t, int conditional, uint32_t sweep) {
+  return conditional ? (static_cast<uint64_t>(static_cast<uint32_t>(t)) |
+                        (static_cast<uint64_t>(sweep) << 32))
+                     : static_cast<uint64_t>(t);
+}
+
+// FP64 leaf: states and RAW log weights (log_init_weight, fk_model.cpp:43-59).
+__global__ void leaf64_kernel(Bufs b, const double* inj_x, const double* inj_lw) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y, ch = blockIdx.z;
+  if (n >= b.N) return;
+  const DevModel& M = b.models[ch];
+  const TimeConst& tc = b.tc[(size_t)ch * b.K + t];
+  const int d = b.d;
+  double x[4] = {0, 0, 0, 0};
+  const size_t off = ((size_t)ch * b.K + t) * b.N + n;
+  if (b.conditional && n == 0) {
+    for (int k = 0; k < d; ++k) x[k] = b.star[((size_t)ch * b.K + t) * d + k];
+  } else if (inj_x) {
+    for (int k = 0; k < d; ++k) x[k] = inj_x[off * d + k];
+  } else {
+    const StreamId id = stream_id(b.seeds[ch], 0, leaf_node(t, b.conditional, b.sweep),
+                                  DSMC_ROLE_LEAF_PROPOSAL, 0);
+    const uint64_t p = b.conditional ? n - 1 : n;
+    double z[4];
+    for (int k = 0; k < d; ++k) z[k] = leaf_normal64(id, p * d + k);
+    if (M.kind == DSMC_MODEL_SV) {
+      x[0] = DSUB(DMUL(2.0, tc.logabsy), log(DMUL(z[0], z[0])));
+    } else if (d == 1 && M.dy == 1) {
+      const double sd = sqrt(M.prop_cov[t]);
+      x[0] = DADD(M.prop_mean[t], DMUL(sd, z[0]));
+    } else {
+      for (int k = 0; k < d; ++k) {
+        double acc = 0.0;
+        for (int l = 0; l <= k; ++l) acc = DADD(acc, DMUL(tc.pL[k * d + l], z[l]));
+        x[k] = DADD(tc.pm[k], acc);
+      }
+    }
+  }
+  for (int k = 0; k < d; ++k) b.X64[off * d + k] = x[k];
+  double w;
+  if (inj_lw && !b.conditional) {
+    w = inj_lw[off];
+  } else if (t == 0) {
+    double W0[16], norm0 = 0.0;
+    if (M.kind == DSMC_MODEL_LGSSM && !(d == 1 && M.dy == 1)) {
+      double L0[16];
+      dchol(M.P0, d, L0);
+      dtri_inv(L0, d, W0);
+      norm0 = dnorm_of(L0, d);
+    }
+    const double pot = cb_log_h(M, tc, 0, x);
+    const double p0 = cb_init_logdensity(M, tc, x, W0, norm0);
+    const double q = cb_prop_logdensity(M, tc, 0, x);
+    w = DSUB(DADD(pot, p0), q);
+    if (pot == -CUDART_INF || p0 == -CUDART_INF) w = -CUDART_INF;
+  } else {
+    const double nu = cb_prop_logdensity(M, tc, t, x);
+    const double q = nu;  // aux == proposal for every device model
+    w = nu == -CUDART_INF ? -CUDART_INF : DSUB(nu, q);
+  }
+  if (isnan(w)) raise_err(b.err, DSMC_E_INVALID_ARGUMENT, t, 0, kReasonNaN);
+  b.LW64[off] = w;
+}
+
+// Leaf normalisation (smoother.cpp:117-128): one warp per (time, chain).
+// LSE with the 8-lane contract (kernels.cpp:46-55), weights_uniform iff
+// min == max, log_norm_const = lse - log N.
+__global__ void leafnorm64_kernel(Bufs b) {
+  const int t = blockIdx.x, ch = blockIdx.y, lane = threadIdx.x;
+  const int N = b.N;
+  double* lw = b.LW64 + ((size_t)ch * b.K + t) * N;
+  double mx = -CUDART_INF, lo = CUDART_INF, hi = -CUDART_INF;
+  int nan = 0;
+  for (int i = lane; i < N; i += 32) {
+    const double v = lw[i];
+    nan |= isnan(v);
+    if (v > mx) mx = v;
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+  for (int o = 16; o; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(~0u, mx, o));
+    lo = fmin(lo, __shfl_xor_sync(~0u, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(~0u, hi, o));
+    nan |= __shfl_xor_sync(~0u, nan, o);
+  }
+  if (nan) {
+    if (lane == 0) raise_err(b.err, DSMC_E_DOMAIN, t, 0, kReasonNaN);
+    return;
+  }
+  if (b.conditional && lw[0] == -CUDART_INF) {
+    if (lane == 0) raise_err(b.err, DSMC_E_INVALID_ARGUMENT, t, 0, kReasonRefLeaf);
+    return;
+  }
+  if (mx == -CUDART_INF) {
+    if (lane == 0) raise_err(b.err, DSMC_E_RUNTIME, t, 0, kReasonLeafZero);
+    return;
+  }
+  const int n8 = N & ~7;
+  double acc = 0.0;
+  if (lane < 8)
+    for (int i = lane; i < n8; i += 8) acc = DADD(acc, exp_w(DSUB(lw[i], mx)));
+  double a8[8];
+  for (int l = 0; l < 8; ++l) a8[l] = __shfl_sync(~0u, acc, l);
+  double lse = 0.0;
+  if (lane == 0) {
+    double tot = combine8(a8);
+    for (int i = n8; i < N; ++i) tot = DADD(tot, exp_w(DSUB(lw[i], mx)));
+    lse = DADD(mx, log(tot));
+  }
+  lse = __shfl_sync(~0u, lse, 0);
+  const double nl = -lse;
+  __syncwarp();
+  for (int i = lane; i < N; i += 32) lw[i] = DADD(lw[i], nl);
+  if (lane == 0) {
+    const size_t o = (size_t)ch * b.K + t;
+    b.LNC[o] = DSUB(lse, log((double)N));
+    b.UNI[o] = lo == hi;
+    b.LWMAX[o] = DADD(mx, nl);
+  }
+}
+
+// FP32 leaf: centred state x - m_t = L_t z (float4), column term
+// log2e * (log h_t - log nu_t + log N-normaliser of the transition into t)
+// written from z directly (no cancellation), leaf-0 raw weight in
+// FP64. For every device model q_t = nu_t, so leaves t >= 1 are uniform.
+__global__ void leaf32_kernel(Bufs b, double* raw0) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y, ch = blockIdx.z;
+  if (n >= b.N) return;
+  const DevModel& M = b.models[ch];
+  const TimeConst& tc = b.tc[(size_t)ch * b.K + t];
+  const int d = b.d;
+  const size_t off = ((size_t)ch * b.K + t) * b.N + n;
+  float z[4] = {0.f, 0.f, 0.f, 0.f};
+  float4 xs = make_float4(0.f, 0.f, 0.f, 0.f);
+  float col;
+  const bool is_star = b.conditional && n == 0;
+  double xstar[4] = {0, 0, 0, 0};
+  if (is_star) {
+    for (int k = 0; k < d; ++k) xstar[k] = b.star[((size_t)ch * b.K + t) * d + k];
+  } else {
+    const StreamId id = stream_id(b.seeds[ch], 0, leaf_node(t, b.conditional, b.sweep),
+                                  DSMC_ROLE_LEAF_PROPOSAL, 0);
+    const uint64_t p = b.conditional ? n - 1 : n;
+    // d normals from ceil(d/2)... counter-addressed Box-Muller pairs
+    for (int k = 0; k < d; ++k) {
+      const uint64_t i = p * d + k;
+      const uint64_t q = 2 * (i >> 1);
+      const U64x4 blk = stream_block(id, q >> 2);
+      const float u1 = (float)u64_uniform_pos(blk.v[q & 3]);
+      const float u2 = (float)u64_uniform(blk.v[(q & 3) + 1]);
+      const float r = sqrtf(-2.0f * __logf(u1));
+      float s, c;
+      sincospif(2.0f * u2, &s, &c);
+      z[k] = (i & 1) ? r * s : r * c;
+    }
+  }
+  float xv[4] = {0.f, 0.f, 0.f, 0.f};
+  if (M.kind == DSMC_MODEL_SV) {
+    const double xd = is_star ? xstar[0]
+                              : DSUB(DMUL(2.0, tc.logabsy), (double)__logf(z[0] * z[0]));
+    xv[0] = (float)xd;
+    col = (float)(kLog2E * tc.shift1);
+  } else {
+    if (is_star) {
+      // z = W_P (x* - m_t): the reference state expressed in proposal units
+      double e[4];
+      for (int k = 0; k < d; ++k) e[k] = xstar[k] - tc.pm[k];
+      for (int k = 0; k < d; ++k) {
+        double acc = 0.0;
+        for (int l = 0; l <= k; ++l) acc += tc.pW[k * d + l] * e[l];
+        z[k] = (float)acc;
+      }
+      for (int k = 0; k < d; ++k) xv[k] = (float)e[k];
+    } else {
+      for (int k = 0; k < d; ++k) {
+        float acc = 0.f;
+        for (int l = 0; l <= k; ++l) acc = fmaf((float)tc.pL[k * d + l], z[l], acc);
+        xv[k] = acc;
+      }
+    }
+    float zz = 0.f, rr = 0.f;
+    for (int k = 0; k < d; ++k) zz = fmaf(z[k], z[k], zz);
+    if (tc.obs) {
+      for (int a = 0; a < M.dy; ++a) {
+        float g = (float)tc.e[a];
+        for (int l = 0; l < d; ++l) g = fmaf(-(float)tc.G[a * d + l], z[l], g);
+        rr = fmaf(g, g, rr);
+      }
+    }
+    col = (float)kLog2E * ((float)tc.cconst + 0.5f * (zz - rr));
+  }
+  xs.x = xv[0];
+  xs.y = xv[1];
+  xs.z = xv[2];
+  xs.w = xv[3];
+  b.X32[off] = xs;
+  b.COL[off] = col;
+  if (n == 0 && t > 0) {  // q_t = nu_t: uniform leaf, lse = log N exactly
+    const size_t o = (size_t)ch * b.K + t;
+    b.LNC[o] = 0.0;
+    b.UNI[o] = 1;
+    b.LWMAX[o] = -log((double)b.N);
+  }
+  if (t == 0) {
+    // leaf-0 raw weight h0 + P0 - q0 in FP64
+    double x[4];
+    for (int k = 0; k < d; ++k) x[k] = is_star ? xstar[k] : (double)xv[k] + tc.pm[k];
+    double w;
+    if (M.kind == DSMC_MODEL_SV) {
+      const double v0 = M.sv_s2 / (1.0 - M.sv_phi * M.sv_phi);
+      const double dx = x[0] - M.sv_mu;
+      w = -0.5 * (kLog2Pi + log(v0)) - dx * dx / (2.0 * v0) - tc.logabsy;
+    } else {
+      double W0[16], L0[16];
+      dchol(M.P0, d, L0);
+      dtri_inv(L0, d, W0);
+      const double norm0 = dnorm_of(L0, d);
+      const double p0 = norm0 - 0.5 * dquad(W0, d, x, M.m0);
+      double zz = 0.0;
+      double e[4];
+      for (int k = 0; k < d; ++k) e[k] = x[k] - tc.pm[k];
+      for (int k = 0; k < d; ++k) {
+        double acc = 0.0;
+        for (int l = 0; l <= k; ++l) acc += tc.pW[k * d + l] * e[l];
+        zz += acc * acc;
+      }
+      const double q0 = tc.p_norm - 0.5 * zz;
+      double h0 = 0.0;
+      if (tc.obs) {
+        const double* H = at(M.H, M.H_s, 0);
+        double hx[4];
+        for (int a = 0; a < M.dy; ++a) {
+          double s = 0.0;
+          for (int l = 0; l < d; ++l) s += H[a * d + l] * x[l];
+          hx[a] = s;
+        }
+        h0 = tc.o_norm - 0.5 * dquad(tc.oW, M.dy, M.y, hx);
+      }
+      w = h0 + p0 - q0;
+    }
+    raw0[(size_t)ch * b.N + n] = w;
+  }
+}
+
+// Leaf-0 normalisation for the FP32 path (log2 units) + leaf meta for all t.
+__global__ void leafnorm32_kernel(Bufs b, const double* raw0) {
+  const int ch = blockIdx.x, lane = threadIdx.x;
+  const int N = b.N;
+  const double* lw = raw0 + (size_t)ch * N;
+  double mx = -CUDART_INF, lo = CUDART_INF, hi = -CUDART_INF;
+  int nan = 0;
+  for (int i = lane; i < N; i += 32) {
+    const double v = lw[i];
+    nan |= isnan(v);
+    mx = fmax(mx, v);
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+  for (int o = 16; o; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(~0u, mx, o));
+    lo = fmin(lo, __shfl_xor_sync(~0u, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(~0u, hi, o));
+    nan |= __shfl_xor_sync(~0u, nan, o);
+  }
+  if (nan || mx == -CUDART_INF) {
+    if (lane == 0) raise_err(b.err, nan ? DSMC_E_DOMAIN : DSMC_E_RUNTIME, 0, 0, nan ? kReasonNaN : kReasonLeafZero);
+    return;
+  }
+  double s = 0.0;
+  for (int i = lane; i < N; i += 32) s += exp(lw[i] - mx);
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(~0u, s, o);
+  const double lse = mx + log(s);
+  for (int i = lane; i < N; i += 32)
+    b.LW32[(size_t)ch * N + i] = (float)((lw[i] - lse) * kLog2E);
+  if (lane == 0) {
+    const size_t o = (size_t)ch * b.K;
+    b.LNC[o] = lse - log((double)N);
+    b.UNI[o] = lo == hi;
+    b.LWMAX[o] = mx - lse;
+  }
+}
+
+}  // namespace dsmc_dev

@@ -1,0 +1,109 @@
+"""Host-side model builders for the BASELINE configurations.
+
+These play the role of the reference harness's prepare() (experiment.cpp:
+436-468): simulate synthetic data, build the proposal marginals (exact RTS
+smoother, the reference's make_lgssm_fk recipe: q_t = nu_t = smoothing
+marginals), and hand a plain-data descriptor (abi.Model) to the engine.
+
+  lgssm_check  C1: d=1 LGSSM of experiment.hpp:20-27 (coef 0.9, Q 0.25,
+               x0 ~ N(0,1), R 0.25)
+  cv_tracking  C2/C5: d=4 2-D constant-velocity model
+  sv           C3/C4: stochastic volatility
+  ar1          the reference test fixture tests/support/ar1.hpp (stationary
+               proposals)
+"""
+import numpy as np
+from scipy.signal import lfilter
+
+from . import abi
+
+
+def _lgssm(T, d, dy, m0, P0, F, b, Q, H, R, y, prop_mean=None, prop_cov=None,
+           has_obs=None, inflation=1.0):
+    K = T + 1
+    if prop_mean is None:
+        prop_mean = np.zeros((K, d))
+        prop_cov = np.tile(np.eye(d), (K, 1, 1))
+    m = abi.Model(abi.MODEL_LGSSM, T, d, dy, m0=m0, P0=P0, F=F, b=b, Q=Q, H=H,
+                  R=R, y=y, has_obs=has_obs, prop_mean=prop_mean, prop_cov=prop_cov)
+    return m
+
+
+def with_rts_proposals(model, inflation=1.0):
+    """Replace the proposals by the exact smoothing marginals (x inflation)."""
+    from .dsmc import kalman_smooth
+    mean, cov, _ = kalman_smooth(model)
+    A = dict(model.arrays)
+    A["prop_mean"] = mean
+    A["prop_cov"] = cov * inflation
+    out = abi.Model(model.kind, model.horizon, model.d, model.dy, **A)
+    return out
+
+
+def lgssm_check(T, coef=0.9, shift=0.0, trans_var=0.25, init_mean=0.0,
+                init_var=1.0, obs_var=0.25, data_seed=90210, ys=None,
+                inflation=1.0):
+    """C1 (experiment.hpp:20-27, experiment.cpp:367-381)."""
+    K = T + 1
+    if ys is None:
+        rng = np.random.default_rng(data_seed)
+        x0 = init_mean + np.sqrt(init_var) * rng.standard_normal()
+        e = np.sqrt(trans_var) * rng.standard_normal(K)
+        e[0] = x0
+        x = lfilter([1.0], [1.0, -coef], e + np.r_[0.0, np.full(T, shift)])
+        ys = x + np.sqrt(obs_var) * rng.standard_normal(K)
+    m = _lgssm(T, 1, 1, [init_mean], [[init_var]], [coef], [shift], [trans_var],
+               [1.0], [obs_var], np.asarray(ys, float).reshape(K, 1))
+    return with_rts_proposals(m, inflation)
+
+
+def ar1(ys, rho=0.8, q=0.3, r=0.4):
+    """tests/support/ar1.hpp:23-126: stationary proposals N(0, q/(1-rho^2))."""
+    T = len(ys) - 1
+    K = T + 1
+    s2 = q / (1.0 - rho * rho)
+    return _lgssm(T, 1, 1, [0.0], [[s2]], [rho], [0.0], [q], [1.0], [r],
+                  np.asarray(ys, float).reshape(K, 1),
+                  prop_mean=np.zeros((K, 1)), prop_cov=np.full((K, 1, 1), s2))
+
+
+def cv_matrices(q=0.05, r=0.3, dt=1.0):
+    I2 = np.eye(2)
+    F = np.block([[I2, dt * I2], [np.zeros((2, 2)), I2]])
+    Q = q * np.block([[dt ** 3 / 3 * I2, dt ** 2 / 2 * I2], [dt ** 2 / 2 * I2, dt * I2]])
+    H = np.hstack([I2, np.zeros((2, 2))])
+    R = r * I2
+    return F, Q, H, R
+
+
+def cv_tracking(T, q=0.05, r=0.3, data_seed=90210, inflation=1.0):
+    """C2 / C5: x = (p_x, p_y, v_x, v_y), white-noise acceleration."""
+    K = T + 1
+    F, Q, H, R = cv_matrices(q, r)
+    rng = np.random.default_rng(data_seed)
+    Lq = np.linalg.cholesky(Q)
+    w = rng.standard_normal((K, 4)) @ Lq.T
+    w[0] = rng.standard_normal(4)  # x0 ~ N(0, I)
+    # x_t = F x_{t-1} + w_t with F = [[I, I], [0, I]]: v = cumsum(w_v),
+    # p_t = p_{t-1} + v_{t-1} + w_p,t
+    v = np.cumsum(w[:, 2:], axis=0)
+    vprev = np.vstack([np.zeros((1, 2)), v[:-1]])
+    p = np.cumsum(w[:, :2] + vprev, axis=0)
+    x = np.hstack([p, v])
+    y = x[:, :2] + np.sqrt(r) * rng.standard_normal((K, 2))
+    m = _lgssm(T, 4, 2, np.zeros(4), np.eye(4), F, np.zeros(4), Q, H, R, y)
+    return with_rts_proposals(m, inflation)
+
+
+def sv(T, mu=-1.0, phi=0.95, sigma=0.3, data_seed=90210, ys=None):
+    """C3 / C4: x_t = mu + phi (x_{t-1} - mu) + sigma e, y_t ~ N(0, e^{x_t})."""
+    K = T + 1
+    if ys is None:
+        rng = np.random.default_rng(data_seed)
+        s2 = sigma * sigma
+        e = sigma * rng.standard_normal(K)
+        e[0] = np.sqrt(s2 / (1 - phi * phi)) * rng.standard_normal()
+        x = mu + lfilter([1.0], [1.0, -phi], e)
+        ys = np.exp(x / 2) * rng.standard_normal(K)
+    return abi.Model(abi.MODEL_SV, T, 1, 1, y=np.asarray(ys, float),
+                     sv=(mu, phi, sigma * sigma))
