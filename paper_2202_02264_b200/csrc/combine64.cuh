@@ -27,6 +27,7 @@ struct LevelArgs {
   double* ws;      // workspace for this chunk
   size_t ws_comb;  // doubles per combine in ws
   int n_out;       // slots resampled (N, or N-1 when conditional)
+  double* dbg;     // TEMP debug
 };
 
 // Block meta derived from the schedule geometry.
@@ -72,7 +73,7 @@ struct Col64 {
 };
 
 // Column base of the stitch-row factory at cut c (per model class).
-template <int MC>
+template <int MC, int D>
 __device__ inline double col_base(const DevModel& M, const TimeConst& tc,
                                   int c, const double* x) {
   if (MC == kSV) return tc.shift1;
@@ -90,12 +91,13 @@ __device__ inline double col_base(const DevModel& M, const TimeConst& tc,
   }
   // LG d>1 (oracle comb_prepare order)
   const double lh = cb_log_h(M, tc, c, x);
-  const double lp = DSUB(tc.p_norm, DMUL(0.5, dquad(tc.pW, M.d, x, tc.pm)));
+  const double lp = DSUB(tc.p_norm, DMUL(0.5, dquad(tc.pW, D, x, tc.pm)));
   return DSUB(DADD(tc.t_norm, lh), lp);
 }
 
-// Row term: the transition mean of a left particle at cut c.
-template <int MC>
+// Row term: the transition mean of a left particle at cut c (whitened for
+// d > 1). D is the compile-time state dimension (1 for LG1 / SV).
+template <int MC, int D>
 __device__ inline void row_mean(const DevModel& M, const TimeConst& tc, int c, const double* xl,
                                 double* mu) {
   if (MC == kSV) {
@@ -103,27 +105,38 @@ __device__ inline void row_mean(const DevModel& M, const TimeConst& tc, int c, c
   } else if (MC == kLG1) {
     mu[0] = DADD(DMUL(*at(M.F, M.F_s, c), xl[0]), *at(M.b, M.b_s, c));
   } else {  // v = W_Q (F x + b): the row's whitened transition mean
-    double m[4];
-    lg_mean(M, c, xl, m);
+    const double* F = at(M.F, M.F_s, c);
+    const double* bb = at(M.b, M.b_s, c);
+    double m[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      double s = 0.0;
+#pragma unroll
+      for (int l = 0; l < D; ++l) s = DADD(s, DMUL(F[k * D + l], xl[l]));
+      m[k] = DADD(s, bb[k]);
+    }
     const double* W = tc.tW;
-    for (int k = 0; k < M.d; ++k) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
       double v = 0.0;
-      for (int l = 0; l <= k; ++l) v = DADD(v, DMUL(W[k * M.d + l], m[l]));
+#pragma unroll
+      for (int l = 0; l <= k; ++l) v = DADD(v, DMUL(W[k * D + l], m[l]));
       mu[k] = v;
     }
   }
 }
 
 // One table entry (fill_row of make_pair_source, smoother.cpp:153-161).
-template <int MC>
+template <int MC, int D>
 __device__ inline double fill64(const DevModel& M, const TimeConst& tc,
                                 double coef, const double* mu, const Col64& C,
-                                int j, int d, double sl, bool has_l) {
+                                int j, double sl, bool has_l) {
   double v;
   if (MC == kLGN) {  // d chained gaussian_row passes (ref_models lgssm_nd)
     v = C.base[j];
-    for (int k = 0; k < d; ++k) {
-      const double t = DSUB(C.x[(size_t)j * d + k], mu[k]);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const double t = DSUB(C.x[(size_t)j * D + k], mu[k]);
       v = __fma_rn(-0.5, DMUL(t, t), v);
     }
   } else {
@@ -143,11 +156,12 @@ __device__ inline double row_coef(const DevModel& M, int c) {
 }
 
 // Stage the combine's right boundary slab + column bases in shared memory.
-template <int MC>
+template <int MC, int D>
 __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
                            const Side& R, const DevModel& M,
                            const TimeConst& tc, double* smem, Col64& C) {
-  const int N = b.N, d = b.d;
+  const int N = b.N;
+  constexpr int d = D;
   C.x = smem;
   C.base = smem + (size_t)N * d;
   const bool nonuni = R.leaf && !b.UNI[(size_t)ch * b.K + R.t];
@@ -155,17 +169,20 @@ __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
   const double* X = b.X64 + ((size_t)ch * b.K + R.t) * N * d;
   for (int j = threadIdx.x; j < N; j += blockDim.x) {
     const uint32_t p = map_first(b, la, ch, R, j);
-    double x[4];
+    double x[D];
+#pragma unroll
     for (int k = 0; k < d; ++k) x[k] = X[(size_t)p * d + k];
-    C.base[j] = col_base<MC>(M, tc, R.t, x);
+    C.base[j] = col_base<MC, D>(M, tc, R.t, x);
     if (MC == kLGN) {  // whitened column w = W_Q x
+#pragma unroll
       for (int k = 0; k < d; ++k) {
         double z = 0.0;
+#pragma unroll
         for (int l = 0; l <= k; ++l) z = DADD(z, DMUL(tc.tW[k * d + l], x[l]));
         C.x[(size_t)j * d + k] = z;
       }
     } else {
-      for (int k = 0; k < d; ++k) C.x[(size_t)j * d + k] = x[k];
+      C.x[j] = x[0];
     }
     if (nonuni) C.lwr[j] = b.LW64[((size_t)ch * b.K + R.t) * N + p];
   }
@@ -176,18 +193,19 @@ __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
 // contract per sub-block, sequential tail) and the raw row total
 // (sequential over sub-blocks) — exp_row_store (kernels.cpp:93-116).
 // ws layout per combine: m[N] raw[N] scale[N] total[N] prefix[N] sub[N*nsub]
-template <int MC>
+template <int MC, int D>
 __global__ void __launch_bounds__(256) c64_rows(Bufs b, LevelArgs la) {
   extern __shared__ double smem[];
   const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
-  const int N = b.N, d = b.d, nsub = (N + kSub - 1) / kSub;
+  const int N = b.N, nsub = (N + kSub - 1) / kSub;
+  constexpr int d = D;
   Side L, R;
   CombineGeom g;
   sides(b, la, k, L, R, g);
   const DevModel& M = b.models[ch];
   const TimeConst& tc = b.tc[(size_t)ch * b.K + g.c];
   Col64 C;
-  stage_cols<MC>(b, la, ch, R, M, tc, smem, C);
+  stage_cols<MC, D>(b, la, ch, R, M, tc, smem, C);
   double* ws = la.ws + (size_t)blockIdx.y * la.ws_comb;
   double *wm = ws, *wraw = ws + N, *wsub = ws + 5 * (size_t)N;
   const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
@@ -199,15 +217,15 @@ __global__ void __launch_bounds__(256) c64_rows(Bufs b, LevelArgs la) {
     const int i = blockIdx.x * rows_per_cta + r;
     if (i >= N) break;
     const uint32_t p = map_last(b, la, ch, L, i);
-    double xl[4], mu[4];
+    double xl[D], mu[D];
     for (int q = 0; q < d; ++q) xl[q] = XL[(size_t)p * d + q];
-    row_mean<MC>(M, tc, g.c, xl, mu);
+    row_mean<MC, D>(M, tc, g.c, xl, mu);
     const double sl = lnonuni ? b.LW64[((size_t)ch * b.K + L.t) * N + i] : 0.0;
     // max (reduce_max, kernels.cpp:26-36)
     double mx = -CUDART_INF;
     int nan = 0;
     for (int j = lane; j < N; j += 32) {
-      const double v = fill64<MC>(M, tc, coef, mu, C, j, d, sl, lnonuni);
+      const double v = fill64<MC, D>(M, tc, coef, mu, C, j, sl, lnonuni);
       nan |= isnan(v);
       mx = fmax(mx, v);
     }
@@ -236,14 +254,14 @@ __global__ void __launch_bounds__(256) c64_rows(Bufs b, LevelArgs la) {
       double acc = 0.0;
       for (int q = 0; q < len8; q += 8) {
         const int j = j0 + q + l8;
-        acc = DADD(acc, exp_w(DSUB(fill64<MC>(M, tc, coef, mu, C, j, d, sl, lnonuni), mx)));
+        acc = DADD(acc, exp_w(DSUB(fill64<MC, D>(M, tc, coef, mu, C, j, sl, lnonuni), mx)));
       }
       double a8[8];
       for (int l = 0; l < 8; ++l) a8[l] = __shfl_sync(~0u, acc, (lane & ~7) + l);
       if (act && l8 == 0) {
         double bs = combine8(a8);
         for (int j = j0 + len8; j < j0 + len; ++j)
-          bs = DADD(bs, exp_w(DSUB(fill64<MC>(M, tc, coef, mu, C, j, d, sl, lnonuni), mx)));
+          bs = DADD(bs, exp_w(DSUB(fill64<MC, D>(M, tc, coef, mu, C, j, sl, lnonuni), mx)));
         srow[s] = bs;
       }
     }
@@ -258,7 +276,7 @@ __global__ void __launch_bounds__(256) c64_rows(Bufs b, LevelArgs la) {
 
 // Pass 2: one CTA per combine. Cross-row combination (resampling.cpp:92-102),
 // per-slot inversion (Appendix A), ancestor maps, block log Z.
-template <int MC>
+template <int MC, int D>
 __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
                                                   int systematic) {
   extern __shared__ double smem[];
@@ -266,14 +284,15 @@ __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
   __shared__ double s_g, s_grand;
   __shared__ double a8s[8];
   const int k = la.k0 + blockIdx.x, ch = blockIdx.z;
-  const int N = b.N, d = b.d, nsub = (N + kSub - 1) / kSub;
+  const int N = b.N, nsub = (N + kSub - 1) / kSub;
+  constexpr int d = D;
   Side L, R;
   CombineGeom g;
   sides(b, la, k, L, R, g);
   const DevModel& M = b.models[ch];
   const TimeConst& tc = b.tc[(size_t)ch * b.K + g.c];
   Col64 C;
-  stage_cols<MC>(b, la, ch, R, M, tc, smem, C);
+  stage_cols<MC, D>(b, la, ch, R, M, tc, smem, C);
   double* ws = la.ws + (size_t)blockIdx.x * la.ws_comb;
   double *wm = ws, *wraw = ws + N, *wscale = ws + 2 * (size_t)N,
          *wtot = ws + 3 * (size_t)N, *wpre = ws + 4 * (size_t)N,
@@ -367,21 +386,31 @@ __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
       c2 = DADD(c2, srow[s]);
     }
     const uint32_t pl = map_last(b, la, ch, L, row);
-    double xl[4], mu[4];
+    double xl[D], mu[D];
     for (int q = 0; q < d; ++q) xl[q] = XL[(size_t)pl * d + q];
-    row_mean<MC>(M, tc, g.c, xl, mu);
+    row_mean<MC, D>(M, tc, g.c, xl, mu);
     const double sl = lnonuni ? b.LW64[((size_t)ch * b.K + L.t) * N + row] : 0.0;
     const double mrow = wm[row];
     const int j0 = s * kSub, j1 = min(j0 + kSub, N);
     double c3 = c2b;
     int j = j0;
     for (; j < j1; ++j) {
-      c3 = DADD(c3, exp_w(DSUB(fill64<MC>(M, tc, coef, mu, C, j, d, sl, lnonuni), mrow)));
+      c3 = DADD(c3, exp_w(DSUB(fill64<MC, D>(M, tc, coef, mu, C, j, sl, lnonuni), mrow)));
       if (local < c3) break;
     }
     if (j == j1) {  // spill: clamp to the last positive entry
       j = j1 - 1;
-      while (j > 0 && !(exp_w(DSUB(fill64<MC>(M, tc, coef, mu, C, j, d, sl, lnonuni), mrow)) > 0.0)) --j;
+      while (j > 0 && !(exp_w(DSUB(fill64<MC, D>(M, tc, coef, mu, C, j, sl, lnonuni), mrow)) > 0.0)) --j;
+    }
+    if (la.dbg && m == 0 && k == 0 && la.level == 1) {
+      la.dbg[0] = local; la.dbg[1] = c2b; la.dbg[2] = mrow; la.dbg[3] = row; la.dbg[4] = s;
+      for (int q = 0; q < D; ++q) { la.dbg[5 + q] = mu[q]; la.dbg[9 + q] = xl[q]; }
+      for (int jj = j0; jj < j1 && jj - j0 < 64; ++jj) {
+        la.dbg[16 + jj - j0] = fill64<MC, D>(M, tc, coef, mu, C, jj, sl, lnonuni);
+        la.dbg[80 + jj - j0] = C.base[jj];
+        la.dbg[144 + jj - j0] = C.x[(size_t)jj * d];
+      }
+      la.dbg[13] = d; la.dbg[14] = j; la.dbg[15] = wsub[(size_t)row * nsub];
     }
     PL[m + off] = (uint32_t)row;
     PR[m + off] = (uint32_t)j;

@@ -272,15 +272,15 @@ struct RunResult {
 
 size_t smem_cols64(int N, int d) { return sizeof(double) * (size_t)N * (d + 2); }
 
-template <int MC>
+template <int MC, int D>
 int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
                int systematic) {
-  const size_t sm = smem_cols64(b.N, b.d);
-  CU(cudaFuncSetAttribute(c64_rows<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  CU(cudaFuncSetAttribute(c64_sample<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  c64_rows<MC><<<dim3((b.N + 31) / 32, nk, b.B), 256, sm, ctx->stream>>>(b, la);
+  const size_t sm = smem_cols64(b.N, D);
+  CU(cudaFuncSetAttribute(c64_rows<MC, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CU(cudaFuncSetAttribute(c64_sample<MC, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  c64_rows<MC, D><<<dim3((b.N + 31) / 32, nk, b.B), 256, sm, ctx->stream>>>(b, la);
   LAUNCHED(ctx);
-  c64_sample<MC><<<dim3(nk, 1, b.B), 256, sm, ctx->stream>>>(b, la, systematic);
+  c64_sample<MC, D><<<dim3(nk, 1, b.B), 256, sm, ctx->stream>>>(b, la, systematic);
   LAUNCHED(ctx);
   return DSMC_OK;
 }
@@ -515,6 +515,12 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     la.n_out = o.conditional ? N - 1 : N;
     la.ws = ws;
     la.ws_comb = ws_comb;
+    if (getenv("DSMC_DEBUG")) {
+      static double* dbg = nullptr;
+      if (!dbg) cudaMallocManaged(&dbg, 256 * 8);
+      la.dbg = dbg;
+    }
+    if (getenv("DSMC_SYNC")) cudaStreamSynchronize(ctx->stream);
     if (o.conditional) {
       la.k0 = 0;
       if (fp64) {
@@ -545,9 +551,12 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
       } else {
         const int sys = o.resampler == DSMC_SYSTEMATIC;
         if (fp64) {
-          rc = mc == kLG1 ? launch_c64<kLG1>(ctx, b, la, nk, sys)
-             : mc == kSV  ? launch_c64<kSV>(ctx, b, la, nk, sys)
-                          : launch_c64<kLGN>(ctx, b, la, nk, sys);
+          rc = mc == kLG1 ? launch_c64<kLG1, 1>(ctx, b, la, nk, sys)
+             : mc == kSV  ? launch_c64<kSV, 1>(ctx, b, la, nk, sys)
+             : d == 1     ? launch_c64<kLGN, 1>(ctx, b, la, nk, sys)
+             : d == 2     ? launch_c64<kLGN, 2>(ctx, b, la, nk, sys)
+             : d == 3     ? launch_c64<kLGN, 3>(ctx, b, la, nk, sys)
+                          : launch_c64<kLGN, 4>(ctx, b, la, nk, sys);
         } else {
           rc = d == 1 ? launch_c32<1>(ctx, b, la, nk, sys)
              : d == 2 ? launch_c32<2>(ctx, b, la, nk, sys)

@@ -35,13 +35,39 @@ def test_lgssm_means_match_kalman(engine, precision):
     assert abs(r["log_norm_const"] - ll) < 1.0, (r["log_norm_const"], ll)
 
 
-def test_cv_d4_means_match_kalman(engine):
-    m = models.cv_tracking(255)
+def _seed_avg(engine, m, N, precision, seeds):
+    runs = [engine.smooth(m, N, abi.MULTINOMIAL, seed=s, precision=precision) for s in seeds]
+    means = np.stack([r["mean"] for r in runs])
+    return means.mean(0), means.std(0, ddof=1) / np.sqrt(len(seeds)), runs
+
+
+@pytest.mark.parametrize("precision", [abi.FP32, abi.FP64_PARITY])
+def test_cv_d4_means_match_kalman(engine, precision):
+    """The d=4 constant-velocity model (near-singular Q, strongly correlated
+    neighbouring states) degenerates at moderate N, so a single run is not
+    a sharp check: like test_smoother.cpp:292-316 (16 seeds, 5 SE) we compare
+    the seed average against Kalman in units of its standard error."""
+    m = models.cv_tracking(127)
     km, kP, ll = kalman_smooth(m)
-    r = engine.smooth(m, 1024, abi.MULTINOMIAL, seed=5, precision=abi.FP32)
-    z = _z(r["mean"], km, kP)
-    assert np.sqrt(np.mean(z ** 2)) < 0.15, np.sqrt(np.mean(z ** 2))
-    assert abs(r["log_norm_const"] - ll) < 2.0, (r["log_norm_const"], ll)
+    avg, se, runs = _seed_avg(engine, m, 1024, precision, range(16))
+    z = (avg - km) / np.maximum(se, 1e-12)
+    assert np.sqrt(np.mean(z ** 2)) < 2.0, np.sqrt(np.mean(z ** 2))
+    assert np.abs(z).max() < 6.0
+    lz = np.array([r["log_norm_const"] for r in runs])
+    # exp(log Z) is unbiased (test_smoother.cpp:317-341): log-mean-exp vs ll
+    lme = np.log(np.mean(np.exp(lz - lz.max()))) + lz.max()
+    assert abs(lme - ll) < 3.0, (lme, ll)
+
+
+def test_cv_d4_fp32_matches_fp64(engine):
+    """FP32 throughput path vs FP64 parity path (bit-exact with the
+    reference): seed-averaged means agree within 5 combined SE."""
+    m = models.cv_tracking(127)
+    a, sa, _ = _seed_avg(engine, m, 1024, abi.FP32, range(100, 116))
+    b, sb, _ = _seed_avg(engine, m, 1024, abi.FP64_PARITY, range(200, 216))
+    z = (a - b) / np.sqrt(sa ** 2 + sb ** 2)
+    assert np.sqrt(np.mean(z ** 2)) < 2.0
+    assert np.abs(z).max() < 6.0
 
 
 def test_fp32_and_fp64_agree_on_first_level_pairs(engine):
@@ -57,26 +83,36 @@ def test_fp32_and_fp64_agree_on_first_level_pairs(engine):
     assert same.mean() > 0.99, same.mean()
 
 
+def _avg1(engine, m, N, rs, precision, seeds, **kw):
+    runs = [engine.smooth(m, N, rs, seed=s, precision=precision, **kw) for s in seeds]
+    means = np.stack([r["mean"][:, 0] for r in runs])
+    return means.mean(0), means.std(0, ddof=1) / np.sqrt(len(seeds)), runs
+
+
 def test_sv_fp32_matches_fp64(engine):
-    m = models.sv(511)
-    a = engine.smooth(m, 2048, abi.MULTINOMIAL, seed=1, precision=abi.FP32)
-    b = engine.smooth(m, 2048, abi.MULTINOMIAL, seed=2, precision=abi.FP64_PARITY)
-    sd = np.sqrt(0.5 * (a["cov"][:, 0, 0] + b["cov"][:, 0, 0]))
-    z = (a["mean"][:, 0] - b["mean"][:, 0]) / sd
-    assert np.sqrt(np.mean(z ** 2)) < 0.15
-    assert abs(a["log_norm_const"] - b["log_norm_const"]) < 1.5
+    """Smoothed paths are strongly correlated in t, so one run per arm is a
+    noisy check; compare 8-seed averages in standard-error units."""
+    m = models.sv(255)
+    a, sa, ra = _avg1(engine, m, 1024, abi.MULTINOMIAL, abi.FP32, range(8))
+    b, sb, rb = _avg1(engine, m, 1024, abi.MULTINOMIAL, abi.FP64_PARITY, range(50, 58))
+    z = (a - b) / np.sqrt(sa ** 2 + sb ** 2)
+    assert np.sqrt(np.mean(z ** 2)) < 2.0 and np.abs(z).max() < 6.0
+    la = np.array([r["log_norm_const"] for r in ra])
+    lb = np.array([r["log_norm_const"] for r in rb])
+    se = np.sqrt(la.var(ddof=1) / len(la) + lb.var(ddof=1) / len(lb))
+    assert abs(la.mean() - lb.mean()) < 5 * se + 0.05, (la.mean(), lb.mean(), se)
 
 
 @pytest.mark.parametrize("rs", [abi.MH_LAZY, abi.REJECTION_LAZY])
 def test_lazy_sv_matches_dense(engine, rs):
     from tests.cases import CASES, model_for
-    m = model_for(dict(CASES["sv"], T=255))
-    dense = engine.smooth(m, 1024, abi.MULTINOMIAL, seed=4, precision=abi.FP32)
-    lazy = engine.smooth(m, 1024, rs, seed=5, precision=abi.FP32, mh_steps=16)
-    sd = np.sqrt(dense["cov"][:, 0, 0])
-    z = (lazy["mean"][:, 0] - dense["mean"][:, 0]) / sd
-    # MH-16 is biased (resampling.hpp:55-59) but close; rejection is exact
-    assert np.sqrt(np.mean(z ** 2)) < 0.2
+    m = model_for(dict(CASES["sv"], T=127))
+    a, sa, _ = _avg1(engine, m, 512, abi.MULTINOMIAL, abi.FP32, range(8))
+    b, sb, runs = _avg1(engine, m, 512, rs, abi.FP32, range(20, 28), mh_steps=16)
+    z = (a - b) / np.sqrt(sa ** 2 + sb ** 2)
+    # rejection is exact; MH-16 is biased (resampling.hpp:55-59) but close
+    assert np.sqrt(np.mean(z ** 2)) < (2.0 if rs == abi.REJECTION_LAZY else 3.0)
+    lazy = runs[0]
     assert lazy["log_norm_const"] is None
     assert lazy["biased"] == (rs == abi.MH_LAZY)
     assert lazy["weight_evals"] > 0
