@@ -115,10 +115,68 @@ struct Side32 {
   const float* COL;
 };
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// One row against this lane's 16 columns: the 64-column sub-block's max and
+// sum of exp2(t - max) (identical in the 4 lanes of the sub-block).
+template <int D>
+__device__ __forceinline__ void row_sub(const float2 (&y2)[D][kCPL / 2],
+                                        const float2 (&A2)[kCPL / 2],
+                                        const float* u, float& m_out,
+                                        float& s_out) {
+  float2 t[kCPL / 2];
+  float2 uu[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) uu[q] = make_float2(u[q], u[q]);
+#pragma unroll
+  for (int c2 = 0; c2 < kCPL / 2; ++c2) {
+    float2 acc = A2[c2];
+#pragma unroll
+    for (int q = 0; q < D; ++q) acc = __ffma2_rn(uu[q], y2[q][c2], acc);
+    t[c2] = acc;
+  }
+  // max tree with 3-input FMNMX
+  const float a0 = fmax3(t[0].x, t[0].y, t[1].x);
+  const float a1 = fmax3(t[1].y, t[2].x, t[2].y);
+  const float a2 = fmax3(t[3].x, t[3].y, t[4].x);
+  const float a3 = fmax3(t[4].y, t[5].x, t[5].y);
+  const float a4 = fmax3(t[6].x, t[6].y, t[7].x);
+  float m = fmax3(fmax3(a0, a1, a2), fmax3(a3, a4, t[7].y), a0);
+  m = fmaxf(m, __shfl_xor_sync(~0u, m, 1));
+  m = fmaxf(m, __shfl_xor_sync(~0u, m, 2));
+  const float mm = (m == -CUDART_INF_F) ? 0.f : m;
+  const float2 nm = make_float2(-mm, -mm);
+  float2 e[kCPL / 2];
+#pragma unroll
+  for (int c2 = 0; c2 < kCPL / 2; ++c2) {
+    const float2 dd = __fadd2_rn(t[c2], nm);
+    e[c2] = make_float2(ex2(dd.x), ex2(dd.y));
+  }
+  const float2 s01 = __fadd2_rn(__fadd2_rn(e[0], e[1]), __fadd2_rn(e[2], e[3]));
+  const float2 s23 = __fadd2_rn(__fadd2_rn(e[4], e[5]), __fadd2_rn(e[6], e[7]));
+  const float2 s2 = __fadd2_rn(s01, s23);
+  float sm = s2.x + s2.y;
+  sm += __shfl_xor_sync(~0u, sm, 1);
+  sm += __shfl_xor_sync(~0u, sm, 2);
+  m_out = m;
+  s_out = sm;
+}
+
+// Pass 1. Grid (row tiles, combines, chains); la.rows_per_cta rows per CTA
+// (a multiple of 32, chosen per level so the grid fills the GPU). Warps take
+// (512-column chunk, row slice) items; rows go 4 at a time so that each lane
+// finishes exactly one (row, sub-block) log-sum: one LG2 and one store per
+// 64 pair evaluations, no divergent tail.
 template <int D>
 __global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
-  __shared__ float s_u[kRT][4];
-  __shared__ float s_B[kRT];
+  extern __shared__ float sm32[];
+  const int RT = la.rows_per_cta;
+  float* s_u = sm32;            // [RT][D]
+  float* s_B = sm32 + RT * D;   // [RT]
   const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
   const int N = b.N;
   Side L, R;
@@ -130,29 +188,31 @@ __global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
   const int nch = (N + kChunk - 1) / kChunk;
   const int nsubp = nch * (kChunk / kSub);
   float* ws = reinterpret_cast<float*>(la.ws) + (size_t)blockIdx.y * la.ws_comb * 2;
-  const int row0 = blockIdx.x * kRT;
-  const int nrows = min(kRT, N - row0);
-  // rows of this tile -> shared memory
+  const int row0 = blockIdx.x * RT;
+  const int nrows = min(RT, N - row0);
   const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
   const float4* XL = b.X32 + ((size_t)ch * b.K + L.t) * N;
-  for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
-    const int i = row0 + r;
-    const uint32_t p = map_last(b, la, ch, L, i);
-    const float lw2 = lnonuni ? b.LW32[(size_t)ch * N + i] : 0.f;
-    float u[4] = {0, 0, 0, 0}, Bv;
-    row32<D>(cc, XL[p], lw2, u, Bv);
-    for (int q = 0; q < 4; ++q) s_u[r][q] = u[q];
+  for (int r = threadIdx.x; r < RT; r += blockDim.x) {
+    float u[4] = {0, 0, 0, 0}, Bv = -CUDART_INF_F;
+    if (r < nrows) {
+      const int i = row0 + r;
+      const uint32_t p = map_last(b, la, ch, L, i);
+      const float lw2 = lnonuni ? b.LW32[(size_t)ch * N + i] : 0.f;
+      row32<D>(cc, XL[p], lw2, u, Bv);
+    }
+#pragma unroll
+    for (int q = 0; q < D; ++q) s_u[r * D + q] = u[q];
     s_B[r] = Bv;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = max(1, 8 / nch);          // row slices per chunk
+  const int S = max(1, 8 / nch);
   const int items = nch * S;
   const float4* XR = b.X32 + ((size_t)ch * b.K + R.t) * N;
   const float* CR = b.COL + ((size_t)ch * b.K + R.t) * N;
+  const int q4 = lane & 3;
   for (int it = warp; it < items; it += 8) {
     const int chunk = it % nch, slice = it / nch;
-    // this lane's 16 columns -> registers (packed pairs)
     float2 y2[D][kCPL / 2];
     float2 A2[kCPL / 2];
 #pragma unroll
@@ -174,38 +234,25 @@ __global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
       for (int q = 0; q < D; ++q) y2[q][c2] = make_float2(yv[0][q], yv[1][q]);
       A2[c2] = make_float2(Av[0], Av[1]);
     }
-    float* wrow_base = ws + (size_t)row0 * nsubp + chunk * (kChunk / kSub) + (lane >> 2);
-    for (int r = slice; r < nrows; r += S) {
-      float2 t[kCPL / 2];
-      float2 uu[D];
+    const int sub = chunk * (kChunk / kSub) + (lane >> 2);
+    // rows slice, slice+S, ... taken 4 at a time (RT is a multiple of 4*S;
+    // padded rows have B = -inf and are never stored)
+    for (int base = slice; base < nrows; base += 4 * S) {
+      float m4[4], s4[4];
 #pragma unroll
-      for (int q = 0; q < D; ++q) uu[q] = make_float2(s_u[r][q], s_u[r][q]);
+      for (int j = 0; j < 4; ++j) {
+        const int r = base + j * S;
+        float u[D];
 #pragma unroll
-      for (int c2 = 0; c2 < kCPL / 2; ++c2) {
-        float2 acc = A2[c2];
-#pragma unroll
-        for (int q = 0; q < D; ++q) acc = __ffma2_rn(uu[q], y2[q][c2], acc);
-        t[c2] = acc;
+        for (int q = 0; q < D; ++q) u[q] = s_u[r * D + q];
+        row_sub<D>(y2, A2, u, m4[j], s4[j]);
       }
-      float m = fmaxf(t[0].x, t[0].y);
-#pragma unroll
-      for (int c2 = 1; c2 < kCPL / 2; ++c2) m = fmaxf(m, fmaxf(t[c2].x, t[c2].y));
-      m = fmaxf(m, __shfl_xor_sync(~0u, m, 1));
-      m = fmaxf(m, __shfl_xor_sync(~0u, m, 2));
-      const float mm = (m == -CUDART_INF_F) ? 0.f : m;
-      const float2 nm = make_float2(-mm, -mm);
-      float2 s2 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int c2 = 0; c2 < kCPL / 2; ++c2) {
-        const float2 dd = __fadd2_rn(t[c2], nm);
-        s2 = __fadd2_rn(s2, make_float2(ex2(dd.x), ex2(dd.y)));
-      }
-      float s = s2.x + s2.y;
-      s += __shfl_xor_sync(~0u, s, 1);
-      s += __shfl_xor_sync(~0u, s, 2);
-      if ((lane & 3) == 0) {
-        const float Ls = s > 0.f ? m + lg2(s) + s_B[r] : -CUDART_INF_F;
-        wrow_base[(size_t)r * nsubp] = Ls;
+      const int rq = base + q4 * S;
+      const float mq = q4 == 0 ? m4[0] : q4 == 1 ? m4[1] : q4 == 2 ? m4[2] : m4[3];
+      const float sq = q4 == 0 ? s4[0] : q4 == 1 ? s4[1] : q4 == 2 ? s4[2] : s4[3];
+      if (rq < nrows) {
+        const float Ls = sq > 0.f ? mq + lg2(sq) + s_B[rq] : -CUDART_INF_F;
+        ws[(size_t)(row0 + rq) * nsubp + sub] = Ls;
       }
     }
   }
@@ -234,13 +281,20 @@ __device__ inline double block_scan_incl(double v, double* sh) {
   return v + add;
 }
 
+// Pass 2. Grid (slot blocks, combines, chains), 256 threads. Every slot block
+// rebuilds the combine's row CDF (N row totals from the sub-block sums, read
+// with independent vector loads) and samples its slice of the n_out slots:
+// binary search over the row CDF in shared memory, a walk over the row's
+// sub-block sums held in registers, and a recomputation of <= 64 weights of
+// the chosen sub-block with pass 1's FP32 operations.
 template <int D>
-__global__ void __launch_bounds__(512) c32_sample(Bufs b, LevelArgs la,
-                                                  int systematic) {
+__global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
+                                                     int systematic) {
   extern __shared__ double smem[];
   __shared__ double sh[32];
   __shared__ float s_g;
-  const int k = la.k0 + blockIdx.x, ch = blockIdx.z;
+  const int sb = blockIdx.x;
+  const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
   const int N = b.N;
   Side L, R;
   CombineGeom g;
@@ -251,27 +305,38 @@ __global__ void __launch_bounds__(512) c32_sample(Bufs b, LevelArgs la,
   const int nch = (N + kChunk - 1) / kChunk;
   const int nsubp = nch * (kChunk / kSub);
   const int nsub = (N + kSub - 1) / kSub;
-  const float* ws = reinterpret_cast<const float*>(la.ws) + (size_t)blockIdx.x * la.ws_comb * 2;
-  double* S = smem;                                   // N
-  float* Lrow = reinterpret_cast<float*>(S + N);      // N
-  float* ycol = Lrow + N;                             // N*D
-  float* Acol = ycol + (size_t)N * D;                 // N
+  const float* ws = reinterpret_cast<const float*>(la.ws) + (size_t)blockIdx.y * la.ws_comb * 2;
+  // columns padded to a multiple of 64 (y = 0, A = -inf -> weight 0) so the
+  // per-slot recomputation is branch-free
+  const int NP = (N + kSub - 1) / kSub * kSub;
+  double* S = smem;                                            // N
+  float4* ycol = reinterpret_cast<float4*>(S + ((N + 1) & ~1));  // NP, 16B aligned
+  float* Acol = reinterpret_cast<float*>(ycol + NP);            // NP
+  float* Lrow = Acol + NP;                                     // N
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float4* XR = b.X32 + ((size_t)ch * b.K + R.t) * N;
   const float* CR = b.COL + ((size_t)ch * b.K + R.t) * N;
-  for (int j = tid; j < N; j += blockDim.x) {
-    const uint32_t p = map_first(b, la, ch, R, j);
-    float y[4], A;
-    col32<D>(cc, XR[p], CR[p], y, A);
-    for (int q = 0; q < D; ++q) ycol[(size_t)j * D + q] = y[q];
+  for (int j = tid; j < NP; j += blockDim.x) {
+    float y[4] = {0, 0, 0, 0}, A = -CUDART_INF_F;
+    if (j < N) {
+      const uint32_t p = map_first(b, la, ch, R, j);
+      col32<D>(cc, XR[p], CR[p], y, A);
+    }
+    ycol[j] = make_float4(y[0], y[1], y[2], y[3]);
     Acol[j] = A;
   }
-  // row totals (log2) from the sub-block sums
+  // row totals (log2): nsub independent loads per row, then LSE
   float gm = -CUDART_INF_F;
   for (int i = tid; i < N; i += blockDim.x) {
     const float* w = ws + (size_t)i * nsubp;
     float m = -CUDART_INF_F;
-    for (int s = 0; s < nsub; ++s) m = fmaxf(m, w[s]);
+    for (int s0 = 0; s0 < nsub; s0 += 16) {
+      float v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = (s0 + q < nsub) ? w[s0 + q] : -CUDART_INF_F;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) m = fmaxf(m, v[q]);
+    }
     float L2 = -CUDART_INF_F;
     if (m != -CUDART_INF_F) {
       float acc = 0.f;
@@ -292,10 +357,9 @@ __global__ void __launch_bounds__(512) c32_sample(Bufs b, LevelArgs la,
   __syncthreads();
   const float G = s_g;
   if (G == -CUDART_INF_F) {
-    if (tid == 0) raise_err(b.err, DSMC_E_RUNTIME, g.c, la.level, kReasonZeroTable);
+    if (tid == 0 && sb == 0) raise_err(b.err, DSMC_E_RUNTIME, g.c, la.level, kReasonZeroTable);
     return;
   }
-  // row CDF: each thread scans a contiguous segment, then a block scan
   const int per = (N + blockDim.x - 1) / blockDim.x;
   const int i0 = tid * per, i1 = min(N, i0 + per);
   double seg = 0.0;
@@ -309,7 +373,7 @@ __global__ void __launch_bounds__(512) c32_sample(Bufs b, LevelArgs la,
   __syncthreads();
   const double total = S[N - 1];
   const size_t gidx = (size_t)ch * b.T + la.cursor + k;
-  if (tid == 0) b.LMW[gidx] = ((double)G + log2(total)) * kLn2;
+  if (tid == 0 && sb == 0) b.LMW[gidx] = ((double)G + log2(total)) * kLn2;
   const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
   const float4* XL = b.X32 + ((size_t)ch * b.K + L.t) * N;
   const int off = b.conditional ? 1 : 0;
@@ -325,78 +389,114 @@ __global__ void __launch_bounds__(512) c32_sample(Bufs b, LevelArgs la,
   }
   uint32_t* PL = b.PL + gidx * N;
   uint32_t* PR = b.PR + gidx * N;
-  for (int m = tid; m < la.n_out; m += blockDim.x) {
-    const double pt = systematic ? (u0 + (double)m) * step
-                                 : u64_uniform(stream_u64(id, m)) * total;
-    int lo = 0, hi = N;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (pt < S[mid]) hi = mid;
-      else lo = mid + 1;
+  const size_t nbase = ((size_t)ch * b.cap + k) * N;
+  const int m0 = sb * la.slots_per_cta, m1 = min(la.n_out, m0 + la.slots_per_cta);
+  // each thread takes 4 consecutive slots = one Philox block of uniforms
+  // (slot m uses u64 number m of the stream, rng.cpp:45-68)
+  for (int q0 = (m0 & ~3) + 4 * tid; q0 < m1; q0 += 4 * blockDim.x) {
+    U64x4 blk;
+    if (!systematic) blk = stream_block(id, (uint64_t)q0 >> 2);
+#pragma unroll 1
+    for (int qq = 0; qq < 4; ++qq) {
+      const int m = q0 + qq;
+      if (m < m0 || m >= m1) continue;
+      const double pt = systematic ? (u0 + (double)m) * step : u64_uniform(blk.v[qq]) * total;
+      int lo = 0, hi = N;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (pt < S[mid]) hi = mid;
+        else lo = mid + 1;
+      }
+      int i = lo < N ? lo : N - 1;
+      const double before = i > 0 ? S[i - 1] : 0.0;
+      while (i > 0 && !(Lrow[i] > -CUDART_INF_F)) --i;
+      const float Li = Lrow[i];
+      const float local0 = (float)((pt - before) / (double)ex2(Li - G));
+      const float local = local0 >= 0.f ? local0 : 0.f;
+      // sub-block walk over the row's sub-block sums (relative to the row
+      // total), branch-free, 16 at a time from vector loads
+      const float* w = ws + (size_t)i * nsubp;
+      int s = -1, last_pos = 0;
+      float cum = 0.f, before_s = 0.f, wsel = 0.f, Ls_sel = 0.f;
+      for (int s0 = 0; s0 < nsub; s0 += 16) {
+        float v[16];
+        if (s0 + 16 <= nsubp) {
+          const float4* w4 = reinterpret_cast<const float4*>(w + s0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 t4 = w4[q];
+            v[4 * q] = t4.x;
+            v[4 * q + 1] = t4.y;
+            v[4 * q + 2] = t4.z;
+            v[4 * q + 3] = t4.w;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) v[q] = (s0 + q < nsubp) ? w[s0 + q] : -CUDART_INF_F;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const float e = (s0 + q < nsub) ? ex2(v[q] - Li) : 0.f;
+          const float c2 = cum + e;
+          const bool hit = s < 0 && local < c2;
+          last_pos = (s < 0 && e > 0.f) ? s0 + q : last_pos;
+          before_s = hit ? cum : before_s;
+          wsel = hit ? e : wsel;
+          Ls_sel = hit ? v[q] : Ls_sel;
+          s = hit ? s0 + q : s;
+          cum = c2;
+        }
+      }
+      if (s < 0) {  // spill: clamp to the last positive sub-block
+        s = last_pos;
+        Ls_sel = w[s];
+        wsel = ex2(Ls_sel - Li);
+        before_s = cum - wsel;
+      }
+      float frac = wsel > 0.f ? (local - before_s) / wsel : 0.f;
+      frac = fminf(fmaxf(frac, 0.f), 1.f);
+      const uint32_t p = map_last(b, la, ch, L, i);
+      const float lw2 = lnonuni ? b.LW32[(size_t)ch * N + i] : 0.f;
+      float u[4] = {0, 0, 0, 0}, Bv;
+      row32<D>(cc, XL[p], lw2, u, Bv);
+      const float shift = Ls_sel - Bv;
+      // recompute the sub-block's 64 weights (pass-1 arithmetic; padding
+      // columns give 0), branch-free walk to the first prefix above frac
+      const int j0 = s * kSub;
+      const float4* yb = ycol + j0;
+      const float* ab = Acol + j0;
+      float c3 = 0.f;
+      int jsel = kSub, lastj = 0;
+#pragma unroll 16
+      for (int q = 0; q < kSub; ++q) {
+        const float4 yv = yb[q];
+        const float yy[4] = {yv.x, yv.y, yv.z, yv.w};
+        const float e = ex2(pair32<D>(u, yy, ab[q]) - shift);
+        c3 += e;
+        lastj = e > 0.f ? q : lastj;
+        jsel = (frac < c3 && q < jsel) ? q : jsel;
+      }
+      const int j = j0 + (jsel < kSub ? (jsel <= lastj ? jsel : lastj) : lastj);
+      PL[m + off] = (uint32_t)i;
+      PR[m + off] = (uint32_t)j;
+      la.first_next[nbase + m + off] = map_first(b, la, ch, L, (uint32_t)i);
+      la.last_next[nbase + m + off] = map_last(b, la, ch, R, (uint32_t)j);
     }
-    int i = lo < N ? lo : N - 1;
-    const double before = i > 0 ? S[i - 1] : 0.0;
-    while (i > 0 && !(Lrow[i] > -CUDART_INF_F)) --i;
-    const double ri = (double)ex2(Lrow[i] - G);
-    float local = (float)((pt - before) / ri);
-    if (!(local >= 0.f)) local = 0.f;
-    // sub-block walk (weights relative to the row total)
-    const float* w = ws + (size_t)i * nsubp;
-    const float Li = Lrow[i];
-    int s = 0;
-    float cum = 0.f, before_s = 0.f;
-    int last_pos = 0;
-    for (; s < nsub; ++s) {
-      const float ws_ = ex2(w[s] - Li);
-      if (ws_ > 0.f) last_pos = s;
-      before_s = cum;
-      cum += ws_;
-      if (local < cum) break;
-    }
-    if (s == nsub) {
-      s = last_pos;
-      before_s = cum - ex2(w[s] - Li);
-    }
-    const float wsub = ex2(w[s] - Li);
-    float frac = wsub > 0.f ? (local - before_s) / wsub : 0.f;
-    frac = fminf(fmaxf(frac, 0.f), 1.f);
-    // recompute the sub-block's weights (row-local, shifted by its log-sum)
-    const uint32_t p = map_last(b, la, ch, L, i);
-    const float lw2 = lnonuni ? b.LW32[(size_t)ch * N + i] : 0.f;
-    float u[4] = {0, 0, 0, 0}, Bv;
-    row32<D>(cc, XL[p], lw2, u, Bv);
-    const float shift = w[s] - Bv;
-    const int j0 = s * kSub, j1 = min(j0 + kSub, N);
-    float c3 = 0.f;
-    int j = j0, lastj = j0;
-    for (; j < j1; ++j) {
-      const float e = ex2(pair32<D>(u, ycol + (size_t)j * D, Acol[j]) - shift);
-      if (e > 0.f) lastj = j;
-      c3 += e;
-      if (frac < c3) break;
-    }
-    if (j == j1) j = lastj;
-    PL[m + off] = (uint32_t)i;
-    PR[m + off] = (uint32_t)j;
   }
-  if (b.conditional && tid == 0) {
+  if (b.conditional && tid == 0 && sb == 0) {
     PL[0] = 0;
     PR[0] = 0;
+    la.first_next[nbase] = map_first(b, la, ch, L, 0);
+    la.last_next[nbase] = map_last(b, la, ch, R, 0);
   }
-  __syncthreads();
-  const size_t nbase = ((size_t)ch * b.cap + k) * N;
-  for (int q = tid; q < N; q += blockDim.x) {
-    la.first_next[nbase + q] = map_first(b, la, ch, L, PL[q]);
-    la.last_next[nbase + q] = map_last(b, la, ch, R, PR[q]);
-  }
-  if (tid == 0) {
+  if (tid == 0 && sb == 0) {
     const double logn = log((double)N);
     const bool luni = !L.leaf || b.UNI[(size_t)ch * b.K + L.t];
     const bool runi = !R.leaf || b.UNI[(size_t)ch * b.K + R.t];
     const double shift = (luni ? -logn : 0.0) + (runi ? -logn : 0.0);
     const double ll = block_lnc(b, la, ch, L, g.a);
     const double rl = block_lnc(b, la, ch, R, g.c);
-    la.blnc_next[(size_t)ch * b.cap + k] = ll + rl + b.LMW[gidx] + shift;
+    la.blnc_next[(size_t)ch * b.cap + k] = ll + rl + ((double)G + log2(total)) * kLn2 + shift;
   }
 }
 

@@ -27,7 +27,9 @@ struct LevelArgs {
   double* ws;      // workspace for this chunk
   size_t ws_comb;  // doubles per combine in ws
   int n_out;       // slots resampled (N, or N-1 when conditional)
-  double* dbg;     // TEMP debug
+  int rows_per_cta;   // FP32 pass 1 row tile (multiple of 32)
+  int slots_per_cta;  // FP32 pass 2 slot slice per CTA
+  double* dbg;        // optional debug sink (DSMC_DEBUG)
 };
 
 // Block meta derived from the schedule geometry.

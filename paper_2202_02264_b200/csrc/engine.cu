@@ -286,10 +286,29 @@ int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
 }
 
 template <int D>
-int launch_c32(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
-               int systematic) {
-  const size_t sm = sizeof(double) * b.N + sizeof(float) * (size_t)b.N * (D + 2);
-  CU(cudaFuncSetAttribute(c32_sample<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systematic) {
+  // Pass-1 row tile: as tall as possible (amortises the per-warp column load)
+  // while the grid still covers ~4 resident CTAs per SM.
+  const int target = 148 * 4;
+  const int N = b.N;
+  int rt = std::min(256, (N + 31) / 32 * 32);
+  while (rt > 32 && (long)nk * b.B * ((N + rt - 1) / rt) < target) rt = std::max(32, rt / 2 / 32 * 32);
+  la.rows_per_cta = rt;
+  // Pass-2: split a combine's slots over several CTAs when combines are few.
+  int sb = 1;
+  if ((long)nk * b.B < target / 2)
+    sb = std::max(1, std::min((la.n_out + 63) / 64, (int)((target / 2 + nk * b.B - 1) / (nk * b.B))));
+  la.slots_per_cta = (la.n_out + sb - 1) / sb;
+  const size_t sm1 = sizeof(float) * (size_t)rt * (D + 1);
+  const size_t NP = (N + 63) / 64 * 64;
+  const size_t sm2 = sizeof(double) * (N + 1) + sizeof(float) * (NP * 5 + N);
+  static bool configured = false;
+  if (!configured) {
+    CU(cudaFuncSetAttribute(c32_sample<D>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            cudaSharedmemCarveoutMaxShared));
+    configured = true;
+  }
+  CU(cudaFuncSetAttribute(c32_sample<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
   cudaEvent_t* ev = nullptr;
   if (ctx->time_kernels) {  // 3 events: pair start, pair end = sample start, sample end
     while ((int)ctx->kev.size() < ctx->kev_used + 3) {
@@ -301,10 +320,10 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
     ctx->kev_used += 3;
     CU(cudaEventRecord(ev[0], ctx->stream));
   }
-  c32_pair<D><<<dim3((b.N + kRT - 1) / kRT, nk, b.B), 256, 0, ctx->stream>>>(b, la);
+  c32_pair<D><<<dim3((N + rt - 1) / rt, nk, b.B), 256, sm1, ctx->stream>>>(b, la);
   LAUNCHED(ctx);
   if (ev) CU(cudaEventRecord(ev[1], ctx->stream));
-  c32_sample<D><<<dim3(nk, 1, b.B), 512, sm, ctx->stream>>>(b, la, systematic);
+  c32_sample<D><<<dim3(sb, nk, b.B), 256, sm2, ctx->stream>>>(b, la, systematic);
   LAUNCHED(ctx);
   if (ev) CU(cudaEventRecord(ev[2], ctx->stream));
   return DSMC_OK;
