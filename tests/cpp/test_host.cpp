@@ -1,0 +1,316 @@
+// C++ host API tests, written like the reference's doctest cases (the
+// reference's test names are kept in the CASE titles; file:line cites the
+// case each one ports). Runs on the GPU through include/dsmc/dsmc.hpp.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dsmc/dsmc.hpp"
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                      \
+  do {                                                                   \
+    ++g_checks;                                                          \
+    if (!(cond)) {                                                       \
+      ++g_fail;                                                          \
+      std::printf("  CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+    }                                                                    \
+  } while (0)
+#define CHECK_THROWS_AS(expr, exc)                                       \
+  do {                                                                   \
+    ++g_checks;                                                          \
+    bool ok = false;                                                     \
+    try {                                                                \
+      expr;                                                              \
+    } catch (const exc&) {                                               \
+      ok = true;                                                         \
+    } catch (...) {                                                      \
+    }                                                                    \
+    if (!ok) {                                                           \
+      ++g_fail;                                                          \
+      std::printf("  CHECK_THROWS_AS failed %s:%d: %s\n", __FILE__, __LINE__, #expr); \
+    }                                                                    \
+  } while (0)
+
+struct Case {
+  const char* name;
+  std::function<void()> fn;
+};
+static std::vector<Case>& cases() {
+  static std::vector<Case> v;
+  return v;
+}
+struct Reg {
+  Reg(const char* n, std::function<void()> f) { cases().push_back({n, std::move(f)}); }
+};
+#define TEST_CASE(name) \
+  static void name##_fn(); \
+  static Reg name##_reg(#name, name##_fn); \
+  static void name##_fn()
+
+namespace {
+
+// tests/support/ar1.hpp:23-126: stationary AR(1), Gaussian observations
+dsmc::LinearGaussianModel ar1_exact(const std::vector<double>& ys, double rho = 0.8,
+                                    double q = 0.3, double r = 0.4) {
+  const int T = (int)ys.size() - 1;
+  dsmc::LinearGaussianModel m;
+  m.horizon = T;
+  const double s2 = q / (1 - rho * rho);
+  m.m0 = {0.0};
+  m.P0 = {s2};
+  for (int t = 0; t <= T; ++t) {
+    m.F.push_back({rho});
+    m.b.push_back({0.0});
+    m.Q.push_back({q});
+    m.H.push_back({1.0});
+    m.R.push_back({r});
+    m.y.push_back({ys[t]});
+    m.has_obs.push_back(1);
+  }
+  return m;
+}
+
+std::vector<double> default_ys(int T) {
+  const double pool[] = {0.4, -0.1, 0.9, 1.3, 0.2, -0.7, -0.2, 0.5, 1.1, 0.3, -0.4, 0.1,
+                         0.8, -0.9, 0.0, 0.6, -0.3, 0.7, 1.0, -0.5, 0.2, -0.8, 0.35, 0.15};
+  std::vector<double> ys(T + 1);
+  for (int t = 0; t <= T; ++t) ys[t] = pool[t % 24];
+  return ys;
+}
+
+dsmc::FeynmanKacModel ar1_fk(int T) {
+  auto lg = ar1_exact(default_ys(T));
+  const double s2 = 0.3 / (1 - 0.64);
+  std::vector<dsmc::ProposalMarginal> marg(T + 1, {{0.0}, {s2}});
+  return dsmc::make_lgssm_fk(lg, marg);
+}
+
+}  // namespace
+
+// test_smoother.cpp:195-227
+TEST_CASE(combine_schedule_packed_pairing_clipped_blocks_log_depth) {
+  for (int T : {0, 1, 2, 5, 6, 11, 100}) {
+    auto s = dsmc::build_schedule(T);
+    CHECK((int)s.pairs.size() == T);
+    CHECK(s.levels == dsmc::reference_tree_depth(T));
+    CHECK(s.levels == (T == 0 ? 0 : (int)std::ceil(std::log2(T + 1.0))));
+  }
+  auto s = dsmc::build_schedule(5);
+  CHECK(s.pairs[2].level == 1 && s.pairs[2].left_a == 4 && s.pairs[2].right_b == 5);
+  CHECK(s.pairs.back().left_a == 0 && s.pairs.back().right_b == 5);
+}
+
+// test_smoother.cpp:292-316: means and evidence vs the exact answers
+TEST_CASE(smoothed_means_and_evidence_match_the_exact_Kalman_answers) {
+  const int T = 11;
+  auto lg = ar1_exact(default_ys(T));
+  auto kr = dsmc::kalman_smooth(lg);
+  auto model = ar1_fk(T);
+  const int reps = 16;
+  std::vector<double> mean_sum(T + 1, 0.0), mean_sq(T + 1, 0.0);
+  double lz_sum = 0, lz_sq = 0;
+  for (int s = 0; s < reps; ++s) {
+    dsmc::SmootherOptions o;
+    o.n_particles = 1500;
+    o.seed = 100 + s;
+    auto res = dsmc::run_smoother(model, o);
+    for (int t = 0; t <= T; ++t) {
+      const double m = dsmc::weighted_time_mean(res.root, t)[0];
+      mean_sum[t] += m;
+      mean_sq[t] += m * m;
+    }
+    lz_sum += *res.meta.log_norm_const;
+    lz_sq += *res.meta.log_norm_const * *res.meta.log_norm_const;
+  }
+  for (int t = 0; t <= T; ++t) {
+    const double mu = mean_sum[t] / reps;
+    const double se = std::sqrt(std::max(mean_sq[t] / reps - mu * mu, 1e-12) / (reps - 1));
+    CHECK(std::fabs(mu - kr.smooth_mean[t][0]) < 5 * se + 1e-3);
+  }
+  const double lz = lz_sum / reps;
+  const double lse = std::sqrt(std::max(lz_sq / reps - lz * lz, 1e-12) / (reps - 1));
+  CHECK(std::fabs(lz - kr.log_likelihood) < 5 * lse + 0.05);
+}
+
+// test_smoother.cpp:343-385
+TEST_CASE(runs_are_deterministic_and_precision_invariant_in_structure) {
+  auto model = ar1_fk(30);
+  dsmc::SmootherOptions o;
+  o.n_particles = 200;
+  o.seed = 7;
+  auto a = dsmc::run_smoother(model, o);
+  auto b = dsmc::run_smoother(model, o);
+  CHECK(a.root.paths == b.root.paths);
+  CHECK(*a.meta.log_norm_const == *b.meta.log_norm_const);
+  o.precision = dsmc::Precision::fp64_parity;
+  auto c = dsmc::run_smoother(model, o);
+  auto d = dsmc::run_smoother(model, o);
+  CHECK(c.root.paths == d.root.paths);
+  CHECK(c.meta.weight_evals == 30ull * 200 * 200);  // T * N^2 (test_smoother.cpp:382)
+  CHECK(c.meta.levels == 5);
+}
+
+// test_smoother.cpp:387-414
+TEST_CASE(MH_chain_stitching_zero_steps_keeps_identity_pairs_and_is_flagged) {
+  auto model = ar1_fk(7);
+  dsmc::SmootherOptions o;
+  o.n_particles = 16;
+  o.resampler = dsmc::Resampler::mh_lazy;
+  o.mh_steps = 0;
+  auto res = dsmc::run_smoother(model, o);
+  CHECK(res.meta.biased);
+  CHECK(res.meta.weight_evals == 0);
+  CHECK(!res.meta.log_norm_const.has_value());
+}
+
+// test_smoother.cpp:416-434
+TEST_CASE(rejection_stitching_matches_the_dense_smoother_statistically) {
+  auto model = ar1_fk(11);
+  dsmc::SmootherOptions o;
+  o.n_particles = 2000;
+  o.resampler = dsmc::Resampler::rejection_lazy;
+  auto res = dsmc::run_smoother(model, o);
+  auto kr = dsmc::kalman_smooth(ar1_exact(default_ys(11)));
+  for (int t = 0; t <= 11; ++t)
+    CHECK(std::fabs(dsmc::weighted_time_mean(res.root, t)[0] - kr.smooth_mean[t][0]) < 0.15);
+  CHECK(!res.meta.biased);
+}
+
+// test_smoother.cpp:502-527
+TEST_CASE(single_time_models_skip_combining_entirely) {
+  auto model = ar1_fk(0);
+  dsmc::SmootherOptions o;
+  o.n_particles = 64;
+  auto res = dsmc::run_smoother(model, o);
+  CHECK(res.meta.levels == 0);
+  CHECK(res.meta.weight_evals == 0);
+  CHECK(res.root.len() == 1);
+}
+
+TEST_CASE(models_without_a_device_descriptor_are_rejected) {
+  dsmc::FeynmanKacModel m;
+  m.horizon = 3;
+  CHECK_THROWS_AS(dsmc::run_smoother(m, dsmc::SmootherOptions{}), std::invalid_argument);
+}
+
+// test_resampling.cpp:65-89
+TEST_CASE(multinomial_frequencies_and_log_total_match_an_independent_normalization) {
+  const std::vector<double> logw = {0.3, -1.2, 0.8, -0.4, 1.5, -2.0, 0.0, 0.7, -0.9};
+  long double mx = -INFINITY, tot = 0;
+  for (double v : logw) mx = std::max<long double>(mx, v);
+  for (double v : logw) tot += std::exp((long double)v - mx);
+  const std::size_t n_out = 60000;
+  auto ps = dsmc::resample_pairs(dsmc::Resampler::multinomial, logw, 3, n_out, 0,
+                                 {11, 2, 5, dsmc::StreamRole::pair_resample});
+  CHECK(std::fabs(*ps.log_mean_weight - (double)(mx + std::log(tot))) < 1e-12);
+  CHECK(ps.weight_evals == 9);
+  std::vector<double> cnt(9, 0);
+  for (std::size_t k = 0; k < n_out; ++k) cnt[ps.left[k] * 3 + ps.right[k]] += 1;
+  for (int k = 0; k < 9; ++k) {
+    const double p = (double)(std::exp((long double)logw[k] - mx) / tot);
+    CHECK(std::fabs(cnt[k] - n_out * p) <= 5 * std::sqrt(n_out * p * (1 - p)) + 1);
+  }
+  CHECK_THROWS_AS(dsmc::resample_pairs(dsmc::Resampler::multinomial,
+                                       std::vector<double>(25, -INFINITY), 5, 10, 0, {}),
+                  std::runtime_error);
+}
+
+// test_conditional.cpp:317-329
+TEST_CASE(ordered_and_biased_resamplers_are_rejected_at_configuration) {
+  auto model = ar1_fk(5);
+  std::vector<double> ref(6, 0.1);
+  dsmc::ConditionalOptions o;
+  o.n_particles = 8;
+  o.resampler = dsmc::Resampler::systematic;
+  CHECK_THROWS_AS(dsmc::run_conditional(model, ref.data(), o, 0), std::invalid_argument);
+  o.resampler = dsmc::Resampler::mh_lazy;
+  CHECK_THROWS_AS(dsmc::run_conditional(model, ref.data(), o, 0), std::invalid_argument);
+}
+
+// test_conditional.cpp:360-391
+TEST_CASE(sweeps_are_deterministic_and_keyed_by_seed_and_sweep_index) {
+  auto model = ar1_fk(9);
+  std::vector<double> ref(10, 0.2);
+  dsmc::ConditionalOptions o;
+  o.n_particles = 64;
+  o.seed = 5;
+  auto a = dsmc::run_conditional(model, ref.data(), o, 3);
+  auto b = dsmc::run_conditional(model, ref.data(), o, 3);
+  auto c = dsmc::run_conditional(model, ref.data(), o, 4);
+  CHECK(a.path == b.path);
+  CHECK(a.path != c.path);
+  CHECK(a.meta.weight_evals == 9ull * (64 * 64 + 1));  // test_conditional.cpp:188
+}
+
+// test_pgibbs.cpp:160-202
+TEST_CASE(pgibbs_sweep_aborts_cleanly_when_a_kernel_or_builder_throws) {
+  dsmc::GibbsState st;
+  st.theta = {1.0};
+  st.star.assign(8, 0.1);
+  const auto saved = st;
+  auto bad_kernel = [](dsmc::GibbsState&, std::uint64_t, std::uint32_t) {
+    throw std::runtime_error("kernel failed");
+  };
+  auto builder = [](dsmc::GibbsState&) { return ar1_fk(7); };
+  dsmc::ConditionalOptions o;
+  o.n_particles = 16;
+  CHECK_THROWS_AS(dsmc::pgibbs_sweep(st, builder, bad_kernel, o, 0), std::runtime_error);
+  CHECK(st.star == saved.star && st.theta == saved.theta);
+  auto id_kernel = [](dsmc::GibbsState&, std::uint64_t, std::uint32_t) {};
+  auto out = dsmc::pgibbs_sweep(st, builder, id_kernel, o, 1);
+  CHECK(out.state.star.size() == 8);
+  CHECK(out.changed.size() == 8);
+  CHECK(st.star == saved.star);
+}
+
+TEST_CASE(batched_sv_particle_gibbs_moves_parameters_and_paths) {
+  const int T = 63, B = 4;
+  std::vector<double> ys(T + 1);
+  for (int t = 0; t <= T; ++t) ys[t] = std::exp(-0.5) * ((t % 3) ? 1.0 : -1.3);
+  dsmc::SvGibbsChains ch;
+  ch.theta.assign(B * 3, 0.0);
+  for (int c = 0; c < B; ++c) {
+    ch.theta[3 * c] = -1.0;
+    ch.theta[3 * c + 1] = 0.9;
+    ch.theta[3 * c + 2] = 0.1;
+    ch.seeds.push_back(1000 + c);
+  }
+  ch.stars.assign((size_t)B * (T + 1), -1.0);
+  dsmc_sv_prior prior{-1.0, 1.0, 2.0, 0.2, 0.05};
+  dsmc::ConditionalOptions o;
+  o.n_particles = 128;
+  const auto theta0 = ch.theta;
+  std::size_t moved = 0;
+  for (std::uint32_t s = 0; s < 5; ++s) {
+    auto changed = dsmc::sv_pgibbs_sweep(ch, ys, prior, o, s);
+    for (char v : changed) moved += v;
+  }
+  CHECK(ch.theta != theta0);
+  CHECK(moved > (std::size_t)(B * (T + 1)));
+  for (double v : ch.stars) CHECK(std::isfinite(v));
+}
+
+int main(int argc, char** argv) {
+  const char* only = argc > 1 ? argv[1] : nullptr;
+  int failed_cases = 0;
+  for (auto& c : cases()) {
+    if (only && std::strstr(c.name, only) == nullptr) continue;
+    const int before = g_fail;
+    try {
+      c.fn();
+    } catch (const std::exception& e) {
+      ++g_fail;
+      std::printf("  exception: %s\n", e.what());
+    }
+    const bool ok = g_fail == before;
+    failed_cases += !ok;
+    std::printf("[%s] %s\n", ok ? "PASS" : "FAIL", c.name);
+  }
+  std::printf("%d checks, %d failed, %d failing cases\n", g_checks, g_fail, failed_cases);
+  return failed_cases ? 1 : 0;
+}
