@@ -269,6 +269,45 @@ DSMC_API int dsmc_sv_pgibbs_sweep(dsmc_ctx* ctx, int n_chains, int horizon,
                          uint8_t* changed, uint64_t* accepted_phi);
 
 /* ------------------------------------------------------------------------
+ * Time-sharded smoothing (multi-GPU). The reference has no
+ * distribution; these stages let one process per GPU run contiguous time
+ * windows with the reference's GLOBAL stream keys, so a P-GPU run
+ * reproduces the 1-GPU run bit for bit. The host protocol
+ * (paper_2202_02264_b200/sharded.py) exchanges only boundary slabs, block
+ * log Z and ancestor indices over NCCL for the top log2(P) levels.
+ *
+ *   dsmc_window_run       leaves [t0, t0+len) + the len-local combine levels
+ *   dsmc_window_boundary  slab of the window root's first (side 0: states +
+ *                         column terms) or last (side 1) leaf, device out
+ *   dsmc_cross_combine    one cross-window combine at cut `cut`, global
+ *                         (level, node) stream key, on gathered slabs
+ *   dsmc_window_remap     root first (side 0) / last (side 1) map := map[idx]
+ *   dsmc_window_finish    top-down composition from the window root's map
+ *                         (NULL = identity) + per-time moments (device) */
+typedef struct dsmc_window_opts {
+  size_t n_particles;
+  int resampler;   /* dense (multinomial / systematic) for cross combines */
+  size_t mh_steps;
+  uint64_t seed;
+  int t0;          /* first leaf; a multiple of len */
+  int len;         /* leaves in the window; a power of two >= 2 */
+} dsmc_window_opts;
+
+DSMC_API int dsmc_window_run(dsmc_ctx* ctx, const dsmc_model_handle* h,
+                             const dsmc_window_opts* opts);
+DSMC_API int dsmc_window_boundary(dsmc_ctx* ctx, int side, void* d_states,
+                                  float* d_col, double* root_log_norm_const);
+DSMC_API int dsmc_cross_combine(dsmc_ctx* ctx, const dsmc_model_handle* h,
+                                const dsmc_window_opts* opts, int cut, int level,
+                                long long node, const void* d_left_states,
+                                const void* d_right_states, const float* d_right_col,
+                                double lnc_left, double lnc_right, uint32_t* d_left_idx,
+                                uint32_t* d_right_idx, double* lnc_out);
+DSMC_API int dsmc_window_remap(dsmc_ctx* ctx, int side, const uint32_t* d_idx);
+DSMC_API int dsmc_window_finish(dsmc_ctx* ctx, const uint32_t* d_root_map,
+                                double* d_mean, double* d_cov);
+
+/* ------------------------------------------------------------------------
  * Proposal construction (host, FP64, the step before the
  * leaves): exact Kalman filter + RTS smoother of a DSMC_MODEL_LGSSM
  * descriptor (prop_mean / prop_cov are ignored). Restates kalman_smooth

@@ -74,6 +74,13 @@ class CondOpts(C.Structure):
     ]
 
 
+class WindowOpts(C.Structure):
+    _fields_ = [
+        ("n_particles", C.c_size_t), ("resampler", C.c_int), ("mh_steps", C.c_size_t),
+        ("seed", C.c_uint64), ("t0", C.c_int), ("len", C.c_int),
+    ]
+
+
 class SvPrior(C.Structure):
     _fields_ = [
         ("mu_mean", C.c_double), ("mu_var", C.c_double),

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
   Side L, R;
   CombineGeom g;
   sides(b, la, k, L, R, g);
-  const TimeConst& tc = b.tc[(size_t)ch * b.K + g.c];
+  const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + g.c];
   CutConst32 cc;
   load_cut32<D>(tc, cc);
   const int nch = (N + kChunk - 1) / kChunk;
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
   Side L, R;
   CombineGeom g;
   sides(b, la, k, L, R, g);
-  const TimeConst& tc = b.tc[(size_t)ch * b.K + g.c];
+  const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + g.c];
   CutConst32 cc;
   load_cut32<D>(tc, cc);
   const int nch = (N + kChunk - 1) / kChunk;
@@ -378,10 +378,10 @@ __global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
   const float4* XL = b.X32 + ((size_t)ch * b.K + L.t) * N;
   const int off = b.conditional ? 1 : 0;
   const uint64_t node = b.conditional
-                            ? (static_cast<uint64_t>(static_cast<uint32_t>(k)) |
+                            ? (static_cast<uint64_t>(static_cast<uint32_t>(k + la.node_off)) |
                                (static_cast<uint64_t>(b.sweep) << 32))
-                            : static_cast<uint64_t>(k);
-  const StreamId id = stream_id(b.seeds[ch], la.level, node, DSMC_ROLE_PAIR_RESAMPLE, 0);
+                            : static_cast<uint64_t>(k + la.node_off);
+  const StreamId id = stream_id(b.seeds[ch], la.key_level, node, DSMC_ROLE_PAIR_RESAMPLE, 0);
   double u0 = 0.0, step = 0.0;
   if (systematic) {
     u0 = u64_uniform(stream_u64(id, 0));
@@ -510,7 +510,7 @@ __global__ void lazy32_kernel(Bufs b, LevelArgs la, int mh, size_t mh_steps) {
   Side L, R;
   CombineGeom g;
   sides(b, la, k, L, R, g);
-  const TimeConst& tc = b.tc[(size_t)ch * b.K + g.c];
+  const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + g.c];
   CutConst32 cc;
   load_cut32<D>(tc, cc);
   const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
@@ -544,11 +544,11 @@ __global__ void lazy32_kernel(Bufs b, LevelArgs la, int mh, size_t mh_steps) {
   int err = 0, why = 0;
   if (m < la.n_out) {
     const uint64_t node = b.conditional
-                              ? (static_cast<uint64_t>(static_cast<uint32_t>(k)) |
+                              ? (static_cast<uint64_t>(static_cast<uint32_t>(k + la.node_off)) |
                                  (static_cast<uint64_t>(b.sweep) << 32))
-                              : static_cast<uint64_t>(k);
+                              : static_cast<uint64_t>(k + la.node_off);
     StreamReader s;
-    s.init(stream_id(b.seeds[ch], la.level, node, DSMC_ROLE_PAIR_RESAMPLE, m + 1));
+    s.init(stream_id(b.seeds[ch], la.key_level, node, DSMC_ROLE_PAIR_RESAMPLE, m + 1));
     uint32_t oi = 0, oj = 0;
     if (mh) {
       uint32_t i = (uint32_t)(m % N), j = i;

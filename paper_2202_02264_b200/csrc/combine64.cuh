@@ -27,6 +27,8 @@ struct LevelArgs {
   double* ws;      // workspace for this chunk
   size_t ws_comb;  // doubles per combine in ws
   int n_out;       // slots resampled (N, or N-1 when conditional)
+  int key_level;      // level in the stream key (global tree level)
+  long long node_off; // global node index of local combine 0 (windows)
   int rows_per_cta;   // FP32 pass 1 row tile (multiple of 32)
   int slots_per_cta;  // FP32 pass 2 slot slice per CTA
   double* dbg;        // optional debug sink (DSMC_DEBUG)
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(256) c64_rows(Bufs b, LevelArgs la) {
   CombineGeom g;
   sides(b, la, k, L, R, g);
   const DevModel& M = b.models[ch];
-  const TimeConst& tc = b.tc[(size_t)ch * b.K + g.c];
+  const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + g.c];
   Col64 C;
   stage_cols<MC, D>(b, la, ch, R, M, tc, smem, C);
   double* ws = la.ws + (size_t)blockIdx.y * la.ws_comb;
@@ -292,7 +294,7 @@ __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
   CombineGeom g;
   sides(b, la, k, L, R, g);
   const DevModel& M = b.models[ch];
-  const TimeConst& tc = b.tc[(size_t)ch * b.K + g.c];
+  const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + g.c];
   Col64 C;
   stage_cols<MC, D>(b, la, ch, R, M, tc, smem, C);
   double* ws = la.ws + (size_t)blockIdx.x * la.ws_comb;
@@ -350,10 +352,10 @@ __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
   const double coef = row_coef<MC>(M, g.c);
   const int off = b.conditional ? 1 : 0;
   const uint64_t node = b.conditional
-                            ? (static_cast<uint64_t>(static_cast<uint32_t>(k)) |
+                            ? (static_cast<uint64_t>(static_cast<uint32_t>(k + la.node_off)) |
                                (static_cast<uint64_t>(b.sweep) << 32))
-                            : static_cast<uint64_t>(k);
-  const StreamId id = stream_id(b.seeds[ch], la.level, node,
+                            : static_cast<uint64_t>(k + la.node_off);
+  const StreamId id = stream_id(b.seeds[ch], la.key_level, node,
                                 DSMC_ROLE_PAIR_RESAMPLE, 0);
   double u0 = 0.0, step = 0.0;
   if (systematic) {
@@ -474,7 +476,7 @@ __global__ void lazy64_kernel(Bufs b, LevelArgs la, int mh, size_t mh_steps) {
   const bool rnonuni = R.leaf && !b.UNI[(size_t)ch * b.K + R.t];
   Probe64 P;
   P.M = &b.models[ch];
-  P.tc = &b.tc[(size_t)ch * b.K + g.c];
+  P.tc = &b.tc[(size_t)ch * b.Kt + b.t0 + g.c];
   P.XL = b.X64 + ((size_t)ch * b.K + L.t) * N * b.d;
   P.XR = b.X64 + ((size_t)ch * b.K + R.t) * N * b.d;
   P.lwl = lnonuni ? b.LW64 + ((size_t)ch * b.K + L.t) * N : nullptr;
@@ -492,11 +494,11 @@ __global__ void lazy64_kernel(Bufs b, LevelArgs la, int mh, size_t mh_steps) {
   int err = 0, why = 0;
   if (m < la.n_out) {
     const uint64_t node = b.conditional
-                              ? (static_cast<uint64_t>(static_cast<uint32_t>(k)) |
+                              ? (static_cast<uint64_t>(static_cast<uint32_t>(k + la.node_off)) |
                                  (static_cast<uint64_t>(b.sweep) << 32))
-                              : static_cast<uint64_t>(k);
+                              : static_cast<uint64_t>(k + la.node_off);
     StreamReader s;
-    s.init(stream_id(b.seeds[ch], la.level, node, DSMC_ROLE_PAIR_RESAMPLE, m + 1));
+    s.init(stream_id(b.seeds[ch], la.key_level, node, DSMC_ROLE_PAIR_RESAMPLE, m + 1));
     uint32_t oi = 0, oj = 0;
     if (mh) {  // mh_lazy_pairs (resampling.cpp:250-279)
       uint32_t i = (uint32_t)(m % N), j = i;
@@ -593,7 +595,7 @@ __global__ void refpair_check_kernel(Bufs b, LevelArgs la) {
   const bool rnonuni = R.leaf && !b.UNI[(size_t)ch * b.K + R.t];
   Probe64 P;
   P.M = &b.models[ch];
-  P.tc = &b.tc[(size_t)ch * b.K + g.c];
+  P.tc = &b.tc[(size_t)ch * b.Kt + b.t0 + g.c];
   P.XL = b.X64 + ((size_t)ch * b.K + L.t) * N * b.d;
   P.XR = b.X64 + ((size_t)ch * b.K + R.t) * N * b.d;
   P.lwl = lnonuni ? b.LW64 + ((size_t)ch * b.K + L.t) * N : nullptr;

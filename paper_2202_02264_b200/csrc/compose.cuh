@@ -15,12 +15,14 @@ namespace dsmc_dev {
 // One top-down level (level >= 2): maps of level l -> maps of level l-1.
 __global__ void td_kernel(Bufs b, int level, size_t cursor, int nb_l,
                           int nb_lm1, const uint32_t* Mcur, uint32_t* Mnext,
-                          int root) {
+                          int root, const uint32_t* root_map) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   const int k = blockIdx.y, ch = blockIdx.z;
   const int N = b.N;
   if (q >= N) return;
-  const uint32_t m = root ? (uint32_t)q : Mcur[((size_t)ch * b.cap + k) * N + q];
+  // root map: identity, or the window root's map from the cross-shard levels
+  const uint32_t m = root ? (root_map ? root_map[(size_t)ch * N + q] : (uint32_t)q)
+                          : Mcur[((size_t)ch * b.cap + k) * N + q];
   if (2 * k + 1 < nb_lm1) {
     const size_t gidx = (size_t)ch * b.T + cursor + k;
     Mnext[((size_t)ch * b.cap + 2 * k) * N + q] = b.PL[gidx * N + m];
@@ -32,10 +34,12 @@ __global__ void td_kernel(Bufs b, int level, size_t cursor, int nb_l,
 
 // sigma_t[q] from the level-1 maps (root = identity when K <= 2).
 __device__ inline uint32_t leaf_sigma(const Bufs& b, int ch, int t, int q,
-                                      const uint32_t* M1, int root1) {
-  if (b.K == 1) return (uint32_t)q;
+                                      const uint32_t* M1, int root1,
+                                      const uint32_t* root_map) {
+  const uint32_t r0 = root_map ? root_map[(size_t)ch * b.N + q] : (uint32_t)q;
+  if (b.K == 1) return r0;
   const int k = t >> 1;
-  const uint32_t m = root1 ? (uint32_t)q : M1[((size_t)ch * b.cap + k) * b.N + q];
+  const uint32_t m = root1 ? r0 : M1[((size_t)ch * b.cap + k) * b.N + q];
   if (2 * k + 1 < b.K) {
     const size_t gidx = (size_t)ch * b.T + k;  // level-1 cursor is 0
     return (t & 1) ? b.PR[gidx * b.N + m] : b.PL[gidx * b.N + m];
@@ -47,14 +51,15 @@ __device__ inline uint32_t leaf_sigma(const Bufs& b, int ch, int t, int q,
 // (time, chain). FP64 leaves (parity path).
 __global__ void __launch_bounds__(256) gather64_kernel(Bufs b, const uint32_t* M1,
                                                        int root1, double* paths,
-                                                       double* mean, double* cov) {
+                                                       double* mean, double* cov,
+                                                       const uint32_t* root_map) {
   const int t = blockIdx.x, ch = blockIdx.y;
   const int N = b.N, d = b.d;
   __shared__ double red[8][20];
   double s1[4] = {0, 0, 0, 0}, s2[16] = {0};
   const double* X = b.X64 + ((size_t)ch * b.K + t) * N * d;
   for (int q = threadIdx.x; q < N; q += blockDim.x) {
-    const uint32_t sg = leaf_sigma(b, ch, t, q, M1, root1);
+    const uint32_t sg = leaf_sigma(b, ch, t, q, M1, root1, root_map);
     double x[4];
     for (int k = 0; k < d; ++k) x[k] = X[(size_t)sg * d + k];
     if (paths)
@@ -93,15 +98,16 @@ __global__ void __launch_bounds__(256) gather64_kernel(Bufs b, const uint32_t* M
 template <int D>
 __global__ void __launch_bounds__(256) gather32_kernel(Bufs b, const uint32_t* M1,
                                                        int root1, double* paths,
-                                                       double* mean, double* cov) {
+                                                       double* mean, double* cov,
+                                                       const uint32_t* root_map) {
   const int t = blockIdx.x, ch = blockIdx.y;
   const int N = b.N;
   __shared__ double red[8][20];
-  const TimeConst& tc = b.tc[(size_t)ch * b.K + t];
+  const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + t];
   double s1[4] = {0, 0, 0, 0}, s2[16] = {0};
   const float4* X = b.X32 + ((size_t)ch * b.K + t) * N;
   for (int q = threadIdx.x; q < N; q += blockDim.x) {
-    const uint32_t sg = leaf_sigma(b, ch, t, q, M1, root1);
+    const uint32_t sg = leaf_sigma(b, ch, t, q, M1, root1, root_map);
     const float4 xv = X[sg];
     double x[4];
 #pragma unroll

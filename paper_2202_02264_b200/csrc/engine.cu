@@ -84,6 +84,7 @@ struct dsmc_ctx {
   int last_levels = 0;
   int last_biased = 0;
   double* h_lnc = nullptr;  // pinned scratch
+  void* window = nullptr;   // WindowState of the last run (time-sharded API)
 };
 
 namespace {
@@ -253,6 +254,12 @@ struct RunOpts {
   double* star_out = nullptr;   // device [B][K][d]
   uint8_t* changed = nullptr;   // device [B][K]
   bool timing = false;
+  // time-sharded windows (FP32): leaves [t0, t0 + len) of the model, global
+  // stream keys; composition optional, from a given root map
+  int t0 = 0;
+  int len = -1;
+  bool compose = true;
+  const uint32_t* root_map = nullptr;  // device [B][N]
 };
 
 struct RunResult {
@@ -395,8 +402,20 @@ std::string err_message(const ErrFlag& e, int K) {
 }
 
 // Core: leaves + levels (+ composition/gather). B chains share K, N, d.
+struct WindowState {
+  bool valid = false;
+  Bufs b{};
+  int levels = 0, cur = 0;
+  uint32_t* maps[4] = {};
+  double* blnc[2] = {};
+  int resampler = 0;
+};
+WindowState& window_state(dsmc_ctx* ctx);
+
 int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* res) {
-  const int B = h->B, K = h->K, T = K - 1, d = h->d;
+  const int B = h->B, K = o.len > 0 ? o.len : h->K, T = K - 1, d = h->d;
+  if (o.t0 < 0 || o.t0 + K > h->K)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "window outside the model's horizon");
   const int N = (int)o.N;
   if (N < 1) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "make_leaf: n must be >= 1");
   if (o.conditional && N < 2)
@@ -425,6 +444,8 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
   b.conditional = o.conditional;
   b.sweep = o.sweep;
   b.star = o.star;
+  b.t0 = o.t0;
+  b.Kt = h->K;
   Arena& A = ctx->arena;
   void* p;
   const size_t BK = (size_t)B * K, BKN = BK * N, BT = (size_t)B * std::max(T, 1);
@@ -494,8 +515,10 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     CU(A.get("RAW0", (size_t)B * N * sizeof(double), &p));
     leaf32_kernel<<<dim3((N + 127) / 128, K, B), 128, 0, ctx->stream>>>(b, (double*)p);
     LAUNCHED(ctx);
-    leafnorm32_kernel<<<B, 32, 0, ctx->stream>>>(b, (const double*)p);
-    LAUNCHED(ctx);
+    if (o.t0 == 0) {  // only global leaf 0 carries non-uniform weights
+      leafnorm32_kernel<<<B, 32, 0, ctx->stream>>>(b, (const double*)p);
+      LAUNCHED(ctx);
+    }
   }
   CU(cudaGetLastError());
   if (o.timing) CU(cudaEventRecord(ctx->ev[1], ctx->stream));
@@ -534,6 +557,8 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     la.n_out = o.conditional ? N - 1 : N;
     la.ws = ws;
     la.ws_comb = ws_comb;
+    la.key_level = level;
+    la.node_off = (long long)(o.t0 >> level);
     if (getenv("DSMC_DEBUG")) {
       static double* dbg = nullptr;
       if (!dbg) cudaMallocManaged(&dbg, 256 * 8);
@@ -612,6 +637,18 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
   res->LNC = b.LNC;
   res->X64 = b.X64;
   res->LW64 = b.LW64;
+  {
+    WindowState& st = window_state(ctx);
+    st.valid = true;
+    st.b = b;
+    st.levels = level;
+    st.cur = cur;
+    for (int i = 0; i < 4; ++i) st.maps[i] = maps[i];
+    st.blnc[0] = blnc[0];
+    st.blnc[1] = blnc[1];
+    st.resampler = o.resampler;
+  }
+  if (!o.compose) return DSMC_OK;
 
   // ----------------------------------------------------------- composition
   if (o.conditional) {
@@ -647,22 +684,23 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     bool root = true;
     for (int l = level; l >= 2; --l) {
       td_kernel<<<dim3((N + 255) / 256, nbs[l], B), 256, 0, ctx->stream>>>(
-          b, l, cursors[l], nbs[l], nbs[l - 1], Mb[mcur], Mb[1 - mcur], root ? 1 : 0);
+          b, l, cursors[l], nbs[l], nbs[l - 1], Mb[mcur], Mb[1 - mcur], root ? 1 : 0,
+          o.root_map);
       LAUNCHED(ctx);
       root = false;
       mcur = 1 - mcur;
     }
     if (fp64) {
       gather64_kernel<<<dim3(K, B), 256, 0, ctx->stream>>>(b, Mb[mcur], root ? 1 : 0,
-                                                           o.paths, o.mean, o.cov);
+                                                           o.paths, o.mean, o.cov, o.root_map);
     } else {
       const uint32_t* M1 = Mb[mcur];
       const int r1 = root ? 1 : 0;
       switch (d) {
-        case 1: gather32_kernel<1><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov); break;
-        case 2: gather32_kernel<2><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov); break;
-        case 3: gather32_kernel<3><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov); break;
-        default: gather32_kernel<4><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov); break;
+        case 1: gather32_kernel<1><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
+        case 2: gather32_kernel<2><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
+        case 3: gather32_kernel<3><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
+        default: gather32_kernel<4><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
       }
     }
     LAUNCHED(ctx);
@@ -717,6 +755,8 @@ void dsmc_destroy(dsmc_ctx* ctx) {
   if (ctx->d_cov) cudaFree(ctx->d_cov);
   if (ctx->h_lnc) cudaFreeHost(ctx->h_lnc);
   for (auto& e : ctx->ev) cudaEventDestroy(e);
+  for (auto& e : ctx->kev) cudaEventDestroy(e);
+  delete static_cast<WindowState*>(ctx->window);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -1438,3 +1478,222 @@ extern "C" int dsmc_sv_pgibbs_sweep(dsmc_ctx* ctx, int B, int T, const double* y
   if (accepted_phi) *accepted_phi = acc;
   return DSMC_OK;
 }
+
+// ------------------------------------------------------ time-sharded API
+namespace {
+
+WindowState& window_state_impl(dsmc_ctx* ctx) {
+  if (!ctx->window) ctx->window = new WindowState();
+  return *static_cast<WindowState*>(ctx->window);
+}
+
+__global__ void boundary_kernel(const float4* X, const float* COL, const uint32_t* map,
+                                int N, float4* out_x, float* out_col) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= N) return;
+  const uint32_t p = map ? map[q] : (uint32_t)q;
+  out_x[q] = X[p];
+  if (out_col) out_col[q] = COL[p];
+}
+
+__global__ void remap_kernel(uint32_t* map, const uint32_t* idx, uint32_t* tmp, int N) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < N) tmp[q] = map[idx[q]];
+}
+
+}  // namespace
+
+namespace {
+WindowState& window_state(dsmc_ctx* ctx) { return window_state_impl(ctx); }
+}  // namespace
+
+extern "C" {
+
+int dsmc_window_run(dsmc_ctx* ctx, const dsmc_model_handle* hc, const dsmc_window_opts* wo) {
+  if (!ctx || !hc || !wo) return DSMC_E_INVALID_ARGUMENT;
+  auto* h = const_cast<dsmc_model_handle*>(hc);
+  const int len = wo->len;
+  if (len < 2 || (len & (len - 1)) || wo->t0 % len || wo->t0 + len > h->K)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                   "window: len must be a power of two >= 2 dividing t0, inside the horizon");
+  RunOpts o;
+  o.precision = DSMC_FP32;
+  o.resampler = wo->resampler;
+  o.mh_steps = wo->mh_steps;
+  o.N = wo->n_particles;
+  o.t0 = wo->t0;
+  o.len = len;
+  o.compose = false;
+  void* p;
+  CU(ctx->arena.get("SEEDS", sizeof(uint64_t), &p));
+  CU(cudaMemcpyAsync(p, &wo->seed, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+  o.seeds = (const uint64_t*)p;
+  RunResult res;
+  return run_tree(ctx, h, o, &res);
+}
+
+int dsmc_window_boundary(dsmc_ctx* ctx, int side, void* d_x, float* d_col, double* root_lnc) {
+  if (!ctx) return DSMC_E_INVALID_ARGUMENT;
+  WindowState& st = window_state(ctx);
+  if (!st.valid) return set_err(ctx, DSMC_E_LOGIC, "no window run on this context");
+  const Bufs& b = st.b;
+  const int N = b.N;
+  const int t = side == 0 ? 0 : b.K - 1;
+  const uint32_t* map = st.maps[2 * st.cur + (side == 0 ? 0 : 1)];
+  if (d_x)
+    boundary_kernel<<<(N + 255) / 256, 256, 0, ctx->stream>>>(
+        b.X32 + (size_t)t * N, b.COL + (size_t)t * N, map, N, (float4*)d_x,
+        side == 0 ? d_col : nullptr);
+  LAUNCHED(ctx);
+  CU(cudaGetLastError());
+  if (root_lnc) {
+    CU(cudaMemcpyAsync(ctx->h_lnc, st.blnc[st.cur], 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    *root_lnc = ctx->h_lnc[0];
+  }
+  return DSMC_OK;
+}
+
+int dsmc_window_remap(dsmc_ctx* ctx, int side, const uint32_t* d_idx) {
+  if (!ctx || !d_idx) return DSMC_E_INVALID_ARGUMENT;
+  WindowState& st = window_state(ctx);
+  if (!st.valid) return set_err(ctx, DSMC_E_LOGIC, "no window run on this context");
+  const int N = st.b.N;
+  uint32_t* map = st.maps[2 * st.cur + (side == 0 ? 0 : 1)];
+  void* p;
+  CU(ctx->arena.get("RTMP", (size_t)N * 4, &p));
+  remap_kernel<<<(N + 255) / 256, 256, 0, ctx->stream>>>(map, d_idx, (uint32_t*)p, N);
+  LAUNCHED(ctx);
+  CU(cudaMemcpyAsync(map, p, (size_t)N * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  return DSMC_OK;
+}
+
+int dsmc_window_finish(dsmc_ctx* ctx, const uint32_t* d_root_map, double* d_mean, double* d_cov) {
+  if (!ctx) return DSMC_E_INVALID_ARGUMENT;
+  WindowState& st = window_state(ctx);
+  if (!st.valid) return set_err(ctx, DSMC_E_LOGIC, "no window run on this context");
+  const Bufs& b = st.b;
+  const int K = b.K, N = b.N, d = b.d, B = b.B;
+  std::vector<int> nbs{K};
+  while (nbs.back() > 1) nbs.push_back((nbs.back() + 1) / 2);
+  std::vector<size_t> cursors(nbs.size() + 1, 0);
+  for (size_t l = 1; l + 1 <= nbs.size() - 1; ++l) cursors[l + 1] = cursors[l] + nbs[l - 1] / 2;
+  uint32_t* Mb[2] = {st.maps[0], st.maps[2]};
+  int mcur = 0;
+  bool root = true;
+  for (int l = st.levels; l >= 2; --l) {
+    td_kernel<<<dim3((N + 255) / 256, nbs[l], B), 256, 0, ctx->stream>>>(
+        b, l, cursors[l], nbs[l], nbs[l - 1], Mb[mcur], Mb[1 - mcur], root ? 1 : 0, d_root_map);
+    LAUNCHED(ctx);
+    root = false;
+    mcur = 1 - mcur;
+  }
+  const uint32_t* M1 = Mb[mcur];
+  const int r1 = root ? 1 : 0;
+  switch (d) {
+    case 1: gather32_kernel<1><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, nullptr, d_mean, d_cov, d_root_map); break;
+    case 2: gather32_kernel<2><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, nullptr, d_mean, d_cov, d_root_map); break;
+    case 3: gather32_kernel<3><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, nullptr, d_mean, d_cov, d_root_map); break;
+    default: gather32_kernel<4><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, nullptr, d_mean, d_cov, d_root_map); break;
+  }
+  LAUNCHED(ctx);
+  CU(cudaGetLastError());
+  st.valid = false;  // the maps were consumed by the composition
+  return DSMC_OK;
+}
+
+int dsmc_cross_combine(dsmc_ctx* ctx, const dsmc_model_handle* hc, const dsmc_window_opts* wo,
+                       int cut, int level, long long node, const void* d_xl, const void* d_xr,
+                       const float* d_colr, double lnc_l, double lnc_r, uint32_t* d_l,
+                       uint32_t* d_r, double* lnc_out) {
+  if (!ctx || !hc || !wo || !d_xl || !d_xr || !d_colr || !d_l || !d_r)
+    return DSMC_E_INVALID_ARGUMENT;
+  auto* h = const_cast<dsmc_model_handle*>(hc);
+  if (cut < 1 || cut >= h->K) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "cross_combine: bad cut");
+  if (wo->resampler != DSMC_MULTINOMIAL && wo->resampler != DSMC_SYSTEMATIC)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "cross_combine: dense resamplers only");
+  const int N = (int)wo->n_particles, d = h->d;
+  Arena& A = ctx->arena;
+  auto s = ctx->stream;
+  void* p;
+  // a two-leaf window [cut-1, cut] whose "leaves" are the two boundary slabs
+  Bufs b{};
+  b.K = 2;
+  b.T = 1;
+  b.N = N;
+  b.d = d;
+  b.B = 1;
+  b.cap = 1;
+  b.t0 = cut - 1;
+  b.Kt = h->K;
+  b.models = h->models_dev;
+  b.tc = h->tc;
+  b.bounded = h->bounded;
+  CU(A.get("CX32", 2 * (size_t)N * sizeof(float4), &p));
+  b.X32 = (float4*)p;
+  CU(cudaMemcpyAsync(b.X32, d_xl, (size_t)N * sizeof(float4), cudaMemcpyDeviceToDevice, s));
+  CU(cudaMemcpyAsync(b.X32 + N, d_xr, (size_t)N * sizeof(float4), cudaMemcpyDeviceToDevice, s));
+  CU(A.get("CCOL", 2 * (size_t)N * sizeof(float), &p));
+  b.COL = (float*)p;
+  CU(cudaMemcpyAsync(b.COL + N, d_colr, (size_t)N * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  CU(A.get("CMISC", 256, &p));
+  double* lnc = (double*)p;  // [0..1] leaf lnc, [2] new block lnc
+  uint8_t* uni = (uint8_t*)p + 64;
+  uint64_t* seed = (uint64_t*)((char*)p + 128);
+  ErrFlag* err = (ErrFlag*)((char*)p + 160);
+  const double hl[2] = {lnc_l, lnc_r};
+  const uint8_t hu[2] = {1, 1};
+  CU(cudaMemcpyAsync(lnc, hl, 16, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(uni, hu, 2, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(seed, &wo->seed, 8, cudaMemcpyHostToDevice, s));
+  CU(cudaMemsetAsync(err, 0, sizeof(ErrFlag), s));
+  b.LNC = lnc;
+  b.UNI = uni;
+  b.LWMAX = lnc;  // unused (uniform sides)
+  b.seeds = seed;
+  b.err = err;
+  CU(A.get("CPL", (size_t)N * 4, &p));
+  b.PL = (uint32_t*)p;
+  CU(A.get("CPR", (size_t)N * 4, &p));
+  b.PR = (uint32_t*)p;
+  CU(A.get("CLMW", 8, &p));
+  b.LMW = (double*)p;
+  CU(A.get("CMAPS", 2 * (size_t)N * 4, &p));
+  const int nsubp = ((N + kChunk - 1) / kChunk) * (kChunk / kSub);
+  const size_t ws_comb = ((size_t)N * nsubp + 1) / 2;
+  LevelArgs la{};
+  la.level = 1;
+  la.np = 1;
+  la.nb_prev = 2;
+  la.k0 = 0;
+  la.cursor = 0;
+  la.first_next = (uint32_t*)p;
+  la.last_next = (uint32_t*)p + N;
+  la.blnc_next = lnc + 2;
+  la.n_out = N;
+  la.key_level = level;
+  la.node_off = node;
+  CU(A.get("CWS", ws_comb * 8, &p));
+  la.ws = (double*)p;
+  la.ws_comb = ws_comb;
+  const int sys = wo->resampler == DSMC_SYSTEMATIC;
+  const bool keep = ctx->time_kernels;
+  ctx->time_kernels = false;
+  int rc = d == 1 ? launch_c32<1>(ctx, b, la, 1, sys)
+         : d == 2 ? launch_c32<2>(ctx, b, la, 1, sys)
+         : d == 3 ? launch_c32<3>(ctx, b, la, 1, sys)
+                  : launch_c32<4>(ctx, b, la, 1, sys);
+  ctx->time_kernels = keep;
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(d_l, b.PL, (size_t)N * 4, cudaMemcpyDeviceToDevice, s));
+  CU(cudaMemcpyAsync(d_r, b.PR, (size_t)N * 4, cudaMemcpyDeviceToDevice, s));
+  ErrFlag e;
+  CU(cudaMemcpyAsync(&e, err, sizeof e, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(ctx->h_lnc, lnc + 2, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (e.code) return set_err(ctx, e.code, err_message(e, h->K));
+  if (lnc_out) *lnc_out = ctx->h_lnc[0];
+  return DSMC_OK;
+}
+
+}  // extern "C"

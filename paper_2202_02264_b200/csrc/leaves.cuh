@@ -10,6 +10,8 @@ namespace dsmc_dev {
 
 struct Bufs {
   int K, T, N, d, B, cap;  // cap: map capacity (blocks) per chain
+  int t0;  // global time of local leaf 0 (time-sharded windows; 0 otherwise)
+  int Kt;  // leaves of the whole model (TimeConst stride per chain)
   const DevModel* models;  // [B]
   const uint64_t* seeds;   // [B]
   const TimeConst* tc;     // [B][K]
@@ -61,7 +63,7 @@ __global__ void leaf64_kernel(Bufs b, const double* inj_x, const double* inj_lw)
   const int t = blockIdx.y, ch = blockIdx.z;
   if (n >= b.N) return;
   const DevModel& M = b.models[ch];
-  const TimeConst& tc = b.tc[(size_t)ch * b.K + t];
+  const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + t];
   const int d = b.d;
   double x[4] = {0, 0, 0, 0};
   const size_t off = ((size_t)ch * b.K + t) * b.N + n;
@@ -179,9 +181,10 @@ __global__ void leafnorm64_kernel(Bufs b) {
 __global__ void leaf32_kernel(Bufs b, double* raw0) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = blockIdx.y, ch = blockIdx.z;
+  const int gt = b.t0 + t;  // global time (stream key, model data)
   if (n >= b.N) return;
   const DevModel& M = b.models[ch];
-  const TimeConst& tc = b.tc[(size_t)ch * b.K + t];
+  const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + t];
   const int d = b.d;
   const size_t off = ((size_t)ch * b.K + t) * b.N + n;
   float z[4] = {0.f, 0.f, 0.f, 0.f};
@@ -192,7 +195,7 @@ __global__ void leaf32_kernel(Bufs b, double* raw0) {
   if (is_star) {
     for (int k = 0; k < d; ++k) xstar[k] = b.star[((size_t)ch * b.K + t) * d + k];
   } else {
-    const StreamId id = stream_id(b.seeds[ch], 0, leaf_node(t, b.conditional, b.sweep),
+    const StreamId id = stream_id(b.seeds[ch], 0, leaf_node(gt, b.conditional, b.sweep),
                                   DSMC_ROLE_LEAF_PROPOSAL, 0);
     const uint64_t p = b.conditional ? n - 1 : n;
     // d normals from ceil(d/2)... counter-addressed Box-Muller pairs
@@ -249,13 +252,13 @@ __global__ void leaf32_kernel(Bufs b, double* raw0) {
   xs.w = xv[3];
   b.X32[off] = xs;
   b.COL[off] = col;
-  if (n == 0 && t > 0) {  // q_t = nu_t: uniform leaf, lse = log N exactly
+  if (n == 0 && gt > 0) {  // q_t = nu_t: uniform leaf, lse = log N exactly
     const size_t o = (size_t)ch * b.K + t;
     b.LNC[o] = 0.0;
     b.UNI[o] = 1;
     b.LWMAX[o] = -log((double)b.N);
   }
-  if (t == 0) {
+  if (gt == 0) {
     // leaf-0 raw weight h0 + P0 - q0 in FP64
     double x[4];
     for (int k = 0; k < d; ++k) x[k] = is_star ? xstar[k] : (double)xv[k] + tc.pm[k];

@@ -62,6 +62,12 @@ def load_library():
         "dsmc_conditional_sweep": (i, [vp, C.POINTER(abi.ModelDesc), i, dp, u64p,
                                        C.POINTER(abi.CondOpts), u32, dp, u8p, dp, u64p]),
         "dsmc_kalman_smooth": (i, [C.POINTER(abi.ModelDesc), dp, dp, dp]),
+        "dsmc_window_run": (i, [vp, vp, C.POINTER(abi.WindowOpts)]),
+        "dsmc_window_boundary": (i, [vp, i, vp, vp, dp]),
+        "dsmc_cross_combine": (i, [vp, vp, C.POINTER(abi.WindowOpts), i, i, C.c_longlong, vp, vp,
+                                   vp, C.c_double, C.c_double, vp, vp, dp]),
+        "dsmc_window_remap": (i, [vp, i, vp]),
+        "dsmc_window_finish": (i, [vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -219,6 +225,34 @@ class Engine:
         ms = (C.c_double * 6)()
         n = self.lib.dsmc_last_timings(self.ctx, ms, 6)
         return list(ms[:n])
+
+    # ------------------------------------------------- time-sharded stages
+    # Device buffers are passed as raw pointers (e.g. torch tensor data_ptr()
+    # on the engine's stream); see paper_2202_02264_b200/sharded.py.
+    def window_run(self, handle, n_particles, t0, length, seed, resampler=abi.MULTINOMIAL,
+                   mh_steps=16):
+        o = abi.WindowOpts(n_particles, resampler, mh_steps, seed, t0, length)
+        self._check(self.lib.dsmc_window_run(self.ctx, handle, C.byref(o)))
+
+    def window_boundary(self, side, d_states, d_col=None):
+        lnc = C.c_double()
+        self._check(self.lib.dsmc_window_boundary(self.ctx, side, d_states, d_col, C.byref(lnc)))
+        return lnc.value
+
+    def cross_combine(self, handle, n_particles, seed, cut, level, node, d_xl, d_xr, d_colr,
+                      lnc_l, lnc_r, d_l, d_r, resampler=abi.MULTINOMIAL):
+        o = abi.WindowOpts(n_particles, resampler, 16, seed, 0, 2)
+        out = C.c_double()
+        self._check(self.lib.dsmc_cross_combine(self.ctx, handle, C.byref(o), cut, level, node,
+                                                d_xl, d_xr, d_colr, lnc_l, lnc_r, d_l, d_r,
+                                                C.byref(out)))
+        return out.value
+
+    def window_remap(self, side, d_idx):
+        self._check(self.lib.dsmc_window_remap(self.ctx, side, d_idx))
+
+    def window_finish(self, d_root_map, d_mean, d_cov):
+        self._check(self.lib.dsmc_window_finish(self.ctx, d_root_map, d_mean, d_cov))
 
     # ------------------------------------------------------- conditional
     def conditional_sweep(self, models, refs, seeds, n_particles, sweep,

@@ -1,0 +1,100 @@
+"""Time-sharded (multi-GPU) protocol: a P-rank run must reproduce the 1-rank
+run exactly, because every combine keeps its global stream key.
+
+CPU: the protocol over gloo with world_size 2 (two processes) and with
+in-process virtual ranks, on the CPU test backend.
+GPU: virtual ranks (one engine context each) on one GPU against the plain
+single-GPU dsmc_smooth of the same model and seed, bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from paper_2202_02264_b200 import abi, models
+from paper_2202_02264_b200.sharded import TorchComm, sharded_smooth
+
+K, N, SEED = 64, 24, 17
+
+
+def _model():
+    return models.lgssm_check(K - 1)
+
+
+def _cpu_run(P, ranks=None, comm=None):
+    from oracle.py import Oracle
+    from tests.sharded_cpu import CpuBackend
+    m, O = _model(), Oracle()
+    ranks = range(P) if ranks is None else ranks
+    backends = {g: CpuBackend(m, N, SEED, O) for g in ranks}
+    out, lz = sharded_smooth(backends, comm, K, N, P)
+    mean = torch.cat([out[g][0] for g in sorted(out)])
+    return mean.numpy(), lz
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_virtual_ranks_reproduce_single_rank_cpu(P):
+    m1, lz1 = _cpu_run(1)
+    mP, lzP = _cpu_run(P)
+    assert np.array_equal(m1, mP)
+    assert lz1 == lzP
+
+
+def _gloo_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mean, lz = _cpu_run(world, ranks=[rank], comm=TorchComm())
+        q.put((rank, mean, lz))
+    finally:
+        torch.distributed.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_world_size_2_reproduces_single_rank(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort(key=lambda x: x[0])
+    mean = np.concatenate([r[1] for r in res])
+    m1, lz1 = _cpu_run(1)
+    assert np.array_equal(mean, m1)
+    assert all(r[2] == lz1 for r in res)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 4])
+def test_virtual_ranks_on_gpu_match_single_gpu(P):
+    from paper_2202_02264_b200.dsmc import Engine
+    from paper_2202_02264_b200.sharded import GpuBackend
+    KK, NN = 256, 128
+    m = models.cv_tracking(KK - 1)
+    ref_eng = Engine(0)
+    ref = ref_eng.smooth(m, NN, abi.MULTINOMIAL, seed=SEED, precision=abi.FP32)
+    engines = {g: Engine(0) for g in range(P)}
+    backends = {g: GpuBackend(e, e.upload(m), NN, m.d, SEED) for g, e in engines.items()}
+    out, lz = sharded_smooth(backends, None, KK, NN, P)
+    for b in backends.values():
+        b.sync()
+    mean = torch.cat([out[g][0] for g in range(P)]).cpu().numpy()
+    cov = torch.cat([out[g][1] for g in range(P)]).cpu().numpy()
+    assert np.array_equal(mean, ref["mean"])
+    assert np.array_equal(cov, ref["cov"])
+    assert lz == ref["log_norm_const"]
