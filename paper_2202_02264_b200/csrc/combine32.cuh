@@ -166,6 +166,49 @@ __device__ __forceinline__ void row_sub(const float2 (&y2)[D][kCPL / 2],
   s_out = sm;
 }
 
+// Fast-path row: sum over this lane's 16 columns of 2^(A'_j + u.y_j) with no
+// max subtraction. A'_j = A_j - cmax_s where cmax_s bounds col2 over the
+// sub-block, so the argument equals w_ij - lw2_i - cmax_s + |nu_i|^2 and
+// w_ij - lw2_i <= col2_j (the transition term -|y - nu|^2 is <= 0): the sum
+// only leaves [2^-60, 2^100] for rows far from every column (the caller then
+// recomputes them with the exact max).
+// The argument is also <= |nu_i|^2, so rows with |nu_i|^2 > 100 (a few %)
+// run the SHIFT variant with c_i = |nu_i|^2 - 100 subtracted (one FADD2 per
+// two pairs), which keeps every exponent <= 100.
+template <int D, bool SHIFT>
+__device__ __forceinline__ float row_sum_fast(const float2 (&y2)[D][kCPL / 2],
+                                              const float2 (&A2)[kCPL / 2],
+                                              const float* u, float c) {
+  float2 uu[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) uu[q] = make_float2(u[q], u[q]);
+  const float2 nc = make_float2(-c, -c);
+  float2 e[kCPL / 2];
+#pragma unroll
+  for (int c2 = 0; c2 < kCPL / 2; ++c2) {
+    float2 acc = SHIFT ? __fadd2_rn(A2[c2], nc) : A2[c2];
+#pragma unroll
+    for (int q = 0; q < D; ++q) acc = __ffma2_rn(uu[q], y2[q][c2], acc);
+    e[c2] = make_float2(ex2(acc.x), ex2(acc.y));
+  }
+  const float2 s01 = __fadd2_rn(__fadd2_rn(e[0], e[1]), __fadd2_rn(e[2], e[3]));
+  const float2 s23 = __fadd2_rn(__fadd2_rn(e[4], e[5]), __fadd2_rn(e[6], e[7]));
+  const float2 s2 = __fadd2_rn(s01, s23);
+  return s2.x + s2.y;
+}
+
+// 4 rows x 4 lanes transpose-reduce: lane q (of a 4-lane sub-block group)
+// returns the 4-lane total of row q (3 SHFL instead of 8).
+__device__ __forceinline__ float quad_transpose_sum(const float (&s4)[4], int q4) {
+  const bool b1 = q4 & 2, b0 = q4 & 1;
+  float k0 = b1 ? s4[2] : s4[0], k1 = b1 ? s4[3] : s4[1];
+  const float o0 = b1 ? s4[0] : s4[2], o1 = b1 ? s4[1] : s4[3];
+  k0 += __shfl_xor_sync(~0u, o0, 2);
+  k1 += __shfl_xor_sync(~0u, o1, 2);
+  const float keep = b0 ? k1 : k0, send = b0 ? k0 : k1;
+  return keep + __shfl_xor_sync(~0u, send, 1);
+}
+
 // Pass 1. Grid (row tiles, combines, chains); la.rows_per_cta rows per CTA
 // (a multiple of 32, chosen per level so the grid fills the GPU). Warps take
 // (512-column chunk, row slice) items; rows go 4 at a time so that each lane
@@ -177,6 +220,7 @@ __global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
   const int RT = la.rows_per_cta;
   float* s_u = sm32;            // [RT][D]
   float* s_B = sm32 + RT * D;   // [RT]
+  float* s_c = s_B + RT;        // [RT] fast-path shift c_i (0 for most rows)
   const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
   const int N = b.N;
   Side L, R;
@@ -203,6 +247,10 @@ __global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
 #pragma unroll
     for (int q = 0; q < D; ++q) s_u[r * D + q] = u[q];
     s_B[r] = Bv;
+    float nn = 0.f;
+#pragma unroll
+    for (int q = 0; q < D; ++q) nn = fmaf(0.5f * u[q], 0.5f * u[q], nn);
+    s_c[r] = nn > 100.f ? nn - 100.f : 0.f;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -215,6 +263,7 @@ __global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
     const int chunk = it % nch, slice = it / nch;
     float2 y2[D][kCPL / 2];
     float2 A2[kCPL / 2];
+    float cm = -CUDART_INF_F;
 #pragma unroll
     for (int c2 = 0; c2 < kCPL / 2; ++c2) {
       float yv[2][4], Av[2];
@@ -223,7 +272,9 @@ __global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
         const int j = chunk * kChunk + lane * kCPL + 2 * c2 + h;
         if (j < N) {
           const uint32_t p = map_first(b, la, ch, R, j);
-          col32<D>(cc, XR[p], CR[p], yv[h], Av[h]);
+          const float cv = CR[p];
+          col32<D>(cc, XR[p], cv, yv[h], Av[h]);
+          cm = fmaxf(cm, cv);
         } else {
 #pragma unroll
           for (int q = 0; q < D; ++q) yv[h][q] = 0.f;
@@ -235,23 +286,59 @@ __global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
       A2[c2] = make_float2(Av[0], Av[1]);
     }
     const int sub = chunk * (kChunk / kSub) + (lane >> 2);
+    // column bound of the sub-block: cmax = max_j col2_j (4-lane max), folded
+    // into A so the fast rows need no max (row_sum_fast)
+    cm = fmaxf(cm, __shfl_xor_sync(~0u, cm, 1));
+    cm = fmaxf(cm, __shfl_xor_sync(~0u, cm, 2));
+    const bool live = cm > -CUDART_INF_F;
+#pragma unroll
+    for (int c2 = 0; c2 < kCPL / 2; ++c2)
+      A2[c2] = live ? make_float2(A2[c2].x - cm, A2[c2].y - cm)
+                    : make_float2(-CUDART_INF_F, -CUDART_INF_F);
     // rows slice, slice+S, ... taken 4 at a time (RT is a multiple of 4*S;
     // padded rows have B = -inf and are never stored)
     for (int base = slice; base < nrows; base += 4 * S) {
-      float m4[4], s4[4];
+      float s4[4], c4[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int r = base + j * S;
-        float u[D];
+      for (int j = 0; j < 4; ++j) c4[j] = s_c[base + j * S];
+      if (fmaxf(fmaxf(c4[0], c4[1]), fmaxf(c4[2], c4[3])) == 0.f) {  // warp-uniform
 #pragma unroll
-        for (int q = 0; q < D; ++q) u[q] = s_u[r * D + q];
-        row_sub<D>(y2, A2, u, m4[j], s4[j]);
+        for (int j = 0; j < 4; ++j) {
+          const int r = base + j * S;
+          float u[D];
+#pragma unroll
+          for (int q = 0; q < D; ++q) u[q] = s_u[r * D + q];
+          s4[j] = row_sum_fast<D, false>(y2, A2, u, 0.f);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = base + j * S;
+          float u[D];
+#pragma unroll
+          for (int q = 0; q < D; ++q) u[q] = s_u[r * D + q];
+          s4[j] = row_sum_fast<D, true>(y2, A2, u, c4[j]);
+        }
       }
       const int rq = base + q4 * S;
-      const float mq = q4 == 0 ? m4[0] : q4 == 1 ? m4[1] : q4 == 2 ? m4[2] : m4[3];
-      const float sq = q4 == 0 ? s4[0] : q4 == 1 ? s4[1] : q4 == 2 ? s4[2] : s4[3];
+      float sq = quad_transpose_sum(s4, q4);
+      float mq = q4 == 0 ? c4[0] : q4 == 1 ? c4[1] : q4 == 2 ? c4[2] : c4[3];
+      const bool odd = live && rq < nrows && !(sq >= 0x1p-60f && sq <= 0x1p120f);
+      if (__any_sync(~0u, odd)) {  // rare: exact per-sub-block max
+        float m4[4];
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+          const int r = base + j * S;
+          float u[D];
+#pragma unroll
+          for (int q = 0; q < D; ++q) u[q] = s_u[r * D + q];
+          row_sub<D>(y2, A2, u, m4[j], s4[j]);
+        }
+        mq = q4 == 0 ? m4[0] : q4 == 1 ? m4[1] : q4 == 2 ? m4[2] : m4[3];
+        sq = q4 == 0 ? s4[0] : q4 == 1 ? s4[1] : q4 == 2 ? s4[2] : s4[3];
+      }
       if (rq < nrows) {
-        const float Ls = sq > 0.f ? mq + lg2(sq) + s_B[rq] : -CUDART_INF_F;
+        const float Ls = sq > 0.f ? mq + lg2(sq) + cm + s_B[rq] : -CUDART_INF_F;
         ws[(size_t)(row0 + rq) * nsubp + sub] = Ls;
       }
     }
@@ -308,11 +395,15 @@ __global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
   const float* ws = reinterpret_cast<const float*>(la.ws) + (size_t)blockIdx.y * la.ws_comb * 2;
   // columns padded to a multiple of 64 (y = 0, A = -inf -> weight 0) so the
   // per-slot recomputation is branch-free
+  // Column j lives at j + j/64 (one pad entry per sub-block): the per-slot
+  // recompute loops read column 64 s + q of different sub-blocks s at the
+  // same q, which without the skew all map to the same banks.
   const int NP = (N + kSub - 1) / kSub * kSub;
+  const int NPS = NP + NP / kSub;
   double* S = smem;                                            // N
-  float4* ycol = reinterpret_cast<float4*>(S + ((N + 1) & ~1));  // NP, 16B aligned
-  float* Acol = reinterpret_cast<float*>(ycol + NP);            // NP
-  float* Lrow = Acol + NP;                                     // N
+  float4* ycol = reinterpret_cast<float4*>(S + ((N + 1) & ~1));  // NPS, 16B aligned
+  float* Acol = reinterpret_cast<float*>(ycol + NPS);           // NPS
+  float* Lrow = Acol + NPS;                                    // N
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float4* XR = b.X32 + ((size_t)ch * b.K + R.t) * N;
   const float* CR = b.COL + ((size_t)ch * b.K + R.t) * N;
@@ -322,8 +413,8 @@ __global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
       const uint32_t p = map_first(b, la, ch, R, j);
       col32<D>(cc, XR[p], CR[p], y, A);
     }
-    ycol[j] = make_float4(y[0], y[1], y[2], y[3]);
-    Acol[j] = A;
+    ycol[j + j / kSub] = make_float4(y[0], y[1], y[2], y[3]);
+    Acol[j + j / kSub] = A;
   }
   // row totals (log2): nsub independent loads per row, then LSE
   float gm = -CUDART_INF_F;
@@ -463,8 +554,8 @@ __global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
       // recompute the sub-block's 64 weights (pass-1 arithmetic; padding
       // columns give 0), branch-free walk to the first prefix above frac
       const int j0 = s * kSub;
-      const float4* yb = ycol + j0;
-      const float* ab = Acol + j0;
+      const float4* yb = ycol + j0 + s;
+      const float* ab = Acol + j0 + s;
       float c3 = 0.f;
       int jsel = kSub, lastj = 0;
 #pragma unroll 16

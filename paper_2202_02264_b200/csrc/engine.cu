@@ -294,21 +294,24 @@ int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
 
 template <int D>
 int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systematic) {
-  // Pass-1 row tile: as tall as possible (amortises the per-warp column load)
-  // while the grid still covers ~4 resident CTAs per SM.
-  const int target = 148 * 4;
+  // Pass-1 row tile: as tall as possible (each warp loads its 16 columns per
+  // lane once per tile, so tall tiles amortise the column load and the
+  // per-cut constants) while the grid still gives >= 6 waves of the 2
+  // resident CTAs per SM (bounds the tail of the last wave).
+  const int target = 148 * 2 * 6;
   const int N = b.N;
-  int rt = std::min(256, (N + 31) / 32 * 32);
+  int rt = std::min(1024, (N + 31) / 32 * 32);
   while (rt > 32 && (long)nk * b.B * ((N + rt - 1) / rt) < target) rt = std::max(32, rt / 2 / 32 * 32);
   la.rows_per_cta = rt;
   // Pass-2: split a combine's slots over several CTAs when combines are few.
   int sb = 1;
-  if ((long)nk * b.B < target / 2)
-    sb = std::max(1, std::min((la.n_out + 63) / 64, (int)((target / 2 + nk * b.B - 1) / (nk * b.B))));
+  const int target2 = 148 * 2;
+  if ((long)nk * b.B < target2)
+    sb = std::max(1, std::min((la.n_out + 63) / 64, (int)((target2 + nk * b.B - 1) / (nk * b.B))));
   la.slots_per_cta = (la.n_out + sb - 1) / sb;
-  const size_t sm1 = sizeof(float) * (size_t)rt * (D + 1);
+  const size_t sm1 = sizeof(float) * (size_t)rt * (D + 2);
   const size_t NP = (N + 63) / 64 * 64;
-  const size_t sm2 = sizeof(double) * (N + 1) + sizeof(float) * (NP * 5 + N);
+  const size_t sm2 = sizeof(double) * (N + 1) + sizeof(float) * ((NP + NP / 64) * 5 + N);
   static bool configured = false;
   if (!configured) {
     CU(cudaFuncSetAttribute(c32_sample<D>, cudaFuncAttributePreferredSharedMemoryCarveout,

@@ -198,16 +198,25 @@ __global__ void leaf32_kernel(Bufs b, double* raw0) {
     const StreamId id = stream_id(b.seeds[ch], 0, leaf_node(gt, b.conditional, b.sweep),
                                   DSMC_ROLE_LEAF_PROPOSAL, 0);
     const uint64_t p = b.conditional ? n - 1 : n;
-    // d normals from ceil(d/2)... counter-addressed Box-Muller pairs
+    // d normals, counter-addressed Box-Muller pairs (normal i uses u64s
+    // 2*(i/2) and 2*(i/2)+1, rng.cpp:74-86): one Philox block serves up to
+    // two pairs and one (r, theta) serves both normals of a pair
+    U64x4 blk;
+    uint64_t have = ~0ull;
+    float r = 0.f, s = 0.f, c = 0.f;
     for (int k = 0; k < d; ++k) {
       const uint64_t i = p * d + k;
-      const uint64_t q = 2 * (i >> 1);
-      const U64x4 blk = stream_block(id, q >> 2);
-      const float u1 = (float)u64_uniform_pos(blk.v[q & 3]);
-      const float u2 = (float)u64_uniform(blk.v[(q & 3) + 1]);
-      const float r = sqrtf(-2.0f * __logf(u1));
-      float s, c;
-      sincospif(2.0f * u2, &s, &c);
+      if (k == 0 || !(i & 1)) {
+        const uint64_t q = 2 * (i >> 1);
+        if ((q >> 2) != have) {
+          blk = stream_block(id, q >> 2);
+          have = q >> 2;
+        }
+        const float u1 = (float)u64_uniform_pos(blk.v[q & 3]);
+        const float u2 = (float)u64_uniform(blk.v[(q & 3) + 1]);
+        r = sqrtf(-2.0f * __logf(u1));
+        sincospif(2.0f * u2, &s, &c);
+      }
       z[k] = (i & 1) ? r * s : r * c;
     }
   }
