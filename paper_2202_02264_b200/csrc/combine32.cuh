@@ -209,6 +209,25 @@ __device__ __forceinline__ float quad_transpose_sum(const float (&s4)[4], int q4
   return keep + __shfl_xor_sync(~0u, send, 1);
 }
 
+// Per-combine data pass 1 hands to the sampler (la.aux, la.aux_comb floats
+// per combine of the chunk): whitened columns y_j / A_j and rows u_i / B_i,
+// computed once by pass 1 instead of being re-gathered through the block maps.
+struct Aux32 {
+  float4* y;  // [N] column y_j (zero-padded to 4)
+  float4* u;  // [N] row u_i = 2 nu_i
+  float* A;   // [N] column A_j
+  float* B;   // [N] row B_i
+};
+__device__ __forceinline__ Aux32 aux32(const LevelArgs& la, int comb, int N) {
+  float* base = la.aux + (size_t)comb * la.aux_comb;
+  Aux32 a;
+  a.y = reinterpret_cast<float4*>(base);
+  a.u = reinterpret_cast<float4*>(base + 4 * (size_t)N);
+  a.A = base + 8 * (size_t)N;
+  a.B = base + 9 * (size_t)N;
+  return a;
+}
+
 // Pass 1. Grid (row tiles, combines, chains); la.rows_per_cta rows per CTA
 // (a multiple of 32, chosen per level so the grid fills the GPU). Warps take
 // (512-column chunk, row slice) items; rows go 4 at a time so that each lane
@@ -231,9 +250,12 @@ __global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
   load_cut32<D>(tc, cc);
   const int nch = (N + kChunk - 1) / kChunk;
   const int nsubp = nch * (kChunk / kSub);
-  float* ws = reinterpret_cast<float*>(la.ws) + (size_t)blockIdx.y * la.ws_comb * 2;
+  // per (chain, combine of the chunk) workspace
+  const size_t cslot = (size_t)blockIdx.z * gridDim.y + blockIdx.y;
+  float* ws = reinterpret_cast<float*>(la.ws) + cslot * la.ws_comb * 2;
   const int row0 = blockIdx.x * RT;
   const int nrows = min(RT, N - row0);
+  const Aux32 ax = aux32(la, cslot, N);
   const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
   const float4* XL = b.X32 + ((size_t)ch * b.K + L.t) * N;
   for (int r = threadIdx.x; r < RT; r += blockDim.x) {
@@ -243,6 +265,8 @@ __global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
       const uint32_t p = map_last(b, la, ch, L, i);
       const float lw2 = lnonuni ? b.LW32[(size_t)ch * N + i] : 0.f;
       row32<D>(cc, XL[p], lw2, u, Bv);
+      ax.u[i] = make_float4(u[0], u[1], u[2], u[3]);
+      ax.B[i] = Bv;
     }
 #pragma unroll
     for (int q = 0; q < D; ++q) s_u[r * D + q] = u[q];
@@ -259,6 +283,15 @@ __global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
   const float4* XR = b.X32 + ((size_t)ch * b.K + R.t) * N;
   const float* CR = b.COL + ((size_t)ch * b.K + R.t) * N;
   const int q4 = lane & 3;
+  if (blockIdx.x == 0) {  // hand the combine's columns to the sampler
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+      const uint32_t p = map_first(b, la, ch, R, j);
+      float y[4] = {0.f, 0.f, 0.f, 0.f}, A;
+      col32<D>(cc, XR[p], CR[p], y, A);
+      ax.y[j] = make_float4(y[0], y[1], y[2], y[3]);
+      ax.A[j] = A;
+    }
+  }
   for (int it = warp; it < items; it += 8) {
     const int chunk = it % nch, slice = it / nch;
     float2 y2[D][kCPL / 2];
@@ -275,6 +308,7 @@ __global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
           const float cv = CR[p];
           col32<D>(cc, XR[p], cv, yv[h], Av[h]);
           cm = fmaxf(cm, cv);
+
         } else {
 #pragma unroll
           for (int q = 0; q < D; ++q) yv[h][q] = 0.f;
@@ -369,11 +403,11 @@ __device__ inline double block_scan_incl(double v, double* sh) {
 }
 
 // Pass 2. Grid (slot blocks, combines, chains), 256 threads. Every slot block
-// rebuilds the combine's row CDF (N row totals from the sub-block sums, read
-// with independent vector loads) and samples its slice of the n_out slots:
-// binary search over the row CDF in shared memory, a walk over the row's
-// sub-block sums held in registers, and a recomputation of <= 64 weights of
-// the chosen sub-block with pass 1's FP32 operations.
+// rebuilds the combine's row CDF (N row log-totals from the sub-block sums,
+// vector loads + online LSE) and samples its slice of the n_out slots: binary
+// search over the row CDF in shared memory, a walk over the row's sub-block
+// sums, and a recomputation of the chosen sub-block's <= 64 weights with
+// pass 1's FP32 pair arithmetic (two columns per FFMA2 / FADD2).
 template <int D>
 __global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
                                                      int systematic) {
@@ -386,15 +420,12 @@ __global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
   Side L, R;
   CombineGeom g;
   sides(b, la, k, L, R, g);
-  const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + g.c];
-  CutConst32 cc;
-  load_cut32<D>(tc, cc);
   const int nch = (N + kChunk - 1) / kChunk;
   const int nsubp = nch * (kChunk / kSub);
   const int nsub = (N + kSub - 1) / kSub;
-  const float* ws = reinterpret_cast<const float*>(la.ws) + (size_t)blockIdx.y * la.ws_comb * 2;
-  // columns padded to a multiple of 64 (y = 0, A = -inf -> weight 0) so the
-  // per-slot recomputation is branch-free
+  const size_t cslot = (size_t)blockIdx.z * gridDim.y + blockIdx.y;
+  const float* ws = reinterpret_cast<const float*>(la.ws) + cslot * la.ws_comb * 2;
+  const Aux32 ax = aux32(la, cslot, N);
   // Column j lives at j + j/64 (one pad entry per sub-block): the per-slot
   // recompute loops read column 64 s + q of different sub-blocks s at the
   // same q, which without the skew all map to the same banks.
@@ -405,35 +436,45 @@ __global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
   float* Acol = reinterpret_cast<float*>(ycol + NPS);           // NPS
   float* Lrow = Acol + NPS;                                    // N
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const float4* XR = b.X32 + ((size_t)ch * b.K + R.t) * N;
-  const float* CR = b.COL + ((size_t)ch * b.K + R.t) * N;
   for (int j = tid; j < NP; j += blockDim.x) {
-    float y[4] = {0, 0, 0, 0}, A = -CUDART_INF_F;
+    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+    float A = -CUDART_INF_F;
     if (j < N) {
-      const uint32_t p = map_first(b, la, ch, R, j);
-      col32<D>(cc, XR[p], CR[p], y, A);
+      y = ax.y[j];
+      A = ax.A[j];
     }
-    ycol[j + j / kSub] = make_float4(y[0], y[1], y[2], y[3]);
+    ycol[j + j / kSub] = y;
     Acol[j + j / kSub] = A;
   }
-  // row totals (log2): nsub independent loads per row, then LSE
+  // row log2-totals: online LSE over the row's sub-block sums, 16 at a time
+  // (pass 1 writes all nsubp entries; padding is -inf)
   float gm = -CUDART_INF_F;
   for (int i = tid; i < N; i += blockDim.x) {
-    const float* w = ws + (size_t)i * nsubp;
-    float m = -CUDART_INF_F;
-    for (int s0 = 0; s0 < nsub; s0 += 16) {
+    const float4* w4 = reinterpret_cast<const float4*>(ws + (size_t)i * nsubp);
+    float m = -CUDART_INF_F, acc = 0.f;
+    for (int s0 = 0; s0 < nsubp; s0 += 16) {
       float v[16];
+      const int nq = min(4, (nsubp - s0) >> 2);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = (s0 + q < nsub) ? w[s0 + q] : -CUDART_INF_F;
+      for (int q = 0; q < 4; ++q) {
+        const float4 t4 = q < nq ? w4[(s0 >> 2) + q]
+                                 : make_float4(-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F);
+        v[4 * q] = t4.x;
+        v[4 * q + 1] = t4.y;
+        v[4 * q + 2] = t4.z;
+        v[4 * q + 3] = t4.w;
+      }
+      float cm = fmax3(fmax3(v[0], v[1], v[2]), fmax3(v[3], v[4], v[5]), fmax3(v[6], v[7], v[8]));
+      cm = fmax3(cm, fmax3(v[9], v[10], v[11]), fmax3(v[12], v[13], fmaxf(v[14], v[15])));
+      if (cm == -CUDART_INF_F) continue;
+      if (cm > m) {
+        acc = m == -CUDART_INF_F ? 0.f : acc * ex2(m - cm);
+        m = cm;
+      }
 #pragma unroll
-      for (int q = 0; q < 16; ++q) m = fmaxf(m, v[q]);
+      for (int q = 0; q < 16; ++q) acc += ex2(v[q] - m);
     }
-    float L2 = -CUDART_INF_F;
-    if (m != -CUDART_INF_F) {
-      float acc = 0.f;
-      for (int s = 0; s < nsub; ++s) acc += ex2(w[s] - m);
-      L2 = m + lg2(acc);
-    }
+    const float L2 = m == -CUDART_INF_F ? -CUDART_INF_F : m + lg2(acc);
     Lrow[i] = L2;
     gm = fmaxf(gm, L2);
   }
@@ -465,8 +506,6 @@ __global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
   const double total = S[N - 1];
   const size_t gidx = (size_t)ch * b.T + la.cursor + k;
   if (tid == 0 && sb == 0) b.LMW[gidx] = ((double)G + log2(total)) * kLn2;
-  const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
-  const float4* XL = b.X32 + ((size_t)ch * b.K + L.t) * N;
   const int off = b.conditional ? 1 : 0;
   const uint64_t node = b.conditional
                             ? (static_cast<uint64_t>(static_cast<uint32_t>(k + la.node_off)) |
@@ -502,6 +541,8 @@ __global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
       const double before = i > 0 ? S[i - 1] : 0.0;
       while (i > 0 && !(Lrow[i] > -CUDART_INF_F)) --i;
       const float Li = Lrow[i];
+      const float4 urow = ax.u[i];
+      const float Brow = ax.B[i];
       const float local0 = (float)((pt - before) / (double)ex2(Li - G));
       const float local = local0 >= 0.f ? local0 : 0.f;
       // sub-block walk over the row's sub-block sums (relative to the row
@@ -546,27 +587,39 @@ __global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
       }
       float frac = wsel > 0.f ? (local - before_s) / wsel : 0.f;
       frac = fminf(fmaxf(frac, 0.f), 1.f);
-      const uint32_t p = map_last(b, la, ch, L, i);
-      const float lw2 = lnonuni ? b.LW32[(size_t)ch * N + i] : 0.f;
-      float u[4] = {0, 0, 0, 0}, Bv;
-      row32<D>(cc, XL[p], lw2, u, Bv);
-      const float shift = Ls_sel - Bv;
-      // recompute the sub-block's 64 weights (pass-1 arithmetic; padding
-      // columns give 0), branch-free walk to the first prefix above frac
+      // recompute the sub-block's 64 weights (pass-1 pair arithmetic, two
+      // columns per packed op; padding columns give 0): jsel = number of
+      // prefix sums <= frac (the first prefix above frac), lastj = last
+      // positive weight
+      const float shift = Ls_sel - Brow;
       const int j0 = s * kSub;
       const float4* yb = ycol + j0 + s;
-      const float* ab = Acol + j0 + s;
+      const float2* ab = reinterpret_cast<const float2*>(Acol + j0 + s);
+      const float ur[4] = {urow.x, urow.y, urow.z, urow.w};
+      float2 uu[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) uu[q] = make_float2(ur[q], ur[q]);
+      const float2 nsh = make_float2(-shift, -shift);
       float c3 = 0.f;
-      int jsel = kSub, lastj = 0;
-#pragma unroll 16
-      for (int q = 0; q < kSub; ++q) {
-        const float4 yv = yb[q];
-        const float yy[4] = {yv.x, yv.y, yv.z, yv.w};
-        const float e = ex2(pair32<D>(u, yy, ab[q]) - shift);
-        c3 += e;
-        lastj = e > 0.f ? q : lastj;
-        jsel = (frac < c3 && q < jsel) ? q : jsel;
+      int cnt = 0, lastj = 0;
+#pragma unroll 8
+      for (int q = 0; q < kSub; q += 2) {
+        const float4 ya = yb[q], yc = yb[q + 1];
+        const float2 a2 = (s & 1) ? make_float2(Acol[j0 + s + q], Acol[j0 + s + q + 1]) : ab[q >> 1];
+        float2 t = __fadd2_rn(a2, nsh);
+        t = __ffma2_rn(uu[0], make_float2(ya.x, yc.x), t);
+        if (D > 1) t = __ffma2_rn(uu[1], make_float2(ya.y, yc.y), t);
+        if (D > 2) t = __ffma2_rn(uu[2], make_float2(ya.z, yc.z), t);
+        if (D > 3) t = __ffma2_rn(uu[3], make_float2(ya.w, yc.w), t);
+        const float e0 = ex2(t.x), e1 = ex2(t.y);
+        c3 += e0;
+        cnt += c3 <= frac;
+        c3 += e1;
+        cnt += c3 <= frac;
+        lastj = e0 > 0.f ? q : lastj;
+        lastj = e1 > 0.f ? q + 1 : lastj;
       }
+      const int jsel = cnt;
       const int j = j0 + (jsel < kSub ? (jsel <= lastj ? jsel : lastj) : lastj);
       PL[m + off] = (uint32_t)i;
       PR[m + off] = (uint32_t)j;

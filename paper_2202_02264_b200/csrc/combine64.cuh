@@ -31,6 +31,8 @@ struct LevelArgs {
   long long node_off; // global node index of local combine 0 (windows)
   int rows_per_cta;   // FP32 pass 1 row tile (multiple of 32)
   int slots_per_cta;  // FP32 pass 2 slot slice per CTA
+  float* aux;         // FP32 pass 1 -> pass 2 column/row data (Aux32)
+  size_t aux_comb;    // floats per combine in aux
   double* dbg;        // optional debug sink (DSMC_DEBUG)
 };
 
@@ -210,7 +212,8 @@ __global__ void __launch_bounds__(256) c64_rows(Bufs b, LevelArgs la) {
   const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + g.c];
   Col64 C;
   stage_cols<MC, D>(b, la, ch, R, M, tc, smem, C);
-  double* ws = la.ws + (size_t)blockIdx.y * la.ws_comb;
+  // per (chain, combine of the chunk) workspace
+  double* ws = la.ws + ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * la.ws_comb;
   double *wm = ws, *wraw = ws + N, *wsub = ws + 5 * (size_t)N;
   const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
   const double coef = row_coef<MC>(M, g.c);
@@ -297,7 +300,7 @@ __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
   const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + g.c];
   Col64 C;
   stage_cols<MC, D>(b, la, ch, R, M, tc, smem, C);
-  double* ws = la.ws + (size_t)blockIdx.x * la.ws_comb;
+  double* ws = la.ws + ((size_t)blockIdx.z * gridDim.x + blockIdx.x) * la.ws_comb;
   double *wm = ws, *wraw = ws + N, *wscale = ws + 2 * (size_t)N,
          *wtot = ws + 3 * (size_t)N, *wpre = ws + 4 * (size_t)N,
          *wsub = ws + 5 * (size_t)N;

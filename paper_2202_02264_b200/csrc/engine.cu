@@ -319,6 +319,12 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
     configured = true;
   }
   CU(cudaFuncSetAttribute(c32_sample<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+  la.aux_comb = ((size_t)10 * N + 3) & ~(size_t)3;
+  {
+    void* p;
+    CU(ctx->arena.get("AUX32", la.aux_comb * sizeof(float) * (size_t)nk * b.B, &p));
+    la.aux = (float*)p;
+  }
   cudaEvent_t* ev = nullptr;
   if (ctx->time_kernels) {  // 3 events: pair start, pair end = sample start, sample end
     while ((int)ctx->kev.size() < ctx->kev_used + 3) {

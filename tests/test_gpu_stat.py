@@ -149,3 +149,19 @@ def test_kernel_launch_counter_moves(engine):
     before = engine.launches
     engine.smooth(models.lgssm_check(15), 64, seed=1)
     assert engine.launches > before
+
+
+@pytest.mark.parametrize("precision", [abi.FP32, abi.FP64_PARITY])
+def test_batched_chains_equal_single_chain_runs(engine, precision):
+    """Chains of one batched conditional sweep are independent: chain c of a
+    B=4 batch equals the same chain run alone (per-chain workspaces; keys
+    depend only on the chain's own seed, conditional.cpp:22-25)."""
+    m = models.sv(127)
+    refs = np.stack([np.full((128, 1), v) for v in (-1.0, -0.5, -1.5, -1.2)])
+    seeds = [11, 12, 13, 14]
+    both = engine.conditional_sweep([m] * 4, refs, seeds, 200, 3, precision=precision)
+    for c in range(4):
+        one = engine.conditional_sweep([m], refs[c:c + 1], seeds[c:c + 1], 200, 3,
+                                       precision=precision)
+        assert np.array_equal(both["paths"][c], one["paths"][0])
+        assert both["log_norm_const"][c] == one["log_norm_const"][0]
