@@ -1,21 +1,31 @@
 """dSMC smoothing throughput on B200: smoothed particle-timesteps/s (T.N/s).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c2|c1|c3|c5]
+                  [--config c5|c2|c1|c3]
 
 A step is one full dSMC smoothing run (leaves -> ceil(log2 K) combine levels
 -> ancestor composition -> per-time mean/cov) over the configuration's
-synthetic trajectory (BASELINE.json configs; default C2: 2-D constant-velocity
-LGSSM, d = 4, K = T+1 = 2^14, N = 1024, multinomial stitching, FP32).
+synthetic trajectory (BASELINE.json configs; default C5: 2-D constant-velocity
+LGSSM, d = 4, K = T+1 = 2^20, N = 1024, multinomial stitching, FP32 — the
+north-star workload, quoted at 1/2/4/8 GPUs).
 
-  value  = K.N / device time per step, inputs (prepared model) resident in HBM,
-           CUDA events on the engine's stream, max over ranks.
-  e2e    = the same metric through the public C ABI call dsmc_smooth with host
-           (pinned) model arrays: H2D upload + per-time prep + run + D2H of the
-           moments inside the timed region, host wall clock.
+  N = 1    the whole trajectory on one GPU (dsmc_smooth_resident).
+  N > 1    time-sharded (paper_2202_02264_b200/sharded.py): rank g
+           owns K/N contiguous leaves and its local levels; the top log2(N)
+           levels exchange boundary slabs + indices over NCCL P2P. Total work
+           is fixed (scaling "strong"); results equal the 1-GPU run bit for bit.
+
+  value  = K.N / device time per step (CUDA events on the engine stream,
+           barrier + synchronize around the timed region, max over ranks),
+           model resident in HBM.
+  e2e    = the same metric through the public API with host (pinned) model
+           arrays: H2D upload + per-time prep + run + D2H of the moments inside
+           the timed region (N = 1: dsmc_smooth; N > 1: dsmc_model_upload +
+           the sharded stages + D2H of the rank's window), max over ranks.
   roofline = the pair kernel (c32_pair) against the MUFU.EX2 roofline: 1 exp2
-           per pair evaluation; algorithmic work = (combines per level) x N^2
-           pair evaluations per launch.
+           per pair evaluation; algorithmic work = N^2 pair evaluations per
+           combine x the combines of each launch, divided by the
+           summed CUDA-event time of the pair launches of one step.
   cpu_baseline / --impl reference = the reference's own run_smoother compiled
            from /root/reference (oracle/_ref/libdsmc_ref.so) on all host
            threads, on a bounded sample (fewer leaves) of the same workload.
@@ -40,9 +50,10 @@ CONFIGS = {
                     "RTS-marginal proposals", model="cv", K=1 << 14, N=1024, resampler=0),
     "c3": dict(desc="C3: stochastic volatility, K=T+1=2^16, N=4096, MH-lazy (B=16)",
                model="sv", K=1 << 16, N=4096, resampler=2),
-    "c5": dict(desc="C5: 2-D constant-velocity LGSSM d=4, K=T+1=2^20, N=1024, multinomial",
-               model="cv", K=1 << 20, N=1024, resampler=0),
+    "c5": dict(desc="C5: 2-D constant-velocity LGSSM d=4, K=T+1=2^20, N=1024, multinomial, "
+                    "RTS-marginal proposals", model="cv", K=1 << 20, N=1024, resampler=0),
 }
+DEFAULT_CONFIG = "c5"
 METRIC = "smoothed particle-timesteps/sec (T·N/s)"
 UNIT = "particle-timesteps/s"
 
@@ -86,24 +97,25 @@ def host_threads():
         return os.cpu_count() or 1
 
 
-def cpu_reference(cfg, budget_s=8.0):
+def cpu_reference(cfg, budget_s=8.0, Kp=None):
     """Reference run_smoother (compiled from /root/reference) on a bounded
-    sample: K' leaves with the same N, d, model family; doubles K' until the
-    run takes >= budget_s / 4. Returns (T.N/s, cores, sample text)."""
+    sample: K' leaves with the same N, d, model family. Without Kp, doubles K'
+    from 16 until one run takes >= budget_s / 4. Returns (T.N/s, cores,
+    sample text, wall, K')."""
     from oracle.py import Reference
     if not Reference.available():
         return None
     R = Reference()
     threads = host_threads()
-    Kp = 16
+    fixed = Kp is not None
+    Kp = Kp or 16
     while True:
-        sub = dict(cfg, K=Kp)
-        m = build_model(sub)
+        m = build_model(dict(cfg, K=Kp))
         t0 = time.perf_counter()
         r = R.run_smoother(m, cfg["N"], cfg["resampler"], seed=1, mh_steps=16, threads=threads,
                            want_paths=False)
         wall = time.perf_counter() - t0
-        if wall >= budget_s / 4 or Kp >= cfg["K"]:
+        if fixed or wall >= budget_s / 4 or Kp >= cfg["K"]:
             break
         Kp *= 2
     val = Kp * cfg["N"] / wall
@@ -111,7 +123,7 @@ def cpu_reference(cfg, budget_s=8.0):
               f"K'={Kp} leaves (T'={Kp - 1}), N={cfg['N']}, same model family, {threads} threads, "
               f"wall {wall:.2f} s (RunMetadata wall {r['wall_time_ms']:.0f} ms); dense cost is "
               f"exactly T*N^2 pair evaluations so T*N/s does not depend on T")
-    return val, threads, sample, wall
+    return val, threads, sample, wall, Kp
 
 
 class ClockSampler:
@@ -169,94 +181,149 @@ def sfu_peak_pairs_per_s(sm_max_mhz):
     return 148 * 16 * mhz * 1e6, "nominal 16 ex2/clk/SM x 148 SMs at sm_max_mhz"
 
 
+def _red_device(device):
+    import torch
+    d = torch.distributed
+    if d.is_available() and d.is_initialized() and d.get_backend() == "gloo":
+        return "cpu"
+    return f"cuda:{device}"
+
+
+def _time_steps(stream, steps, fn, world, device):
+    """Barrier + synchronize, CUDA events on `stream` around exactly `steps`
+    calls of fn(step), synchronize; returns the max over ranks of ms/step."""
+    import torch
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for st in range(steps):
+        fn(st)
+    end.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([start.elapsed_time(end) / steps], device=_red_device(device))
+    if world > 1:
+        torch.distributed.all_reduce(ms, op=torch.distributed.ReduceOp.MAX)
+    return float(ms.item())
+
+
+def _max_over_ranks(v, world, device):
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=_red_device(device))
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args, cfg, rank, world, device):
     import torch
-    from paper_2202_02264_b200 import abi
     from paper_2202_02264_b200.dsmc import Engine
+    from paper_2202_02264_b200.sharded import GpuBackend, TorchComm, sharded_smooth
 
     torch.cuda.set_device(device)
     eng = Engine(device)
     model = build_model(cfg, pinned=True)
-    K, N, d = cfg["K"], cfg["N"], model.d
-    seed_base = 1 + (1 << 32)
-    # ---- device-resident throughput (value)
+    K, N, d, rs = cfg["K"], cfg["N"], model.d, cfg["resampler"]
+    seed_base = 1 + (1 << 32)  # experiment.cpp:42-45 salting of seed 1, replicate 0
+    stream = torch.cuda.ExternalStream(eng.stream_handle(), device=torch.device("cuda", device))
     h = eng.upload(model)
     eng.sync()
+    if world == 1:
+        def step(s):
+            eng.smooth_resident(h, N, rs, seed=seed_base + s)
+    else:
+        if K % world or (K // world) < 2:
+            raise SystemExit(f"K={K} does not split over {world} ranks")
+        comm = TorchComm()
+        be = GpuBackend(eng, h, N, d, seed_base, rs, device)
+
+        def step(s):
+            be.seed = seed_base + s
+            return sharded_smooth({rank: be}, comm, K, N, world)
+    # ---- device-resident throughput (value)
     for w in range(args.warmup):
-        eng.smooth_resident(h, N, cfg["resampler"], seed=seed_base + w)
-    eng.sync()
-    stream = torch.cuda.ExternalStream(eng.stream_handle())
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        torch.distributed.barrier()
+        step(10_000 + w)
     torch.cuda.synchronize()
     launches0 = eng.launches
     with ClockSampler(device) as clocks:
-        start.record(stream)
-        for s in range(args.steps):
-            eng.smooth_resident(h, N, cfg["resampler"], seed=seed_base + 1000 + s)
-        end.record(stream)
-        torch.cuda.synchronize()
+        ms_max = _time_steps(stream, args.steps, step, world, device)
     launches = eng.launches - launches0
-    ms = start.elapsed_time(end) / args.steps
-    timings = eng.timings()
-    mean, cov, lnc = eng.resident_results(K, d)
-    ms_t = torch.tensor([ms], device=f"cuda:{device}")
-    if world > 1:
-        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    value = world * K * N / (ms_max * 1e-3)
+    timings = eng.timings()  # last step's per-kernel-class event times
+    value = K * N / (ms_max * 1e-3)
     # ---- end to end through the public API (host pinned in, host out)
     h2d = sum(a.nbytes for a in model.arrays.values() if a is not None)
-    d2h = K * d * 8 + K * d * d * 8 + 8
     e2e_steps = max(3, min(args.steps, 10))
-    eng.smooth(model, N, cfg["resampler"], seed=7)  # warm (pool allocations)
+    if world == 1:
+        d2h = K * d * 8 + K * d * d * 8 + 8
+
+        def e2e_step(s):
+            eng.smooth(model, N, rs, seed=seed_base + 5000 + s)
+    else:
+        Kloc = K // world
+        d2h = Kloc * (d + d * d) * 8 + 8
+
+        def e2e_step(s):
+            hh = eng.upload(model)
+            b2 = GpuBackend(eng, hh, N, d, seed_base + 5000 + s, rs, device)
+            out, lz = sharded_smooth({rank: b2}, comm, K, N, world)
+            mean, cov = out[rank]
+            mean.cpu(), cov.cpu()
+            eng.free_model(hh)
+    e2e_step(-1)  # warm (pool allocations)
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
     for s in range(e2e_steps):
-        eng.smooth(model, N, cfg["resampler"], seed=seed_base + 5000 + s)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e_t = torch.tensor([e2e_s], device=f"cuda:{device}")
-    if world > 1:
-        torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
-    e2e_val = world * K * N / float(e2e_t.item())
-    eng.free_model(h)
+        e2e_step(s)
+    torch.cuda.synchronize()
+    e2e_s = _max_over_ranks((time.perf_counter() - t0) / e2e_steps, world, device)
+    e2e_val = K * N / e2e_s
     out = None
     if rank == 0:
         ck = clocks.summary()
         pair_ms = timings[3] if len(timings) > 3 else None
-        pairs_total = (K - 1) * N * N
+        Kloc = K // world
+        pairs_local = (Kloc - 1) * N * N  # rank 0's local combines (all of them at N=1)
         peak, peak_src = sfu_peak_pairs_per_s(ck.get("sm_max_mhz"))
-        ach = pairs_total / (pair_ms * 1e-3) if pair_ms else None
+        ach = pairs_local / (pair_ms * 1e-3) if pair_ms else None
         roof = {"bound": "sfu", "kernel": "c32_pair", "achieved": ach, "peak": peak,
                 "unit": "pair-evals/s (1 MUFU.EX2 each)", "frac": ach / peak if ach else None,
                 "peak_source": peak_src, "traffic": None,
+                "work": f"{pairs_local:.4g} pair evaluations per step on rank 0 "
+                        f"({Kloc - 1} combines x N^2)",
                 "pair_kernel_ms_per_step": pair_ms,
                 "sample_kernel_ms_per_step": timings[4] if len(timings) > 4 else None,
-                "pair_kernel_share_of_step": pair_ms / ms if pair_ms else None,
-                "leaf_ms": timings[0], "levels_ms": timings[1], "compose_gather_ms": timings[2]}
+                "pair_kernel_share_of_step": pair_ms / ms_max if pair_ms else None,
+                "leaf_ms": timings[0], "levels_ms": timings[1],
+                "compose_gather_ms": timings[2] if world == 1 else None}
         prof = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(prof):
             roof["traffic"] = json.load(open(prof)).get(args.config)
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (simulated trajectory, numpy seed 90210; RTS-marginal proposals)",
+            "data": "synthetic (trajectory simulated with numpy seed 90210; RTS-marginal proposals)",
             "config": {"workload": cfg["desc"], "K": K, "T": K - 1, "N": N, "d": d,
                        "resampler": ["multinomial", "systematic", "mh-lazy",
-                                     "rejection-lazy"][cfg["resampler"]],
+                                     "rejection-lazy"][rs],
                        "precision": "fp32 throughput path",
-                       "l2": "inputs larger than L2 (leaf slab %.0f MB > 126 MB)" % (K * N * 16 / 1e6),
-                       "parallelism": f"time-sharded x{world}" if world > 1 else "single GPU"},
+                       "l2": "inputs larger than L2 (leaf slab %.0f MB > 126 MB)" % (K * N * 20 / 1e6),
+                       "parallelism": (f"time-sharded x{world} (NCCL P2P boundary exchange)"
+                                       if world > 1 else "single GPU")},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "api": "dsmc_smooth (C ABI), host pinned arrays"},
+                    "d2h_bytes_per_step": int(d2h),
+                    "api": ("dsmc_smooth (C ABI), host pinned arrays" if world == 1 else
+                            "dsmc_model_upload + sharded window stages (C ABI), host pinned "
+                            "arrays, D2H of the rank's window moments")},
             "gpu_launches": int(launches),
             "roofline": roof,
             "clocks": ck,
-            "log_norm_const_last": lnc,
         }
+    eng.free_model(h)
     eng.close()
     return out
 
@@ -267,7 +334,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=list(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=list(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
@@ -285,8 +352,9 @@ def main():
                               "oracle/_ref/libdsmc_ref.so not built (needs /root/reference)"}))
             return
         vals = []
+        v, cores, sample, wall, Kp = cpu_reference(cfg, budget_s=4.0)  # sizes the sample
         for s in range(args.warmup + args.steps):
-            v, cores, sample, wall = cpu_reference(cfg, budget_s=4.0)
+            v, cores, sample, wall, _ = cpu_reference(cfg, Kp=Kp)
             if s >= args.warmup:
                 vals.append(v)
         val = float(np.median(vals))
@@ -303,13 +371,21 @@ def main():
 
     if world > 1:
         import torch
-        torch.distributed.init_process_group("nccl")
+        # one rank per GPU over NCCL; DSMC_DIST_BACKEND=gloo (host-staged, ranks
+        # may share a GPU) only exercises the protocol, it is not a bench number
+        local = local % torch.cuda.device_count()
+        torch.cuda.set_device(local)
+        backend = os.environ.get("DSMC_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            torch.distributed.init_process_group(backend)
     out = run_ours(args, cfg, rank, world, local)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_reference(cfg)
             if cb is not None:
-                v, cores, sample, wall = cb
+                v, cores, sample, wall, _ = cb
                 out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores,
                                        "kind": "reference", "sample": sample}
         print(json.dumps(out))

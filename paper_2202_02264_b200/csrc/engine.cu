@@ -516,13 +516,13 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
       CU(cudaMemcpyAsync(p, o.inj_lw, BKN * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
       dinj_lw = (const double*)p;
     }
-    leaf64_kernel<<<dim3((N + 127) / 128, K, B), 128, 0, ctx->stream>>>(b, dinj_x, dinj_lw);
+    leaf64_kernel<<<dim3(K, (N + 127) / 128, B), 128, 0, ctx->stream>>>(b, dinj_x, dinj_lw);
     LAUNCHED(ctx);
     leafnorm64_kernel<<<dim3(K, B), 32, 0, ctx->stream>>>(b);
     LAUNCHED(ctx);
   } else {
     CU(A.get("RAW0", (size_t)B * N * sizeof(double), &p));
-    leaf32_kernel<<<dim3((N + 127) / 128, K, B), 128, 0, ctx->stream>>>(b, (double*)p);
+    leaf32_kernel<<<dim3(K, (N + 127) / 128, B), 128, 0, ctx->stream>>>(b, (double*)p);
     LAUNCHED(ctx);
     if (o.t0 == 0) {  // only global leaf 0 carries non-uniform weights
       leafnorm32_kernel<<<B, 32, 0, ctx->stream>>>(b, (const double*)p);
@@ -657,7 +657,10 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     st.blnc[1] = blnc[1];
     st.resampler = o.resampler;
   }
-  if (!o.compose) return DSMC_OK;
+  if (!o.compose) {
+    if (o.timing) CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+    return DSMC_OK;
+  }
 
   // ----------------------------------------------------------- composition
   if (o.conditional) {
@@ -692,7 +695,7 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     int mcur = 0;
     bool root = true;
     for (int l = level; l >= 2; --l) {
-      td_kernel<<<dim3((N + 255) / 256, nbs[l], B), 256, 0, ctx->stream>>>(
+      td_kernel<<<dim3(nbs[l], (N + 255) / 256, B), 256, 0, ctx->stream>>>(
           b, l, cursors[l], nbs[l], nbs[l - 1], Mb[mcur], Mb[1 - mcur], root ? 1 : 0,
           o.root_map);
       LAUNCHED(ctx);
@@ -1533,6 +1536,9 @@ int dsmc_window_run(dsmc_ctx* ctx, const dsmc_model_handle* hc, const dsmc_windo
   o.t0 = wo->t0;
   o.len = len;
   o.compose = false;
+  o.timing = true;  // per-kernel-class device times (dsmc_last_timings)
+  ctx->time_kernels = true;
+  ctx->kev_used = 0;
   void* p;
   CU(ctx->arena.get("SEEDS", sizeof(uint64_t), &p));
   CU(cudaMemcpyAsync(p, &wo->seed, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
@@ -1591,7 +1597,7 @@ int dsmc_window_finish(dsmc_ctx* ctx, const uint32_t* d_root_map, double* d_mean
   int mcur = 0;
   bool root = true;
   for (int l = st.levels; l >= 2; --l) {
-    td_kernel<<<dim3((N + 255) / 256, nbs[l], B), 256, 0, ctx->stream>>>(
+    td_kernel<<<dim3(nbs[l], (N + 255) / 256, B), 256, 0, ctx->stream>>>(
         b, l, cursors[l], nbs[l], nbs[l - 1], Mb[mcur], Mb[1 - mcur], root ? 1 : 0, d_root_map);
     LAUNCHED(ctx);
     root = false;

@@ -27,6 +27,7 @@ in-process virtual ranks (several backends hosted by one process exchange
 tensors directly). Backends: `GpuBackend` (the CUDA engine); tests add a CPU
 backend implementing the same five stages.
 """
+import contextlib
 import math
 
 import numpy as np
@@ -107,9 +108,23 @@ class TorchComm:
         import torch.distributed as dist
         self.dist = dist
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        # gloo cannot move CUDA tensors: stage them through host memory (used
+        # only to exercise the protocol; NCCL is the GPU transport)
+        self.stage = dist.get_backend() == "gloo"
 
     def exchange(self, sends, recvs):
         """sends: [(dst, tensor)], recvs: [(src, tensor)]; batched P2P."""
+        if self.stage:
+            sends = [(dst, t.cpu()) for dst, t in sends]
+            host = [(src, t, torch.empty(t.shape, dtype=t.dtype)) for src, t in recvs]
+            ops = [self.dist.P2POp(self.dist.isend, t, dst) for dst, t in sends]
+            ops += [self.dist.P2POp(self.dist.irecv, h, src) for src, _, h in host]
+            if ops:
+                for w in self.dist.batch_isend_irecv(ops):
+                    w.wait()
+            for _, t, h in host:
+                t.copy_(h)
+            return
         ops = [self.dist.P2POp(self.dist.isend, t, dst) for dst, t in sends]
         ops += [self.dist.P2POp(self.dist.irecv, t, src) for src, t in recvs]
         if ops:
@@ -117,6 +132,11 @@ class TorchComm:
                 w.wait()
 
     def all_reduce_sum(self, t):
+        if self.stage and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h)
+            t.copy_(h)
+            return t
         self.dist.all_reduce(t)
         return t
 
@@ -128,7 +148,22 @@ def sharded_smooth(backends, comm, K, N, world):
     one-process-per-GPU; all of them for in-process virtual ranks).
     comm: TorchComm, or None when every rank is hosted here.
     Returns ({rank: (mean, cov)} for the hosted windows, log Z).
+
+    With a transport (one backend per process) every torch op of the
+    protocol — the exchange tensors and the NCCL P2P calls — is issued on the
+    engine's own stream, so kernel outputs and transfers are stream-ordered
+    without host synchronisation.
     """
+    one = backends[sorted(backends)[0]]
+    if comm is not None and len(backends) == 1 and getattr(one, "stream", None) is not None:
+        ctx = torch.cuda.stream(one.stream)
+    else:
+        ctx = contextlib.nullcontext()
+    with ctx:
+        return _sharded_smooth(backends, comm, K, N, world)
+
+
+def _sharded_smooth(backends, comm, K, N, world):
     P = world
     Kloc = K // P
     s, L = _log2(Kloc), _log2(K)

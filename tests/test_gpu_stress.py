@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from paper_2202_02264_b200 import abi, models
+from paper_2202_02264_b200.dsmc import kalman_smooth
 
 pytestmark = pytest.mark.gpu
 
@@ -42,3 +43,16 @@ def test_fp64_device_vs_oracle(engine, oracle, d, N):
         if o["log_norm_const"] is not None:
             assert abs(r["log_norm_const"] - o["log_norm_const"]) < 1e-10
         assert r["weight_evals"] == o["weight_evals"]
+
+
+def test_horizon_beyond_grid_y_limit(engine):
+    """K = 2^17 leaves: per-time and per-block grids exceed 65535, so time and
+    block indices must live in grid x (C5 runs K = 2^20)."""
+    K = 1 << 17
+    m = models.lgssm_check(K - 1)
+    r = engine.smooth(m, 16, abi.MULTINOMIAL, seed=3, precision=abi.FP32)
+    assert r["levels"] == 17
+    assert np.isfinite(r["mean"]).all() and np.isfinite(r["log_norm_const"])
+    km, kP, _ = kalman_smooth(m)
+    z = (r["mean"][:, 0] - km[:, 0]) / np.sqrt(kP[:, 0, 0])
+    assert np.sqrt(np.mean(z ** 2)) < 1.0
