@@ -95,57 +95,80 @@ __global__ void __launch_bounds__(256) gather64_kernel(Bufs b, const uint32_t* M
   }
 }
 
-// FP32 leaves: centred states; moments accumulated on x - m_t in double.
+// FP32 leaves: centred states. One warp per time t (8 per CTA): lanes gather
+// 4 particles per round with independent loads (sigma map -> leaf slab), sum
+// x and the upper triangle of x x^T in FP32 over their particles, one warp
+// reduction of the D + D(D+1)/2 sums, FP64 moments written by lane 0.
 template <int D>
 __global__ void __launch_bounds__(256) gather32_kernel(Bufs b, const uint32_t* M1,
                                                        int root1, double* paths,
                                                        double* mean, double* cov,
                                                        const uint32_t* root_map) {
-  const int t = blockIdx.x, ch = blockIdx.y;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5), ch = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  if (t >= b.K) return;
   const int N = b.N;
-  __shared__ double red[8][20];
   const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + t];
-  double s1[4] = {0, 0, 0, 0}, s2[16] = {0};
+  constexpr int NT = D * (D + 1) / 2;
+  float s1[D], s2[NT];
+#pragma unroll
+  for (int k = 0; k < D; ++k) s1[k] = 0.f;
+#pragma unroll
+  for (int k = 0; k < NT; ++k) s2[k] = 0.f;
   const float4* X = b.X32 + ((size_t)ch * b.K + t) * N;
-  for (int q = threadIdx.x; q < N; q += blockDim.x) {
-    const uint32_t sg = leaf_sigma(b, ch, t, q, M1, root1, root_map);
-    const float4 xv = X[sg];
-    double x[4];
+  for (int q0 = lane; q0 < N; q0 += 128) {
+    uint32_t sg[4];
 #pragma unroll
-    for (int k = 0; k < D; ++k) x[k] = (double)comp(xv, k);
-    if (paths)
-      for (int k = 0; k < D; ++k)
-        paths[(((size_t)ch * b.K + t) * N + q) * D + k] = x[k] + tc.pm[k];
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + 32 * u;
+      sg[u] = q < N ? leaf_sigma(b, ch, t, q, M1, root1, root_map) : 0u;
+    }
+    float4 xv[4];
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      s1[k] += x[k];
+    for (int u = 0; u < 4; ++u) xv[u] = X[sg[u]];
 #pragma unroll
-      for (int l = 0; l < D; ++l) s2[k * D + l] += x[k] * x[l];
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + 32 * u;
+      if (q >= N) continue;
+      float x[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
+      if (paths)
+        for (int k = 0; k < D; ++k)
+          paths[(((size_t)ch * b.K + t) * N + q) * D + k] = (double)x[k] + tc.pm[k];
+      int c = 0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        s1[k] += x[k];
+#pragma unroll
+        for (int l = k; l < D; ++l) {
+          s2[c] = fmaf(x[k], x[l], s2[c]);
+          ++c;
+        }
+      }
     }
   }
   if (!mean && !cov) return;
-  constexpr int nv = D + D * D;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int v = 0; v < nv; ++v) {
-    double a = v < D ? s1[v] : s2[v - D];
-    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(~0u, a, o);
-    if (lane == 0) red[warp][v] = a;
+  for (int o = 16; o; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) s1[k] += __shfl_xor_sync(~0u, s1[k], o);
+#pragma unroll
+    for (int k = 0; k < NT; ++k) s2[k] += __shfl_xor_sync(~0u, s2[k], o);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double tot[20] = {0};
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
-      for (int v = 0; v < nv; ++v) tot[v] += red[w][v];
+  if (lane == 0) {
     double mu[4];
-    for (int k = 0; k < D; ++k) mu[k] = tot[k] / N;
+    for (int k = 0; k < D; ++k) mu[k] = (double)s1[k] / N;
     const size_t o = (size_t)ch * b.K + t;
     if (mean)
       for (int k = 0; k < D; ++k) mean[o * D + k] = mu[k] + tc.pm[k];
-    if (cov)
+    if (cov) {
+      int c = 0;
       for (int k = 0; k < D; ++k)
-        for (int l = 0; l < D; ++l)
-          cov[o * D * D + k * D + l] = tot[D + k * D + l] / N - mu[k] * mu[l];
+        for (int l = k; l < D; ++l, ++c) {
+          const double v = (double)s2[c] / N - mu[k] * mu[l];
+          cov[o * D * D + k * D + l] = v;
+          cov[o * D * D + l * D + k] = v;
+        }
+    }
   }
 }
 

@@ -522,7 +522,13 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     LAUNCHED(ctx);
   } else {
     CU(A.get("RAW0", (size_t)B * N * sizeof(double), &p));
-    leaf32_kernel<<<dim3(K, (N + 127) / 128, B), 128, 0, ctx->stream>>>(b, (double*)p);
+    const dim3 lg(K, (N + 127) / 128, B);
+    switch (d) {
+      case 1: leaf32_kernel<1><<<lg, 128, 0, ctx->stream>>>(b, (double*)p); break;
+      case 2: leaf32_kernel<2><<<lg, 128, 0, ctx->stream>>>(b, (double*)p); break;
+      case 3: leaf32_kernel<3><<<lg, 128, 0, ctx->stream>>>(b, (double*)p); break;
+      default: leaf32_kernel<4><<<lg, 128, 0, ctx->stream>>>(b, (double*)p); break;
+    }
     LAUNCHED(ctx);
     if (o.t0 == 0) {  // only global leaf 0 carries non-uniform weights
       leafnorm32_kernel<<<B, 32, 0, ctx->stream>>>(b, (const double*)p);
@@ -709,10 +715,10 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
       const uint32_t* M1 = Mb[mcur];
       const int r1 = root ? 1 : 0;
       switch (d) {
-        case 1: gather32_kernel<1><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
-        case 2: gather32_kernel<2><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
-        case 3: gather32_kernel<3><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
-        default: gather32_kernel<4><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
+        case 1: gather32_kernel<1><<<dim3((K + 7) / 8, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
+        case 2: gather32_kernel<2><<<dim3((K + 7) / 8, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
+        case 3: gather32_kernel<3><<<dim3((K + 7) / 8, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
+        default: gather32_kernel<4><<<dim3((K + 7) / 8, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
       }
     }
     LAUNCHED(ctx);
@@ -1606,10 +1612,10 @@ int dsmc_window_finish(dsmc_ctx* ctx, const uint32_t* d_root_map, double* d_mean
   const uint32_t* M1 = Mb[mcur];
   const int r1 = root ? 1 : 0;
   switch (d) {
-    case 1: gather32_kernel<1><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, nullptr, d_mean, d_cov, d_root_map); break;
-    case 2: gather32_kernel<2><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, nullptr, d_mean, d_cov, d_root_map); break;
-    case 3: gather32_kernel<3><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, nullptr, d_mean, d_cov, d_root_map); break;
-    default: gather32_kernel<4><<<dim3(K, B), 256, 0, ctx->stream>>>(b, M1, r1, nullptr, d_mean, d_cov, d_root_map); break;
+    case 1: gather32_kernel<1><<<dim3((K + 7) / 8, B), 256, 0, ctx->stream>>>(b, M1, r1, nullptr, d_mean, d_cov, d_root_map); break;
+    case 2: gather32_kernel<2><<<dim3((K + 7) / 8, B), 256, 0, ctx->stream>>>(b, M1, r1, nullptr, d_mean, d_cov, d_root_map); break;
+    case 3: gather32_kernel<3><<<dim3((K + 7) / 8, B), 256, 0, ctx->stream>>>(b, M1, r1, nullptr, d_mean, d_cov, d_root_map); break;
+    default: gather32_kernel<4><<<dim3((K + 7) / 8, B), 256, 0, ctx->stream>>>(b, M1, r1, nullptr, d_mean, d_cov, d_root_map); break;
   }
   LAUNCHED(ctx);
   CU(cudaGetLastError());

@@ -175,39 +175,87 @@ __global__ void leafnorm64_kernel(Bufs b) {
   }
 }
 
+// Leaf-0 raw weight h0 + P0 - q0 in FP64 (only the CTAs of global time 0;
+// kept out of line so its local arrays stay off the hot path).
+__device__ __noinline__ double leaf0_raw_weight(const DevModel& M, const TimeConst& tc, int d,
+                                                const double* x) {
+  if (M.kind == DSMC_MODEL_SV) {
+    const double v0 = M.sv_s2 / (1.0 - M.sv_phi * M.sv_phi);
+    const double dx = x[0] - M.sv_mu;
+    return -0.5 * (kLog2Pi + log(v0)) - dx * dx / (2.0 * v0) - tc.logabsy;
+  }
+  double W0[16], L0[16];
+  dchol(M.P0, d, L0);
+  dtri_inv(L0, d, W0);
+  const double norm0 = dnorm_of(L0, d);
+  const double p0 = norm0 - 0.5 * dquad(W0, d, x, M.m0);
+  double zz = 0.0;
+  double e[4];
+  for (int k = 0; k < d; ++k) e[k] = x[k] - tc.pm[k];
+  for (int k = 0; k < d; ++k) {
+    double acc = 0.0;
+    for (int l = 0; l <= k; ++l) acc += tc.pW[k * d + l] * e[l];
+    zz += acc * acc;
+  }
+  const double q0 = tc.p_norm - 0.5 * zz;
+  double h0 = 0.0;
+  if (tc.obs) {
+    const double* H = at(M.H, M.H_s, 0);
+    double hx[4];
+    for (int a = 0; a < M.dy; ++a) {
+      double s = 0.0;
+      for (int l = 0; l < d; ++l) s += H[a * d + l] * x[l];
+      hx[a] = s;
+    }
+    h0 = tc.o_norm - 0.5 * dquad(tc.oW, M.dy, M.y, hx);
+  }
+  return h0 + p0 - q0;
+}
+
 // FP32 leaf: centred state x - m_t = L_t z (float4), column term
 // log2e * (log h_t - log nu_t + log N-normaliser of the transition into t)
 // written from z directly (no cancellation), leaf-0 raw weight in
 // FP64. For every device model q_t = nu_t, so leaves t >= 1 are uniform.
-__global__ void leaf32_kernel(Bufs b, double* raw0) {
-  // grid (time, particle chunk, chain): time in x (up to 2^31 leaves)
+// Grid (time, particle chunk, chain); the time's FP32 constants are staged
+// in shared memory once per CTA.
+template <int D>
+__global__ void __launch_bounds__(128) leaf32_kernel(Bufs b, double* raw0) {
   const int n = blockIdx.y * blockDim.x + threadIdx.x;
   const int t = blockIdx.x, ch = blockIdx.z;
   const int gt = b.t0 + t;  // global time (stream key, model data)
-  if (n >= b.N) return;
   const DevModel& M = b.models[ch];
   const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + t];
-  const int d = b.d;
+  __shared__ float s_L[16], s_G[16], s_e[4], s_c;
+  if (threadIdx.x < 16) {
+    s_L[threadIdx.x] = (float)tc.pL[threadIdx.x];
+    s_G[threadIdx.x] = (float)tc.G[threadIdx.x];
+  }
+  if (threadIdx.x < 4) s_e[threadIdx.x] = (float)tc.e[threadIdx.x];
+  if (threadIdx.x == 0) s_c = (float)tc.cconst;
+  __syncthreads();
+  if (n >= b.N) return;
   const size_t off = ((size_t)ch * b.K + t) * b.N + n;
   float z[4] = {0.f, 0.f, 0.f, 0.f};
-  float4 xs = make_float4(0.f, 0.f, 0.f, 0.f);
+  float xv[4] = {0.f, 0.f, 0.f, 0.f};
   float col;
   const bool is_star = b.conditional && n == 0;
   double xstar[4] = {0, 0, 0, 0};
   if (is_star) {
-    for (int k = 0; k < d; ++k) xstar[k] = b.star[((size_t)ch * b.K + t) * d + k];
+#pragma unroll
+    for (int k = 0; k < D; ++k) xstar[k] = b.star[((size_t)ch * b.K + t) * D + k];
   } else {
     const StreamId id = stream_id(b.seeds[ch], 0, leaf_node(gt, b.conditional, b.sweep),
                                   DSMC_ROLE_LEAF_PROPOSAL, 0);
     const uint64_t p = b.conditional ? n - 1 : n;
-    // d normals, counter-addressed Box-Muller pairs (normal i uses u64s
+    // D normals, counter-addressed Box-Muller pairs (normal i uses u64s
     // 2*(i/2) and 2*(i/2)+1, rng.cpp:74-86): one Philox block serves up to
     // two pairs and one (r, theta) serves both normals of a pair
     U64x4 blk;
     uint64_t have = ~0ull;
-    float r = 0.f, s = 0.f, c = 0.f;
-    for (int k = 0; k < d; ++k) {
-      const uint64_t i = p * d + k;
+    float r = 0.f, sn = 0.f, cs = 0.f;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const uint64_t i = p * D + k;
       if (k == 0 || !(i & 1)) {
         const uint64_t q = 2 * (i >> 1);
         if ((q >> 2) != have) {
@@ -217,12 +265,11 @@ __global__ void leaf32_kernel(Bufs b, double* raw0) {
         const float u1 = (float)u64_uniform_pos(blk.v[q & 3]);
         const float u2 = (float)u64_uniform(blk.v[(q & 3) + 1]);
         r = sqrtf(-2.0f * __logf(u1));
-        sincospif(2.0f * u2, &s, &c);
+        sincospif(2.0f * u2, &sn, &cs);
       }
-      z[k] = (i & 1) ? r * s : r * c;
+      z[k] = (i & 1) ? r * sn : r * cs;
     }
   }
-  float xv[4] = {0.f, 0.f, 0.f, 0.f};
   if (M.kind == DSMC_MODEL_SV) {
     const double xd = is_star ? xstar[0]
                               : DSUB(DMUL(2.0, tc.logabsy), (double)__logf(z[0] * z[0]));
@@ -232,36 +279,43 @@ __global__ void leaf32_kernel(Bufs b, double* raw0) {
     if (is_star) {
       // z = W_P (x* - m_t): the reference state expressed in proposal units
       double e[4];
-      for (int k = 0; k < d; ++k) e[k] = xstar[k] - tc.pm[k];
-      for (int k = 0; k < d; ++k) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) e[k] = xstar[k] - tc.pm[k];
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
         double acc = 0.0;
-        for (int l = 0; l <= k; ++l) acc += tc.pW[k * d + l] * e[l];
+#pragma unroll
+        for (int l = 0; l <= k; ++l) acc += tc.pW[k * D + l] * e[l];
         z[k] = (float)acc;
       }
-      for (int k = 0; k < d; ++k) xv[k] = (float)e[k];
+#pragma unroll
+      for (int k = 0; k < D; ++k) xv[k] = (float)e[k];
     } else {
-      for (int k = 0; k < d; ++k) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
         float acc = 0.f;
-        for (int l = 0; l <= k; ++l) acc = fmaf((float)tc.pL[k * d + l], z[l], acc);
+#pragma unroll
+        for (int l = 0; l <= k; ++l) acc = fmaf(s_L[k * D + l], z[l], acc);
         xv[k] = acc;
       }
     }
     float zz = 0.f, rr = 0.f;
-    for (int k = 0; k < d; ++k) zz = fmaf(z[k], z[k], zz);
+#pragma unroll
+    for (int k = 0; k < D; ++k) zz = fmaf(z[k], z[k], zz);
     if (tc.obs) {
-      for (int a = 0; a < M.dy; ++a) {
-        float g = (float)tc.e[a];
-        for (int l = 0; l < d; ++l) g = fmaf(-(float)tc.G[a * d + l], z[l], g);
+      const int dy = M.dy;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        if (a >= dy) break;
+        float g = s_e[a];
+#pragma unroll
+        for (int l = 0; l < D; ++l) g = fmaf(-s_G[a * D + l], z[l], g);
         rr = fmaf(g, g, rr);
       }
     }
-    col = (float)kLog2E * ((float)tc.cconst + 0.5f * (zz - rr));
+    col = (float)kLog2E * (s_c + 0.5f * (zz - rr));
   }
-  xs.x = xv[0];
-  xs.y = xv[1];
-  xs.z = xv[2];
-  xs.w = xv[3];
-  b.X32[off] = xs;
+  b.X32[off] = make_float4(xv[0], xv[1], xv[2], xv[3]);
   b.COL[off] = col;
   if (n == 0 && gt > 0) {  // q_t = nu_t: uniform leaf, lse = log N exactly
     const size_t o = (size_t)ch * b.K + t;
@@ -270,43 +324,10 @@ __global__ void leaf32_kernel(Bufs b, double* raw0) {
     b.LWMAX[o] = -log((double)b.N);
   }
   if (gt == 0) {
-    // leaf-0 raw weight h0 + P0 - q0 in FP64
     double x[4];
-    for (int k = 0; k < d; ++k) x[k] = is_star ? xstar[k] : (double)xv[k] + tc.pm[k];
-    double w;
-    if (M.kind == DSMC_MODEL_SV) {
-      const double v0 = M.sv_s2 / (1.0 - M.sv_phi * M.sv_phi);
-      const double dx = x[0] - M.sv_mu;
-      w = -0.5 * (kLog2Pi + log(v0)) - dx * dx / (2.0 * v0) - tc.logabsy;
-    } else {
-      double W0[16], L0[16];
-      dchol(M.P0, d, L0);
-      dtri_inv(L0, d, W0);
-      const double norm0 = dnorm_of(L0, d);
-      const double p0 = norm0 - 0.5 * dquad(W0, d, x, M.m0);
-      double zz = 0.0;
-      double e[4];
-      for (int k = 0; k < d; ++k) e[k] = x[k] - tc.pm[k];
-      for (int k = 0; k < d; ++k) {
-        double acc = 0.0;
-        for (int l = 0; l <= k; ++l) acc += tc.pW[k * d + l] * e[l];
-        zz += acc * acc;
-      }
-      const double q0 = tc.p_norm - 0.5 * zz;
-      double h0 = 0.0;
-      if (tc.obs) {
-        const double* H = at(M.H, M.H_s, 0);
-        double hx[4];
-        for (int a = 0; a < M.dy; ++a) {
-          double s = 0.0;
-          for (int l = 0; l < d; ++l) s += H[a * d + l] * x[l];
-          hx[a] = s;
-        }
-        h0 = tc.o_norm - 0.5 * dquad(tc.oW, M.dy, M.y, hx);
-      }
-      w = h0 + p0 - q0;
-    }
-    raw0[(size_t)ch * b.N + n] = w;
+#pragma unroll
+    for (int k = 0; k < D; ++k) x[k] = is_star ? xstar[k] : (double)xv[k] + tc.pm[k];
+    raw0[(size_t)ch * b.N + n] = leaf0_raw_weight(M, tc, D, x);
   }
 }
 
