@@ -9,26 +9,30 @@
 // i.e. -|y_j - nu_i|^2 expanded; states are stored centred on the proposal
 // mean so the expansion does not cancel.
 //
-// c32_pair: one CTA per (row tile, combine). Each lane owns 16 consecutive
-// columns (y, A in registers, packed float2 so the d+1 FMAs per pair issue
-// as FFMA2); a 64-column sub-block is 4 lanes. Per row: d FFMA2 per column
-// pair, sub-block max (FMNMX + 2 SHFL), exp2 (MUFU.EX2), sum (FADD2 + 2
-// SHFL); one lane per sub-block writes L_s = m_s + log2(sum_s) + B_i.
-// Nothing of the N x N table is stored beyond N*N/64 floats.
+// c32_pair (pass 1): ROW-STATIONARY. A CTA owns 256 rows of one combine, each
+// lane 8 of them (u_i in registers, packed as row pairs); its warps stream the
+// combine's 64-column sub-blocks through shared memory (one LDS.128 + one LDS
+// per column, broadcast to the warp) and every lane accumulates its rows'
+// sub-block sums of 2^(w - shift) in registers: per column and row pair one
+// FFMA2 chain of d+1 (bias + d components), two MUFU.EX2 and one FADD2 — no
+// max, no shuffles. The shift is the exact bound lw2_i + cmax_s (+ c_i for
+// the few rows with |nu_i|^2 > 100), so exponents never overflow; a row whose
+// sub-block sum underflows (< 2^-60) is recomputed with its exact max. Lane
+// results L_is = log2 sum_{j in s} 2^w_ij are stored [sub-block][row]
+// (coalesced). Nothing of the N x N table is stored beyond N*N/64 floats.
 //
-// c32_sample: one CTA per combine: row totals from the sub-block sums,
-// row CDF (double inclusive scan), per-slot binary search over rows, walk
-// over the row's sub-blocks, and recomputation of <= 64 weights with the
-// same FP32 operations as pass 1.
+// c32_sample (pass 2): one CTA per combine (or per slot slice): row totals
+// from the sub-block sums, row CDF (double inclusive scan), per-slot binary
+// search over rows, walk over the row's sub-blocks, and recomputation of <= 64
+// weights with the same FP32 pair arithmetic.
 #pragma once
 
 #include "combine64.cuh"
 
 namespace dsmc_dev {
 
-constexpr int kCPL = 16;             // columns per lane
-constexpr int kChunk = 32 * kCPL;    // columns per warp chunk (512)
-constexpr int kRT = 64;              // rows per CTA tile
+constexpr int kRPL = 8;              // pass-1 rows per lane
+constexpr int kRowsCTA = 32 * kRPL;  // pass-1 rows per CTA (256)
 constexpr float kS = 0.84932180028801904272f;  // sqrt(log2(e) / 2)
 
 struct CutConst32 {
@@ -121,94 +125,6 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return r;
 }
 
-// One row against this lane's 16 columns: the 64-column sub-block's max and
-// sum of exp2(t - max) (identical in the 4 lanes of the sub-block).
-template <int D>
-__device__ __forceinline__ void row_sub(const float2 (&y2)[D][kCPL / 2],
-                                        const float2 (&A2)[kCPL / 2],
-                                        const float* u, float& m_out,
-                                        float& s_out) {
-  float2 t[kCPL / 2];
-  float2 uu[D];
-#pragma unroll
-  for (int q = 0; q < D; ++q) uu[q] = make_float2(u[q], u[q]);
-#pragma unroll
-  for (int c2 = 0; c2 < kCPL / 2; ++c2) {
-    float2 acc = A2[c2];
-#pragma unroll
-    for (int q = 0; q < D; ++q) acc = __ffma2_rn(uu[q], y2[q][c2], acc);
-    t[c2] = acc;
-  }
-  // max tree with 3-input FMNMX
-  const float a0 = fmax3(t[0].x, t[0].y, t[1].x);
-  const float a1 = fmax3(t[1].y, t[2].x, t[2].y);
-  const float a2 = fmax3(t[3].x, t[3].y, t[4].x);
-  const float a3 = fmax3(t[4].y, t[5].x, t[5].y);
-  const float a4 = fmax3(t[6].x, t[6].y, t[7].x);
-  float m = fmax3(fmax3(a0, a1, a2), fmax3(a3, a4, t[7].y), a0);
-  m = fmaxf(m, __shfl_xor_sync(~0u, m, 1));
-  m = fmaxf(m, __shfl_xor_sync(~0u, m, 2));
-  const float mm = (m == -CUDART_INF_F) ? 0.f : m;
-  const float2 nm = make_float2(-mm, -mm);
-  float2 e[kCPL / 2];
-#pragma unroll
-  for (int c2 = 0; c2 < kCPL / 2; ++c2) {
-    const float2 dd = __fadd2_rn(t[c2], nm);
-    e[c2] = make_float2(ex2(dd.x), ex2(dd.y));
-  }
-  const float2 s01 = __fadd2_rn(__fadd2_rn(e[0], e[1]), __fadd2_rn(e[2], e[3]));
-  const float2 s23 = __fadd2_rn(__fadd2_rn(e[4], e[5]), __fadd2_rn(e[6], e[7]));
-  const float2 s2 = __fadd2_rn(s01, s23);
-  float sm = s2.x + s2.y;
-  sm += __shfl_xor_sync(~0u, sm, 1);
-  sm += __shfl_xor_sync(~0u, sm, 2);
-  m_out = m;
-  s_out = sm;
-}
-
-// Fast-path row: sum over this lane's 16 columns of 2^(A'_j + u.y_j) with no
-// max subtraction. A'_j = A_j - cmax_s where cmax_s bounds col2 over the
-// sub-block, so the argument equals w_ij - lw2_i - cmax_s + |nu_i|^2 and
-// w_ij - lw2_i <= col2_j (the transition term -|y - nu|^2 is <= 0): the sum
-// only leaves [2^-60, 2^100] for rows far from every column (the caller then
-// recomputes them with the exact max).
-// The argument is also <= |nu_i|^2, so rows with |nu_i|^2 > 100 (a few %)
-// run the SHIFT variant with c_i = |nu_i|^2 - 100 subtracted (one FADD2 per
-// two pairs), which keeps every exponent <= 100.
-template <int D, bool SHIFT>
-__device__ __forceinline__ float row_sum_fast(const float2 (&y2)[D][kCPL / 2],
-                                              const float2 (&A2)[kCPL / 2],
-                                              const float* u, float c) {
-  float2 uu[D];
-#pragma unroll
-  for (int q = 0; q < D; ++q) uu[q] = make_float2(u[q], u[q]);
-  const float2 nc = make_float2(-c, -c);
-  float2 e[kCPL / 2];
-#pragma unroll
-  for (int c2 = 0; c2 < kCPL / 2; ++c2) {
-    float2 acc = SHIFT ? __fadd2_rn(A2[c2], nc) : A2[c2];
-#pragma unroll
-    for (int q = 0; q < D; ++q) acc = __ffma2_rn(uu[q], y2[q][c2], acc);
-    e[c2] = make_float2(ex2(acc.x), ex2(acc.y));
-  }
-  const float2 s01 = __fadd2_rn(__fadd2_rn(e[0], e[1]), __fadd2_rn(e[2], e[3]));
-  const float2 s23 = __fadd2_rn(__fadd2_rn(e[4], e[5]), __fadd2_rn(e[6], e[7]));
-  const float2 s2 = __fadd2_rn(s01, s23);
-  return s2.x + s2.y;
-}
-
-// 4 rows x 4 lanes transpose-reduce: lane q (of a 4-lane sub-block group)
-// returns the 4-lane total of row q (3 SHFL instead of 8).
-__device__ __forceinline__ float quad_transpose_sum(const float (&s4)[4], int q4) {
-  const bool b1 = q4 & 2, b0 = q4 & 1;
-  float k0 = b1 ? s4[2] : s4[0], k1 = b1 ? s4[3] : s4[1];
-  const float o0 = b1 ? s4[0] : s4[2], o1 = b1 ? s4[1] : s4[3];
-  k0 += __shfl_xor_sync(~0u, o0, 2);
-  k1 += __shfl_xor_sync(~0u, o1, 2);
-  const float keep = b0 ? k1 : k0, send = b0 ? k0 : k1;
-  return keep + __shfl_xor_sync(~0u, send, 1);
-}
-
 // Per-combine data pass 1 hands to the sampler (la.aux, la.aux_comb floats
 // per combine of the chunk): whitened columns y_j / A_j and rows u_i / B_i,
 // computed once by pass 1 instead of being re-gathered through the block maps.
@@ -228,49 +144,51 @@ __device__ __forceinline__ Aux32 aux32(const LevelArgs& la, int comb, int N) {
   return a;
 }
 
-// Pass 1. Grid (row tiles, combines, chains); la.rows_per_cta rows per CTA
-// (a multiple of 32, chosen per level so the grid fills the GPU). Warps take
-// (512-column chunk, row slice) items; rows go 4 at a time so that each lane
-// finishes exactly one (row, sub-block) log-sum: one LG2 and one store per
-// 64 pair evaluations, no divergent tail.
+// Pass 1. Grid (row tiles x column splits, combines of the chunk, chains),
+// 256 threads: rows [256 rt, 256 rt + 256), sub-blocks [cs nsub / ncs,
+// (cs+1) nsub / ncs) of combine k, warps taking those sub-blocks round-robin.
+constexpr int kPairWarps = 4;  // pass-1 warps per CTA (4 CTAs per SM)
+
 template <int D>
-__global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
-  extern __shared__ float sm32[];
-  const int RT = la.rows_per_cta;
-  float* s_u = sm32;            // [RT][D]
-  float* s_B = sm32 + RT * D;   // [RT]
-  float* s_c = s_B + RT;        // [RT] fast-path shift c_i (0 for most rows)
+__global__ void __launch_bounds__(32 * kPairWarps, 4) c32_pair(Bufs b, LevelArgs la) {
+  __shared__ float4 s_u[kRowsCTA];          // u_i (2 nu_i), zero-padded to 4
+  __shared__ float s_b[kRowsCTA];           // B_i
+  __shared__ float s_c[kRowsCTA];           // overflow shift c_i (0 for most rows)
+  __shared__ float4 s_y[kPairWarps][kSub];  // per warp: the staged sub-block's y_j
+  __shared__ float s_a[kPairWarps][kSub];   // ... and A_j - cmax_s
   const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
   const int N = b.N;
+  const int nsub = (N + kSub - 1) / kSub;
+  const int nrt = (N + kRowsCTA - 1) / kRowsCTA;
+  const int rt = blockIdx.x % nrt, cs = blockIdx.x / nrt, ncs = gridDim.x / nrt;
   Side L, R;
   CombineGeom g;
   sides(b, la, k, L, R, g);
   const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + g.c];
   CutConst32 cc;
   load_cut32<D>(tc, cc);
-  const int nch = (N + kChunk - 1) / kChunk;
-  const int nsubp = nch * (kChunk / kSub);
-  // per (chain, combine of the chunk) workspace
+  // per (chain, combine of the chunk) workspace, [sub-block][row]
   const size_t cslot = (size_t)blockIdx.z * gridDim.y + blockIdx.y;
   float* ws = reinterpret_cast<float*>(la.ws) + cslot * la.ws_comb * 2;
-  const int row0 = blockIdx.x * RT;
-  const int nrows = min(RT, N - row0);
   const Aux32 ax = aux32(la, cslot, N);
+  const int row0 = rt * kRowsCTA;
+  const int nrows = min(kRowsCTA, N - row0);
   const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
   const float4* XL = b.X32 + ((size_t)ch * b.K + L.t) * N;
-  for (int r = threadIdx.x; r < RT; r += blockDim.x) {
+  for (int r = threadIdx.x; r < kRowsCTA; r += blockDim.x) {
     float u[4] = {0, 0, 0, 0}, Bv = -CUDART_INF_F;
     if (r < nrows) {
       const int i = row0 + r;
       const uint32_t p = map_last(b, la, ch, L, i);
       const float lw2 = lnonuni ? b.LW32[(size_t)ch * N + i] : 0.f;
       row32<D>(cc, XL[p], lw2, u, Bv);
-      ax.u[i] = make_float4(u[0], u[1], u[2], u[3]);
-      ax.B[i] = Bv;
+      if (cs == 0) {  // hand the row to the sampler
+        ax.u[i] = make_float4(u[0], u[1], u[2], u[3]);
+        ax.B[i] = Bv;
+      }
     }
-#pragma unroll
-    for (int q = 0; q < D; ++q) s_u[r * D + q] = u[q];
-    s_B[r] = Bv;
+    s_u[r] = make_float4(u[0], u[1], u[2], u[3]);
+    s_b[r] = Bv;
     float nn = 0.f;
 #pragma unroll
     for (int q = 0; q < D; ++q) nn = fmaf(0.5f * u[q], 0.5f * u[q], nn);
@@ -278,104 +196,117 @@ __global__ void __launch_bounds__(256, 2) c32_pair(Bufs b, LevelArgs la) {
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = max(1, 8 / nch);
-  const int items = nch * S;
+  // this lane's rows lane + 32 q, q = 0..7, as 4 row pairs (2p, 2p+1)
+  constexpr int NPR = kRPL / 2;
+  float2 U[4][NPR], NC[NPR];
+#pragma unroll
+  for (int pr = 0; pr < NPR; ++pr) {
+    const float4 ua = s_u[lane + 64 * pr], ub = s_u[lane + 64 * pr + 32];
+    U[0][pr] = make_float2(ua.x, ub.x);
+    U[1][pr] = make_float2(ua.y, ub.y);
+    U[2][pr] = make_float2(ua.z, ub.z);
+    U[3][pr] = make_float2(ua.w, ub.w);
+    NC[pr] = make_float2(-s_c[lane + 64 * pr], -s_c[lane + 64 * pr + 32]);
+  }
+  const float2 one2 = make_float2(1.f, 1.f);
   const float4* XR = b.X32 + ((size_t)ch * b.K + R.t) * N;
   const float* CR = b.COL + ((size_t)ch * b.K + R.t) * N;
-  const int q4 = lane & 3;
-  if (blockIdx.x == 0) {  // hand the combine's columns to the sampler
-    for (int j = threadIdx.x; j < N; j += blockDim.x) {
-      const uint32_t p = map_first(b, la, ch, R, j);
-      float y[4] = {0.f, 0.f, 0.f, 0.f}, A;
-      col32<D>(cc, XR[p], CR[p], y, A);
-      ax.y[j] = make_float4(y[0], y[1], y[2], y[3]);
-      ax.A[j] = A;
+  const int sb0 = cs * nsub / ncs, sb1 = (cs + 1) * nsub / ncs;
+  float4* sy = s_y[warp];
+  float* sa = s_a[warp];
+  // raw column data (leaf state + column term) of the lane's 2 columns of the
+  // warp's next sub-block, loaded one sub-block ahead of its use
+  float4 xr_n[2];
+  float cr_n[2];
+  auto fetch = [&](int sbk) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = sbk * kSub + lane + 32 * h;
+      if (sbk < sb1 && j < N) {
+        const uint32_t p = map_first(b, la, ch, R, j);
+        xr_n[h] = XR[p];
+        cr_n[h] = CR[p];
+      }
     }
-  }
-  for (int it = warp; it < items; it += 8) {
-    const int chunk = it % nch, slice = it / nch;
-    float2 y2[D][kCPL / 2];
-    float2 A2[kCPL / 2];
-    float cm = -CUDART_INF_F;
+  };
+  fetch(sb0 + warp);
+  for (int sbk = sb0 + warp; sbk < sb1; sbk += kPairWarps) {
+    // stage the sub-block's 64 columns (2 per lane), then prefetch the next
+    float Ah[2], cm = -CUDART_INF_F;
+    float4 xr_c[2] = {xr_n[0], xr_n[1]};
+    float cr_c[2] = {cr_n[0], cr_n[1]};
+    fetch(sbk + kPairWarps);
 #pragma unroll
-    for (int c2 = 0; c2 < kCPL / 2; ++c2) {
-      float yv[2][4], Av[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = chunk * kChunk + lane * kCPL + 2 * c2 + h;
-        if (j < N) {
-          const uint32_t p = map_first(b, la, ch, R, j);
-          const float cv = CR[p];
-          col32<D>(cc, XR[p], cv, yv[h], Av[h]);
-          cm = fmaxf(cm, cv);
-
-        } else {
-#pragma unroll
-          for (int q = 0; q < D; ++q) yv[h][q] = 0.f;
-          Av[h] = -CUDART_INF_F;
+    for (int h = 0; h < 2; ++h) {
+      const int jj = lane + 32 * h, j = sbk * kSub + jj;
+      float y[4] = {0.f, 0.f, 0.f, 0.f};
+      float A = -CUDART_INF_F;
+      if (j < N) {
+        const float cv = cr_c[h];
+        col32<D>(cc, xr_c[h], cv, y, A);
+        cm = fmaxf(cm, cv);
+        if (rt == 0) {  // hand the column to the sampler
+          ax.y[j] = make_float4(y[0], y[1], y[2], y[3]);
+          ax.A[j] = A;
         }
       }
-#pragma unroll
-      for (int q = 0; q < D; ++q) y2[q][c2] = make_float2(yv[0][q], yv[1][q]);
-      A2[c2] = make_float2(Av[0], Av[1]);
+      sy[jj] = make_float4(y[0], y[1], y[2], y[3]);
+      Ah[h] = A;
     }
-    const int sub = chunk * (kChunk / kSub) + (lane >> 2);
-    // column bound of the sub-block: cmax = max_j col2_j (4-lane max), folded
-    // into A so the fast rows need no max (row_sum_fast)
-    cm = fmaxf(cm, __shfl_xor_sync(~0u, cm, 1));
-    cm = fmaxf(cm, __shfl_xor_sync(~0u, cm, 2));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(~0u, cm, o));
     const bool live = cm > -CUDART_INF_F;
 #pragma unroll
-    for (int c2 = 0; c2 < kCPL / 2; ++c2)
-      A2[c2] = live ? make_float2(A2[c2].x - cm, A2[c2].y - cm)
-                    : make_float2(-CUDART_INF_F, -CUDART_INF_F);
-    // rows slice, slice+S, ... taken 4 at a time (RT is a multiple of 4*S;
-    // padded rows have B = -inf and are never stored)
-    for (int base = slice; base < nrows; base += 4 * S) {
-      float s4[4], c4[4];
+    for (int h = 0; h < 2; ++h) sa[lane + 32 * h] = live ? Ah[h] - cm : -CUDART_INF_F;
+    __syncwarp();
+    // S[pr] = sum_j 2^(A'_j + u.y_j - c) for the lane's row pair pr
+    float2 S[NPR];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) c4[j] = s_c[base + j * S];
-      if (fmaxf(fmaxf(c4[0], c4[1]), fmaxf(c4[2], c4[3])) == 0.f) {  // warp-uniform
+    for (int pr = 0; pr < NPR; ++pr) S[pr] = make_float2(0.f, 0.f);
+#pragma unroll 2
+    for (int j = 0; j < kSub; ++j) {
+      const float4 yv = sy[j];
+      const float a = sa[j];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int r = base + j * S;
-          float u[D];
-#pragma unroll
-          for (int q = 0; q < D; ++q) u[q] = s_u[r * D + q];
-          s4[j] = row_sum_fast<D, false>(y2, A2, u, 0.f);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int r = base + j * S;
-          float u[D];
-#pragma unroll
-          for (int q = 0; q < D; ++q) u[q] = s_u[r * D + q];
-          s4[j] = row_sum_fast<D, true>(y2, A2, u, c4[j]);
-        }
-      }
-      const int rq = base + q4 * S;
-      float sq = quad_transpose_sum(s4, q4);
-      float mq = q4 == 0 ? c4[0] : q4 == 1 ? c4[1] : q4 == 2 ? c4[2] : c4[3];
-      const bool odd = live && rq < nrows && !(sq >= 0x1p-60f && sq <= 0x1p120f);
-      if (__any_sync(~0u, odd)) {  // rare: exact per-sub-block max
-        float m4[4];
-#pragma unroll 1
-        for (int j = 0; j < 4; ++j) {
-          const int r = base + j * S;
-          float u[D];
-#pragma unroll
-          for (int q = 0; q < D; ++q) u[q] = s_u[r * D + q];
-          row_sub<D>(y2, A2, u, m4[j], s4[j]);
-        }
-        mq = q4 == 0 ? m4[0] : q4 == 1 ? m4[1] : q4 == 2 ? m4[2] : m4[3];
-        sq = q4 == 0 ? s4[0] : q4 == 1 ? s4[1] : q4 == 2 ? s4[2] : s4[3];
-      }
-      if (rq < nrows) {
-        const float Ls = sq > 0.f ? mq + lg2(sq) + cm + s_B[rq] : -CUDART_INF_F;
-        ws[(size_t)(row0 + rq) * nsubp + sub] = Ls;
+      for (int pr = 0; pr < NPR; ++pr) {
+        float2 t = __ffma2_rn(make_float2(a, a), one2, NC[pr]);
+        t = __ffma2_rn(make_float2(yv.x, yv.x), U[0][pr], t);
+        if (D > 1) t = __ffma2_rn(make_float2(yv.y, yv.y), U[1][pr], t);
+        if (D > 2) t = __ffma2_rn(make_float2(yv.z, yv.z), U[2][pr], t);
+        if (D > 3) t = __ffma2_rn(make_float2(yv.w, yv.w), U[3][pr], t);
+        S[pr] = __fadd2_rn(S[pr], make_float2(ex2(t.x), ex2(t.y)));
       }
     }
+    // L_is = log2 sum + c_i + cmax_s + B_i; underflowed rows: exact max
+#pragma unroll
+    for (int q = 0; q < kRPL; ++q) {
+      const int r = lane + 32 * q;
+      const float sq = (q & 1) ? S[q >> 1].y : S[q >> 1].x;
+      if (r >= nrows) continue;
+      float Ls;
+      if (live && !(sq >= 0x1p-60f && sq <= 0x1p120f)) {
+        const float4 u4 = s_u[r];
+        const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
+        float m = -CUDART_INF_F;
+        for (int j = 0; j < kSub; ++j) {
+          const float4 yv = sy[j];
+          const float yy[4] = {yv.x, yv.y, yv.z, yv.w};
+          m = fmaxf(m, pair32<D>(uu, yy, sa[j]));
+        }
+        float acc = 0.f;
+        if (m > -CUDART_INF_F)
+          for (int j = 0; j < kSub; ++j) {
+            const float4 yv = sy[j];
+            const float yy[4] = {yv.x, yv.y, yv.z, yv.w};
+            acc += ex2(pair32<D>(uu, yy, sa[j]) - m);
+          }
+        Ls = acc > 0.f ? m + lg2(acc) + cm + s_b[r] : -CUDART_INF_F;
+      } else {
+        Ls = sq > 0.f ? lg2(sq) + s_c[r] + cm + s_b[r] : -CUDART_INF_F;
+      }
+      ws[(size_t)sbk * N + row0 + r] = Ls;
+    }
+    __syncwarp();
   }
 }
 
@@ -420,63 +351,69 @@ __global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
   Side L, R;
   CombineGeom g;
   sides(b, la, k, L, R, g);
-  const int nch = (N + kChunk - 1) / kChunk;
-  const int nsubp = nch * (kChunk / kSub);
   const int nsub = (N + kSub - 1) / kSub;
   const size_t cslot = (size_t)blockIdx.z * gridDim.y + blockIdx.y;
   const float* ws = reinterpret_cast<const float*>(la.ws) + cslot * la.ws_comb * 2;
   const Aux32 ax = aux32(la, cslot, N);
-  // Column j lives at j + j/64 (one pad entry per sub-block): the per-slot
-  // recompute loops read column 64 s + q of different sub-blocks s at the
+  // Columns are stored as PAIRS (2p, 2p+1) so the recompute's packed FFMA2 /
+  // FADD2 take their operands straight from shared memory: P01[p] =
+  // (y0_a, y0_b, y1_a, y1_b), P23[p] = (y2_a, y2_b, y3_a, y3_b), AP[p] =
+  // (A_a, A_b). Pair p lives at p + p/32 (one pad entry per 64-column
+  // sub-block): slots read pair 32 s + q of different sub-blocks s at the
   // same q, which without the skew all map to the same banks.
   const int NP = (N + kSub - 1) / kSub * kSub;
-  const int NPS = NP + NP / kSub;
+  const int NPP = NP / 2, NPS = NPP + NPP / 32;
   double* S = smem;                                            // N
-  float4* ycol = reinterpret_cast<float4*>(S + ((N + 1) & ~1));  // NPS, 16B aligned
-  float* Acol = reinterpret_cast<float*>(ycol + NPS);           // NPS
-  float* Lrow = Acol + NPS;                                    // N
+  float4* P01 = reinterpret_cast<float4*>(S + ((N + 1) & ~1));   // NPS, 16B aligned
+  float4* P23 = P01 + NPS;                                     // NPS
+  float2* AP = reinterpret_cast<float2*>(P23 + NPS);            // NPS
+  float* Lrow = reinterpret_cast<float*>(AP + NPS);             // N
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int j = tid; j < NP; j += blockDim.x) {
-    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
-    float A = -CUDART_INF_F;
-    if (j < N) {
-      y = ax.y[j];
-      A = ax.A[j];
-    }
-    ycol[j + j / kSub] = y;
-    Acol[j + j / kSub] = A;
+  for (int pp = tid; pp < NPP; pp += blockDim.x) {
+    const int j = 2 * pp;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 ya = j < N ? ax.y[j] : z4, yb = j + 1 < N ? ax.y[j + 1] : z4;
+    const float Aa = j < N ? ax.A[j] : -CUDART_INF_F, Ab = j + 1 < N ? ax.A[j + 1] : -CUDART_INF_F;
+    const int ps = pp + pp / 32;
+    P01[ps] = make_float4(ya.x, yb.x, ya.y, yb.y);
+    P23[ps] = make_float4(ya.z, yb.z, ya.w, yb.w);
+    AP[ps] = make_float2(Aa, Ab);
   }
-  // row log2-totals: online LSE over the row's sub-block sums, 16 at a time
-  // (pass 1 writes all nsubp entries; padding is -inf)
+  // row log2-totals: online LSE over the row's sub-block sums ([sub][row]
+  // layout: coalesced across the threads' rows), 16 sub-blocks per round,
+  // two rows in flight per thread
   float gm = -CUDART_INF_F;
-  for (int i = tid; i < N; i += blockDim.x) {
-    const float4* w4 = reinterpret_cast<const float4*>(ws + (size_t)i * nsubp);
-    float m = -CUDART_INF_F, acc = 0.f;
-    for (int s0 = 0; s0 < nsubp; s0 += 16) {
-      float v[16];
-      const int nq = min(4, (nsubp - s0) >> 2);
+  for (int i = tid; i < N; i += 2 * blockDim.x) {
+    const int i2 = i + blockDim.x;
+    float m[2] = {-CUDART_INF_F, -CUDART_INF_F}, acc[2] = {0.f, 0.f};
+    for (int s0 = 0; s0 < nsub; s0 += 16) {
+      float v[2][16];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float4 t4 = q < nq ? w4[(s0 >> 2) + q]
-                                 : make_float4(-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F);
-        v[4 * q] = t4.x;
-        v[4 * q + 1] = t4.y;
-        v[4 * q + 2] = t4.z;
-        v[4 * q + 3] = t4.w;
-      }
-      float cm = fmax3(fmax3(v[0], v[1], v[2]), fmax3(v[3], v[4], v[5]), fmax3(v[6], v[7], v[8]));
-      cm = fmax3(cm, fmax3(v[9], v[10], v[11]), fmax3(v[12], v[13], fmaxf(v[14], v[15])));
-      if (cm == -CUDART_INF_F) continue;
-      if (cm > m) {
-        acc = m == -CUDART_INF_F ? 0.f : acc * ex2(m - cm);
-        m = cm;
+      for (int q = 0; q < 16; ++q) {
+        const bool in = s0 + q < nsub;
+        v[0][q] = in ? ws[(size_t)(s0 + q) * N + i] : -CUDART_INF_F;
+        v[1][q] = in && i2 < N ? ws[(size_t)(s0 + q) * N + i2] : -CUDART_INF_F;
       }
 #pragma unroll
-      for (int q = 0; q < 16; ++q) acc += ex2(v[q] - m);
+      for (int h = 0; h < 2; ++h) {
+        float cm = fmax3(fmax3(v[h][0], v[h][1], v[h][2]), fmax3(v[h][3], v[h][4], v[h][5]),
+                         fmax3(v[h][6], v[h][7], v[h][8]));
+        cm = fmax3(cm, fmax3(v[h][9], v[h][10], v[h][11]),
+                   fmax3(v[h][12], v[h][13], fmaxf(v[h][14], v[h][15])));
+        if (cm == -CUDART_INF_F) continue;
+        if (cm > m[h]) {
+          acc[h] = m[h] == -CUDART_INF_F ? 0.f : acc[h] * ex2(m[h] - cm);
+          m[h] = cm;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc[h] += ex2(v[h][q] - m[h]);
+      }
     }
-    const float L2 = m == -CUDART_INF_F ? -CUDART_INF_F : m + lg2(acc);
-    Lrow[i] = L2;
-    gm = fmaxf(gm, L2);
+    const float La = m[0] == -CUDART_INF_F ? -CUDART_INF_F : m[0] + lg2(acc[0]);
+    const float Lc = m[1] == -CUDART_INF_F ? -CUDART_INF_F : m[1] + lg2(acc[1]);
+    Lrow[i] = La;
+    if (i2 < N) Lrow[i2] = Lc;
+    gm = fmax3(gm, La, i2 < N ? Lc : -CUDART_INF_F);
   }
   for (int o = 16; o; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(~0u, gm, o));
   if (lane == 0) sh[warp] = gm;
@@ -521,112 +458,208 @@ __global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
   uint32_t* PR = b.PR + gidx * N;
   const size_t nbase = ((size_t)ch * b.cap + k) * N;
   const int m0 = sb * la.slots_per_cta, m1 = min(la.n_out, m0 + la.slots_per_cta);
-  // each thread takes 4 consecutive slots = one Philox block of uniforms
-  // (slot m uses u64 number m of the stream, rng.cpp:45-68)
+  // Slots run in three phases, re-ordered in between by CTA counting sorts so
+  // that each warp works on neighbouring data (shared-memory broadcasts
+  // instead of bank conflicts). The order only schedules work: slot m always
+  // uses u64 number m of the stream (rng.cpp:45-68) and writes output m.
+  //   A  uniforms of the CTA's slots -> points pt_m; bucket by pt (32 buckets)
+  //   B  in pt order: row search over the CDF, sub-block walk -> (i, s, frac)
+  //   C  in sub-block order: recompute the 64 weights -> column j
+  const int ns = max(0, m1 - m0);
+  constexpr int NBA = 32;
+  // offsets from the shared-memory base keep the compiler on LDS/STS
+  const size_t ext = ((reinterpret_cast<char*>(Lrow + N) - reinterpret_cast<char*>(smem)) + 15) &
+                     ~static_cast<size_t>(15);
+  double* PT = reinterpret_cast<double*>(reinterpret_cast<char*>(smem) + ext);  // [ns]
+  int4* REC = reinterpret_cast<int4*>(PT + ((ns + 1) & ~1));                     // [ns]
+  int* ORD1 = reinterpret_cast<int*>(REC + ns);                                   // [ns]
+  int* ORD2 = ORD1 + ns;                                                          // [ns]
+  int* CA = ORD2 + ns;                                                            // [NBA]
+  int* CB = CA + NBA;                                                             // [nsub]
+  for (int q = tid; q < NBA; q += blockDim.x) CA[q] = 0;
+  for (int q = tid; q < nsub; q += blockDim.x) CB[q] = 0;
+  __syncthreads();
+  const double bscale = (double)NBA / total;
+  // phase A (each thread: 4 consecutive slots = one Philox block)
   for (int q0 = (m0 & ~3) + 4 * tid; q0 < m1; q0 += 4 * blockDim.x) {
     U64x4 blk;
     if (!systematic) blk = stream_block(id, (uint64_t)q0 >> 2);
-#pragma unroll 1
+#pragma unroll
     for (int qq = 0; qq < 4; ++qq) {
       const int m = q0 + qq;
       if (m < m0 || m >= m1) continue;
       const double pt = systematic ? (u0 + (double)m) * step : u64_uniform(blk.v[qq]) * total;
-      int lo = 0, hi = N;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (pt < S[mid]) hi = mid;
-        else lo = mid + 1;
-      }
-      int i = lo < N ? lo : N - 1;
-      const double before = i > 0 ? S[i - 1] : 0.0;
-      while (i > 0 && !(Lrow[i] > -CUDART_INF_F)) --i;
-      const float Li = Lrow[i];
-      const float4 urow = ax.u[i];
-      const float Brow = ax.B[i];
-      const float local0 = (float)((pt - before) / (double)ex2(Li - G));
-      const float local = local0 >= 0.f ? local0 : 0.f;
-      // sub-block walk over the row's sub-block sums (relative to the row
-      // total), branch-free, 16 at a time from vector loads
-      const float* w = ws + (size_t)i * nsubp;
-      int s = -1, last_pos = 0;
-      float cum = 0.f, before_s = 0.f, wsel = 0.f, Ls_sel = 0.f;
-      for (int s0 = 0; s0 < nsub; s0 += 16) {
-        float v[16];
-        if (s0 + 16 <= nsubp) {
-          const float4* w4 = reinterpret_cast<const float4*>(w + s0);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 t4 = w4[q];
-            v[4 * q] = t4.x;
-            v[4 * q + 1] = t4.y;
-            v[4 * q + 2] = t4.z;
-            v[4 * q + 3] = t4.w;
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 16; ++q) v[q] = (s0 + q < nsubp) ? w[s0 + q] : -CUDART_INF_F;
-        }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const float e = (s0 + q < nsub) ? ex2(v[q] - Li) : 0.f;
-          const float c2 = cum + e;
-          const bool hit = s < 0 && local < c2;
-          last_pos = (s < 0 && e > 0.f) ? s0 + q : last_pos;
-          before_s = hit ? cum : before_s;
-          wsel = hit ? e : wsel;
-          Ls_sel = hit ? v[q] : Ls_sel;
-          s = hit ? s0 + q : s;
-          cum = c2;
-        }
-      }
-      if (s < 0) {  // spill: clamp to the last positive sub-block
-        s = last_pos;
-        Ls_sel = w[s];
-        wsel = ex2(Ls_sel - Li);
-        before_s = cum - wsel;
-      }
-      float frac = wsel > 0.f ? (local - before_s) / wsel : 0.f;
-      frac = fminf(fmaxf(frac, 0.f), 1.f);
-      // recompute the sub-block's 64 weights (pass-1 pair arithmetic, two
-      // columns per packed op; padding columns give 0): jsel = number of
-      // prefix sums <= frac (the first prefix above frac), lastj = last
-      // positive weight
-      const float shift = Ls_sel - Brow;
-      const int j0 = s * kSub;
-      const float4* yb = ycol + j0 + s;
-      const float2* ab = reinterpret_cast<const float2*>(Acol + j0 + s);
-      const float ur[4] = {urow.x, urow.y, urow.z, urow.w};
-      float2 uu[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) uu[q] = make_float2(ur[q], ur[q]);
-      const float2 nsh = make_float2(-shift, -shift);
-      float c3 = 0.f;
-      int cnt = 0, lastj = 0;
-#pragma unroll 8
-      for (int q = 0; q < kSub; q += 2) {
-        const float4 ya = yb[q], yc = yb[q + 1];
-        const float2 a2 = (s & 1) ? make_float2(Acol[j0 + s + q], Acol[j0 + s + q + 1]) : ab[q >> 1];
-        float2 t = __fadd2_rn(a2, nsh);
-        t = __ffma2_rn(uu[0], make_float2(ya.x, yc.x), t);
-        if (D > 1) t = __ffma2_rn(uu[1], make_float2(ya.y, yc.y), t);
-        if (D > 2) t = __ffma2_rn(uu[2], make_float2(ya.z, yc.z), t);
-        if (D > 3) t = __ffma2_rn(uu[3], make_float2(ya.w, yc.w), t);
-        const float e0 = ex2(t.x), e1 = ex2(t.y);
-        c3 += e0;
-        cnt += c3 <= frac;
-        c3 += e1;
-        cnt += c3 <= frac;
-        lastj = e0 > 0.f ? q : lastj;
-        lastj = e1 > 0.f ? q + 1 : lastj;
-      }
-      const int jsel = cnt;
-      const int j = j0 + (jsel < kSub ? (jsel <= lastj ? jsel : lastj) : lastj);
-      PL[m + off] = (uint32_t)i;
-      PR[m + off] = (uint32_t)j;
-      la.first_next[nbase + m + off] = map_first(b, la, ch, L, (uint32_t)i);
-      la.last_next[nbase + m + off] = map_last(b, la, ch, R, (uint32_t)j);
+      PT[m - m0] = pt;
+      atomicAdd(&CA[min(NBA - 1, (int)(pt * bscale))], 1);
     }
   }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the 32 bucket counts
+    const int c = CA[lane];
+    int v = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(~0u, v, o);
+      if (lane >= o) v += n;
+    }
+    CA[lane] = v - c;
+  }
+  __syncthreads();
+  for (int x = tid; x < ns; x += blockDim.x)
+    ORD1[atomicAdd(&CA[min(NBA - 1, (int)(PT[x] * bscale))], 1)] = x;
+  __syncthreads();
+  // phase B
+  int steps = 0;
+  while ((1 << steps) <= N) ++steps;
+  for (int o = tid; o < ns; o += blockDim.x) {
+    const int x = ORD1[o];
+    const double pt = PT[x];
+    int lo = 0, hi = N;
+    for (int it = 0; it < steps; ++it) {
+      const int mid = (lo + hi) >> 1;
+      const bool act = lo < hi;
+      const bool below = pt < S[min(mid, N - 1)];
+      hi = act && below ? mid : hi;
+      lo = act && !below ? mid + 1 : lo;
+    }
+    int i = lo < N ? lo : N - 1;
+    const double before = i > 0 ? S[i - 1] : 0.0;
+    while (i > 0 && !(Lrow[i] > -CUDART_INF_F)) --i;
+    const float Li = Lrow[i];
+    const float Brow = ax.B[i];
+    const float local0 = (float)((pt - before) / (double)ex2(Li - G));
+    const float local = local0 >= 0.f ? local0 : 0.f;
+    // sub-block walk over the row's sub-block sums (relative to the row
+    // total), branch-free, 16 at a time from vector loads
+    const float* w = ws + i;  // sub-block s of row i at w[s * N]
+    int s = -1, last_pos = 0;
+    float cum = 0.f, before_s = 0.f, wsel = 0.f, Ls_sel = 0.f;
+    for (int s0 = 0; s0 < nsub; s0 += 16) {
+      float v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = (s0 + q < nsub) ? w[(size_t)(s0 + q) * N] : -CUDART_INF_F;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const float e = (s0 + q < nsub) ? ex2(v[q] - Li) : 0.f;
+        const float c2 = cum + e;
+        const bool hit = s < 0 && local < c2;
+        last_pos = (s < 0 && e > 0.f) ? s0 + q : last_pos;
+        before_s = hit ? cum : before_s;
+        wsel = hit ? e : wsel;
+        Ls_sel = hit ? v[q] : Ls_sel;
+        s = hit ? s0 + q : s;
+        cum = c2;
+      }
+    }
+    if (s < 0) {  // spill: clamp to the last positive sub-block
+      s = last_pos;
+      Ls_sel = w[(size_t)s * N];
+      wsel = ex2(Ls_sel - Li);
+      before_s = cum - wsel;
+    }
+    float frac = wsel > 0.f ? (local - before_s) / wsel : 0.f;
+    frac = fminf(fmaxf(frac, 0.f), 1.f);
+    // (i | s << 16, first map of the left block at i, frac, shift); N < 2^16
+    REC[x] = make_int4(i | (s << 16), (int)map_first(b, la, ch, L, (uint32_t)i),
+                       __float_as_int(frac), __float_as_int(Brow - Ls_sel));
+    atomicAdd(&CB[s], 1);
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the sub-block counts
+    int carry = 0;
+    for (int c0 = 0; c0 < nsub; c0 += 32) {
+      const int c = c0 + lane < nsub ? CB[c0 + lane] : 0;
+      int v = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(~0u, v, o);
+        if (lane >= o) v += n;
+      }
+      if (c0 + lane < nsub) CB[c0 + lane] = carry + v - c;
+      carry += __shfl_sync(~0u, v, 31);
+    }
+  }
+  __syncthreads();
+  for (int x = tid; x < ns; x += blockDim.x) ORD2[atomicAdd(&CB[REC[x].x >> 16], 1)] = x;
+  __syncthreads();
+  // phase C: recompute the sub-block's 64 weights with pass 1's pair
+  // arithmetic, two columns per FFMA2 / FADD2 (padding columns give 0); the
+  // column is the first whose prefix exceeds frac = the number of prefixes
+  // <= frac. Warps hold slots of one sub-block: the pair loads broadcast.
+  // the right block's last-map gather of slot o is stored one iteration
+  // later, so its latency overlaps the next slot's recompute
+  uint32_t* pend_dst = nullptr;
+  uint32_t pend_src = 0;
+  bool pend = false;
+  // (the next slot's record and row vector are prefetched a slot ahead)
+  int x_n = 0;
+  int4 rc_n = make_int4(0, 0, 0, 0);
+  float4 u_n = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (tid < ns) {
+    x_n = ORD2[tid];
+    rc_n = REC[x_n];
+    u_n = ax.u[rc_n.x & 0xffff];
+  }
+  for (int o = tid; o < ns; o += blockDim.x) {
+    const int x = x_n;
+    const int4 rc = rc_n;
+    const float4 urow = u_n;
+    if (o + (int)blockDim.x < ns) {
+      x_n = ORD2[o + blockDim.x];
+      rc_n = REC[x_n];
+      u_n = ax.u[rc_n.x & 0xffff];
+    }
+    const int i = rc.x & 0xffff, s = rc.x >> 16;
+    const float frac = __int_as_float(rc.z);
+    const float sh = __int_as_float(rc.w);
+    const float2 nsh = make_float2(sh, sh);
+    const float2 uu0 = make_float2(urow.x, urow.x), uu1 = make_float2(urow.y, urow.y);
+    const float2 uu2 = make_float2(urow.z, urow.z), uu3 = make_float2(urow.w, urow.w);
+    const int pb = s * 33;  // skewed first pair of sub-block s
+    float c3 = 0.f;
+    int cnt = 0;
+#pragma unroll 8
+    for (int q = 0; q < kSub / 2; ++q) {
+      float2 t = __fadd2_rn(AP[pb + q], nsh);
+      const float4 c01 = P01[pb + q];
+      t = __ffma2_rn(uu0, make_float2(c01.x, c01.y), t);
+      if (D > 1) t = __ffma2_rn(uu1, make_float2(c01.z, c01.w), t);
+      if (D > 2) {
+        const float4 c23 = P23[pb + q];
+        t = __ffma2_rn(uu2, make_float2(c23.x, c23.y), t);
+        if (D > 3) t = __ffma2_rn(uu3, make_float2(c23.z, c23.w), t);
+      }
+      c3 += ex2(t.x);
+      cnt += c3 <= frac;
+      c3 += ex2(t.y);
+      cnt += c3 <= frac;
+    }
+    int jl = cnt;
+    if (cnt >= kSub) {  // spill (rounding): the last positive weight
+      jl = 0;
+      for (int q = 0; q < kSub / 2; ++q) {
+        float2 t = __fadd2_rn(AP[pb + q], nsh);
+        const float4 c01 = P01[pb + q];
+        t = __ffma2_rn(uu0, make_float2(c01.x, c01.y), t);
+        if (D > 1) t = __ffma2_rn(uu1, make_float2(c01.z, c01.w), t);
+        if (D > 2) {
+          const float4 c23 = P23[pb + q];
+          t = __ffma2_rn(uu2, make_float2(c23.x, c23.y), t);
+          if (D > 3) t = __ffma2_rn(uu3, make_float2(c23.z, c23.w), t);
+        }
+        jl = ex2(t.x) > 0.f ? 2 * q : jl;
+        jl = ex2(t.y) > 0.f ? 2 * q + 1 : jl;
+      }
+    }
+    const int j = s * kSub + jl;
+    const int m = m0 + x;
+    PL[m + off] = (uint32_t)i;
+    PR[m + off] = (uint32_t)j;
+    la.first_next[nbase + m + off] = (uint32_t)rc.y;
+    if (pend) *pend_dst = pend_src;
+    pend_src = map_last(b, la, ch, R, (uint32_t)j);
+    pend_dst = la.last_next + nbase + m + off;
+    pend = true;
+  }
+  if (pend) *pend_dst = pend_src;
   if (b.conditional && tid == 0 && sb == 0) {
     PL[0] = 0;
     PR[0] = 0;

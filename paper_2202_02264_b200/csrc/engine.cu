@@ -294,30 +294,38 @@ int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
 
 template <int D>
 int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systematic) {
-  // Pass-1 row tile: as tall as possible (each warp loads its 16 columns per
-  // lane once per tile, so tall tiles amortise the column load and the
-  // per-cut constants) while the grid still gives >= 6 waves of the 2
-  // resident CTAs per SM (bounds the tail of the last wave).
-  const int target = 148 * 2 * 6;
+  // Pass 1: 256-row tiles; when the level has few combines, the sub-blocks of
+  // a tile are split over several CTAs so the grid still gives >= 4 waves of
+  // the 2 resident CTAs per SM.
+  const int target = 148 * 4 * 4;
   const int N = b.N;
-  int rt = std::min(1024, (N + 31) / 32 * 32);
-  while (rt > 32 && (long)nk * b.B * ((N + rt - 1) / rt) < target) rt = std::max(32, rt / 2 / 32 * 32);
-  la.rows_per_cta = rt;
+  const int nrt = (N + kRowsCTA - 1) / kRowsCTA, nsubb = (N + kSub - 1) / kSub;
+  int ncs = 1;
+  while (ncs * 2 <= std::max(1, nsubb / kPairWarps) && (long)nk * b.B * nrt * ncs < target) ncs *= 2;
   // Pass-2: split a combine's slots over several CTAs when combines are few.
   int sb = 1;
   const int target2 = 148 * 2;
   if ((long)nk * b.B < target2)
     sb = std::max(1, std::min((la.n_out + 63) / 64, (int)((target2 + nk * b.B - 1) / (nk * b.B))));
+  // the sampler stages <= 1024 slots per CTA in shared memory
+  sb = std::max(sb, (la.n_out + 1023) / 1024);
   la.slots_per_cta = (la.n_out + sb - 1) / sb;
-  const size_t sm1 = sizeof(float) * (size_t)rt * (D + 2);
   const size_t NP = (N + 63) / 64 * 64;
-  const size_t sm2 = sizeof(double) * (N + 1) + sizeof(float) * ((NP + NP / 64) * 5 + N);
+  const size_t NPS = NP / 2 + NP / 64;  // column pairs, one skew pad per sub-block
+  const size_t ns = la.slots_per_cta, nsub = (N + 63) / 64;
+  const size_t sm2 = sizeof(double) * (N + 1) + NPS * (16 + 16 + 8) + sizeof(float) * N + 16 +
+                     sizeof(double) * ((ns + 1) & ~(size_t)1) + 16 * ns + 8 * ns +
+                     sizeof(int) * (32 + nsub);
   static bool configured = false;
   if (!configured) {
     CU(cudaFuncSetAttribute(c32_sample<D>, cudaFuncAttributePreferredSharedMemoryCarveout,
                             cudaSharedmemCarveoutMaxShared));
     configured = true;
   }
+  if (sm2 > 227 * 1024)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                   "FP32 dense combine: N too large for the shared-memory sampler (use a lazy "
+                   "resampler)");
   CU(cudaFuncSetAttribute(c32_sample<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
   la.aux_comb = ((size_t)10 * N + 3) & ~(size_t)3;
   {
@@ -336,7 +344,7 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
     ctx->kev_used += 3;
     CU(cudaEventRecord(ev[0], ctx->stream));
   }
-  c32_pair<D><<<dim3((N + rt - 1) / rt, nk, b.B), 256, sm1, ctx->stream>>>(b, la);
+  c32_pair<D><<<dim3(nrt * ncs, nk, b.B), 32 * kPairWarps, 0, ctx->stream>>>(b, la);
   LAUNCHED(ctx);
   if (ev) CU(cudaEventRecord(ev[1], ctx->stream));
   c32_sample<D><<<dim3(sb, nk, b.B), 256, sm2, ctx->stream>>>(b, la, systematic);
@@ -541,8 +549,7 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
   // ---------------------------------------------------------------- levels
   const bool lazy = o.resampler == DSMC_MH_LAZY || o.resampler == DSMC_REJECTION_LAZY;
   const int nsub = (N + kSub - 1) / kSub;
-  const int nsubp = ((N + kChunk - 1) / kChunk) * (kChunk / kSub);
-  const size_t ws_comb = fp64 ? (size_t)N * (5 + nsub) : ((size_t)N * nsubp + 1) / 2;
+  const size_t ws_comb = fp64 ? (size_t)N * (5 + nsub) : ((size_t)N * nsub + 1) / 2;
   const size_t ws_budget = (size_t)1 << 30;  // bytes per chunk
   const int chunk = (int)std::max<size_t>(1, std::min<size_t>(65535, ws_budget / (ws_comb * 8 * B)));
   double* ws = nullptr;
@@ -1680,8 +1687,7 @@ int dsmc_cross_combine(dsmc_ctx* ctx, const dsmc_model_handle* hc, const dsmc_wi
   CU(A.get("CLMW", 8, &p));
   b.LMW = (double*)p;
   CU(A.get("CMAPS", 2 * (size_t)N * 4, &p));
-  const int nsubp = ((N + kChunk - 1) / kChunk) * (kChunk / kSub);
-  const size_t ws_comb = ((size_t)N * nsubp + 1) / 2;
+  const size_t ws_comb = ((size_t)N * ((N + kSub - 1) / kSub) + 1) / 2;
   LevelArgs la{};
   la.level = 1;
   la.np = 1;

@@ -23,11 +23,20 @@ def _z(mean, km, kP):
 def test_lgssm_means_match_kalman(engine, precision):
     m = models.lgssm_check(255)
     km, kP, ll = kalman_smooth(m)
-    r = engine.smooth(m, 2048, abi.MULTINOMIAL, seed=3, precision=precision)
-    z = _z(r["mean"], km, kP)
-    # standardized error ~ 1/sqrt(N_eff); N_eff >= 256 here -> rms <= 0.1
-    assert np.sqrt(np.mean(z ** 2)) < 0.1, np.sqrt(np.mean(z ** 2))
-    assert np.abs(z).max() < 0.45
+    # standardized error ~ 1/sqrt(N_eff): at N = 2048, N * mean z^2 ~ 13.5 for
+    # both precisions (tools/zcheck.py, 12 seeds); a single run's mean z^2 has
+    # a heavy right tail (errors are correlated along the path), so the bound
+    # is on the 4-seed average: rms <= 0.1 is ~4 standard errors above it
+    # (max |z| over t: median 0.25, p90 0.34, worst of 40 seeds ~0.7 for both
+    # precisions, tools/zcheck2.py — so the bound is on the 4-seed median)
+    zs, mx = [], []
+    for seed in (3, 4, 5, 6):
+        r = engine.smooth(m, 2048, abi.MULTINOMIAL, seed=seed, precision=precision)
+        z = _z(r["mean"], km, kP)
+        zs.append(np.mean(z ** 2))
+        mx.append(np.abs(z).max())
+    assert np.sqrt(np.mean(zs)) < 0.1, np.sqrt(np.mean(zs))
+    assert np.median(mx) < 0.45, mx
     # posterior variances within 15%
     ratio = r["cov"][:, 0, 0] / kP[:, 0, 0]
     assert 0.85 < np.median(ratio) < 1.15
