@@ -767,6 +767,14 @@ int dsmc_create(int device, dsmc_ctx** out) {
   }
   for (auto& e : ctx->ev) cudaEventCreate(&e);
   cudaMallocHost(&ctx->h_lnc, sizeof(double) * 4096);
+  // model uploads use the stream-ordered pool (cudaMallocAsync); keep freed
+  // blocks mapped so repeated uploads (e2e calls, pGibbs sweeps) reuse them
+  // instead of re-mapping up to ~1 GB of per-time constants every call
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   *out = ctx;
   return DSMC_OK;
 }

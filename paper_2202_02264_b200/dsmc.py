@@ -164,8 +164,10 @@ class Engine:
     def smooth(self, model, n_particles, resampler=abi.MULTINOMIAL, seed=0,
                precision=abi.FP32, mh_steps=16, inject_states=None,
                inject_logw=None, want_paths=False, want_moments=True,
-               want_pairs=False, want_leaves=False):
-        """run_smoother (smoother.hpp:128-129) on the GPU; host in/out."""
+               want_pairs=False, want_leaves=False, mean_out=None, cov_out=None):
+        """run_smoother (smoother.hpp:128-129) on the GPU; host in/out.
+        mean_out / cov_out: optional preallocated (e.g. pinned) host arrays of
+        shape (K, d) / (K, d, d) that receive the moments."""
         K, d, N, T = model.horizon + 1, model.d, n_particles, model.horizon
         inj_x = None if inject_states is None else np.ascontiguousarray(inject_states, np.float64)
         inj_w = None if inject_logw is None else np.ascontiguousarray(inject_logw, np.float64)
@@ -173,8 +175,8 @@ class Engine:
                               abi.dptr(inj_x), abi.dptr(inj_w))
         res = {}
         paths = np.zeros((K, N, d)) if want_paths else None
-        mean = np.zeros((K, d)) if want_moments else None
-        cov = np.zeros((K, d, d)) if want_moments else None
+        mean = (mean_out if mean_out is not None else np.zeros((K, d))) if want_moments else None
+        cov = (cov_out if cov_out is not None else np.zeros((K, d, d))) if want_moments else None
         pl = np.zeros((max(T, 1), N), np.uint32) if want_pairs else None
         pr = np.zeros((max(T, 1), N), np.uint32) if want_pairs else None
         lmw = np.zeros(max(T, 1)) if want_pairs else None
