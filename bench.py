@@ -52,6 +52,9 @@ CONFIGS = {
                model="sv", K=1 << 16, N=4096, resampler=2),
     "c5": dict(desc="C5: 2-D constant-velocity LGSSM d=4, K=T+1=2^20, N=1024, multinomial, "
                     "RTS-marginal proposals", model="cv", K=1 << 20, N=1024, resampler=0),
+    "c4": dict(desc="C4: SV particle Gibbs (batched c-dSMC sweep + device parameter kernel), "
+                    "64 chains, K=T+1=2^12, N=512, multinomial", model="sv_pgibbs", K=1 << 12,
+               N=512, resampler=0, chains=64),
 }
 DEFAULT_CONFIG = "c5"
 METRIC = "smoothed particle-timesteps/sec (T·N/s)"
@@ -216,7 +219,56 @@ def _max_over_ranks(v, world, device):
     return float(t.item())
 
 
+def run_pgibbs(args, cfg, rank, world, device):
+    """C4: one step = one particle-Gibbs sweep of this rank's chains (chains
+    shard across ranks: replicas, no exchange). T.N/s counts every chain."""
+    import torch
+    from paper_2202_02264_b200 import abi, models
+    from paper_2202_02264_b200.dsmc import Engine
+    torch.cuda.set_device(device)
+    eng = Engine(device)
+    K, N, B = cfg["K"], cfg["N"], cfg["chains"] // world
+    ys = np.asarray(models.sv(K - 1).arrays["y"], np.float64)
+    prior = abi.SvPrior(-1.0, 1.0, 2.0, 0.2, 0.05)
+    theta = torch.empty((B, 3), dtype=torch.float64, pin_memory=True).numpy()
+    stars = torch.empty((B, K), dtype=torch.float64, pin_memory=True).numpy()
+    theta[:] = [-1.0, 0.9, 0.1]
+    stars[:] = -1.0
+    seeds = np.arange(B, dtype=np.uint64) + 1000 * (rank + 1)
+    stream = torch.cuda.ExternalStream(eng.stream_handle(), device=torch.device("cuda", device))
+
+    def step(s):
+        eng.sv_pgibbs_sweep(ys, theta, stars, seeds, prior, N, s)
+    for w in range(args.warmup):
+        step(w)
+    launches0 = eng.launches
+    with ClockSampler(device) as clocks:
+        ms = _time_steps(stream, args.steps, lambda s: step(args.warmup + s), world, device)
+    launches = eng.launches - launches0
+    value = cfg["chains"] * K * N / (ms * 1e-3)
+    out = None
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": "f32+f64 (FP32 c-dSMC, FP64 parameter kernel)",
+               "data": "synthetic SV series (numpy seed 90210)",
+               "config": {"workload": cfg["desc"], "K": K, "N": N, "chains": cfg["chains"],
+                          "parallelism": f"chains split x{world}" if world > 1 else "single GPU"},
+               "e2e": {"value": value, "unit": UNIT,
+                       "h2d_bytes_per_step": int(theta.nbytes + stars.nbytes + ys.nbytes),
+                       "d2h_bytes_per_step": int(theta.nbytes + stars.nbytes + B * K),
+                       "api": "dsmc_sv_pgibbs_sweep (C ABI) with host arrays: value is already "
+                              "end to end"},
+               "gpu_launches": int(launches), "clocks": clocks.summary(),
+               "chain_state": {"mean_theta": theta.mean(0).tolist()}}
+    eng.close()
+    return out
+
+
 def run_ours(args, cfg, rank, world, device):
+    if cfg["model"] == "sv_pgibbs":
+        return run_pgibbs(args, cfg, rank, world, device)
     import torch
     from paper_2202_02264_b200.dsmc import Engine
     from paper_2202_02264_b200.sharded import GpuBackend, TorchComm, sharded_smooth
@@ -394,7 +446,7 @@ def main():
             torch.distributed.init_process_group(backend)
     out = run_ours(args, cfg, rank, world, local)
     if rank == 0:
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and cfg["model"] != "sv_pgibbs":
             cb = cpu_reference(cfg)
             if cb is not None:
                 v, cores, sample, wall, _ = cb

@@ -256,6 +256,28 @@ class Engine:
     def window_finish(self, d_root_map, d_mean, d_cov):
         self._check(self.lib.dsmc_window_finish(self.ctx, d_root_map, d_mean, d_cov))
 
+    # --------------------------------------------------------- SV pGibbs
+    def sv_pgibbs_sweep(self, ys, theta, stars, seeds, prior, n_particles, sweep,
+                        resampler=abi.MULTINOMIAL):
+        """One batched SV particle-Gibbs sweep (pgibbs_sweep, pgibbs.hpp:55-59):
+        theta (B, 3) = (mu, phi, sigma2) and stars (B, T+1) are updated IN
+        PLACE (float64, C-contiguous); returns (changed (B, T+1) bool, number
+        of accepted phi moves)."""
+        theta = np.asarray(theta)
+        stars = np.asarray(stars)
+        assert theta.dtype == np.float64 and theta.flags.c_contiguous
+        assert stars.dtype == np.float64 and stars.flags.c_contiguous
+        B, K = stars.shape
+        ys = np.ascontiguousarray(ys, np.float64)
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        changed = np.zeros((B, K), np.uint8)
+        acc = C.c_uint64()
+        self._check(self.lib.dsmc_sv_pgibbs_sweep(
+            self.ctx, B, K - 1, abi.dptr(ys), C.byref(prior), abi.dptr(theta), abi.dptr(stars),
+            seeds.ctypes.data_as(C.POINTER(C.c_uint64)), n_particles, resampler, sweep,
+            abi.u8ptr(changed), C.byref(acc)))
+        return changed.astype(bool), acc.value
+
     # ------------------------------------------------------- conditional
     def conditional_sweep(self, models, refs, seeds, n_particles, sweep,
                           resampler=abi.MULTINOMIAL, precision=abi.FP32,
