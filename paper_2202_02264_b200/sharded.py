@@ -160,7 +160,14 @@ def sharded_smooth(backends, comm, K, N, world):
     else:
         ctx = contextlib.nullcontext()
     with ctx:
-        return _sharded_smooth(backends, comm, K, N, world)
+        out = _sharded_smooth(backends, comm, K, N, world)
+    # the window moments are produced on the engine stream(s): order the
+    # caller's stream after them (no host synchronisation)
+    for be in backends.values():
+        st = getattr(be, "stream", None)
+        if st is not None:
+            torch.cuda.current_stream(st.device).wait_stream(st)
+    return out
 
 
 def _sharded_smooth(backends, comm, K, N, world):

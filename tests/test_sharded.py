@@ -60,8 +60,8 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2])
-def test_gloo_world_size_2_reproduces_single_rank(world):
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_world_size_reproduces_single_rank(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -80,11 +80,10 @@ def test_gloo_world_size_2_reproduces_single_rank(world):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("P", [2, 4])
-def test_virtual_ranks_on_gpu_match_single_gpu(P):
+@pytest.mark.parametrize("P,KK,NN", [(2, 256, 128), (4, 256, 128), (8, 4096, 512)])
+def test_virtual_ranks_on_gpu_match_single_gpu(P, KK, NN):
     from paper_2202_02264_b200.dsmc import Engine
     from paper_2202_02264_b200.sharded import GpuBackend
-    KK, NN = 256, 128
     m = models.cv_tracking(KK - 1)
     ref_eng = Engine(0)
     ref = ref_eng.smooth(m, NN, abi.MULTINOMIAL, seed=SEED, precision=abi.FP32)
@@ -98,3 +97,46 @@ def test_virtual_ranks_on_gpu_match_single_gpu(P):
     assert np.array_equal(mean, ref["mean"])
     assert np.array_equal(cov, ref["cov"])
     assert lz == ref["log_norm_const"]
+
+
+def _gpu_gloo_worker(rank, world, port, q, KK, NN):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2202_02264_b200.dsmc import Engine
+        from paper_2202_02264_b200.sharded import GpuBackend
+        m = models.cv_tracking(KK - 1)
+        e = Engine(0)
+        be = GpuBackend(e, e.upload(m), NN, m.d, SEED)
+        out, lz = sharded_smooth({rank: be}, TorchComm(), KK, NN, world)
+        q.put((rank, out[rank][0].cpu().numpy(), out[rank][1].cpu().numpy(), lz))
+        e.close()
+    finally:
+        torch.distributed.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_process_ranks_on_gpu_match_single_gpu():
+    """One process per rank through TorchComm (gloo, host-staged, both ranks
+    on GPU 0) — the multi-process path bench.py takes at N > 1, with the
+    protocol's torch ops on the engine stream — equals the single-GPU run."""
+    from paper_2202_02264_b200.dsmc import Engine
+    KK, NN, world = 1024, 256, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_gloo_worker, args=(r, world, port, q, KK, NN))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    res.sort(key=lambda x: x[0])
+    m = models.cv_tracking(KK - 1)
+    ref = Engine(0).smooth(m, NN, abi.MULTINOMIAL, seed=SEED, precision=abi.FP32)
+    assert np.array_equal(np.concatenate([r[1] for r in res]), ref["mean"])
+    assert np.array_equal(np.concatenate([r[2] for r in res]), ref["cov"])
+    assert all(r[3] == ref["log_norm_const"] for r in res)
