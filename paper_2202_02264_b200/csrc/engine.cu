@@ -24,9 +24,11 @@ namespace {
 
 struct Arena {
   std::map<std::string, std::pair<void*, size_t>> bufs;
+  uint64_t epoch = 0;  // bumped whenever a buffer moves (invalidates graphs)
   cudaError_t get(const char* name, size_t bytes, void** out) {
     auto& e = bufs[name];
     if (e.second < bytes) {
+      ++epoch;
       if (e.first) cudaFree(e.first);
       e.first = nullptr;
       e.second = 0;
@@ -52,6 +54,7 @@ struct Status {
 }  // namespace
 
 struct dsmc_model_handle {
+  uint64_t id = 0;  // unique per upload (graph cache key)
   int B = 1;
   dsmc_model_desc desc{};
   int K = 0, d = 1, dy = 1;
@@ -85,7 +88,29 @@ struct dsmc_ctx {
   int last_biased = 0;
   double* h_lnc = nullptr;  // pinned scratch
   void* window = nullptr;   // WindowState of the last run (time-sharded API)
+  // CUDA graph of the last resident run (dsmc_smooth_resident): the whole
+  // leaves -> levels -> composition sequence replayed with one launch; only
+  // the seed (a kernel-node argument) changes between replays
+  struct GraphCache {
+    uint64_t handle = 0, epoch = 0;
+    size_t N = 0, mh = 0;
+    int rs = -1, prec = -1, seen = 0;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t seed_node = nullptr;
+    cudaKernelNodeParams seed_params{};
+    uint64_t* seed_dst = nullptr;
+    uint64_t launches = 0;
+    int kev_used = 0, levels = 0;
+    void reset() {
+      if (exec) cudaGraphExecDestroy(exec);
+      if (graph) cudaGraphDestroy(graph);
+      *this = GraphCache();
+    }
+  } gc;
 };
+
+static uint64_t g_handle_ids = 0;
 
 namespace {
 
@@ -102,6 +127,15 @@ int set_err(dsmc_ctx* ctx, int code, std::string msg) {
                                            #call);                        \
   } while (0)
 #define LAUNCHED(ctx) (++(ctx)->launches)
+
+// Timing events: recorded as EXTERNAL event nodes while the stream is being
+// captured into a CUDA graph (plain graph event nodes cannot be timed).
+cudaError_t rec_event(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &st);
+  return st == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                                             : cudaEventRecord(e, s);
+}
 
 int validate_desc(dsmc_ctx* ctx, const dsmc_model_desc* m) {
   if (!m) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "model descriptor is null");
@@ -158,6 +192,7 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
       return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "chains must share kind, horizon and dims");
   }
   auto h = std::make_unique<dsmc_model_handle>();
+  h->id = ++g_handle_ids;
   h->B = B;
   h->stream = ctx->stream;
   h->desc = descs[0];
@@ -342,14 +377,14 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
     }
     ev = &ctx->kev[ctx->kev_used];
     ctx->kev_used += 3;
-    CU(cudaEventRecord(ev[0], ctx->stream));
+    CU(rec_event(ev[0], ctx->stream));
   }
   c32_pair<D><<<dim3(nrt * ncs, nk, b.B), 32 * kPairWarps, 0, ctx->stream>>>(b, la);
   LAUNCHED(ctx);
-  if (ev) CU(cudaEventRecord(ev[1], ctx->stream));
+  if (ev) CU(rec_event(ev[1], ctx->stream));
   c32_sample<D><<<dim3(sb, nk, b.B), 256, sm2, ctx->stream>>>(b, la, systematic);
   LAUNCHED(ctx);
-  if (ev) CU(cudaEventRecord(ev[2], ctx->stream));
+  if (ev) CU(rec_event(ev[2], ctx->stream));
   return DSMC_OK;
 }
 
@@ -509,7 +544,7 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
   CU(A.get("BLNCB", (size_t)B * cap * sizeof(double), &p));
   blnc[1] = (double*)p;
 
-  if (o.timing) CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+  if (o.timing) CU(rec_event(ctx->ev[0], ctx->stream));
   // ---------------------------------------------------------------- leaves
   if (fp64) {
     const double* dinj_x = nullptr;
@@ -544,7 +579,7 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     }
   }
   CU(cudaGetLastError());
-  if (o.timing) CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+  if (o.timing) CU(rec_event(ctx->ev[1], ctx->stream));
 
   // ---------------------------------------------------------------- levels
   const bool lazy = o.resampler == DSMC_MH_LAZY || o.resampler == DSMC_REJECTION_LAZY;
@@ -647,7 +682,7 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     cursor += np;
     nb = (nb + 1) / 2;
   }
-  if (o.timing) CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+  if (o.timing) CU(rec_event(ctx->ev[2], ctx->stream));
   res->levels = level;
   res->PL = b.PL;
   res->PR = b.PR;
@@ -671,7 +706,7 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     st.resampler = o.resampler;
   }
   if (!o.compose) {
-    if (o.timing) CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+    if (o.timing) CU(rec_event(ctx->ev[3], ctx->stream));
     return DSMC_OK;
   }
 
@@ -731,7 +766,7 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     LAUNCHED(ctx);
   }
   CU(cudaGetLastError());
-  if (o.timing) CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+  if (o.timing) CU(rec_event(ctx->ev[3], ctx->stream));
   return DSMC_OK;
 }
 
@@ -783,6 +818,7 @@ void dsmc_destroy(dsmc_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  ctx->gc.reset();
   ctx->arena.release();
   if (ctx->d_mean) cudaFree(ctx->d_mean);
   if (ctx->d_cov) cudaFree(ctx->d_cov);
@@ -811,8 +847,11 @@ int dsmc_model_upload(dsmc_ctx* ctx, const dsmc_model_desc* model,
 
 void dsmc_model_free(dsmc_ctx* ctx, dsmc_model_handle* h) {
   if (ctx) cudaStreamSynchronize(ctx->stream);
+  if (ctx && h && ctx->gc.handle == h->id) ctx->gc.reset();
   free_handle(h);
 }
+
+__global__ void set_seed_kernel(uint64_t* dst, uint64_t v) { *dst = v; }
 
 static int smooth_common(dsmc_ctx* ctx, dsmc_model_handle* h, const dsmc_smooth_opts* opts,
                          double* d_paths, double* d_mean, double* d_cov, RunResult* res,
@@ -833,7 +872,12 @@ static int smooth_common(dsmc_ctx* ctx, dsmc_model_handle* h, const dsmc_smooth_
   ctx->kev_used = 0;
   void* p;
   CU(ctx->arena.get("SEEDS", sizeof(uint64_t), &p));
-  CU(cudaMemcpyAsync(p, &opts->seed, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+  // the seed travels as a kernel argument (a graph replay updates it there);
+  // timing events are recorded as EXTERNAL nodes so they stay measurable
+  // when the run is replayed from a CUDA graph
+  set_seed_kernel<<<1, 1, 0, ctx->stream>>>((uint64_t*)p, opts->seed);
+  LAUNCHED(ctx);
+  ctx->gc.seed_dst = (uint64_t*)p;
   o.seeds = (const uint64_t*)p;
   return run_tree(ctx, h, o, res);
 }
@@ -908,12 +952,104 @@ int dsmc_smooth_resident(dsmc_ctx* ctx, const dsmc_model_handle* hc,
     CU(cudaMalloc(&ctx->d_cov, (size_t)K * d * d * sizeof(double)));
     ctx->last_K = K;
     ctx->last_d = d;
+    ++ctx->arena.epoch;  // moved outputs invalidate a captured graph
+  }
+  auto& gc = ctx->gc;
+  const bool same = gc.handle == h->id && gc.epoch == ctx->arena.epoch && gc.N == opts->n_particles &&
+                    gc.rs == opts->resampler && gc.prec == opts->precision &&
+                    gc.mh == opts->mh_steps && !opts->inject_states && !opts->inject_logw;
+  const bool graphs = !getenv("DSMC_NO_GRAPH");
+  if (graphs && same && gc.exec) {  // replay with the new seed
+    uint64_t* dst = gc.seed_dst;
+    uint64_t seed = opts->seed;
+    void* args[2] = {&dst, &seed};
+    cudaKernelNodeParams kp = gc.seed_params;
+    kp.kernelParams = args;
+    kp.extra = nullptr;
+    CU(cudaGraphExecKernelNodeSetParams(gc.exec, gc.seed_node, &kp));
+    CU(cudaGraphLaunch(gc.exec, ctx->stream));
+    ctx->launches += gc.launches;
+    ctx->kev_used = gc.kev_used;
+    ctx->time_kernels = true;
+    ctx->last_levels = gc.levels;
+    return DSMC_OK;
+  }
+  auto run = [&](RunResult& res) -> int {
+    int rc = smooth_common(ctx, h, opts, nullptr, ctx->d_mean, ctx->d_cov, &res, true);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(ctx->h_lnc, res.root_lnc, sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    return DSMC_OK;
+  };
+  if (graphs && same && gc.seen >= 1 && !gc.exec) {  // second identical call: capture
+    const uint64_t l0 = ctx->launches;
+    const uint64_t epoch0 = ctx->arena.epoch;
+    RunResult res;
+    int rc = DSMC_OK;
+    cudaGraph_t graph = nullptr;
+    if (cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      rc = run(res);
+      cudaStreamEndCapture(ctx->stream, &graph);
+    }
+    cudaGraphExec_t exec = nullptr;
+    bool ok = rc == DSMC_OK && graph && ctx->arena.epoch == epoch0 &&
+              cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    cudaGraphNode_t seed_node = nullptr;
+    cudaKernelNodeParams seed_params{};
+    if (ok) {
+      size_t n = 0;
+      cudaGraphGetNodes(graph, nullptr, &n);
+      std::vector<cudaGraphNode_t> nodes(n);
+      cudaGraphGetNodes(graph, nodes.data(), &n);
+      for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        cudaKernelNodeParams kp;
+        if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel &&
+            cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess &&
+            kp.func == reinterpret_cast<void*>(set_seed_kernel)) {
+          seed_node = nd;
+          seed_params = kp;
+        }
+      }
+      ok = seed_node != nullptr;
+    }
+    if (ok) {
+      gc.graph = graph;
+      gc.exec = exec;
+      gc.seed_node = seed_node;
+      gc.seed_params = seed_params;
+      gc.launches = ctx->launches - l0;
+      gc.kev_used = ctx->kev_used;
+      gc.levels = res.levels;
+      ctx->launches = l0;
+      CU(cudaGraphLaunch(gc.exec, ctx->stream));
+      ctx->launches += gc.launches;
+      ctx->last_levels = gc.levels;
+      return DSMC_OK;
+    }
+    // capture failed: drop it and run eagerly (and do not try again)
+    cudaGetLastError();
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    ctx->launches = l0;
+    gc.seen = -1000000;
+  }
+  if (!same) {
+    if (gc.exec) cudaStreamSynchronize(ctx->stream);
+    gc.reset();
+    gc.handle = h->id;
+    gc.N = opts->n_particles;
+    gc.rs = opts->resampler;
+    gc.prec = opts->precision;
+    gc.mh = opts->mh_steps;
+    gc.seen = 0;
   }
   RunResult res;
-  int rc = smooth_common(ctx, h, opts, nullptr, ctx->d_mean, ctx->d_cov, &res, true);
+  int rc = run(res);
   if (rc) return rc;
-  CU(cudaMemcpyAsync(ctx->h_lnc, res.root_lnc, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->last_levels = res.levels;
+  gc.epoch = ctx->arena.epoch;  // buffers as left by this run
+  ++gc.seen;
   return DSMC_OK;
 }
 
@@ -933,24 +1069,23 @@ int dsmc_last_timings(const dsmc_ctx* ctx, double* ms, int cap) {
   if (!ctx || cap < 3) return 0;
   if (cap >= 6) {  // [3] pair-kernel ms, [4] sample-kernel ms, [5] pair launches
     double pk = 0, sk = 0;
+    bool ok = true;
     for (int i = 0; i + 2 < ctx->kev_used; i += 3) {
       float a = 0, b = 0;
-      cudaEventElapsedTime(&a, ctx->kev[i], ctx->kev[i + 1]);
-      cudaEventElapsedTime(&b, ctx->kev[i + 1], ctx->kev[i + 2]);
+      ok &= cudaEventElapsedTime(&a, ctx->kev[i], ctx->kev[i + 1]) == cudaSuccess;
+      ok &= cudaEventElapsedTime(&b, ctx->kev[i + 1], ctx->kev[i + 2]) == cudaSuccess;
       pk += a;
       sk += b;
     }
-    ms[3] = pk;
-    ms[4] = sk;
+    ms[3] = ok ? pk : -1.0;
+    ms[4] = ok ? sk : -1.0;
     ms[5] = ctx->kev_used / 3;
   }
-  float a = 0, b2 = 0, c = 0;
-  cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
-  cudaEventElapsedTime(&b2, ctx->ev[1], ctx->ev[2]);
-  cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
-  ms[0] = a;
-  ms[1] = b2;
-  ms[2] = c;
+  float t[3] = {0, 0, 0};
+  for (int i = 0; i < 3; ++i)
+    if (cudaEventElapsedTime(&t[i], ctx->ev[i], ctx->ev[i + 1]) != cudaSuccess) t[i] = -1.f;
+  for (int i = 0; i < 3; ++i) ms[i] = t[i];
+  cudaGetLastError();  // an unavailable timing must not leak into the next call
   return cap >= 6 ? 6 : 3;
 }
 

@@ -174,3 +174,24 @@ def test_batched_chains_equal_single_chain_runs(engine, precision):
                                        precision=precision)
         assert np.array_equal(both["paths"][c], one["paths"][0])
         assert both["log_norm_const"][c] == one["log_norm_const"][0]
+
+
+def test_resident_graph_replays_match_eager(engine):
+    """dsmc_smooth_resident captures the whole run into a CUDA graph on the
+    second identical call and replays it with the seed as a kernel-node
+    argument: every call must equal the eager dsmc_smooth of its seed."""
+    m = models.cv_tracking(255)
+    seeds = [5, 6, 7, 5, 8]
+    refs = {s: engine.smooth(m, 256, abi.MULTINOMIAL, seed=s, precision=abi.FP32) for s in set(seeds)}
+    h = engine.upload(m)
+    try:
+        for s in seeds:
+            before = engine.launches
+            engine.smooth_resident(h, 256, abi.MULTINOMIAL, seed=s)
+            mean, cov, lnc = engine.resident_results(256, 4)
+            assert engine.launches > before
+            assert np.array_equal(mean, refs[s]["mean"]), s
+            assert np.array_equal(cov, refs[s]["cov"]), s
+            assert lnc == refs[s]["log_norm_const"]
+    finally:
+        engine.free_model(h)
