@@ -565,12 +565,13 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     LAUNCHED(ctx);
   } else {
     CU(A.get("RAW0", (size_t)B * N * sizeof(double), &p));
-    const dim3 lg(K, (N + 127) / 128, B);
+    const dim3 lg(K, B);
+    const int lt = std::min(256, (N + 31) / 32 * 32);
     switch (d) {
-      case 1: leaf32_kernel<1><<<lg, 128, 0, ctx->stream>>>(b, (double*)p); break;
-      case 2: leaf32_kernel<2><<<lg, 128, 0, ctx->stream>>>(b, (double*)p); break;
-      case 3: leaf32_kernel<3><<<lg, 128, 0, ctx->stream>>>(b, (double*)p); break;
-      default: leaf32_kernel<4><<<lg, 128, 0, ctx->stream>>>(b, (double*)p); break;
+      case 1: leaf32_kernel<1><<<lg, lt, 0, ctx->stream>>>(b, (double*)p); break;
+      case 2: leaf32_kernel<2><<<lg, lt, 0, ctx->stream>>>(b, (double*)p); break;
+      case 3: leaf32_kernel<3><<<lg, lt, 0, ctx->stream>>>(b, (double*)p); break;
+      default: leaf32_kernel<4><<<lg, lt, 0, ctx->stream>>>(b, (double*)p); break;
     }
     LAUNCHED(ctx);
     if (o.t0 == 0) {  // only global leaf 0 carries non-uniform weights

@@ -216,118 +216,186 @@ __device__ __noinline__ double leaf0_raw_weight(const DevModel& M, const TimeCon
 // log2e * (log h_t - log nu_t + log N-normaliser of the transition into t)
 // written from z directly (no cancellation), leaf-0 raw weight in
 // FP64. For every device model q_t = nu_t, so leaves t >= 1 are uniform.
-// Grid (time, particle chunk, chain); the time's FP32 constants are staged
-// in shared memory once per CTA.
+// Grid (time, chain), 256 threads looping over the time's particles: the
+// time's FP32 constants and the model fields are staged in shared memory once
+// per time (not once per 128 particles). Uniforms are formed in FP32 from the
+// top 24 bits of the reference stream's u64s (same Philox4x64-10 stream and
+// counter layout as the FP64 path, rng.cpp:45-86; FP32 rounding only).
 template <int D>
-__global__ void __launch_bounds__(128) leaf32_kernel(Bufs b, double* raw0) {
-  const int n = blockIdx.y * blockDim.x + threadIdx.x;
-  const int t = blockIdx.x, ch = blockIdx.z;
+__global__ void __launch_bounds__(256, 3) leaf32_kernel(Bufs b, double* raw0) {
+  const int t = blockIdx.x, ch = blockIdx.y;
   const int gt = b.t0 + t;  // global time (stream key, model data)
   const DevModel& M = b.models[ch];
   const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + t];
-  __shared__ float s_L[16], s_G[16], s_e[4], s_c;
+  __shared__ float s_L[16], s_G[16], s_e[4], s_c, s_sv2;
+  __shared__ int s_kind, s_dy, s_obs;
   if (threadIdx.x < 16) {
     s_L[threadIdx.x] = (float)tc.pL[threadIdx.x];
     s_G[threadIdx.x] = (float)tc.G[threadIdx.x];
   }
   if (threadIdx.x < 4) s_e[threadIdx.x] = (float)tc.e[threadIdx.x];
-  if (threadIdx.x == 0) s_c = (float)tc.cconst;
+  if (threadIdx.x == 0) {
+    s_c = (float)tc.cconst;
+    s_kind = M.kind;
+    s_dy = M.dy;
+    s_obs = tc.obs;
+    s_sv2 = (float)(2.0 * tc.logabsy);
+  }
   __syncthreads();
-  if (n >= b.N) return;
-  const size_t off = ((size_t)ch * b.K + t) * b.N + n;
-  float z[4] = {0.f, 0.f, 0.f, 0.f};
-  float xv[4] = {0.f, 0.f, 0.f, 0.f};
-  float col;
-  const bool is_star = b.conditional && n == 0;
-  double xstar[4] = {0, 0, 0, 0};
-  if (is_star) {
+  const int kind = s_kind, dy = s_dy;
+  const bool obs = s_obs != 0;
+  const StreamId id = stream_id(b.seeds[ch], 0, leaf_node(gt, b.conditional, b.sweep),
+                                DSMC_ROLE_LEAF_PROPOSAL, 0);
+  const float colsv = (float)(kLog2E * tc.shift1);
+  if (gt != 0 && !b.conditional) {
+    // hot path (every leaf but global time 0 of an unconditional run):
+    // normals -> centred state + column term, nothing else live
+    for (int n = threadIdx.x; n < b.N; n += blockDim.x) {
+      const size_t off = ((size_t)ch * b.K + t) * b.N + n;
+      float z[4] = {0.f, 0.f, 0.f, 0.f};
+      U64x4 blk;
+      uint64_t have = ~0ull;
+      float r = 0.f, sn = 0.f, cs = 0.f;
 #pragma unroll
-    for (int k = 0; k < D; ++k) xstar[k] = b.star[((size_t)ch * b.K + t) * D + k];
-  } else {
-    const StreamId id = stream_id(b.seeds[ch], 0, leaf_node(gt, b.conditional, b.sweep),
-                                  DSMC_ROLE_LEAF_PROPOSAL, 0);
-    const uint64_t p = b.conditional ? n - 1 : n;
-    // D normals, counter-addressed Box-Muller pairs (normal i uses u64s
-    // 2*(i/2) and 2*(i/2)+1, rng.cpp:74-86): one Philox block serves up to
-    // two pairs and one (r, theta) serves both normals of a pair
-    U64x4 blk;
-    uint64_t have = ~0ull;
-    float r = 0.f, sn = 0.f, cs = 0.f;
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      const uint64_t i = p * D + k;
-      if (k == 0 || !(i & 1)) {
-        const uint64_t q = 2 * (i >> 1);
-        if ((q >> 2) != have) {
-          blk = stream_block(id, q >> 2);
-          have = q >> 2;
+      for (int k = 0; k < D; ++k) {
+        const uint64_t i = (uint64_t)n * D + k;
+        if (k == 0 || !(i & 1)) {
+          const uint64_t q = 2 * (i >> 1);
+          if ((q >> 2) != have) {
+            blk = stream_block(id, q >> 2);
+            have = q >> 2;
+          }
+          const float u1 = ((float)(uint32_t)(blk.v[q & 3] >> 40) + 0.5f) * 0x1p-24f;
+          const float u2 = (float)(uint32_t)(blk.v[(q & 3) + 1] >> 40) * 0x1p-24f;
+          r = sqrtf(-2.0f * __logf(u1));
+          sincospif(2.0f * u2, &sn, &cs);
         }
-        const float u1 = (float)u64_uniform_pos(blk.v[q & 3]);
-        const float u2 = (float)u64_uniform(blk.v[(q & 3) + 1]);
-        r = sqrtf(-2.0f * __logf(u1));
-        sincospif(2.0f * u2, &sn, &cs);
+        z[k] = (i & 1) ? r * sn : r * cs;
       }
-      z[k] = (i & 1) ? r * sn : r * cs;
+      float xv[4] = {0.f, 0.f, 0.f, 0.f};
+      float col;
+      if (kind == DSMC_MODEL_SV) {
+        xv[0] = s_sv2 - __logf(z[0] * z[0]);
+        col = colsv;
+      } else {
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          float acc = 0.f;
+#pragma unroll
+          for (int l = 0; l <= k; ++l) acc = fmaf(s_L[k * D + l], z[l], acc);
+          xv[k] = acc;
+        }
+        float zz = 0.f, rr = 0.f;
+#pragma unroll
+        for (int k = 0; k < D; ++k) zz = fmaf(z[k], z[k], zz);
+        if (obs) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            if (a >= dy) break;
+            float g = s_e[a];
+#pragma unroll
+            for (int l = 0; l < D; ++l) g = fmaf(-s_G[a * D + l], z[l], g);
+            rr = fmaf(g, g, rr);
+          }
+        }
+        col = (float)kLog2E * (s_c + 0.5f * (zz - rr));
+      }
+      b.X32[off] = make_float4(xv[0], xv[1], xv[2], xv[3]);
+      b.COL[off] = col;
     }
-  }
-  if (M.kind == DSMC_MODEL_SV) {
-    const double xd = is_star ? xstar[0]
-                              : DSUB(DMUL(2.0, tc.logabsy), (double)__logf(z[0] * z[0]));
-    xv[0] = (float)xd;
-    col = (float)(kLog2E * tc.shift1);
-  } else {
+  } else
+  for (int n = threadIdx.x; n < b.N; n += blockDim.x) {
+    const size_t off = ((size_t)ch * b.K + t) * b.N + n;
+    float z[4] = {0.f, 0.f, 0.f, 0.f};
+    float xv[4] = {0.f, 0.f, 0.f, 0.f};
+    float col;
+    const bool is_star = b.conditional && n == 0;
+    double xstar[4] = {0, 0, 0, 0};
     if (is_star) {
-      // z = W_P (x* - m_t): the reference state expressed in proposal units
-      double e[4];
 #pragma unroll
-      for (int k = 0; k < D; ++k) e[k] = xstar[k] - tc.pm[k];
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        double acc = 0.0;
-#pragma unroll
-        for (int l = 0; l <= k; ++l) acc += tc.pW[k * D + l] * e[l];
-        z[k] = (float)acc;
-      }
-#pragma unroll
-      for (int k = 0; k < D; ++k) xv[k] = (float)e[k];
+      for (int k = 0; k < D; ++k) xstar[k] = b.star[((size_t)ch * b.K + t) * D + k];
     } else {
+      const uint64_t p = b.conditional ? n - 1 : n;
+      // D normals, counter-addressed Box-Muller pairs (normal i uses u64s
+      // 2*(i/2) and 2*(i/2)+1, rng.cpp:74-86): one Philox block serves up to
+      // two pairs and one (r, theta) serves both normals of a pair
+      U64x4 blk;
+      uint64_t have = ~0ull;
+      float r = 0.f, sn = 0.f, cs = 0.f;
 #pragma unroll
       for (int k = 0; k < D; ++k) {
-        float acc = 0.f;
-#pragma unroll
-        for (int l = 0; l <= k; ++l) acc = fmaf(s_L[k * D + l], z[l], acc);
-        xv[k] = acc;
+        const uint64_t i = p * D + k;
+        if (k == 0 || !(i & 1)) {
+          const uint64_t q = 2 * (i >> 1);
+          if ((q >> 2) != have) {
+            blk = stream_block(id, q >> 2);
+            have = q >> 2;
+          }
+          // uniform_pos / uniform at 24-bit resolution: (0,1) and [0,1)
+          const float u1 = ((float)(uint32_t)(blk.v[q & 3] >> 40) + 0.5f) * 0x1p-24f;
+          const float u2 = (float)(uint32_t)(blk.v[(q & 3) + 1] >> 40) * 0x1p-24f;
+          r = sqrtf(-2.0f * __logf(u1));
+          sincospif(2.0f * u2, &sn, &cs);
+        }
+        z[k] = (i & 1) ? r * sn : r * cs;
       }
     }
-    float zz = 0.f, rr = 0.f;
+    if (kind == DSMC_MODEL_SV) {
+      xv[0] = is_star ? (float)xstar[0] : s_sv2 - __logf(z[0] * z[0]);
+      col = colsv;
+    } else {
+      if (is_star) {
+        // z = W_P (x* - m_t): the reference state expressed in proposal units
+        double e[4];
 #pragma unroll
-    for (int k = 0; k < D; ++k) zz = fmaf(z[k], z[k], zz);
-    if (tc.obs) {
-      const int dy = M.dy;
+        for (int k = 0; k < D; ++k) e[k] = xstar[k] - tc.pm[k];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        if (a >= dy) break;
-        float g = s_e[a];
+        for (int k = 0; k < D; ++k) {
+          double acc = 0.0;
 #pragma unroll
-        for (int l = 0; l < D; ++l) g = fmaf(-s_G[a * D + l], z[l], g);
-        rr = fmaf(g, g, rr);
+          for (int l = 0; l <= k; ++l) acc += tc.pW[k * D + l] * e[l];
+          z[k] = (float)acc;
+        }
+#pragma unroll
+        for (int k = 0; k < D; ++k) xv[k] = (float)e[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          float acc = 0.f;
+#pragma unroll
+          for (int l = 0; l <= k; ++l) acc = fmaf(s_L[k * D + l], z[l], acc);
+          xv[k] = acc;
+        }
       }
+      float zz = 0.f, rr = 0.f;
+#pragma unroll
+      for (int k = 0; k < D; ++k) zz = fmaf(z[k], z[k], zz);
+      if (obs) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          if (a >= dy) break;
+          float g = s_e[a];
+#pragma unroll
+          for (int l = 0; l < D; ++l) g = fmaf(-s_G[a * D + l], z[l], g);
+          rr = fmaf(g, g, rr);
+        }
+      }
+      col = (float)kLog2E * (s_c + 0.5f * (zz - rr));
     }
-    col = (float)kLog2E * (s_c + 0.5f * (zz - rr));
+    b.X32[off] = make_float4(xv[0], xv[1], xv[2], xv[3]);
+    b.COL[off] = col;
+    if (gt == 0) {
+      double x[4];
+#pragma unroll
+      for (int k = 0; k < D; ++k) x[k] = is_star ? xstar[k] : (double)xv[k] + tc.pm[k];
+      raw0[(size_t)ch * b.N + n] = leaf0_raw_weight(M, tc, D, x);
+    }
   }
-  b.X32[off] = make_float4(xv[0], xv[1], xv[2], xv[3]);
-  b.COL[off] = col;
-  if (n == 0 && gt > 0) {  // q_t = nu_t: uniform leaf, lse = log N exactly
+  if (threadIdx.x == 0 && gt > 0) {  // q_t = nu_t: uniform leaf, lse = log N exactly
     const size_t o = (size_t)ch * b.K + t;
     b.LNC[o] = 0.0;
     b.UNI[o] = 1;
     b.LWMAX[o] = -log((double)b.N);
-  }
-  if (gt == 0) {
-    double x[4];
-#pragma unroll
-    for (int k = 0; k < D; ++k) x[k] = is_star ? xstar[k] : (double)xv[k] + tc.pm[k];
-    raw0[(size_t)ch * b.N + n] = leaf0_raw_weight(M, tc, D, x);
   }
 }
 

@@ -61,7 +61,12 @@ def test_cv_d4_means_match_kalman(engine, precision):
     avg, se, runs = _seed_avg(engine, m, 1024, precision, range(16))
     z = (avg - km) / np.maximum(se, 1e-12)
     assert np.sqrt(np.mean(z ** 2)) < 2.0, np.sqrt(np.mean(z ** 2))
-    assert np.abs(z).max() < 6.0
+    # z is a t-statistic with 15 dof and heavy tails (path degeneracy): over
+    # 128 x 4 entries the max is 3-6 and occasionally ~7.6 for BOTH
+    # precisions (tools/zcheck3.py, 20 groups of 16 seeds), so bound the
+    # bulk and only gross outliers
+    assert np.mean(np.abs(z) > 4.0) < 0.01, np.mean(np.abs(z) > 4.0)
+    assert np.abs(z).max() < 10.0
     lz = np.array([r["log_norm_const"] for r in runs])
     # exp(log Z) is unbiased (test_smoother.cpp:317-341): log-mean-exp vs ll
     lme = np.log(np.mean(np.exp(lz - lz.max()))) + lz.max()
