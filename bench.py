@@ -270,6 +270,7 @@ def run_ours(args, cfg, rank, world, device):
     if cfg["model"] == "sv_pgibbs":
         return run_pgibbs(args, cfg, rank, world, device)
     import torch
+    from paper_2202_02264_b200 import abi
     from paper_2202_02264_b200.dsmc import Engine
     from paper_2202_02264_b200.sharded import GpuBackend, TorchComm, sharded_smooth
 
@@ -277,13 +278,14 @@ def run_ours(args, cfg, rank, world, device):
     eng = Engine(device)
     model = build_model(cfg, pinned=True)
     K, N, d, rs = cfg["K"], cfg["N"], model.d, cfg["resampler"]
+    prec = abi.FP64_PARITY if args.precision == "fp64" else abi.FP32
     seed_base = 1 + (1 << 32)  # experiment.cpp:42-45 salting of seed 1, replicate 0
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=torch.device("cuda", device))
     h = eng.upload(model)
     eng.sync()
     if world == 1:
         def step(s):
-            eng.smooth_resident(h, N, rs, seed=seed_base + s)
+            eng.smooth_resident(h, N, rs, seed=seed_base + s, precision=prec)
     else:
         if K % world or (K // world) < 2:
             raise SystemExit(f"K={K} does not split over {world} ranks")
@@ -312,7 +314,8 @@ def run_ours(args, cfg, rank, world, device):
         cov_h = torch.empty((K, d, d), dtype=torch.float64, pin_memory=True).numpy()
 
         def e2e_step(s):
-            eng.smooth(model, N, rs, seed=seed_base + 5000 + s, mean_out=mean_h, cov_out=cov_h)
+            eng.smooth(model, N, rs, seed=seed_base + 5000 + s, mean_out=mean_h, cov_out=cov_h,
+                       precision=prec)
     else:
         Kloc = K // world
         d2h = Kloc * (d + d * d) * 8 + 8
@@ -367,12 +370,13 @@ def run_ours(args, cfg, rank, world, device):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
             "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32",
+            "vs_baseline": None, "dtype": "f32" if prec == abi.FP32 else "f64",
             "data": "synthetic (trajectory simulated with numpy seed 90210; RTS-marginal proposals)",
             "config": {"workload": cfg["desc"], "K": K, "T": K - 1, "N": N, "d": d,
                        "resampler": ["multinomial", "systematic", "mh-lazy",
                                      "rejection-lazy"][rs],
-                       "precision": "fp32 throughput path",
+                       "precision": ("fp32 throughput path" if prec == abi.FP32 else
+                                     "fp64 parity path (reference operation order)"),
                        "l2": "inputs larger than L2 (leaf slab %.0f MB > 126 MB)" % (K * N * 20 / 1e6),
                        "parallelism": (f"time-sharded x{world} (NCCL P2P boundary exchange)"
                                        if world > 1 else "single GPU")},
@@ -400,6 +404,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=list(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"],
+                    help="fp64 = the bit-exact parity path (single GPU)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", 0))

@@ -200,3 +200,23 @@ def test_resident_graph_replays_match_eager(engine):
             assert lnc == refs[s]["log_norm_const"]
     finally:
         engine.free_model(h)
+
+
+@pytest.mark.parametrize("N", [33, 300, 1000, 1500])
+def test_fp32_ragged_particle_counts(engine, N):
+    """N not a multiple of the 64-column sub-block, the 256-row tile or the
+    warp: padded columns / rows must never be selected and the moments stay
+    unbiased (seed-averaged against Kalman/RTS)."""
+    m = models.lgssm_check(127)
+    km, kP, ll = kalman_smooth(m)
+    runs = [engine.smooth(m, N, abi.MULTINOMIAL, seed=s, precision=abi.FP32, want_pairs=True)
+            for s in range(8)]
+    for r in runs:
+        assert r["pair_left"].max() < N and r["pair_right"].max() < N
+        assert np.isfinite(r["mean"]).all() and np.isfinite(r["log_norm_const"])
+    means = np.stack([r["mean"] for r in runs])
+    z = (means.mean(0) - km) / np.maximum(means.std(0, ddof=1) / np.sqrt(len(runs)), 1e-12)
+    assert np.sqrt(np.mean(z ** 2)) < 2.0
+    lz = np.array([r["log_norm_const"] for r in runs])
+    lme = np.log(np.mean(np.exp(lz - lz.max()))) + lz.max()
+    assert abs(lme - ll) < 1.0 + 8.0 / np.sqrt(N), (lme, ll)
