@@ -96,6 +96,17 @@ typedef enum dsmc_precision {
  *        log omega_c = log p(x_c|x_{c-1}) - log|y_c| <= -0.5 log(2 pi s2)
  *        - log|y_c| (the rejection bound). See DESIGN.md.
  *
+ *  DSMC_MODEL_COX   log-Gaussian Cox counts over an AR(1) intensity, d = 1 —
+ *      make_cox_model (models.hpp:29-50, models.cpp:111-216), par = (mu, rho,
+ *      sigma2, lambda) as dsmc::CoxParams: slope a = rho lambda, intercept
+ *      b = mu (1 - rho); x_t = b + a x_{t-1} + N(0, sigma2); y_t ~
+ *      Poisson(exp x_t) (y = T+1 counts); q_t = nu_t = x_0 law = the
+ *      stationary N(b / (1 - a), sigma2 / (1 - a^2)). No rejection bound.
+ *  DSMC_MODEL_CRW   random walk conditioned to stay in [-1, 1], d = 1 —
+ *      make_constrained_rw (models.cpp:263-338), par[0] = sigma: x_0 ~
+ *      N(0, 1), x_t = x_{t-1} + N(0, sigma^2), potential 1{|x_t| <= 1},
+ *      q_t = nu_t = U[-1, 1]; rejection bound -0.5 log(2 pi sigma^2) - log 1/2.
+ *
  * Per-time arrays carry an element stride (in doubles) per time index; a
  * stride of 0 broadcasts one matrix to every time. Transition arrays are
  * indexed by t = 0..T with index 0 unused, exactly like
@@ -103,7 +114,9 @@ typedef enum dsmc_precision {
  * ------------------------------------------------------------------------ */
 typedef enum dsmc_model_kind {
   DSMC_MODEL_LGSSM = 1,
-  DSMC_MODEL_SV = 2
+  DSMC_MODEL_SV = 2,
+  DSMC_MODEL_COX = 3,
+  DSMC_MODEL_CRW = 4
 } dsmc_model_kind;
 
 typedef struct dsmc_model_desc {
@@ -127,6 +140,9 @@ typedef struct dsmc_model_desc {
 
   /* SV */
   double sv_mu, sv_phi, sv_sigma2;
+
+  /* COX / CRW parameters (see dsmc_model_kind) */
+  double par[4];
 } dsmc_model_desc;
 
 /* Options of one smoothing run. Replaces SmootherOptions (smoother.hpp:50-56)

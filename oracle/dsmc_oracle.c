@@ -599,6 +599,9 @@ typedef struct {
   gauss_t *prop, *trans, *obs, init;
   /* SV */
   double* logabsy;
+  /* COX (models.cpp:127-135) / CRW (models.cpp:269-270) constants */
+  double slope, icept, stat_mean, stat_var, trans_norm, var;
+  double* lgam;
 } model_t;
 
 static const double* at(const double* p, int64_t stride, int t) {
@@ -626,6 +629,35 @@ static int model_init(model_t* M, const dsmc_model_desc* m) {
     }
     return 0;
   }
+  if (m->kind == DSMC_MODEL_COX) { /* make_cox_model, models.cpp:113-135 */
+    if (M->d != 1) return fail(DSMC_E_INVALID_ARGUMENT, "cox: state_dim must be 1");
+    double mu = m->par[0], rho = m->par[1], s2 = m->par[2], lam = m->par[3];
+    if (!(s2 > 0.0)) return fail(DSMC_E_INVALID_ARGUMENT, "make_cox_model: sigma2 must be > 0");
+    if (!(fabs(rho * lam) < 1.0))
+      return fail(DSMC_E_INVALID_ARGUMENT, "make_cox_model: need |rho * lambda| < 1");
+    M->lgam = malloc(sizeof(double) * K);
+    for (int t = 0; t < K; ++t) {
+      double y = m->y[t];
+      if (y < 0.0 || floor(y) != y)
+        return fail(DSMC_E_INVALID_ARGUMENT, "make_cox_model: counts must be nonnegative integers");
+      M->lgam[t] = lgamma(y + 1.0);
+    }
+    M->slope = rho * lam;
+    M->icept = mu * (1.0 - rho);
+    M->stat_mean = M->icept / (1.0 - M->slope);
+    M->stat_var = s2 / (1.0 - M->slope * M->slope);
+    M->trans_norm = -0.5 * (kLog2Pi + log(s2));
+    M->var = s2;
+    return 0;
+  }
+  if (m->kind == DSMC_MODEL_CRW) { /* make_constrained_rw, models.cpp:265-270 */
+    if (M->d != 1) return fail(DSMC_E_INVALID_ARGUMENT, "crw: state_dim must be 1");
+    double sigma = m->par[0];
+    if (!(sigma > 0.0)) return fail(DSMC_E_INVALID_ARGUMENT, "make_constrained_rw: sigma must be > 0");
+    M->var = sigma * sigma;
+    M->trans_norm = -0.5 * (kLog2Pi + log(M->var));
+    return 0;
+  }
   if (m->kind != DSMC_MODEL_LGSSM) return fail(DSMC_E_INVALID_ARGUMENT, "unknown model kind");
   int d = M->d, dy = M->dy;
   if (d < 1 || d > 4 || dy < 1 || dy > 4)
@@ -651,6 +683,15 @@ static void model_free(model_t* M) {
   free(M->trans);
   free(M->obs);
   free(M->logabsy);
+  free(M->lgam);
+}
+#define COX(M) ((M)->kind == DSMC_MODEL_COX)
+#define CRW(M) ((M)->kind == DSMC_MODEL_CRW)
+static const double kLogHalf = -0.6931471805599453; /* models.cpp:274 */
+static int in_box(double x) { return x >= -1.0 && x <= 1.0; } /* models.cpp:260 */
+/* models.cpp:103-106 */
+static double cox_log_poisson(const model_t* M, int t, double x) {
+  return M->m->y[t] * x - exp(x) - M->lgam[t];
 }
 static int has_obs(const model_t* M, int t) {
   return M->m->has_obs ? M->m->has_obs[t] != 0 : 1;
@@ -692,11 +733,15 @@ static double sv_log_h(const model_t* M, int t, double x) {
 
 /* FeynmanKacModel callbacks restated per model (oracle/ref_models.cpp). */
 static double cb_proposal_logdensity(const model_t* M, int t, const double* x) {
+  if (COX(M)) return log_normal_pdf(*x, M->stat_mean, M->stat_var);
+  if (CRW(M)) return in_box(*x) ? kLogHalf : NEG_INF;
   if (M->kind == DSMC_MODEL_SV) return M->logabsy[t] + sv_log_h(M, t, *x);
   if (lg1(M)) return log_normal_pdf(*x, M->m->prop_mean[t], M->m->prop_cov[t]);
   return gauss_logpdf(&M->prop[t], x, M->m->prop_mean + (size_t)t * M->d);
 }
 static double cb_log_potential(const model_t* M, int t, const double* x) {
+  if (COX(M)) return cox_log_poisson(M, t, *x);
+  if (CRW(M)) return in_box(*x) ? 0.0 : NEG_INF;
   if (M->kind == DSMC_MODEL_SV) return sv_log_h(M, t, *x);
   if (lg1(M)) {
     if (!has_obs(M, t)) return 0.0;
@@ -705,6 +750,8 @@ static double cb_log_potential(const model_t* M, int t, const double* x) {
   return lg_log_h(M, t, x);
 }
 static double cb_init_logdensity(const model_t* M, const double* x) {
+  if (COX(M)) return log_normal_pdf(*x, M->stat_mean, M->stat_var);
+  if (CRW(M)) return log_normal_pdf(*x, 0.0, 1.0);
   if (M->kind == DSMC_MODEL_SV) {
     double p = M->m->sv_phi;
     return log_normal_pdf(*x, M->m->sv_mu, M->m->sv_sigma2 / (1.0 - p * p));
@@ -714,6 +761,8 @@ static double cb_init_logdensity(const model_t* M, const double* x) {
 }
 static double cb_transition(const model_t* M, int t, const double* xp,
                             const double* xc) {
+  if (COX(M)) return log_normal_pdf(*xc, M->icept + M->slope * *xp, M->var);
+  if (CRW(M)) return log_normal_pdf(*xc, *xp, M->var);
   if (M->kind == DSMC_MODEL_SV) {
     double mu = M->m->sv_mu;
     return log_normal_pdf(*xc, mu + M->m->sv_phi * (*xp - mu), M->m->sv_sigma2);
@@ -728,7 +777,17 @@ static double cb_transition(const model_t* M, int t, const double* xp,
 static void cb_proposal_sampler(const model_t* M, int t, size_t n,
                                 stream_t* s, double* out) {
   int d = M->d;
+  if (CRW(M)) { /* models.cpp:278-282: fill_uniform, 2u - 1 */
+    for (size_t i = 0; i < n; ++i) out[i] = st_uniform(s);
+    for (size_t i = 0; i < n; ++i) out[i] = 2.0 * out[i] - 1.0;
+    return;
+  }
   for (size_t i = 0; i < n * (size_t)d; ++i) out[i] = st_normal(s);
+  if (COX(M)) { /* models.cpp:143-148 */
+    double sd = sqrt(M->stat_var);
+    for (size_t i = 0; i < n; ++i) out[i] = M->stat_mean + sd * out[i];
+    return;
+  }
   if (M->kind == DSMC_MODEL_SV) {
     double ly2 = 2.0 * M->logabsy[t];
     for (size_t i = 0; i < n; ++i) out[i] = ly2 - log(out[i] * out[i]);
@@ -756,6 +815,15 @@ static void cb_proposal_sampler(const model_t* M, int t, size_t n,
 /* log_init_weight (fk_model.cpp:43-59) */
 static int leaf_weight(const model_t* M, int t, const double* x, double* w) {
   double v;
+  if (COX(M)) { /* init_weight_batch, models.cpp:169-177 */
+    *w = t == 0 ? cox_log_poisson(M, 0, *x) : 0.0;
+    return 0;
+  }
+  if (CRW(M)) { /* init_weight_batch, models.cpp:301-311 */
+    const double norm = -0.5 * kLog2Pi - kLogHalf;
+    *w = !in_box(*x) ? NEG_INF : t == 0 ? norm - 0.5 * *x * *x : 0.0;
+    return 0;
+  }
   if (t == 0) {
     double pot = cb_log_potential(M, 0, x);
     double p0 = cb_init_logdensity(M, x);
@@ -795,6 +863,11 @@ static int stitch_weight(const model_t* M, int c, const double* xp,
 /* Optional sup of log omega_c (rejection bound): models.cpp:657-683 rule for
  * LG d=1; exact for SV; none for LG d>1. */
 static int stitch_bound(const model_t* M, int c, double* out) {
+  if (COX(M)) return 0; /* models.cpp:210-212: unbounded */
+  if (CRW(M)) {         /* models.cpp:334-335 */
+    *out = M->trans_norm - kLogHalf;
+    return 1;
+  }
   if (M->kind == DSMC_MODEL_SV) {
     *out = -0.5 * (kLog2Pi + log(M->m->sv_sigma2)) - M->logabsy[c];
     return 1;
@@ -842,7 +915,14 @@ static void comb_prepare(comb_ctx* cc) {
   int c = cc->c;
   size_t n = cc->n;
   cc->base = malloc(sizeof(double) * n);
-  if (M->kind == DSMC_MODEL_SV) {
+  if (COX(M)) { /* models.cpp:182-187 */
+    for (size_t j = 0; j < n; ++j)
+      cc->base[j] = cox_log_poisson(M, c, cc->xr[j]) -
+                    log_normal_pdf(cc->xr[j], M->stat_mean, M->stat_var) + M->trans_norm;
+  } else if (CRW(M)) { /* models.cpp:313-315 */
+    for (size_t j = 0; j < n; ++j)
+      cc->base[j] = in_box(cc->xr[j]) ? M->trans_norm - kLogHalf : NEG_INF;
+  } else if (M->kind == DSMC_MODEL_SV) {
     double b = -0.5 * (kLog2Pi + log(M->m->sv_sigma2)) - M->logabsy[c];
     for (size_t j = 0; j < n; ++j) cc->base[j] = b;
   } else if (lg1(M)) { /* models.cpp:611-627 */
@@ -882,7 +962,12 @@ static int comb_fill(const pair_src* s, size_t i, double* out) {
   const model_t* M = cc->M;
   size_t n = cc->n;
   int c = cc->c;
-  if (M->kind == DSMC_MODEL_SV) {
+  if (COX(M)) { /* models.cpp:188-191 */
+    gaussian_row(cc->xr, n, M->icept + M->slope * cc->xl[i], -1.0 / (2.0 * M->var), cc->base,
+                 out);
+  } else if (CRW(M)) { /* models.cpp:316-319 */
+    gaussian_row(cc->xr, n, cc->xl[i], -1.0 / (2.0 * M->var), cc->base, out);
+  } else if (M->kind == DSMC_MODEL_SV) {
     double mu = M->m->sv_mu;
     double mean = mu + M->m->sv_phi * (cc->xl[i] - mu);
     gaussian_row(cc->xr, n, mean, -1.0 / (2.0 * M->m->sv_sigma2), cc->base, out);

@@ -403,6 +403,122 @@ dsmc::FeynmanKacModel sv_model(const dsmc_model_desc& desc) {
   return m;
 }
 
+// ----------------------------------------------------------------- Cox
+// Restates make_cox_model (models.cpp:111-216) against the reference API
+// (models.cpp needs Eigen through models.hpp, so it cannot be compiled here).
+struct CoxPrep {
+  std::vector<double> y, lgam;
+  double slope = 0, icept = 0, stat_mean = 0, stat_var = 1, s2 = 1, tnorm = 0;
+  double log_poisson(int t, double x) const {  // models.cpp:103-106
+    return y[static_cast<std::size_t>(t)] * x - std::exp(x) - lgam[static_cast<std::size_t>(t)];
+  }
+};
+
+dsmc::FeynmanKacModel cox_model(const dsmc_model_desc& desc) {
+  auto P = std::make_shared<CoxPrep>();
+  const double mu = desc.par[0], rho = desc.par[1], lam = desc.par[3];
+  P->s2 = desc.par[2];
+  if (!(P->s2 > 0.0)) throw std::invalid_argument("make_cox_model: sigma2 must be > 0");
+  if (!(std::abs(rho * lam) < 1.0))
+    throw std::invalid_argument("make_cox_model: need |rho * lambda| < 1");
+  P->y.assign(desc.y, desc.y + desc.horizon + 1);
+  for (double v : P->y) {
+    if (v < 0.0 || std::floor(v) != v)
+      throw std::invalid_argument("make_cox_model: counts must be nonnegative integers");
+    P->lgam.push_back(std::lgamma(v + 1.0));
+  }
+  P->slope = rho * lam;
+  P->icept = mu * (1.0 - rho);
+  P->stat_mean = P->icept / (1.0 - P->slope);
+  P->stat_var = P->s2 / (1.0 - P->slope * P->slope);
+  P->tnorm = -0.5 * (kLog2Pi + std::log(P->s2));
+
+  dsmc::FeynmanKacModel m;
+  m.state_dim = 1;
+  m.horizon = desc.horizon;
+  // proposals / aux / init: the stationary law
+  m.proposal_sampler = [P](int, std::size_t count, dsmc::RngStream& s, double* out) {
+    const double sd = std::sqrt(P->stat_var);
+    s.fill_normal(out, count);
+    for (std::size_t i = 0; i < count; ++i) out[i] = P->stat_mean + sd * out[i];
+  };
+  m.proposal_logdensity = [P](int, const double* x) {
+    return log_normal_pdf(*x, P->stat_mean, P->stat_var);
+  };
+  m.aux_logdensity = m.proposal_logdensity;
+  m.init_logdensity = [P](const double* x) {
+    return log_normal_pdf(*x, P->stat_mean, P->stat_var);
+  };
+  m.log_potential = [P](int t, const double* x) { return P->log_poisson(t, *x); };
+  m.transition_logdensity = [P](int, const double* xp, const double* xc) {
+    return log_normal_pdf(*xc, P->icept + P->slope * *xp, P->s2);
+  };
+  m.transition_sampler = [P](int, const double* xp, dsmc::RngStream& s, double* out) {
+    *out = P->icept + P->slope * *xp + std::sqrt(P->s2) * s.normal();
+  };
+  // t = 0: the Poisson potential alone (init law == proposal); t >= 1 uniform
+  m.init_weight_batch = [P](int t, const double* xs, std::size_t n, double* out) {
+    for (std::size_t j = 0; j < n; ++j) out[j] = t == 0 ? P->log_poisson(0, xs[j]) : 0.0;
+  };
+  // column base log h_c - log nu_c + trans_norm, row = one gaussian_row
+  m.stitch_row_factory = [P](int c, const double* right, std::size_t n) {
+    auto base = std::make_shared<std::vector<double>>(n);
+    for (std::size_t j = 0; j < n; ++j)
+      (*base)[j] = P->log_poisson(c, right[j]) -
+                   log_normal_pdf(right[j], P->stat_mean, P->stat_var) + P->tnorm;
+    return [P, base, right, n](const double* xp, double* out) {
+      dsmc::kernels::gaussian_row(right, n, P->icept + P->slope * *xp, -1.0 / (2.0 * P->s2),
+                                  base->data(), out);
+    };
+  };
+  return m;  // no log_stitch_bound (models.cpp:210-212)
+}
+
+// -------------------------------------------------------- constrained RW
+// Restates make_constrained_rw (models.cpp:263-338).
+dsmc::FeynmanKacModel crw_model(const dsmc_model_desc& desc) {
+  const double sigma = desc.par[0];
+  if (!(sigma > 0.0)) throw std::invalid_argument("make_constrained_rw: sigma must be > 0");
+  const double var = sigma * sigma;
+  const double tnorm = -0.5 * (kLog2Pi + std::log(var));
+  constexpr double kLogHalf = -0.6931471805599453;
+  auto inside = [](double x) { return x >= -1.0 && x <= 1.0; };
+  dsmc::FeynmanKacModel m;
+  m.state_dim = 1;
+  m.horizon = desc.horizon;
+  m.proposal_sampler = [](int, std::size_t count, dsmc::RngStream& s, double* out) {
+    s.fill_uniform(out, count);
+    for (std::size_t i = 0; i < count; ++i) out[i] = 2.0 * out[i] - 1.0;
+  };
+  m.proposal_logdensity = [inside](int, const double* x) {
+    return inside(*x) ? kLogHalf : -INFINITY;
+  };
+  m.aux_logdensity = m.proposal_logdensity;
+  m.init_logdensity = [](const double* x) { return log_normal_pdf(*x, 0.0, 1.0); };
+  m.log_potential = [inside](int, const double* x) { return inside(*x) ? 0.0 : -INFINITY; };
+  m.transition_logdensity = [var](int, const double* xp, const double* xc) {
+    return log_normal_pdf(*xc, *xp, var);
+  };
+  m.transition_sampler = [sigma](int, const double* xp, dsmc::RngStream& s, double* out) {
+    *out = *xp + sigma * s.normal();
+  };
+  m.init_weight_batch = [inside](int t, const double* xs, std::size_t n, double* out) {
+    constexpr double norm = -0.5 * kLog2Pi - kLogHalf;
+    for (std::size_t j = 0; j < n; ++j)
+      out[j] = !inside(xs[j]) ? -INFINITY : t == 0 ? norm - 0.5 * xs[j] * xs[j] : 0.0;
+  };
+  m.stitch_row_factory = [var, tnorm, inside](int, const double* right, std::size_t n) {
+    auto base = std::make_shared<std::vector<double>>(n);
+    for (std::size_t j = 0; j < n; ++j)
+      (*base)[j] = inside(right[j]) ? tnorm - kLogHalf : -INFINITY;
+    return [base, right, n, var](const double* xp, double* out) {
+      dsmc::kernels::gaussian_row(right, n, *xp, -1.0 / (2.0 * var), base->data(), out);
+    };
+  };
+  m.log_stitch_bound = [tnorm](int) { return tnorm - kLogHalf; };
+  return m;
+}
+
 }  // namespace
 
 dsmc::FeynmanKacModel build_model(const dsmc_model_desc& desc) {
@@ -412,6 +528,8 @@ dsmc::FeynmanKacModel build_model(const dsmc_model_desc& desc) {
                                                         : lgssm_nd(ctx);
   }
   if (desc.kind == DSMC_MODEL_SV) return sv_model(desc);
+  if (desc.kind == DSMC_MODEL_COX) return cox_model(desc);
+  if (desc.kind == DSMC_MODEL_CRW) return crw_model(desc);
   throw std::invalid_argument("unknown model kind");
 }
 

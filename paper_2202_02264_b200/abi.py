@@ -25,7 +25,7 @@ ROLE_GIBBS_PARAM = 4
 ROLE_DATA_SIM = 5
 
 FP32, FP64_PARITY = 0, 1
-MODEL_LGSSM, MODEL_SV = 1, 2
+MODEL_LGSSM, MODEL_SV, MODEL_COX, MODEL_CRW = 1, 2, 3, 4
 
 _dp = C.POINTER(C.c_double)
 _u8p = C.POINTER(C.c_uint8)
@@ -45,6 +45,7 @@ class ModelDesc(C.Structure):
         ("y", _dp), ("has_obs", _u8p),
         ("prop_mean", _dp), ("prop_cov", _dp),
         ("sv_mu", C.c_double), ("sv_phi", C.c_double), ("sv_sigma2", C.c_double),
+        ("par", C.c_double * 4),
     ]
 
 
@@ -123,8 +124,10 @@ class Model:
         self.d = state_dim
         self.dy = obs_dim
         self.arrays = {k: (None if v is None else np.ascontiguousarray(v, dtype=np.uint8 if k == "has_obs" else np.float64))
-                       for k, v in arrays.items() if k not in ("sv",)}
+                       for k, v in arrays.items() if k not in ("sv", "par")}
         self.sv = arrays.get("sv", (0.0, 0.0, 1.0))
+        par = tuple(arrays.get("par", ()))
+        self.par = par + (0.0,) * (4 - len(par))
         self.strides = {}
         d, dy, K = state_dim, obs_dim, horizon + 1
         per = {"F": d * d, "b": d, "Q": d * d, "H": dy * d, "R": dy * dy}
@@ -148,5 +151,5 @@ class Model:
                 g("m0"), g("P0"), g("F"), self.strides["F"], g("b"), self.strides["b"],
                 g("Q"), self.strides["Q"], g("H"), self.strides["H"],
                 g("R"), self.strides["R"], g("y"), u8ptr(A.get("has_obs")),
-                g("prop_mean"), g("prop_cov"), *self.sv)
+                g("prop_mean"), g("prop_cov"), *self.sv, (C.c_double * 4)(*self.par))
         return self._desc

@@ -83,6 +83,11 @@ template <int MC, int D>
 __device__ inline double col_base(const DevModel& M, const TimeConst& tc,
                                   int c, const double* x) {
   if (MC == kSV) return tc.shift1;
+  if (MC == kCOX)  // models.cpp:183-186
+    return DADD(DSUB(cox_log_poisson(M, c, x[0]), dlog_normal_pdf(x[0], M.mp[2], M.mp[3])),
+                M.mp[4]);
+  if (MC == kCRW)  // models.cpp:314-315
+    return crw_in_box(x[0]) ? DSUB(M.mp[1], kLogHalf) : -CUDART_INF;
   if (MC == kLG1) {  // models.cpp:617-627
     double bs = 0.0;
     if (tc.obs) {
@@ -108,6 +113,10 @@ __device__ inline void row_mean(const DevModel& M, const TimeConst& tc, int c, c
                                 double* mu) {
   if (MC == kSV) {
     mu[0] = DADD(M.sv_mu, DMUL(M.sv_phi, DSUB(xl[0], M.sv_mu)));
+  } else if (MC == kCOX) {  // models.cpp:189: icept + slope * xp
+    mu[0] = DADD(M.mp[1], DMUL(M.mp[0], xl[0]));
+  } else if (MC == kCRW) {  // models.cpp:318: the row's own state
+    mu[0] = xl[0];
   } else if (MC == kLG1) {
     mu[0] = DADD(DMUL(*at(M.F, M.F_s, c), xl[0]), *at(M.b, M.b_s, c));
   } else {  // v = W_Q (F x + b): the row's whitened transition mean
@@ -157,6 +166,8 @@ __device__ inline double fill64(const DevModel& M, const TimeConst& tc,
 template <int MC>
 __device__ inline double row_coef(const DevModel& M, int c) {
   if (MC == kSV) return DDIV(-1.0, DMUL(2.0, M.sv_s2));
+  if (MC == kCOX) return DDIV(-1.0, DMUL(2.0, M.mp[5]));
+  if (MC == kCRW) return DDIV(-1.0, DMUL(2.0, M.mp[0]));
   if (MC == kLG1) return DDIV(-1.0, DMUL(2.0, *at(M.Q, M.Q_s, c)));
   return 0.0;
 }

@@ -154,6 +154,28 @@ int validate_desc(dsmc_ctx* ctx, const dsmc_model_desc* m) {
                        "sv descriptor: observations must be finite and nonzero");
     return DSMC_OK;
   }
+  if (m->kind == DSMC_MODEL_COX) {  // make_cox_model (models.cpp:113-125)
+    if (m->state_dim != 1) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "cox: state_dim must be 1");
+    if (!(m->par[2] > 0.0))
+      return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "make_cox_model: sigma2 must be > 0");
+    if (!(std::fabs(m->par[1] * m->par[3]) < 1.0))
+      return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "make_cox_model: need |rho * lambda| < 1");
+    if (!m->y) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "make_cox_model: observations are empty");
+    for (int t = 0; t <= m->horizon; ++t) {
+      const double y = m->y[t];
+      if (!std::isfinite(y)) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "make_cox_model: observations must be finite");
+      if (y < 0.0 || std::floor(y) != y)
+        return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                       "make_cox_model: counts must be nonnegative integers");
+    }
+    return DSMC_OK;
+  }
+  if (m->kind == DSMC_MODEL_CRW) {  // make_constrained_rw (models.cpp:265-268)
+    if (m->state_dim != 1) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "crw: state_dim must be 1");
+    if (!(m->par[0] > 0.0))
+      return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "make_constrained_rw: sigma must be > 0");
+    return DSMC_OK;
+  }
   if (m->kind != DSMC_MODEL_LGSSM)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "unknown model kind");
   if (m->state_dim < 1 || m->state_dim > 4 || m->obs_dim < 1 || m->obs_dim > 4)
@@ -219,7 +241,32 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
     M.R_s = m.R_stride;
     int rc = 0;
     const size_t nT = (size_t)K;
-    if (m.kind == DSMC_MODEL_SV) {
+    for (int q = 0; q < 8; ++q) M.mp[q] = 0.0;
+    M.lgam = nullptr;
+    if (m.kind == DSMC_MODEL_COX || m.kind == DSMC_MODEL_CRW) {
+      M.has_obs = nullptr;
+      M.prop_mean = M.prop_cov = M.F = M.b = M.Q = M.H = M.R = M.m0 = M.P0 = nullptr;
+      M.y = nullptr;
+      if (m.kind == DSMC_MODEL_COX) {  // models.cpp:127-135 (same expressions)
+        const double mu = m.par[0], rho = m.par[1], s2 = m.par[2], lam = m.par[3];
+        const double slope = rho * lam, icept = mu * (1.0 - rho);
+        const double stat_mean = icept / (1.0 - slope);
+        const double stat_var = s2 / (1.0 - slope * slope);
+        const double mp[8] = {slope, icept, stat_mean, stat_var,
+                              -0.5 * (kLog2Pi + std::log(s2)), s2, std::sqrt(stat_var), 0.0};
+        for (int q = 0; q < 8; ++q) M.mp[q] = mp[q];
+        std::vector<double> lg(nT);
+        for (size_t t = 0; t < nT; ++t) lg[t] = std::lgamma(m.y[t] + 1.0);
+        rc |= upload(ctx, h.get(), m.y, nT, &M.y);
+        rc |= upload(ctx, h.get(), lg.data(), nT, &M.lgam);
+        CU(cudaStreamSynchronize(ctx->stream));  // lg is a local host buffer
+      } else {  // models.cpp:269-270
+        const double sigma = m.par[0], var = sigma * sigma;
+        M.mp[0] = var;
+        M.mp[1] = -0.5 * (kLog2Pi + std::log(var));
+        M.mp[2] = sigma;
+      }
+    } else if (m.kind == DSMC_MODEL_SV) {
       rc |= upload(ctx, h.get(), m.y, nT, &M.y);
       M.has_obs = nullptr;
       M.prop_mean = M.prop_cov = M.F = M.b = M.Q = M.H = M.R = M.m0 = M.P0 = nullptr;
@@ -655,6 +702,8 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
         if (fp64) {
           rc = mc == kLG1 ? launch_c64<kLG1, 1>(ctx, b, la, nk, sys)
              : mc == kSV  ? launch_c64<kSV, 1>(ctx, b, la, nk, sys)
+             : mc == kCOX ? launch_c64<kCOX, 1>(ctx, b, la, nk, sys)
+             : mc == kCRW ? launch_c64<kCRW, 1>(ctx, b, la, nk, sys)
              : d == 1     ? launch_c64<kLGN, 1>(ctx, b, la, nk, sys)
              : d == 2     ? launch_c64<kLGN, 2>(ctx, b, la, nk, sys)
              : d == 3     ? launch_c64<kLGN, 3>(ctx, b, la, nk, sys)

@@ -58,6 +58,11 @@ struct DevModel {
   const double *prop_mean, *prop_cov, *F, *b, *Q, *H, *R, *m0, *P0;
   int64_t F_s, b_s, Q_s, H_s, R_s;
   double sv_mu, sv_phi, sv_s2;
+  // COX: {slope a, intercept b, stat mean, stat var, trans_norm, sigma2,
+  //       stat sd, -}; CRW: {var, trans_norm, sigma, -, ...}. Host-computed
+  // (glibc log / lgamma) so the parity path shares the reference's constants.
+  double mp[8];
+  const double* lgam;   // COX: lgamma(y_t + 1), [K]
   const TimeConst* tc;  // [K]
 };
 

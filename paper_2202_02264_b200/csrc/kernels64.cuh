@@ -13,11 +13,20 @@ namespace dsmc_dev {
 #define DMUL __dmul_rn
 #define DDIV __ddiv_rn
 
-enum ModelClass { kLG1 = 0, kSV = 1, kLGN = 2 };
+enum ModelClass { kLG1 = 0, kSV = 1, kLGN = 2, kCOX = 3, kCRW = 4 };
 
 __host__ __device__ inline int model_class(int kind, int d, int dy) {
   if (kind == DSMC_MODEL_SV) return kSV;
+  if (kind == DSMC_MODEL_COX) return kCOX;
+  if (kind == DSMC_MODEL_CRW) return kCRW;
   return (d == 1 && dy == 1) ? kLG1 : kLGN;
+}
+// models.cpp:260: in_box; :274 kLogHalf
+__device__ inline bool crw_in_box(double x) { return x >= -1.0 && x <= 1.0; }
+constexpr double kLogHalf = -0.6931471805599453;
+// models.cpp:103-106: y x - exp(x) - lgamma(y + 1)
+__device__ inline double cox_log_poisson(const DevModel& M, int t, double x) {
+  return DSUB(DSUB(DMUL(M.y[t], x), exp(x)), M.lgam[t]);
 }
 
 // ----------------------------------------------------------- small LA
@@ -94,7 +103,26 @@ __global__ void prep_kernel(const DevModel* models, TimeConst* tc_all, int K,
   tc.obs = 0;
   tc.bounded = 0;
   const int d = M.d, dy = M.dy;
-  if (M.kind == DSMC_MODEL_SV) {
+  if (M.kind == DSMC_MODEL_COX || M.kind == DSMC_MODEL_CRW) {
+    // d = 1 Gaussian-transition models with host-computed constants (mp):
+    // centre = proposal mean, whitening = 1 / transition sd
+    const bool cox = M.kind == DSMC_MODEL_COX;
+    const double m = cox ? M.mp[2] : 0.0;
+    tc.pm[0] = m;
+    tc.pL[0] = cox ? M.mp[6] : 1.0;
+    tc.pW[0] = DDIV(1.0, tc.pL[0]);
+    tc.t_norm = cox ? M.mp[4] : M.mp[1];
+    tc.tW[0] = DDIV(1.0, cox ? __dsqrt_rn(M.mp[5]) : M.mp[2]);
+    tc.F[0] = cox ? M.mp[0] : 1.0;
+    // centring offset F m + b - m of the transition into t
+    tc.delta[0] = cox ? DSUB(DADD(DMUL(M.mp[0], m), M.mp[1]), m) : 0.0;
+    tc.obs = 1;
+    if (!cox && t >= 1) {  // models.cpp:334-335
+      tc.bound = DSUB(M.mp[1], kLogHalf);
+      tc.bounded = 1;
+    }
+    if (t >= 1 && !tc.bounded) atomicAnd(bounded_all + ch, ~1);
+  } else if (M.kind == DSMC_MODEL_SV) {
     const double y = M.y[t];
     tc.logabsy = log(fabs(y));
     tc.obs = 1;
@@ -203,6 +231,8 @@ __global__ void prep_kernel(const DevModel* models, TimeConst* tc_all, int K,
 // per model class; fk_model.cpp / oracle ref_models.cpp).
 __device__ inline double cb_log_h(const DevModel& M, const TimeConst& tc,
                                   int t, const double* x) {
+  if (M.kind == DSMC_MODEL_COX) return cox_log_poisson(M, t, x[0]);
+  if (M.kind == DSMC_MODEL_CRW) return crw_in_box(x[0]) ? 0.0 : -CUDART_INF;
   if (M.kind == DSMC_MODEL_SV) {
     const double y = M.y[t];
     return DSUB(DMUL(-0.5, DADD(kLog2Pi, x[0])), DDIV(DMUL(y, y), DMUL(2.0, exp(x[0]))));
@@ -223,6 +253,8 @@ __device__ inline double cb_prop_logdensity(const DevModel& M,
                                             const TimeConst& tc, int t,
                                             const double* x) {
   if (M.kind == DSMC_MODEL_SV) return DADD(tc.logabsy, cb_log_h(M, tc, t, x));
+  if (M.kind == DSMC_MODEL_COX) return dlog_normal_pdf(x[0], M.mp[2], M.mp[3]);
+  if (M.kind == DSMC_MODEL_CRW) return crw_in_box(x[0]) ? kLogHalf : -CUDART_INF;
   if (M.d == 1 && M.dy == 1)
     return dlog_normal_pdf(x[0], M.prop_mean[t], M.prop_cov[t]);
   return DSUB(tc.p_norm, DMUL(0.5, dquad(tc.pW, M.d, x, tc.pm)));
@@ -234,6 +266,8 @@ __device__ inline double cb_init_logdensity(const DevModel& M,
   if (M.kind == DSMC_MODEL_SV)
     return dlog_normal_pdf(x[0], M.sv_mu,
                            DDIV(M.sv_s2, DSUB(1.0, DMUL(M.sv_phi, M.sv_phi))));
+  if (M.kind == DSMC_MODEL_COX) return dlog_normal_pdf(x[0], M.mp[2], M.mp[3]);
+  if (M.kind == DSMC_MODEL_CRW) return dlog_normal_pdf(x[0], 0.0, 1.0);
   if (M.d == 1 && M.dy == 1) return dlog_normal_pdf(x[0], M.m0[0], M.P0[0]);
   return DSUB(norm0, DMUL(0.5, dquad(W0, M.d, x, M.m0)));
 }
@@ -253,6 +287,10 @@ __device__ inline double cb_transition(const DevModel& M, const TimeConst& tc,
   if (M.kind == DSMC_MODEL_SV)
     return dlog_normal_pdf(xc[0], DADD(M.sv_mu, DMUL(M.sv_phi, DSUB(xp[0], M.sv_mu))),
                            M.sv_s2);
+  if (M.kind == DSMC_MODEL_COX)  // models.cpp:163-165
+    return dlog_normal_pdf(xc[0], DADD(M.mp[1], DMUL(M.mp[0], xp[0])), M.mp[5]);
+  if (M.kind == DSMC_MODEL_CRW)  // models.cpp:292-294
+    return dlog_normal_pdf(xc[0], xp[0], M.mp[0]);
   if (M.d == 1 && M.dy == 1)
     return dlog_normal_pdf(xc[0], DADD(DMUL(*at(M.F, M.F_s, t), xp[0]), *at(M.b, M.b_s, t)),
                            *at(M.Q, M.Q_s, t));

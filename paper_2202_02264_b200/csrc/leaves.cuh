@@ -77,8 +77,16 @@ __global__ void leaf64_kernel(Bufs b, const double* inj_x, const double* inj_lw)
                                   DSMC_ROLE_LEAF_PROPOSAL, 0);
     const uint64_t p = b.conditional ? n - 1 : n;
     double z[4];
-    for (int k = 0; k < d; ++k) z[k] = leaf_normal64(id, p * d + k);
-    if (M.kind == DSMC_MODEL_SV) {
+    if (M.kind == DSMC_MODEL_CRW) {
+      // fill_uniform (rng.cpp:95-97): element p is u64 number p; x = 2u - 1
+      x[0] = DSUB(DMUL(2.0, u64_uniform(stream_u64(id, p))), 1.0);
+    } else {
+      for (int k = 0; k < d; ++k) z[k] = leaf_normal64(id, p * d + k);
+    }
+    if (M.kind == DSMC_MODEL_CRW) {
+    } else if (M.kind == DSMC_MODEL_COX) {  // models.cpp:143-148
+      x[0] = DADD(M.mp[2], DMUL(M.mp[6], z[0]));
+    } else if (M.kind == DSMC_MODEL_SV) {
       x[0] = DSUB(DMUL(2.0, tc.logabsy), log(DMUL(z[0], z[0])));
     } else if (d == 1 && M.dy == 1) {
       const double sd = sqrt(M.prop_cov[t]);
@@ -95,6 +103,13 @@ __global__ void leaf64_kernel(Bufs b, const double* inj_x, const double* inj_lw)
   double w;
   if (inj_lw && !b.conditional) {
     w = inj_lw[off];
+  } else if (M.kind == DSMC_MODEL_COX) {  // init_weight_batch, models.cpp:169-177
+    w = t == 0 ? cox_log_poisson(M, 0, x[0]) : 0.0;
+  } else if (M.kind == DSMC_MODEL_CRW) {  // init_weight_batch, models.cpp:301-311
+    const double norm = DSUB(DMUL(-0.5, kLog2Pi), kLogHalf);
+    w = !crw_in_box(x[0]) ? -CUDART_INF
+        : t == 0          ? DSUB(norm, DMUL(DMUL(0.5, x[0]), x[0]))
+                          : 0.0;
   } else if (t == 0) {
     double W0[16], norm0 = 0.0;
     if (M.kind == DSMC_MODEL_LGSSM && !(d == 1 && M.dy == 1)) {
@@ -179,6 +194,11 @@ __global__ void leafnorm64_kernel(Bufs b) {
 // kept out of line so its local arrays stay off the hot path).
 __device__ __noinline__ double leaf0_raw_weight(const DevModel& M, const TimeConst& tc, int d,
                                                 const double* x) {
+  if (M.kind == DSMC_MODEL_COX) return cox_log_poisson(M, 0, x[0]);
+  if (M.kind == DSMC_MODEL_CRW) {
+    const double norm = DSUB(DMUL(-0.5, kLog2Pi), kLogHalf);
+    return crw_in_box(x[0]) ? DSUB(norm, DMUL(DMUL(0.5, x[0]), x[0])) : -CUDART_INF;
+  }
   if (M.kind == DSMC_MODEL_SV) {
     const double v0 = M.sv_s2 / (1.0 - M.sv_phi * M.sv_phi);
     const double dx = x[0] - M.sv_mu;
@@ -227,7 +247,7 @@ __global__ void __launch_bounds__(256, 3) leaf32_kernel(Bufs b, double* raw0) {
   const int gt = b.t0 + t;  // global time (stream key, model data)
   const DevModel& M = b.models[ch];
   const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + t];
-  __shared__ float s_L[16], s_G[16], s_e[4], s_c, s_sv2;
+  __shared__ float s_L[16], s_G[16], s_e[4], s_c, s_sv2, s_y, s_cc, s_m;
   __shared__ int s_kind, s_dy, s_obs;
   if (threadIdx.x < 16) {
     s_L[threadIdx.x] = (float)tc.pL[threadIdx.x];
@@ -240,6 +260,15 @@ __global__ void __launch_bounds__(256, 3) leaf32_kernel(Bufs b, double* raw0) {
     s_dy = M.dy;
     s_obs = tc.obs;
     s_sv2 = (float)(2.0 * tc.logabsy);
+    if (M.kind == DSMC_MODEL_COX) {
+      // column term log h - log nu + trans_norm = y x - e^x + [-lgam - p_norm
+      // + trans_norm] + z^2 / 2 (p_norm = -0.5 log(2 pi v*), z = (x - m*) / sd)
+      s_y = (float)M.y[gt];
+      s_cc = (float)(-M.lgam[gt] + 0.5 * (kLog2Pi + log(M.mp[3])) + M.mp[4]);
+      s_m = (float)M.mp[2];
+    } else if (M.kind == DSMC_MODEL_CRW) {
+      s_cc = (float)(M.mp[1] - kLogHalf);
+    }
   }
   __syncthreads();
   const int kind = s_kind, dy = s_dy;
@@ -253,6 +282,12 @@ __global__ void __launch_bounds__(256, 3) leaf32_kernel(Bufs b, double* raw0) {
     for (int n = threadIdx.x; n < b.N; n += blockDim.x) {
       const size_t off = ((size_t)ch * b.K + t) * b.N + n;
       float z[4] = {0.f, 0.f, 0.f, 0.f};
+      if (kind == DSMC_MODEL_CRW) {  // U[-1, 1] proposal, u64 number n
+        const float x = 2.f * ((float)(uint32_t)(stream_u64(id, n) >> 40) * 0x1p-24f) - 1.f;
+        b.X32[off] = make_float4(x, 0.f, 0.f, 0.f);
+        b.COL[off] = (float)kLog2E * s_cc;
+        continue;
+      }
       U64x4 blk;
       uint64_t have = ~0ull;
       float r = 0.f, sn = 0.f, cs = 0.f;
@@ -277,6 +312,10 @@ __global__ void __launch_bounds__(256, 3) leaf32_kernel(Bufs b, double* raw0) {
       if (kind == DSMC_MODEL_SV) {
         xv[0] = s_sv2 - __logf(z[0] * z[0]);
         col = colsv;
+      } else if (kind == DSMC_MODEL_COX) {
+        xv[0] = s_L[0] * z[0];
+        const float x = s_m + xv[0];
+        col = (float)kLog2E * (fmaf(s_y, x, -__expf(x)) + s_cc + 0.5f * z[0] * z[0]);
       } else {
 #pragma unroll
         for (int k = 0; k < D; ++k) {
@@ -314,6 +353,9 @@ __global__ void __launch_bounds__(256, 3) leaf32_kernel(Bufs b, double* raw0) {
     if (is_star) {
 #pragma unroll
       for (int k = 0; k < D; ++k) xstar[k] = b.star[((size_t)ch * b.K + t) * D + k];
+    } else if (kind == DSMC_MODEL_CRW) {
+      const uint64_t p = b.conditional ? n - 1 : n;
+      xv[0] = 2.f * ((float)(uint32_t)(stream_u64(id, p) >> 40) * 0x1p-24f) - 1.f;
     } else {
       const uint64_t p = b.conditional ? n - 1 : n;
       // D normals, counter-addressed Box-Muller pairs (normal i uses u64s
@@ -343,6 +385,18 @@ __global__ void __launch_bounds__(256, 3) leaf32_kernel(Bufs b, double* raw0) {
     if (kind == DSMC_MODEL_SV) {
       xv[0] = is_star ? (float)xstar[0] : s_sv2 - __logf(z[0] * z[0]);
       col = colsv;
+    } else if (kind == DSMC_MODEL_CRW) {
+      if (is_star) xv[0] = (float)xstar[0];
+      col = (xv[0] >= -1.f && xv[0] <= 1.f) ? (float)kLog2E * s_cc : -CUDART_INF_F;
+    } else if (kind == DSMC_MODEL_COX) {
+      if (is_star) {
+        xv[0] = (float)(xstar[0] - tc.pm[0]);
+        z[0] = (float)((xstar[0] - tc.pm[0]) * tc.pW[0]);
+      } else {
+        xv[0] = s_L[0] * z[0];
+      }
+      const float x = s_m + xv[0];
+      col = (float)kLog2E * (fmaf(s_y, x, -__expf(x)) + s_cc + 0.5f * z[0] * z[0]);
     } else {
       if (is_star) {
         // z = W_P (x* - m_t): the reference state expressed in proposal units

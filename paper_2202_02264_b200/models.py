@@ -107,3 +107,26 @@ def sv(T, mu=-1.0, phi=0.95, sigma=0.3, data_seed=90210, ys=None):
         ys = np.exp(x / 2) * rng.standard_normal(K)
     return abi.Model(abi.MODEL_SV, T, 1, 1, y=np.asarray(ys, float),
                      sv=(mu, phi, sigma * sigma))
+
+
+def cox(T, mu=0.0, rho=0.9, sigma2=0.25, lam=1.0, data_seed=90210, ys=None):
+    """Log-Gaussian Cox counts (make_cox_model, models.cpp:111-216; defaults
+    = dsmc::CoxParams): x_t = mu(1 - rho) + rho lam x_{t-1} + N(0, sigma2),
+    y_t ~ Poisson(exp x_t); counts simulated with numpy unless given."""
+    K = T + 1
+    if ys is None:
+        rng = np.random.default_rng(data_seed)
+        a, b = rho * lam, mu * (1.0 - rho)
+        x = np.empty(K)
+        x[0] = b / (1 - a) + np.sqrt(sigma2 / (1 - a * a)) * rng.standard_normal()
+        for t in range(1, K):
+            x[t] = b + a * x[t - 1] + np.sqrt(sigma2) * rng.standard_normal()
+        ys = rng.poisson(np.exp(x)).astype(np.float64)
+    return abi.Model(abi.MODEL_COX, T, 1, 1, y=np.asarray(ys, np.float64),
+                     par=(mu, rho, sigma2, lam))
+
+
+def constrained_rw(T, sigma=0.3):
+    """Random walk conditioned to stay in [-1, 1] (make_constrained_rw,
+    models.cpp:263-338)."""
+    return abi.Model(abi.MODEL_CRW, T, 1, 1, par=(sigma,))

@@ -23,6 +23,11 @@ CASES = {
                sweeps=[0, 3]),
     "cv": dict(kind="cv", T=20, N=33, seed=9, resamplers=[MULT, SYS]),
     "ar1": dict(kind="ar1", T=23, N=40, seed=11, resamplers=[MULT, REJ], sweeps=[1]),
+    # the reference's own benchmark models (models.cpp:111-338), SURVEY 8f.1
+    "cox": dict(kind="cox", T=40, N=50, seed=13, resamplers=[MULT, SYS, MH], mh_steps=4,
+                sweeps=[0, 2], par=(0.5, 0.9, 0.25, 1.0)),
+    "crw": dict(kind="crw", T=30, N=37, seed=17, resamplers=[MULT, SYS, MH, REJ], mh_steps=4,
+                sweeps=[1], par=(0.3,)),
 }
 
 # table resampling fixtures: n, n_out, spread (nats), dead fraction, seed
@@ -60,6 +65,11 @@ def model_for(spec):
         return models.cv_tracking(T)
     if spec["kind"] == "ar1":
         return models.ar1([AR1_POOL[t % len(AR1_POOL)] for t in range(T + 1)])
+    if spec["kind"] == "cox":
+        mu, rho, s2, lam = spec["par"]
+        return models.cox(T, mu, rho, s2, lam)
+    if spec["kind"] == "crw":
+        return models.constrained_rw(T, spec["par"][0])
     raise ValueError(spec["kind"])
 
 
@@ -73,6 +83,10 @@ def rebuild(spec, arrays):
     T = spec["T"]
     if kind == "sv":
         return abi.Model(abi.MODEL_SV, T, 1, 1, y=arrays["y"], sv=(-1.0, 0.95, 0.09))
+    if kind == "cox":
+        return abi.Model(abi.MODEL_COX, T, 1, 1, y=arrays["y"], par=spec["par"])
+    if kind == "crw":
+        return abi.Model(abi.MODEL_CRW, T, 1, 1, par=spec["par"])
     d = 4 if kind == "cv" else 1
     dy = 2 if kind == "cv" else 1
     return abi.Model(abi.MODEL_LGSSM, T, d, dy, **arrays)

@@ -220,3 +220,44 @@ def test_fp32_ragged_particle_counts(engine, N):
     lz = np.array([r["log_norm_const"] for r in runs])
     lme = np.log(np.mean(np.exp(lz - lz.max()))) + lz.max()
     assert abs(lme - ll) < 1.0 + 8.0 / np.sqrt(N), (lme, ll)
+
+
+@pytest.mark.parametrize("kind,precision", [("cox", abi.FP32), ("cox", abi.FP64_PARITY),
+                                            ("crw", abi.FP32), ("crw", abi.FP64_PARITY)])
+def test_reference_models_match_grid(engine, kind, precision):
+    """The reference's own benchmark models on the device (Cox counts,
+    constrained random walk, models.cpp:111-338) against the dense-grid
+    forward-backward oracle (grid_oracle.hpp): seed-averaged smoothed means
+    within Monte-Carlo error, exp(log Z) unbiased (test_smoother.cpp:416-456
+    checks the Poisson model against the grid the same way)."""
+    from tests.grid_oracle import grid_truth
+    T = 63
+    m = models.cox(T) if kind == "cox" else models.constrained_rw(T, 0.3)
+    gm, gv, glz = grid_truth(m)
+    runs = [engine.smooth(m, 512, abi.MULTINOMIAL, seed=s, precision=precision)
+            for s in range(12)]
+    means = np.stack([r["mean"][:, 0] for r in runs])
+    z = (means.mean(0) - gm) / np.maximum(means.std(0, ddof=1) / np.sqrt(len(runs)), 1e-12)
+    assert np.sqrt(np.mean(z ** 2)) < 2.0, np.sqrt(np.mean(z ** 2))
+    assert np.mean(np.abs(z) > 4.0) < 0.05
+    var = np.median(np.stack([r["cov"][:, 0, 0] for r in runs]).mean(0) / gv)
+    assert 0.8 < var < 1.2, var
+    lz = np.array([r["log_norm_const"] for r in runs])
+    lme = np.log(np.mean(np.exp(lz - lz.max()))) + lz.max()
+    assert abs(lme - glz) < 1.0, (lme, glz)
+
+
+def test_constrained_rw_rejection_sampling(engine):
+    """The constrained walk exposes a finite stitch bound (models.cpp:334),
+    so rejection-lazy stitching runs exactly (log Z unavailable) and agrees
+    with dense multinomial stitching in distribution."""
+    from tests.grid_oracle import grid_truth
+    m = models.constrained_rw(63, 0.3)
+    gm, _, _ = grid_truth(m)
+    for precision in (abi.FP32, abi.FP64_PARITY):
+        runs = [engine.smooth(m, 512, abi.REJECTION_LAZY, seed=s, precision=precision)
+                for s in range(12)]
+        assert all(r["log_norm_const"] is None for r in runs)
+        means = np.stack([r["mean"][:, 0] for r in runs])
+        z = (means.mean(0) - gm) / np.maximum(means.std(0, ddof=1) / np.sqrt(len(runs)), 1e-12)
+        assert np.sqrt(np.mean(z ** 2)) < 2.0, (precision, np.sqrt(np.mean(z ** 2)))
