@@ -123,6 +123,21 @@ struct SvParams {
 // Stochastic volatility with q_t = nu_t = |y_t| h_t.
 FeynmanKacModel make_sv_model(const SvParams& p, const std::vector<double>& ys);
 
+// models.hpp:29-50 / models.cpp:111-216: log-Gaussian Cox counts over an
+// AR(1) intensity, proposals = the stationary law (same fields and defaults
+// as the reference's CoxParams). ys.size() == T + 1 sets the horizon.
+struct CoxParams {
+  double mu = 0.0;
+  double rho = 0.9;
+  double sigma2 = 0.25;
+  double lambda = 1.0;
+};
+FeynmanKacModel make_cox_model(const CoxParams& p, const std::vector<double>& ys);
+
+// models.cpp:263-338: random walk conditioned to stay inside [-1, 1],
+// U[-1, 1] proposals, finite log_stitch_bound.
+FeynmanKacModel make_constrained_rw(double sigma, int horizon);
+
 // ------------------------------------------------------ smoother.hpp
 enum class Precision { fp32 = DSMC_FP32, fp64_parity = DSMC_FP64_PARITY };
 

@@ -287,6 +287,70 @@ FeynmanKacModel make_sv_model(const SvParams& p, const std::vector<double>& ys) 
   return fk;
 }
 
+FeynmanKacModel make_cox_model(const CoxParams& p, const std::vector<double>& ys) {
+  if (ys.empty()) throw std::invalid_argument("make_cox_model: observations are empty");
+  auto dm = std::make_shared<DeviceModel>();
+  dm->y = ys;
+  dsmc_model_desc& ds = dm->desc;
+  ds.kind = DSMC_MODEL_COX;
+  ds.state_dim = 1;
+  ds.obs_dim = 1;
+  ds.horizon = static_cast<int>(ys.size()) - 1;
+  ds.par[0] = p.mu;
+  ds.par[1] = p.rho;
+  ds.par[2] = p.sigma2;
+  ds.par[3] = p.lambda;
+  dm->bind();
+  // host callbacks (validation / scalar checks), models.cpp:127-167
+  const double a = p.rho * p.lambda, b = p.mu * (1.0 - p.rho);
+  const double sm = b / (1.0 - a), sv = p.sigma2 / (1.0 - a * a);
+  FeynmanKacModel fk;
+  fk.state_dim = 1;
+  fk.horizon = ds.horizon;
+  fk.device = dm;
+  DeviceModel* D = dm.get();
+  fk.log_potential = [D](int t, const double* x) {
+    const double y = D->y[static_cast<std::size_t>(t)];
+    return y * *x - std::exp(*x) - std::lgamma(y + 1.0);
+  };
+  fk.proposal_logdensity = [sm, sv](int, const double* x) { return log_normal_pdf(*x, sm, sv); };
+  fk.aux_logdensity = fk.proposal_logdensity;
+  fk.init_logdensity = [sm, sv](const double* x) { return log_normal_pdf(*x, sm, sv); };
+  fk.transition_logdensity = [a, b, p](int, const double* xp, const double* xc) {
+    return log_normal_pdf(*xc, b + a * *xp, p.sigma2);
+  };
+  return fk;
+}
+
+FeynmanKacModel make_constrained_rw(double sigma, int horizon) {
+  if (horizon < 0) throw std::invalid_argument("make_constrained_rw: horizon must be >= 0");
+  auto dm = std::make_shared<DeviceModel>();
+  dsmc_model_desc& ds = dm->desc;
+  ds.kind = DSMC_MODEL_CRW;
+  ds.state_dim = 1;
+  ds.obs_dim = 1;
+  ds.horizon = horizon;
+  ds.par[0] = sigma;
+  dm->bind();
+  const double var = sigma * sigma, lhalf = -0.6931471805599453;
+  auto inside = [](double x) { return x >= -1.0 && x <= 1.0; };
+  FeynmanKacModel fk;
+  fk.state_dim = 1;
+  fk.horizon = horizon;
+  fk.device = dm;
+  fk.log_potential = [inside](int, const double* x) { return inside(*x) ? 0.0 : -INFINITY; };
+  fk.proposal_logdensity = [inside, lhalf](int, const double* x) {
+    return inside(*x) ? lhalf : -INFINITY;
+  };
+  fk.aux_logdensity = fk.proposal_logdensity;
+  fk.init_logdensity = [](const double* x) { return log_normal_pdf(*x, 0.0, 1.0); };
+  fk.transition_logdensity = [var](int, const double* xp, const double* xc) {
+    return log_normal_pdf(*xc, *xp, var);
+  };
+  fk.log_stitch_bound = [var, lhalf](int) { return -0.5 * (kLog2Pi + std::log(var)) - lhalf; };
+  return fk;
+}
+
 // -------------------------------------------------------------- fk_model
 void validate_model(const FeynmanKacModel& model) {
   if (model.state_dim < 1) throw std::invalid_argument("model: state_dim must be >= 1");

@@ -192,6 +192,35 @@ TEST_CASE(single_time_models_skip_combining_entirely) {
   CHECK(res.root.len() == 1);
 }
 
+// test_models.cpp / test_smoother.cpp:416-456: the reference's own models
+TEST_CASE(cox_and_constrained_walk_models_run_through_the_reference_api) {
+  std::vector<double> ys = {0, 1, 3, 2, 0, 1, 4, 2, 1, 0, 0, 2, 3, 1, 1, 0};
+  dsmc::CoxParams cp;
+  auto cox = dsmc::make_cox_model(cp, ys);
+  CHECK(cox.horizon == 15);
+  dsmc::SmootherOptions o;
+  o.n_particles = 256;
+  o.seed = 3;
+  auto r = dsmc::run_smoother(cox, o);
+  CHECK(r.meta.log_norm_const.has_value());
+  CHECK(std::isfinite(*r.meta.log_norm_const));
+  CHECK(r.meta.weight_evals == 15ull * 256 * 256);
+  CHECK_THROWS_AS(dsmc::make_cox_model(cp, {}), std::invalid_argument);
+  auto bad = dsmc::make_cox_model(cp, {0.5, 1.0});  // non-integer count
+  CHECK_THROWS_AS(dsmc::run_smoother(bad, o), std::invalid_argument);
+  // constrained walk: rejection stitching is available (finite bound) and
+  // every smoothed state stays in the box
+  auto rw = dsmc::make_constrained_rw(0.3, 20);
+  o.resampler = dsmc::Resampler::rejection_lazy;
+  auto rr = dsmc::run_smoother(rw, o);
+  CHECK(!rr.meta.log_norm_const.has_value());
+  for (int t = 0; t <= 20; ++t) CHECK(std::fabs(dsmc::weighted_time_mean(rr.root, t)[0]) <= 1.0);
+  o.precision = dsmc::Precision::fp64_parity;
+  o.resampler = dsmc::Resampler::multinomial;
+  auto r64 = dsmc::run_smoother(rw, o);
+  CHECK(std::isfinite(*r64.meta.log_norm_const));
+}
+
 TEST_CASE(models_without_a_device_descriptor_are_rejected) {
   dsmc::FeynmanKacModel m;
   m.horizon = 3;
