@@ -106,6 +106,11 @@ typedef enum dsmc_precision {
  *      make_constrained_rw (models.cpp:263-338), par[0] = sigma: x_0 ~
  *      N(0, 1), x_t = x_{t-1} + N(0, sigma^2), potential 1{|x_t| <= 1},
  *      q_t = nu_t = U[-1, 1]; rejection bound -0.5 log(2 pi sigma^2) - log 1/2.
+ *  DSMC_MODEL_THETA theta-logistic population dynamics, d = 1 —
+ *      make_theta_logistic (models.cpp:407-491), par = (tau0, tau1, tau2, q2,
+ *      r2): x_0 ~ N(0, 1), x_t = x_{t-1} + tau0 - tau1 exp(tau2 x_{t-1}) +
+ *      N(0, q2), y_t ~ N(x_t, r2) (y = T+1 values); q_t = nu_t =
+ *      N(prop_mean_t, prop_cov_t) (the caller's marginals, e.g. IEKS).
  *
  * Per-time arrays carry an element stride (in doubles) per time index; a
  * stride of 0 broadcasts one matrix to every time. Transition arrays are
@@ -116,7 +121,8 @@ typedef enum dsmc_model_kind {
   DSMC_MODEL_LGSSM = 1,
   DSMC_MODEL_SV = 2,
   DSMC_MODEL_COX = 3,
-  DSMC_MODEL_CRW = 4
+  DSMC_MODEL_CRW = 4,
+  DSMC_MODEL_THETA = 5
 } dsmc_model_kind;
 
 typedef struct dsmc_model_desc {
@@ -141,8 +147,8 @@ typedef struct dsmc_model_desc {
   /* SV */
   double sv_mu, sv_phi, sv_sigma2;
 
-  /* COX / CRW parameters (see dsmc_model_kind) */
-  double par[4];
+  /* COX / CRW / THETA parameters (see dsmc_model_kind) */
+  double par[8];
 } dsmc_model_desc;
 
 /* Options of one smoothing run. Replaces SmootherOptions (smoother.hpp:50-56)

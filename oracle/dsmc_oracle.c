@@ -599,8 +599,10 @@ typedef struct {
   gauss_t *prop, *trans, *obs, init;
   /* SV */
   double* logabsy;
-  /* COX (models.cpp:127-135) / CRW (models.cpp:269-270) constants */
-  double slope, icept, stat_mean, stat_var, trans_norm, var;
+  /* COX (models.cpp:127-135) / CRW (models.cpp:269-270) / THETA
+     (models.cpp:427-431) constants */
+  double slope, icept, stat_mean, stat_var, trans_norm, var, obs_norm, r2;
+  double tau0, tau1, tau2;
   double* lgam;
 } model_t;
 
@@ -658,6 +660,23 @@ static int model_init(model_t* M, const dsmc_model_desc* m) {
     M->trans_norm = -0.5 * (kLog2Pi + log(M->var));
     return 0;
   }
+  if (m->kind == DSMC_MODEL_THETA) { /* make_theta_logistic, models.cpp:407-431 */
+    if (M->d != 1) return fail(DSMC_E_INVALID_ARGUMENT, "theta: state_dim must be 1");
+    M->tau0 = m->par[0];
+    M->tau1 = m->par[1];
+    M->tau2 = m->par[2];
+    M->var = m->par[3];
+    M->r2 = m->par[4];
+    if (!(M->var > 0.0) || !(M->r2 > 0.0))
+      return fail(DSMC_E_INVALID_ARGUMENT, "make_theta_logistic: q2 and r2 must be > 0");
+    for (int t = 0; t < K; ++t)
+      if (!(m->prop_cov[t] > 0.0) || !isfinite(m->prop_mean[t]))
+        return fail(DSMC_E_INVALID_ARGUMENT,
+                    "make_theta_logistic: proposal marginals must have positive variance");
+    M->trans_norm = -0.5 * (kLog2Pi + log(M->var));
+    M->obs_norm = -0.5 * (kLog2Pi + log(M->r2));
+    return 0;
+  }
   if (m->kind != DSMC_MODEL_LGSSM) return fail(DSMC_E_INVALID_ARGUMENT, "unknown model kind");
   int d = M->d, dy = M->dy;
   if (d < 1 || d > 4 || dy < 1 || dy > 4)
@@ -684,6 +703,11 @@ static void model_free(model_t* M) {
   free(M->obs);
   free(M->logabsy);
   free(M->lgam);
+}
+#define THETA(M) ((M)->kind == DSMC_MODEL_THETA)
+/* models.cpp:361-363 */
+static double theta_drift(const model_t* M, double x) {
+  return x + M->tau0 - M->tau1 * exp(M->tau2 * x);
 }
 #define COX(M) ((M)->kind == DSMC_MODEL_COX)
 #define CRW(M) ((M)->kind == DSMC_MODEL_CRW)
@@ -733,6 +757,7 @@ static double sv_log_h(const model_t* M, int t, double x) {
 
 /* FeynmanKacModel callbacks restated per model (oracle/ref_models.cpp). */
 static double cb_proposal_logdensity(const model_t* M, int t, const double* x) {
+  if (THETA(M)) return log_normal_pdf(*x, M->m->prop_mean[t], M->m->prop_cov[t]);
   if (COX(M)) return log_normal_pdf(*x, M->stat_mean, M->stat_var);
   if (CRW(M)) return in_box(*x) ? kLogHalf : NEG_INF;
   if (M->kind == DSMC_MODEL_SV) return M->logabsy[t] + sv_log_h(M, t, *x);
@@ -740,6 +765,7 @@ static double cb_proposal_logdensity(const model_t* M, int t, const double* x) {
   return gauss_logpdf(&M->prop[t], x, M->m->prop_mean + (size_t)t * M->d);
 }
 static double cb_log_potential(const model_t* M, int t, const double* x) {
+  if (THETA(M)) return log_normal_pdf(M->m->y[t], *x, M->r2);
   if (COX(M)) return cox_log_poisson(M, t, *x);
   if (CRW(M)) return in_box(*x) ? 0.0 : NEG_INF;
   if (M->kind == DSMC_MODEL_SV) return sv_log_h(M, t, *x);
@@ -751,7 +777,7 @@ static double cb_log_potential(const model_t* M, int t, const double* x) {
 }
 static double cb_init_logdensity(const model_t* M, const double* x) {
   if (COX(M)) return log_normal_pdf(*x, M->stat_mean, M->stat_var);
-  if (CRW(M)) return log_normal_pdf(*x, 0.0, 1.0);
+  if (CRW(M) || THETA(M)) return log_normal_pdf(*x, 0.0, 1.0);
   if (M->kind == DSMC_MODEL_SV) {
     double p = M->m->sv_phi;
     return log_normal_pdf(*x, M->m->sv_mu, M->m->sv_sigma2 / (1.0 - p * p));
@@ -763,6 +789,7 @@ static double cb_transition(const model_t* M, int t, const double* xp,
                             const double* xc) {
   if (COX(M)) return log_normal_pdf(*xc, M->icept + M->slope * *xp, M->var);
   if (CRW(M)) return log_normal_pdf(*xc, *xp, M->var);
+  if (THETA(M)) return log_normal_pdf(*xc, theta_drift(M, *xp), M->var);
   if (M->kind == DSMC_MODEL_SV) {
     double mu = M->m->sv_mu;
     return log_normal_pdf(*xc, mu + M->m->sv_phi * (*xp - mu), M->m->sv_sigma2);
@@ -783,6 +810,11 @@ static void cb_proposal_sampler(const model_t* M, int t, size_t n,
     return;
   }
   for (size_t i = 0; i < n * (size_t)d; ++i) out[i] = st_normal(s);
+  if (THETA(M)) { /* models.cpp:434-439 */
+    double sd = sqrt(M->m->prop_cov[t]);
+    for (size_t i = 0; i < n; ++i) out[i] = M->m->prop_mean[t] + sd * out[i];
+    return;
+  }
   if (COX(M)) { /* models.cpp:143-148 */
     double sd = sqrt(M->stat_var);
     for (size_t i = 0; i < n; ++i) out[i] = M->stat_mean + sd * out[i];
@@ -864,6 +896,23 @@ static int stitch_weight(const model_t* M, int c, const double* xp,
  * LG d=1; exact for SV; none for LG d>1. */
 static int stitch_bound(const model_t* M, int c, double* out) {
   if (COX(M)) return 0; /* models.cpp:210-212: unbounded */
+  if (THETA(M)) {       /* models.cpp:473-489: finite at every cut, or none */
+    if (M->T < 1) return 0;
+    double sc = 0.0;
+    for (int cc = 1; cc <= M->T; ++cc) {
+      double y = M->m->y[cc], m = M->m->prop_mean[cc], v = M->m->prop_cov[cc];
+      double alpha = 1.0 / (2.0 * v) - 1.0 * 1.0 / (2.0 * M->r2);
+      double beta = 1.0 * y / M->r2 - m / v;
+      double gamma = -y * y / (2.0 * M->r2) + m * m / (2.0 * v) + 0.5 * log(v / M->r2);
+      double sv;
+      if (alpha < 0.0) sv = gamma - beta * beta / (4.0 * alpha);
+      else if (alpha == 0.0 && beta == 0.0) sv = gamma;
+      else return 0;
+      if (cc == c) sc = sv;
+    }
+    *out = M->trans_norm + sc;
+    return 1;
+  }
   if (CRW(M)) {         /* models.cpp:334-335 */
     *out = M->trans_norm - kLogHalf;
     return 1;
@@ -922,6 +971,12 @@ static void comb_prepare(comb_ctx* cc) {
   } else if (CRW(M)) { /* models.cpp:313-315 */
     for (size_t j = 0; j < n; ++j)
       cc->base[j] = in_box(cc->xr[j]) ? M->trans_norm - kLogHalf : NEG_INF;
+  } else if (THETA(M)) { /* models.cpp:450-458 */
+    double var = M->m->prop_cov[c];
+    gaussian_row(cc->xr, n, M->m->y[c], -1.0 / (2.0 * M->r2), NULL, cc->base);
+    gaussian_row(cc->xr, n, M->m->prop_mean[c], 1.0 / (2.0 * var), cc->base, cc->base);
+    double sh = M->obs_norm + 0.5 * (kLog2Pi + log(var)) + M->trans_norm;
+    for (size_t j = 0; j < n; ++j) cc->base[j] += sh;
   } else if (M->kind == DSMC_MODEL_SV) {
     double b = -0.5 * (kLog2Pi + log(M->m->sv_sigma2)) - M->logabsy[c];
     for (size_t j = 0; j < n; ++j) cc->base[j] = b;
@@ -967,6 +1022,8 @@ static int comb_fill(const pair_src* s, size_t i, double* out) {
                  out);
   } else if (CRW(M)) { /* models.cpp:316-319 */
     gaussian_row(cc->xr, n, cc->xl[i], -1.0 / (2.0 * M->var), cc->base, out);
+  } else if (THETA(M)) { /* models.cpp:459-462 */
+    gaussian_row(cc->xr, n, theta_drift(M, cc->xl[i]), -1.0 / (2.0 * M->var), cc->base, out);
   } else if (M->kind == DSMC_MODEL_SV) {
     double mu = M->m->sv_mu;
     double mean = mu + M->m->sv_phi * (cc->xl[i] - mu);

@@ -519,6 +519,73 @@ dsmc::FeynmanKacModel crw_model(const dsmc_model_desc& desc) {
   return m;
 }
 
+// ------------------------------------------------------ theta-logistic
+// Restates make_theta_logistic (models.cpp:407-491) with the descriptor's
+// proposal marginals.
+dsmc::FeynmanKacModel theta_model(const dsmc_model_desc& desc) {
+  struct Ctx {
+    double tau0, tau1, tau2, q2, r2, tnorm, onorm;
+    std::vector<double> y, mean, var;
+    double drift(double x) const { return x + tau0 - tau1 * std::exp(tau2 * x); }
+  };
+  auto C = std::make_shared<Ctx>();
+  C->tau0 = desc.par[0];
+  C->tau1 = desc.par[1];
+  C->tau2 = desc.par[2];
+  C->q2 = desc.par[3];
+  C->r2 = desc.par[4];
+  if (!(C->q2 > 0.0) || !(C->r2 > 0.0))
+    throw std::invalid_argument("make_theta_logistic: q2 and r2 must be > 0");
+  const int K = desc.horizon + 1;
+  C->y.assign(desc.y, desc.y + K);
+  C->mean.assign(desc.prop_mean, desc.prop_mean + K);
+  C->var.assign(desc.prop_cov, desc.prop_cov + K);
+  C->tnorm = -0.5 * (kLog2Pi + std::log(C->q2));
+  C->onorm = -0.5 * (kLog2Pi + std::log(C->r2));
+  dsmc::FeynmanKacModel m;
+  m.state_dim = 1;
+  m.horizon = desc.horizon;
+  m.proposal_sampler = [C](int t, std::size_t count, dsmc::RngStream& s, double* out) {
+    const double sd = std::sqrt(C->var[t]);
+    s.fill_normal(out, count);
+    for (std::size_t i = 0; i < count; ++i) out[i] = C->mean[t] + sd * out[i];
+  };
+  m.proposal_logdensity = [C](int t, const double* x) {
+    return log_normal_pdf(*x, C->mean[t], C->var[t]);
+  };
+  m.aux_logdensity = m.proposal_logdensity;
+  m.init_logdensity = [](const double* x) { return log_normal_pdf(*x, 0.0, 1.0); };
+  m.log_potential = [C](int t, const double* x) { return log_normal_pdf(C->y[t], *x, C->r2); };
+  m.transition_logdensity = [C](int, const double* xp, const double* xc) {
+    return log_normal_pdf(*xc, C->drift(*xp), C->q2);
+  };
+  m.transition_sampler = [C](int, const double* xp, dsmc::RngStream& s, double* out) {
+    *out = C->drift(*xp) + std::sqrt(C->q2) * s.normal();
+  };
+  m.stitch_row_factory = [C](int c, const double* right, std::size_t n) {
+    auto base = std::make_shared<std::vector<double>>(n);
+    dsmc::kernels::gaussian_row(right, n, C->y[c], -1.0 / (2.0 * C->r2), nullptr, base->data());
+    dsmc::kernels::gaussian_row(right, n, C->mean[c], 1.0 / (2.0 * C->var[c]), base->data(),
+                                base->data());
+    dsmc::kernels::add_vec_scalar(base->data(), n,
+                                  C->onorm + 0.5 * (kLog2Pi + std::log(C->var[c])) + C->tnorm,
+                                  nullptr);
+    return [C, base, right, n](const double* xp, double* out) {
+      dsmc::kernels::gaussian_row(right, n, C->drift(*xp), -1.0 / (2.0 * C->q2), base->data(),
+                                  out);
+    };
+  };
+  std::vector<double> bounds(K, 0.0);
+  bool bounded = desc.horizon >= 1;
+  for (int c = 1; c <= desc.horizon && bounded; ++c) {
+    const double s = obs_over_aux_sup(C->y[c], 1.0, C->r2, C->mean[c], C->var[c]);
+    if (!std::isfinite(s)) bounded = false;
+    else bounds[c] = C->tnorm + s;
+  }
+  if (bounded) m.log_stitch_bound = [bounds](int c) { return bounds[c]; };
+  return m;
+}
+
 }  // namespace
 
 dsmc::FeynmanKacModel build_model(const dsmc_model_desc& desc) {
@@ -530,6 +597,7 @@ dsmc::FeynmanKacModel build_model(const dsmc_model_desc& desc) {
   if (desc.kind == DSMC_MODEL_SV) return sv_model(desc);
   if (desc.kind == DSMC_MODEL_COX) return cox_model(desc);
   if (desc.kind == DSMC_MODEL_CRW) return crw_model(desc);
+  if (desc.kind == DSMC_MODEL_THETA) return theta_model(desc);
   throw std::invalid_argument("unknown model kind");
 }
 

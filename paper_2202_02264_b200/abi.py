@@ -25,7 +25,7 @@ ROLE_GIBBS_PARAM = 4
 ROLE_DATA_SIM = 5
 
 FP32, FP64_PARITY = 0, 1
-MODEL_LGSSM, MODEL_SV, MODEL_COX, MODEL_CRW = 1, 2, 3, 4
+MODEL_LGSSM, MODEL_SV, MODEL_COX, MODEL_CRW, MODEL_THETA = 1, 2, 3, 4, 5
 
 _dp = C.POINTER(C.c_double)
 _u8p = C.POINTER(C.c_uint8)
@@ -45,7 +45,7 @@ class ModelDesc(C.Structure):
         ("y", _dp), ("has_obs", _u8p),
         ("prop_mean", _dp), ("prop_cov", _dp),
         ("sv_mu", C.c_double), ("sv_phi", C.c_double), ("sv_sigma2", C.c_double),
-        ("par", C.c_double * 4),
+        ("par", C.c_double * 8),
     ]
 
 
@@ -127,7 +127,7 @@ class Model:
                        for k, v in arrays.items() if k not in ("sv", "par")}
         self.sv = arrays.get("sv", (0.0, 0.0, 1.0))
         par = tuple(arrays.get("par", ()))
-        self.par = par + (0.0,) * (4 - len(par))
+        self.par = par + (0.0,) * (8 - len(par))
         self.strides = {}
         d, dy, K = state_dim, obs_dim, horizon + 1
         per = {"F": d * d, "b": d, "Q": d * d, "H": dy * d, "R": dy * dy}
@@ -151,5 +151,5 @@ class Model:
                 g("m0"), g("P0"), g("F"), self.strides["F"], g("b"), self.strides["b"],
                 g("Q"), self.strides["Q"], g("H"), self.strides["H"],
                 g("R"), self.strides["R"], g("y"), u8ptr(A.get("has_obs")),
-                g("prop_mean"), g("prop_cov"), *self.sv, (C.c_double * 4)(*self.par))
+                g("prop_mean"), g("prop_cov"), *self.sv, (C.c_double * 8)(*self.par))
         return self._desc

@@ -39,6 +39,8 @@ struct CutConst32 {
   float W[16];   // s * tW (lower)
   float F[16];
   float delta[4];
+  int drift;     // THETA: row mean = drift(x~ + m_{c-1}) - m_c
+  float th[5];   // tau0, tau1, tau2, m_{c-1}, m_c
 };
 
 template <int D>
@@ -50,11 +52,30 @@ __device__ inline void load_cut32(const TimeConst& tc, CutConst32& cc) {
     }
     cc.delta[k] = (float)tc.delta[k];
   }
+  cc.drift = tc.drift;
+  for (int k = 0; k < 4; ++k) cc.th[k] = (float)tc.th[k];
+  cc.th[4] = (float)tc.pm[0];
 }
-
 __device__ inline float comp(const float4& v, int k) {
   return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
 }
+// Centred transition mean of a left state x~ (the row term before whitening)
+template <int D>
+__device__ inline void row_mu32(const CutConst32& cc, float4 xv, float* mu) {
+  if (cc.drift) {  // models.cpp:361-363 in absolute coordinates
+    const float xa = xv.x + cc.th[3];
+    mu[0] = xa + cc.th[0] - cc.th[1] * __expf(cc.th[2] * xa) - cc.th[4];
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    float acc = cc.delta[k];
+#pragma unroll
+    for (int l = 0; l < D; ++l) acc = fmaf(cc.F[k * D + l], comp(xv, l), acc);
+    mu[k] = acc;
+  }
+}
+
 
 // Column data y_j (whitened), A_j. Shared by pass 1 and the sampler so the
 // recomputed weights are bit-identical.
@@ -76,13 +97,7 @@ template <int D>
 __device__ inline void row32(const CutConst32& cc, float4 xv, float lw2,
                             float* u, float& Bv) {
   float mu[4];
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    float acc = cc.delta[k];
-#pragma unroll
-    for (int l = 0; l < D; ++l) acc = fmaf(cc.F[k * D + l], comp(xv, l), acc);
-    mu[k] = acc;
-  }
+  row_mu32<D>(cc, xv, mu);
   float nrm = 0.f;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -699,11 +714,7 @@ __global__ void lazy32_kernel(Bufs b, LevelArgs la, int mh, size_t mh_steps) {
     const uint32_t pj = map_first(b, la, ch, R, j);
     const float4 xl = XL[pi], xr = XR[pj];
     float mu[4], e[4];
-    for (int q = 0; q < D; ++q) {
-      float acc = cc.delta[q];
-      for (int l = 0; l < D; ++l) acc = fmaf(cc.F[q * D + l], comp(xl, l), acc);
-      mu[q] = acc;
-    }
+    row_mu32<D>(cc, xl, mu);
     for (int q = 0; q < D; ++q) e[q] = comp(xr, q) - mu[q];
     float qd = 0.f;
     for (int q = 0; q < D; ++q) {

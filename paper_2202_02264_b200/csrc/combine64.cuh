@@ -88,6 +88,13 @@ __device__ inline double col_base(const DevModel& M, const TimeConst& tc,
                 M.mp[4]);
   if (MC == kCRW)  // models.cpp:314-315
     return crw_in_box(x[0]) ? DSUB(M.mp[1], kLogHalf) : -CUDART_INF;
+  if (MC == kTHETA) {  // models.cpp:450-458: two gaussian_row passes + shift
+    const double tt = DSUB(x[0], M.y[c]);
+    double bs = __fma_rn(DDIV(-1.0, DMUL(2.0, M.mp[4])), DMUL(tt, tt), 0.0);
+    const double t2 = DSUB(x[0], M.prop_mean[c]);
+    bs = __fma_rn(DDIV(1.0, DMUL(2.0, M.prop_cov[c])), DMUL(t2, t2), bs);
+    return DADD(bs, tc.shift1);
+  }
   if (MC == kLG1) {  // models.cpp:617-627
     double bs = 0.0;
     if (tc.obs) {
@@ -117,6 +124,8 @@ __device__ inline void row_mean(const DevModel& M, const TimeConst& tc, int c, c
     mu[0] = DADD(M.mp[1], DMUL(M.mp[0], xl[0]));
   } else if (MC == kCRW) {  // models.cpp:318: the row's own state
     mu[0] = xl[0];
+  } else if (MC == kTHETA) {  // models.cpp:461: the drifted left endpoint
+    mu[0] = theta_drift(M, xl[0]);
   } else if (MC == kLG1) {
     mu[0] = DADD(DMUL(*at(M.F, M.F_s, c), xl[0]), *at(M.b, M.b_s, c));
   } else {  // v = W_Q (F x + b): the row's whitened transition mean
@@ -168,6 +177,7 @@ __device__ inline double row_coef(const DevModel& M, int c) {
   if (MC == kSV) return DDIV(-1.0, DMUL(2.0, M.sv_s2));
   if (MC == kCOX) return DDIV(-1.0, DMUL(2.0, M.mp[5]));
   if (MC == kCRW) return DDIV(-1.0, DMUL(2.0, M.mp[0]));
+  if (MC == kTHETA) return DDIV(-1.0, DMUL(2.0, M.mp[3]));
   if (MC == kLG1) return DDIV(-1.0, DMUL(2.0, *at(M.Q, M.Q_s, c)));
   return 0.0;
 }

@@ -176,6 +176,22 @@ int validate_desc(dsmc_ctx* ctx, const dsmc_model_desc* m) {
       return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "make_constrained_rw: sigma must be > 0");
     return DSMC_OK;
   }
+  if (m->kind == DSMC_MODEL_THETA) {  // make_theta_logistic (models.cpp:410-425)
+    if (m->state_dim != 1) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "theta: state_dim must be 1");
+    if (!(m->par[3] > 0.0) || !(m->par[4] > 0.0))
+      return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "make_theta_logistic: q2 and r2 must be > 0");
+    if (!m->y || !m->prop_mean || !m->prop_cov)
+      return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                     "make_theta_logistic: need one proposal marginal per observation");
+    for (int t = 0; t <= m->horizon; ++t) {
+      if (!std::isfinite(m->y[t]))
+        return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "make_theta_logistic: observations must be finite");
+      if (!(m->prop_cov[t] > 0.0) || !std::isfinite(m->prop_mean[t]))
+        return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                       "make_theta_logistic: proposal marginals must have positive variance");
+    }
+    return DSMC_OK;
+  }
   if (m->kind != DSMC_MODEL_LGSSM)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "unknown model kind");
   if (m->state_dim < 1 || m->state_dim > 4 || m->obs_dim < 1 || m->obs_dim > 4)
@@ -266,6 +282,16 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
         M.mp[1] = -0.5 * (kLog2Pi + std::log(var));
         M.mp[2] = sigma;
       }
+    } else if (m.kind == DSMC_MODEL_THETA) {  // models.cpp:427-431
+      M.has_obs = nullptr;
+      M.F = M.b = M.Q = M.H = M.R = M.m0 = M.P0 = nullptr;
+      const double mp[8] = {m.par[0], m.par[1], m.par[2], m.par[3], m.par[4],
+                            -0.5 * (kLog2Pi + std::log(m.par[3])),
+                            -0.5 * (kLog2Pi + std::log(m.par[4])), 0.0};
+      for (int q = 0; q < 8; ++q) M.mp[q] = mp[q];
+      rc |= upload(ctx, h.get(), m.y, nT, &M.y);
+      rc |= upload(ctx, h.get(), m.prop_mean, nT, &M.prop_mean);
+      rc |= upload(ctx, h.get(), m.prop_cov, nT, &M.prop_cov);
     } else if (m.kind == DSMC_MODEL_SV) {
       rc |= upload(ctx, h.get(), m.y, nT, &M.y);
       M.has_obs = nullptr;
@@ -704,6 +730,7 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
              : mc == kSV  ? launch_c64<kSV, 1>(ctx, b, la, nk, sys)
              : mc == kCOX ? launch_c64<kCOX, 1>(ctx, b, la, nk, sys)
              : mc == kCRW ? launch_c64<kCRW, 1>(ctx, b, la, nk, sys)
+             : mc == kTHETA ? launch_c64<kTHETA, 1>(ctx, b, la, nk, sys)
              : d == 1     ? launch_c64<kLGN, 1>(ctx, b, la, nk, sys)
              : d == 2     ? launch_c64<kLGN, 2>(ctx, b, la, nk, sys)
              : d == 3     ? launch_c64<kLGN, 3>(ctx, b, la, nk, sys)

@@ -48,6 +48,8 @@ struct TimeConst {
   double logabsy;   // SV: log|y_t|
   int obs;          // has_obs[t]
   int bounded;      // bound is finite
+  int drift;        // THETA: nonlinear row mean (FP32 path)
+  double th[4];     // THETA: tau0, tau1, tau2, proposal mean at t - 1
 };
 
 // Device view of a model (pointers are device memory).
@@ -59,7 +61,8 @@ struct DevModel {
   int64_t F_s, b_s, Q_s, H_s, R_s;
   double sv_mu, sv_phi, sv_s2;
   // COX: {slope a, intercept b, stat mean, stat var, trans_norm, sigma2,
-  //       stat sd, -}; CRW: {var, trans_norm, sigma, -, ...}. Host-computed
+  //       stat sd, -}; CRW: {var, trans_norm, sigma, -, ...}; THETA: {tau0,
+  //       tau1, tau2, q2, r2, trans_norm, obs_norm, -}. Host-computed
   // (glibc log / lgamma) so the parity path shares the reference's constants.
   double mp[8];
   const double* lgam;   // COX: lgamma(y_t + 1), [K]

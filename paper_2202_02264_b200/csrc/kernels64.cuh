@@ -13,13 +13,18 @@ namespace dsmc_dev {
 #define DMUL __dmul_rn
 #define DDIV __ddiv_rn
 
-enum ModelClass { kLG1 = 0, kSV = 1, kLGN = 2, kCOX = 3, kCRW = 4 };
+enum ModelClass { kLG1 = 0, kSV = 1, kLGN = 2, kCOX = 3, kCRW = 4, kTHETA = 5 };
 
 __host__ __device__ inline int model_class(int kind, int d, int dy) {
   if (kind == DSMC_MODEL_SV) return kSV;
   if (kind == DSMC_MODEL_COX) return kCOX;
   if (kind == DSMC_MODEL_CRW) return kCRW;
+  if (kind == DSMC_MODEL_THETA) return kTHETA;
   return (d == 1 && dy == 1) ? kLG1 : kLGN;
+}
+// models.cpp:361-363: x + tau0 - tau1 exp(tau2 x)
+__device__ inline double theta_drift(const DevModel& M, double x) {
+  return DSUB(DADD(x, M.mp[0]), DMUL(M.mp[1], exp(DMUL(M.mp[2], x))));
 }
 // models.cpp:260: in_box; :274 kLogHalf
 __device__ inline bool crw_in_box(double x) { return x >= -1.0 && x <= 1.0; }
@@ -102,8 +107,48 @@ __global__ void prep_kernel(const DevModel* models, TimeConst* tc_all, int K,
   tc.logabsy = 0.0;
   tc.obs = 0;
   tc.bounded = 0;
+  tc.drift = 0;
+  for (int i = 0; i < 4; ++i) tc.th[i] = 0.0;
   const int d = M.d, dy = M.dy;
-  if (M.kind == DSMC_MODEL_COX || M.kind == DSMC_MODEL_CRW) {
+  if (M.kind == DSMC_MODEL_THETA) {
+    // Gaussian proposal / observation (h = 1) constants as for the LGSSM FP32
+    // leaves; the row term is the nonlinear drift (no F / delta)
+    const double m = M.prop_mean[t], v = M.prop_cov[t];
+    tc.pm[0] = m;
+    tc.pL[0] = __dsqrt_rn(v);
+    tc.pW[0] = DDIV(1.0, tc.pL[0]);
+    tc.p_norm = DMUL(-0.5, DADD(kLog2Pi, log(v)));
+    tc.obs = 1;
+    tc.o_norm = M.mp[6];
+    tc.oW[0] = DDIV(1.0, __dsqrt_rn(M.mp[4]));
+    tc.e[0] = DMUL(tc.oW[0], DSUB(M.y[t], m));
+    tc.G[0] = DMUL(tc.oW[0], tc.pL[0]);
+    tc.t_norm = M.mp[5];
+    tc.tW[0] = DDIV(1.0, __dsqrt_rn(M.mp[3]));
+    tc.cconst = DADD(DSUB(tc.o_norm, tc.p_norm), t >= 1 ? tc.t_norm : 0.0);
+    // models.cpp:454-457 (same expression order): obs_norm + 0.5 (log 2 pi +
+    // log var) + trans_norm
+    tc.shift1 = DADD(DADD(M.mp[6], DMUL(0.5, DADD(kLog2Pi, log(v)))), M.mp[5]);
+    tc.drift = 1;
+    tc.th[0] = M.mp[0];
+    tc.th[1] = M.mp[1];
+    tc.th[2] = M.mp[2];
+    tc.th[3] = t >= 1 ? M.prop_mean[t - 1] : 0.0;
+    if (t >= 1) {  // models.cpp:473-483: obs_over_aux_sup(y, 1, r2, m, v)
+      const double y = M.y[t], r2 = M.mp[4];
+      const double alpha = DSUB(DDIV(1.0, DMUL(2.0, v)), DDIV(1.0, DMUL(2.0, r2)));
+      const double beta = DSUB(DDIV(y, r2), DDIV(m, v));
+      const double gamma = DADD(DADD(DDIV(DMUL(-y, y), DMUL(2.0, r2)), DDIV(DMUL(m, m), DMUL(2.0, v))),
+                                DMUL(0.5, log(DDIV(v, r2))));
+      double sv;
+      if (alpha < 0.0) sv = DSUB(gamma, DDIV(DMUL(beta, beta), DMUL(4.0, alpha)));
+      else if (alpha == 0.0 && beta == 0.0) sv = gamma;
+      else sv = CUDART_INF;
+      tc.bounded = isfinite(sv);
+      if (tc.bounded) tc.bound = DADD(M.mp[5], sv);
+      if (!tc.bounded) atomicAnd(bounded_all + ch, ~1);
+    }
+  } else if (M.kind == DSMC_MODEL_COX || M.kind == DSMC_MODEL_CRW) {
     // d = 1 Gaussian-transition models with host-computed constants (mp):
     // centre = proposal mean, whitening = 1 / transition sd
     const bool cox = M.kind == DSMC_MODEL_COX;
@@ -233,6 +278,7 @@ __device__ inline double cb_log_h(const DevModel& M, const TimeConst& tc,
                                   int t, const double* x) {
   if (M.kind == DSMC_MODEL_COX) return cox_log_poisson(M, t, x[0]);
   if (M.kind == DSMC_MODEL_CRW) return crw_in_box(x[0]) ? 0.0 : -CUDART_INF;
+  if (M.kind == DSMC_MODEL_THETA) return dlog_normal_pdf(M.y[t], x[0], M.mp[4]);
   if (M.kind == DSMC_MODEL_SV) {
     const double y = M.y[t];
     return DSUB(DMUL(-0.5, DADD(kLog2Pi, x[0])), DDIV(DMUL(y, y), DMUL(2.0, exp(x[0]))));
@@ -255,7 +301,7 @@ __device__ inline double cb_prop_logdensity(const DevModel& M,
   if (M.kind == DSMC_MODEL_SV) return DADD(tc.logabsy, cb_log_h(M, tc, t, x));
   if (M.kind == DSMC_MODEL_COX) return dlog_normal_pdf(x[0], M.mp[2], M.mp[3]);
   if (M.kind == DSMC_MODEL_CRW) return crw_in_box(x[0]) ? kLogHalf : -CUDART_INF;
-  if (M.d == 1 && M.dy == 1)
+  if (M.kind == DSMC_MODEL_THETA || (M.d == 1 && M.dy == 1))
     return dlog_normal_pdf(x[0], M.prop_mean[t], M.prop_cov[t]);
   return DSUB(tc.p_norm, DMUL(0.5, dquad(tc.pW, M.d, x, tc.pm)));
 }
@@ -267,7 +313,7 @@ __device__ inline double cb_init_logdensity(const DevModel& M,
     return dlog_normal_pdf(x[0], M.sv_mu,
                            DDIV(M.sv_s2, DSUB(1.0, DMUL(M.sv_phi, M.sv_phi))));
   if (M.kind == DSMC_MODEL_COX) return dlog_normal_pdf(x[0], M.mp[2], M.mp[3]);
-  if (M.kind == DSMC_MODEL_CRW) return dlog_normal_pdf(x[0], 0.0, 1.0);
+  if (M.kind == DSMC_MODEL_CRW || M.kind == DSMC_MODEL_THETA) return dlog_normal_pdf(x[0], 0.0, 1.0);
   if (M.d == 1 && M.dy == 1) return dlog_normal_pdf(x[0], M.m0[0], M.P0[0]);
   return DSUB(norm0, DMUL(0.5, dquad(W0, M.d, x, M.m0)));
 }
@@ -291,6 +337,8 @@ __device__ inline double cb_transition(const DevModel& M, const TimeConst& tc,
     return dlog_normal_pdf(xc[0], DADD(M.mp[1], DMUL(M.mp[0], xp[0])), M.mp[5]);
   if (M.kind == DSMC_MODEL_CRW)  // models.cpp:292-294
     return dlog_normal_pdf(xc[0], xp[0], M.mp[0]);
+  if (M.kind == DSMC_MODEL_THETA)  // models.cpp:443-445
+    return dlog_normal_pdf(xc[0], theta_drift(M, xp[0]), M.mp[3]);
   if (M.d == 1 && M.dy == 1)
     return dlog_normal_pdf(xc[0], DADD(DMUL(*at(M.F, M.F_s, t), xp[0]), *at(M.b, M.b_s, t)),
                            *at(M.Q, M.Q_s, t));

@@ -88,7 +88,7 @@ __global__ void leaf64_kernel(Bufs b, const double* inj_x, const double* inj_lw)
       x[0] = DADD(M.mp[2], DMUL(M.mp[6], z[0]));
     } else if (M.kind == DSMC_MODEL_SV) {
       x[0] = DSUB(DMUL(2.0, tc.logabsy), log(DMUL(z[0], z[0])));
-    } else if (d == 1 && M.dy == 1) {
+    } else if (M.kind == DSMC_MODEL_THETA || (d == 1 && M.dy == 1)) {
       const double sd = sqrt(M.prop_cov[t]);
       x[0] = DADD(M.prop_mean[t], DMUL(sd, z[0]));
     } else {
@@ -195,6 +195,9 @@ __global__ void leafnorm64_kernel(Bufs b) {
 __device__ __noinline__ double leaf0_raw_weight(const DevModel& M, const TimeConst& tc, int d,
                                                 const double* x) {
   if (M.kind == DSMC_MODEL_COX) return cox_log_poisson(M, 0, x[0]);
+  if (M.kind == DSMC_MODEL_THETA)
+    return dlog_normal_pdf(M.y[0], x[0], M.mp[4]) + dlog_normal_pdf(x[0], 0.0, 1.0) -
+           dlog_normal_pdf(x[0], M.prop_mean[0], M.prop_cov[0]);
   if (M.kind == DSMC_MODEL_CRW) {
     const double norm = DSUB(DMUL(-0.5, kLog2Pi), kLogHalf);
     return crw_in_box(x[0]) ? DSUB(norm, DMUL(DMUL(0.5, x[0]), x[0])) : -CUDART_INF;

@@ -130,3 +130,47 @@ def constrained_rw(T, sigma=0.3):
     """Random walk conditioned to stay in [-1, 1] (make_constrained_rw,
     models.cpp:263-338)."""
     return abi.Model(abi.MODEL_CRW, T, 1, 1, par=(sigma,))
+
+
+def theta_logistic_marginals(T, ys, tau0, tau1, tau2, q2, r2, iterations=10, inflation=1.0):
+    """Proposal marginals by the iterated extended Kalman smoother
+    (iterated_smooth, kalman.cpp:220-243): linearise the drift around the
+    previous smoothed means (linearize, :192-218, analytic Jacobian as
+    f_jac, models.cpp:387-391), run the exact Kalman/RTS smoother of the
+    linearised LGSSM (dsmc_kalman_smooth), repeat."""
+    from .dsmc import kalman_smooth
+    K = T + 1
+    f = lambda x: x + tau0 - tau1 * np.exp(tau2 * x)
+    ref = np.zeros(K)
+    for t in range(1, K):
+        ref[t] = f(ref[t - 1])
+    for _ in range(iterations):
+        F = np.ones(K)
+        b = np.zeros(K)
+        F[1:] = 1.0 - tau1 * tau2 * np.exp(tau2 * ref[:-1])
+        b[1:] = f(ref[:-1]) - F[1:] * ref[:-1]
+        lin = _lgssm(T, 1, 1, [0.0], [[1.0]], F.reshape(K, 1, 1), b.reshape(K, 1), [q2],
+                     [1.0], [r2], np.asarray(ys, float).reshape(K, 1),
+                     prop_mean=np.zeros((K, 1)), prop_cov=np.ones((K, 1, 1)))
+        km, kP, _ = kalman_smooth(lin)
+        ref = km[:, 0]
+    return km[:, 0], inflation * kP[:, 0, 0]
+
+
+def theta_logistic(T, tau0=0.15, tau1=0.10, tau2=0.10, q2=0.05, r2=0.05, data_seed=90210,
+                   ys=None, inflation=1.0):
+    """Theta-logistic population dynamics (make_theta_logistic,
+    models.cpp:407-491; defaults = dsmc::ThetaLogisticParams) with IEKS
+    proposal marginals; data simulated with numpy unless given."""
+    K = T + 1
+    if ys is None:
+        rng = np.random.default_rng(data_seed)
+        x = np.empty(K)
+        x[0] = rng.standard_normal()
+        for t in range(1, K):
+            x[t] = x[t - 1] + tau0 - tau1 * np.exp(tau2 * x[t - 1]) + np.sqrt(q2) * rng.standard_normal()
+        ys = x + np.sqrt(r2) * rng.standard_normal(K)
+    ys = np.asarray(ys, np.float64)
+    pm, pv = theta_logistic_marginals(T, ys, tau0, tau1, tau2, q2, r2, inflation=inflation)
+    return abi.Model(abi.MODEL_THETA, T, 1, 1, y=ys, prop_mean=pm.reshape(K, 1),
+                     prop_cov=pv.reshape(K, 1, 1), par=(tau0, tau1, tau2, q2, r2))

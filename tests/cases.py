@@ -28,6 +28,9 @@ CASES = {
                 sweeps=[0, 2], par=(0.5, 0.9, 0.25, 1.0)),
     "crw": dict(kind="crw", T=30, N=37, seed=17, resamplers=[MULT, SYS, MH, REJ], mh_steps=4,
                 sweeps=[1], par=(0.3,)),
+    # IEKS marginals inflated x3 so every cut has a finite bound (rejection)
+    "theta": dict(kind="theta", T=40, N=37, seed=19, resamplers=[MULT, SYS, MH, REJ],
+                  mh_steps=4, sweeps=[0], par=(0.15, 0.10, 0.10, 0.05, 0.05), inflation=3.0),
 }
 
 # table resampling fixtures: n, n_out, spread (nats), dead fraction, seed
@@ -70,6 +73,8 @@ def model_for(spec):
         return models.cox(T, mu, rho, s2, lam)
     if spec["kind"] == "crw":
         return models.constrained_rw(T, spec["par"][0])
+    if spec["kind"] == "theta":
+        return models.theta_logistic(T, *spec["par"], inflation=spec["inflation"])
     raise ValueError(spec["kind"])
 
 
@@ -87,6 +92,9 @@ def rebuild(spec, arrays):
         return abi.Model(abi.MODEL_COX, T, 1, 1, y=arrays["y"], par=spec["par"])
     if kind == "crw":
         return abi.Model(abi.MODEL_CRW, T, 1, 1, par=spec["par"])
+    if kind == "theta":
+        return abi.Model(abi.MODEL_THETA, T, 1, 1, y=arrays["y"], prop_mean=arrays["prop_mean"],
+                         prop_cov=arrays["prop_cov"], par=spec["par"])
     d = 4 if kind == "cv" else 1
     dy = 2 if kind == "cv" else 1
     return abi.Model(abi.MODEL_LGSSM, T, d, dy, **arrays)

@@ -21,7 +21,7 @@ def model_fns(model):
     grid lo, hi) of a DSMC_MODEL_COX / DSMC_MODEL_CRW descriptor."""
     from paper_2202_02264_b200 import abi
     if model.kind == abi.MODEL_COX:
-        mu, rho, s2, lam = model.par
+        mu, rho, s2, lam = model.par[:4]
         a, b = rho * lam, mu * (1 - rho)
         m, v = b / (1 - a), s2 / (1 - a * a)
         y = model.arrays["y"]
@@ -35,7 +35,16 @@ def model_fns(model):
                 lambda xp, xc: _lnorm(xc, xp, s2),
                 lambda t, x: np.where(np.abs(x) <= 1.0, 0.0, -np.inf),
                 -1.0, 1.0)
-    raise ValueError("grid oracle: scalar COX / CRW models only")
+    if model.kind == abi.MODEL_THETA:
+        tau0, tau1, tau2, q2, r2 = model.par[:5]
+        y = model.arrays["y"]
+        drift = lambda x: x + tau0 - tau1 * np.exp(tau2 * x)
+        lo, hi = float(np.min(y)) - 3.0, float(np.max(y)) + 3.0
+        return (lambda x: _lnorm(x, 0.0, 1.0),
+                lambda xp, xc: _lnorm(xc, drift(xp), q2),
+                lambda t, x: _lnorm(y[t], x, r2),
+                lo, hi)
+    raise ValueError("grid oracle: scalar COX / CRW / THETA models only")
 
 
 def grid_truth(model, cells=2000):

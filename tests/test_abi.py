@@ -95,5 +95,5 @@ def test_engine_fails_loudly_without_gpu():
 
 def test_descriptor_layout_matches_header():
     # the ctypes mirror must match the C struct layout
-    assert ctypes.sizeof(abi.ModelDesc) == 4 * 4 + 8 * 2 + 16 * 5 + 8 * 4 + 8 * 3 + 8 * 4
+    assert ctypes.sizeof(abi.ModelDesc) == 4 * 4 + 8 * 2 + 16 * 5 + 8 * 4 + 8 * 3 + 8 * 8
     assert abi.SmoothOpts.inject_logw.offset == 48

@@ -223,7 +223,8 @@ def test_fp32_ragged_particle_counts(engine, N):
 
 
 @pytest.mark.parametrize("kind,precision", [("cox", abi.FP32), ("cox", abi.FP64_PARITY),
-                                            ("crw", abi.FP32), ("crw", abi.FP64_PARITY)])
+                                            ("crw", abi.FP32), ("crw", abi.FP64_PARITY),
+                                            ("theta", abi.FP32), ("theta", abi.FP64_PARITY)])
 def test_reference_models_match_grid(engine, kind, precision):
     """The reference's own benchmark models on the device (Cox counts,
     constrained random walk, models.cpp:111-338) against the dense-grid
@@ -232,7 +233,8 @@ def test_reference_models_match_grid(engine, kind, precision):
     checks the Poisson model against the grid the same way)."""
     from tests.grid_oracle import grid_truth
     T = 63
-    m = models.cox(T) if kind == "cox" else models.constrained_rw(T, 0.3)
+    m = (models.cox(T) if kind == "cox" else models.constrained_rw(T, 0.3) if kind == "crw"
+         else models.theta_logistic(T, inflation=1.5))
     gm, gv, glz = grid_truth(m)
     runs = [engine.smooth(m, 512, abi.MULTINOMIAL, seed=s, precision=precision)
             for s in range(12)]
