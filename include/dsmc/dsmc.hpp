@@ -138,6 +138,18 @@ FeynmanKacModel make_cox_model(const CoxParams& p, const std::vector<double>& ys
 // U[-1, 1] proposals, finite log_stitch_bound.
 FeynmanKacModel make_constrained_rw(double sigma, int horizon);
 
+// models.hpp:86-110 / models.cpp:407-491: theta-logistic dynamics with the
+// caller's per-time proposal marginals (1-d ProposalMarginal entries).
+struct ThetaLogisticParams {
+  double tau0 = 0.15;
+  double tau1 = 0.10;
+  double tau2 = 0.10;
+  double q2 = 0.05;
+  double r2 = 0.05;
+};
+FeynmanKacModel make_theta_logistic(const ThetaLogisticParams& p, const std::vector<double>& ys,
+                                    const std::vector<ProposalMarginal>& marginals);
+
 // ------------------------------------------------------ smoother.hpp
 enum class Precision { fp32 = DSMC_FP32, fp64_parity = DSMC_FP64_PARITY };
 

@@ -351,6 +351,48 @@ FeynmanKacModel make_constrained_rw(double sigma, int horizon) {
   return fk;
 }
 
+FeynmanKacModel make_theta_logistic(const ThetaLogisticParams& p, const std::vector<double>& ys,
+                                    const std::vector<ProposalMarginal>& marginals) {
+  if (ys.empty() || marginals.size() != ys.size())
+    throw std::invalid_argument(
+        "make_theta_logistic: need one proposal marginal per observation");
+  auto dm = std::make_shared<DeviceModel>();
+  dm->y = ys;
+  for (const auto& g : marginals) {
+    if (g.mean.size() != 1 || g.cov.size() != 1)
+      throw std::invalid_argument("make_theta_logistic: marginals must be 1-d");
+    dm->prop_mean.push_back(g.mean[0]);
+    dm->prop_cov.push_back(g.cov[0]);
+  }
+  dsmc_model_desc& ds = dm->desc;
+  ds.kind = DSMC_MODEL_THETA;
+  ds.state_dim = 1;
+  ds.obs_dim = 1;
+  ds.horizon = static_cast<int>(ys.size()) - 1;
+  const double par[5] = {p.tau0, p.tau1, p.tau2, p.q2, p.r2};
+  for (int q = 0; q < 5; ++q) ds.par[q] = par[q];
+  dm->bind();
+  FeynmanKacModel fk;
+  fk.state_dim = 1;
+  fk.horizon = ds.horizon;
+  fk.device = dm;
+  DeviceModel* D = dm.get();
+  auto drift = [p](double x) { return x + p.tau0 - p.tau1 * std::exp(p.tau2 * x); };
+  fk.log_potential = [D, p](int t, const double* x) {
+    return log_normal_pdf(D->y[static_cast<std::size_t>(t)], *x, p.r2);
+  };
+  fk.proposal_logdensity = [D](int t, const double* x) {
+    return log_normal_pdf(*x, D->prop_mean[static_cast<std::size_t>(t)],
+                          D->prop_cov[static_cast<std::size_t>(t)]);
+  };
+  fk.aux_logdensity = fk.proposal_logdensity;
+  fk.init_logdensity = [](const double* x) { return log_normal_pdf(*x, 0.0, 1.0); };
+  fk.transition_logdensity = [drift, p](int, const double* xp, const double* xc) {
+    return log_normal_pdf(*xc, drift(*xp), p.q2);
+  };
+  return fk;
+}
+
 // -------------------------------------------------------------- fk_model
 void validate_model(const FeynmanKacModel& model) {
   if (model.state_dim < 1) throw std::invalid_argument("model: state_dim must be >= 1");

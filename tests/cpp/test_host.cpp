@@ -219,6 +219,22 @@ TEST_CASE(cox_and_constrained_walk_models_run_through_the_reference_api) {
   o.resampler = dsmc::Resampler::multinomial;
   auto r64 = dsmc::run_smoother(rw, o);
   CHECK(std::isfinite(*r64.meta.log_norm_const));
+  // theta-logistic with flat-ish marginals around the observations
+  std::vector<double> ty(21);
+  std::vector<dsmc::ProposalMarginal> mg(21);
+  for (int t = 0; t <= 20; ++t) {
+    ty[t] = 0.3 * std::sin(0.3 * t);
+    mg[t].mean = {ty[t]};
+    mg[t].cov = {0.2};
+  }
+  auto th = dsmc::make_theta_logistic(dsmc::ThetaLogisticParams{}, ty, mg);
+  o.precision = dsmc::Precision::fp32;
+  auto rt = dsmc::run_smoother(th, o);
+  CHECK(std::isfinite(*rt.meta.log_norm_const));
+  for (int t = 0; t <= 20; ++t)
+    CHECK(std::fabs(dsmc::weighted_time_mean(rt.root, t)[0] - ty[t]) < 0.5);
+  CHECK_THROWS_AS(dsmc::make_theta_logistic(dsmc::ThetaLogisticParams{}, ty, {}),
+                  std::invalid_argument);
 }
 
 TEST_CASE(models_without_a_device_descriptor_are_rejected) {
