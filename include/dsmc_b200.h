@@ -330,6 +330,27 @@ DSMC_API int dsmc_window_finish(dsmc_ctx* ctx, const uint32_t* d_root_map,
                                 double* d_mean, double* d_cov);
 
 /* ------------------------------------------------------------------------
+ * Sequential comparator: particle filter with resampling
+ * at every step + forward-filtering backward-sampling of n_draws joint paths.
+ * Replaces run_particle_filter (baselines.hpp:42-49, baselines.cpp:36-98)
+ * followed by ffbs_sample (baselines.hpp:62-63, baselines.cpp:100-160), with
+ * the same stream keys ({seed, 0|1, t, filter_step}, {seed, 0|1, t,
+ * backward_sample} substream m+1); FP32 arithmetic. Outputs: per-time mean /
+ * cov of the draws ((T+1)*d, (T+1)*d*d), optional draws (n_draws*(T+1)*d,
+ * draw-major as FfbsResult::paths) and the filter's log-likelihood estimate.
+ * ------------------------------------------------------------------------ */
+typedef struct dsmc_ffbs_opts {
+  size_t n_particles;
+  size_t n_draws;
+  int resampler;  /* multinomial or systematic */
+  uint64_t seed;
+} dsmc_ffbs_opts;
+
+DSMC_API int dsmc_ffbs_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
+                              const dsmc_ffbs_opts* opts, double* mean, double* cov,
+                              double* paths, double* log_likelihood);
+
+/* ------------------------------------------------------------------------
  * Proposal construction (host, FP64, the step before the
  * leaves): exact Kalman filter + RTS smoother of a DSMC_MODEL_LGSSM
  * descriptor (prop_mean / prop_cov are ignored). Restates kalman_smooth

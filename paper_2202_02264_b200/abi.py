@@ -82,6 +82,11 @@ class WindowOpts(C.Structure):
     ]
 
 
+class FfbsOpts(C.Structure):
+    _fields_ = [("n_particles", C.c_size_t), ("n_draws", C.c_size_t),
+                ("resampler", C.c_int), ("seed", C.c_uint64)]
+
+
 class SvPrior(C.Structure):
     _fields_ = [
         ("mu_mean", C.c_double), ("mu_var", C.c_double),

@@ -15,7 +15,7 @@
 #include <string>
 #include <vector>
 
-#include "compose.cuh"
+#include "ffbs.cuh"
 #include "dsmc_b200.h"
 
 using namespace dsmc_dev;
@@ -1944,3 +1944,124 @@ int dsmc_cross_combine(dsmc_ctx* ctx, const dsmc_model_handle* hc, const dsmc_wi
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ FFBS
+// Sequential comparator: particle filter + backward sampling on the device
+// (run_particle_filter / ffbs_sample, baselines.cpp:36-160), FP32.
+extern "C" int dsmc_ffbs_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
+                                const dsmc_ffbs_opts* opts, double* mean, double* cov,
+                                double* paths, double* log_likelihood) {
+  if (!ctx || !model || !opts) return DSMC_E_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  const int N = (int)opts->n_particles, M = (int)opts->n_draws;
+  if (N < 1) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "particle filter: need n >= 1");
+  if (M < 1) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "ffbs: need n_draws >= 1");
+  if (opts->resampler != DSMC_MULTINOMIAL && opts->resampler != DSMC_SYSTEMATIC)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                   "particle filter: dense resampling only (multinomial or systematic)");
+  dsmc_model_handle* h = nullptr;
+  int rc = make_handle(ctx, model, 1, &h);
+  if (rc) return rc;
+  std::unique_ptr<dsmc_model_handle, void (*)(dsmc_model_handle*)> hold(h, free_handle);
+  const int K = h->K, d = h->d;
+  Arena& A = ctx->arena;
+  void* p;
+  Bufs b{};
+  b.K = K;
+  b.T = K - 1;
+  b.N = N;
+  b.d = d;
+  b.B = 1;
+  b.cap = 1;
+  b.Kt = K;
+  b.models = h->models_dev;
+  b.tc = h->tc;
+  b.bounded = h->bounded;
+  b.leaf_role = DSMC_ROLE_FILTER_STEP;
+  const size_t KN = (size_t)K * N;
+  CU(A.get("X32", KN * sizeof(float4), &p));
+  b.X32 = (float4*)p;
+  CU(A.get("COL", KN * sizeof(float), &p));
+  b.COL = (float*)p;
+  CU(A.get("LW32", (size_t)N * sizeof(float), &p));
+  b.LW32 = (float*)p;
+  CU(A.get("LNC", (size_t)K * sizeof(double), &p));
+  b.LNC = (double*)p;
+  CU(A.get("LWMAX", (size_t)K * sizeof(double), &p));
+  b.LWMAX = (double*)p;
+  CU(A.get("UNI", (size_t)K, &p));
+  b.UNI = (uint8_t*)p;
+  CU(A.get("ERR", sizeof(ErrFlag), &p));
+  b.err = (ErrFlag*)p;
+  CU(A.get("SEEDS", sizeof(uint64_t), &p));
+  b.seeds = (const uint64_t*)p;
+  set_seed_kernel<<<1, 1, 0, ctx->stream>>>((uint64_t*)p, opts->seed);
+  LAUNCHED(ctx);
+  CU(cudaMemsetAsync(b.err, 0, sizeof(ErrFlag), ctx->stream));
+  float* LW;
+  uint32_t *ANC, *P;
+  double *dll, *dmean, *dcov, *dpaths = nullptr;
+  CU(A.get("FF_LW", KN * sizeof(float), &p));
+  LW = (float*)p;
+  CU(A.get("FF_ANC", (size_t)std::max(K - 1, 1) * N * sizeof(uint32_t), &p));
+  ANC = (uint32_t*)p;
+  CU(A.get("FF_P", (size_t)M * K * sizeof(uint32_t), &p));
+  P = (uint32_t*)p;
+  CU(A.get("FF_LL", sizeof(double), &p));
+  dll = (double*)p;
+  CU(A.get("OMEAN", (size_t)K * d * sizeof(double), &p));
+  dmean = (double*)p;
+  CU(A.get("OCOV", (size_t)K * d * d * sizeof(double), &p));
+  dcov = (double*)p;
+  if (paths) {
+    CU(A.get("OPATH", (size_t)M * K * d * sizeof(double), &p));
+    dpaths = (double*)p;
+  }
+  CU(A.get("RAW0", (size_t)N * sizeof(double), &p));
+  double* raw0 = (double*)p;
+  const int lt = std::min(256, (N + 31) / 32 * 32);
+  const int pt = std::min(512, (N + 31) / 32 * 32);
+  const size_t smf = sizeof(double) * N;
+  const size_t smb = sizeof(float4) * N + sizeof(float) * ((N + 1) & ~1) + sizeof(double) * N;
+  if (smb > 227 * 1024) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "ffbs: N too large");
+#define FFBS_RUN(DD)                                                                          \
+  do {                                                                                        \
+    leaf32_kernel<DD><<<dim3(K, 1), lt, 0, ctx->stream>>>(b, raw0);                           \
+    LAUNCHED(ctx);                                                                            \
+    leafnorm32_kernel<<<1, 32, 0, ctx->stream>>>(b, raw0);                                    \
+    LAUNCHED(ctx);                                                                            \
+    CU(cudaFuncSetAttribute(pf_forward_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                            (int)smf));                                                       \
+    pf_forward_kernel<DD><<<1, pt, smf, ctx->stream>>>(b, LW, ANC,                            \
+                                                       opts->resampler == DSMC_SYSTEMATIC, dll); \
+    LAUNCHED(ctx);                                                                            \
+    CU(cudaFuncSetAttribute(ffbs_backward_kernel<DD>,                                         \
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));          \
+    ffbs_backward_kernel<DD><<<(M + 7) / 8, 256, smb, ctx->stream>>>(b, LW, M, P);            \
+    LAUNCHED(ctx);                                                                            \
+    ffbs_moments_kernel<DD><<<(K + 7) / 8, 256, 0, ctx->stream>>>(b, P, M, dmean, dcov,        \
+                                                                   dpaths);                   \
+    LAUNCHED(ctx);                                                                            \
+  } while (0)
+  switch (d) {
+    case 1: FFBS_RUN(1); break;
+    case 2: FFBS_RUN(2); break;
+    case 3: FFBS_RUN(3); break;
+    default: FFBS_RUN(4); break;
+  }
+#undef FFBS_RUN
+  CU(cudaGetLastError());
+  ErrFlag e;
+  CU(cudaMemcpyAsync(&e, b.err, sizeof e, cudaMemcpyDeviceToHost, ctx->stream));
+  double ll = 0.0;
+  CU(cudaMemcpyAsync(&ll, dll, sizeof ll, cudaMemcpyDeviceToHost, ctx->stream));
+  if (mean) CU(cudaMemcpyAsync(mean, dmean, (size_t)K * d * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (cov) CU(cudaMemcpyAsync(cov, dcov, (size_t)K * d * d * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (paths) CU(cudaMemcpyAsync(paths, dpaths, (size_t)M * K * d * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (e.code) return set_err(ctx, e.code, e.reason == kReasonLeafZero
+                                             ? "particle filter: every weight is zero at a time step"
+                                             : "ffbs: every backward weight is zero at a time step");
+  if (log_likelihood) *log_likelihood = ll;
+  return DSMC_OK;
+}

@@ -36,6 +36,8 @@ struct Bufs {
   int conditional;
   uint32_t sweep;
   const double* star;  // [B][K][d] (conditional)
+  int leaf_role;       // FP32 leaf stream role (0 = leaf_proposal; the particle
+                       // filter draws with filter_step, baselines.cpp:17-20)
 };
 
 // Normal number i of a leaf stream (rng.cpp:74-86 via counter addressing:
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(256, 3) leaf32_kernel(Bufs b, double* raw0) {
   const int kind = s_kind, dy = s_dy;
   const bool obs = s_obs != 0;
   const StreamId id = stream_id(b.seeds[ch], 0, leaf_node(gt, b.conditional, b.sweep),
-                                DSMC_ROLE_LEAF_PROPOSAL, 0);
+                                b.leaf_role ? b.leaf_role : DSMC_ROLE_LEAF_PROPOSAL, 0);
   const float colsv = (float)(kLog2E * tc.shift1);
   if (gt != 0 && !b.conditional) {
     // hot path (every leaf but global time 0 of an unconditional run):

@@ -68,6 +68,8 @@ def load_library():
                                    vp, C.c_double, C.c_double, vp, vp, dp]),
         "dsmc_window_remap": (i, [vp, i, vp]),
         "dsmc_window_finish": (i, [vp, vp, vp, vp]),
+        "dsmc_ffbs_smooth": (i, [vp, C.POINTER(abi.ModelDesc), C.POINTER(abi.FfbsOpts), dp, dp,
+                                 dp, dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -255,6 +257,23 @@ class Engine:
 
     def window_finish(self, d_root_map, d_mean, d_cov):
         self._check(self.lib.dsmc_window_finish(self.ctx, d_root_map, d_mean, d_cov))
+
+    # ------------------------------------------------------------- FFBS
+    def ffbs(self, model, n_particles, n_draws=None, resampler=abi.MULTINOMIAL, seed=0,
+             want_paths=False):
+        """Sequential comparator: run_particle_filter + ffbs_sample
+        (baselines.hpp:42-63) on the device, FP32. Returns per-time moments of
+        the n_draws backward draws and the filter's log-likelihood."""
+        K, d = model.horizon + 1, model.d
+        M = n_particles if n_draws is None else n_draws
+        mean, cov = np.zeros((K, d)), np.zeros((K, d, d))
+        paths = np.zeros((M, K, d)) if want_paths else None
+        ll = C.c_double()
+        o = abi.FfbsOpts(n_particles, M, resampler, seed)
+        self._check(self.lib.dsmc_ffbs_smooth(self.ctx, C.byref(model.desc), C.byref(o),
+                                              abi.dptr(mean), abi.dptr(cov), abi.dptr(paths),
+                                              C.byref(ll)))
+        return dict(mean=mean, cov=cov, paths=paths, log_likelihood=ll.value)
 
     # --------------------------------------------------------- SV pGibbs
     def sv_pgibbs_sweep(self, ys, theta, stars, seeds, prior, n_particles, sweep,

@@ -25,7 +25,8 @@ def declared_symbols():
 def test_header_declares_the_boundary():
     syms = declared_symbols()
     for s in ["dsmc_create", "dsmc_smooth", "dsmc_resample_table", "dsmc_conditional_sweep",
-              "dsmc_sv_pgibbs_sweep", "dsmc_smooth_resident", "dsmc_kalman_smooth"]:
+              "dsmc_sv_pgibbs_sweep", "dsmc_smooth_resident", "dsmc_kalman_smooth",
+              "dsmc_ffbs_smooth"]:
         assert s in syms
 
 
