@@ -363,6 +363,18 @@ def run_ours(args, cfg, rank, world, device):
                 "pair_kernel_share_of_step": pair_ms / ms_max if pair_ms else None,
                 "leaf_ms": timings[0], "levels_ms": timings[1],
                 "compose_gather_ms": timings[2] if world == 1 else None}
+        # HBM-class kernels: algorithmic bytes / event time
+        if world == 1 and timings[0] > 0 and timings[2] > 0:
+            leaf_b = K * N * (16 + 4)            # float4 state + column term written
+            gath_b = K * N * (16 + 4 + 4)        # state + level-1 pair + map read
+            hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]) \
+                if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6551.0
+            roof["hbm_kernels"] = {
+                "peak_GBps": hbm,
+                "leaf32": {"bytes": leaf_b, "ms": timings[0],
+                           "GBps": leaf_b / (timings[0] * 1e-3) / 1e9},
+                "compose_gather": {"bytes": gath_b, "ms": timings[2],
+                                   "GBps": gath_b / (timings[2] * 1e-3) / 1e9}}
         prof = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(prof):
             roof["traffic"] = json.load(open(prof)).get(args.config)
