@@ -1604,44 +1604,67 @@ __device__ double sv_loglik(const double* x, int T, double mu, double phi, doubl
 
 // SV ParamKernel (oracle or_sv_param_update): sigma2 | rest
 // (inverse gamma), mu | rest (normal), random-walk Metropolis on phi. One
-// thread per chain, sequential sums (same order as the oracle).
+// warp per chain: the O(T) path sums are lane-strided + a warp reduction
+// (the oracle sums sequentially: values agree to ~1e-15 relative); lane 0
+// draws from the chain's stream in the oracle's order.
+__device__ inline double warp_sum(double v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(~0u, v, o);
+  return v;
+}
 __global__ void sv_param_kernel(DevModel* models, double* theta, const double* stars,
                                 const uint64_t* seeds, dsmc_sv_prior pr, int T,
                                 uint32_t sweep, int B, unsigned long long* acc_phi) {
-  const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ch = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (ch >= B) return;
   const double* x = stars + (size_t)ch * (T + 1);
-  StreamReader s;
-  s.init(stream_id(seeds[ch], 0, sweep, DSMC_ROLE_GIBBS_PARAM, 0));
   double mu = theta[3 * ch], phi = theta[3 * ch + 1], s2 = theta[3 * ch + 2];
-  double ss = (1.0 - phi * phi) * (x[0] - mu) * (x[0] - mu);
-  for (int t = 1; t <= T; ++t) {
+  double ss = 0.0, acc = 0.0;
+  for (int t = 1 + lane; t <= T; t += 32) {
     const double e = x[t] - mu - phi * (x[t - 1] - mu);
     ss += e * e;
+    acc += x[t] - phi * x[t - 1];
   }
-  const double prec = gamma_draw_dev(pr.s2_shape + 0.5 * (double)(T + 1), pr.s2_rate + 0.5 * ss, s);
-  s2 = 1.0 / prec;
-  const double p = 1.0 / pr.mu_var + (1.0 - phi * phi) / s2 +
-                   (double)T * (1.0 - phi) * (1.0 - phi) / s2;
-  double acc = 0.0;
-  for (int t = 1; t <= T; ++t) acc += x[t] - phi * x[t - 1];
-  const double h = pr.mu_mean / pr.mu_var + (1.0 - phi * phi) * x[0] / s2 + (1.0 - phi) * acc / s2;
-  mu = h / p + sqrt(1.0 / p) * s.normal();
-  const double prop = phi + pr.phi_step * s.normal();
-  const double lu = log(s.uniform_pos());
-  if (fabs(prop) < 1.0) {
-    const double dl = sv_loglik(x, T, mu, prop, s2) - sv_loglik(x, T, mu, phi, s2);
-    if (lu < dl) {
-      phi = prop;
-      atomicAdd(acc_phi, 1ull);
+  ss = warp_sum(ss) + (1.0 - phi * phi) * (x[0] - mu) * (x[0] - mu);
+  acc = warp_sum(acc);
+  double prop = 0.0, lu = 0.0;
+  StreamReader s;
+  if (lane == 0) {
+    s.init(stream_id(seeds[ch], 0, sweep, DSMC_ROLE_GIBBS_PARAM, 0));
+    const double prec = gamma_draw_dev(pr.s2_shape + 0.5 * (double)(T + 1), pr.s2_rate + 0.5 * ss, s);
+    s2 = 1.0 / prec;
+    const double p = 1.0 / pr.mu_var + (1.0 - phi * phi) / s2 +
+                     (double)T * (1.0 - phi) * (1.0 - phi) / s2;
+    const double h = pr.mu_mean / pr.mu_var + (1.0 - phi * phi) * x[0] / s2 + (1.0 - phi) * acc / s2;
+    mu = h / p + sqrt(1.0 / p) * s.normal();
+    prop = phi + pr.phi_step * s.normal();
+    lu = log(s.uniform_pos());
+  }
+  mu = __shfl_sync(~0u, mu, 0);
+  s2 = __shfl_sync(~0u, s2, 0);
+  prop = __shfl_sync(~0u, prop, 0);
+  if (fabs(prop) < 1.0) {  // sv_loglik(prop) - sv_loglik(phi), lane-strided
+    double d = 0.0;
+    for (int t = 1 + lane; t <= T; t += 32)
+      d += dlog_normal_pdf(x[t], mu + prop * (x[t - 1] - mu), s2) -
+           dlog_normal_pdf(x[t], mu + phi * (x[t - 1] - mu), s2);
+    d = warp_sum(d);
+    if (lane == 0) {
+      const double dl = d + dlog_normal_pdf(x[0], mu, s2 / (1.0 - prop * prop)) -
+                        dlog_normal_pdf(x[0], mu, s2 / (1.0 - phi * phi));
+      if (lu < dl) {
+        phi = prop;
+        atomicAdd(acc_phi, 1ull);
+      }
     }
   }
-  theta[3 * ch] = mu;
-  theta[3 * ch + 1] = phi;
-  theta[3 * ch + 2] = s2;
-  models[ch].sv_mu = mu;
-  models[ch].sv_phi = phi;
-  models[ch].sv_s2 = s2;
+  if (lane == 0) {
+    theta[3 * ch] = mu;
+    theta[3 * ch + 1] = phi;
+    theta[3 * ch + 2] = s2;
+    models[ch].sv_mu = mu;
+    models[ch].sv_phi = phi;
+    models[ch].sv_s2 = s2;
+  }
 }
 
 }  // namespace
@@ -1692,7 +1715,7 @@ extern "C" int dsmc_sv_pgibbs_sweep(dsmc_ctx* ctx, int B, int T, const double* y
   CU(A.get("GCHG", (size_t)B * K, &p));
   uint8_t* dchg = (uint8_t*)p;
   // parameter kernel (pgibbs_sweep: param_kernel then model rebuild)
-  sv_param_kernel<<<(B + 63) / 64, 64, 0, s>>>(h->models_dev, dtheta, dstar, dseeds, *prior, T,
+  sv_param_kernel<<<(B + 7) / 8, 256, 0, s>>>(h->models_dev, dtheta, dstar, dseeds, *prior, T,
                                                sweep, B, dacc);
   LAUNCHED(ctx);
   std::vector<int> ones(B, 3);
