@@ -690,12 +690,6 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     la.ws_comb = ws_comb;
     la.key_level = level;
     la.node_off = (long long)(o.t0 >> level);
-    if (getenv("DSMC_DEBUG")) {
-      static double* dbg = nullptr;
-      if (!dbg) cudaMallocManaged(&dbg, 256 * 8);
-      la.dbg = dbg;
-    }
-    if (getenv("DSMC_SYNC")) cudaStreamSynchronize(ctx->stream);
     if (o.conditional) {
       la.k0 = 0;
       if (fp64) {
