@@ -33,7 +33,6 @@ struct LevelArgs {
   int slots_per_cta;  // FP32 pass 2 slot slice per CTA
   float* aux;         // FP32 pass 1 -> pass 2 column/row data (Aux32)
   size_t aux_comb;    // floats per combine in aux
-  double* dbg;        // optional debug sink (DSMC_DEBUG)
 };
 
 // Block meta derived from the schedule geometry.
@@ -429,16 +428,6 @@ __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
     if (j == j1) {  // spill: clamp to the last positive entry
       j = j1 - 1;
       while (j > 0 && !(exp_w(DSUB(fill64<MC, D>(M, tc, coef, mu, C, j, sl, lnonuni), mrow)) > 0.0)) --j;
-    }
-    if (la.dbg && m == 0 && k == 0 && la.level == 1) {
-      la.dbg[0] = local; la.dbg[1] = c2b; la.dbg[2] = mrow; la.dbg[3] = row; la.dbg[4] = s;
-      for (int q = 0; q < D; ++q) { la.dbg[5 + q] = mu[q]; la.dbg[9 + q] = xl[q]; }
-      for (int jj = j0; jj < j1 && jj - j0 < 64; ++jj) {
-        la.dbg[16 + jj - j0] = fill64<MC, D>(M, tc, coef, mu, C, jj, sl, lnonuni);
-        la.dbg[80 + jj - j0] = C.base[jj];
-        la.dbg[144 + jj - j0] = C.x[(size_t)jj * d];
-      }
-      la.dbg[13] = d; la.dbg[14] = j; la.dbg[15] = wsub[(size_t)row * nsub];
     }
     PL[m + off] = (uint32_t)row;
     PR[m + off] = (uint32_t)j;
