@@ -190,47 +190,16 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) c32_pair(Bufs b, LevelArgs
   const int nrows = min(kRowsCTA, N - row0);
   const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
   const float4* XL = b.X32 + ((size_t)ch * b.K + L.t) * N;
-  for (int r = threadIdx.x; r < kRowsCTA; r += blockDim.x) {
-    float u[4] = {0, 0, 0, 0}, Bv = -CUDART_INF_F;
-    if (r < nrows) {
-      const int i = row0 + r;
-      const uint32_t p = map_last(b, la, ch, L, i);
-      const float lw2 = lnonuni ? b.LW32[(size_t)ch * N + i] : 0.f;
-      row32<D>(cc, XL[p], lw2, u, Bv);
-      if (cs == 0) {  // hand the row to the sampler
-        ax.u[i] = make_float4(u[0], u[1], u[2], u[3]);
-        ax.B[i] = Bv;
-      }
-    }
-    s_u[r] = make_float4(u[0], u[1], u[2], u[3]);
-    s_b[r] = Bv;
-    float nn = 0.f;
-#pragma unroll
-    for (int q = 0; q < D; ++q) nn = fmaf(0.5f * u[q], 0.5f * u[q], nn);
-    s_c[r] = nn > 100.f ? nn - 100.f : 0.f;
-  }
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // this lane's rows lane + 32 q, q = 0..7, as 4 row pairs (2p, 2p+1)
-  constexpr int NPR = kRPL / 2;
-  float2 U[4][NPR], NC[NPR];
-#pragma unroll
-  for (int pr = 0; pr < NPR; ++pr) {
-    const float4 ua = s_u[lane + 64 * pr], ub = s_u[lane + 64 * pr + 32];
-    U[0][pr] = make_float2(ua.x, ub.x);
-    U[1][pr] = make_float2(ua.y, ub.y);
-    U[2][pr] = make_float2(ua.z, ub.z);
-    U[3][pr] = make_float2(ua.w, ub.w);
-    NC[pr] = make_float2(-s_c[lane + 64 * pr], -s_c[lane + 64 * pr + 32]);
-  }
-  const float2 one2 = make_float2(1.f, 1.f);
   const float4* XR = b.X32 + ((size_t)ch * b.K + R.t) * N;
   const float* CR = b.COL + ((size_t)ch * b.K + R.t) * N;
   const int sb0 = cs * nsub / ncs, sb1 = (cs + 1) * nsub / ncs;
   float4* sy = s_y[warp];
   float* sa = s_a[warp];
   // raw column data (leaf state + column term) of the lane's 2 columns of the
-  // warp's next sub-block, loaded one sub-block ahead of its use
+  // warp's next sub-block, loaded one sub-block ahead of its use; the first
+  // sub-block's gathers are issued before the row prologue so both latencies
+  // overlap
   float4 xr_n[2];
   float cr_n[2];
   auto fetch = [&](int sbk) {
@@ -245,6 +214,55 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) c32_pair(Bufs b, LevelArgs
     }
   };
   fetch(sb0 + warp);
+  // row prologue: the CTA's rows (kRowsCTA / blockDim per thread), all
+  // gathers issued before the arithmetic
+  constexpr int RPT = kRowsCTA / (32 * kPairWarps);
+  float4 xl[RPT];
+  float lwr[RPT];
+#pragma unroll
+  for (int h = 0; h < RPT; ++h) {
+    const int r = threadIdx.x + h * 32 * kPairWarps;
+    xl[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+    lwr[h] = 0.f;
+    if (r < nrows) {
+      const int i = row0 + r;
+      xl[h] = XL[map_last(b, la, ch, L, i)];
+      if (lnonuni) lwr[h] = b.LW32[(size_t)ch * N + i];
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < RPT; ++h) {
+    const int r = threadIdx.x + h * 32 * kPairWarps;
+    float u[4] = {0, 0, 0, 0}, Bv = -CUDART_INF_F;
+    if (r < nrows) {
+      const int i = row0 + r;
+      row32<D>(cc, xl[h], lwr[h], u, Bv);
+      if (cs == 0) {  // hand the row to the sampler
+        ax.u[i] = make_float4(u[0], u[1], u[2], u[3]);
+        ax.B[i] = Bv;
+      }
+    }
+    s_u[r] = make_float4(u[0], u[1], u[2], u[3]);
+    s_b[r] = Bv;
+    float nn = 0.f;
+#pragma unroll
+    for (int q = 0; q < D; ++q) nn = fmaf(0.5f * u[q], 0.5f * u[q], nn);
+    s_c[r] = nn > 100.f ? nn - 100.f : 0.f;
+  }
+  __syncthreads();
+  // this lane's rows lane + 32 q, q = 0..7, as 4 row pairs (2p, 2p+1)
+  constexpr int NPR = kRPL / 2;
+  float2 U[4][NPR], NC[NPR];
+#pragma unroll
+  for (int pr = 0; pr < NPR; ++pr) {
+    const float4 ua = s_u[lane + 64 * pr], ub = s_u[lane + 64 * pr + 32];
+    U[0][pr] = make_float2(ua.x, ub.x);
+    U[1][pr] = make_float2(ua.y, ub.y);
+    U[2][pr] = make_float2(ua.z, ub.z);
+    U[3][pr] = make_float2(ua.w, ub.w);
+    NC[pr] = make_float2(-s_c[lane + 64 * pr], -s_c[lane + 64 * pr + 32]);
+  }
+  const float2 one2 = make_float2(1.f, 1.f);
   for (int sbk = sb0 + warp; sbk < sb1; sbk += kPairWarps) {
     // stage the sub-block's 64 columns (2 per lane), then prefetch the next
     float Ah[2], cm = -CUDART_INF_F;
