@@ -292,6 +292,33 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) c32_pair(Bufs b, LevelArgs
 #pragma unroll
     for (int h = 0; h < 2; ++h) sa[lane + 32 * h] = live ? Ah[h] - cm : -CUDART_INF_F;
     __syncwarp();
+    if (D == 1) {
+      // d = 1: the exact per-(row, sub-block) max as the shift, in a max-only
+      // pass (one FFMA2 + one FMNMX3 per row pair and column, no MUFU) that
+      // hides under the MUFU-bound sum pass of the other warps. The bound
+      // shift is not enough here: column terms spread over hundreds of
+      // log-units (e.g. stochastic volatility, Poisson counts), so far rows'
+      // sums underflow and the per-row fallback below would run for most
+      // warps. With the exact max every sum is >= 1.
+      float2 M[NPR];
+#pragma unroll
+      for (int pr = 0; pr < NPR; ++pr) M[pr] = make_float2(-CUDART_INF_F, -CUDART_INF_F);
+#pragma unroll 2
+      for (int j = 0; j < kSub; j += 2) {
+        const float y0 = sy[j].x, y1 = sy[j + 1].x, a0 = sa[j], a1 = sa[j + 1];
+#pragma unroll
+        for (int pr = 0; pr < NPR; ++pr) {
+          const float2 t0 = __ffma2_rn(make_float2(y0, y0), U[0][pr], make_float2(a0, a0));
+          const float2 t1 = __ffma2_rn(make_float2(y1, y1), U[0][pr], make_float2(a1, a1));
+          M[pr].x = fmax3(M[pr].x, t0.x, t1.x);
+          M[pr].y = fmax3(M[pr].y, t0.y, t1.y);
+        }
+      }
+#pragma unroll
+      for (int pr = 0; pr < NPR; ++pr)
+        NC[pr] = make_float2(M[pr].x > -CUDART_INF_F ? -M[pr].x : 0.f,
+                             M[pr].y > -CUDART_INF_F ? -M[pr].y : 0.f);
+    }
     // S[pr] = sum_j 2^(A'_j + u.y_j - c) for the lane's row pair pr
     float2 S[NPR];
 #pragma unroll
@@ -335,7 +362,8 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) c32_pair(Bufs b, LevelArgs
           }
         Ls = acc > 0.f ? m + lg2(acc) + cm + s_b[r] : -CUDART_INF_F;
       } else {
-        Ls = sq > 0.f ? lg2(sq) + s_c[r] + cm + s_b[r] : -CUDART_INF_F;
+        const float shift = D == 1 ? -((q & 1) ? NC[q >> 1].y : NC[q >> 1].x) : s_c[r];
+        Ls = sq > 0.f ? lg2(sq) + shift + cm + s_b[r] : -CUDART_INF_F;
       }
       ws[(size_t)sbk * N + row0 + r] = Ls;
     }
