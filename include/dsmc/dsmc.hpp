@@ -15,6 +15,7 @@
 //  * Matrices are row-major std::vector<double> (no Eigen in this image).
 #pragma once
 
+#include <array>
 #include <cstddef>
 #include <cstdint>
 #include <functional>
@@ -44,6 +45,35 @@ struct StreamKey {
   std::uint32_t level = 0;
   std::uint64_t node = 0;
   StreamRole role = StreamRole::leaf_proposal;
+};
+
+// Host Philox4x64-10 streams (rng.hpp:33-62, rng.cpp:27-101): the same
+// counter layout {block, node, level << 16 | role, substream} and key {seed,
+// 0x243F6A8885A308D3}, four u64 per block. The GPU kernels draw from the same
+// counters; host streams serve data simulation and the particle-Gibbs
+// parameter kernels.
+namespace rng_detail {
+std::array<std::uint64_t, 4> philox4x64_10(const std::array<std::uint64_t, 4>& ctr,
+                                           const std::array<std::uint64_t, 2>& key);
+}  // namespace rng_detail
+
+class RngStream {
+ public:
+  explicit RngStream(const StreamKey& key, std::uint64_t substream = 0);
+  std::uint64_t next_u64();
+  double uniform();      // [0, 1), 53 bits
+  double uniform_pos();  // (0, 1)
+  double normal();       // Box-Muller, cos first then the cached sin
+  std::uint64_t uniform_index(std::uint64_t n);
+  void fill_uniform(double* out, std::size_t n);
+  void fill_normal(double* out, std::size_t n);
+
+ private:
+  std::array<std::uint64_t, 4> ctr_, buf_{};
+  std::array<std::uint64_t, 2> key_;
+  int pos_ = 4;
+  bool has_cached_ = false;
+  double cached_ = 0.0;
 };
 
 // ------------------------------------------------------ resampling.hpp
@@ -82,9 +112,37 @@ struct KalmanResult {
 };
 KalmanResult kalman_smooth(const LinearGaussianModel& m);
 
-// ------------------------------------------------------ fk_model.hpp
-class RngStream;  // host streams are not needed on the GPU path
+// kalman.hpp:59-63 / kalman.cpp:157-175: x_0 ~ N(m0, P0), x_t ~ N(F x + b, Q),
+// then y_t ~ N(H x_t, R) where observed; Gaussian draws through the
+// jitter-escalating Cholesky (kalman.cpp:15-26) and fill_normal.
+struct LgssmSample {
+  std::vector<std::vector<double>> x, y;
+};
+LgssmSample simulate_lgssm(const LinearGaussianModel& m, RngStream& stream);
 
+// kalman.hpp:65-110: additive-noise nonlinear dynamics, linearisation around a
+// reference trajectory (analytic Jacobian when given, else central
+// differences) and the iterated (IEKS) smoother.
+struct NonlinearGaussianModel {
+  int dim_x = 1, dim_y = 1, horizon = 0;
+  std::vector<double> m0, P0;
+  std::function<std::vector<double>(int t, const std::vector<double>& x)> f;
+  std::function<std::vector<double>(int t, const std::vector<double>& x)> f_jac;  // d*d
+  std::vector<std::vector<double>> Q, H, R, y;
+  std::vector<char> has_obs;
+};
+LinearGaussianModel linearize(const NonlinearGaussianModel& m,
+                              const std::vector<std::vector<double>>& ref);
+struct IteratedSmoothResult {
+  LinearGaussianModel linearized;
+  KalmanResult kr;
+  std::vector<std::vector<double>> ref;
+  int iterations = 0;
+};
+IteratedSmoothResult iterated_smooth(const NonlinearGaussianModel& m, int iterations,
+                                     const std::vector<std::vector<double>>* initial_ref = nullptr);
+
+// ------------------------------------------------------ fk_model.hpp
 struct DeviceModel;  // owning storage behind a dsmc_model_desc
 
 struct FeynmanKacModel {
@@ -133,10 +191,19 @@ struct CoxParams {
   double lambda = 1.0;
 };
 FeynmanKacModel make_cox_model(const CoxParams& p, const std::vector<double>& ys);
+// models.hpp:52-60: the score functional of the experiments and the data
+// simulation (stream {seed, 0, 0, data_sim}, Poisson by product of uniforms
+// in chunks of rate <= 30).
+double cox_score(const CoxParams& p, const double* path, int horizon);
+struct CoxData {
+  std::vector<double> xs, ys;
+};
+CoxData simulate_cox(const CoxParams& p, int horizon, std::uint64_t seed);
 
 // models.cpp:263-338: random walk conditioned to stay inside [-1, 1],
 // U[-1, 1] proposals, finite log_stitch_bound.
 FeynmanKacModel make_constrained_rw(double sigma, int horizon);
+double rw_score(double sigma, const double* path, int horizon);  // models.cpp:340-347
 
 // models.hpp:86-110 / models.cpp:407-491: theta-logistic dynamics with the
 // caller's per-time proposal marginals (1-d ProposalMarginal entries).
@@ -149,6 +216,14 @@ struct ThetaLogisticParams {
 };
 FeynmanKacModel make_theta_logistic(const ThetaLogisticParams& p, const std::vector<double>& ys,
                                     const std::vector<ProposalMarginal>& marginals);
+NonlinearGaussianModel theta_logistic_nonlinear(const ThetaLogisticParams& p,
+                                                const std::vector<double>& ys);
+struct ThetaLogisticData {
+  std::vector<double> xs, ys;
+};
+// stream {seed, 0, 1, data_sim} (models.cpp:517-540)
+ThetaLogisticData simulate_theta_logistic(const ThetaLogisticParams& p, int horizon,
+                                          std::uint64_t seed);
 
 // ------------------------------------------------------ smoother.hpp
 enum class Precision { fp32 = DSMC_FP32, fp64_parity = DSMC_FP64_PARITY };
@@ -239,9 +314,12 @@ std::vector<char> path_changed_times(const double* a, const double* b, int len,
 struct GibbsState {
   std::vector<double> theta;
   std::vector<double> star;
+  std::vector<ProposalMarginal> proposal_cache;
+  std::vector<std::vector<double>> ieks_ref;
 };
-using ParamKernel = std::function<void(GibbsState&, std::uint64_t seed,
-                                       std::uint32_t sweep)>;
+// pgibbs.hpp:43-47: the kernel draws from the sweep's parameter stream
+// {options.seed, 0, sweep, gibbs_param}.
+using ParamKernel = std::function<void(GibbsState&, RngStream&)>;
 using GibbsModelBuilder = std::function<FeynmanKacModel(GibbsState&)>;
 
 struct SweepOutcome {
@@ -261,6 +339,56 @@ SweepOutcome pgibbs_sweep(const GibbsState& state,
 
 std::vector<double> update_rate(const std::vector<std::vector<double>>& stars,
                                 int dim = 1);
+
+// pgibbs.cpp:80-102: Marsaglia-Tsang with the shape < 1 boost.
+double gamma_draw(double shape, double rate, RngStream& stream);
+
+// pgibbs.hpp:70-115: the theta-logistic particle-Gibbs driver (precision
+// draws, joint RWM on (tau0, tau1, tau2, x_0), one warm IEKS refresh of the
+// proposals, c-dSMC path update on the GPU).
+struct ThetaLogisticGibbsConfig {
+  double prec_x_shape = 2.0, prec_x_rate = 1.0;
+  double prec_y_shape = 2.0, prec_y_rate = 1.0;
+  double tau0_sd = 1.0, tau1_sd = 1.0, tau2_sd = 1.0;
+  double rwm_step_tau = 0.05, rwm_step_x0 = 0.1;
+  std::size_t n_particles = 64;
+  Resampler resampler = Resampler::multinomial;
+  int ieks_cold_iterations = 25;
+  double proposal_inflation = 1.0;
+  Precision precision = Precision::fp32;
+  int device = 0;
+};
+ThetaLogisticParams draw_precisions(const ThetaLogisticParams& params,
+                                    const std::vector<double>& ys,
+                                    const std::vector<double>& star,
+                                    const ThetaLogisticGibbsConfig& config, RngStream& stream);
+struct ThetaLogisticChain {
+  std::vector<ThetaLogisticParams> thetas;
+  std::vector<std::vector<double>> stars;
+  std::vector<std::vector<char>> changed;
+  std::size_t rwm_accepts = 0;
+  std::uint64_t weight_evals = 0;
+};
+ThetaLogisticChain run_theta_logistic_pgibbs(const std::vector<double>& ys,
+                                             const ThetaLogisticParams& init,
+                                             const ThetaLogisticGibbsConfig& config,
+                                             std::size_t sweeps, std::uint64_t seed);
+
+// ------------------------------------------------------ baselines.hpp
+// run_particle_filter + ffbs_sample (baselines.hpp:42-63) as one device call
+// (dsmc_ffbs_smooth): n_draws joint draws, draw-major paths.
+struct FfbsResult {
+  std::size_t n_draws = 0;
+  int horizon = 0, dim = 1;
+  std::vector<double> paths;
+  std::uint64_t density_evals = 0;  // n_draws * T * n, as ffbs_sample counts
+  double log_likelihood = 0.0;      // the filter's estimate
+  const double* path(std::size_t m) const {
+    return paths.data() + m * static_cast<std::size_t>(horizon + 1) * dim;
+  }
+};
+FfbsResult ffbs_smooth(const FeynmanKacModel& model, std::size_t n, Resampler resampler,
+                       std::uint64_t seed, std::size_t n_draws = 0, int device = 0);
 
 // Batched SV particle Gibbs: n_chains chains advanced one sweep each, the
 // parameter kernel and the c-dSMC path update both on the device.

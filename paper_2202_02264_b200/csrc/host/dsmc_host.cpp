@@ -3,6 +3,7 @@
 // is delegated to the CUDA engine (libdsmc_b200.so).
 #include "dsmc/dsmc.hpp"
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -553,7 +554,8 @@ SweepOutcome pgibbs_sweep(const GibbsState& state, const GibbsModelBuilder& buil
   if (state.star.empty()) throw std::invalid_argument("pgibbs_sweep: empty reference path");
   SweepOutcome out;
   out.state = state;  // private copy: strong guarantee
-  kernel(out.state, o.seed, sweep);
+  RngStream pstream({o.seed, 0, sweep, StreamRole::gibbs_param});
+  kernel(out.state, pstream);
   FeynmanKacModel model = builder(out.state);
   const std::size_t want = (size_t)(model.horizon + 1) * model.state_dim;
   if (out.state.star.size() != want)
@@ -596,6 +598,473 @@ std::vector<char> sv_pgibbs_sweep(SvGibbsChains& ch, const std::vector<double>& 
                                 sweep, reinterpret_cast<uint8_t*>(changed.data()), &acc));
   ch.phi_accepts += acc;
   return changed;
+}
+
+
+// ------------------------------------------------------------------- rng
+namespace rng_detail {
+std::array<std::uint64_t, 4> philox4x64_10(const std::array<std::uint64_t, 4>& ctr,
+                                           const std::array<std::uint64_t, 2>& key) {
+  // Philox4x64 with the Random123 multipliers and Weyl key increments
+  std::uint64_t x0 = ctr[0], x1 = ctr[1], x2 = ctr[2], x3 = ctr[3];
+  std::uint64_t k0 = key[0], k1 = key[1];
+  for (int r = 0; r < 10; ++r) {
+    const unsigned __int128 p0 = (unsigned __int128)0xD2E7470EE14C6C93ull * x0;
+    const unsigned __int128 p1 = (unsigned __int128)0xCA5A826395121157ull * x2;
+    const std::uint64_t hi0 = (std::uint64_t)(p0 >> 64), lo0 = (std::uint64_t)p0;
+    const std::uint64_t hi1 = (std::uint64_t)(p1 >> 64), lo1 = (std::uint64_t)p1;
+    x0 = hi1 ^ x1 ^ k0;
+    x1 = lo1;
+    x2 = hi0 ^ x3 ^ k1;
+    x3 = lo0;
+    k0 += 0x9E3779B97F4A7C15ull;
+    k1 += 0xBB67AE8584CAA73Bull;
+  }
+  return {x0, x1, x2, x3};
+}
+}  // namespace rng_detail
+
+RngStream::RngStream(const StreamKey& key, std::uint64_t substream)
+    : ctr_{0, key.node, (static_cast<std::uint64_t>(key.level) << 16) |
+                            static_cast<std::uint64_t>(key.role),
+           substream},
+      key_{key.seed, 0x243F6A8885A308D3ull} {}
+
+std::uint64_t RngStream::next_u64() {
+  if (pos_ == 4) {
+    buf_ = rng_detail::philox4x64_10(ctr_, key_);
+    ++ctr_[0];
+    pos_ = 0;
+  }
+  return buf_[pos_++];
+}
+double RngStream::uniform() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+double RngStream::uniform_pos() {
+  return (static_cast<double>(next_u64() >> 12) + 0.5) * 0x1.0p-52;
+}
+double RngStream::normal() {
+  if (has_cached_) {
+    has_cached_ = false;
+    return cached_;
+  }
+  const double u1 = uniform_pos(), u2 = uniform();
+  const double r = std::sqrt(-2.0 * std::log(u1));
+  const double th = 2.0 * 3.141592653589793238462643383279502884 * u2;
+  cached_ = r * std::sin(th);
+  has_cached_ = true;
+  return r * std::cos(th);
+}
+std::uint64_t RngStream::uniform_index(std::uint64_t n) {
+  if (n == 0) throw std::invalid_argument("uniform_index: n must be >= 1");
+  return static_cast<std::uint64_t>(((unsigned __int128)next_u64() * n) >> 64);
+}
+void RngStream::fill_uniform(double* out, std::size_t n) {
+  for (std::size_t i = 0; i < n; ++i) out[i] = uniform();
+}
+void RngStream::fill_normal(double* out, std::size_t n) {
+  for (std::size_t i = 0; i < n; ++i) out[i] = normal();
+}
+
+// ------------------------------------------------------- kalman extras
+namespace {
+
+// Lower Cholesky factor with the escalating jitter of kalman.cpp:15-26
+// (symmetrise, then up to 4 attempts adding scale * 10^(k-12) I).
+std::vector<double> robust_cholesky(std::vector<double> P, int d, const char* what) {
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < i; ++j) P[i * d + j] = P[j * d + i] = 0.5 * (P[i * d + j] + P[j * d + i]);
+  double tr = 0.0;
+  for (int i = 0; i < d; ++i) tr += P[i * d + i];
+  const double scale = std::max(tr / d, 1e-300);
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    std::vector<double> L(d * d, 0.0);
+    bool ok = true;
+    for (int j = 0; j < d && ok; ++j) {
+      double s = P[j * d + j];
+      for (int k = 0; k < j; ++k) s -= L[j * d + k] * L[j * d + k];
+      if (!(s > 0.0)) {
+        ok = false;
+        break;
+      }
+      L[j * d + j] = std::sqrt(s);
+      for (int i = j + 1; i < d; ++i) {
+        double v = P[i * d + j];
+        for (int k = 0; k < j; ++k) v -= L[i * d + k] * L[j * d + k];
+        L[i * d + j] = v / L[j * d + j];
+      }
+    }
+    if (ok) return L;
+    for (int i = 0; i < d; ++i) P[i * d + i] += scale * std::pow(10.0, attempt - 12);
+  }
+  throw std::runtime_error(std::string(what) + ": covariance is not positive definite");
+}
+
+std::vector<double> draw_gaussian(const std::vector<double>& mean, const std::vector<double>& cov,
+                                  RngStream& stream, const char* what) {
+  const int d = static_cast<int>(mean.size());
+  const std::vector<double> L = robust_cholesky(cov, d, what);
+  std::vector<double> z(d), x(mean);
+  stream.fill_normal(z.data(), d);
+  for (int i = 0; i < d; ++i)
+    for (int k = 0; k <= i; ++k) x[i] += L[i * d + k] * z[k];
+  return x;
+}
+
+std::vector<double> matvec(const std::vector<double>& A, const std::vector<double>& x, int rows) {
+  const int cols = static_cast<int>(x.size());
+  std::vector<double> y(rows, 0.0);
+  for (int i = 0; i < rows; ++i)
+    for (int k = 0; k < cols; ++k) y[i] += A[i * cols + k] * x[k];
+  return y;
+}
+
+}  // namespace
+
+LgssmSample simulate_lgssm(const LinearGaussianModel& m, RngStream& stream) {
+  const int T = m.horizon, dx = m.dim_x, dy = m.dim_y;
+  if (T < 0 || (int)m.F.size() != T + 1 || (int)m.H.size() != T + 1 ||
+      (int)m.has_obs.size() != T + 1)
+    throw std::invalid_argument("simulate_lgssm: arrays must have horizon+1 entries");
+  LgssmSample out;
+  out.x.resize(T + 1);
+  out.y.assign(T + 1, std::vector<double>(dy, 0.0));
+  out.x[0] = draw_gaussian(m.m0, m.P0, stream, "simulate");
+  for (int t = 1; t <= T; ++t) {
+    std::vector<double> mu = matvec(m.F[t], out.x[t - 1], dx);
+    for (int k = 0; k < dx; ++k) mu[k] += m.b[t][k];
+    out.x[t] = draw_gaussian(mu, m.Q[t], stream, "simulate");
+  }
+  for (int t = 0; t <= T; ++t)
+    if (m.has_obs[t]) out.y[t] = draw_gaussian(matvec(m.H[t], out.x[t], dy), m.R[t], stream,
+                                               "simulate");
+  return out;
+}
+
+LinearGaussianModel linearize(const NonlinearGaussianModel& m,
+                              const std::vector<std::vector<double>>& ref) {
+  if ((int)ref.size() != m.horizon + 1)
+    throw std::invalid_argument("linearize: reference length != horizon+1");
+  const int d = m.dim_x;
+  LinearGaussianModel lin;
+  lin.dim_x = d;
+  lin.dim_y = m.dim_y;
+  lin.horizon = m.horizon;
+  lin.m0 = m.m0;
+  lin.P0 = m.P0;
+  lin.F.assign(m.horizon + 1, std::vector<double>(d * d, 0.0));
+  lin.b.assign(m.horizon + 1, std::vector<double>(d, 0.0));
+  lin.Q = m.Q;
+  lin.H = m.H;
+  lin.R = m.R;
+  lin.y = m.y;
+  lin.has_obs = m.has_obs;
+  for (int t = 1; t <= m.horizon; ++t) {
+    const std::vector<double>& r = ref[t - 1];
+    std::vector<double> J(d * d);
+    if (m.f_jac) {
+      J = m.f_jac(t, r);
+    } else {  // central differences, step 1e-6 (1 + |x_i|) (kalman.cpp:177-190)
+      for (int i = 0; i < d; ++i) {
+        const double h = 1e-6 * (1.0 + std::fabs(r[i]));
+        std::vector<double> xp = r, xm = r;
+        xp[i] += h;
+        xm[i] -= h;
+        const std::vector<double> fp = m.f(t, xp), fm = m.f(t, xm);
+        for (int k = 0; k < d; ++k) J[k * d + i] = (fp[k] - fm[k]) / (2.0 * h);
+      }
+    }
+    lin.F[t] = J;
+    const std::vector<double> fr = m.f(t, r), Jr = matvec(J, r, d);
+    for (int k = 0; k < d; ++k) lin.b[t][k] = fr[k] - Jr[k];
+  }
+  return lin;
+}
+
+IteratedSmoothResult iterated_smooth(const NonlinearGaussianModel& m, int iterations,
+                                     const std::vector<std::vector<double>>* initial_ref) {
+  if (iterations < 1) throw std::invalid_argument("iterated_smooth: iterations must be >= 1");
+  std::vector<std::vector<double>> ref;
+  if (initial_ref) {
+    ref = *initial_ref;
+  } else {
+    ref.resize(m.horizon + 1);
+    ref[0] = m.m0;
+    for (int t = 1; t <= m.horizon; ++t) ref[t] = m.f(t, ref[t - 1]);
+  }
+  IteratedSmoothResult out;
+  for (int it = 0; it < iterations; ++it) {
+    out.linearized = linearize(m, ref);
+    out.kr = kalman_smooth(out.linearized);
+    ref = out.kr.smooth_mean;
+    out.iterations = it + 1;
+  }
+  out.ref = ref;
+  return out;
+}
+
+// ------------------------------------------------------- model extras
+double cox_score(const CoxParams& p, const double* path, int horizon) {
+  const double s2 = p.sigma2;
+  const double d0 = path[0] - p.mu;
+  double acc = -(horizon + 1) / (2.0 * s2) + (1.0 - p.rho * p.rho) / (2.0 * s2 * s2) * d0 * d0;
+  for (int t = 1; t <= horizon; ++t) {
+    const double e = path[t] - p.mu - p.rho * (path[t - 1] - p.mu);
+    acc += e * e / (2.0 * s2 * s2);
+  }
+  return acc;
+}
+
+namespace {
+std::uint64_t poisson_by_products(double rate, RngStream& stream) {
+  if (!(rate >= 0.0)) throw std::invalid_argument("poisson_draw: rate must be nonnegative");
+  std::uint64_t total = 0;
+  while (rate > 0.0) {  // chunks of <= 30 keep exp(-chunk) representable
+    const double chunk = std::min(rate, 30.0);
+    rate -= chunk;
+    const double limit = std::exp(-chunk);
+    double prod = 1.0;
+    std::uint64_t k = 0;
+    do {
+      ++k;
+      prod *= stream.uniform_pos();
+    } while (prod > limit);
+    total += k - 1;
+  }
+  return total;
+}
+}  // namespace
+
+CoxData simulate_cox(const CoxParams& p, int horizon, std::uint64_t seed) {
+  if (horizon < 0) throw std::invalid_argument("simulate_cox: horizon must be >= 0");
+  const double a = p.rho * p.lambda;
+  if (!(p.sigma2 > 0.0) || !(std::abs(a) < 1.0))
+    throw std::invalid_argument("simulate_cox: invalid parameters");
+  const double c = p.mu * (1.0 - p.rho);
+  RngStream st({seed, 0, 0, StreamRole::data_sim});
+  CoxData d;
+  d.xs.resize(horizon + 1);
+  d.ys.resize(horizon + 1);
+  d.xs[0] = c / (1.0 - a) + std::sqrt(p.sigma2 / (1.0 - a * a)) * st.normal();
+  for (int t = 1; t <= horizon; ++t) d.xs[t] = c + a * d.xs[t - 1] + std::sqrt(p.sigma2) * st.normal();
+  for (int t = 0; t <= horizon; ++t)
+    d.ys[t] = static_cast<double>(poisson_by_products(std::exp(d.xs[t]), st));
+  return d;
+}
+
+double rw_score(double sigma, const double* path, int horizon) {
+  double acc = 0.0;
+  for (int t = 1; t <= horizon; ++t) acc += (path[t] - path[t - 1]) * (path[t] - path[t - 1]);
+  return std::log(sigma) + acc / (sigma * sigma * sigma);
+}
+
+NonlinearGaussianModel theta_logistic_nonlinear(const ThetaLogisticParams& p,
+                                                const std::vector<double>& ys) {
+  if (!(p.q2 > 0.0) || !(p.r2 > 0.0))
+    throw std::invalid_argument("theta_logistic_nonlinear: q2 and r2 must be > 0");
+  if (ys.empty()) throw std::invalid_argument("theta_logistic_nonlinear: no observations");
+  for (double y : ys)
+    if (!std::isfinite(y))
+      throw std::invalid_argument("theta_logistic_nonlinear: observations must be finite");
+  const int T = static_cast<int>(ys.size()) - 1;
+  NonlinearGaussianModel m;
+  m.horizon = T;
+  m.m0 = {0.0};
+  m.P0 = {1.0};
+  m.f = [p](int, const std::vector<double>& x) {
+    return std::vector<double>{x[0] + p.tau0 - p.tau1 * std::exp(p.tau2 * x[0])};
+  };
+  m.f_jac = [p](int, const std::vector<double>& x) {
+    return std::vector<double>{1.0 - p.tau1 * p.tau2 * std::exp(p.tau2 * x[0])};
+  };
+  m.Q.assign(T + 1, {p.q2});
+  m.H.assign(T + 1, {1.0});
+  m.R.assign(T + 1, {p.r2});
+  m.y.resize(T + 1);
+  for (int t = 0; t <= T; ++t) m.y[t] = {ys[t]};
+  m.has_obs.assign(T + 1, 1);
+  return m;
+}
+
+ThetaLogisticData simulate_theta_logistic(const ThetaLogisticParams& p, int horizon,
+                                          std::uint64_t seed) {
+  if (horizon < 0) throw std::invalid_argument("simulate_theta_logistic: horizon must be >= 0");
+  if (!(p.q2 > 0.0) || !(p.r2 > 0.0))
+    throw std::invalid_argument("simulate_theta_logistic: invalid parameters");
+  RngStream st({seed, 0, 1, StreamRole::data_sim});
+  ThetaLogisticData d;
+  d.xs.resize(horizon + 1);
+  d.ys.resize(horizon + 1);
+  d.xs[0] = st.normal();
+  for (int t = 1; t <= horizon; ++t) {
+    const double x = d.xs[t - 1];
+    d.xs[t] = x + p.tau0 - p.tau1 * std::exp(p.tau2 * x) + std::sqrt(p.q2) * st.normal();
+  }
+  for (int t = 0; t <= horizon; ++t) d.ys[t] = d.xs[t] + std::sqrt(p.r2) * st.normal();
+  return d;
+}
+
+// ------------------------------------------------------- pgibbs extras
+double gamma_draw(double shape, double rate, RngStream& stream) {
+  if (!(shape > 0.0) || !(rate > 0.0))
+    throw std::invalid_argument("gamma_draw: shape and rate must be > 0");
+  double boost = 1.0;
+  if (shape < 1.0) {
+    boost = std::pow(stream.uniform_pos(), 1.0 / shape);
+    shape += 1.0;
+  }
+  const double d = shape - 1.0 / 3.0, c = 1.0 / std::sqrt(9.0 * d);
+  for (;;) {
+    double x, v;
+    do {
+      x = stream.normal();
+      v = 1.0 + c * x;
+    } while (v <= 0.0);
+    v = v * v * v;
+    const double u = stream.uniform_pos();
+    if (std::log(u) < 0.5 * x * x + d - d * v + d * std::log(v)) return boost * d * v / rate;
+  }
+}
+
+namespace {
+double theta_drift(const ThetaLogisticParams& p, double x) {
+  return x + p.tau0 - p.tau1 * std::exp(p.tau2 * x);
+}
+
+// pgibbs.cpp:114-134: every joint-density term that moves with (tau, x_0)
+double rwm_target(const ThetaLogisticParams& p, double x0, const std::vector<double>& ys,
+                  const std::vector<double>& star, const ThetaLogisticGibbsConfig& g) {
+  if (p.tau1 <= 0.0 || p.tau2 <= 0.0) return -INFINITY;
+  double acc = log_normal_pdf(p.tau0, 0.0, g.tau0_sd * g.tau0_sd) +
+               log_normal_pdf(p.tau1, 0.0, g.tau1_sd * g.tau1_sd) +
+               log_normal_pdf(p.tau2, 0.0, g.tau2_sd * g.tau2_sd) +
+               log_normal_pdf(x0, 0.0, 1.0) + log_normal_pdf(ys[0], x0, p.r2);
+  double prev = x0;
+  for (std::size_t t = 1; t < star.size(); ++t) {
+    acc += log_normal_pdf(star[t], theta_drift(p, prev), p.q2);
+    prev = star[t];
+  }
+  return acc;
+}
+
+ThetaLogisticParams unpack_theta(const std::vector<double>& v) {
+  if (v.size() != 5) throw std::invalid_argument("theta vector has the wrong size");
+  return {v[0], v[1], v[2], v[3], v[4]};
+}
+std::vector<double> pack_theta(const ThetaLogisticParams& p) {
+  return {p.tau0, p.tau1, p.tau2, p.q2, p.r2};
+}
+}  // namespace
+
+ThetaLogisticParams draw_precisions(const ThetaLogisticParams& params,
+                                    const std::vector<double>& ys,
+                                    const std::vector<double>& star,
+                                    const ThetaLogisticGibbsConfig& g, RngStream& stream) {
+  if (star.size() != ys.size() || star.empty())
+    throw std::invalid_argument("draw_precisions: path and observations must have equal length");
+  const std::size_t T = star.size() - 1;
+  double ssx = 0.0, ssy = 0.0;
+  for (std::size_t t = 1; t <= T; ++t) {
+    const double r = star[t] - theta_drift(params, star[t - 1]);
+    ssx += r * r;
+  }
+  for (std::size_t t = 0; t <= T; ++t) ssy += (ys[t] - star[t]) * (ys[t] - star[t]);
+  ThetaLogisticParams out = params;
+  const double px = gamma_draw(g.prec_x_shape + 0.5 * T, g.prec_x_rate + 0.5 * ssx, stream);
+  const double py = gamma_draw(g.prec_y_shape + 0.5 * (T + 1), g.prec_y_rate + 0.5 * ssy, stream);
+  out.q2 = 1.0 / px;
+  out.r2 = 1.0 / py;
+  return out;
+}
+
+ThetaLogisticChain run_theta_logistic_pgibbs(const std::vector<double>& ys,
+                                             const ThetaLogisticParams& init,
+                                             const ThetaLogisticGibbsConfig& g,
+                                             std::size_t sweeps, std::uint64_t seed) {
+  if (ys.size() < 2)
+    throw std::invalid_argument("run_theta_logistic_pgibbs: need at least two observations");
+  if (!(init.q2 > 0.0) || !(init.r2 > 0.0) || init.tau1 <= 0.0 || init.tau2 <= 0.0)
+    throw std::invalid_argument(
+        "run_theta_logistic_pgibbs: initial parameters outside the prior support");
+  if (g.ieks_cold_iterations < 1)
+    throw std::invalid_argument(
+        "run_theta_logistic_pgibbs: need at least one cold-start iteration");
+  // cold start: linearised smoothing at init; the retained path = smoothed means
+  GibbsState state;
+  state.theta = pack_theta(init);
+  {
+    const IteratedSmoothResult it =
+        iterated_smooth(theta_logistic_nonlinear(init, ys), g.ieks_cold_iterations);
+    state.proposal_cache = proposal_marginals(it.kr, g.proposal_inflation);
+    state.ieks_ref = it.ref;
+    state.star.resize(ys.size());
+    for (std::size_t t = 0; t < ys.size(); ++t) state.star[t] = it.kr.smooth_mean[t][0];
+  }
+  ConditionalOptions co;
+  co.n_particles = g.n_particles;
+  co.resampler = g.resampler;
+  co.seed = seed;
+  co.precision = g.precision;
+  co.device = g.device;
+  ThetaLogisticChain chain;
+  std::size_t* accepts = &chain.rwm_accepts;
+  ParamKernel kernel = [&ys, &g, accepts](GibbsState& s, RngStream& st) {
+    ThetaLogisticParams p = draw_precisions(unpack_theta(s.theta), ys, s.star, g, st);
+    ThetaLogisticParams q = p;
+    q.tau0 = p.tau0 + g.rwm_step_tau * st.normal();
+    q.tau1 = p.tau1 + g.rwm_step_tau * st.normal();
+    q.tau2 = p.tau2 + g.rwm_step_tau * st.normal();
+    const double x0 = s.star[0], x0q = x0 + g.rwm_step_x0 * st.normal();
+    const double delta = rwm_target(q, x0q, ys, s.star, g) - rwm_target(p, x0, ys, s.star, g);
+    if (std::log(st.uniform_pos()) < delta) {
+      p = q;
+      s.star[0] = x0q;
+      ++*accepts;
+    }
+    s.theta = pack_theta(p);
+  };
+  // one warm IEKS step per sweep refreshes the proposals (pgibbs.cpp:244-252)
+  GibbsModelBuilder builder = [&ys, &g](GibbsState& s) {
+    const ThetaLogisticParams p = unpack_theta(s.theta);
+    const IteratedSmoothResult it = iterated_smooth(theta_logistic_nonlinear(p, ys), 1, &s.ieks_ref);
+    s.proposal_cache = proposal_marginals(it.kr, g.proposal_inflation);
+    s.ieks_ref = it.ref;
+    return make_theta_logistic(p, ys, s.proposal_cache);
+  };
+  chain.thetas.reserve(sweeps);
+  chain.stars.reserve(sweeps);
+  chain.changed.reserve(sweeps);
+  for (std::size_t s = 1; s <= sweeps; ++s) {
+    SweepOutcome out = pgibbs_sweep(state, builder, kernel, co, static_cast<std::uint32_t>(s));
+    state = std::move(out.state);
+    chain.thetas.push_back(unpack_theta(state.theta));
+    chain.stars.push_back(state.star);
+    chain.changed.push_back(std::move(out.changed));
+    chain.weight_evals += out.meta.weight_evals;
+  }
+  return chain;
+}
+
+// ------------------------------------------------------------- baselines
+FfbsResult ffbs_smooth(const FeynmanKacModel& model, std::size_t n, Resampler resampler,
+                       std::uint64_t seed, std::size_t n_draws, int device) {
+  validate_model(model);
+  if (resampler_is_lazy(resampler))
+    throw std::invalid_argument("the particle filter resamples with a dense scheme "
+                                "(multinomial or systematic)");
+  const dsmc_model_desc& desc = desc_of(model);
+  dsmc_ctx* c = context(device);
+  const int K = model.horizon + 1, d = model.state_dim;
+  FfbsResult r;
+  r.n_draws = n_draws ? n_draws : n;
+  r.horizon = model.horizon;
+  r.dim = d;
+  r.paths.resize(r.n_draws * K * d);
+  std::vector<double> mean((size_t)K * d), cov((size_t)K * d * d);
+  dsmc_ffbs_opts fo{n, r.n_draws, static_cast<int>(resampler), seed};
+  check(c, dsmc_ffbs_smooth(c, &desc, &fo, mean.data(), cov.data(), r.paths.data(),
+                            &r.log_likelihood));
+  r.density_evals = static_cast<std::uint64_t>(r.n_draws) * model.horizon * n;
+  return r;
 }
 
 }  // namespace dsmc

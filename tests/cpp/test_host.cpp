@@ -1,6 +1,7 @@
 // C++ host API tests, written like the reference's doctest cases (the
 // reference's test names are kept in the CASE titles; file:line cites the
 // case each one ports). Runs on the GPU through include/dsmc/dsmc.hpp.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -298,7 +299,7 @@ TEST_CASE(pgibbs_sweep_aborts_cleanly_when_a_kernel_or_builder_throws) {
   st.theta = {1.0};
   st.star.assign(8, 0.1);
   const auto saved = st;
-  auto bad_kernel = [](dsmc::GibbsState&, std::uint64_t, std::uint32_t) {
+  auto bad_kernel = [](dsmc::GibbsState&, dsmc::RngStream&) {
     throw std::runtime_error("kernel failed");
   };
   auto builder = [](dsmc::GibbsState&) { return ar1_fk(7); };
@@ -306,7 +307,7 @@ TEST_CASE(pgibbs_sweep_aborts_cleanly_when_a_kernel_or_builder_throws) {
   o.n_particles = 16;
   CHECK_THROWS_AS(dsmc::pgibbs_sweep(st, builder, bad_kernel, o, 0), std::runtime_error);
   CHECK(st.star == saved.star && st.theta == saved.theta);
-  auto id_kernel = [](dsmc::GibbsState&, std::uint64_t, std::uint32_t) {};
+  auto id_kernel = [](dsmc::GibbsState&, dsmc::RngStream&) {};
   auto out = dsmc::pgibbs_sweep(st, builder, id_kernel, o, 1);
   CHECK(out.state.star.size() == 8);
   CHECK(out.changed.size() == 8);
@@ -338,6 +339,140 @@ TEST_CASE(batched_sv_particle_gibbs_moves_parameters_and_paths) {
   CHECK(ch.theta != theta0);
   CHECK(moved > (std::size_t)(B * (T + 1)));
   for (double v : ch.stars) CHECK(std::isfinite(v));
+}
+
+// ---------------------------------------------------------------------------
+// Host-only cases (no GPU): run with `test_host cpu_`.
+
+// test_rng.cpp:32-47: Philox4x64-10 known-answer vectors
+TEST_CASE(cpu_philox4x64_10_known_answer_vectors) {
+  const auto z = dsmc::rng_detail::philox4x64_10({0, 0, 0, 0}, {0, 0});
+  CHECK(z[0] == 0x16554d9eca36314cull);
+  CHECK(z[1] == 0xdb20fe9d672d0fdcull);
+  CHECK(z[2] == 0xd7e772cee186176bull);
+  CHECK(z[3] == 0x7e68b68aec7ba23bull);
+  const auto w = dsmc::rng_detail::philox4x64_10(
+      {0xdeadbeefull, 1, 2, 3}, {0x9E3779B97F4A7C15ull, 0x243F6A8885A308D3ull});
+  CHECK(w[0] == 0x89aa73bbe8e9ebdbull);
+  CHECK(w[1] == 0x42065f627a6e7ccfull);
+  CHECK(w[2] == 0xf103ff19821da020ull);
+  CHECK(w[3] == 0x0cf1b816fdc3eb80ull);
+}
+
+// test_rng.cpp:49-80: identical keys give identical streams, distinct
+// substreams and roles differ, uniforms stay in range
+TEST_CASE(cpu_streams_are_keyed_and_in_range) {
+  const dsmc::StreamKey key{42, 3, 17, dsmc::StreamRole::pair_resample};
+  dsmc::RngStream a(key), b(key), c(key, 1);
+  dsmc::StreamKey k2 = key;
+  k2.role = dsmc::StreamRole::leaf_proposal;
+  dsmc::RngStream d(k2);
+  int same_c = 0, same_d = 0;
+  for (int i = 0; i < 64; ++i) {
+    const std::uint64_t x = a.next_u64();
+    CHECK(x == b.next_u64());
+    same_c += x == c.next_u64();
+    same_d += x == d.next_u64();
+  }
+  CHECK(same_c == 0 && same_d == 0);
+  dsmc::RngStream u({7, 0, 0, dsmc::StreamRole::data_sim});
+  double lo = 1, hi = 0, s = 0, s2 = 0;
+  for (int i = 0; i < 20000; ++i) {
+    const double x = u.uniform_pos();
+    lo = std::min(lo, x);
+    hi = std::max(hi, x);
+    const double z = u.normal();
+    s += z;
+    s2 += z * z;
+  }
+  CHECK(lo > 0.0 && hi < 1.0);
+  CHECK(std::fabs(s / 20000) < 0.05 && std::fabs(s2 / 20000 - 1.0) < 0.05);
+  for (int i = 0; i < 1000; ++i) CHECK(u.uniform_index(7) < 7);
+}
+
+// Data simulation follows the reference's streams: values pinned by
+// tests/golden/make_harness_golden.py (reference Philox, restated simulators)
+TEST_CASE(cpu_simulated_data_matches_the_reference_streams) {
+  const auto cox = dsmc::simulate_cox(dsmc::CoxParams{}, 15, 90210);
+  const std::vector<double> want = {4, 3, 6, 6, 11, 3, 6, 1, 5, 2, 0, 0, 0, 1, 0, 1};
+  CHECK(cox.ys == want);
+  dsmc::LinearGaussianModel m;
+  m.horizon = 31;
+  m.m0 = {0.0};
+  m.P0 = {1.0};
+  m.F.assign(32, {0.9});
+  m.b.assign(32, {0.0});
+  m.Q.assign(32, {0.25});
+  m.H.assign(32, {1.0});
+  m.R.assign(32, {0.25});
+  m.y.assign(32, {0.0});
+  m.has_obs.assign(32, 1);
+  dsmc::RngStream st({90210, 0, 0, dsmc::StreamRole::data_sim});
+  const auto s = dsmc::simulate_lgssm(m, st);
+  CHECK(s.y[0][0] == 1.5863467310809578);
+  CHECK(s.y[1][0] == 1.0690823364517432);
+  CHECK(s.y[2][0] == -0.16730312329906827);
+  CHECK(s.y[3][0] == 1.8049285543505404);
+  const auto th = dsmc::simulate_theta_logistic(dsmc::ThetaLogisticParams{}, 40, 5);
+  CHECK(th.ys.size() == 41);
+  CHECK_THROWS_AS(dsmc::simulate_cox(dsmc::CoxParams{0, 0.9, -1, 1}, 3, 1), std::invalid_argument);
+}
+
+// pgibbs.cpp:80-102: gamma draws have mean shape / rate (both branches)
+TEST_CASE(cpu_gamma_draw_moments) {
+  dsmc::RngStream st({11, 0, 0, dsmc::StreamRole::gibbs_param});
+  for (double shape : {0.5, 3.0}) {
+    double acc = 0.0;
+    const int n = 40000;
+    for (int i = 0; i < n; ++i) acc += dsmc::gamma_draw(shape, 2.0, st);
+    const double m = acc / n, sd = std::sqrt(shape) / 2.0 / std::sqrt((double)n);
+    CHECK(std::fabs(m - shape / 2.0) < 5 * sd);
+  }
+  CHECK_THROWS_AS(dsmc::gamma_draw(0.0, 1.0, st), std::invalid_argument);
+}
+
+// kalman.cpp:192-243: linear dynamics linearise exactly, so one IEKS
+// iteration equals the Kalman/RTS smoother; the theta-logistic IEKS
+// converges (fixed point of the reference trajectory)
+TEST_CASE(cpu_iterated_smoother) {
+  const int T = 30;
+  dsmc::NonlinearGaussianModel nl;
+  nl.horizon = T;
+  nl.m0 = {0.0};
+  nl.P0 = {1.0};
+  nl.f = [](int, const std::vector<double>& x) { return std::vector<double>{0.8 * x[0] + 0.1}; };
+  nl.Q.assign(T + 1, {0.3});
+  nl.H.assign(T + 1, {1.0});
+  nl.R.assign(T + 1, {0.4});
+  nl.y.resize(T + 1);
+  for (int t = 0; t <= T; ++t) nl.y[t] = {std::sin(0.3 * t)};
+  nl.has_obs.assign(T + 1, 1);
+  const auto it = dsmc::iterated_smooth(nl, 1);
+  dsmc::LinearGaussianModel lin = it.linearized;
+  for (int t = 1; t <= T; ++t) {
+    CHECK(std::fabs(lin.F[t][0] - 0.8) < 1e-8);  // central differences
+    CHECK(std::fabs(lin.b[t][0] - 0.1) < 1e-8);
+  }
+  std::vector<double> ys(T + 1);
+  for (int t = 0; t <= T; ++t) ys[t] = 0.5 + 0.1 * std::cos(0.2 * t);
+  const auto th = dsmc::theta_logistic_nonlinear(dsmc::ThetaLogisticParams{}, ys);
+  const auto a = dsmc::iterated_smooth(th, 25);
+  const auto b = dsmc::iterated_smooth(th, 1, &a.ref);
+  double diff = 0.0;
+  for (int t = 0; t <= T; ++t) diff = std::max(diff, std::fabs(a.ref[t][0] - b.ref[t][0]));
+  CHECK(diff < 1e-9);
+  CHECK(a.iterations == 25 && b.iterations == 1);
+}
+
+TEST_CASE(cpu_scores_match_their_definitions) {
+  const double path[3] = {0.1, -0.2, 0.4};
+  const dsmc::CoxParams p{};
+  const double s2 = p.sigma2;
+  double want = -3 / (2 * s2) + (1 - p.rho * p.rho) / (2 * s2 * s2) * 0.01;
+  const double e1 = -0.2 - 0.9 * 0.1, e2 = 0.4 - 0.9 * -0.2;
+  want += e1 * e1 / (2 * s2 * s2) + e2 * e2 / (2 * s2 * s2);
+  CHECK(std::fabs(dsmc::cox_score(p, path, 2) - want) < 1e-12);
+  CHECK(std::fabs(dsmc::rw_score(0.5, path, 2) - (std::log(0.5) + (0.09 + 0.36) / 0.125)) < 1e-12);
 }
 
 int main(int argc, char** argv) {
