@@ -33,6 +33,8 @@ struct LevelArgs {
   int slots_per_cta;  // FP32 pass 2 slot slice per CTA
   float* aux;         // FP32 pass 1 -> pass 2 column/row data (Aux32)
   size_t aux_comb;    // floats per combine in aux
+  int tc_ncs;         // tensor-core pass 1: column splits per 128-row tile
+  int tc_nk;          // ... and combines in this chunk (persistent work list)
 };
 
 // Block meta derived from the schedule geometry.

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "ffbs.cuh"
+#include "pair_tc.cuh"
 #include "dsmc_b200.h"
 
 using namespace dsmc_dev;
@@ -77,6 +78,10 @@ struct dsmc_ctx {
   std::vector<cudaEvent_t> kev;
   int kev_used = 0;
   bool time_kernels = false;
+  // FP32 pass 1: the CUDA-core kernel c32_pair (default, faster today) or
+  // the tcgen05 kernel c32_pair_tc (DSMC_PAIR_KERNEL=tc)
+  bool pair_tc = false;
+  int num_sms = 148;
   // last resident run
   int last_K = 0, last_d = 0, last_B = 0;
   double* d_mean = nullptr;
@@ -452,7 +457,28 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
     ctx->kev_used += 3;
     CU(rec_event(ev[0], ctx->stream));
   }
-  c32_pair<D><<<dim3(nrt * ncs, nk, b.B), 32 * kPairWarps, 0, ctx->stream>>>(b, la);
+  const bool use_tc = ctx->pair_tc && nsubb <= kTcMaxSub &&
+                      tc_smem_bytes<D>(nsubb) <= (size_t)64 * 1024;
+  if (use_tc) {
+    // persistent tensor-core pass 1: items = (column split, combine, chain),
+    // 3 CTAs per SM, the item's columns cached in dynamic shared memory
+    int ncs_tc = 1;
+    while (ncs_tc * 2 <= nsubb && (long)nk * b.B * ncs_tc < 148 * kTcCtasPerSm * 2) ncs_tc *= 2;
+    la.tc_ncs = ncs_tc;
+    la.tc_nk = nk;
+    const size_t smem = tc_smem_bytes<D>((nsubb + ncs_tc - 1) / ncs_tc);
+    static bool tc_configured = false;
+    if (!tc_configured) {
+      CU(cudaFuncSetAttribute(c32_pair_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              64 * 1024));
+      tc_configured = true;
+    }
+    const long W = (long)ncs_tc * nk * b.B;
+    const int grid = (int)std::min<long>(W, (long)ctx->num_sms * kTcCtasPerSm);
+    c32_pair_tc<D><<<grid, kTcThreads, smem, ctx->stream>>>(b, la);
+  } else {
+    c32_pair<D><<<dim3(nrt * ncs, nk, b.B), 32 * kPairWarps, 0, ctx->stream>>>(b, la);
+  }
   LAUNCHED(ctx);
   if (ev) CU(rec_event(ev[1], ctx->stream));
   c32_sample<D><<<dim3(sb, nk, b.B), 256, sm2, ctx->stream>>>(b, la, systematic);
@@ -866,6 +892,8 @@ int dsmc_create(int device, dsmc_ctx** out) {
     return DSMC_E_NO_DEVICE;
   auto* ctx = new dsmc_ctx();
   ctx->device = device;
+  if (const char* pk = getenv("DSMC_PAIR_KERNEL")) ctx->pair_tc = strcmp(pk, "tc") == 0;
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
