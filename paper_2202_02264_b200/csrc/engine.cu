@@ -457,25 +457,13 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
     ctx->kev_used += 3;
     CU(rec_event(ev[0], ctx->stream));
   }
-  const bool use_tc = ctx->pair_tc && nsubb <= kTcMaxSub &&
-                      tc_smem_bytes<D>(nsubb) <= (size_t)64 * 1024;
+  const bool use_tc = ctx->pair_tc && D >= 2;
   if (use_tc) {
-    // persistent tensor-core pass 1: items = (column split, combine, chain),
-    // 3 CTAs per SM, the item's columns cached in dynamic shared memory
+    // tensor-core pass 1: 128-row tiles, 4 CTAs per SM (128 TMEM columns each)
+    const int nrt_tc = (N + kTcRows - 1) / kTcRows;
     int ncs_tc = 1;
-    while (ncs_tc * 2 <= nsubb && (long)nk * b.B * ncs_tc < 148 * kTcCtasPerSm * 2) ncs_tc *= 2;
-    la.tc_ncs = ncs_tc;
-    la.tc_nk = nk;
-    const size_t smem = tc_smem_bytes<D>((nsubb + ncs_tc - 1) / ncs_tc);
-    static bool tc_configured = false;
-    if (!tc_configured) {
-      CU(cudaFuncSetAttribute(c32_pair_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              64 * 1024));
-      tc_configured = true;
-    }
-    const long W = (long)ncs_tc * nk * b.B;
-    const int grid = (int)std::min<long>(W, (long)ctx->num_sms * kTcCtasPerSm);
-    c32_pair_tc<D><<<grid, kTcThreads, smem, ctx->stream>>>(b, la);
+    while (ncs_tc * 2 <= nsubb && (long)nk * b.B * nrt_tc * ncs_tc < target) ncs_tc *= 2;
+    c32_pair_tc<D><<<dim3(nrt_tc * ncs_tc, nk, b.B), kTcThreads, 0, ctx->stream>>>(b, la);
   } else {
     c32_pair<D><<<dim3(nrt * ncs, nk, b.B), 32 * kPairWarps, 0, ctx->stream>>>(b, la);
   }
