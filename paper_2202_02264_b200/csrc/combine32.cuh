@@ -400,8 +400,10 @@ __device__ inline double block_scan_incl(double v, double* sh) {
 // search over the row CDF in shared memory, a walk over the row's sub-block
 // sums, and a recomputation of the chosen sub-block's <= 64 weights with
 // pass 1's FP32 pair arithmetic (two columns per FFMA2 / FADD2).
-template <int D>
-__global__ void __launch_bounds__(256, 3) c32_sample(Bufs b, LevelArgs la,
+// MINB: 3 CTAs/SM when N ~ 1024 fills shared memory, 4 (64 registers) for
+// smaller N where the occupancy gain wins (C4 N = 512: 35.1 -> 34.1 ms/sweep)
+template <int D, int MINB>
+__global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
                                                      int systematic) {
   extern __shared__ double smem[];
   __shared__ double sh[32];

@@ -431,15 +431,21 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
                      sizeof(int) * (32 + nsub);
   static bool configured = false;
   if (!configured) {
-    CU(cudaFuncSetAttribute(c32_sample<D>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    CU(cudaFuncSetAttribute(c32_sample<D, 3>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            cudaSharedmemCarveoutMaxShared));
+    CU(cudaFuncSetAttribute(c32_sample<D, 4>, cudaFuncAttributePreferredSharedMemoryCarveout,
                             cudaSharedmemCarveoutMaxShared));
     configured = true;
   }
+  const bool sample4 = sm2 <= 48 * 1024;
   if (sm2 > 227 * 1024)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
                    "FP32 dense combine: N too large for the shared-memory sampler (use a lazy "
                    "resampler)");
-  CU(cudaFuncSetAttribute(c32_sample<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+  CU(cudaFuncSetAttribute(c32_sample<D, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+  if (sample4)
+    CU(cudaFuncSetAttribute(c32_sample<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sm2));
   la.aux_comb = ((size_t)10 * N + 3) & ~(size_t)3;
   {
     void* p;
@@ -469,7 +475,10 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
   }
   LAUNCHED(ctx);
   if (ev) CU(rec_event(ev[1], ctx->stream));
-  c32_sample<D><<<dim3(sb, nk, b.B), 256, sm2, ctx->stream>>>(b, la, systematic);
+  if (sample4)
+    c32_sample<D, 4><<<dim3(sb, nk, b.B), 256, sm2, ctx->stream>>>(b, la, systematic);
+  else
+    c32_sample<D, 3><<<dim3(sb, nk, b.B), 256, sm2, ctx->stream>>>(b, la, systematic);
   LAUNCHED(ctx);
   if (ev) CU(rec_event(ev[2], ctx->stream));
   return DSMC_OK;
