@@ -120,7 +120,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 constexpr int kTcConsumers = kTcRows;               // warps 0-3: one row (TMEM lane) each
-constexpr int kTcThreads = kTcConsumers + kSub;      // + warps 4-5: one column each
+constexpr int kTcProducers = kSub;                   // warps 4-5: one column each
+constexpr int kTcThreads = kTcConsumers + kTcProducers + 32;  // + warp 6: MMA issue
+constexpr int kTcBufs = 4;     // staged sub-blocks in flight (shared memory)
 constexpr int kTcStages = 4;   // TMEM accumulator stages of kTcHalf columns
 constexpr int kTcHalf = 32;    // columns per MMA / TMEM stage (half a sub-block)
 constexpr int kTcCtasPerSm = 4;  // 4 x 128 TMEM columns
@@ -141,11 +143,12 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, 
   using L = TcK<D>;
   constexpr int CB = kSub / 8 * L::SBO;  // bytes of one staged sub-block
   __shared__ __align__(128) uint8_t sA[kTcRows / 8 * L::SBO];
-  __shared__ __align__(128) uint8_t sB[2][CB];
-  __shared__ __align__(8) uint64_t bar_full[2], bar_tfull[kTcStages], bar_tempty[kTcStages];
+  __shared__ __align__(128) uint8_t sB[kTcBufs][CB];
+  __shared__ __align__(8) uint64_t bar_full[kTcBufs], bar_bfree[kTcBufs], bar_tfull[kTcStages],
+      bar_tempty[kTcStages];
   __shared__ uint32_t s_tmem;
-  __shared__ float s_cm[2][2];  // per buffer: the two producer warps' column maxima
-  __shared__ float s_cmax[2];   // per buffer: cmax of the staged sub-block
+  __shared__ float s_cm[kTcBufs][2];  // per buffer: the two producer warps' column maxima
+  __shared__ float s_cmax[kTcBufs];   // per buffer: cmax of the staged sub-block
   const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
   const int N = b.N;
   const int nsub = (N + kSub - 1) / kSub;
@@ -169,7 +172,10 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, 
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == kTcConsumers) {
-    for (int q = 0; q < 2; ++q) mbar_init(&bar_full[q], kSub);
+    for (int q = 0; q < kTcBufs; ++q) {
+      mbar_init(&bar_full[q], kTcProducers);
+      mbar_init(&bar_bfree[q], kTcConsumers / 32);
+    }
     for (int q = 0; q < kTcStages; ++q) {
       mbar_init(&bar_tfull[q], 1);
       mbar_init(&bar_tempty[q], kTcConsumers / 32);
@@ -177,7 +183,45 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, 
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
 
-  if (tid >= kTcConsumers) {
+  if (tid >= kTcConsumers + kTcProducers) {
+    // ----------------------------------------------------------- issuer
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();  // (1)
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = s_tmem;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                           ((uint32_t)(kTcHalf >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
+    __syncthreads();  // (2) the rows are in sA
+    for (int q = 0; q < nq; ++q) {
+      mbar_wait(smem_u32(&bar_full[q % kTcBufs]), (q / kTcBufs) & 1);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int hq = 2 * q + h;
+        if (hq >= kTcStages)
+          mbar_wait(smem_u32(&bar_tempty[hq % kTcStages]), ((hq / kTcStages) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (lane == 0) {
+          const uint32_t dcol = tmem + (uint32_t)((hq % kTcStages) * kTcHalf);
+#pragma unroll
+          for (int ks = 0; ks < L::KS; ++ks) {
+            const uint64_t da = umma_sdesc(smem_u32(sA) + ks * 2 * L::LBO, L::LBO, L::SBO);
+            // columns 32h..32h+31 = core-matrix groups 4h..4h+3
+            const uint64_t db = umma_sdesc(
+                smem_u32(sB[q % kTcBufs]) + h * 4 * L::SBO + ks * 2 * L::LBO, L::LBO, L::SBO);
+            const uint32_t acc = ks > 0;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dcol),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                  smem_u32(&bar_tfull[hq % kTcStages])));
+        }
+        __syncwarp();
+      }
+    }
+  } else if (tid >= kTcConsumers) {
     // -------------------------------------------------------- producers
     const int p = tid - kTcConsumers;
     const int pw = p >> 5;  // producer warp 0 / 1
@@ -201,12 +245,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, 
         k0 = CR[i0];
       }
     }
-    asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();  // (1) barriers initialised, TMEM allocated
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t tmem = s_tmem;
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
-                           ((uint32_t)(kTcHalf >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
     __syncthreads();  // (2) the rows are in sA
     for (int q = 0; q < nq; ++q) {
       const int sbk = sb0 + q;
@@ -240,16 +279,14 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, 
       float cm = cv;
 #pragma unroll
       for (int o = 16; o; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(~0u, cm, o));
-      // buffer q & 1 (and its cmax slot) is free once the consumers released
-      // the second half of sub-block q - 2: its MMAs completed and cmax was read
-      if (q >= 2) {
-        const int hq = 2 * (q - 2) + 1;
-        mbar_wait(smem_u32(&bar_tempty[hq % kTcStages]), (hq / kTcStages) & 1);
-      }
-      if (lane == 0) s_cm[q & 1][pw] = cm;
-      asm volatile("bar.sync 1, %0;" ::"n"(kSub));
-      cm = fmaxf(s_cm[q & 1][0], s_cm[q & 1][1]);
-      if (p == 0) s_cmax[q & 1] = cm;
+      // buffer q % kTcBufs (and its cmax slot) is free once the consumers
+      // finished reading sub-block q - kTcBufs (its MMAs completed before)
+      const int bq = q % kTcBufs;
+      if (q >= kTcBufs) mbar_wait(smem_u32(&bar_bfree[bq]), ((q / kTcBufs) - 1) & 1);
+      if (lane == 0) s_cm[bq][pw] = cm;
+      asm volatile("bar.sync 1, %0;" ::"n"(kTcProducers));
+      cm = fmaxf(s_cm[bq][0], s_cm[bq][1]);
+      if (p == 0) s_cmax[bq] = cm;
       float vals[16];
 #pragma unroll
       for (int c = 0; c < 16; ++c) vals[c] = 0.f;
@@ -267,36 +304,9 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, 
       vals[3 * D + 1] = clive ? a - ah : 0.f;
       vals[3 * D + 2] = 1.f;
       vals[3 * D + 3] = 1.f;
-      tc_store_row<D>(sB[q & 1], p, vals);
+      tc_store_row<D>(sB[bq], p, vals);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&bar_full[q & 1]);
-      if (p == 0) {
-        mbar_wait(smem_u32(&bar_full[q & 1]), (q >> 1) & 1);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int hq = 2 * q + h;
-          if (hq >= kTcStages)
-            mbar_wait(smem_u32(&bar_tempty[hq % kTcStages]), ((hq / kTcStages) - 1) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t dcol = tmem + (uint32_t)((hq % kTcStages) * kTcHalf);
-#pragma unroll
-          for (int ks = 0; ks < L::KS; ++ks) {
-            const uint64_t da = umma_sdesc(smem_u32(sA) + ks * 2 * L::LBO, L::LBO, L::SBO);
-            // columns 32h..32h+31 = core-matrix groups 4h..4h+3
-            const uint64_t db = umma_sdesc(smem_u32(sB[q & 1]) + h * 4 * L::SBO + ks * 2 * L::LBO,
-                                           L::LBO, L::SBO);
-            const uint32_t acc = ks > 0;
-            asm volatile(
-                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dcol),
-                "l"(da), "l"(db), "r"(idesc), "r"(acc));
-          }
-          asm volatile(
-              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                  smem_u32(&bar_tfull[hq % kTcStages])));
-        }
-      }
-      __syncwarp();
+      mbar_arrive(&bar_full[bq]);
       x0 = x1;
       k0 = k1;
       i1 = i2;
@@ -371,13 +381,16 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, 
         const int hq = 2 * q + h;
         mbar_wait(smem_u32(&bar_tfull[hq % kTcStages]), (hq / kTcStages) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        if (h == 0) cmx = s_cmax[q & 1];  // read before the stage is released
+        if (h == 0) cmx = s_cmax[q % kTcBufs];  // read before the buffer is released
         float v[32];
         tmem_ld32(tmem + lane_off + (uint32_t)((hq % kTcStages) * kTcHalf), v);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bar_tempty[hq % kTcStages]);
+        if (lane == 0) {
+          mbar_arrive(&bar_tempty[hq % kTcStages]);
+          if (h == 1) mbar_arrive(&bar_bfree[q % kTcBufs]);
+        }
         float2 a4[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) a4[c] = make_float2(0.f, 0.f);
