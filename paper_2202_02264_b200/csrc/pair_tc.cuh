@@ -110,6 +110,35 @@ __device__ __forceinline__ void tc_store_row(uint8_t* base, int r, const float* 
 
 constexpr float kDeadCol = -1e30f;  // finite stand-in for A_j = -inf
 
+// 2^x for a pair on the FMA / ALU pipes (no MUFU): round-to-nearest split
+// x = n + r (magic-number add), r in [-1/2, 1/2], degree-6 Taylor of 2^r
+// (relative error < 1.3e-7, the order of ex2.approx), 2^n added to the
+// exponent bits. x is clamped to [-125, 127]: results below 2^-125 are
+// negligible next to a sum >= 2^-60 (the pass-1 range check).
+#ifndef DSMC_TC_POLY
+#define DSMC_TC_POLY 1
+#endif
+constexpr bool kTcPolyExp = DSMC_TC_POLY != 0;
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fminf(fmaxf(x.x, -125.f), 127.f);
+  x.y = fminf(fmaxf(x.y, -125.f), 127.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 f = __fadd2_rn(x, magic);
+  const float2 nr = __fadd2_rn(f, make_float2(-12582912.f, -12582912.f));
+  const float2 r = __fadd2_rn(x, make_float2(-nr.x, -nr.y));
+  const int nx = __float_as_int(f.x) - 0x4B400000, ny = __float_as_int(f.y) - 0x4B400000;
+  // Taylor coefficients (ln 2)^k / k!
+  float2 p = make_float2(1.5403530393381606e-4f, 1.5403530393381606e-4f);
+  p = __ffma2_rn(p, r, make_float2(1.3333558146428443e-3f, 1.3333558146428443e-3f));
+  p = __ffma2_rn(p, r, make_float2(9.6181291076284772e-3f, 9.6181291076284772e-3f));
+  p = __ffma2_rn(p, r, make_float2(5.5504108664821580e-2f, 5.5504108664821580e-2f));
+  p = __ffma2_rn(p, r, make_float2(2.4022650695910071e-1f, 2.4022650695910071e-1f));
+  p = __ffma2_rn(p, r, make_float2(6.9314718055994531e-1f, 6.9314718055994531e-1f));
+  p = __ffma2_rn(p, r, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (nx << 23)),
+                     __int_as_float(__float_as_int(p.y) + (ny << 23)));
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -397,8 +426,12 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, 
 #pragma unroll
         for (int c = 0; c < 32; c += 8) {
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            a4[e] = __fadd2_rn(a4[e], make_float2(ex2(v[c + 2 * e]), ex2(v[c + 2 * e + 1])));
+          for (int e = 0; e < 4; ++e) {
+            const float2 x = make_float2(v[c + 2 * e], v[c + 2 * e + 1]);
+            // one pair in four on the FMA pipe (idle here): MUFU.EX2 is the roof
+            const float2 ev = (kTcPolyExp && e == 3) ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+            a4[e] = __fadd2_rn(a4[e], ev);
+          }
         }
         const float2 s01 = __fadd2_rn(a4[0], a4[1]), s23 = __fadd2_rn(a4[2], a4[3]);
         const float2 s4 = __fadd2_rn(s01, s23);
