@@ -356,6 +356,9 @@ def run_ours(args, cfg, rank, world, device):
         roof = {"bound": "sfu", "kernel": "c32_pair", "achieved": ach, "peak": peak,
                 "unit": "pair-evals/s (1 MUFU.EX2 each)", "frac": ach / peak if ach else None,
                 "peak_source": peak_src, "traffic": None,
+                "bound_note": "the dominant kernel is bound by the special-function unit "
+                              "(MUFU.EX2, one exp per pair), neither HBM nor tensor cores; "
+                              "peak = measured ex2/s (DESIGN.md 5.3 for the mix ceilings)",
                 "work": f"{pairs_local:.4g} pair evaluations per step on rank 0 "
                         f"({Kloc - 1} combines x N^2)",
                 "pair_kernel_ms_per_step": pair_ms,
@@ -377,7 +380,13 @@ def run_ours(args, cfg, rank, world, device):
                                    "GBps": gath_b / (timings[2] * 1e-3) / 1e9}}
         prof = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(prof):
-            roof["traffic"] = json.load(open(prof)).get(args.config)
+            # traffic = DRAM bytes (read + write) per launch of the dominant
+            # kernel from one ncu --set full capture; the capture's context
+            # (which launch, algorithmic units per launch) in traffic_detail
+            det = json.load(open(prof)).get(args.config)
+            if det:
+                roof["traffic"] = det.get("bytes_per_launch")
+                roof["traffic_detail"] = det
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
