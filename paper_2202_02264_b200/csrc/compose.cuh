@@ -103,10 +103,11 @@ template <int D>
 __global__ void __launch_bounds__(256) gather32_kernel(Bufs b, const uint32_t* M1,
                                                        int root1, double* paths,
                                                        double* mean, double* cov,
-                                                       const uint32_t* root_map) {
-  const int t = blockIdx.x * 8 + (threadIdx.x >> 5), ch = blockIdx.y;
+                                                       const uint32_t* root_map,
+                                                       int t_begin = 0, int t_end = 1 << 30) {
+  const int t = t_begin + blockIdx.x * 8 + (threadIdx.x >> 5), ch = blockIdx.y;
   const int lane = threadIdx.x & 31;
-  if (t >= b.K) return;
+  if (t >= b.K || t >= t_end) return;
   const int N = b.N;
   const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + t];
   constexpr int NT = D * (D + 1) / 2;

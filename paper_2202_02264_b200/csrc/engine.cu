@@ -82,6 +82,9 @@ struct dsmc_ctx {
   // the tcgen05 kernel c32_pair_tc (DSMC_PAIR_KERNEL=tc)
   bool pair_tc = false;
   int num_sms = 148;
+  cudaStream_t copy_stream = nullptr;  // device->host copies overlapping the gather
+  static constexpr int kGatherChunks = 8;
+  cudaEvent_t gather_ev[kGatherChunks] = {};
   // last resident run
   int last_K = 0, last_d = 0, last_B = 0;
   double* d_mean = nullptr;
@@ -366,6 +369,11 @@ struct RunOpts {
   double* cov = nullptr;
   double* star_out = nullptr;   // device [B][K][d]
   uint8_t* changed = nullptr;   // device [B][K]
+  // optional host destinations of mean / cov (B = 1, FP32): the final gather
+  // then runs in time chunks and each chunk's moments are copied back on
+  // the copy stream while the next chunk is gathered
+  double* host_mean = nullptr;
+  double* host_cov = nullptr;
   bool timing = false;
   // time-sharded windows (FP32): leaves [t0, t0 + len) of the model, global
   // stream keys; composition optional, from a given root map
@@ -850,14 +858,34 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     } else {
       const uint32_t* M1 = Mb[mcur];
       const int r1 = root ? 1 : 0;
-      switch (d) {
-        case 1: gather32_kernel<1><<<dim3((K + 7) / 8, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
-        case 2: gather32_kernel<2><<<dim3((K + 7) / 8, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
-        case 3: gather32_kernel<3><<<dim3((K + 7) / 8, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
-        default: gather32_kernel<4><<<dim3((K + 7) / 8, B), 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map); break;
+      const bool overlap = (o.host_mean || o.host_cov) && B == 1 && ctx->copy_stream;
+      const int nch = overlap ? dsmc_ctx::kGatherChunks : 1;
+      for (int c = 0; c < nch; ++c) {
+        const int ta = (int)((long)K * c / nch), tb = (int)((long)K * (c + 1) / nch);
+        if (tb <= ta) continue;
+        const dim3 grid((tb - ta + 7) / 8, B);
+        switch (d) {
+          case 1: gather32_kernel<1><<<grid, 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map, ta, tb); break;
+          case 2: gather32_kernel<2><<<grid, 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map, ta, tb); break;
+          case 3: gather32_kernel<3><<<grid, 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map, ta, tb); break;
+          default: gather32_kernel<4><<<grid, 256, 0, ctx->stream>>>(b, M1, r1, o.paths, o.mean, o.cov, o.root_map, ta, tb); break;
+        }
+        LAUNCHED(ctx);
+        if (overlap) {
+          CU(cudaEventRecord(ctx->gather_ev[c], ctx->stream));
+          CU(cudaStreamWaitEvent(ctx->copy_stream, ctx->gather_ev[c], 0));
+          const size_t n = (size_t)(tb - ta);
+          if (o.host_mean && o.mean)
+            CU(cudaMemcpyAsync(o.host_mean + (size_t)ta * d, o.mean + (size_t)ta * d,
+                               n * d * sizeof(double), cudaMemcpyDeviceToHost, ctx->copy_stream));
+          if (o.host_cov && o.cov)
+            CU(cudaMemcpyAsync(o.host_cov + (size_t)ta * d * d, o.cov + (size_t)ta * d * d,
+                               n * d * d * sizeof(double), cudaMemcpyDeviceToHost,
+                               ctx->copy_stream));
+        }
       }
     }
-    LAUNCHED(ctx);
+    if (fp64) LAUNCHED(ctx);
   }
   CU(cudaGetLastError());
   if (o.timing) CU(rec_event(ctx->ev[3], ctx->stream));
@@ -897,6 +925,8 @@ int dsmc_create(int device, dsmc_ctx** out) {
     return DSMC_E_NO_DEVICE;
   }
   for (auto& e : ctx->ev) cudaEventCreate(&e);
+  cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+  for (auto& e : ctx->gather_ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   cudaMallocHost(&ctx->h_lnc, sizeof(double) * 4096);
   // model uploads use the stream-ordered pool (cudaMallocAsync); keep freed
   // blocks mapped so repeated uploads (e2e calls, pGibbs sweeps) reuse them
@@ -923,6 +953,9 @@ void dsmc_destroy(dsmc_ctx* ctx) {
   for (auto& e : ctx->kev) cudaEventDestroy(e);
   delete static_cast<WindowState*>(ctx->window);
   cudaStreamDestroy(ctx->stream);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  for (auto& e : ctx->gather_ev)
+    if (e) cudaEventDestroy(e);
   delete ctx;
 }
 
@@ -951,7 +984,7 @@ __global__ void set_seed_kernel(uint64_t* dst, uint64_t v) { *dst = v; }
 
 static int smooth_common(dsmc_ctx* ctx, dsmc_model_handle* h, const dsmc_smooth_opts* opts,
                          double* d_paths, double* d_mean, double* d_cov, RunResult* res,
-                         bool timing) {
+                         bool timing, double* host_mean = nullptr, double* host_cov = nullptr) {
   if (!opts) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "options are null");
   RunOpts o;
   o.precision = opts->precision;
@@ -963,6 +996,8 @@ static int smooth_common(dsmc_ctx* ctx, dsmc_model_handle* h, const dsmc_smooth_
   o.paths = d_paths;
   o.mean = d_mean;
   o.cov = d_cov;
+  o.host_mean = host_mean;
+  o.host_cov = host_cov;
   o.timing = timing;
   ctx->time_kernels = timing;
   ctx->kev_used = 0;
@@ -1004,14 +1039,34 @@ int dsmc_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
     dc = (double*)p;
   }
   RunResult res;
-  rc = smooth_common(ctx, h, opts, dp, dm, dc, &res, false);
-  if (rc) return rc;
+  // FP32 with pinned outputs: the moments come back in chunks overlapping the
+  // final gather (a copy to pageable memory would block the host per chunk)
+  auto pinned = [](const void* ptr) {
+    if (!ptr) return true;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+  };
+  const bool overlap = opts && opts->precision == DSMC_FP32 && (dm || dc) &&
+                       pinned(out->mean) && pinned(out->cov);
+  rc = smooth_common(ctx, h, opts, dp, dm, dc, &res, false, overlap ? out->mean : nullptr,
+                     overlap ? out->cov : nullptr);
+  if (rc) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    return rc;
+  }
   rc = check_device_error(ctx, res, K);
-  if (rc) return rc;
+  if (rc) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    return rc;
+  }
   auto s = ctx->stream;
   if (dp) CU(cudaMemcpyAsync(out->paths, dp, (size_t)K * N * d * sizeof(double), cudaMemcpyDeviceToHost, s));
-  if (dm) CU(cudaMemcpyAsync(out->mean, dm, (size_t)K * d * sizeof(double), cudaMemcpyDeviceToHost, s));
-  if (dc) CU(cudaMemcpyAsync(out->cov, dc, (size_t)K * d * d * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (dm && !overlap) CU(cudaMemcpyAsync(out->mean, dm, (size_t)K * d * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (dc && !overlap) CU(cudaMemcpyAsync(out->cov, dc, (size_t)K * d * d * sizeof(double), cudaMemcpyDeviceToHost, s));
   if (out->pair_left && T > 0) {
     CU(cudaMemcpyAsync(out->pair_left, res.PL, (size_t)T * N * 4, cudaMemcpyDeviceToHost, s));
     CU(cudaMemcpyAsync(out->pair_right, res.PR, (size_t)T * N * 4, cudaMemcpyDeviceToHost, s));
@@ -1025,6 +1080,7 @@ int dsmc_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
   CU(cudaMemcpyAsync(&lnc, res.root_lnc, sizeof(double), cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(&evals, res.evals, sizeof evals, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
+  if (overlap) CU(cudaStreamSynchronize(ctx->copy_stream));
   const bool lazy = opts->resampler == DSMC_MH_LAZY || opts->resampler == DSMC_REJECTION_LAZY;
   out->log_norm_const = lnc;
   out->has_log_norm_const = !std::isnan(lnc);
