@@ -64,6 +64,17 @@ struct dsmc_model_handle {
   int* bounded = nullptr;          // [B]
   std::vector<void*> owned;
   cudaStream_t stream = nullptr;  // owned memory is stream-ordered
+  // deferred upload (dsmc_smooth with pinned host arrays): the per-time
+  // arrays are copied in time chunks on the copy stream, each chunk's prep +
+  // leaves starting as soon as it lands (run_tree); until then tc is unset
+  bool defer = false;
+  bool prep_pending = false;
+  struct Deferred {
+    void* dst;
+    const void* src;
+    size_t bytes_per_t;
+  };
+  std::vector<Deferred> deferred;
 };
 
 struct dsmc_ctx {
@@ -212,9 +223,10 @@ int validate_desc(dsmc_ctx* ctx, const dsmc_model_desc* m) {
   return DSMC_OK;
 }
 
+// per_t > 0: a per-time array of n = K * per_t elements (deferrable)
 template <class T>
 int upload(dsmc_ctx* ctx, dsmc_model_handle* h, const T* src, size_t n,
-           const T** dst) {
+           const T** dst, size_t per_t = 0) {
   if (!src || n == 0) {
     *dst = nullptr;
     return DSMC_OK;
@@ -222,14 +234,17 @@ int upload(dsmc_ctx* ctx, dsmc_model_handle* h, const T* src, size_t n,
   void* p = nullptr;
   CU(cudaMallocAsync(&p, n * sizeof(T), ctx->stream));
   h->owned.push_back(p);
-  CU(cudaMemcpyAsync(p, src, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  if (h->defer && per_t > 0)
+    h->deferred.push_back({p, src, per_t * sizeof(T)});
+  else
+    CU(cudaMemcpyAsync(p, src, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
   *dst = static_cast<const T*>(p);
   return DSMC_OK;
 }
 
 // Upload B descriptors (same K, d) and run the prep kernel.
 int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
-                dsmc_model_handle** out) {
+                dsmc_model_handle** out, bool defer = false) {
   for (int c = 0; c < B; ++c) {
     int rc = validate_desc(ctx, &descs[c]);
     if (rc) return rc;
@@ -241,6 +256,7 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
   h->id = ++g_handle_ids;
   h->B = B;
   h->stream = ctx->stream;
+  h->defer = defer && B == 1;
   h->desc = descs[0];
   const int K = descs[0].horizon + 1, d = descs[0].state_dim, dy = descs[0].obs_dim;
   h->K = K;
@@ -297,19 +313,19 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
                             -0.5 * (kLog2Pi + std::log(m.par[3])),
                             -0.5 * (kLog2Pi + std::log(m.par[4])), 0.0};
       for (int q = 0; q < 8; ++q) M.mp[q] = mp[q];
-      rc |= upload(ctx, h.get(), m.y, nT, &M.y);
-      rc |= upload(ctx, h.get(), m.prop_mean, nT, &M.prop_mean);
-      rc |= upload(ctx, h.get(), m.prop_cov, nT, &M.prop_cov);
+      rc |= upload(ctx, h.get(), m.y, nT, &M.y, 1);
+      rc |= upload(ctx, h.get(), m.prop_mean, nT, &M.prop_mean, 1);
+      rc |= upload(ctx, h.get(), m.prop_cov, nT, &M.prop_cov, 1);
     } else if (m.kind == DSMC_MODEL_SV) {
       rc |= upload(ctx, h.get(), m.y, nT, &M.y);
       M.has_obs = nullptr;
       M.prop_mean = M.prop_cov = M.F = M.b = M.Q = M.H = M.R = M.m0 = M.P0 = nullptr;
     } else {
       auto span = [&](int64_t stride, size_t per) { return stride ? nT * stride : per; };
-      rc |= upload(ctx, h.get(), m.y, nT * dy, &M.y);
+      rc |= upload(ctx, h.get(), m.y, nT * dy, &M.y, (size_t)dy);
       rc |= upload(ctx, h.get(), m.has_obs, m.has_obs ? nT : 0, &M.has_obs);
-      rc |= upload(ctx, h.get(), m.prop_mean, nT * d, &M.prop_mean);
-      rc |= upload(ctx, h.get(), m.prop_cov, nT * d * d, &M.prop_cov);
+      rc |= upload(ctx, h.get(), m.prop_mean, nT * d, &M.prop_mean, (size_t)d);
+      rc |= upload(ctx, h.get(), m.prop_cov, nT * d * d, &M.prop_cov, (size_t)d * d);
       rc |= upload(ctx, h.get(), m.m0, (size_t)d, &M.m0);
       rc |= upload(ctx, h.get(), m.P0, (size_t)d * d, &M.P0);
       rc |= upload(ctx, h.get(), m.H, span(m.H_stride, (size_t)dy * d), &M.H);
@@ -337,9 +353,14 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
   h->bounded = static_cast<int*>(p);
   std::vector<int> ones(B, 3);
   CU(cudaMemcpyAsync(p, ones.data(), sizeof(int) * B, cudaMemcpyHostToDevice, ctx->stream));
-  prep_kernel<<<dim3((K + 127) / 128, B), 128, 0, ctx->stream>>>(h->models_dev, h->tc, K,
-                                                                 h->bounded);
-  LAUNCHED(ctx);
+  if (h->deferred.empty()) {
+    h->defer = false;
+    prep_kernel<<<dim3((K + 127) / 128, B), 128, 0, ctx->stream>>>(h->models_dev, h->tc, K,
+                                                                   h->bounded);
+    LAUNCHED(ctx);
+  } else {
+    h->prep_pending = true;  // run_tree copies, preps and draws leaves chunk by chunk
+  }
   CU(cudaGetLastError());
   *out = h.release();
   return DSMC_OK;
@@ -568,6 +589,23 @@ struct WindowState {
 };
 WindowState& window_state(dsmc_ctx* ctx);
 
+// A deferred upload not consumed chunk by chunk: copy everything and prep.
+static cudaError_t flush_deferred(dsmc_ctx* ctx, dsmc_model_handle* h) {
+  if (!h->prep_pending) return cudaSuccess;
+  const size_t K = (size_t)h->K;
+  for (const auto& df : h->deferred) {
+    cudaError_t e = cudaMemcpyAsync(df.dst, df.src, K * df.bytes_per_t, cudaMemcpyHostToDevice,
+                                    ctx->stream);
+    if (e != cudaSuccess) return e;
+  }
+  prep_kernel<<<dim3((h->K + 127) / 128, h->B), 128, 0, ctx->stream>>>(h->models_dev, h->tc, h->K,
+                                                                       h->bounded);
+  ++ctx->launches;
+  h->prep_pending = false;
+  h->deferred.clear();
+  return cudaGetLastError();
+}
+
 int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* res) {
   const int B = h->B, K = o.len > 0 ? o.len : h->K, T = K - 1, d = h->d;
   if (o.t0 < 0 || o.t0 + K > h->K)
@@ -663,21 +701,51 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
       CU(cudaMemcpyAsync(p, o.inj_lw, BKN * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
       dinj_lw = (const double*)p;
     }
+    CU(flush_deferred(ctx, h));
     leaf64_kernel<<<dim3(K, (N + 127) / 128, B), 128, 0, ctx->stream>>>(b, dinj_x, dinj_lw);
     LAUNCHED(ctx);
     leafnorm64_kernel<<<dim3(K, B), 32, 0, ctx->stream>>>(b);
     LAUNCHED(ctx);
   } else {
     CU(A.get("RAW0", (size_t)B * N * sizeof(double), &p));
-    const dim3 lg(K, B);
     const int lt = std::min(256, (N + 31) / 32 * 32);
-    switch (d) {
-      case 1: leaf32_kernel<1><<<lg, lt, 0, ctx->stream>>>(b, (double*)p); break;
-      case 2: leaf32_kernel<2><<<lg, lt, 0, ctx->stream>>>(b, (double*)p); break;
-      case 3: leaf32_kernel<3><<<lg, lt, 0, ctx->stream>>>(b, (double*)p); break;
-      default: leaf32_kernel<4><<<lg, lt, 0, ctx->stream>>>(b, (double*)p); break;
+    auto leaves = [&](int ta, int tb) {
+      const dim3 lg(tb - ta, B);
+      switch (d) {
+        case 1: leaf32_kernel<1><<<lg, lt, 0, ctx->stream>>>(b, (double*)p, ta); break;
+        case 2: leaf32_kernel<2><<<lg, lt, 0, ctx->stream>>>(b, (double*)p, ta); break;
+        case 3: leaf32_kernel<3><<<lg, lt, 0, ctx->stream>>>(b, (double*)p, ta); break;
+        default: leaf32_kernel<4><<<lg, lt, 0, ctx->stream>>>(b, (double*)p, ta); break;
+      }
+      LAUNCHED(ctx);
+    };
+    if (h->prep_pending && o.t0 == 0 && K == h->K) {
+      // deferred upload: per time chunk, H2D on the copy stream, then that
+      // chunk's prep and leaves on the compute stream
+      CU(cudaEventRecord(ctx->gather_ev[0], ctx->stream));  // allocations done
+      CU(cudaStreamWaitEvent(ctx->copy_stream, ctx->gather_ev[0], 0));
+      const int nch = dsmc_ctx::kGatherChunks;
+      for (int c = 0; c < nch; ++c) {
+        const int ta = (int)((long)K * c / nch), tb = (int)((long)K * (c + 1) / nch);
+        if (tb <= ta) continue;
+        for (const auto& df : h->deferred)
+          CU(cudaMemcpyAsync(static_cast<char*>(df.dst) + (size_t)ta * df.bytes_per_t,
+                             static_cast<const char*>(df.src) + (size_t)ta * df.bytes_per_t,
+                             (size_t)(tb - ta) * df.bytes_per_t, cudaMemcpyHostToDevice,
+                             ctx->copy_stream));
+        CU(cudaEventRecord(ctx->gather_ev[c], ctx->copy_stream));
+        CU(cudaStreamWaitEvent(ctx->stream, ctx->gather_ev[c], 0));
+        prep_kernel<<<dim3((tb - ta + 127) / 128, B), 128, 0, ctx->stream>>>(
+            h->models_dev, h->tc, h->K, h->bounded, ta, tb);
+        LAUNCHED(ctx);
+        leaves(ta, tb);
+      }
+      h->prep_pending = false;
+      h->deferred.clear();
+    } else {
+      CU(flush_deferred(ctx, h));
+      leaves(0, K);
     }
-    LAUNCHED(ctx);
     if (o.t0 == 0) {  // only global leaf 0 carries non-uniform weights
       leafnorm32_kernel<<<B, 32, 0, ctx->stream>>>(b, (const double*)p);
       LAUNCHED(ctx);
@@ -1013,13 +1081,33 @@ static int smooth_common(dsmc_ctx* ctx, dsmc_model_handle* h, const dsmc_smooth_
   return run_tree(ctx, h, o, res);
 }
 
+// page-locked (or absent) host memory: async copies really overlap
+static bool host_pinned(const void* ptr) {
+  if (!ptr) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 int dsmc_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
                 const dsmc_smooth_opts* opts, dsmc_smooth_out* out) {
   if (!ctx || !out) return DSMC_E_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   const auto t0 = std::chrono::steady_clock::now();
   dsmc_model_handle* h = nullptr;
-  int rc = make_handle(ctx, model, 1, &h);
+  // FP32 with pinned per-time arrays: upload them in time chunks that
+  // overlap the first chunks' prep and leaves (run_tree)
+  // (only for large horizons: below ~32 MB the chunking costs more than the copy)
+  const size_t big = model ? (size_t)(model->horizon + 1) * model->state_dim *
+                                 (model->state_dim + 1) * sizeof(double)
+                           : 0;
+  const bool defer = opts && opts->precision == DSMC_FP32 && model && big >= (32u << 20) &&
+                     host_pinned(model->y) && host_pinned(model->prop_mean) &&
+                     host_pinned(model->prop_cov);
+  int rc = make_handle(ctx, model, 1, &h, defer);
   if (rc) return rc;
   std::unique_ptr<dsmc_model_handle, void (*)(dsmc_model_handle*)> hold(h, free_handle);
   const int K = h->K, d = h->d, T = K - 1;
@@ -1041,17 +1129,9 @@ int dsmc_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
   RunResult res;
   // FP32 with pinned outputs: the moments come back in chunks overlapping the
   // final gather (a copy to pageable memory would block the host per chunk)
-  auto pinned = [](const void* ptr) {
-    if (!ptr) return true;
-    cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    return a.type == cudaMemoryTypeHost;
-  };
   const bool overlap = opts && opts->precision == DSMC_FP32 && (dm || dc) &&
-                       pinned(out->mean) && pinned(out->cov);
+                       (size_t)K * d * (d + 1) * sizeof(double) >= (32u << 20) &&
+                       host_pinned(out->mean) && host_pinned(out->cov);
   rc = smooth_common(ctx, h, opts, dp, dm, dc, &res, false, overlap ? out->mean : nullptr,
                      overlap ? out->cov : nullptr);
   if (rc) {

@@ -93,10 +93,10 @@ __device__ inline const double* at(const double* p, int64_t s, int t) {
 // ------------------------------------------------------------------ prep
 // Per-time constants (TimeConst) of chain `ch`, one thread per time.
 __global__ void prep_kernel(const DevModel* models, TimeConst* tc_all, int K,
-                            int* bounded_all) {
+                            int* bounded_all, int t_begin = 0, int t_end = 1 << 30) {
   const int ch = blockIdx.y;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= K) return;
+  const int t = t_begin + blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= K || t >= t_end) return;
   const DevModel M = models[ch];
   TimeConst tc;
   for (int i = 0; i < 4; ++i) tc.pm[i] = tc.delta[i] = tc.e[i] = 0.0;
