@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, 
   __shared__ uint32_t s_tmem;
   __shared__ float s_cm[kTcBufs][2];  // per buffer: the two producer warps' column maxima
   __shared__ float s_cmax[kTcBufs];   // per buffer: cmax of the staged sub-block
+  __shared__ CutConst32 s_cc;          // the cut's constants (loaded once per CTA)
   const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
   const int N = b.N;
   const int nsub = (N + kSub - 1) / kSub;
@@ -214,6 +215,21 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, 
 
   if (tid >= kTcConsumers + kTcProducers) {
     // ----------------------------------------------------------- issuer
+    {  // the cut constants for everyone, one entry per lane (load_cut32's
+       // fields; published by barrier 1)
+      if (lane < D * D) {
+        s_cc.W[lane] = (float)(tc.tW[lane]) * kS;
+        s_cc.F[lane] = (float)tc.F[lane];
+      } else if (lane >= 16 && lane < 16 + D) {
+        s_cc.delta[lane - 16] = (float)tc.delta[lane - 16];
+      } else if (lane == 24) {
+        s_cc.drift = tc.drift;
+      } else if (lane >= 25 && lane < 29) {
+        s_cc.th[lane - 25] = (float)tc.th[lane - 25];
+      } else if (lane == 29) {
+        s_cc.th[4] = (float)tc.pm[0];
+      }
+    }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();  // (1)
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -254,8 +270,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, 
     // -------------------------------------------------------- producers
     const int p = tid - kTcConsumers;
     const int pw = p >> 5;  // producer warp 0 / 1
-    CutConst32 cc;
-    load_cut32<D>(tc, cc);
+    const CutConst32& cc = s_cc;  // valid after barrier (1)
     const float4* XR = b.X32 + ((size_t)ch * b.K + Rsd.t) * N;
     const float* CR = b.COL + ((size_t)ch * b.K + Rsd.t) * N;
     // gathers: block-map index two sub-blocks ahead, state one ahead
@@ -345,15 +360,18 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, 
     const int i = row0 + tid;
     const bool row_ok = i < N;
     float Brow = -CUDART_INF_F, crow = 0.f;
+    float4 xl = make_float4(0.f, 0.f, 0.f, 0.f);
+    float lwr = 0.f;
+    if (row_ok) {  // row gathers in flight across barrier (1)
+      xl = b.X32[((size_t)ch * b.K + Lsd.t) * N + map_last(b, la, ch, Lsd, i)];
+      if (Lsd.leaf && !b.UNI[(size_t)ch * b.K + Lsd.t]) lwr = b.LW32[(size_t)ch * N + i];
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();  // (1) barriers, TMEM and the cut constants are ready
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = s_tmem;
     {
-      float4 xl = make_float4(0.f, 0.f, 0.f, 0.f);
-      float lwr = 0.f;
-      if (row_ok) {
-        xl = b.X32[((size_t)ch * b.K + Lsd.t) * N + map_last(b, la, ch, Lsd, i)];
-        if (Lsd.leaf && !b.UNI[(size_t)ch * b.K + Lsd.t]) lwr = b.LW32[(size_t)ch * N + i];
-      }
-      CutConst32 cc;
-      load_cut32<D>(tc, cc);
+      const CutConst32& cc = s_cc;
       float u[4] = {0.f, 0.f, 0.f, 0.f};
       float vals[16];
 #pragma unroll
@@ -392,10 +410,6 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, 
       tc_store_row<D>(sA, tid, vals);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();  // (1)
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t tmem = s_tmem;
     __syncthreads();  // (2) rows staged
     const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
     for (int q = 0; q < nq; ++q) {
