@@ -378,6 +378,17 @@ def run_ours(args, cfg, rank, world, device):
                            "GBps": leaf_b / (timings[0] * 1e-3) / 1e9},
                 "compose_gather": {"bytes": gath_b, "ms": timings[2],
                                    "GBps": gath_b / (timings[2] * 1e-3) / 1e9}}
+        # the sampler (pass 2): its MUFU work is the row log-sum-exp over the
+        # sub-block sums (N * N/64 per combine) plus the recompute of <= 64
+        # weights per slot (N * 64); it is latency-bound, far below that roof
+        sample_ms = timings[4] if len(timings) > 4 else None
+        if sample_ms and world == 1 and cfg["resampler"] in (0, 1):
+            nsub = (N + 63) // 64
+            ex = (K - 1) * (N * nsub + N * 64)
+            roof["sfu_kernels"] = {
+                "c32_sample": {"exps": ex, "ms": sample_ms,
+                               "exps_per_s": ex / (sample_ms * 1e-3),
+                               "frac": ex / (sample_ms * 1e-3) / peak}}
         prof = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(prof):
             # traffic = DRAM bytes (read + write) per launch of the dominant
