@@ -792,7 +792,7 @@ __global__ void lazy32_kernel(Bufs b, LevelArgs la, int mh, size_t mh_steps) {
       bool have = false;
       for (size_t st = 0; st < mh_steps; ++st) {
         const uint32_t pi = (uint32_t)s.index(N), pj = (uint32_t)s.index(N);
-        const float lu = (float)(log2(s.uniform_pos()));
+        const float lu = lg2((float)s.uniform_pos());  // FP32 path: MUFU, not FP64 log2
         if (!have) {
           cur = probe(i, j);
           ++evals;
@@ -822,7 +822,7 @@ __global__ void lazy32_kernel(Bufs b, LevelArgs la, int mh, size_t mh_steps) {
           err = DSMC_E_INVALID_ARGUMENT; why = isnan(lw) ? kReasonNaN : kReasonOverBound;
           break;
         }
-        if ((float)log2(s.uniform_pos()) <= lw - bound2) {
+        if (lg2((float)s.uniform_pos()) <= lw - bound2) {
           oi = i;
           oj = j;
           ok = true;
