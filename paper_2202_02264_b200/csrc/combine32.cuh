@@ -589,6 +589,9 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
     while (i > 0 && !(Lrow[i] > -CUDART_INF_F)) --i;
     const float Li = Lrow[i];
     const float Brow = ax.B[i];
+    // phase C reads this row's u_i: pull it into L1 now so the prefetch
+    // there (one slot ahead) does not wait on L2
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(ax.u + i));
     const float local0 = (float)((pt - before) / (double)ex2(Li - G));
     const float local = local0 >= 0.f ? local0 : 0.f;
     // sub-block walk over the row's sub-block sums (relative to the row
@@ -621,8 +624,9 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
     }
     float frac = wsel > 0.f ? (local - before_s) / wsel : 0.f;
     frac = fminf(fmaxf(frac, 0.f), 1.f);
-    // (i | s << 16, first map of the left block at i, frac, shift); N < 2^16
-    REC[x] = make_int4(i | (s << 16), (int)map_first(b, la, ch, L, (uint32_t)i),
+    // (i | s << 16, -, frac, shift); N < 2^16. The left block's first map at
+    // i is read in phase C, where its latency hides under the recompute.
+    REC[x] = make_int4(i | (s << 16), 0,
                        __float_as_int(frac), __float_as_int(Brow - Ls_sel));
     atomicAdd(&CB[s], 1);
   }
@@ -671,6 +675,7 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
       u_n = ax.u[rc_n.x & 0xffff];
     }
     const int i = rc.x & 0xffff, s = rc.x >> 16;
+    const uint32_t first_i = map_first(b, la, ch, L, (uint32_t)i);  // used at the end
     const float frac = __int_as_float(rc.z);
     const float sh = __int_as_float(rc.w);
     const float2 nsh = make_float2(sh, sh);
@@ -716,7 +721,7 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
     const int m = m0 + x;
     PL[m + off] = (uint32_t)i;
     PR[m + off] = (uint32_t)j;
-    la.first_next[nbase + m + off] = (uint32_t)rc.y;
+    la.first_next[nbase + m + off] = first_i;
     if (pend) *pend_dst = pend_src;
     pend_src = map_last(b, la, ch, R, (uint32_t)j);
     pend_dst = la.last_next + nbase + m + off;
