@@ -482,6 +482,9 @@ def main():
             torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             torch.distributed.init_process_group(backend)
+        # one all-rank collective before any P2P: the protocol's first
+        # batch_isend_irecv then never initialises a communicator on a subset
+        torch.distributed.barrier()
     out = run_ours(args, cfg, rank, world, local)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline and cfg["model"] != "sv_pgibbs":
