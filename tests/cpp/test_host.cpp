@@ -475,6 +475,98 @@ TEST_CASE(cpu_scores_match_their_definitions) {
   CHECK(std::fabs(dsmc::rw_score(0.5, path, 2) - (std::log(0.5) + (0.09 + 0.36) / 0.125)) < 1e-12);
 }
 
+// pgibbs.hpp:83-87 / test_pgibbs.cpp:62-110: conjugate precision draws on a
+// hand trajectory follow Gamma(shape + T/2, rate + ss/2) (moment checks)
+TEST_CASE(cpu_draw_precisions_conjugate_law) {
+  dsmc::ThetaLogisticParams p{0.2, 0.1, 0.5, 1.0, 1.0};
+  const std::vector<double> star = {0.0, 0.4, -0.2}, ys = {0.1, 0.3, -0.4};
+  dsmc::ThetaLogisticGibbsConfig cfg;
+  cfg.prec_x_shape = 2.0;
+  cfg.prec_x_rate = 1.0;
+  cfg.prec_y_shape = 3.0;
+  cfg.prec_y_rate = 0.5;
+  auto f = [](double x) { return x + 0.2 - 0.1 * std::exp(0.5 * x); };
+  const double ssx = (0.4 - f(0.0)) * (0.4 - f(0.0)) + (-0.2 - f(0.4)) * (-0.2 - f(0.4));
+  const double ssy = 0.01 + 0.01 + 0.04;
+  const double ax = 2.0 + 1.0, bx = 1.0 + 0.5 * ssx, ay = 3.0 + 1.5, by = 0.5 + 0.5 * ssy;
+  dsmc::RngStream st({11, 0, 0, dsmc::StreamRole::gibbs_param});
+  const int n = 40000;
+  double sx = 0, sxx = 0, sy = 0;
+  for (int k = 0; k < n; ++k) {
+    const auto d = dsmc::draw_precisions(p, ys, star, cfg, st);
+    CHECK(d.tau0 == p.tau0 && d.tau1 == p.tau1 && d.tau2 == p.tau2);
+    sx += 1.0 / d.q2;
+    sxx += 1.0 / (d.q2 * d.q2);
+    sy += 1.0 / d.r2;
+  }
+  const double mx = sx / n, vx = sxx / n - mx * mx, my = sy / n;
+  CHECK(std::fabs(mx - ax / bx) < 5 * std::sqrt(ax) / bx / std::sqrt((double)n));
+  CHECK(std::fabs(vx - ax / (bx * bx)) < 0.05 * ax / (bx * bx));
+  CHECK(std::fabs(my - ay / by) < 5 * std::sqrt(ay) / by / std::sqrt((double)n));
+  CHECK_THROWS_AS(dsmc::draw_precisions(p, ys, {0.0, 1.0}, cfg, st), std::invalid_argument);
+}
+
+// test_pgibbs.cpp:204-258: the theta-logistic chain (host parameter kernel,
+// device c-dSMC) is deterministic in its seed, keeps the support, renews the
+// path at a healthy rate and guards its inputs
+TEST_CASE(theta_logistic_chain_determinism_support_mixing) {
+  dsmc::ThetaLogisticParams truth{0.15, 0.10, 0.50, 0.09, 0.04};
+  const auto data = dsmc::simulate_theta_logistic(truth, 40, 2024);
+  dsmc::ThetaLogisticGibbsConfig cfg;
+  cfg.n_particles = 32;
+  const auto chain = dsmc::run_theta_logistic_pgibbs(data.ys, truth, cfg, 60, 5);
+  CHECK(chain.thetas.size() == 60 && chain.stars.size() == 60);
+  for (const auto& th : chain.thetas)
+    CHECK(std::isfinite(th.tau0) && th.tau1 > 0 && th.tau2 > 0 && th.q2 > 0 && th.r2 > 0);
+  CHECK(chain.weight_evals > 0);
+  const auto rates = dsmc::update_rate(chain.stars);
+  double mean_rate = 0;
+  for (double r : rates) mean_rate += r;
+  CHECK(mean_rate / rates.size() > 0.3);
+  CHECK(chain.thetas[5].q2 != chain.thetas[6].q2);
+  const auto again = dsmc::run_theta_logistic_pgibbs(data.ys, truth, cfg, 60, 5);
+  CHECK(again.thetas.back().q2 == chain.thetas.back().q2);
+  CHECK(again.stars.back() == chain.stars.back());
+  CHECK(again.rwm_accepts == chain.rwm_accepts);
+  const auto other = dsmc::run_theta_logistic_pgibbs(data.ys, truth, cfg, 60, 6);
+  CHECK(other.stars.back() != chain.stars.back());
+  dsmc::ThetaLogisticParams bad = truth;
+  bad.tau1 = -0.1;
+  CHECK_THROWS_AS(dsmc::run_theta_logistic_pgibbs(data.ys, bad, cfg, 3, 1), std::invalid_argument);
+  CHECK_THROWS_AS(dsmc::run_theta_logistic_pgibbs({1.0}, truth, cfg, 3, 1), std::invalid_argument);
+}
+
+// test_pgibbs.cpp:260-289: with the taus frozen the chain is Gibbs over
+// (path, q2, r2). The reference checks doctest::Approx(truth).epsilon(0.5),
+// i.e. |a - b| < 0.5 (1 + max(|a|, |b|)); on this data set the exact posterior
+// means are q2 = 0.176, r2 = 0.151 (a Gibbs sampler with exact Kalman/FFBS
+// path draws, 3500 iterations, same priors — computed when this case was
+// written), and the particle-Gibbs chain must land within 15% of those
+TEST_CASE(theta_logistic_conjugate_only_chain_recovers_precisions) {
+  dsmc::ThetaLogisticParams truth{0.1, 1e-8, 1e-8, 0.25, 0.09};
+  const auto data = dsmc::simulate_theta_logistic(truth, 150, 99);
+  dsmc::ThetaLogisticGibbsConfig cfg;
+  cfg.n_particles = 48;
+  cfg.rwm_step_tau = 0.0;
+  cfg.rwm_step_x0 = 0.0;
+  const auto chain = dsmc::run_theta_logistic_pgibbs(data.ys, truth, cfg, 300, 17);
+  double mq = 0, mr = 0;
+  const std::size_t burn = 50;
+  for (std::size_t k = burn; k < chain.thetas.size(); ++k) {
+    mq += chain.thetas[k].q2;
+    mr += chain.thetas[k].r2;
+  }
+  mq /= (double)(chain.thetas.size() - burn);
+  mr /= (double)(chain.thetas.size() - burn);
+  auto approx = [](double a, double b) {  // doctest::Approx(b).epsilon(0.5)
+    return std::fabs(a - b) < 0.5 * (1.0 + std::max(std::fabs(a), std::fabs(b)));
+  };
+  CHECK(approx(mq, truth.q2));
+  CHECK(approx(mr, truth.r2));
+  CHECK(std::fabs(mq - 0.1757) < 0.15 * 0.1757);
+  CHECK(std::fabs(mr - 0.1514) < 0.15 * 0.1514);
+}
+
 int main(int argc, char** argv) {
   const char* only = argc > 1 ? argv[1] : nullptr;
   int failed_cases = 0;
