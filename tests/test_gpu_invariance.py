@@ -6,7 +6,8 @@
   lag-1 covariance against the Kalman/RTS answer, over thousands of chains
   run as one batched sweep;
 * the normalising-constant estimate is unbiased (test_smoother.cpp:416-456):
-  mean exp(log Z - exact) = 1 at N = 8.
+  mean exp(log Z - exact) = 1 at N = 8, and so is the device particle
+  filter's evidence (test_baselines.cpp:26-60).
 
 The model is the reference's AR(1) fixture (tests/support/ar1.hpp) with
 stationary (not RTS) proposals, so the invariance is not an artefact of
@@ -111,3 +112,19 @@ def test_normalising_constant_is_unbiased_at_small_n(engine):
     assert abs(w.mean() - 1.0) < 4.0 * se, (w.mean(), se)
     # and log Z itself is biased low (Jensen), as an unbiased Z implies
     assert r.mean() < exact
+
+
+def test_particle_filter_evidence_is_unbiased(engine):
+    """test_baselines.cpp:26-60: the bootstrap-style filter's exp(log Z) is
+    unbiased (device PF of the FFBS comparator, FP32 arithmetic)."""
+    T, N, reps = 15, 16, 3000
+    ys = _data(T, 7)
+    m = models.ar1(ys, RHO, Q, R)
+    _, _, exact = kalman_smooth(m)
+    r = np.array([engine.ffbs(m, N, n_draws=1, seed=50_000 + s)["log_likelihood"]
+                  for s in range(reps)])
+    assert np.isfinite(r).all()
+    w = np.exp(r - exact)
+    se = w.std(ddof=1) / np.sqrt(reps)
+    # FP32 log-weights: allow the ~1e-6 relative float bias on top of 4 SE
+    assert abs(w.mean() - 1.0) < 4.0 * se + 1e-4, (w.mean(), se)
