@@ -49,6 +49,14 @@ for s in range(4):
     r = e.smooth(m, 1024, abi.MULTINOMIAL, seed=100 + s, precision=abi.FP32)
     z.append((r["mean"] - km) / np.sqrt(np.einsum("tii->ti", kP)))
 z = np.mean(z, 0)
+# ragged particle counts (partial 128-row tiles and 64-column sub-blocks)
+for N in (100, 300):
+    zs = []
+    for s in range(4):
+        r = e.smooth(m, N, abi.MULTINOMIAL, seed=200 + s, precision=abi.FP32)
+        assert np.isfinite(r["mean"]).all() and np.isfinite(r["log_norm_const"])
+        zs.append((r["mean"] - km) / np.sqrt(np.einsum("tii->ti", kP)))
+    assert float(np.sqrt(np.mean(np.mean(zs, 0) ** 2))) < 0.6, N
 print(float(np.sqrt(np.mean(z ** 2))))
 """
     env = dict(os.environ, DSMC_PAIR_KERNEL="tc", PYTHONPATH=ROOT)
