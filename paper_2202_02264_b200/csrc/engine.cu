@@ -6,6 +6,7 @@
 // moments. Every kernel goes on the context's stream; the host synchronises
 // once at the end to read the device error record (no per-level sync).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -129,7 +130,7 @@ struct dsmc_ctx {
   } gc;
 };
 
-static uint64_t g_handle_ids = 0;
+static std::atomic<uint64_t> g_handle_ids{0};  // handles from several host threads
 
 namespace {
 

@@ -182,6 +182,19 @@ def test_smooth_cox_and_theta_logistic(tmp_path):
 
 
 @pytest.mark.gpu
+def test_threads_give_the_same_rows(tmp_path):
+    """--threads runs replicates on several host threads (one engine context
+    each): the rows (seeded per replicate) are the same as a serial run."""
+    a, b = tmp_path / "a.csv", tmp_path / "b.csv"
+    args = ["smooth", "--experiment", "lgssm-check", "--T", "63", "--N", "128",
+            "--replicates", "6", "--stable-timing"]
+    r1 = run(args + ["--out", str(a)], tmp_path)
+    r2 = run(args + ["--threads", "3", "--out", str(b)], tmp_path)
+    assert r1.returncode == 0 and r2.returncode == 0, r2.stderr
+    assert a.read_bytes() == b.read_bytes()
+
+
+@pytest.mark.gpu
 def test_check_oracle_passes(tmp_path):
     r = run(["check-oracle", "--T", "63", "--N", "512", "--replicates", "8"], tmp_path)
     assert r.returncode == 0, r.stdout + r.stderr
