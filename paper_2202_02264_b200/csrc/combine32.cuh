@@ -118,6 +118,10 @@ __device__ inline float pair32(const float* u, const float* y, float A) {
   return t;
 }
 
+// Launched with programmatic stream serialization (engine.cu launch_pdl) a
+// kernel may start while its predecessor drains; it waits here until that
+// grid has completed and its memory is visible (a no-op otherwise).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ float ex2(float x) {
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -166,6 +170,7 @@ constexpr int kPairWarps = 4;  // pass-1 warps per CTA (4 CTAs per SM)
 
 template <int D>
 __global__ void __launch_bounds__(32 * kPairWarps, 4) c32_pair(Bufs b, LevelArgs la) {
+  pdl_wait();  // programmatic dependent launch: the previous kernel's writes
   __shared__ float4 s_u[kRowsCTA];          // u_i (2 nu_i), zero-padded to 4
   __shared__ float s_b[kRowsCTA];           // B_i
   __shared__ float s_c[kRowsCTA];           // overflow shift c_i (0 for most rows)
@@ -405,6 +410,7 @@ __device__ inline double block_scan_incl(double v, double* sh) {
 template <int D, int MINB>
 __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
                                                      int systematic) {
+  pdl_wait();
   extern __shared__ double smem[];
   __shared__ double sh[32];
   __shared__ float s_g;

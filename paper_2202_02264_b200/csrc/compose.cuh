@@ -16,6 +16,7 @@ namespace dsmc_dev {
 __global__ void td_kernel(Bufs b, int level, size_t cursor, int nb_l,
                           int nb_lm1, const uint32_t* Mcur, uint32_t* Mnext,
                           int root, const uint32_t* root_map) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // see pdl_wait
   // grid (block, slot chunk, chain): blocks in x (up to 2^31)
   const int q = blockIdx.y * blockDim.x + threadIdx.x;
   const int k = blockIdx.x, ch = blockIdx.z;

@@ -435,6 +435,25 @@ int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
   return DSMC_OK;
 }
 
+// Launch with programmatic stream serialization: the kernel (which starts
+// with griddepcontrol.wait) is set up while its predecessor drains, hiding
+// the launch gap between the many short kernels of the upper levels.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <int D>
 int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systematic) {
   // Pass 1: 256-row tiles; when the level has few combines, the sub-blocks of
@@ -501,14 +520,17 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
     while (ncs_tc * 2 <= nsubb && (long)nk * b.B * nrt_tc * ncs_tc < target) ncs_tc *= 2;
     c32_pair_tc<D><<<dim3(nrt_tc * ncs_tc, nk, b.B), kTcThreads, 0, ctx->stream>>>(b, la);
   } else {
-    c32_pair<D><<<dim3(nrt * ncs, nk, b.B), 32 * kPairWarps, 0, ctx->stream>>>(b, la);
+    CU(launch_pdl(c32_pair<D>, dim3(nrt * ncs, nk, b.B), dim3(32 * kPairWarps), 0, ctx->stream,
+                  b, la));
   }
   LAUNCHED(ctx);
   if (ev) CU(rec_event(ev[1], ctx->stream));
   if (sample4)
-    c32_sample<D, 4><<<dim3(sb, nk, b.B), 256, sm2, ctx->stream>>>(b, la, systematic);
+    CU(launch_pdl(c32_sample<D, 4>, dim3(sb, nk, b.B), dim3(256), sm2, ctx->stream, b, la,
+                  systematic));
   else
-    c32_sample<D, 3><<<dim3(sb, nk, b.B), 256, sm2, ctx->stream>>>(b, la, systematic);
+    CU(launch_pdl(c32_sample<D, 3>, dim3(sb, nk, b.B), dim3(256), sm2, ctx->stream, b, la,
+                  systematic));
   LAUNCHED(ctx);
   if (ev) CU(rec_event(ev[2], ctx->stream));
   return DSMC_OK;
@@ -914,9 +936,9 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     int mcur = 0;
     bool root = true;
     for (int l = level; l >= 2; --l) {
-      td_kernel<<<dim3(nbs[l], (N + 255) / 256, B), 256, 0, ctx->stream>>>(
-          b, l, cursors[l], nbs[l], nbs[l - 1], Mb[mcur], Mb[1 - mcur], root ? 1 : 0,
-          o.root_map);
+      CU(launch_pdl(td_kernel, dim3(nbs[l], (N + 255) / 256, B), dim3(256), 0, ctx->stream, b, l,
+                    cursors[l], nbs[l], nbs[l - 1], (const uint32_t*)Mb[mcur], Mb[1 - mcur],
+                    root ? 1 : 0, o.root_map));
       LAUNCHED(ctx);
       root = false;
       mcur = 1 - mcur;
