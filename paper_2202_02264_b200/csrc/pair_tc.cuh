@@ -1,29 +1,30 @@
-// FP32 pass 1 on the 5th-generation tensor cores (tcgen05, sm_100a).
+// FP32 pass 1 on the 5th-generation tensor cores (tcgen05, sm_100a),
+// selected with DSMC_PAIR_KERNEL=tc (d >= 2).
 //
-// The pair exponent in log2 units is w_ij = A_j + u_i . y_j + B_i (whitened
-// expanded form, col32 / row32): a rank-(d+1) product plus row and column
-// terms. A CTA owns 128 rows of one combine (one TMEM lane per row and per
-// thread); per 64-column sub-block one elected thread issues
-//     D[128 x 64] (TMEM, FP32) = A_rows[128 x K] . B_cols[64 x K]^T
-// (kind::tf32, K-major shared-memory operands, no swizzle) and the four
-// warps read their rows back with tcgen05.ld, take the exact row max over
-// the 64 columns and sum 2^(t - max) on MUFU.EX2: no FP32-pipe dot products
-// remain, so the kernel runs at the MUFU roof instead of the FFMA2+MUFU mix
-// roof of c32_pair.
+// The bound-shifted pair exponent of c32_pair, t_ij = (A_j - cmax_s) +
+// u_i . y_j - c_i (log2 units, whitened expanded form), is a rank-(d+2)
+// product: a CTA owns 128 rows of one combine (one TMEM lane per row) and
+// per 64-column sub-block issues two
+//     D[128 x 32] (TMEM, FP32) = A_rows[128 x K] . B_cols[32 x K]^T
+// (kind::tf32, K-major shared-memory operands, no swizzle) into one of four
+// 32-column TMEM stages. The consumer warps read a stage with one
+// tcgen05.ld.32x32b.x32, release it, and sum 2^t on MUFU.EX2 (one pair in
+// four through an FMA-pipe polynomial) with packed FADD2 accumulators; a
+// half sub-block whose sum leaves [2^-60, 2^120] is redone from its exact max.
 //
 // Precision: TF32 keeps 10 mantissa bits, so every operand is split
 // x = x_hi + x_lo (x_hi = x with the low 13 mantissa bits cleared) and the
 // product is taken as u_hi y_hi + u_lo y_hi + u_hi y_lo ("3xTF32"), the
-// column term as a_hi + a_lo; K = 3d + 2 padded to 8 or 16. The dropped
-// u_lo y_lo term is ~2^-22 relative, the FP32 accumulation ~2^-23 of the
-// term magnitudes — the same order as the FFMA chain it replaces.
+// column and row shifts as hi + lo pairs; K = 3d + 4 padded to 8 or 16. The
+// dropped u_lo y_lo term is ~2^-22 relative, the FP32 accumulation ~2^-23 of
+// the term magnitudes — the same order as the FFMA chain it replaces.
 //
-// Pipeline per sub-block s: threads 0..63 write B_s (one column each, from
-// raw data prefetched a sub-block ahead) into shared buffer s & 1; barrier;
-// thread 0 issues the MMAs into TMEM buffer s & 1 and commits to mbarrier
-// s & 1; every thread then finishes sub-block s - 1 (wait on its mbarrier,
-// tcgen05.ld, max / exp2 / sum, store L_is). 128 TMEM columns per CTA, 4 CTAs
-// per SM.
+// Roles per CTA (224 threads, 4 CTAs per SM = 4 x 128 TMEM columns): warps
+// 0-3 consume (one row each), warps 4-5 produce (one column each: gather,
+// whiten, split, write the K-major row of the B operand into one of four
+// shared buffers), warp 6 issues the MMAs once a buffer is full and its TMEM
+// stage was released. Barriers are mbarriers with per-buffer / per-stage
+// phase parities; every wait traps after 10 s instead of hanging.
 #pragma once
 
 #include "combine32.cuh"
