@@ -158,16 +158,18 @@ constexpr int kTcHalf = 32;    // columns per MMA / TMEM stage (half a sub-block
 constexpr int kTcCtasPerSm = 4;  // 4 x 128 TMEM columns
 
 // Tensor-core pass 1 (one CTA per 128-row tile and column split, 4 CTAs per
-// SM). Producers (warps 4-5, one column each) stage sub-block s into shared
-// buffer s & 1: y_j, a_j = A_j - cmax_s (the two producer warps exchange their
-// column maxima), then arrive on full[s & 1]; producer thread 0 issues the
-// sub-block as two N = 32 MMAs into TMEM stages, each committed to its own
-// mbarrier. Consumers (warps 0-3) take a stage with one tcgen05.ld.x32,
-// release it at once and sum 2^D_ij with four packed accumulators: the
-// exponent is bound-shifted exactly as in c32_pair (shift c_i + cmax_s), so
-// the SM executes only MUFU.EX2 and FADD2 per pair. A half sub-block whose
-// sum leaves [2^-60, 2^120] (rare: rows far from every column) is redone
-// with its exact max from the values still in registers, in log form.
+// SM). Producers (warps 4-5, one column each) stage sub-block q into shared
+// buffer q % 4: y_j and a_j = A_j - cmax_s (the two producer warps exchange
+// their column maxima), then arrive on full[q % 4]; they reuse a buffer once
+// the consumers released its second half (bfree). The issuer warp waits for
+// a full buffer and a released TMEM stage and issues the sub-block as two
+// N = 32 MMAs, each committed to its stage's mbarrier. Consumers (warps 0-3)
+// take a stage with one tcgen05.ld.x32, release it at once and sum 2^t with
+// four packed accumulators: the exponent is bound-shifted exactly as in
+// c32_pair (shift c_i + cmax_s), so the SM executes only MUFU.EX2 (or the
+// FMA-pipe polynomial) and FADD2 per pair. A half sub-block whose sum leaves
+// [2^-60, 2^120] (rare: rows far from every column) is redone with its exact
+// max from the values still in registers, in log form.
 template <int D>
 __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, LevelArgs la) {
   using L = TcK<D>;
