@@ -17,9 +17,13 @@
 // FFMA2 chain of d+1 (bias + d components), two MUFU.EX2 and one FADD2 — no
 // max, no shuffles. The shift is the exact bound lw2_i + cmax_s (+ c_i for
 // the few rows with |nu_i|^2 > 100), so exponents never overflow; a row whose
-// sub-block sum underflows (< 2^-60) is recomputed with its exact max. Lane
-// results L_is = log2 sum_{j in s} 2^w_ij are stored [sub-block][row]
-// (coalesced). Nothing of the N x N table is stored beyond N*N/64 floats.
+// sub-block sum underflows (< 2^-60) is recomputed with its exact max. At
+// d = 1 (SV, Cox, theta-logistic: column terms spread over hundreds of
+// log-units) each row's exact max per sub-block comes from a MUFU-free max
+// pass instead, so no fallback is needed. Lane results L_is = log2 sum_{j in
+// s} 2^w_ij are stored [sub-block][row] (coalesced). Nothing of the N x N
+// table is stored beyond N*N/64 floats. (pair_tc.cuh: the same pass with the
+// dot products on tcgen05, opt-in.)
 //
 // c32_sample (pass 2): one CTA per combine (or per slot slice): row totals
 // from the sub-block sums, row CDF (double inclusive scan), per-slot binary
