@@ -1,3 +1,6 @@
+#!/bin/bash
+# A/B of engine builds made by tools/build_variant.sh: swap each variant .so in
+# as libdsmc_b200.so and bench C4 / C5 with it (run under gpurun).
 cd $GRAFT_REPO_ROOT; P=paper_2202_02264_b200
 cp $P/libdsmc_b200.so /tmp/base.so
 for v in base s4 s5; do

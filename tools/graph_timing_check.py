@@ -1,3 +1,5 @@
+"""Check that the CUDA-graph replay of the resident path reports the same
+per-kernel timings (external event nodes) as eager launches, on C2."""
 import sys, os
 sys.path.insert(0, '.')
 import bench

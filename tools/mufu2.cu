@@ -1,3 +1,6 @@
+// Packed ex2.approx.{bf16x2,f16x2} vs FP32 MUFU.EX2 throughput (DESIGN.md 5.1:
+// all three reach the same exps/s, so packing does not help pass 1).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/mufu2.cu -o tools/mufu2
 #include <cstdio>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>

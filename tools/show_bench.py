@@ -1,3 +1,4 @@
+"""Print the key fields of bench.py JSON lines (value, e2e, roofline, clocks)."""
 import json, sys
 for f in sys.argv[1:]:
     try:
