@@ -131,7 +131,11 @@ struct StreamReader {
       buf = stream_block(id, blk++);
       pos = 0;
     }
-    return buf.v[pos++];
+    // select chain instead of buf.v[pos]: a dynamic index would put the
+    // block in local memory (STL per refill, LDL per draw)
+    const uint64_t v = pos == 0 ? buf.v[0] : pos == 1 ? buf.v[1] : pos == 2 ? buf.v[2] : buf.v[3];
+    ++pos;
+    return v;
   }
   __device__ double uniform() { return u64_uniform(next()); }
   __device__ double uniform_pos() { return u64_uniform_pos(next()); }
