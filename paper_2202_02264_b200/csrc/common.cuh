@@ -77,6 +77,12 @@ __device__ __forceinline__ U64x4 philox_k(uint64_t c0, uint64_t c1,
   return o;
 }
 
+// Word p (0..3) of a block by select chain: indexing v[] with a runtime value
+// would place the block in local memory.
+__device__ __forceinline__ uint64_t pick4(const U64x4& b, uint32_t p) {
+  return p == 0 ? b.v[0] : p == 1 ? b.v[1] : p == 2 ? b.v[2] : b.v[3];
+}
+
 // Stream identity (rng.cpp:45-53).
 struct StreamId {
   uint64_t seed, node, lvrole, sub;
@@ -97,7 +103,7 @@ __device__ __forceinline__ U64x4 stream_block(const StreamId& s, uint64_t blk) {
 // u64 number q of the stream.
 __device__ __forceinline__ uint64_t stream_u64(const StreamId& s, uint64_t q) {
   const U64x4 b = stream_block(s, q >> 2);
-  return b.v[q & 3];
+  return pick4(b, (uint32_t)(q & 3));
 }
 
 // rng.cpp:66-72.
@@ -131,9 +137,9 @@ struct StreamReader {
       buf = stream_block(id, blk++);
       pos = 0;
     }
-    // select chain instead of buf.v[pos]: a dynamic index would put the
-    // block in local memory (STL per refill, LDL per draw)
-    const uint64_t v = pos == 0 ? buf.v[0] : pos == 1 ? buf.v[1] : pos == 2 ? buf.v[2] : buf.v[3];
+    // pick4, not buf.v[pos]: no local memory (an STL per refill and an LDL
+    // per draw otherwise)
+    const uint64_t v = pick4(buf, (uint32_t)pos);
     ++pos;
     return v;
   }

@@ -46,8 +46,8 @@ struct Bufs {
 __device__ inline double leaf_normal64(const StreamId& id, uint64_t i) {
   const uint64_t q = 2 * (i >> 1);
   const U64x4 blk = stream_block(id, q >> 2);
-  const double u1 = u64_uniform_pos(blk.v[q & 3]);
-  const double u2 = u64_uniform(blk.v[(q & 3) + 1]);
+  const double u1 = u64_uniform_pos(pick4(blk, (uint32_t)(q & 3)));
+  const double u2 = u64_uniform(pick4(blk, (uint32_t)(q & 3) + 1));
   const double r = sqrt(DMUL(-2.0, log(u1)));
   const double th = DMUL(2.0 * 3.14159265358979323846, u2);
   return (i & 1) ? DMUL(r, sin(th)) : DMUL(r, cos(th));
@@ -305,8 +305,8 @@ __global__ void __launch_bounds__(256, 3) leaf32_kernel(Bufs b, double* raw0, in
             blk = stream_block(id, q >> 2);
             have = q >> 2;
           }
-          const float u1 = ((float)(uint32_t)(blk.v[q & 3] >> 40) + 0.5f) * 0x1p-24f;
-          const float u2 = (float)(uint32_t)(blk.v[(q & 3) + 1] >> 40) * 0x1p-24f;
+          const float u1 = ((float)(uint32_t)(pick4(blk, (uint32_t)(q & 3)) >> 40) + 0.5f) * 0x1p-24f;
+          const float u2 = (float)(uint32_t)(pick4(blk, (uint32_t)(q & 3) + 1) >> 40) * 0x1p-24f;
           r = sqrtf(-2.0f * __logf(u1));
           sincospif(2.0f * u2, &sn, &cs);
         }
@@ -379,8 +379,8 @@ __global__ void __launch_bounds__(256, 3) leaf32_kernel(Bufs b, double* raw0, in
             have = q >> 2;
           }
           // uniform_pos / uniform at 24-bit resolution: (0,1) and [0,1)
-          const float u1 = ((float)(uint32_t)(blk.v[q & 3] >> 40) + 0.5f) * 0x1p-24f;
-          const float u2 = (float)(uint32_t)(blk.v[(q & 3) + 1] >> 40) * 0x1p-24f;
+          const float u1 = ((float)(uint32_t)(pick4(blk, (uint32_t)(q & 3)) >> 40) + 0.5f) * 0x1p-24f;
+          const float u2 = (float)(uint32_t)(pick4(blk, (uint32_t)(q & 3) + 1) >> 40) * 0x1p-24f;
           r = sqrtf(-2.0f * __logf(u1));
           sincospif(2.0f * u2, &sn, &cs);
         }
