@@ -50,6 +50,8 @@ CONFIGS = {
                     "RTS-marginal proposals", model="cv", K=1 << 14, N=1024, resampler=0),
     "c3": dict(desc="C3: stochastic volatility, K=T+1=2^16, N=4096, MH-lazy (B=16)",
                model="sv", K=1 << 16, N=4096, resampler=2),
+    "c3r": dict(desc="C3: stochastic volatility, K=T+1=2^16, N=4096, rejection-lazy (exact)",
+                model="sv", K=1 << 16, N=4096, resampler=3),
     "c5": dict(desc="C5: 2-D constant-velocity LGSSM d=4, K=T+1=2^20, N=1024, multinomial, "
                     "RTS-marginal proposals", model="cv", K=1 << 20, N=1024, resampler=0),
     "c4": dict(desc="C4: SV particle Gibbs (batched c-dSMC sweep + device parameter kernel), "
@@ -57,17 +59,24 @@ CONFIGS = {
                N=512, resampler=0, chains=64),
 }
 DEFAULT_CONFIG = "c5"
+# CPU sample size shared by the --impl reference arm and the cpu_baseline leg
+# (runs too long for the host are timed at K' = 2^16 leaves and
+# extrapolated linearly in T; dense cost is exactly T*N^2 pair evaluations)
+REF_KPRIME = 1 << 16
+RESAMPLERS = ["multinomial", "systematic", "mh-lazy", "rejection-lazy"]
 METRIC = "smoothed particle-timesteps/sec (T·N/s)"
 UNIT = "particle-timesteps/s"
 
 
-def build_model(cfg, pinned=False):
+def build_model(cfg, pinned=False, smoother=None):
+    """smoother: the RTS used for the proposals (default: the engine's host
+    RTS; the reference arm passes the oracle's so it never maps the product)."""
     from paper_2202_02264_b200 import abi, models
     T = cfg["K"] - 1
     if cfg["model"] == "cv":
-        m = models.cv_tracking(T)
+        m = models.cv_tracking(T, smoother=smoother)
     elif cfg["model"] == "lgssm":
-        m = models.lgssm_check(T)
+        m = models.lgssm_check(T, smoother=smoother)
     else:
         m = models.sv(T)
     if pinned:
@@ -100,33 +109,90 @@ def host_threads():
         return os.cpu_count() or 1
 
 
-def cpu_reference(cfg, budget_s=8.0, Kp=None):
-    """Reference run_smoother (compiled from /root/reference) on a bounded
-    sample: K' leaves with the same N, d, model family. Without Kp, doubles K'
-    from 16 until one run takes >= budget_s / 4. Returns (T.N/s, cores,
-    sample text, wall, K')."""
-    from oracle.py import Reference
+def bench_config(cfg, world=1):
+    """The `config` object of both arms (identical, so the driver can pair
+    them), including the CPU sample both arms' CPU legs run."""
+    K = cfg["K"]
+    c = {"workload": cfg["desc"], "K": K, "T": K - 1, "N": cfg["N"],
+         "resampler": RESAMPLERS[cfg["resampler"]],
+         "l2": ("inputs larger than L2 (leaf slab %.0f MB > 126 MB)" % (K * cfg["N"] * 20 * cfg.get("chains", 1) / 1e6)
+                if K * cfg["N"] * 20 * cfg.get("chains", 1) > 126e6 else
+                "working set %.0f MB fits in L2 (small config; no flush between steps)"
+                % (K * cfg["N"] * 20 * cfg.get("chains", 1) / 1e6)),
+         "parallelism": (f"time-sharded x{world} (NCCL P2P boundary exchange)" if world > 1
+                         else "single GPU")}
+    if "chains" in cfg:
+        c["chains"] = cfg["chains"]
+        c["parallelism"] = (f"chains split x{world}" if world > 1 else "single GPU")
+        c["cpu_sample"] = {"K_prime": K, "chains": cfg["chains"], "extrapolated": False}
+    else:
+        kp = min(K, REF_KPRIME)
+        c["cpu_sample"] = {"K_prime": kp, "extrapolated": kp < K,
+                           "rule": "K' = min(K, 2^16) leaves, same N, d, model family; "
+                                   "T*N/s extrapolated linearly in T (dense cost = T*N^2)"}
+    return c
+
+
+def cpu_reference(cfg):
+    """One step of the reference's own CPU implementation (oracle/_ref,
+    compiled from /root/reference) on all host threads: run_smoother on
+    K' = min(K, 2^16) leaves with the same N, d, model family and resampler
+    (C4: run_conditional for every chain, chains over threads as
+    experiment.cpp:618-642). The model (RTS proposals included) is built with
+    the oracle, so this process never maps the product library.
+    Returns (T.N/s, cores, sample text, wall seconds)."""
+    from oracle.py import Oracle, Reference
     if not Reference.available():
         return None
     R = Reference()
     threads = host_threads()
-    fixed = Kp is not None
-    Kp = Kp or 16
-    while True:
-        m = build_model(dict(cfg, K=Kp))
-        t0 = time.perf_counter()
-        r = R.run_smoother(m, cfg["N"], cfg["resampler"], seed=1, mh_steps=16, threads=threads,
-                           want_paths=False)
-        wall = time.perf_counter() - t0
-        if fixed or wall >= budget_s / 4 or Kp >= cfg["K"]:
-            break
-        Kp *= 2
+    if cfg["model"] == "sv_pgibbs":
+        return cpu_reference_pgibbs(cfg, R, threads)
+    Kp = min(cfg["K"], REF_KPRIME)
+    m = build_model(dict(cfg, K=Kp), smoother=Oracle().kalman_smooth)
+    t0 = time.perf_counter()
+    r = R.run_smoother(m, cfg["N"], cfg["resampler"], seed=1 + (1 << 32), mh_steps=16,
+                       threads=threads, want_paths=False)
+    wall = time.perf_counter() - t0
     val = Kp * cfg["N"] / wall
     sample = (f"reference run_smoother (oracle/_ref, compiled from /root/reference) on "
-              f"K'={Kp} leaves (T'={Kp - 1}), N={cfg['N']}, same model family, {threads} threads, "
-              f"wall {wall:.2f} s (RunMetadata wall {r['wall_time_ms']:.0f} ms); dense cost is "
-              f"exactly T*N^2 pair evaluations so T*N/s does not depend on T")
-    return val, threads, sample, wall, Kp
+              f"K'={Kp} leaves (T'={Kp - 1}), N={cfg['N']}, {RESAMPLERS[cfg['resampler']]}, "
+              f"same model family, {threads} threads, wall {wall:.2f} s (RunMetadata wall "
+              f"{r['wall_time_ms']:.0f} ms); "
+              + ("extrapolated linearly in T to K=%d (dense cost is exactly T*N^2 pair "
+                 "evaluations)" % cfg["K"] if Kp < cfg["K"] else "full workload"))
+    return val, threads, sample, wall
+
+
+def _pgibbs_inputs(cfg):
+    from paper_2202_02264_b200 import models
+    K = cfg["K"]
+    ys = np.asarray(models.sv(K - 1).arrays["y"], np.float64)
+    return ys, np.array([-1.0, 0.9, 0.1]), np.full(K, -1.0)
+
+
+def cpu_reference_pgibbs(cfg, R, threads):
+    """C4 on the CPU: the reference's run_conditional (conditional.cpp:156-216)
+    for each of the chains (SV model at the chains' current theta, K = 2^12,
+    N = 512, multinomial), chains spread over the host threads."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2202_02264_b200 import models
+    K, N, B = cfg["K"], cfg["N"], cfg["chains"]
+    ys, theta, star = _pgibbs_inputs(cfg)
+    m = models.sv(K - 1, mu=theta[0], phi=theta[1], sigma=float(np.sqrt(theta[2])), ys=ys)
+
+    def chain(c):
+        return R.conditional(m, star, N, 1000 + c, 0)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(chain, range(B)))
+    wall = time.perf_counter() - t0
+    val = B * K * N / wall
+    sample = (f"reference run_conditional (oracle/_ref, compiled from /root/reference) for "
+              f"{B} chains x K={K} x N={N} (SV, multinomial), chains over {threads} host "
+              f"threads, wall {wall:.2f} s; full workload, no extrapolation (the parameter "
+              f"update is O(T) per chain and not timed)")
+    return val, threads, sample, wall
 
 
 class ClockSampler:
@@ -228,12 +294,12 @@ def run_pgibbs(args, cfg, rank, world, device):
     torch.cuda.set_device(device)
     eng = Engine(device)
     K, N, B = cfg["K"], cfg["N"], cfg["chains"] // world
-    ys = np.asarray(models.sv(K - 1).arrays["y"], np.float64)
+    ys, theta0, star0 = _pgibbs_inputs(cfg)
     prior = abi.SvPrior(-1.0, 1.0, 2.0, 0.2, 0.05)
     theta = torch.empty((B, 3), dtype=torch.float64, pin_memory=True).numpy()
     stars = torch.empty((B, K), dtype=torch.float64, pin_memory=True).numpy()
-    theta[:] = [-1.0, 0.9, 0.1]
-    stars[:] = -1.0
+    theta[:] = theta0
+    stars[:] = star0
     seeds = np.arange(B, dtype=np.uint64) + 1000 * (rank + 1)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=torch.device("cuda", device))
 
@@ -253,8 +319,7 @@ def run_pgibbs(args, cfg, rank, world, device):
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                "dtype": "f32+f64 (FP32 c-dSMC, FP64 parameter kernel)",
                "data": "synthetic SV series (numpy seed 90210)",
-               "config": {"workload": cfg["desc"], "K": K, "N": N, "chains": cfg["chains"],
-                          "parallelism": f"chains split x{world}" if world > 1 else "single GPU"},
+               "config": bench_config(cfg, world),
                "e2e": {"value": value, "unit": UNIT,
                        "h2d_bytes_per_step": int(theta.nbytes + stars.nbytes + ys.nbytes),
                        "d2h_bytes_per_step": int(theta.nbytes + stars.nbytes + B * K),
@@ -303,6 +368,7 @@ def run_ours(args, cfg, rank, world, device):
     with ClockSampler(device) as clocks:
         ms_max = _time_steps(stream, args.steps, step, world, device)
     launches = eng.launches - launches0
+    eng.sync()  # surfaces any device error of the timed runs
     timings = eng.timings()  # last step's per-kernel-class event times
     value = K * N / (ms_max * 1e-3)
     # ---- end to end through the public API (host pinned in, host out)
@@ -345,6 +411,21 @@ def run_ours(args, cfg, rank, world, device):
     e2e_s = _max_over_ranks(float(np.median(walls)), world, device)
     e2e_mean = _max_over_ranks(float(np.mean(walls)), world, device)
     e2e_val = K * N / e2e_s
+    # ---- equal-precision record: the FP64 parity path (the reference's
+    # operation order, bit-exact ancestors) on the same resident workload
+    fp64 = None
+    if world == 1 and prec == abi.FP32 and not args.no_fp64:
+        f_steps = 2
+        eng.smooth_resident(h, N, rs, seed=seed_base + 7000, precision=abi.FP64_PARITY)
+        eng.sync()
+        f_ms = _time_steps(stream, f_steps, lambda s: eng.smooth_resident(
+            h, N, rs, seed=seed_base + 7001 + s, precision=abi.FP64_PARITY), world, device)
+        eng.sync()
+        fp64 = {"value": K * N / (f_ms * 1e-3), "unit": UNIT, "ms_per_step": f_ms,
+                "steps": f_steps, "warmup": 1, "dtype": "f64",
+                "note": "same workload through the FP64 parity path (reference operation "
+                        "order; ancestors bit-identical to the CPU reference on the same "
+                        "leaves), CUDA events on the engine stream"}
     out = None
     if rank == 0:
         ck = clocks.summary()
@@ -404,14 +485,9 @@ def run_ours(args, cfg, rank, world, device):
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32" if prec == abi.FP32 else "f64",
             "data": "synthetic (trajectory simulated with numpy seed 90210; RTS-marginal proposals)",
-            "config": {"workload": cfg["desc"], "K": K, "T": K - 1, "N": N, "d": d,
-                       "resampler": ["multinomial", "systematic", "mh-lazy",
-                                     "rejection-lazy"][rs],
-                       "precision": ("fp32 throughput path" if prec == abi.FP32 else
-                                     "fp64 parity path (reference operation order)"),
-                       "l2": "inputs larger than L2 (leaf slab %.0f MB > 126 MB)" % (K * N * 20 / 1e6),
-                       "parallelism": (f"time-sharded x{world} (NCCL P2P boundary exchange)"
-                                       if world > 1 else "single GPU")},
+            "config": bench_config(cfg, world),
+            "precision": ("fp32 throughput path" if prec == abi.FP32 else
+                          "fp64 parity path (reference operation order)"),
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                     "timing": "host wall clock per call, median of the steps (mean-based "
@@ -423,6 +499,8 @@ def run_ours(args, cfg, rank, world, device):
             "roofline": roof,
             "clocks": ck,
         }
+        if fp64:
+            out["fp64_parity"] = fp64
     eng.free_model(h)
     eng.close()
     return out
@@ -436,6 +514,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=list(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true",
+                    help="skip the FP64 parity-path record of the N=1 line")
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"],
                     help="fp64 = the bit-exact parity path (single GPU)")
     args = ap.parse_args()
@@ -453,18 +533,20 @@ def main():
             print(json.dumps({"impl": "reference", "unavailable":
                               "oracle/_ref/libdsmc_ref.so not built (needs /root/reference)"}))
             return
-        vals = []
-        v, cores, sample, wall, Kp = cpu_reference(cfg, budget_s=4.0)  # sizes the sample
+        vals, walls = [], []
         for s in range(args.warmup + args.steps):
-            v, cores, sample, wall, _ = cpu_reference(cfg, Kp=Kp)
+            v, cores, sample, wall = cpu_reference(cfg)
             if s >= args.warmup:
                 vals.append(v)
+                walls.append(wall)
         val = float(np.median(vals))
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "higher_is_better": True, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "K": cfg["K"], "N": cfg["N"]},
+            "ms_per_step": float(np.median(walls)) * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (same generator and seeds as the GPU arm)",
+            "config": bench_config(cfg, world),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "reference",
                              "sample": sample},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -487,10 +569,10 @@ def main():
         torch.distributed.barrier()
     out = run_ours(args, cfg, rank, world, local)
     if rank == 0:
-        if world == 1 and not args.no_cpu_baseline and cfg["model"] != "sv_pgibbs":
+        if world == 1 and not args.no_cpu_baseline:
             cb = cpu_reference(cfg)
             if cb is not None:
-                v, cores, sample, wall, _ = cb
+                v, cores, sample, wall = cb
                 out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores,
                                        "kind": "reference", "sample": sample}
         print(json.dumps(out))

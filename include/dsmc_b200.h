@@ -176,8 +176,11 @@ typedef struct dsmc_smooth_out {
   uint32_t* pair_left;      /* T*N: per combine in schedule order, left idx */
   uint32_t* pair_right;     /* T*N: right idx */
   double* log_mean_weight;  /* T: per-combine log mean pair weight (dense) */
-  double* leaf_states;      /* (T+1)*N*d leaf states as generated */
-  double* leaf_logw;        /* (T+1)*N raw leaf log-weights */
+  double* leaf_states;      /* (T+1)*N*d leaf states as generated (FP64
+                               parity only; DSMC_E_INVALID_ARGUMENT under FP32) */
+  double* leaf_logw;        /* (T+1)*N normalised leaf log-weights, each
+                               leaf's BlockEstimate::log_w (smoother.cpp:117-128);
+                               FP64 parity only */
   /* RunMetadata (smoother.hpp:58-68) */
   double log_norm_const;
   int has_log_norm_const;

@@ -1557,3 +1557,169 @@ int or_sv_param_update(const double* x, int T, const dsmc_sv_prior* pr,
   if (accepted_phi) *accepted_phi = acc_phi;
   return 0;
 }
+
+/* ------------------------------------------------------------------------
+ * Kalman filter + RTS smoother of a DSMC_MODEL_LGSSM descriptor (host FP64),
+ * restating kalman_smooth (kalman.cpp:78-138): predicted covariance
+ * symmetrised, Joseph-form update, RTS gain by solving against the predicted
+ * covariance, symmetrisation after every step, the jitter-escalating
+ * Cholesky of robust_llt (kalman.cpp:15-26) and log_gaussian (:28-36). Used
+ * by bench.py's reference arm to build the RTS-marginal proposals without
+ * loading the product library. */
+#define KMAXD 8
+static void km_sym(double* P, int d) {
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < i; ++j) {
+      double v = (P[i * d + j] + P[j * d + i]) * 0.5;
+      P[i * d + j] = P[j * d + i] = v;
+    }
+}
+/* robust_llt: symmetrise, then up to 4 Cholesky attempts with jitter
+   scale * 10^(attempt - 12), scale = max(trace / n, 1e-300) */
+static int km_llt(const double* A, int d, double* L) {
+  double P[KMAXD * KMAXD];
+  memcpy(P, A, sizeof(double) * d * d);
+  km_sym(P, d);
+  double tr = 0.0;
+  for (int i = 0; i < d; ++i) tr += P[i * d + i];
+  double scale = tr / d > 1e-300 ? tr / d : 1e-300;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    if (chol(P, d, L)) return 1;
+    for (int i = 0; i < d; ++i) P[i * d + i] += scale * pow(10.0, attempt - 12);
+  }
+  return 0;
+}
+/* X := A^{-1} B for A = L L' (B: d x m, row-major) */
+static void km_solve(const double* L, int d, const double* B, int m, double* X) {
+  for (int c = 0; c < m; ++c) {
+    double z[KMAXD];
+    for (int i = 0; i < d; ++i) {
+      double s = B[i * m + c];
+      for (int k = 0; k < i; ++k) s -= L[i * d + k] * z[k];
+      z[i] = s / L[i * d + i];
+    }
+    for (int i = d - 1; i >= 0; --i) {
+      double s = z[i];
+      for (int k = i + 1; k < d; ++k) s -= L[k * d + i] * X[k * m + c];
+      X[i * m + c] = s / L[i * d + i];
+    }
+  }
+}
+/* C (n x m) = A (n x k) * B (k x m), optional transposes of the stored arrays */
+static void km_mul(const double* A, int ta, const double* B, int tb, int n, int k, int m,
+                   double* C) {
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < m; ++j) {
+      double s = 0.0;
+      for (int q = 0; q < k; ++q)
+        s += (ta ? A[q * n + i] : A[i * k + q]) * (tb ? B[j * k + q] : B[q * m + j]);
+      C[i * m + j] = s;
+    }
+}
+
+int or_kalman_smooth(const dsmc_model_desc* m, double* sm, double* sc, double* loglik) {
+  if (!m || m->kind != DSMC_MODEL_LGSSM)
+    return fail(DSMC_E_INVALID_ARGUMENT, "kalman_smooth: LGSSM descriptor required");
+  const int d = m->state_dim, dy = m->obs_dim, T = m->horizon, K = T + 1;
+  if (d < 1 || d > KMAXD || dy < 1 || dy > KMAXD)
+    return fail(DSMC_E_INVALID_ARGUMENT, "kalman_smooth: dims must be 1..8");
+  const size_t dd = (size_t)d * d;
+  double* pm = malloc(sizeof(double) * K * d);
+  double* pc = malloc(sizeof(double) * K * dd);
+  double* fm = malloc(sizeof(double) * K * d);
+  double* fc = malloc(sizeof(double) * K * dd);
+  double ll = 0.0;
+  int rc = 0;
+  for (int t = 0; t <= T && !rc; ++t) {
+    double* Pp = pc + t * dd;
+    if (t == 0) {
+      memcpy(pm, m->m0, sizeof(double) * d);
+      memcpy(Pp, m->P0, sizeof(double) * dd);
+    } else {
+      const double* F = at(m->F, m->F_stride, t);
+      const double* b = at(m->b, m->b_stride, t);
+      const double* Q = at(m->Q, m->Q_stride, t);
+      double tmp[KMAXD * KMAXD];
+      km_mul(F, 0, fm + (t - 1) * d, 0, d, d, 1, pm + t * d);
+      for (int i = 0; i < d; ++i) pm[t * d + i] += b[i];
+      km_mul(F, 0, fc + (t - 1) * dd, 0, d, d, d, tmp);
+      km_mul(tmp, 0, F, 1, d, d, d, Pp);
+      for (size_t i = 0; i < dd; ++i) Pp[i] += Q[i];
+      km_sym(Pp, d);
+    }
+    if (m->has_obs ? m->has_obs[t] != 0 : 1) {
+      const double* H = at(m->H, m->H_stride, t);
+      const double* R = at(m->R, m->R_stride, t);
+      const double* y = m->y + (size_t)t * dy;
+      double resid[KMAXD], HP[KMAXD * KMAXD], S[KMAXD * KMAXD], L[KMAXD * KMAXD];
+      double Kt[KMAXD * KMAXD], Kg[KMAXD * KMAXD], A[KMAXD * KMAXD], t1[KMAXD * KMAXD];
+      double t2[KMAXD * KMAXD];
+      km_mul(H, 0, pm + t * d, 0, dy, d, 1, resid);
+      for (int i = 0; i < dy; ++i) resid[i] = y[i] - resid[i];
+      km_mul(H, 0, Pp, 0, dy, d, d, HP);
+      km_mul(HP, 0, H, 1, dy, d, dy, S);
+      for (int i = 0; i < dy * dy; ++i) S[i] += R[i];
+      if (!km_llt(S, dy, L)) {
+        rc = fail(DSMC_E_RUNTIME, "kalman update: covariance is not positive definite");
+        break;
+      }
+      double ld = 0.0, z2 = 0.0, z[KMAXD];
+      for (int i = 0; i < dy; ++i) ld += 2.0 * log(L[i * dy + i]);
+      for (int i = 0; i < dy; ++i) {
+        double s = resid[i];
+        for (int k = 0; k < i; ++k) s -= L[i * dy + k] * z[k];
+        z[i] = s / L[i * dy + i];
+        z2 += z[i] * z[i];
+      }
+      ll += -0.5 * (dy * log(2.0 * M_PI) + ld + z2);
+      km_solve(L, dy, HP, d, Kt); /* (dy x d) = S^{-1} H P */
+      for (int i = 0; i < d; ++i)
+        for (int j = 0; j < dy; ++j) Kg[i * dy + j] = Kt[j * d + i];
+      km_mul(Kg, 0, resid, 0, d, dy, 1, fm + t * d);
+      for (int i = 0; i < d; ++i) fm[t * d + i] += pm[t * d + i];
+      km_mul(Kg, 0, H, 0, d, dy, d, A);
+      for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j) A[i * d + j] = (i == j) - A[i * d + j];
+      km_mul(A, 0, Pp, 0, d, d, d, t1);
+      km_mul(t1, 0, A, 1, d, d, d, fc + t * dd);
+      km_mul(Kg, 0, R, 0, d, dy, dy, t1);
+      km_mul(t1, 0, Kg, 1, d, dy, d, t2);
+      for (size_t i = 0; i < dd; ++i) fc[t * dd + i] += t2[i];
+      km_sym(fc + t * dd, d);
+    } else {
+      memcpy(fm + t * d, pm + t * d, sizeof(double) * d);
+      memcpy(fc + t * dd, Pp, sizeof(double) * dd);
+    }
+  }
+  if (!rc) {
+    memcpy(sm + (size_t)T * d, fm + (size_t)T * d, sizeof(double) * d);
+    memcpy(sc + (size_t)T * dd, fc + (size_t)T * dd, sizeof(double) * dd);
+    for (int t = T - 1; t >= 0; --t) {
+      double L[KMAXD * KMAXD], FP[KMAXD * KMAXD], Gt[KMAXD * KMAXD], G[KMAXD * KMAXD];
+      double e[KMAXD], D[KMAXD * KMAXD], t1[KMAXD * KMAXD];
+      if (!km_llt(pc + (t + 1) * dd, d, L)) {
+        rc = fail(DSMC_E_RUNTIME, "rts gain: covariance is not positive definite");
+        break;
+      }
+      const double* F = at(m->F, m->F_stride, t + 1);
+      km_mul(F, 0, fc + t * dd, 1, d, d, d, FP); /* F * filt_cov' */
+      km_solve(L, d, FP, d, Gt);
+      for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j) G[i * d + j] = Gt[j * d + i];
+      for (int i = 0; i < d; ++i) e[i] = sm[(t + 1) * d + i] - pm[(t + 1) * d + i];
+      km_mul(G, 0, e, 0, d, d, 1, sm + t * d);
+      for (int i = 0; i < d; ++i) sm[t * d + i] += fm[t * d + i];
+      for (size_t i = 0; i < dd; ++i) D[i] = sc[(t + 1) * dd + i] - pc[(t + 1) * dd + i];
+      km_mul(G, 0, D, 0, d, d, d, t1);
+      km_mul(t1, 0, G, 1, d, d, d, sc + t * dd);
+      for (size_t i = 0; i < dd; ++i) sc[t * dd + i] += fc[t * dd + i];
+      km_sym(sc + t * dd, d);
+    }
+  }
+  free(pm);
+  free(pc);
+  free(fm);
+  free(fc);
+  if (!rc && loglik) *loglik = ll;
+  return rc;
+}

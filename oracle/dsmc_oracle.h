@@ -69,6 +69,11 @@ int or_sv_param_update(const double* path, int horizon,
 double or_gamma_draw(double shape, double rate, uint64_t seed, uint32_t level,
                      uint64_t node, int role);
 
+/* kalman_smooth (kalman.cpp:78-138) of an LGSSM descriptor (d, dy <= 8):
+ * smoothed means (T+1)*d, covariances (T+1)*d*d, marginal log-likelihood. */
+int or_kalman_smooth(const dsmc_model_desc* model, double* smooth_mean,
+                     double* smooth_cov, double* log_likelihood);
+
 #ifdef __cplusplus
 }
 #endif

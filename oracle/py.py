@@ -97,6 +97,7 @@ class Oracle(_Base):
         L.or_sv_param_update.argtypes = [_dp, _i, C.POINTER(abi.SvPrior), _u64, _u32, _dp, _ip]
         L.or_gamma_draw.restype = C.c_double
         L.or_gamma_draw.argtypes = [C.c_double, C.c_double, _u64, _u32, _u64, _i]
+        L.or_kalman_smooth.argtypes = [C.POINTER(abi.ModelDesc), _dp, _dp, _dp]
         self._philox = L.or_philox
         self._stream = L.or_stream
         self._resample = L.or_resample_table
@@ -146,6 +147,14 @@ class Oracle(_Base):
                                           abi.dptr(out), C.byref(lnc), C.byref(has), C.byref(ev)))
         return dict(path=out, log_norm_const=lnc.value if has.value else None,
                     weight_evals=ev.value)
+
+    def kalman_smooth(self, model):
+        """kalman.cpp:78-138 restated in C -> (means, covs, loglik)."""
+        K, d = model.horizon + 1, model.d
+        m, P, ll = np.zeros((K, d)), np.zeros((K, d, d)), C.c_double()
+        self._check(self.L.or_kalman_smooth(C.byref(model.desc), abi.dptr(m), abi.dptr(P),
+                                            C.byref(ll)))
+        return m, P, ll.value
 
     def sv_param_update(self, path, theta, prior, seed, sweep):
         th = np.ascontiguousarray(theta, np.float64).copy()

@@ -13,6 +13,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -94,11 +95,15 @@ struct dsmc_ctx {
   // the tcgen05 kernel c32_pair_tc (DSMC_PAIR_KERNEL=tc)
   bool pair_tc = false;
   int num_sms = 148;
+  int smem_optin = 227 * 1024;  // max dynamic shared memory per CTA (opt-in)
   cudaStream_t copy_stream = nullptr;  // device->host copies overlapping the gather
   static constexpr int kGatherChunks = 8;
   cudaEvent_t gather_ev[kGatherChunks] = {};
   // last resident run
-  int last_K = 0, last_d = 0, last_B = 0;
+  int last_K = 0, last_d = 0, last_B = 0;  // shape of the last resident run
+  size_t mean_cap = 0, cov_cap = 0;         // allocated doubles of d_mean / d_cov
+  ErrFlag* last_err = nullptr;              // device error record of the last
+  int last_err_K = 0;                       // resident / window run (unchecked)
   double* d_mean = nullptr;
   double* d_cov = nullptr;
   double last_lnc = NAN;
@@ -120,6 +125,7 @@ struct dsmc_ctx {
     cudaGraphNode_t seed_node = nullptr;
     cudaKernelNodeParams seed_params{};
     uint64_t* seed_dst = nullptr;
+    ErrFlag* err = nullptr;
     uint64_t launches = 0;
     int kev_used = 0, levels = 0;
     void reset() {
@@ -224,6 +230,12 @@ int validate_desc(dsmc_ctx* ctx, const dsmc_model_desc* m) {
   return DSMC_OK;
 }
 
+void free_handle(dsmc_model_handle* h) {
+  if (!h) return;
+  for (void* p : h->owned) cudaFreeAsync(p, h->stream);
+  delete h;
+}
+
 // per_t > 0: a per-time array of n = K * per_t elements (deferrable)
 template <class T>
 int upload(dsmc_ctx* ctx, dsmc_model_handle* h, const T* src, size_t n,
@@ -253,7 +265,8 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
         descs[c].kind != descs[0].kind)
       return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "chains must share kind, horizon and dims");
   }
-  auto h = std::make_unique<dsmc_model_handle>();
+  std::unique_ptr<dsmc_model_handle, void (*)(dsmc_model_handle*)> h(new dsmc_model_handle(),
+                                                                      free_handle);
   h->id = ++g_handle_ids;
   h->B = B;
   h->stream = ctx->stream;
@@ -367,11 +380,6 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
   return DSMC_OK;
 }
 
-void free_handle(dsmc_model_handle* h) {
-  if (!h) return;
-  for (void* p : h->owned) cudaFreeAsync(p, h->stream);
-  delete h;
-}
 
 // --------------------------------------------------------------- the run
 struct RunOpts {
@@ -426,8 +434,11 @@ template <int MC, int D>
 int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
                int systematic) {
   const size_t sm = smem_cols64(b.N, D);
-  CU(cudaFuncSetAttribute(c64_rows<MC, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  CU(cudaFuncSetAttribute(c64_sample<MC, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  if (sm > (size_t)ctx->smem_optin)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                   "FP64 parity combine: N * (d + 2) doubles exceed the shared-memory "
+                   "column stage (N <= " + std::to_string(ctx->smem_optin / (8 * (D + 2))) +
+                       " at this d); use the FP32 path or a lazy resampler");
   c64_rows<MC, D><<<dim3((b.N + 31) / 32, nk, b.B), 256, sm, ctx->stream>>>(b, la);
   LAUNCHED(ctx);
   c64_sample<MC, D><<<dim3(nk, 1, b.B), 256, sm, ctx->stream>>>(b, la, systematic);
@@ -478,23 +489,11 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
   const size_t sm2 = sizeof(double) * (N + 1) + NPS * (16 + 16 + 8) + sizeof(float) * N + 16 +
                      sizeof(double) * ((ns + 1) & ~(size_t)1) + 16 * ns + 8 * ns +
                      sizeof(int) * (32 + nsub);
-  static bool configured = false;
-  if (!configured) {
-    CU(cudaFuncSetAttribute(c32_sample<D, 3>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                            cudaSharedmemCarveoutMaxShared));
-    CU(cudaFuncSetAttribute(c32_sample<D, 4>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                            cudaSharedmemCarveoutMaxShared));
-    configured = true;
-  }
   const bool sample4 = sm2 <= 48 * 1024;
-  if (sm2 > 227 * 1024)
+  if (sm2 > (size_t)ctx->smem_optin)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
                    "FP32 dense combine: N too large for the shared-memory sampler (use a lazy "
                    "resampler)");
-  CU(cudaFuncSetAttribute(c32_sample<D, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-  if (sample4)
-    CU(cudaFuncSetAttribute(c32_sample<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sm2));
   la.aux_comb = ((size_t)10 * N + 3) & ~(size_t)3;
   {
     void* p;
@@ -992,9 +991,67 @@ int check_device_error(dsmc_ctx* ctx, const RunResult& r, int K) {
   return DSMC_OK;
 }
 
+// Device error record of the last resident / window run (enqueued without a
+// host sync): read it once, after the stream drains, and clear it.
+int check_pending_error(dsmc_ctx* ctx) {
+  if (!ctx->last_err) return DSMC_OK;
+  ErrFlag e;
+  CU(cudaMemcpyAsync(&e, ctx->last_err, sizeof e, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->last_err = nullptr;
+  if (e.code) return set_err(ctx, e.code, err_message(e, ctx->last_err_K));
+  return DSMC_OK;
+}
+
 struct DevSeeds {
   uint64_t* p = nullptr;
 };
+
+// Kernel attributes are per function and per device and shared by every
+// context (and host thread) of the process: set them once per device, to the
+// opt-in maximum, under a lock — never per launch (a per-launch
+// cudaFuncSetAttribute with a level-dependent size races with other host
+// threads and could lower a limit another thread's launch needs).
+template <int D>
+cudaError_t configure_d(int smem) {
+  cudaError_t e = cudaSuccess;
+  auto set = [&](auto fn) {
+    if (e != cudaSuccess) return;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+  };
+  set(c32_sample<D, 3>);
+  set(c32_sample<D, 4>);
+  set(c64_rows<kLGN, D>);
+  set(c64_sample<kLGN, D>);
+  set(pf_forward_kernel<D>);
+  set(ffbs_backward_kernel<D>);
+  return e;
+}
+cudaError_t configure_device(int device, int smem) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (std::find(done.begin(), done.end(), device) != done.end()) return cudaSuccess;
+  cudaError_t e = configure_d<1>(smem);
+  if (e == cudaSuccess) e = configure_d<2>(smem);
+  if (e == cudaSuccess) e = configure_d<3>(smem);
+  if (e == cudaSuccess) e = configure_d<4>(smem);
+  for (auto fn : {c64_rows<kLG1, 1>, c64_rows<kSV, 1>, c64_rows<kCOX, 1>, c64_rows<kCRW, 1>,
+                  c64_rows<kTHETA, 1>}) {
+    if (e != cudaSuccess) break;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  }
+  for (auto fn : {c64_sample<kLG1, 1>, c64_sample<kSV, 1>, c64_sample<kCOX, 1>,
+                  c64_sample<kCRW, 1>, c64_sample<kTHETA, 1>}) {
+    if (e != cudaSuccess) break;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  }
+  if (e == cudaSuccess) done.push_back(device);
+  return e;
+}
 
 }  // namespace
 
@@ -1010,8 +1067,15 @@ int dsmc_create(int device, dsmc_ctx** out) {
   ctx->device = device;
   if (const char* pk = getenv("DSMC_PAIR_KERNEL")) ctx->pair_tc = strcmp(pk, "tc") == 0;
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return DSMC_E_NO_DEVICE;
+  }
+  if (configure_device(device, ctx->smem_optin) != cudaSuccess) {
+    cudaGetLastError();
+    cudaStreamDestroy(ctx->stream);
     delete ctx;
     return DSMC_E_NO_DEVICE;
   }
@@ -1054,8 +1118,9 @@ const char* dsmc_last_error(const dsmc_ctx* ctx) { return ctx ? ctx->err.c_str()
 uint64_t dsmc_kernel_launches(const dsmc_ctx* ctx) { return ctx ? ctx->launches : 0; }
 void* dsmc_stream(dsmc_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 int dsmc_sync(dsmc_ctx* ctx) {
+  if (!ctx) return DSMC_E_INVALID_ARGUMENT;
   CU(cudaStreamSynchronize(ctx->stream));
-  return DSMC_OK;
+  return check_pending_error(ctx);
 }
 
 int dsmc_model_upload(dsmc_ctx* ctx, const dsmc_model_desc* model,
@@ -1119,6 +1184,10 @@ int dsmc_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
                 const dsmc_smooth_opts* opts, dsmc_smooth_out* out) {
   if (!ctx || !out) return DSMC_E_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
+  if (opts && opts->precision != DSMC_FP64_PARITY && (out->leaf_states || out->leaf_logw))
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                   "leaf_states / leaf_logw are FP64-parity outputs (the FP32 path stores "
+                   "centred single-precision leaves)");
   const auto t0 = std::chrono::steady_clock::now();
   dsmc_model_handle* h = nullptr;
   // FP32 with pinned per-time arrays: upload them in time chunks that
@@ -1170,14 +1239,16 @@ int dsmc_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
   if (dp) CU(cudaMemcpyAsync(out->paths, dp, (size_t)K * N * d * sizeof(double), cudaMemcpyDeviceToHost, s));
   if (dm && !overlap) CU(cudaMemcpyAsync(out->mean, dm, (size_t)K * d * sizeof(double), cudaMemcpyDeviceToHost, s));
   if (dc && !overlap) CU(cudaMemcpyAsync(out->cov, dc, (size_t)K * d * d * sizeof(double), cudaMemcpyDeviceToHost, s));
-  if (out->pair_left && T > 0) {
+  if (out->pair_left && T > 0)
     CU(cudaMemcpyAsync(out->pair_left, res.PL, (size_t)T * N * 4, cudaMemcpyDeviceToHost, s));
+  if (out->pair_right && T > 0)
     CU(cudaMemcpyAsync(out->pair_right, res.PR, (size_t)T * N * 4, cudaMemcpyDeviceToHost, s));
-  }
   if (out->log_mean_weight && T > 0)
     CU(cudaMemcpyAsync(out->log_mean_weight, res.LMW, (size_t)T * 8, cudaMemcpyDeviceToHost, s));
-  if (out->leaf_states && res.X64 && opts->precision == DSMC_FP64_PARITY)
+  if (out->leaf_states && res.X64)
     CU(cudaMemcpyAsync(out->leaf_states, res.X64, (size_t)K * N * d * 8, cudaMemcpyDeviceToHost, s));
+  if (out->leaf_logw && res.LW64)
+    CU(cudaMemcpyAsync(out->leaf_logw, res.LW64, (size_t)K * N * 8, cudaMemcpyDeviceToHost, s));
   double lnc;
   unsigned long long evals = 0;
   CU(cudaMemcpyAsync(&lnc, res.root_lnc, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1200,15 +1271,24 @@ int dsmc_smooth_resident(dsmc_ctx* ctx, const dsmc_model_handle* hc,
   if (!ctx || !hc || !opts) return DSMC_E_INVALID_ARGUMENT;
   auto* h = const_cast<dsmc_model_handle*>(hc);
   const int K = h->K, d = h->d;
-  if (ctx->last_K < K || ctx->last_d != d) {
+  // capacity is kept apart from the shape of the last run: a smaller run after
+  // a larger one reuses the buffers, and dsmc_resident_results copies exactly
+  // the last run's K x d (never the capacity)
+  if (ctx->mean_cap < (size_t)K * d || ctx->cov_cap < (size_t)K * d * d) {
+    cudaStreamSynchronize(ctx->stream);
     if (ctx->d_mean) cudaFree(ctx->d_mean);
     if (ctx->d_cov) cudaFree(ctx->d_cov);
+    ctx->d_mean = ctx->d_cov = nullptr;
+    ctx->mean_cap = ctx->cov_cap = 0;
     CU(cudaMalloc(&ctx->d_mean, (size_t)K * d * sizeof(double)));
     CU(cudaMalloc(&ctx->d_cov, (size_t)K * d * d * sizeof(double)));
-    ctx->last_K = K;
-    ctx->last_d = d;
+    ctx->mean_cap = (size_t)K * d;
+    ctx->cov_cap = (size_t)K * d * d;
     ++ctx->arena.epoch;  // moved outputs invalidate a captured graph
   }
+  ctx->last_K = K;
+  ctx->last_d = d;
+  ctx->last_err_K = K;
   auto& gc = ctx->gc;
   const bool same = gc.handle == h->id && gc.epoch == ctx->arena.epoch && gc.N == opts->n_particles &&
                     gc.rs == opts->resampler && gc.prec == opts->precision &&
@@ -1223,6 +1303,7 @@ int dsmc_smooth_resident(dsmc_ctx* ctx, const dsmc_model_handle* hc,
     kp.extra = nullptr;
     CU(cudaGraphExecKernelNodeSetParams(gc.exec, gc.seed_node, &kp));
     CU(cudaGraphLaunch(gc.exec, ctx->stream));
+    ctx->last_err = gc.err;  // the replay resets and fills the same record
     ctx->launches += gc.launches;
     ctx->kev_used = gc.kev_used;
     ctx->time_kernels = true;
@@ -1232,6 +1313,7 @@ int dsmc_smooth_resident(dsmc_ctx* ctx, const dsmc_model_handle* hc,
   auto run = [&](RunResult& res) -> int {
     int rc = smooth_common(ctx, h, opts, nullptr, ctx->d_mean, ctx->d_cov, &res, true);
     if (rc) return rc;
+    ctx->last_err = res.err;
     CU(cudaMemcpyAsync(ctx->h_lnc, res.root_lnc, sizeof(double), cudaMemcpyDeviceToHost,
                        ctx->stream));
     return DSMC_OK;
@@ -1274,6 +1356,7 @@ int dsmc_smooth_resident(dsmc_ctx* ctx, const dsmc_model_handle* hc,
       gc.seed_node = seed_node;
       gc.seed_params = seed_params;
       gc.launches = ctx->launches - l0;
+      gc.err = res.err;
       gc.kev_used = ctx->kev_used;
       gc.levels = res.levels;
       ctx->launches = l0;
@@ -1311,6 +1394,9 @@ int dsmc_smooth_resident(dsmc_ctx* ctx, const dsmc_model_handle* hc,
 int dsmc_resident_results(dsmc_ctx* ctx, double* mean, double* cov,
                           double* lnc, int* has_lnc) {
   if (!ctx) return DSMC_E_INVALID_ARGUMENT;
+  if (!ctx->d_mean) return set_err(ctx, DSMC_E_LOGIC, "no resident run on this context");
+  int rc = check_pending_error(ctx);  // syncs; a failed run returns its error, not garbage
+  if (rc) return rc;
   const int K = ctx->last_K, d = ctx->last_d;
   if (mean) CU(cudaMemcpyAsync(mean, ctx->d_mean, (size_t)K * d * 8, cudaMemcpyDeviceToHost, ctx->stream));
   if (cov) CU(cudaMemcpyAsync(cov, ctx->d_cov, (size_t)K * d * d * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1978,7 +2064,11 @@ int dsmc_window_run(dsmc_ctx* ctx, const dsmc_model_handle* hc, const dsmc_windo
   CU(cudaMemcpyAsync(p, &wo->seed, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
   o.seeds = (const uint64_t*)p;
   RunResult res;
-  return run_tree(ctx, h, o, &res);
+  int rc = run_tree(ctx, h, o, &res);
+  if (rc) return rc;
+  ctx->last_err = res.err;  // checked at the next host sync (boundary log Z, dsmc_sync)
+  ctx->last_err_K = h->K;
+  return DSMC_OK;
 }
 
 int dsmc_window_boundary(dsmc_ctx* ctx, int side, void* d_x, float* d_col, double* root_lnc) {
@@ -1998,6 +2088,8 @@ int dsmc_window_boundary(dsmc_ctx* ctx, int side, void* d_x, float* d_col, doubl
   if (root_lnc) {
     CU(cudaMemcpyAsync(ctx->h_lnc, st.blnc[st.cur], 8, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
+    int rc = check_pending_error(ctx);
+    if (rc) return rc;
     *root_lnc = ctx->h_lnc[0];
   }
   return DSMC_OK;
@@ -2224,20 +2316,17 @@ extern "C" int dsmc_ffbs_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
   const int pt = std::min(512, (N + 31) / 32 * 32);
   const size_t smf = sizeof(double) * N;
   const size_t smb = sizeof(float4) * N + sizeof(float) * ((N + 1) & ~1) + sizeof(double) * N;
-  if (smb > 227 * 1024) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "ffbs: N too large");
+  if (smb > (size_t)ctx->smem_optin || smf > (size_t)ctx->smem_optin)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "ffbs: N too large");
 #define FFBS_RUN(DD)                                                                          \
   do {                                                                                        \
     leaf32_kernel<DD><<<dim3(K, 1), lt, 0, ctx->stream>>>(b, raw0);                           \
     LAUNCHED(ctx);                                                                            \
     leafnorm32_kernel<<<1, 32, 0, ctx->stream>>>(b, raw0);                                    \
     LAUNCHED(ctx);                                                                            \
-    CU(cudaFuncSetAttribute(pf_forward_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                            (int)smf));                                                       \
     pf_forward_kernel<DD><<<1, pt, smf, ctx->stream>>>(b, LW, ANC,                            \
                                                        opts->resampler == DSMC_SYSTEMATIC, dll); \
     LAUNCHED(ctx);                                                                            \
-    CU(cudaFuncSetAttribute(ffbs_backward_kernel<DD>,                                         \
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));          \
     ffbs_backward_kernel<DD><<<(M + 7) / 8, 256, smb, ctx->stream>>>(b, LW, M, P);            \
     LAUNCHED(ctx);                                                                            \
     ffbs_moments_kernel<DD><<<(K + 7) / 8, 256, 0, ctx->stream>>>(b, P, M, dmean, dcov,        \

@@ -166,7 +166,8 @@ class Engine:
     def smooth(self, model, n_particles, resampler=abi.MULTINOMIAL, seed=0,
                precision=abi.FP32, mh_steps=16, inject_states=None,
                inject_logw=None, want_paths=False, want_moments=True,
-               want_pairs=False, want_leaves=False, mean_out=None, cov_out=None):
+               want_pairs=False, want_leaves=False, mean_out=None, cov_out=None,
+               want_leaf_logw=False):
         """run_smoother (smoother.hpp:128-129) on the GPU; host in/out.
         mean_out / cov_out: optional preallocated (e.g. pinned) host arrays of
         shape (K, d) / (K, d, d) that receive the moments."""
@@ -183,13 +184,15 @@ class Engine:
         pr = np.zeros((max(T, 1), N), np.uint32) if want_pairs else None
         lmw = np.zeros(max(T, 1)) if want_pairs else None
         leaves = np.zeros((K, N, d)) if want_leaves else None
+        leaf_lw = np.zeros((K, N)) if want_leaf_logw else None
         out = abi.SmoothOut(abi.dptr(paths), abi.dptr(mean), abi.dptr(cov),
                             abi.u32ptr(pl), abi.u32ptr(pr), abi.dptr(lmw),
-                            abi.dptr(leaves), None)
+                            abi.dptr(leaves), abi.dptr(leaf_lw))
         self._check(self.lib.dsmc_smooth(self.ctx, C.byref(model.desc), C.byref(opts), C.byref(out)))
         res.update(paths=paths, mean=mean, cov=cov,
                    pair_left=None if pl is None else pl[:T], pair_right=None if pr is None else pr[:T],
                    log_mean_weight=None if lmw is None else lmw[:T], leaves=leaves,
+                   leaf_logw=leaf_lw,
                    log_norm_const=out.log_norm_const if out.has_log_norm_const else None,
                    levels=out.levels, weight_evals=out.weight_evals,
                    biased=bool(out.biased), wall_time_ms=out.wall_time_ms)

@@ -29,10 +29,14 @@ def _lgssm(T, d, dy, m0, P0, F, b, Q, H, R, y, prop_mean=None, prop_cov=None,
     return m
 
 
-def with_rts_proposals(model, inflation=1.0):
-    """Replace the proposals by the exact smoothing marginals (x inflation)."""
-    from .dsmc import kalman_smooth
-    mean, cov, _ = kalman_smooth(model)
+def with_rts_proposals(model, inflation=1.0, smoother=None):
+    """Replace the proposals by the exact smoothing marginals (x inflation).
+    smoother: model -> (means, covs, loglik); default the engine's host RTS
+    (dsmc_kalman_smooth). bench.py's reference arm passes the oracle's so its
+    process never maps the product library."""
+    if smoother is None:
+        from .dsmc import kalman_smooth as smoother
+    mean, cov, _ = smoother(model)
     A = dict(model.arrays)
     A["prop_mean"] = mean
     A["prop_cov"] = cov * inflation
@@ -42,7 +46,7 @@ def with_rts_proposals(model, inflation=1.0):
 
 def lgssm_check(T, coef=0.9, shift=0.0, trans_var=0.25, init_mean=0.0,
                 init_var=1.0, obs_var=0.25, data_seed=90210, ys=None,
-                inflation=1.0):
+                inflation=1.0, smoother=None):
     """C1 (experiment.hpp:20-27, experiment.cpp:367-381)."""
     K = T + 1
     if ys is None:
@@ -54,7 +58,7 @@ def lgssm_check(T, coef=0.9, shift=0.0, trans_var=0.25, init_mean=0.0,
         ys = x + np.sqrt(obs_var) * rng.standard_normal(K)
     m = _lgssm(T, 1, 1, [init_mean], [[init_var]], [coef], [shift], [trans_var],
                [1.0], [obs_var], np.asarray(ys, float).reshape(K, 1))
-    return with_rts_proposals(m, inflation)
+    return with_rts_proposals(m, inflation, smoother)
 
 
 def ar1(ys, rho=0.8, q=0.3, r=0.4):
@@ -76,7 +80,7 @@ def cv_matrices(q=0.05, r=0.3, dt=1.0):
     return F, Q, H, R
 
 
-def cv_tracking(T, q=0.05, r=0.3, data_seed=90210, inflation=1.0):
+def cv_tracking(T, q=0.05, r=0.3, data_seed=90210, inflation=1.0, smoother=None):
     """C2 / C5: x = (p_x, p_y, v_x, v_y), white-noise acceleration."""
     K = T + 1
     F, Q, H, R = cv_matrices(q, r)
@@ -92,7 +96,7 @@ def cv_tracking(T, q=0.05, r=0.3, data_seed=90210, inflation=1.0):
     x = np.hstack([p, v])
     y = x[:, :2] + np.sqrt(r) * rng.standard_normal((K, 2))
     m = _lgssm(T, 4, 2, np.zeros(4), np.eye(4), F, np.zeros(4), Q, H, R, y)
-    return with_rts_proposals(m, inflation)
+    return with_rts_proposals(m, inflation, smoother)
 
 
 def sv(T, mu=-1.0, phi=0.95, sigma=0.3, data_seed=90210, ys=None):

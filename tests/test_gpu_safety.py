@@ -99,3 +99,72 @@ def test_conditional_sweep_context_history(engine):
         fresh.close()
     assert np.array_equal(a["paths"], b["paths"])
     assert np.array_equal(a["changed"], b["changed"])
+
+
+def test_resident_results_follow_the_last_run_not_the_capacity():
+    """A resident run with a smaller K after a larger one: the results copy
+    exactly the last run's (K, d) / (K, d, d) (the copy used the
+    allocation size) and equal the same run through dsmc_smooth."""
+    e = Engine(0)
+    try:
+        big, small = models.cv_tracking(511), models.lgssm_check(40)
+        hb = e.upload(big)
+        e.smooth_resident(hb, 256, seed=3)
+        e.sync()
+        hs = e.upload(small)
+        e.smooth_resident(hs, 64, seed=9)
+        K, d = small.horizon + 1, small.d
+        mbuf, mean = _guarded((K, d))
+        cbuf, cov = _guarded((K, d, d))
+        import ctypes as C
+        lnc, has = C.c_double(), C.c_int()
+        e._check(e.lib.dsmc_resident_results(e.ctx, abi.dptr(mean), abi.dptr(cov),
+                                             C.byref(lnc), C.byref(has)))
+        assert (mbuf[K * d:] == SENTINEL).all() and (cbuf[K * d * d:] == SENTINEL).all()
+        ref = e.smooth(small, 64, seed=9)
+        assert np.array_equal(mean, ref["mean"]) and np.array_equal(cov, ref["cov"])
+        e.free_model(hb)
+        e.free_model(hs)
+    finally:
+        e.close()
+
+
+def test_resident_run_reports_device_errors():
+    """A NaN leaf weight raised on the device during a resident run surfaces
+    at the next host synchronisation (dsmc_resident_results / dsmc_sync)
+    instead of returning DSMC_OK with garbage moments."""
+    m = models.lgssm_check(31)
+    A = dict(m.arrays)
+    y = np.array(A["y"])
+    y[0, 0] = np.nan
+    A["y"] = y
+    bad = abi.Model(m.kind, m.horizon, m.d, m.dy, **A)
+    e = Engine(0)
+    try:
+        h = e.upload(bad)
+        e.smooth_resident(h, 64, seed=1)  # enqueues, returns OK
+        with pytest.raises(ArithmeticError, match="NaN"):
+            e.resident_results(32, 1)
+        e.smooth_resident(h, 64, seed=2)
+        with pytest.raises(ArithmeticError, match="NaN"):
+            e.sync()
+        e.free_model(h)
+        good = e.upload(m)  # the context stays usable
+        e.smooth_resident(good, 64, seed=1)
+        mean, cov, lnc = e.resident_results(32, 1)
+        assert np.isfinite(mean).all()
+        e.free_model(good)
+    finally:
+        e.close()
+
+
+def test_leaf_outputs_fp64_only(engine):
+    m = models.lgssm_check(9)
+    r = engine.smooth(m, 16, seed=4, precision=abi.FP64_PARITY, want_leaves=True,
+                      want_leaf_logw=True)
+    lw = r["leaf_logw"]
+    # normalised per leaf (BlockEstimate::log_w): logsumexp == 0
+    mx = lw.max(1, keepdims=True)
+    assert np.allclose(np.log(np.exp(lw - mx).sum(1)) + mx[:, 0], 0.0, atol=1e-12)
+    with pytest.raises(ValueError, match="FP64"):
+        engine.smooth(m, 16, seed=4, precision=abi.FP32, want_leaf_logw=True)
