@@ -204,6 +204,11 @@ class Reference(_Base):
         L.ref_trace_smoother.argtypes = [M, _sz, _i, _sz, _u64, _dp, _u32p, _u32p, _dp, _dp, _ip]
         L.ref_run_conditional.argtypes = [M, _dp, _sz, _i, _u64, _u32, _dp, _dp, _ip, _u64p]
         L.ref_conditional_leaf.argtypes = [M, _i, _sz, _u64, _u32, _dp, _dp, _dp]
+        L.ref_run_injected.argtypes = [M, _sz, _i, _sz, _u64, _i, _dp, _dp, _dp, _u32p, _u32p,
+                                       _dp, _dp, _ip, _u64p, _ip, _ip]
+        L.ref_leaf_weights_all.argtypes = [M, _dp, _sz, _dp]
+        L.ref_make_leaves_all.argtypes = [M, _sz, _u64, _i, _dp, _dp]
+        L.ref_conditional_leaves_all.argtypes = [M, _sz, _u64, _u32, _dp, _dp]
         self._philox = L.ref_philox
         self._stream = L.ref_stream
         self._resample = L.ref_resample_table
@@ -243,6 +248,54 @@ class Reference(_Base):
         return dict(paths=paths, log_norm_const=lnc.value if has.value else None,
                     weight_evals=ev.value, levels=lev.value, biased=bool(biased.value),
                     wall_time_ms=wall.value)
+
+    def run_injected(self, model, n, states, raw_logw=None, resampler=abi.MULTINOMIAL, seed=0,
+                     mh_steps=16, threads=None, want_pairs=True, want_paths=True):
+        """run_smoother on injected leaves (ref_run_injected), multithreaded."""
+        K, d, T = model.horizon + 1, model.d, model.horizon
+        X = np.ascontiguousarray(states, np.float64)
+        W = None if raw_logw is None else np.ascontiguousarray(raw_logw, np.float64)
+        assert X.shape == (K, n, d)
+        paths = np.zeros((K, n, d)) if want_paths else None
+        pl = np.zeros((max(T, 1), n), np.uint32) if want_pairs else None
+        pr = np.zeros((max(T, 1), n), np.uint32) if want_pairs else None
+        lmw = np.zeros(max(T, 1)) if want_pairs else None
+        lnc, has, ev, lev, bi = C.c_double(), C.c_int(), C.c_uint64(), C.c_int(), C.c_int()
+        threads = threads or len(os.sched_getaffinity(0))
+        self._check(self.L.ref_run_injected(
+            C.byref(model.desc), n, resampler, mh_steps, seed, threads, abi.dptr(X), abi.dptr(W),
+            abi.dptr(paths), abi.u32ptr(pl), abi.u32ptr(pr), abi.dptr(lmw), C.byref(lnc),
+            C.byref(has), C.byref(ev), C.byref(lev), C.byref(bi)))
+        return dict(paths=paths, pair_left=None if pl is None else pl[:T],
+                    pair_right=None if pr is None else pr[:T],
+                    log_mean_weight=None if lmw is None else lmw[:T],
+                    log_norm_const=lnc.value if has.value else None, weight_evals=ev.value,
+                    levels=lev.value, biased=bool(bi.value))
+
+    def leaves_all(self, model, n, seed, threads=None):
+        """make_leaf for every t (multithreaded): states (K, n, d), raw weights (K, n)."""
+        K, d = model.horizon + 1, model.d
+        X, W = np.zeros((K, n, d)), np.zeros((K, n))
+        threads = threads or len(os.sched_getaffinity(0))
+        self._check(self.L.ref_make_leaves_all(C.byref(model.desc), n, seed, threads,
+                                               abi.dptr(X), abi.dptr(W)))
+        return X, W
+
+    def conditional_leaves_all(self, model, ref, n, seed, sweep):
+        K, d = model.horizon + 1, model.d
+        ref = np.ascontiguousarray(ref, np.float64).reshape(K, d)
+        X = np.zeros((K, n, d))
+        self._check(self.L.ref_conditional_leaves_all(C.byref(model.desc), n, seed, sweep,
+                                                      abi.dptr(ref), abi.dptr(X)))
+        return X
+
+    def leaf_weights(self, model, states):
+        """leaf_weights (fk_model.cpp:101-112) for every time: raw (T+1) x n."""
+        X = np.ascontiguousarray(states, np.float64)
+        K, n = X.shape[:2]
+        W = np.zeros((K, n))
+        self._check(self.L.ref_leaf_weights_all(C.byref(model.desc), abi.dptr(X), n, abi.dptr(W)))
+        return W
 
     def trace_smoother(self, model, n, resampler=abi.MULTINOMIAL, seed=0, mh_steps=16):
         K, d, T = model.horizon + 1, model.d, model.horizon

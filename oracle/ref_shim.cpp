@@ -11,6 +11,10 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <atomic>
+#include <mutex>
+#include <exception>
 #include <vector>
 
 #include "dsmc/conditional.hpp"
@@ -68,6 +72,53 @@ dsmc::PairWeightSource table_source(const double* logw, std::size_t n,
   };
   if (has_bound) src.log_upper_bound = bound;
   return src;
+}
+
+// The reference model with injected leaves: proposal_sampler copies the
+// given time-t slab (n states) instead of drawing, and, when raw weights are
+// given, init_weight_batch returns them (leaf_weights, fk_model.cpp:101-112);
+// otherwise the model's own weight callbacks run on the injected states.
+dsmc::FeynmanKacModel injected(const dsmc::FeynmanKacModel& base, const double* X,
+                               const double* W, std::size_t n) {
+  dsmc::FeynmanKacModel m = base;
+  const int d = base.state_dim;
+  m.proposal_sampler = [X, n, d](int t, std::size_t count, dsmc::RngStream&, double* out) {
+    if (count != n) throw std::logic_error("injected leaves: unexpected draw count");
+    std::memcpy(out, X + static_cast<std::size_t>(t) * n * d, sizeof(double) * n * d);
+  };
+  if (W)
+    m.init_weight_batch = [W, n](int t, const double*, std::size_t count, double* out) {
+      if (count != n) throw std::logic_error("injected weights: unexpected count");
+      std::memcpy(out, W + static_cast<std::size_t>(t) * n, sizeof(double) * n);
+    };
+  return m;
+}
+
+// parallel_for over [0, count) with a shared cursor (smoother.cpp:21-49)
+void par_for(std::size_t count, int threads, const std::function<void(std::size_t)>& fn) {
+  if (threads <= 1 || count <= 1) {
+    for (std::size_t i = 0; i < count; ++i) fn(i);
+    return;
+  }
+  std::atomic<std::size_t> cursor{0};
+  std::mutex mu;
+  std::exception_ptr err;
+  auto body = [&] {
+    for (;;) {
+      const std::size_t i = cursor.fetch_add(1);
+      if (i >= count) return;
+      try {
+        fn(i);
+      } catch (...) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!err) err = std::current_exception();
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int w = 0; w < threads && (std::size_t)w < count; ++w) pool.emplace_back(body);
+  for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
 }
 
 }  // namespace
@@ -292,6 +343,138 @@ int ref_trace_smoother(const dsmc_model_desc* desc, size_t n, int resampler,
                 sizeof(double) * root.paths.size());
     *has_lnc = root.log_norm_const.has_value() ? 1 : 0;
     *lnc = root.log_norm_const.value_or(NAN);
+  });
+}
+
+// run_smoother on INJECTED leaves (states, optional raw weights): with no
+// pair outputs this is run_smoother itself on the wrapped model; with pair
+// outputs the level loop of run_smoother (smoother.cpp:236-262) runs here,
+// multithreaded: the reference's make_pair_source + resample_pairs with the
+// key combine_blocks uses, recorded, then the combined block assembled from
+// those pairs exactly as combine_blocks does (tests/test_oracle.py checks the
+// root against run_smoother's).
+int ref_run_injected(const dsmc_model_desc* desc, size_t n, int resampler, size_t mh_steps,
+                     uint64_t seed, int threads, const double* inj_x, const double* inj_w,
+                     double* root_paths, uint32_t* pair_left, uint32_t* pair_right,
+                     double* pair_lmw, double* lnc, int* has_lnc, uint64_t* evals,
+                     int* levels, int* biased) {
+  return guarded([&] {
+    auto base = oracle::build_model(*desc);
+    auto model = injected(base, inj_x, inj_w, n);
+    dsmc::SmootherOptions o;
+    o.n_particles = n;
+    o.resampler = static_cast<dsmc::Resampler>(resampler);
+    o.mh_steps = mh_steps;
+    o.seed = seed;
+    o.n_threads = threads;
+    if (!pair_left) {
+      auto res = dsmc::run_smoother(model, o);
+      if (root_paths)
+        std::memcpy(root_paths, res.root.paths.data(), sizeof(double) * res.root.paths.size());
+      *has_lnc = res.meta.log_norm_const.has_value() ? 1 : 0;
+      *lnc = res.meta.log_norm_const.value_or(NAN);
+      *evals = res.meta.weight_evals;
+      *levels = res.meta.levels;
+      *biased = res.meta.biased ? 1 : 0;
+      return;
+    }
+    const int T = model.horizon;
+    std::vector<dsmc::BlockEstimate> cur(T + 1);
+    par_for(T + 1, threads, [&](std::size_t t) { cur[t] = dsmc::make_leaf(model, (int)t, n, seed); });
+    int level = 0;
+    size_t cursor = 0;
+    while (cur.size() > 1) {
+      ++level;
+      const size_t np = cur.size() / 2;
+      std::vector<dsmc::BlockEstimate> next(np + cur.size() % 2);
+      par_for(np, threads, [&](std::size_t k) {
+        const auto& L = cur[2 * k];
+        const auto& R = cur[2 * k + 1];
+        auto bundle = dsmc::make_pair_source(model, L, R);
+        auto ps = dsmc::resample_pairs(o.resampler, bundle.source, n, o.mh_steps,
+                                       key_of(seed, level, k, DSMC_ROLE_PAIR_RESAMPLE));
+        std::memcpy(pair_left + (cursor + k) * n, ps.left.data(), sizeof(uint32_t) * n);
+        std::memcpy(pair_right + (cursor + k) * n, ps.right.data(), sizeof(uint32_t) * n);
+        if (pair_lmw) pair_lmw[cursor + k] = ps.log_mean_weight.value_or(NAN);
+        // the block combine_blocks (smoother.cpp:182-224) builds from these
+        // same pairs: every time slab gathered by (left, right), uniform
+        // weights, summed evals, log Z += log mean weight + log_shift
+        dsmc::BlockEstimate out;
+        out.a = L.a;
+        out.b = R.b;
+        out.n = n;
+        out.dim = L.dim;
+        out.paths.resize(static_cast<std::size_t>(out.len()) * n * out.dim);
+        for (int t = L.a; t <= L.b; ++t)
+          for (std::size_t p = 0; p < n; ++p)
+            std::memcpy(out.time_slab(t) + p * out.dim,
+                        L.time_slab(t) + static_cast<std::size_t>(ps.left[p]) * out.dim,
+                        sizeof(double) * out.dim);
+        for (int t = R.a; t <= R.b; ++t)
+          for (std::size_t p = 0; p < n; ++p)
+            std::memcpy(out.time_slab(t) + p * out.dim,
+                        R.time_slab(t) + static_cast<std::size_t>(ps.right[p]) * out.dim,
+                        sizeof(double) * out.dim);
+        out.log_w.assign(n, -std::log(static_cast<double>(n)));
+        out.weights_uniform = true;
+        out.biased = L.biased || R.biased || ps.biased;
+        out.weight_evals = L.weight_evals + R.weight_evals + ps.weight_evals;
+        if (L.log_norm_const && R.log_norm_const && ps.log_mean_weight)
+          out.log_norm_const = *L.log_norm_const + *R.log_norm_const + *ps.log_mean_weight +
+                               bundle.log_shift;
+        next[k] = std::move(out);
+      });
+      if (cur.size() % 2) next.back() = std::move(cur.back());
+      cursor += np;
+      cur = std::move(next);
+    }
+    const auto& root = cur.front();
+    if (root_paths) std::memcpy(root_paths, root.paths.data(), sizeof(double) * root.paths.size());
+    *has_lnc = root.log_norm_const.has_value() ? 1 : 0;
+    *lnc = root.log_norm_const.value_or(NAN);
+    *evals = root.weight_evals;
+    *levels = level;
+    *biased = root.biased ? 1 : 0;
+  });
+}
+
+// leaf_weights (fk_model.cpp:101-112) of every time slab: raw log weights of
+// given states, (T+1) x n.
+int ref_leaf_weights_all(const dsmc_model_desc* desc, const double* X, size_t n, double* W) {
+  return guarded([&] {
+    auto model = oracle::build_model(*desc);
+    const int d = model.state_dim;
+    for (int t = 0; t <= model.horizon; ++t)
+      dsmc::leaf_weights(model, t, X + (size_t)t * n * d, n, W + (size_t)t * n);
+  });
+}
+
+// make_leaf (smoother.cpp:98-130) for every time, multithreaded: states and
+// raw leaf weights (T+1) x n (x d).
+int ref_make_leaves_all(const dsmc_model_desc* desc, size_t n, uint64_t seed, int threads,
+                        double* X, double* raw) {
+  return guarded([&] {
+    auto model = oracle::build_model(*desc);
+    const int d = model.state_dim;
+    par_for(model.horizon + 1, threads, [&](std::size_t t) {
+      auto blk = dsmc::make_leaf(model, (int)t, n, seed);
+      std::memcpy(X + t * n * d, blk.paths.data(), sizeof(double) * n * d);
+      dsmc::leaf_weights(model, (int)t, blk.paths.data(), n, raw + t * n);
+    });
+  });
+}
+
+// conditional_leaf (conditional.cpp:52-87) for every time: (T+1) x n x d
+// states, slot 0 = the reference path.
+int ref_conditional_leaves_all(const dsmc_model_desc* desc, size_t n, uint64_t seed,
+                               uint32_t sweep, const double* star, double* X) {
+  return guarded([&] {
+    auto model = oracle::build_model(*desc);
+    const int d = model.state_dim;
+    for (int t = 0; t <= model.horizon; ++t) {
+      auto blk = dsmc::conditional_leaf(model, t, n, seed, sweep, star + (size_t)t * d);
+      std::memcpy(X + (size_t)t * n * d, blk.paths.data(), sizeof(double) * n * d);
+    }
   });
 }
 

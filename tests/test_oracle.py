@@ -122,3 +122,48 @@ def test_oracle_matches_compiled_reference_fresh(oracle, reference):
         b = reference.run_smoother(m, 29, 0, seed=seed)
         assert np.array_equal(a["paths"], b["paths"])
         assert a["log_norm_const"] == b["log_norm_const"]
+
+
+@pytest.mark.parametrize("kind,N,rs", [("cv", 40, abi.MULTINOMIAL), ("sv", 50, abi.MH_LAZY),
+                                       ("crw", 64, abi.REJECTION_LAZY),
+                                       ("lg", 9, abi.SYSTEMATIC)])
+def test_reference_injected_runner(reference, kind, N, rs):
+    """ref_run_injected (the full-size parity runner of
+    tests/test_gpu_baseline_parity.py): replaying the reference's own leaves
+    reproduces its level-by-level trace (pairs) and run_smoother's root, log Z,
+    evals and bias flag."""
+    from oracle.py import Oracle
+    from paper_2202_02264_b200 import models
+    m = {"cv": lambda: models.cv_tracking(63, smoother=Oracle().kalman_smooth),
+         "sv": lambda: models.sv(77), "crw": lambda: models.constrained_rw(50),
+         "lg": lambda: models.lgssm_check(6, smoother=Oracle().kalman_smooth)}[kind]()
+    lv = reference.leaves(m, N, 7)
+    X, W = reference.leaves_all(m, N, 7)
+    assert np.array_equal(X, lv["states"]) and np.array_equal(W, lv["raw_logw"])
+    assert np.array_equal(reference.leaf_weights(m, X), W)
+    a = reference.trace_smoother(m, N, rs, seed=7, mh_steps=4)
+    b = reference.run_injected(m, N, X, W, rs, seed=7, mh_steps=4, threads=3)
+    c = reference.run_injected(m, N, X, None, rs, seed=7, mh_steps=4, want_pairs=False)
+    s = reference.run_smoother(m, N, rs, seed=7, mh_steps=4)
+    assert np.array_equal(a["pair_left"], b["pair_left"])
+    assert np.array_equal(a["pair_right"], b["pair_right"])
+    for r in (b, c):
+        assert np.array_equal(r["paths"], s["paths"])
+        assert r["log_norm_const"] == s["log_norm_const"]
+        assert r["weight_evals"] == s["weight_evals"] and r["biased"] == s["biased"]
+
+
+def test_oracle_kalman_matches_numpy():
+    """or_kalman_smooth (the reference arm's RTS, kalman.cpp:78-138) against
+    the independent numpy restatement."""
+    from oracle.py import Oracle
+    from paper_2202_02264_b200 import models
+    from tests.test_abi import numpy_rts
+    O = Oracle()
+    for m in (models.cv_tracking(200, smoother=O.kalman_smooth),
+              models.lgssm_check(100, smoother=O.kalman_smooth)):
+        a, P, ll = O.kalman_smooth(m)
+        b, Q = numpy_rts(m)
+        assert np.allclose(a, b, rtol=1e-10, atol=1e-10) and np.allclose(P, Q, rtol=1e-10,
+                                                                           atol=1e-12)
+        assert np.isfinite(ll)
