@@ -434,7 +434,7 @@ template <int MC, int D>
 int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
                int systematic) {
   const size_t sm = smem_cols64(b.N, D);
-  if (sm > (size_t)ctx->smem_optin)
+  if (sm > (size_t)ctx->smem_optin - 1024)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
                    "FP64 parity combine: N * (d + 2) doubles exceed the shared-memory "
                    "column stage (N <= " + std::to_string(ctx->smem_optin / (8 * (D + 2))) +
@@ -490,7 +490,7 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
                      sizeof(double) * ((ns + 1) & ~(size_t)1) + 16 * ns + 8 * ns +
                      sizeof(int) * (32 + nsub);
   const bool sample4 = sm2 <= 48 * 1024;
-  if (sm2 > (size_t)ctx->smem_optin)
+  if (sm2 > (size_t)ctx->smem_optin - 1024)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
                    "FP32 dense combine: N too large for the shared-memory sampler (use a lazy "
                    "resampler)");
@@ -1012,12 +1012,21 @@ struct DevSeeds {
 // opt-in maximum, under a lock — never per launch (a per-launch
 // cudaFuncSetAttribute with a level-dependent size races with other host
 // threads and could lower a limit another thread's launch needs).
+// dynamic limit = opt-in maximum minus the kernel's static shared memory
+template <typename F>
+cudaError_t set_max_dynamic_smem(F fn, int optin) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              optin - (int)fa.sharedSizeBytes);
+}
 template <int D>
 cudaError_t configure_d(int smem) {
   cudaError_t e = cudaSuccess;
   auto set = [&](auto fn) {
     if (e != cudaSuccess) return;
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    e = set_max_dynamic_smem(fn, smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
@@ -1042,12 +1051,12 @@ cudaError_t configure_device(int device, int smem) {
   for (auto fn : {c64_rows<kLG1, 1>, c64_rows<kSV, 1>, c64_rows<kCOX, 1>, c64_rows<kCRW, 1>,
                   c64_rows<kTHETA, 1>}) {
     if (e != cudaSuccess) break;
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    e = set_max_dynamic_smem(fn, smem);
   }
   for (auto fn : {c64_sample<kLG1, 1>, c64_sample<kSV, 1>, c64_sample<kCOX, 1>,
                   c64_sample<kCRW, 1>, c64_sample<kTHETA, 1>}) {
     if (e != cudaSuccess) break;
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    e = set_max_dynamic_smem(fn, smem);
   }
   if (e == cudaSuccess) done.push_back(device);
   return e;
@@ -2316,7 +2325,7 @@ extern "C" int dsmc_ffbs_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
   const int pt = std::min(512, (N + 31) / 32 * 32);
   const size_t smf = sizeof(double) * N;
   const size_t smb = sizeof(float4) * N + sizeof(float) * ((N + 1) & ~1) + sizeof(double) * N;
-  if (smb > (size_t)ctx->smem_optin || smf > (size_t)ctx->smem_optin)
+  if (smb > (size_t)ctx->smem_optin - 1024 || smf > (size_t)ctx->smem_optin - 1024)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "ffbs: N too large");
 #define FFBS_RUN(DD)                                                                          \
   do {                                                                                        \

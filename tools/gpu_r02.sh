@@ -6,9 +6,9 @@ mkdir -p gpurun_out/r02
 O=gpurun_out/r02
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $O/smi.txt 2>&1
 nproc >> $O/smi.txt; lscpu | grep "Model name" >> $O/smi.txt
-timeout 1200 python -m pytest tests -m gpu -q ${PYTEST_ARGS} > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; rc=$?; echo "smoke rc=$rc" >> $O/smoke.log
+[ $rc -ne 0 ] && { echo "smoke failed; stopping"; exit 1; }
+timeout 1800 python -m pytest tests -m gpu -q --timeout 600 ${PYTEST_ARGS} > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 900 python bench.py > $O/bench_c5.json 2> $O/bench_c5.err
-timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err
 timeout 900 python tools/c5_law.py c5 16 > $O/c5_law.jsonl 2> $O/c5_law.err
 echo done
