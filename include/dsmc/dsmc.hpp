@@ -23,6 +23,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <vector>
 
 #include "dsmc_b200.h"
@@ -76,10 +77,45 @@ class RngStream {
   double cached_ = 0.0;
 };
 
+// --------------------------------------------------------- metrics.hpp
+// Process-wide counters of the memory/work contracts (metrics.hpp:10-26,
+// metrics.cpp): stitch-weight evaluations, dense N^2 pair tables, the peak
+// transient of the lazy samplers. The device dense combine evaluates its
+// N x N table once, streaming (only N^2/64 sub-block sums are stored), and is
+// counted here as one dense table of N^2 elements, as the reference counts
+// its materialised table; lazy combines count none.
+namespace metrics {
+struct Snapshot {
+  std::uint64_t weight_evals = 0;
+  std::uint64_t dense_allocs = 0;
+  std::uint64_t dense_max_elems = 0;
+  std::uint64_t lazy_max_elems = 0;
+};
+void reset();
+Snapshot snapshot();
+void add_weight_evals(std::uint64_t n);
+void count_dense_alloc(std::size_t elems);
+void note_lazy_alloc(std::size_t elems);
+}  // namespace metrics
+
+// --------------------------------------------------------- kernels.hpp
+// The reference dispatches its FP64 row kernels over scalar / AVX2 /
+// AVX-512 backends that agree bit for bit (test_kernels.cpp). The device
+// engine has one arithmetic, the scalar backend's operation order (FP64
+// parity path); the selector is kept for source compatibility and records
+// the caller's choice without changing any result.
+namespace kernels {
+enum class Backend { scalar, avx2, avx512 };
+Backend active();
+void set_active(Backend b);
+bool available(Backend b);
+inline constexpr std::size_t kSubBlock = 64;  // kernels.hpp:77
+}  // namespace kernels
+
 // ------------------------------------------------------ resampling.hpp
 enum class Resampler { multinomial, systematic, mh_lazy, rejection_lazy };
 
-std::optional<Resampler> parse_resampler(const std::string& name);
+std::optional<Resampler> parse_resampler(std::string_view name);
 std::string resampler_name(Resampler r);
 bool resampler_is_lazy(Resampler r);
 
@@ -90,12 +126,60 @@ struct PairSample {
   bool biased = false;
 };
 
-// resample_pairs (resampling.hpp:85-87) for a dense table source
-// (n x n row-major log weights; log_upper_bound for rejection).
+namespace detail {
+struct BlockPairSource;  // device attachment of make_pair_source (below)
+}
+
+// resampling.hpp:21-31: a virtual n x n table of log pair weights.
+// fill_row / log_weight_at / log_upper_bound are the reference's fields.
+// `blocks` is set by make_pair_source for a device model: resample_pairs then
+// evaluates and samples the table on the device from the two blocks'
+// boundary slabs (never materialising it); sources built by the caller from
+// host callbacks are evaluated on the host (that is where the callbacks
+// live) and sampled on the device: the dense schemes upload the filled
+// table, the lazy schemes answer the device's per-round probes.
+struct PairWeightSource {
+  std::size_t n = 0;
+  std::function<void(std::size_t i, double* out)> fill_row;
+  std::function<double(std::size_t i, std::size_t j)> log_weight_at;
+  std::optional<double> log_upper_bound;
+  std::shared_ptr<const detail::BlockPairSource> blocks;
+};
+
+// resampling.hpp:44-65, 85-87.
+PairSample multinomial_pairs(const PairWeightSource& src, std::size_t n_out,
+                             const StreamKey& key);
+PairSample systematic_pairs(const PairWeightSource& src, std::size_t n_out,
+                            const StreamKey& key);
+PairSample mh_lazy_pairs(const PairWeightSource& src, std::size_t n_out,
+                         std::size_t mh_steps, const StreamKey& key);
+PairSample rejection_lazy_pairs(const PairWeightSource& src, std::size_t n_out,
+                                const StreamKey& key);
+PairSample resample_pairs(Resampler r, const PairWeightSource& src,
+                          std::size_t n_out, std::size_t mh_steps,
+                          const StreamKey& key);
+
+// resample_pairs for a dense table (n x n row-major log weights;
+// log_upper_bound for rejection): the reference tests' table source.
 PairSample resample_pairs(Resampler r, const std::vector<double>& logw,
                           std::size_t n, std::size_t n_out,
                           std::size_t mh_steps, const StreamKey& key,
                           std::optional<double> log_upper_bound = {});
+
+// resampling.hpp:67-83: single-population resampling for sequential filters.
+struct IndexSample {
+  std::vector<std::uint32_t> idx;
+  double log_mean_weight = 0.0;  // log((1/n) sum_i exp(logw[i]))
+};
+IndexSample multinomial_indices(const double* log_w, std::size_t n,
+                                std::size_t n_out, const StreamKey& key);
+IndexSample systematic_indices(const double* log_w, std::size_t n,
+                               std::size_t n_out, const StreamKey& key);
+IndexSample resample_indices(Resampler r, const double* log_w, std::size_t n,
+                             std::size_t n_out, const StreamKey& key);
+// resampling.hpp:91: a glibc malloc tuning of the reference's dense buffers;
+// nothing to tune here (no host N^2 buffers on the device path).
+void tune_allocator_once();
 
 // ------------------------------------------------------- kalman.hpp
 struct LinearGaussianModel {
@@ -145,24 +229,54 @@ IteratedSmoothResult iterated_smooth(const NonlinearGaussianModel& m, int iterat
 // ------------------------------------------------------ fk_model.hpp
 struct DeviceModel;  // owning storage behind a dsmc_model_desc
 
+// fk_model.hpp:25-35. StitchRowFn fills one row of log omega_c(x_prev, .)
+// against the right slab bound by the factory; the shipped header declares a
+// fused (x_prev, log_add, out) -> row_max form, while every reference .cpp
+// and test uses this (x_prev, out) form, which is the one
+// kept here so reference sources compile against this header.
+using StitchRowFn = std::function<void(const double* x_prev, double* out)>;
+using TransitionRowFn = std::function<void(const double* x_cur, double* out)>;
+
+// fk_model.hpp:37-86: every field of the reference, plus `device`, the
+// plain-data description the kernels run (std::function cannot run on a
+// GPU). The model factories below fill both; a model with callbacks only is
+// accepted by the host helpers (log_init_weight, make_stitch_row, ...) and
+// rejected by the device entry points (there is no CPU fallback).
 struct FeynmanKacModel {
   int state_dim = 1;
   int horizon = 0;
-  // the reference's callbacks (host-side validation / scalar checks)
+  std::function<void(int t, std::size_t count, RngStream& stream, double* out)>
+      proposal_sampler;
   std::function<double(int t, const double* x)> proposal_logdensity;
   std::function<double(int t, const double* x)> aux_logdensity;
   std::function<double(int t, const double* x)> log_potential;
   std::function<double(int t, const double* x_prev, const double* x_cur)>
       transition_logdensity;
   std::function<double(const double* x)> init_logdensity;
+  std::function<void(int t, const double* x_prev, RngStream& stream, double* out)>
+      transition_sampler;
+  std::function<StitchRowFn(int c, const double* right_particles, std::size_t n)>
+      stitch_row_factory;
+  std::function<void(int t, const double* particles, std::size_t n, double* out)>
+      init_weight_batch;
   std::function<double(int c)> log_stitch_bound;
+  std::function<TransitionRowFn(int t, const double* prev_particles, std::size_t n)>
+      transition_row_factory;
   // what the GPU runs
   std::shared_ptr<DeviceModel> device;
 };
 
 void validate_model(const FeynmanKacModel& model);
+// fk_model.hpp:96-116 / fk_model.cpp:43-112 (host, over the callbacks)
+double log_init_weight(const FeynmanKacModel& model, int t, const double* x);
 double log_stitch_weight(const FeynmanKacModel& model, int c,
                          const double* x_prev, const double* x_cur);
+StitchRowFn make_stitch_row(const FeynmanKacModel& model, int c,
+                            const double* right_particles, std::size_t n);
+TransitionRowFn make_transition_row(const FeynmanKacModel& model, int t,
+                                    const double* prev_particles, std::size_t n);
+void leaf_weights(const FeynmanKacModel& model, int t, const double* particles,
+                  std::size_t n, double* out);
 
 struct ProposalMarginal {
   std::vector<double> mean, cov;  // d, d*d
@@ -252,6 +366,9 @@ struct BlockEstimate {
   const double* time_slab(int t) const {
     return paths.data() + static_cast<std::size_t>(t - a) * n * dim;
   }
+  double* time_slab(int t) {
+    return paths.data() + static_cast<std::size_t>(t - a) * n * dim;
+  }
 };
 
 struct RunMetadata {
@@ -281,6 +398,27 @@ struct CombineSchedule {
 };
 CombineSchedule build_schedule(int horizon);
 int reference_tree_depth(int horizon);
+
+// smoother.hpp:98-125, on the device (FP64, the reference's arithmetic):
+// make_leaf draws and weighs one leaf; make_pair_source returns the
+// reference's virtual pair table of two adjacent blocks (host closures over
+// the model callbacks, plus the device attachment resample_pairs uses);
+// combine_blocks resamples n pairs on the device and concatenates the
+// selected paths. Blocks hold full paths, as the reference's.
+BlockEstimate make_leaf(const FeynmanKacModel& model, int t, std::size_t n,
+                        std::uint64_t seed);
+struct PairSourceBundle {
+  PairWeightSource source;
+  double log_shift = 0.0;
+};
+PairSourceBundle make_pair_source(const FeynmanKacModel& model,
+                                  const BlockEstimate& left,
+                                  const BlockEstimate& right);
+BlockEstimate combine_blocks(const FeynmanKacModel& model,
+                             const BlockEstimate& left,
+                             const BlockEstimate& right,
+                             const SmootherOptions& options, int level,
+                             int node);
 
 RunResult run_smoother(const FeynmanKacModel& model,
                        const SmootherOptions& options);

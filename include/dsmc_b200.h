@@ -252,6 +252,77 @@ DSMC_API int dsmc_philox_blocks(dsmc_ctx* ctx, const uint64_t ctr[4],
 DSMC_API int dsmc_exp_w(dsmc_ctx* ctx, const double* x, size_t n, double* out);
 
 /* ------------------------------------------------------------------------
+ * The reference's piecewise smoother API on the device (FP64, the
+ * reference's operation order), for callers that stitch blocks themselves.
+ *
+ * dsmc_make_leaf replaces make_leaf(model, t, n, seed) (smoother.hpp:101-102,
+ * smoother.cpp:98-130): n proposal draws from stream {seed, 0, t,
+ * leaf_proposal} (states n*d), the normalised log weights (n), the
+ * weights_uniform flag and the leaf's log normalising constant.
+ *
+ * dsmc_resample_blocks replaces resample_pairs(r, make_pair_source(model, L,
+ * R).source, n_out, mh_steps, key) (resampling.hpp:85-87, smoother.hpp:
+ * 109-116, smoother.cpp:132-180) for two adjacent blocks: the caller passes
+ * L's terminal slab, R's initial slab and the blocks' normalised log weights
+ * (NULL or *_uniform = 1 for a uniform block, whose weights stay out of the
+ * table); the table logw[i][j] = log omega_cut(xL_i, xR_j) + lwL_i + lwR_j is
+ * evaluated on the device (never materialised for the lazy samplers) and
+ * sampled with key {seed, level, node, pair_resample}. n_out <= n.
+ * log_mean_weight excludes the uniform sides' log_shift, as the reference. */
+typedef struct dsmc_pair_blocks {
+  int cut;                    /* R.a = L.b + 1, 1..T */
+  size_t n;                   /* particles per block */
+  const double* left_states;  /* n*d: L's slab at time cut - 1 */
+  const double* left_logw;    /* n normalised, or NULL (uniform) */
+  int left_uniform;
+  const double* right_states; /* n*d: R's slab at time cut */
+  const double* right_logw;
+  int right_uniform;
+} dsmc_pair_blocks;
+
+DSMC_API int dsmc_make_leaf(dsmc_ctx* ctx, const dsmc_model_desc* model, int t, size_t n,
+                            uint64_t seed, double* states, double* logw,
+                            int* weights_uniform, double* log_norm_const);
+DSMC_API int dsmc_resample_blocks(dsmc_ctx* ctx, const dsmc_model_desc* model,
+                                  const dsmc_pair_blocks* blocks, int resampler,
+                                  size_t n_out, size_t mh_steps, uint64_t seed,
+                                  uint32_t level, uint64_t node, uint32_t* left,
+                                  uint32_t* right, double* lmw, int* has_lmw,
+                                  uint64_t* weight_evals, int* biased);
+
+/* Single-population resampling: multinomial_indices / systematic_indices
+ * (resampling.hpp:69-80, resampling.cpp:360-460) of n_out draws from the
+ * categorical of n unnormalised log weights, stream {seed, level, node,
+ * role}. Returns the indices plus max_i logw and the exp_row_store total
+ * sum_i exp_w(logw_i - max), so log_mean_weight = max + log(total) - log n
+ * (taken on the host with the C library's log). DSMC_E_RUNTIME when every
+ * weight is zero, DSMC_E_DOMAIN on NaN. */
+DSMC_API int dsmc_resample_indices(dsmc_ctx* ctx, int resampler, const double* logw, size_t n,
+                                   size_t n_out, uint64_t seed, uint32_t level, uint64_t node,
+                                   int role, uint32_t* idx, double* max_logw, double* total);
+
+/* Lazy pair resampling over a source only the caller can evaluate (host
+ * callbacks: PairWeightSource::log_weight_at): mh_lazy_pairs /
+ * rejection_lazy_pairs (resampling.hpp:56-65, resampling.cpp:233-324) with
+ * key {seed, level, node, pair_resample}. The device holds every slot's
+ * chain state and counter-addressed stream position; each round it emits the
+ * entries (i, j) its pending slots probe next, the caller evaluates them and
+ * answers with their log weights, until no probe is left:
+ *   dsmc_lazy_begin(...)               -> n_probes
+ *   while (n_probes) { dsmc_lazy_probes(i, j); evaluate;
+ *                      dsmc_lazy_answer(values) -> n_probes }
+ *   dsmc_lazy_finish(left, right, evals)
+ * The probes and their order of evaluation per slot are the reference's, so
+ * weight_evals matches its count. One sampling in flight per context. */
+DSMC_API int dsmc_lazy_begin(dsmc_ctx* ctx, int resampler, size_t n, size_t n_out,
+                             size_t mh_steps, int has_bound, double bound, uint64_t seed,
+                             uint32_t level, uint64_t node, size_t* n_probes);
+DSMC_API int dsmc_lazy_probes(dsmc_ctx* ctx, uint32_t* i, uint32_t* j);
+DSMC_API int dsmc_lazy_answer(dsmc_ctx* ctx, const double* values, size_t* n_probes);
+DSMC_API int dsmc_lazy_finish(dsmc_ctx* ctx, uint32_t* left, uint32_t* right,
+                              uint64_t* weight_evals);
+
+/* ------------------------------------------------------------------------
  * Conditional dSMC / particle Gibbs, batched over independent chains.
  * Replaces run_conditional(model, ref, ConditionalOptions, sweep)
  * (conditional.hpp:48-51) run for n_chains chains at once: chain c uses

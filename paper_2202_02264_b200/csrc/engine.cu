@@ -411,6 +411,14 @@ struct RunOpts {
   int len = -1;
   bool compose = true;
   const uint32_t* root_map = nullptr;  // device [B][N]
+  // block injection (dsmc_resample_blocks): the injected log weights are
+  // already normalised block weights with the given uniform flags and maxima
+  // (no leaf normalisation), and the combines use this stream key
+  const uint8_t* inj_uni = nullptr;    // host [K]
+  const double* inj_lwmax = nullptr;   // host [K]
+  int key_level = -1;                  // -1: the tree level
+  long long key_node = 0;
+  int n_out = -1;                      // slots per combine (-1: N, or N - 1 conditional)
 };
 
 struct RunResult {
@@ -726,8 +734,15 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     CU(flush_deferred(ctx, h));
     leaf64_kernel<<<dim3(K, (N + 127) / 128, B), 128, 0, ctx->stream>>>(b, dinj_x, dinj_lw);
     LAUNCHED(ctx);
-    leafnorm64_kernel<<<dim3(K, B), 32, 0, ctx->stream>>>(b);
-    LAUNCHED(ctx);
+    if (o.inj_uni) {  // normalised block weights: flags and maxima as given
+      CU(cudaMemcpyAsync(b.UNI, o.inj_uni, BK, cudaMemcpyHostToDevice, ctx->stream));
+      CU(cudaMemcpyAsync(b.LWMAX, o.inj_lwmax, BK * sizeof(double), cudaMemcpyHostToDevice,
+                         ctx->stream));
+      CU(cudaMemsetAsync(b.LNC, 0, BK * sizeof(double), ctx->stream));
+    } else {
+      leafnorm64_kernel<<<dim3(K, B), 32, 0, ctx->stream>>>(b);
+      LAUNCHED(ctx);
+    }
   } else {
     CU(A.get("RAW0", (size_t)B * N * sizeof(double), &p));
     const int lt = std::min(256, (N + 31) / 32 * 32);
@@ -806,11 +821,11 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     la.last_next = maps[2 * (1 - cur) + 1];
     la.blnc_prev = blnc[cur];
     la.blnc_next = blnc[1 - cur];
-    la.n_out = o.conditional ? N - 1 : N;
+    la.n_out = o.n_out >= 0 ? o.n_out : (o.conditional ? N - 1 : N);
     la.ws = ws;
     la.ws_comb = ws_comb;
-    la.key_level = level;
-    la.node_off = (long long)(o.t0 >> level);
+    la.key_level = o.key_level >= 0 ? o.key_level : level;
+    la.node_off = o.key_level >= 0 ? o.key_node : (long long)(o.t0 >> level);
     if (o.conditional) {
       la.k0 = 0;
       if (fp64) {
@@ -2364,3 +2379,7 @@ extern "C" int dsmc_ffbs_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
   if (log_likelihood) *log_likelihood = ll;
   return DSMC_OK;
 }
+
+// The reference's piecewise entry points (make_leaf, resample_pairs over a
+// block pair or a caller-evaluated source, index resampling).
+#include "pieces.cuh"

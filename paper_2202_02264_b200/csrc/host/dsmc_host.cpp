@@ -2,6 +2,7 @@
 // reference's dsmc:: entry points and exception classes; all numerical work
 // is delegated to the CUDA engine (libdsmc_b200.so).
 #include "dsmc/dsmc.hpp"
+#include "internal.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -12,29 +13,7 @@
 
 namespace dsmc {
 
-struct DeviceModel {
-  dsmc_model_desc desc{};
-  std::vector<double> m0, P0, F, b, Q, H, R, y, prop_mean, prop_cov;
-  std::vector<uint8_t> has_obs;
-  void bind() {
-    auto p = [](std::vector<double>& v) { return v.empty() ? nullptr : v.data(); };
-    desc.m0 = p(m0);
-    desc.P0 = p(P0);
-    desc.F = p(F);
-    desc.b = p(b);
-    desc.Q = p(Q);
-    desc.H = p(H);
-    desc.R = p(R);
-    desc.y = p(y);
-    desc.prop_mean = p(prop_mean);
-    desc.prop_cov = p(prop_cov);
-    desc.has_obs = has_obs.empty() ? nullptr : has_obs.data();
-  }
-};
-
-namespace {
-
-constexpr double kLog2Pi = 1.8378770664093454836;
+namespace detail {
 
 [[noreturn]] void throw_code(int code, const std::string& msg) {
   switch (code) {
@@ -66,9 +45,21 @@ const dsmc_model_desc& desc_of(const FeynmanKacModel& m) {
   if (!m.device)
     throw std::invalid_argument(
         "model has no device descriptor: the GPU engine runs model families "
-        "described by data (make_lgssm_fk, make_sv_model)");
+        "described by data (make_lgssm_fk, make_sv_model, make_cox_model, "
+        "make_constrained_rw, make_theta_logistic); there is no CPU fallback");
   return m.device->desc;
 }
+
+}  // namespace detail
+
+namespace {
+
+using detail::check;
+using detail::context;
+using detail::desc_of;
+using detail::throw_code;
+
+constexpr double kLog2Pi = 1.8378770664093454836;
 
 double log_normal_pdf(double x, double mean, double var) {
   const double d = x - mean;
@@ -95,10 +86,31 @@ double gauss_logpdf(const double* x, const double* m, const double* S, int d) {
   return -0.5 * (d * kLog2Pi + ld) - 0.5 * q;
 }
 
+// lower Cholesky factor of a d x d (d <= 4) covariance
+void chol4(const double* S, int d, double* L) {
+  for (int i = 0; i < d * d; ++i) L[i] = 0.0;
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double s = S[i * d + j];
+      for (int k = 0; k < j; ++k) s -= L[i * d + k] * L[j * d + k];
+      L[i * d + j] = i == j ? std::sqrt(s) : s / L[j * d + j];
+    }
+}
+// out = mu + L z, z ~ N(0, I) by fill_normal
+void affine_draw(const double* mu, const double* L, int d, RngStream& st, double* out) {
+  double z[4];
+  st.fill_normal(z, d);
+  for (int i = 0; i < d; ++i) {
+    double v = mu[i];
+    for (int k = 0; k <= i; ++k) v += L[i * d + k] * z[k];
+    out[i] = v;
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------ resampling
-std::optional<Resampler> parse_resampler(const std::string& name) {
+std::optional<Resampler> parse_resampler(std::string_view name) {
   if (name == "multinomial") return Resampler::multinomial;
   if (name == "systematic") return Resampler::systematic;
   if (name == "mh-lazy") return Resampler::mh_lazy;
@@ -137,6 +149,11 @@ PairSample resample_pairs(Resampler r, const std::vector<double>& logw,
   if (has) ps.log_mean_weight = lmw;
   ps.weight_evals = ev;
   ps.biased = biased != 0;
+  if (resampler_is_lazy(r))
+    metrics::note_lazy_alloc(2 * n_out);
+  else
+    metrics::count_dense_alloc(n * n);
+  metrics::add_weight_evals(ev);
   return ps;
 }
 
@@ -246,6 +263,24 @@ FeynmanKacModel make_lgssm_fk(const LinearGaussianModel& m,
     }
     return gauss_logpdf(xc, mu, &D->Q[(size_t)t * d * d], d);
   };
+  // host draws (the LinearGaussian draw of kalman.cpp:43-50: mean + chol(S) z,
+  // z by fill_normal); the device draws its own leaves from the same streams
+  fk.proposal_sampler = [D, d](int t, std::size_t count, RngStream& st, double* out) {
+    double L[16];
+    chol4(&D->prop_cov[(size_t)t * d * d], d, L);
+    for (std::size_t p = 0; p < count; ++p)
+      affine_draw(&D->prop_mean[(size_t)t * d], L, d, st, out + p * d);
+  };
+  fk.transition_sampler = [D, d](int t, const double* xp, RngStream& st, double* out) {
+    double L[16], mu[4];
+    chol4(&D->Q[(size_t)t * d * d], d, L);
+    for (int k = 0; k < d; ++k) {
+      double s = 0.0;
+      for (int l = 0; l < d; ++l) s += D->F[(size_t)t * d * d + k * d + l] * xp[l];
+      mu[k] = s + D->b[(size_t)t * d + k];
+    }
+    affine_draw(mu, L, d, st, out);
+  };
   return fk;
 }
 
@@ -285,6 +320,16 @@ FeynmanKacModel make_sv_model(const SvParams& p, const std::vector<double>& ys) 
   fk.log_stitch_bound = [D, p](int c) {
     return -0.5 * (kLog2Pi + std::log(p.sigma2)) - std::log(std::fabs(D->y[c]));
   };
+  fk.proposal_sampler = [D](int t, std::size_t count, RngStream& st, double* out) {
+    const double ly2 = std::log(D->y[t] * D->y[t]);
+    for (std::size_t q = 0; q < count; ++q) {
+      const double z = st.normal();
+      out[q] = ly2 - std::log(z * z);  // x = log y^2 - log z^2
+    }
+  };
+  fk.transition_sampler = [p](int, const double* xp, RngStream& st, double* out) {
+    *out = p.mu + p.phi * (*xp - p.mu) + std::sqrt(p.sigma2) * st.normal();
+  };
   return fk;
 }
 
@@ -320,6 +365,13 @@ FeynmanKacModel make_cox_model(const CoxParams& p, const std::vector<double>& ys
   fk.transition_logdensity = [a, b, p](int, const double* xp, const double* xc) {
     return log_normal_pdf(*xc, b + a * *xp, p.sigma2);
   };
+  fk.proposal_sampler = [sm, sv](int, std::size_t count, RngStream& st, double* out) {
+    const double sd = std::sqrt(sv);
+    for (std::size_t q = 0; q < count; ++q) out[q] = sm + sd * st.normal();
+  };
+  fk.transition_sampler = [a, b, p](int, const double* xp, RngStream& st, double* out) {
+    *out = b + a * *xp + std::sqrt(p.sigma2) * st.normal();
+  };
   return fk;
 }
 
@@ -349,6 +401,13 @@ FeynmanKacModel make_constrained_rw(double sigma, int horizon) {
     return log_normal_pdf(*xc, *xp, var);
   };
   fk.log_stitch_bound = [var, lhalf](int) { return -0.5 * (kLog2Pi + std::log(var)) - lhalf; };
+  fk.proposal_sampler = [](int, std::size_t count, RngStream& st, double* out) {
+    st.fill_uniform(out, count);  // U[-1, 1] (rng.cpp:95-97)
+    for (std::size_t q = 0; q < count; ++q) out[q] = 2.0 * out[q] - 1.0;
+  };
+  fk.transition_sampler = [sigma](int, const double* xp, RngStream& st, double* out) {
+    *out = *xp + sigma * st.normal();
+  };
   return fk;
 }
 
@@ -391,17 +450,41 @@ FeynmanKacModel make_theta_logistic(const ThetaLogisticParams& p, const std::vec
   fk.transition_logdensity = [drift, p](int, const double* xp, const double* xc) {
     return log_normal_pdf(*xc, drift(*xp), p.q2);
   };
+  fk.proposal_sampler = [D](int t, std::size_t count, RngStream& st, double* out) {
+    const double m = D->prop_mean[static_cast<std::size_t>(t)];
+    const double sd = std::sqrt(D->prop_cov[static_cast<std::size_t>(t)]);
+    for (std::size_t q = 0; q < count; ++q) out[q] = m + sd * st.normal();
+  };
+  fk.transition_sampler = [drift, p](int, const double* xp, RngStream& st, double* out) {
+    *out = drift(*xp) + std::sqrt(p.q2) * st.normal();
+  };
   return fk;
 }
 
 // -------------------------------------------------------------- fk_model
+// fk_model.cpp:26-40 (the reference's contract on the callbacks)
 void validate_model(const FeynmanKacModel& model) {
   if (model.state_dim < 1) throw std::invalid_argument("model: state_dim must be >= 1");
   if (model.horizon < 0) throw std::invalid_argument("model: horizon must be >= 0");
+  if (!model.proposal_sampler || !model.proposal_logdensity || !model.log_potential ||
+      !model.init_logdensity)
+    throw std::invalid_argument(
+        "model: proposal sampler/density, potential and initial density are required");
+  if (model.horizon >= 1 && (!model.aux_logdensity || !model.transition_logdensity))
+    throw std::invalid_argument(
+        "model: aux density and transition density are required for T >= 1");
+}
+
+namespace detail {
+// validate_model plus what the device needs: a descriptor that agrees
+const dsmc_model_desc& device_desc(const FeynmanKacModel& model) {
+  validate_model(model);
   const dsmc_model_desc& d = desc_of(model);
   if (d.horizon != model.horizon || d.state_dim != model.state_dim)
     throw std::invalid_argument("model: device descriptor disagrees with the callbacks");
+  return d;
 }
+}  // namespace detail
 
 // fk_model.cpp:61-73
 double log_stitch_weight(const FeynmanKacModel& model, int c, const double* x_prev,
@@ -447,8 +530,7 @@ int reference_tree_depth(int horizon) {
 }
 
 RunResult run_smoother(const FeynmanKacModel& model, const SmootherOptions& o) {
-  validate_model(model);
-  const dsmc_model_desc& desc = desc_of(model);
+  const dsmc_model_desc& desc = detail::device_desc(model);
   dsmc_ctx* c = context(o.device);
   const int T = model.horizon, K = T + 1, d = model.state_dim;
   const std::size_t N = o.n_particles;
@@ -481,6 +563,14 @@ RunResult run_smoother(const FeynmanKacModel& model, const SmootherOptions& o) {
   res.meta.log_norm_const = res.root.log_norm_const;
   res.meta.seed = o.seed;
   res.meta.biased = res.root.biased;
+  // metrics contract (metrics.hpp): one dense N x N table per dense combine
+  // (evaluated on the device, streaming), none for the lazy samplers
+  if (resampler_is_lazy(o.resampler)) {
+    if (T > 0) metrics::note_lazy_alloc(2 * N);
+  } else {
+    for (int k = 0; k < T; ++k) metrics::count_dense_alloc(N * N);
+  }
+  metrics::add_weight_evals(out.weight_evals);
   return res;
 }
 
@@ -506,7 +596,7 @@ void copy_path(const BlockEstimate& block, std::size_t p, double* out) {
 // ------------------------------------------------------------ conditional
 ConditionalResult run_conditional(const FeynmanKacModel& model, const double* ref,
                                   const ConditionalOptions& o, std::uint32_t sweep) {
-  validate_model(model);
+  detail::device_desc(model);
   if (o.resampler != Resampler::multinomial && o.resampler != Resampler::rejection_lazy)
     throw std::invalid_argument(
         "conditional sweeps need exchangeable unbiased slot draws: use the multinomial "
@@ -532,6 +622,13 @@ ConditionalResult run_conditional(const FeynmanKacModel& model, const double* re
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   if (!std::isnan(lnc)) r.meta.log_norm_const = lnc;
   r.meta.seed = o.seed;
+  if (resampler_is_lazy(o.resampler)) {
+    if (model.horizon > 0) metrics::note_lazy_alloc(2 * o.n_particles);
+  } else {
+    for (int k = 0; k < model.horizon; ++k)
+      metrics::count_dense_alloc(o.n_particles * o.n_particles);
+  }
+  metrics::add_weight_evals(ev);
   return r;
 }
 

@@ -63,15 +63,16 @@ __device__ inline uint64_t leaf_node(int t, int conditional, uint32_t sweep) {
 __global__ void leaf64_kernel(Bufs b, const double* inj_x, const double* inj_lw) {
   // grid (time, particle chunk, chain): time in x (up to 2^31 leaves)
   const int n = blockIdx.y * blockDim.x + threadIdx.x;
-  const int t = blockIdx.x, ch = blockIdx.z;
+  const int lt = blockIdx.x, ch = blockIdx.z;
+  const int t = b.t0 + lt;  // global time (stream key, model data); lt indexes the window
   if (n >= b.N) return;
   const DevModel& M = b.models[ch];
-  const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + t];
+  const TimeConst& tc = b.tc[(size_t)ch * b.Kt + t];
   const int d = b.d;
   double x[4] = {0, 0, 0, 0};
-  const size_t off = ((size_t)ch * b.K + t) * b.N + n;
+  const size_t off = ((size_t)ch * b.K + lt) * b.N + n;
   if (b.conditional && n == 0) {
-    for (int k = 0; k < d; ++k) x[k] = b.star[((size_t)ch * b.K + t) * d + k];
+    for (int k = 0; k < d; ++k) x[k] = b.star[((size_t)ch * b.K + lt) * d + k];
   } else if (inj_x) {
     for (int k = 0; k < d; ++k) x[k] = inj_x[off * d + k];
   } else {

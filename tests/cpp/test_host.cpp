@@ -567,6 +567,132 @@ TEST_CASE(theta_logistic_conjugate_only_chain_recovers_precisions) {
   CHECK(std::fabs(mr - 0.1514) < 0.15 * 0.1514);
 }
 
+// smoother.hpp:98-125: the piecewise API (make_leaf + combine_blocks in the
+// packed schedule, smoother.cpp:236-262) on the device reproduces
+// run_smoother's FP64 parity run bit for bit: same leaves, same stitches,
+// same root paths, evals and bias; log Z to rounding.
+static void piecewise_matches(const dsmc::FeynmanKacModel& model, std::size_t n,
+                              dsmc::Resampler rs) {
+  dsmc::SmootherOptions o;
+  o.n_particles = n;
+  o.resampler = rs;
+  o.mh_steps = 5;
+  o.seed = 4242;
+  o.precision = dsmc::Precision::fp64_parity;
+  auto ref = dsmc::run_smoother(model, o);
+  const int T = model.horizon;
+  std::vector<dsmc::BlockEstimate> cur;
+  for (int t = 0; t <= T; ++t) cur.push_back(dsmc::make_leaf(model, t, n, o.seed));
+  int level = 0;
+  while (cur.size() > 1) {
+    ++level;
+    std::vector<dsmc::BlockEstimate> next;
+    for (std::size_t k = 0; k + 1 < cur.size(); k += 2)
+      next.push_back(dsmc::combine_blocks(model, cur[k], cur[k + 1], o, level, (int)(k / 2)));
+    if (cur.size() % 2) next.push_back(cur.back());
+    cur.swap(next);
+  }
+  const auto& root = cur.front();
+  CHECK(level == ref.meta.levels);
+  CHECK(root.paths == ref.root.paths);
+  CHECK(root.weight_evals == ref.meta.weight_evals);
+  CHECK(root.biased == ref.meta.biased);
+  CHECK(root.log_norm_const.has_value() == ref.meta.log_norm_const.has_value());
+  if (root.log_norm_const && ref.meta.log_norm_const)
+    CHECK(std::fabs(*root.log_norm_const - *ref.meta.log_norm_const) <=
+          1e-12 * std::max(1.0, std::fabs(*ref.meta.log_norm_const)));
+}
+
+TEST_CASE(piecewise_make_leaf_and_combine_blocks_reproduce_run_smoother) {
+  piecewise_matches(ar1_fk(21), 37, dsmc::Resampler::multinomial);
+  piecewise_matches(ar1_fk(9), 24, dsmc::Resampler::systematic);
+  piecewise_matches(ar1_fk(12), 30, dsmc::Resampler::mh_lazy);
+  piecewise_matches(ar1_fk(10), 20, dsmc::Resampler::rejection_lazy);
+  std::vector<double> ys(16);
+  for (int t = 0; t < 16; ++t) ys[t] = 0.3 + 0.1 * ((t * 7) % 5);
+  piecewise_matches(dsmc::make_sv_model({-1.0, 0.9, 0.1}, ys), 40, dsmc::Resampler::mh_lazy);
+}
+
+// make_leaf (smoother.cpp:98-130): uniform iff min == max raw weight; the
+// log normalising constant is the leaf's mean raw weight; weights normalised
+TEST_CASE(make_leaf_normalises_and_flags_uniform_leaves) {
+  auto model = ar1_fk(5);
+  auto l0 = dsmc::make_leaf(model, 0, 50, 9);
+  auto l3 = dsmc::make_leaf(model, 3, 50, 9);
+  CHECK(!l0.weights_uniform);  // h0 * P0 / q0 varies
+  CHECK(l3.weights_uniform);   // nu = q at t >= 1
+  double lse = -INFINITY;
+  for (double v : l0.log_w) lse = std::max(lse, v);
+  double acc = 0;
+  for (double v : l0.log_w) acc += std::exp(v - lse);
+  CHECK(std::fabs(lse + std::log(acc)) < 1e-12);
+  CHECK(l0.a == 0 && l0.b == 0 && l0.n == 50 && l0.paths.size() == 50);
+  std::vector<double> raw(50);
+  dsmc::leaf_weights(model, 0, l0.paths.data(), 50, raw.data());
+  double m = -INFINITY;
+  for (double v : raw) m = std::max(m, v);
+  double s = 0;
+  for (double v : raw) s += std::exp(v - m);
+  CHECK(std::fabs(*l0.log_norm_const - (m + std::log(s) - std::log(50.0))) < 1e-9);
+  CHECK_THROWS_AS(dsmc::make_leaf(model, 6, 50, 9), std::invalid_argument);
+  CHECK_THROWS_AS(dsmc::make_leaf(model, 0, 0, 9), std::invalid_argument);
+}
+
+// make_pair_source (smoother.cpp:132-180): host closures over the callbacks,
+// the adjacency / size checks, log_shift and the rejection bound
+TEST_CASE(make_pair_source_closures_shift_and_bound) {
+  auto model = ar1_fk(7);
+  auto a = dsmc::make_leaf(model, 0, 16, 3), b = dsmc::make_leaf(model, 1, 16, 3);
+  auto c = dsmc::make_leaf(model, 2, 16, 3);
+  auto bundle = dsmc::make_pair_source(model, a, b);
+  CHECK(bundle.source.n == 16 && bundle.source.blocks != nullptr);
+  CHECK(std::fabs(bundle.log_shift + std::log(16.0)) < 1e-15);  // only b is uniform
+  std::vector<double> row(16);
+  bundle.source.fill_row(3, row.data());
+  for (std::size_t j = 0; j < 16; ++j)
+    CHECK(std::fabs(row[j] - bundle.source.log_weight_at(3, j)) < 1e-12);
+  CHECK_THROWS_AS(dsmc::make_pair_source(model, a, c), std::invalid_argument);
+  auto d = dsmc::make_leaf(model, 1, 8, 3);
+  CHECK_THROWS_AS(dsmc::make_pair_source(model, a, d), std::invalid_argument);
+  // the device samples the attached blocks; a host copy without the
+  // attachment samples the host-filled table: same law (log mean weight)
+  auto ps = dsmc::resample_pairs(dsmc::Resampler::multinomial, bundle.source, 16, 0,
+                                 {5, 1, 0, dsmc::StreamRole::pair_resample});
+  auto host = bundle.source;
+  host.blocks.reset();
+  auto ph = dsmc::resample_pairs(dsmc::Resampler::multinomial, host, 16, 0,
+                                 {5, 1, 0, dsmc::StreamRole::pair_resample});
+  CHECK(ps.log_mean_weight && ph.log_mean_weight);
+  CHECK(std::fabs(*ps.log_mean_weight - *ph.log_mean_weight) < 1e-9);
+}
+
+// test_smoother.cpp:416-433 + metrics.hpp: rejection stitching builds no
+// dense table, has no evidence estimate; dense stitching counts one N x N
+// table per combine
+TEST_CASE(rejection_stitching_does_no_dense_allocs) {
+  auto model = ar1_fk(11);
+  dsmc::metrics::reset();
+  dsmc::SmootherOptions o;
+  o.n_particles = 400;
+  o.resampler = dsmc::Resampler::rejection_lazy;
+  for (int r = 0; r < 3; ++r) {
+    o.seed = 700 + r;
+    auto res = dsmc::run_smoother(model, o);
+    CHECK(!res.meta.log_norm_const.has_value());
+  }
+  auto snap = dsmc::metrics::snapshot();
+  CHECK(snap.dense_allocs == 0);
+  CHECK(snap.weight_evals > 0);
+  CHECK(snap.lazy_max_elems <= 4 * 400);
+  dsmc::metrics::reset();
+  o.resampler = dsmc::Resampler::multinomial;
+  auto res = dsmc::run_smoother(model, o);
+  snap = dsmc::metrics::snapshot();
+  CHECK(snap.dense_allocs == 11);
+  CHECK(snap.dense_max_elems == 400u * 400u);
+  CHECK(snap.weight_evals == res.meta.weight_evals);
+}
+
 int main(int argc, char** argv) {
   const char* only = argc > 1 ? argv[1] : nullptr;
   int failed_cases = 0;

@@ -7,6 +7,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "tests", "cpp", "test_host")
+REFBIN = os.path.join(ROOT, "tests", "cpp", "_ref")
 HOSTLIB = os.path.join(ROOT, "paper_2202_02264_b200", "libdsmc_host.so")
 
 
@@ -21,5 +22,34 @@ def test_host_library_and_tests_are_built():
 @pytest.mark.gpu
 def test_host_api_cases_pass_on_gpu():
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def _ref_bin(name):
+    path = os.path.join(REFBIN, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not built (tests/cpp/Makefile needs /root/reference)")
+    return path
+
+
+@pytest.mark.parametrize("name", ["test_rng", "test_fk_model"])
+def test_reference_unit_tests_compile_and_pass_host_only(name):
+    """The reference's own test_rng.cpp / test_fk_model.cpp, compiled
+    unmodified against include/dsmc/*.hpp (tests/cpp/Makefile): host-side
+    parts of the API (Philox streams, the fk_model helpers, validate_model)."""
+    r = subprocess.run([_ref_bin(name)], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout.splitlines()[-1]
+
+
+@pytest.mark.gpu
+def test_reference_resampling_unit_tests_pass_on_gpu():
+    """The reference's test_resampling.cpp unmodified: every pair / index
+    sampler, the metrics contract (dense_allocs, lazy_max_elems), error
+    types — all on the device through libdsmc_host."""
+    r = subprocess.run([_ref_bin("test_resampling")], capture_output=True, text=True,
+                       timeout=900)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
