@@ -35,6 +35,7 @@ struct LevelArgs {
   size_t aux_comb;    // floats per combine in aux
   int tc_ncs;         // tensor-core pass 1: column splits per 128-row tile
   int tc_nk;          // ... and combines in this chunk (persistent work list)
+  int rt_ncs;         // FP32: pass-1 column splits that wrote row totals (0: none)
 };
 
 // Block meta derived from the schedule geometry.
@@ -200,7 +201,7 @@ __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
     double x[D];
 #pragma unroll
     for (int k = 0; k < d; ++k) x[k] = X[(size_t)p * d + k];
-    C.base[j] = col_base<MC, D>(M, tc, R.t, x);
+    C.base[j] = col_base<MC, D>(M, tc, b.t0 + R.t, x);  // global time (windows)
     if (MC == kLGN) {  // whitened column w = W_Q x
 #pragma unroll
       for (int k = 0; k < d; ++k) {
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(256) c64_rows(Bufs b, LevelArgs la) {
   double* ws = la.ws + ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * la.ws_comb;
   double *wm = ws, *wraw = ws + N, *wsub = ws + 5 * (size_t)N;
   const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
-  const double coef = row_coef<MC>(M, g.c);
+  const double coef = row_coef<MC>(M, b.t0 + g.c);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rows_per_cta = 32;
   const double* XL = b.X64 + ((size_t)ch * b.K + L.t) * N * d;
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(256) c64_rows(Bufs b, LevelArgs la) {
     const uint32_t p = map_last(b, la, ch, L, i);
     double xl[D], mu[D];
     for (int q = 0; q < d; ++q) xl[q] = XL[(size_t)p * d + q];
-    row_mean<MC, D>(M, tc, g.c, xl, mu);
+    row_mean<MC, D>(M, tc, b.t0 + g.c, xl, mu);
     const double sl = lnonuni ? b.LW64[((size_t)ch * b.K + L.t) * N + i] : 0.0;
     // max (reduce_max, kernels.cpp:26-36)
     double mx = -CUDART_INF;
@@ -374,7 +375,7 @@ __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
   __syncthreads();
   const double grand = s_grand;
   const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
-  const double coef = row_coef<MC>(M, g.c);
+  const double coef = row_coef<MC>(M, b.t0 + g.c);
   const int off = b.conditional ? 1 : 0;
   const uint64_t node = b.conditional
                             ? (static_cast<uint64_t>(static_cast<uint32_t>(k + la.node_off)) |
@@ -417,7 +418,7 @@ __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
     const uint32_t pl = map_last(b, la, ch, L, row);
     double xl[D], mu[D];
     for (int q = 0; q < d; ++q) xl[q] = XL[(size_t)pl * d + q];
-    row_mean<MC, D>(M, tc, g.c, xl, mu);
+    row_mean<MC, D>(M, tc, b.t0 + g.c, xl, mu);
     const double sl = lnonuni ? b.LW64[((size_t)ch * b.K + L.t) * N + row] : 0.0;
     const double mrow = wm[row];
     const int j0 = s * kSub, j1 = min(j0 + kSub, N);
@@ -499,7 +500,7 @@ __global__ void lazy64_kernel(Bufs b, LevelArgs la, int mh, size_t mh_steps) {
   P.b = &b;
   P.la = &la;
   P.ch = ch;
-  P.c = g.c;
+  P.c = b.t0 + g.c;  // global cut: model data
   P.d = b.d;
   P.L = L;
   P.R = R;
@@ -618,7 +619,7 @@ __global__ void refpair_check_kernel(Bufs b, LevelArgs la) {
   P.b = &b;
   P.la = &la;
   P.ch = ch;
-  P.c = g.c;
+  P.c = b.t0 + g.c;  // global cut: model data
   P.d = b.d;
   P.L = L;
   P.R = R;

@@ -502,7 +502,9 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
                    "FP32 dense combine: N too large for the shared-memory sampler (use a lazy "
                    "resampler)");
-  la.aux_comb = ((size_t)10 * N + 3) & ~(size_t)3;
+  const bool use_tc = ctx->pair_tc && D >= 2;
+  la.rt_ncs = use_tc ? 0 : ncs;  // the CUDA-core pass 1 writes per-split row totals
+  la.aux_comb = ((size_t)(10 + ncs) * N + 3) & ~(size_t)3;
   {
     void* p;
     CU(ctx->arena.get("AUX32", la.aux_comb * sizeof(float) * (size_t)nk * b.B, &p));
@@ -519,7 +521,6 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
     ctx->kev_used += 3;
     CU(rec_event(ev[0], ctx->stream));
   }
-  const bool use_tc = ctx->pair_tc && D >= 2;
   if (use_tc) {
     // tensor-core pass 1: 128-row tiles, 4 CTAs per SM (128 TMEM columns each)
     const int nrt_tc = (N + kTcRows - 1) / kTcRows;
