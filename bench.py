@@ -355,7 +355,9 @@ def run_ours(args, cfg, rank, world, device):
         if K % world or (K // world) < 2:
             raise SystemExit(f"K={K} does not split over {world} ranks")
         comm = TorchComm()
-        be = GpuBackend(eng, h, N, d, seed_base, rs, device)
+        # this rank's window (and its right cross cut) only
+        hw = eng.upload_window(model, rank * (K // world), K // world)
+        be = GpuBackend(eng, hw, N, d, seed_base, rs, device)
 
         def step(s):
             be.seed = seed_base + s
@@ -373,6 +375,8 @@ def run_ours(args, cfg, rank, world, device):
     value = K * N / (ms_max * 1e-3)
     # ---- end to end through the public API (host pinned in, host out)
     h2d = sum(a.nbytes for a in model.arrays.values() if a is not None)
+    if world > 1:  # each rank uploads its window's rows (+ one cut on each side)
+        h2d = int(h2d * min(1.0, (K // world + 2) / K))
     e2e_steps = max(3, min(args.steps, 10))
     if world == 1:
         d2h = K * d * 8 + K * d * d * 8 + 8
@@ -389,7 +393,7 @@ def run_ours(args, cfg, rank, world, device):
         cov_w = torch.empty((Kloc, d, d), dtype=torch.float64, pin_memory=True)
 
         def e2e_step(s):
-            hh = eng.upload(model)
+            hh = eng.upload_window(model, rank * Kloc, Kloc)
             b2 = GpuBackend(eng, hh, N, d, seed_base + 5000 + s, rs, device)
             out, lz = sharded_smooth({rank: b2}, comm, K, N, world)
             mean, cov = out[rank]

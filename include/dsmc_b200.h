@@ -372,33 +372,45 @@ DSMC_API int dsmc_sv_pgibbs_sweep(dsmc_ctx* ctx, int n_chains, int horizon,
  * (paper_2202_02264_b200/sharded.py) exchanges only boundary slabs, block
  * log Z and ancestor indices over NCCL for the top log2(P) levels.
  *
+ * Every stage only enqueues work on the context's stream (no host
+ * synchronisation); log Z values and indices stay in device memory, and
+ * device errors raised by any stage surface at the next dsmc_sync.
+ *
+ *   dsmc_model_upload_window  upload + prepare only the times a window
+ *                         [t0, t0+len) and its right cross cut t0+len need
  *   dsmc_window_run       leaves [t0, t0+len) + the len-local combine levels
  *   dsmc_window_boundary  slab of the window root's first (side 0: states +
- *                         column terms) or last (side 1) leaf, device out
+ *                         column terms) or last (side 1) leaf, and the root's
+ *                         log Z (d_root_lnc, one double), device out
  *   dsmc_cross_combine    one cross-window combine at cut `cut`, global
- *                         (level, node) stream key, on gathered slabs
+ *                         (level, node) stream key, on gathered slabs; any
+ *                         resampler (dense, MH-lazy, rejection-lazy); block
+ *                         log Z in / out as device doubles (NaN after lazy)
  *   dsmc_window_remap     root first (side 0) / last (side 1) map := map[idx]
  *   dsmc_window_finish    top-down composition from the window root's map
- *                         (NULL = identity) + per-time moments (device) */
+ *                         (device, NULL = identity) + per-time moments */
 typedef struct dsmc_window_opts {
   size_t n_particles;
-  int resampler;   /* dense (multinomial / systematic) for cross combines */
+  int resampler;
   size_t mh_steps;
   uint64_t seed;
   int t0;          /* first leaf; a multiple of len */
   int len;         /* leaves in the window; a power of two >= 2 */
 } dsmc_window_opts;
 
+DSMC_API int dsmc_model_upload_window(dsmc_ctx* ctx, const dsmc_model_desc* model, int t0,
+                                      int len, dsmc_model_handle** out);
 DSMC_API int dsmc_window_run(dsmc_ctx* ctx, const dsmc_model_handle* h,
                              const dsmc_window_opts* opts);
 DSMC_API int dsmc_window_boundary(dsmc_ctx* ctx, int side, void* d_states,
-                                  float* d_col, double* root_log_norm_const);
+                                  float* d_col, double* d_root_log_norm_const);
 DSMC_API int dsmc_cross_combine(dsmc_ctx* ctx, const dsmc_model_handle* h,
                                 const dsmc_window_opts* opts, int cut, int level,
                                 long long node, const void* d_left_states,
                                 const void* d_right_states, const float* d_right_col,
-                                double lnc_left, double lnc_right, uint32_t* d_left_idx,
-                                uint32_t* d_right_idx, double* lnc_out);
+                                const double* d_lnc_left, const double* d_lnc_right,
+                                uint32_t* d_left_idx, uint32_t* d_right_idx,
+                                double* d_lnc_out);
 DSMC_API int dsmc_window_remap(dsmc_ctx* ctx, int side, const uint32_t* d_idx);
 DSMC_API int dsmc_window_finish(dsmc_ctx* ctx, const uint32_t* d_root_map,
                                 double* d_mean, double* d_cov);

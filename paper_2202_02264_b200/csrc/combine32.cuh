@@ -152,11 +152,10 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 // per combine of the chunk): whitened columns y_j / A_j and rows u_i / B_i,
 // computed once by pass 1 instead of being re-gathered through the block maps.
 struct Aux32 {
-  float4* y;   // [N] column y_j (zero-padded to 4)
-  float4* u;   // [N] row u_i = 2 nu_i
-  float* A;    // [N] column A_j
-  float* B;    // [N] row B_i
-  float* RT;   // [rt_ncs][N] row log2-totals over each column split's sub-blocks
+  float4* y;  // [N] column y_j (zero-padded to 4)
+  float4* u;  // [N] row u_i = 2 nu_i
+  float* A;   // [N] column A_j
+  float* B;   // [N] row B_i
 };
 __device__ __forceinline__ Aux32 aux32(const LevelArgs& la, int comb, int N) {
   float* base = la.aux + (size_t)comb * la.aux_comb;
@@ -165,17 +164,8 @@ __device__ __forceinline__ Aux32 aux32(const LevelArgs& la, int comb, int N) {
   a.u = reinterpret_cast<float4*>(base + 4 * (size_t)N);
   a.A = base + 8 * (size_t)N;
   a.B = base + 9 * (size_t)N;
-  a.RT = base + 10 * (size_t)N;
   return a;
 }
-
-// Pass-1 sub-block sums are staged per round of kStageSub sub-blocks in
-// shared memory and stored ROW-MAJOR, ws[row * nsub + s]: the sampler's walk
-// then reads one row's nsub sums as contiguous vectors (64 B at N = 1024)
-// instead of nsub scattered sectors, and each row's log2-total over the
-// CTA's sub-blocks (online LSE at the flush) goes to Aux32::RT, so the
-// sampler never re-reads the N x nsub sums to build its row CDF.
-constexpr int kStageSub = 16;
 
 // Pass 1. Grid (row tiles x column splits, combines of the chunk, chains),
 // 256 threads: rows [256 rt, 256 rt + 256), sub-blocks [cs nsub / ncs,
@@ -190,8 +180,6 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) c32_pair(Bufs b, LevelArgs
   __shared__ float s_c[kRowsCTA];           // overflow shift c_i (0 for most rows)
   __shared__ float4 s_y[kPairWarps][kSub];  // per warp: the staged sub-block's y_j
   __shared__ float s_a[kPairWarps][kSub];   // ... and A_j - cmax_s
-  __shared__ float s_L[kStageSub][kRowsCTA];  // this round's sub-block sums L_is
-  __shared__ float s_rtm[kRowsCTA], s_rta[kRowsCTA];  // running row totals (max, sum)
   const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
   const int N = b.N;
   const int nsub = (N + kSub - 1) / kSub;
@@ -284,15 +272,7 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) c32_pair(Bufs b, LevelArgs
     NC[pr] = make_float2(-s_c[lane + 64 * pr], -s_c[lane + 64 * pr + 32]);
   }
   const float2 one2 = make_float2(1.f, 1.f);
-  // running row log2-totals (online LSE over the flushes) in shared memory,
-  // not registers: the sum loop needs every register it has
-  for (int r = threadIdx.x; r < kRowsCTA; r += 32 * kPairWarps) {
-    s_rtm[r] = -CUDART_INF_F;
-    s_rta[r] = 0.f;
-  }
-  for (int rs0 = sb0; rs0 < sb1; rs0 += kStageSub) {
-  const int rs1 = min(sb1, rs0 + kStageSub);
-  for (int sbk = rs0 + warp; sbk < rs1; sbk += kPairWarps) {
+  for (int sbk = sb0 + warp; sbk < sb1; sbk += kPairWarps) {
     // stage the sub-block's 64 columns (2 per lane), then prefetch the next
     float Ah[2], cm = -CUDART_INF_F;
     float4 xr_c[2] = {xr_n[0], xr_n[1]};
@@ -394,50 +374,10 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4) c32_pair(Bufs b, LevelArgs
         const float shift = D == 1 ? -((q & 1) ? NC[q >> 1].y : NC[q >> 1].x) : s_c[r];
         Ls = sq > 0.f ? lg2(sq) + shift + cm + s_b[r] : -CUDART_INF_F;
       }
-      s_L[sbk - rs0][r] = Ls;
+      ws[(size_t)sbk * N + row0 + r] = Ls;
     }
     __syncwarp();
   }
-  __syncthreads();
-  // flush the round: each thread owns rows threadIdx.x + 128 h; row-major
-  // stores (float4 when the round is 4-aligned), online LSE of the totals
-  const int nr = rs1 - rs0;
-#pragma unroll
-  for (int h = 0; h < RPT; ++h) {
-    const int r = threadIdx.x + h * 32 * kPairWarps;
-    if (r >= nrows) continue;
-    float v[kStageSub];
-    const float m0 = s_rtm[r];
-    float mx = m0;
-#pragma unroll
-    for (int q = 0; q < kStageSub; ++q) {
-      v[q] = q < nr ? s_L[q][r] : -CUDART_INF_F;
-      mx = fmaxf(mx, v[q]);
-    }
-    float* dst = ws + (size_t)(row0 + r) * nsub + rs0;
-    if (nr == kStageSub && (nsub & 3) == 0 && (rs0 & 3) == 0) {
-      float4* d4 = reinterpret_cast<float4*>(dst);
-#pragma unroll
-      for (int q = 0; q < kStageSub / 4; ++q)
-        d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    } else {
-#pragma unroll
-      for (int q = 0; q < kStageSub; ++q)
-        if (q < nr) dst[q] = v[q];
-    }
-    if (mx > -CUDART_INF_F) {
-      float acc = m0 > -CUDART_INF_F ? s_rta[r] * ex2(m0 - mx) : 0.f;
-#pragma unroll
-      for (int q = 0; q < kStageSub; ++q) acc += ex2(v[q] - mx);  // -inf -> 0
-      s_rtm[r] = mx;
-      s_rta[r] = acc;
-    }
-  }
-  __syncthreads();
-  }
-  for (int r = threadIdx.x; r < nrows; r += 32 * kPairWarps)
-    ax.RT[(size_t)cs * N + row0 + r] =
-        s_rtm[r] > -CUDART_INF_F ? s_rtm[r] + lg2(s_rta[r]) : -CUDART_INF_F;
 }
 
 // Block-wide inclusive scan of doubles (one value per thread).
@@ -512,25 +452,41 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
     P23[ps] = make_float4(ya.z, yb.z, ya.w, yb.w);
     AP[ps] = make_float2(Aa, Ab);
   }
-  // row log2-totals: pass 1's per-split totals (la.rt_ncs of them, online
-  // LSE), or — tensor-core pass 1 (la.rt_ncs == 0) — from the row's nsub
-  // sub-block sums (row-major: contiguous per row)
+  // row log2-totals: online LSE over the row's sub-block sums ([sub][row]
+  // layout: coalesced across the threads' rows), 16 sub-blocks per round,
+  // two rows in flight per thread
   float gm = -CUDART_INF_F;
-  const int nrt_src = la.rt_ncs > 0 ? la.rt_ncs : nsub;
-  for (int i = tid; i < N; i += blockDim.x) {
-    float m = -CUDART_INF_F, acc = 0.f;
-    for (int q = 0; q < nrt_src; ++q) {
-      const float v = la.rt_ncs > 0 ? ax.RT[(size_t)q * N + i] : ws[(size_t)i * nsub + q];
-      if (v == -CUDART_INF_F) continue;
-      if (v > m) {
-        acc = m == -CUDART_INF_F ? 0.f : acc * ex2(m - v);
-        m = v;
+  for (int i = tid; i < N; i += 2 * blockDim.x) {
+    const int i2 = i + blockDim.x;
+    float m[2] = {-CUDART_INF_F, -CUDART_INF_F}, acc[2] = {0.f, 0.f};
+    for (int s0 = 0; s0 < nsub; s0 += 16) {
+      float v[2][16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const bool in = s0 + q < nsub;
+        v[0][q] = in ? ws[(size_t)(s0 + q) * N + i] : -CUDART_INF_F;
+        v[1][q] = in && i2 < N ? ws[(size_t)(s0 + q) * N + i2] : -CUDART_INF_F;
       }
-      acc += ex2(v - m);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float cm = fmax3(fmax3(v[h][0], v[h][1], v[h][2]), fmax3(v[h][3], v[h][4], v[h][5]),
+                         fmax3(v[h][6], v[h][7], v[h][8]));
+        cm = fmax3(cm, fmax3(v[h][9], v[h][10], v[h][11]),
+                   fmax3(v[h][12], v[h][13], fmaxf(v[h][14], v[h][15])));
+        if (cm == -CUDART_INF_F) continue;
+        if (cm > m[h]) {
+          acc[h] = m[h] == -CUDART_INF_F ? 0.f : acc[h] * ex2(m[h] - cm);
+          m[h] = cm;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc[h] += ex2(v[h][q] - m[h]);
+      }
     }
-    const float La = m == -CUDART_INF_F ? -CUDART_INF_F : m + lg2(acc);
+    const float La = m[0] == -CUDART_INF_F ? -CUDART_INF_F : m[0] + lg2(acc[0]);
+    const float Lc = m[1] == -CUDART_INF_F ? -CUDART_INF_F : m[1] + lg2(acc[1]);
     Lrow[i] = La;
-    gm = fmaxf(gm, La);
+    if (i2 < N) Lrow[i2] = Lc;
+    gm = fmax3(gm, La, i2 < N ? Lc : -CUDART_INF_F);
   }
   for (int o = 16; o; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(~0u, gm, o));
   if (lane == 0) sh[warp] = gm;
@@ -649,26 +605,14 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
     const float local0 = (float)((pt - before) / (double)ex2(Li - G));
     const float local = local0 >= 0.f ? local0 : 0.f;
     // sub-block walk over the row's sub-block sums (relative to the row
-    // total), branch-free, 16 at a time from (vector) loads of the row
-    const float* w = ws + (size_t)i * nsub;  // sub-block s of row i at w[s]
-    const bool vec = (nsub & 3) == 0;
+    // total), branch-free, 16 at a time from vector loads
+    const float* w = ws + i;  // sub-block s of row i at w[s * N]
     int s = -1, last_pos = 0;
     float cum = 0.f, before_s = 0.f, wsel = 0.f, Ls_sel = 0.f;
     for (int s0 = 0; s0 < nsub; s0 += 16) {
       float v[16];
-      if (vec && s0 + 16 <= nsub) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 f = reinterpret_cast<const float4*>(w + s0)[q];
-          v[4 * q] = f.x;
-          v[4 * q + 1] = f.y;
-          v[4 * q + 2] = f.z;
-          v[4 * q + 3] = f.w;
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = (s0 + q < nsub) ? w[s0 + q] : -CUDART_INF_F;
-      }
+      for (int q = 0; q < 16; ++q) v[q] = (s0 + q < nsub) ? w[(size_t)(s0 + q) * N] : -CUDART_INF_F;
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const float e = (s0 + q < nsub) ? ex2(v[q] - Li) : 0.f;
@@ -684,7 +628,7 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
     }
     if (s < 0) {  // spill: clamp to the last positive sub-block
       s = last_pos;
-      Ls_sel = w[s];
+      Ls_sel = w[(size_t)s * N];
       wsel = ex2(Ls_sel - Li);
       before_s = cum - wsel;
     }

@@ -35,7 +35,6 @@ struct LevelArgs {
   size_t aux_comb;    // floats per combine in aux
   int tc_ncs;         // tensor-core pass 1: column splits per 128-row tile
   int tc_nk;          // ... and combines in this chunk (persistent work list)
-  int rt_ncs;         // FP32: pass-1 column splits that wrote row totals (0: none)
 };
 
 // Block meta derived from the schedule geometry.

@@ -61,6 +61,7 @@ struct dsmc_model_handle {
   int B = 1;
   dsmc_model_desc desc{};
   int K = 0, d = 1, dy = 1;
+  int t_lo = 0, t_hi = 0;  // prepared times (a window upload: [t0, t0 + len + 1))
   DevModel* models_dev = nullptr;  // [B]
   TimeConst* tc = nullptr;         // [B][K]
   int* bounded = nullptr;          // [B]
@@ -255,9 +256,31 @@ int upload(dsmc_ctx* ctx, dsmc_model_handle* h, const T* src, size_t n,
   return DSMC_OK;
 }
 
-// Upload B descriptors (same K, d) and run the prep kernel.
+// Per-time array restricted to times [lo, hi) (time-sharded windows): only
+// those rows are uploaded, and the device pointer is offset so kernels keep
+// indexing by GLOBAL time (rows outside the range are never read).
+template <class T>
+int upload_rows(dsmc_ctx* ctx, dsmc_model_handle* h, const T* src, size_t per_t, int lo, int hi,
+                const T** dst) {
+  if (!src || per_t == 0) {
+    *dst = nullptr;
+    return DSMC_OK;
+  }
+  void* p = nullptr;
+  const size_t n = (size_t)(hi - lo) * per_t;
+  CU(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), ctx->stream));
+  h->owned.push_back(p);
+  CU(cudaMemcpyAsync(p, src + (size_t)lo * per_t, n * sizeof(T), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  *dst = static_cast<const T*>(p) - (ptrdiff_t)((size_t)lo * per_t);
+  return DSMC_OK;
+}
+
+// Upload B descriptors (same K, d) and run the prep kernel. [w_lo, w_hi):
+// the times whose per-time constants are needed (default all); a window
+// handle uploads model rows [w_lo - 1, w_hi) and prepares only [w_lo, w_hi).
 int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
-                dsmc_model_handle** out, bool defer = false) {
+                dsmc_model_handle** out, bool defer = false, int w_lo = 0, int w_hi = -1) {
   for (int c = 0; c < B; ++c) {
     int rc = validate_desc(ctx, &descs[c]);
     if (rc) return rc;
@@ -276,6 +299,23 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
   h->K = K;
   h->d = d;
   h->dy = dy;
+  if (w_hi < 0) w_hi = K;
+  const bool window = w_lo > 0 || w_hi < K;
+  if (window && (B != 1 || w_lo < 0 || w_hi > K || w_lo >= w_hi))
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "window upload: need one model and 0 <= t0 < t1 <= K");
+  const int rlo = std::max(0, w_lo - 1), rhi = w_hi;  // model rows: the window + its left cut
+  h->t_lo = w_lo;
+  h->t_hi = w_hi;
+  if (window) h->defer = false;
+  // per-time array: the window's rows (offset pointer) or the whole horizon
+  auto per_time = [&](const auto* src, size_t per_t, auto** dst) -> int {
+    if (window) return upload_rows(ctx, h.get(), src, per_t, rlo, rhi, dst);
+    return upload(ctx, h.get(), src, src ? (size_t)K * per_t : 0, dst, per_t);
+  };
+  auto per_time_strided = [&](const double* src, int64_t stride, size_t per, const double** dst) -> int {
+    if (!stride) return upload(ctx, h.get(), src, per, dst);  // one matrix for every time
+    return per_time(src, (size_t)stride, dst);
+  };
   std::vector<DevModel> dm(B);
   for (int c = 0; c < B; ++c) {
     const dsmc_model_desc& m = descs[c];
@@ -311,8 +351,8 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
         for (int q = 0; q < 8; ++q) M.mp[q] = mp[q];
         std::vector<double> lg(nT);
         for (size_t t = 0; t < nT; ++t) lg[t] = std::lgamma(m.y[t] + 1.0);
-        rc |= upload(ctx, h.get(), m.y, nT, &M.y);
-        rc |= upload(ctx, h.get(), lg.data(), nT, &M.lgam);
+        rc |= per_time(m.y, 1, &M.y);
+        rc |= per_time(lg.data(), 1, &M.lgam);
         CU(cudaStreamSynchronize(ctx->stream));  // lg is a local host buffer
       } else {  // models.cpp:269-270
         const double sigma = m.par[0], var = sigma * sigma;
@@ -327,27 +367,26 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
                             -0.5 * (kLog2Pi + std::log(m.par[3])),
                             -0.5 * (kLog2Pi + std::log(m.par[4])), 0.0};
       for (int q = 0; q < 8; ++q) M.mp[q] = mp[q];
-      rc |= upload(ctx, h.get(), m.y, nT, &M.y, 1);
-      rc |= upload(ctx, h.get(), m.prop_mean, nT, &M.prop_mean, 1);
-      rc |= upload(ctx, h.get(), m.prop_cov, nT, &M.prop_cov, 1);
+      rc |= per_time(m.y, 1, &M.y);
+      rc |= per_time(m.prop_mean, 1, &M.prop_mean);
+      rc |= per_time(m.prop_cov, 1, &M.prop_cov);
     } else if (m.kind == DSMC_MODEL_SV) {
-      rc |= upload(ctx, h.get(), m.y, nT, &M.y);
+      rc |= per_time(m.y, 1, &M.y);
       M.has_obs = nullptr;
       M.prop_mean = M.prop_cov = M.F = M.b = M.Q = M.H = M.R = M.m0 = M.P0 = nullptr;
     } else {
-      auto span = [&](int64_t stride, size_t per) { return stride ? nT * stride : per; };
-      rc |= upload(ctx, h.get(), m.y, nT * dy, &M.y, (size_t)dy);
-      rc |= upload(ctx, h.get(), m.has_obs, m.has_obs ? nT : 0, &M.has_obs);
-      rc |= upload(ctx, h.get(), m.prop_mean, nT * d, &M.prop_mean, (size_t)d);
-      rc |= upload(ctx, h.get(), m.prop_cov, nT * d * d, &M.prop_cov, (size_t)d * d);
+      rc |= per_time(m.y, (size_t)dy, &M.y);
+      rc |= per_time(m.has_obs, 1, &M.has_obs);
+      rc |= per_time(m.prop_mean, (size_t)d, &M.prop_mean);
+      rc |= per_time(m.prop_cov, (size_t)d * d, &M.prop_cov);
       rc |= upload(ctx, h.get(), m.m0, (size_t)d, &M.m0);
       rc |= upload(ctx, h.get(), m.P0, (size_t)d * d, &M.P0);
-      rc |= upload(ctx, h.get(), m.H, span(m.H_stride, (size_t)dy * d), &M.H);
-      rc |= upload(ctx, h.get(), m.R, span(m.R_stride, (size_t)dy * dy), &M.R);
+      rc |= per_time_strided(m.H, m.H_stride, (size_t)dy * d, &M.H);
+      rc |= per_time_strided(m.R, m.R_stride, (size_t)dy * dy, &M.R);
       if (m.horizon >= 1) {
-        rc |= upload(ctx, h.get(), m.F, span(m.F_stride, (size_t)d * d), &M.F);
-        rc |= upload(ctx, h.get(), m.b, span(m.b_stride, (size_t)d), &M.b);
-        rc |= upload(ctx, h.get(), m.Q, span(m.Q_stride, (size_t)d * d), &M.Q);
+        rc |= per_time_strided(m.F, m.F_stride, (size_t)d * d, &M.F);
+        rc |= per_time_strided(m.b, m.b_stride, (size_t)d, &M.b);
+        rc |= per_time_strided(m.Q, m.Q_stride, (size_t)d * d, &M.Q);
       } else {
         M.F = M.b = M.Q = nullptr;
       }
@@ -359,9 +398,10 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
   h->owned.push_back(p);
   h->models_dev = static_cast<DevModel*>(p);
   CU(cudaMemcpyAsync(p, dm.data(), sizeof(DevModel) * B, cudaMemcpyHostToDevice, ctx->stream));
-  CU(cudaMallocAsync(&p, sizeof(TimeConst) * B * (size_t)K, ctx->stream));
+  // per-time constants: the prepared range only (offset pointer, global index)
+  CU(cudaMallocAsync(&p, sizeof(TimeConst) * B * (size_t)(w_hi - w_lo), ctx->stream));
   h->owned.push_back(p);
-  h->tc = static_cast<TimeConst*>(p);
+  h->tc = static_cast<TimeConst*>(p) - w_lo;
   CU(cudaMallocAsync(&p, sizeof(int) * B, ctx->stream));
   h->owned.push_back(p);
   h->bounded = static_cast<int*>(p);
@@ -369,8 +409,8 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
   CU(cudaMemcpyAsync(p, ones.data(), sizeof(int) * B, cudaMemcpyHostToDevice, ctx->stream));
   if (h->deferred.empty()) {
     h->defer = false;
-    prep_kernel<<<dim3((K + 127) / 128, B), 128, 0, ctx->stream>>>(h->models_dev, h->tc, K,
-                                                                   h->bounded);
+    prep_kernel<<<dim3((w_hi - w_lo + 127) / 128, B), 128, 0, ctx->stream>>>(
+        h->models_dev, h->tc, K, h->bounded, w_lo, w_hi);
     LAUNCHED(ctx);
   } else {
     h->prep_pending = true;  // run_tree copies, preps and draws leaves chunk by chunk
@@ -503,8 +543,7 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
                    "FP32 dense combine: N too large for the shared-memory sampler (use a lazy "
                    "resampler)");
   const bool use_tc = ctx->pair_tc && D >= 2;
-  la.rt_ncs = use_tc ? 0 : ncs;  // the CUDA-core pass 1 writes per-split row totals
-  la.aux_comb = ((size_t)(10 + ncs) * N + 3) & ~(size_t)3;
+  la.aux_comb = ((size_t)10 * N + 3) & ~(size_t)3;
   {
     void* p;
     CU(ctx->arena.get("AUX32", la.aux_comb * sizeof(float) * (size_t)nk * b.B, &p));
@@ -1153,6 +1192,17 @@ int dsmc_model_upload(dsmc_ctx* ctx, const dsmc_model_desc* model,
   if (!ctx || !out) return DSMC_E_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   return make_handle(ctx, model, 1, out);
+}
+
+int dsmc_model_upload_window(dsmc_ctx* ctx, const dsmc_model_desc* model, int t0, int len,
+                             dsmc_model_handle** out) {
+  if (!ctx || !out || !model) return DSMC_E_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  const int K = model->horizon + 1;
+  if (len < 1 || t0 < 0 || t0 + len > K)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "window upload: [t0, t0 + len) outside the horizon");
+  // the window's times plus its right cross cut t0 + len (combined on this rank)
+  return make_handle(ctx, model, 1, out, false, t0, std::min(K, t0 + len + 1));
 }
 
 void dsmc_model_free(dsmc_ctx* ctx, dsmc_model_handle* h) {
@@ -2073,6 +2123,8 @@ int dsmc_window_run(dsmc_ctx* ctx, const dsmc_model_handle* hc, const dsmc_windo
   if (len < 2 || (len & (len - 1)) || wo->t0 % len || wo->t0 + len > h->K)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
                    "window: len must be a power of two >= 2 dividing t0, inside the horizon");
+  if (wo->t0 < h->t_lo || wo->t0 + len > h->t_hi)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "window: outside the uploaded model window");
   RunOpts o;
   o.precision = DSMC_FP32;
   o.resampler = wo->resampler;
@@ -2096,7 +2148,8 @@ int dsmc_window_run(dsmc_ctx* ctx, const dsmc_model_handle* hc, const dsmc_windo
   return DSMC_OK;
 }
 
-int dsmc_window_boundary(dsmc_ctx* ctx, int side, void* d_x, float* d_col, double* root_lnc) {
+int dsmc_window_boundary(dsmc_ctx* ctx, int side, void* d_x, float* d_col,
+                         double* d_root_lnc) {
   if (!ctx) return DSMC_E_INVALID_ARGUMENT;
   WindowState& st = window_state(ctx);
   if (!st.valid) return set_err(ctx, DSMC_E_LOGIC, "no window run on this context");
@@ -2104,19 +2157,16 @@ int dsmc_window_boundary(dsmc_ctx* ctx, int side, void* d_x, float* d_col, doubl
   const int N = b.N;
   const int t = side == 0 ? 0 : b.K - 1;
   const uint32_t* map = st.maps[2 * st.cur + (side == 0 ? 0 : 1)];
-  if (d_x)
+  if (d_x) {
     boundary_kernel<<<(N + 255) / 256, 256, 0, ctx->stream>>>(
         b.X32 + (size_t)t * N, b.COL + (size_t)t * N, map, N, (float4*)d_x,
         side == 0 ? d_col : nullptr);
-  LAUNCHED(ctx);
-  CU(cudaGetLastError());
-  if (root_lnc) {
-    CU(cudaMemcpyAsync(ctx->h_lnc, st.blnc[st.cur], 8, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
-    int rc = check_pending_error(ctx);
-    if (rc) return rc;
-    *root_lnc = ctx->h_lnc[0];
+    LAUNCHED(ctx);
+    CU(cudaGetLastError());
   }
+  // the window root's log Z stays on the device (stream-ordered, no sync)
+  if (d_root_lnc)
+    CU(cudaMemcpyAsync(d_root_lnc, st.blnc[st.cur], 8, cudaMemcpyDeviceToDevice, ctx->stream));
   return DSMC_OK;
 }
 
@@ -2170,19 +2220,23 @@ int dsmc_window_finish(dsmc_ctx* ctx, const uint32_t* d_root_map, double* d_mean
 
 int dsmc_cross_combine(dsmc_ctx* ctx, const dsmc_model_handle* hc, const dsmc_window_opts* wo,
                        int cut, int level, long long node, const void* d_xl, const void* d_xr,
-                       const float* d_colr, double lnc_l, double lnc_r, uint32_t* d_l,
-                       uint32_t* d_r, double* lnc_out) {
-  if (!ctx || !hc || !wo || !d_xl || !d_xr || !d_colr || !d_l || !d_r)
+                       const float* d_colr, const double* d_lnc_l, const double* d_lnc_r,
+                       uint32_t* d_l, uint32_t* d_r, double* d_lnc_out) {
+  if (!ctx || !hc || !wo || !d_xl || !d_xr || !d_colr || !d_l || !d_r || !d_lnc_l || !d_lnc_r)
     return DSMC_E_INVALID_ARGUMENT;
   auto* h = const_cast<dsmc_model_handle*>(hc);
   if (cut < 1 || cut >= h->K) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "cross_combine: bad cut");
-  if (wo->resampler != DSMC_MULTINOMIAL && wo->resampler != DSMC_SYSTEMATIC)
-    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "cross_combine: dense resamplers only");
+  if (cut < h->t_lo || cut >= h->t_hi)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "cross_combine: cut outside the uploaded window");
+  if (wo->resampler < 0 || wo->resampler > 3)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "unknown resampler");
+  const bool lazy = wo->resampler >= DSMC_MH_LAZY;
   const int N = (int)wo->n_particles, d = h->d;
   Arena& A = ctx->arena;
   auto s = ctx->stream;
   void* p;
   // a two-leaf window [cut-1, cut] whose "leaves" are the two boundary slabs
+  // (both combined blocks: uniform weights)
   Bufs b{};
   b.K = 2;
   b.T = 1;
@@ -2203,21 +2257,27 @@ int dsmc_cross_combine(dsmc_ctx* ctx, const dsmc_model_handle* hc, const dsmc_wi
   b.COL = (float*)p;
   CU(cudaMemcpyAsync(b.COL + N, d_colr, (size_t)N * sizeof(float), cudaMemcpyDeviceToDevice, s));
   CU(A.get("CMISC", 256, &p));
-  double* lnc = (double*)p;  // [0..1] leaf lnc, [2] new block lnc
+  double* lnc = (double*)p;  // [0..1] block log Z, [2] new block log Z
   uint8_t* uni = (uint8_t*)p + 64;
   uint64_t* seed = (uint64_t*)((char*)p + 128);
-  ErrFlag* err = (ErrFlag*)((char*)p + 160);
-  const double hl[2] = {lnc_l, lnc_r};
-  const uint8_t hu[2] = {1, 1};
-  CU(cudaMemcpyAsync(lnc, hl, 16, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(uni, hu, 2, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(seed, &wo->seed, 8, cudaMemcpyHostToDevice, s));
-  CU(cudaMemsetAsync(err, 0, sizeof(ErrFlag), s));
+  unsigned long long* evals = (unsigned long long*)((char*)p + 136);
+  CU(cudaMemcpyAsync(lnc, d_lnc_l, 8, cudaMemcpyDeviceToDevice, s));
+  CU(cudaMemcpyAsync(lnc + 1, d_lnc_r, 8, cudaMemcpyDeviceToDevice, s));
+  CU(cudaMemsetAsync(uni, 1, 2, s));
+  CU(cudaMemsetAsync(evals, 0, 8, s));
+  set_seed_kernel<<<1, 1, 0, s>>>(seed, wo->seed);
+  LAUNCHED(ctx);
+  // device errors accumulate in the window run's record (first error wins)
+  // and surface at the next host synchronisation (dsmc_sync)
+  CU(A.get("ERR", sizeof(ErrFlag), &p));
+  b.err = (ErrFlag*)p;
+  ctx->last_err = b.err;
+  ctx->last_err_K = h->K;
   b.LNC = lnc;
   b.UNI = uni;
   b.LWMAX = lnc;  // unused (uniform sides)
   b.seeds = seed;
-  b.err = err;
+  b.evals = evals;
   CU(A.get("CPL", (size_t)N * 4, &p));
   b.PL = (uint32_t*)p;
   CU(A.get("CPR", (size_t)N * 4, &p));
@@ -2225,7 +2285,6 @@ int dsmc_cross_combine(dsmc_ctx* ctx, const dsmc_model_handle* hc, const dsmc_wi
   CU(A.get("CLMW", 8, &p));
   b.LMW = (double*)p;
   CU(A.get("CMAPS", 2 * (size_t)N * 4, &p));
-  const size_t ws_comb = ((size_t)N * ((N + kSub - 1) / kSub) + 1) / 2;
   LevelArgs la{};
   la.level = 1;
   la.np = 1;
@@ -2238,26 +2297,38 @@ int dsmc_cross_combine(dsmc_ctx* ctx, const dsmc_model_handle* hc, const dsmc_wi
   la.n_out = N;
   la.key_level = level;
   la.node_off = node;
-  CU(A.get("CWS", ws_comb * 8, &p));
-  la.ws = (double*)p;
-  la.ws_comb = ws_comb;
-  const int sys = wo->resampler == DSMC_SYSTEMATIC;
-  const bool keep = ctx->time_kernels;
-  ctx->time_kernels = false;
-  int rc = d == 1 ? launch_c32<1>(ctx, b, la, 1, sys)
-         : d == 2 ? launch_c32<2>(ctx, b, la, 1, sys)
-         : d == 3 ? launch_c32<3>(ctx, b, la, 1, sys)
-                  : launch_c32<4>(ctx, b, la, 1, sys);
-  ctx->time_kernels = keep;
+  int rc = DSMC_OK;
+  if (lazy) {  // MH / rejection lazy cross combine (resampling.cpp:233-324)
+    const int mh = wo->resampler == DSMC_MH_LAZY;
+    const dim3 grid((N + 127) / 128, 1, 1);
+    switch (d) {
+      case 1: lazy32_kernel<1><<<grid, 128, 0, s>>>(b, la, mh, wo->mh_steps); break;
+      case 2: lazy32_kernel<2><<<grid, 128, 0, s>>>(b, la, mh, wo->mh_steps); break;
+      case 3: lazy32_kernel<3><<<grid, 128, 0, s>>>(b, la, mh, wo->mh_steps); break;
+      default: lazy32_kernel<4><<<grid, 128, 0, s>>>(b, la, mh, wo->mh_steps); break;
+    }
+    LAUNCHED(ctx);
+    lazy_finish_kernel<<<dim3(1, 1, 1), 256, 0, s>>>(b, la);
+    LAUNCHED(ctx);
+  } else {
+    const size_t ws_comb = ((size_t)N * ((N + kSub - 1) / kSub) + 1) / 2;
+    CU(A.get("CWS", ws_comb * 8, &p));
+    la.ws = (double*)p;
+    la.ws_comb = ws_comb;
+    const int sys = wo->resampler == DSMC_SYSTEMATIC;
+    const bool keep = ctx->time_kernels;
+    ctx->time_kernels = false;
+    rc = d == 1 ? launch_c32<1>(ctx, b, la, 1, sys)
+       : d == 2 ? launch_c32<2>(ctx, b, la, 1, sys)
+       : d == 3 ? launch_c32<3>(ctx, b, la, 1, sys)
+                : launch_c32<4>(ctx, b, la, 1, sys);
+    ctx->time_kernels = keep;
+  }
   if (rc) return rc;
+  CU(cudaGetLastError());
   CU(cudaMemcpyAsync(d_l, b.PL, (size_t)N * 4, cudaMemcpyDeviceToDevice, s));
   CU(cudaMemcpyAsync(d_r, b.PR, (size_t)N * 4, cudaMemcpyDeviceToDevice, s));
-  ErrFlag e;
-  CU(cudaMemcpyAsync(&e, err, sizeof e, cudaMemcpyDeviceToHost, s));
-  CU(cudaMemcpyAsync(ctx->h_lnc, lnc + 2, 8, cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
-  if (e.code) return set_err(ctx, e.code, err_message(e, h->K));
-  if (lnc_out) *lnc_out = ctx->h_lnc[0];
+  if (d_lnc_out) CU(cudaMemcpyAsync(d_lnc_out, lnc + 2, 8, cudaMemcpyDeviceToDevice, s));
   return DSMC_OK;
 }
 

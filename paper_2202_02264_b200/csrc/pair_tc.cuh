@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) c32_pair_tc(Bufs b, 
           const float mx = fmaxf(l0, l1);
           Ls = mx > -CUDART_INF_F ? mx + lg2(ex2(l0 - mx) + ex2(l1 - mx)) : -CUDART_INF_F;
         }
-        ws[(size_t)i * nsub + sbk] = (Brow > -CUDART_INF_F && cmx > -CUDART_INF_F && Ls > -CUDART_INF_F)
+        ws[(size_t)sbk * N + i] = (Brow > -CUDART_INF_F && cmx > -CUDART_INF_F && Ls > -CUDART_INF_F)
                                       ? Ls + crow + cmx + Brow
                                       : -CUDART_INF_F;
       }

@@ -63,9 +63,10 @@ def load_library():
                                        C.POINTER(abi.CondOpts), u32, dp, u8p, dp, u64p]),
         "dsmc_kalman_smooth": (i, [C.POINTER(abi.ModelDesc), dp, dp, dp]),
         "dsmc_window_run": (i, [vp, vp, C.POINTER(abi.WindowOpts)]),
-        "dsmc_window_boundary": (i, [vp, i, vp, vp, dp]),
+        "dsmc_window_boundary": (i, [vp, i, vp, vp, vp]),
         "dsmc_cross_combine": (i, [vp, vp, C.POINTER(abi.WindowOpts), i, i, C.c_longlong, vp, vp,
-                                   vp, C.c_double, C.c_double, vp, vp, dp]),
+                                   vp, vp, vp, vp, vp, vp]),
+        "dsmc_model_upload_window": (i, [vp, C.POINTER(abi.ModelDesc), i, i, C.POINTER(vp)]),
         "dsmc_window_remap": (i, [vp, i, vp]),
         "dsmc_window_finish": (i, [vp, vp, vp, vp]),
         "dsmc_ffbs_smooth": (i, [vp, C.POINTER(abi.ModelDesc), C.POINTER(abi.FfbsOpts), dp, dp,
@@ -241,19 +242,26 @@ class Engine:
         o = abi.WindowOpts(n_particles, resampler, mh_steps, seed, t0, length)
         self._check(self.lib.dsmc_window_run(self.ctx, handle, C.byref(o)))
 
-    def window_boundary(self, side, d_states, d_col=None):
-        lnc = C.c_double()
-        self._check(self.lib.dsmc_window_boundary(self.ctx, side, d_states, d_col, C.byref(lnc)))
-        return lnc.value
+    def upload_window(self, model, t0, length):
+        """dsmc_model_upload_window: only the rows [t0 - 1, t0 + length] a
+        time-sharded rank needs (its window and its right cross cut)."""
+        h = C.c_void_p()
+        self._check(self.lib.dsmc_model_upload_window(self.ctx, C.byref(model.desc), t0, length,
+                                                      C.byref(h)))
+        return h
+
+    def window_boundary(self, side, d_states, d_col=None, d_root_lnc=None):
+        """Enqueue the boundary slab gather and the root log Z copy (device
+        pointers); no host synchronisation."""
+        self._check(self.lib.dsmc_window_boundary(self.ctx, side, d_states, d_col, d_root_lnc))
 
     def cross_combine(self, handle, n_particles, seed, cut, level, node, d_xl, d_xr, d_colr,
-                      lnc_l, lnc_r, d_l, d_r, resampler=abi.MULTINOMIAL):
-        o = abi.WindowOpts(n_particles, resampler, 16, seed, 0, 2)
-        out = C.c_double()
+                      d_lnc_l, d_lnc_r, d_l, d_r, d_lnc_out, resampler=abi.MULTINOMIAL,
+                      mh_steps=16):
+        o = abi.WindowOpts(n_particles, resampler, mh_steps, seed, 0, 2)
         self._check(self.lib.dsmc_cross_combine(self.ctx, handle, C.byref(o), cut, level, node,
-                                                d_xl, d_xr, d_colr, lnc_l, lnc_r, d_l, d_r,
-                                                C.byref(out)))
-        return out.value
+                                                d_xl, d_xr, d_colr, d_lnc_l, d_lnc_r, d_l, d_r,
+                                                d_lnc_out))
 
     def window_remap(self, side, d_idx):
         self._check(self.lib.dsmc_window_remap(self.ctx, side, d_idx))

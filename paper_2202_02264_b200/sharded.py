@@ -16,11 +16,15 @@ window gB):
   gL -> gA   l, so gA sets first := first[l]   (dsmc_window_remap)
   gL -> gB   r, so gB sets last  := last[r]
 
-Block log Z values are all-reduced after each level (a few doubles), the
-cross-level (l, r) once at the end; every rank then composes its window's
-root map through the cross levels and finishes its window locally (top-down
-composition + per-time moments). Exchanged bytes per cut: 20 N (slab) + 8 N
-(indices), latency bound on NVLink.
+Block log Z values stay on the device and are all-reduced after each level
+(a few doubles), the cross-level (l, r) once at the end; every rank then
+composes its window's root map through the cross levels (device indexing)
+and finishes its window locally (top-down composition + per-time moments).
+No stage synchronises the host: the engine enqueues, NCCL P2P and the
+reductions run on the engine stream, and device errors surface at the next
+dsmc_sync. Exchanged bytes per cut: 20 N (slab) + 8 N (indices), latency
+bound on NVLink. Any resampler works across windows (dense, MH-lazy,
+rejection-lazy; log Z is NaN after a lazy level, as in the reference).
 
 Transports: `TorchComm` (torch.distributed: NCCL on GPUs, gloo on CPU) and
 in-process virtual ranks (several backends hosted by one process exchange
@@ -44,11 +48,13 @@ def _log2(x):
 
 
 class GpuBackend:
-    """One rank's CUDA engine context + uploaded model."""
+    """One rank's CUDA engine context + uploaded model (use
+    Engine.upload_window for a rank that only needs its window)."""
 
-    def __init__(self, engine, handle, N, d, seed, resampler=abi.MULTINOMIAL, device=0):
+    def __init__(self, engine, handle, N, d, seed, resampler=abi.MULTINOMIAL, device=0,
+                 mh_steps=16):
         self.e, self.h, self.N, self.d = engine, handle, N, d
-        self.seed, self.resampler = seed, resampler
+        self.seed, self.resampler, self.mh_steps = seed, resampler, mh_steps
         self.dev = torch.device("cuda", device)
         self.stream = torch.cuda.ExternalStream(engine.stream_handle(), device=self.dev)
         self.len = 0
@@ -69,29 +75,31 @@ class GpuBackend:
 
     def window_run(self, t0, length):
         self.len = length
-        self.e.window_run(self.h, self.N, t0, length, self.seed, self.resampler)
+        self.e.window_run(self.h, self.N, t0, length, self.seed, self.resampler, self.mh_steps)
 
-    def root_lnc(self):
-        return self.e.window_boundary(1, None)
+    def root_lnc(self, out):
+        """The window root's log Z into `out` (a 1-element device tensor)."""
+        self.e.window_boundary(1, None, None, out.data_ptr())
 
     def boundary(self, side):
         x = self.empty_states()
         col = self.empty_col() if side == 0 else None
-        lnc = self.e.window_boundary(side, x.data_ptr(), col.data_ptr() if col is not None else None)
-        return x, col, lnc
+        self.e.window_boundary(side, x.data_ptr(), col.data_ptr() if col is not None else None)
+        return x, col
 
-    def cross(self, cut, level, node, xl, xr, colr, lnc_l, lnc_r):
+    def cross(self, cut, level, node, xl, xr, colr, lnc_l, lnc_r, lnc_out):
         l, r = self.empty_idx(), self.empty_idx()
-        lnc = self.e.cross_combine(self.h, self.N, self.seed, cut, level, node, xl.data_ptr(),
-                                   xr.data_ptr(), colr.data_ptr(), lnc_l, lnc_r, l.data_ptr(),
-                                   r.data_ptr(), self.resampler)
-        return l, r, lnc
+        self.e.cross_combine(self.h, self.N, self.seed, cut, level, node, xl.data_ptr(),
+                             xr.data_ptr(), colr.data_ptr(), lnc_l.data_ptr(), lnc_r.data_ptr(),
+                             l.data_ptr(), r.data_ptr(), lnc_out.data_ptr(), self.resampler,
+                             self.mh_steps)
+        return l, r
 
     def remap(self, side, idx):
         self.e.window_remap(side, idx.data_ptr())
 
     def finish(self, root_map):
-        rm = torch.as_tensor(np.asarray(root_map, np.int32), device=self.dev)
+        rm = root_map.to(device=self.dev, dtype=torch.int32).contiguous()
         mean = torch.empty((self.len, self.d), dtype=torch.float64, device=self.dev)
         cov = torch.empty((self.len, self.d, self.d), dtype=torch.float64, device=self.dev)
         self.e.window_finish(rm.data_ptr(), mean.data_ptr(), cov.data_ptr())
@@ -171,6 +179,11 @@ def sharded_smooth(backends, comm, K, N, world):
 
 
 def _sharded_smooth(backends, comm, K, N, world):
+    """Every value of the protocol stays on the device: block log Z in a
+    float64 tensor, (l, r) in int32 tensors, the window root maps composed
+    with device indexing; no host synchronisation until the returned log Z.
+    Virtual ranks (several backends, each on its own stream, in one
+    process) hand data between streams through a host sync (`handoff`)."""
     P = world
     Kloc = K // P
     s, L = _log2(Kloc), _log2(K)
@@ -178,12 +191,20 @@ def _sharded_smooth(backends, comm, K, N, world):
         raise ValueError("each rank needs at least two leaves")
     ranks = sorted(backends)
     dev = backends[ranks[0]].comm_device
+    virtual = len(backends) > 1
+
+    def handoff():
+        if virtual:
+            for be in backends.values():
+                be.sync()
+
     for g in ranks:
         backends[g].window_run(g * Kloc, Kloc)
     # log Z of every block of the current level (all ranks know all of them)
     lnc = torch.zeros(P, dtype=torch.float64, device=dev)
     for g in ranks:
-        lnc[g] = backends[g].root_lnc()
+        backends[g].root_lnc(lnc[g:g + 1])
+    handoff()
     if comm is not None:
         comm.all_reduce_sum(lnc)
     cross = torch.zeros((max(P - 1, 1), 2, N), dtype=torch.int32, device=dev)
@@ -203,9 +224,8 @@ def _sharded_smooth(backends, comm, K, N, world):
         for gm in geo:
             gL, gR = gm["gL"], gm["gR"]
             if gR in backends:
-                xr, colr, _ = backends[gR].boundary(0)
+                xr, colr = backends[gR].boundary(0)
                 if gL in backends:
-                    backends[gR].sync()  # in-process hand-off between streams
                     slabs[gm["k"]] = (xr, colr)
                 else:
                     sends += [(gL, xr), (gL, colr)]
@@ -213,6 +233,7 @@ def _sharded_smooth(backends, comm, K, N, world):
                 xr, colr = backends[gL].empty_states(), backends[gL].empty_col()
                 recvs += [(gR, xr), (gR, colr)]
                 slabs[gm["k"]] = (xr, colr)
+        handoff()
         if comm is not None:
             comm.exchange(sends, recvs)
         # phase 2: the cross combine on gL; l -> gA, r -> gB
@@ -221,11 +242,10 @@ def _sharded_smooth(backends, comm, K, N, world):
             k, gL = gm["k"], gm["gL"]
             if gL in backends:
                 B = backends[gL]
-                xl, _, _ = B.boundary(1)
+                xl, _ = B.boundary(1)
                 xr, colr = slabs[k]
-                l, r, lnew = B.cross(gm["c"], lev, k, xl, xr, colr, float(lnc[2 * k]),
-                                     float(lnc[2 * k + 1]))
-                new_lnc[k] = lnew
+                l, r = B.cross(gm["c"], lev, k, xl, xr, colr, lnc[2 * k:2 * k + 1],
+                               lnc[2 * k + 1:2 * k + 2], new_lnc[k:k + 1])
                 cross[cidx[(lev, k)], 0] = l
                 cross[cidx[(lev, k)], 1] = r
                 for side, dst, t in ((0, gm["gA"], l), (1, gm["gB"], r)):
@@ -239,23 +259,25 @@ def _sharded_smooth(backends, comm, K, N, world):
                         t = backends[dst].empty_idx()
                         recvs.append((gL, t))
                         remaps.append((dst, side, t))
+        handoff()
         if comm is not None:
             comm.exchange(sends, recvs)
         for dst, side, t in remaps:
             backends[dst].remap(side, t)
+        handoff()
         if comm is not None:
             comm.all_reduce_sum(new_lnc)
         lnc = new_lnc
     if comm is not None and P > 1:
         comm.all_reduce_sum(cross)
-    log_z = float(lnc[0])
-    cross_h = cross.cpu().numpy()
     out = {}
     for g in ranks:
+        # the window root's map through the cross levels, on the device
         t0 = g * Kloc
-        M = np.arange(N, dtype=np.int64)
+        M = torch.arange(N, dtype=torch.int64, device=dev)
         for lev in range(L, s, -1):
-            l, r = cross_h[cidx[(lev, t0 >> lev)]]
+            l, r = cross[cidx[(lev, t0 >> lev)]].long()
             M = l[M] if (t0 % (1 << lev)) < (1 << (lev - 1)) else r[M]
         out[g] = backends[g].finish(M)
-    return out, log_z
+    handoff()
+    return out, float(lnc[0])

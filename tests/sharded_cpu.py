@@ -21,13 +21,14 @@ def lnp(x, m, v):
 class CpuBackend:
     comm_device = torch.device("cpu")
 
-    def __init__(self, model, N, seed, oracle):
+    def __init__(self, model, N, seed, oracle, resampler=abi.MULTINOMIAL, mh_steps=4):
         A = model.arrays
         g = lambda k: np.asarray(A[k], float).ravel()
         self.F, self.b, self.Q, self.H, self.R = (float(g(k)[0]) for k in "F b Q H R".split())
         self.y, self.pm, self.pv = g("y"), g("prop_mean"), g("prop_cov")
         self.m0, self.P0 = float(g("m0")[0]), float(g("P0")[0])
         self.N, self.seed, self.O = N, seed, oracle
+        self.resampler, self.mh_steps = resampler, mh_steps
         self.len = 0
 
     def empty_states(self):
@@ -67,10 +68,13 @@ class CpuBackend:
         table = colr.astype(np.float64)[None, :] - (xr[None, :] - mu[:, None]) ** 2 / (2 * self.Q)
         if lwl is not None:
             table = table + lwl[:, None]
-        r = self.O.resample_table(abi.MULTINOMIAL, table, self.N, (self.seed, level, node))
+        # rejection: the table max is a valid (exact) bound for this test model
+        r = self.O.resample_table(self.resampler, table, self.N, (self.seed, level, node),
+                                  mh_steps=self.mh_steps, bound=float(np.max(table)))
         shift = (-np.log(self.N) if lwl is None else 0.0) - np.log(self.N)
+        lmw = r["log_mean_weight"]
         return r["left"].astype(np.int64), r["right"].astype(np.int64), \
-            lnc_l + lnc_r + r["log_mean_weight"] + shift
+            (lnc_l + lnc_r + lmw + shift) if lmw is not None else float("nan")
 
     def window_run(self, t0, length):
         self.t0, self.len = t0, length
@@ -104,29 +108,31 @@ class CpuBackend:
         self.levels = level
         self.root = blocks[0]
 
-    def root_lnc(self):
-        return float(self.root["lnc"])
+    def root_lnc(self, out):
+        out.fill_(float(self.root["lnc"]))
 
     def boundary(self, side):
         x = self.empty_states()
         if side == 0:
             x[:, 0] = torch.from_numpy(self.X[0][self.root["first"]])
             col = torch.from_numpy(self.C[0][self.root["first"]].copy())
-            return x, col, self.root_lnc()
+            return x, col
         x[:, 0] = torch.from_numpy(self.X[self.len - 1][self.root["last"]])
-        return x, None, self.root_lnc()
+        return x, None
 
-    def cross(self, cut, level, node, xl, xr, colr, lnc_l, lnc_r):
+    def cross(self, cut, level, node, xl, xr, colr, lnc_l, lnc_r, lnc_out):
         l, r, lnc = self._combine(xl[:, 0].numpy(), xr[:, 0].numpy(), colr.numpy(), None, level,
-                                  node, lnc_l, lnc_r)
-        return torch.from_numpy(l.astype(np.int32)), torch.from_numpy(r.astype(np.int32)), lnc
+                                  node, float(lnc_l[0]), float(lnc_r[0]))
+        lnc_out.fill_(lnc)
+        return torch.from_numpy(l.astype(np.int32)), torch.from_numpy(r.astype(np.int32))
 
     def remap(self, side, idx):
         key = "first" if side == 0 else "last"
         self.root[key] = self.root[key][idx.numpy().astype(np.int64)]
 
     def finish(self, root_map):
-        maps = {(self.levels, 0): np.asarray(root_map, np.int64)}
+        maps = {(self.levels, 0): np.asarray(root_map.cpu() if torch.is_tensor(root_map)
+                                             else root_map, np.int64)}
         for level in range(self.levels, 0, -1):
             for k in range(self.len >> level):
                 M = maps[(level, k)]

@@ -23,23 +23,29 @@ def _model():
     return models.lgssm_check(K - 1)
 
 
-def _cpu_run(P, ranks=None, comm=None):
+def _cpu_run(P, ranks=None, comm=None, rs=abi.MULTINOMIAL):
     from oracle.py import Oracle
     from tests.sharded_cpu import CpuBackend
     m, O = _model(), Oracle()
     ranks = range(P) if ranks is None else ranks
-    backends = {g: CpuBackend(m, N, SEED, O) for g in ranks}
+    backends = {g: CpuBackend(m, N, SEED, O, rs) for g in ranks}
     out, lz = sharded_smooth(backends, comm, K, N, P)
     mean = torch.cat([out[g][0] for g in sorted(out)])
     return mean.numpy(), lz
 
 
+def _same_lz(a, b):
+    return (np.isnan(a) and np.isnan(b)) or a == b
+
+
+@pytest.mark.parametrize("rs", [abi.MULTINOMIAL, abi.MH_LAZY, abi.REJECTION_LAZY])
 @pytest.mark.parametrize("P", [2, 4, 8])
-def test_virtual_ranks_reproduce_single_rank_cpu(P):
-    m1, lz1 = _cpu_run(1)
-    mP, lzP = _cpu_run(P)
+def test_virtual_ranks_reproduce_single_rank_cpu(P, rs):
+    m1, lz1 = _cpu_run(1, rs=rs)
+    mP, lzP = _cpu_run(P, rs=rs)
     assert np.array_equal(m1, mP)
-    assert lz1 == lzP
+    assert _same_lz(lz1, lzP)
+    assert np.isnan(lzP) == (rs != abi.MULTINOMIAL)  # lazy levels: no log Z
 
 
 def _gloo_worker(rank, world, port, q):
@@ -88,7 +94,9 @@ def test_virtual_ranks_on_gpu_match_single_gpu(P, KK, NN):
     ref_eng = Engine(0)
     ref = ref_eng.smooth(m, NN, abi.MULTINOMIAL, seed=SEED, precision=abi.FP32)
     engines = {g: Engine(0) for g in range(P)}
-    backends = {g: GpuBackend(e, e.upload(m), NN, m.d, SEED) for g, e in engines.items()}
+    # each rank uploads and prepares only its window (+ its right cross cut)
+    backends = {g: GpuBackend(e, e.upload_window(m, g * (KK // P), KK // P), NN, m.d, SEED)
+                for g, e in engines.items()}
     out, lz = sharded_smooth(backends, None, KK, NN, P)
     for b in backends.values():
         b.sync()
@@ -97,6 +105,31 @@ def test_virtual_ranks_on_gpu_match_single_gpu(P, KK, NN):
     assert np.array_equal(mean, ref["mean"])
     assert np.array_equal(cov, ref["cov"])
     assert lz == ref["log_norm_const"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rs", [abi.MH_LAZY, abi.REJECTION_LAZY])
+def test_virtual_ranks_lazy_c3_shape_p8(rs):
+    """C3's lazy stitching across 8 windows (SV, N = 4096, K = 2^12): MH-lazy
+    (B = 16) and rejection-lazy cross combines reproduce the single-GPU run
+    bit for bit (lazy resamplers could not shard)."""
+    from paper_2202_02264_b200.dsmc import Engine
+    from paper_2202_02264_b200.sharded import GpuBackend
+    KK, NN, P = 1 << 12, 4096, 8
+    ys = np.asarray(models.sv((1 << 16) - 1).arrays["y"], np.float64)[:KK]
+    m = models.sv(KK - 1, ys=ys)
+    ref = Engine(0).smooth(m, NN, rs, seed=SEED, precision=abi.FP32, mh_steps=16)
+    engines = {g: Engine(0) for g in range(P)}
+    backends = {g: GpuBackend(e, e.upload_window(m, g * (KK // P), KK // P), NN, m.d, SEED,
+                              resampler=rs, mh_steps=16) for g, e in engines.items()}
+    out, lz = sharded_smooth(backends, None, KK, NN, P)
+    for b in backends.values():
+        b.sync()
+    mean = torch.cat([out[g][0] for g in range(P)]).cpu().numpy()
+    cov = torch.cat([out[g][1] for g in range(P)]).cpu().numpy()
+    assert np.array_equal(mean, ref["mean"])
+    assert np.array_equal(cov, ref["cov"])
+    assert np.isnan(lz) and ref["log_norm_const"] is None
 
 
 def _gpu_gloo_worker(rank, world, port, q, KK, NN):
@@ -108,8 +141,9 @@ def _gpu_gloo_worker(rank, world, port, q, KK, NN):
         from paper_2202_02264_b200.sharded import GpuBackend
         m = models.cv_tracking(KK - 1)
         e = Engine(0)
-        be = GpuBackend(e, e.upload(m), NN, m.d, SEED)
+        be = GpuBackend(e, e.upload_window(m, rank * (KK // world), KK // world), NN, m.d, SEED)
         out, lz = sharded_smooth({rank: be}, TorchComm(), KK, NN, world)
+        be.sync()
         q.put((rank, out[rank][0].cpu().numpy(), out[rank][1].cpu().numpy(), lz))
         e.close()
     finally:
