@@ -346,7 +346,7 @@ def run_ours(args, cfg, rank, world, device):
     prec = abi.FP64_PARITY if args.precision == "fp64" else abi.FP32
     seed_base = 1 + (1 << 32)  # experiment.cpp:42-45 salting of seed 1, replicate 0
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=torch.device("cuda", device))
-    h = eng.upload(model)
+    h = eng.upload(model) if world == 1 else None
     eng.sync()
     if world == 1:
         def step(s):
@@ -505,7 +505,8 @@ def run_ours(args, cfg, rank, world, device):
         }
         if fp64:
             out["fp64_parity"] = fp64
-    eng.free_model(h)
+    if h is not None:
+        eng.free_model(h)
     eng.close()
     return out
 

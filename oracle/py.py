@@ -208,6 +208,8 @@ class Reference(_Base):
                                        _dp, _dp, _ip, _u64p, _ip, _ip]
         L.ref_leaf_weights_all.argtypes = [M, _dp, _sz, _dp]
         L.ref_make_leaves_all.argtypes = [M, _sz, _u64, _i, _dp, _dp]
+        L.ref_gamma_draw.argtypes = [C.c_double, C.c_double, _u64, _u32, _u64, _i, _dp]
+        L.ref_sv_param_update.argtypes = [_dp, _i, C.POINTER(abi.SvPrior), _u64, _u32, _dp, _ip]
         L.ref_conditional_leaves_all.argtypes = [M, _sz, _u64, _u32, _dp, _dp]
         self._philox = L.ref_philox
         self._stream = L.ref_stream
@@ -271,6 +273,20 @@ class Reference(_Base):
                     log_mean_weight=None if lmw is None else lmw[:T],
                     log_norm_const=lnc.value if has.value else None, weight_evals=ev.value,
                     levels=lev.value, biased=bool(bi.value))
+
+    def gamma_draw(self, shape, rate, key):
+        out = C.c_double()
+        seed, level, node, role = key
+        self._check(self.L.ref_gamma_draw(shape, rate, seed, level, node, role, C.byref(out)))
+        return out.value
+
+    def sv_param_update(self, path, theta, prior, seed, sweep):
+        th = np.ascontiguousarray(theta, np.float64).copy()
+        path = np.ascontiguousarray(path, np.float64)
+        acc = C.c_int()
+        self._check(self.L.ref_sv_param_update(abi.dptr(path), len(path) - 1, C.byref(prior),
+                                               seed, sweep, abi.dptr(th), C.byref(acc)))
+        return th, bool(acc.value)
 
     def leaves_all(self, model, n, seed, threads=None):
         """make_leaf for every t (multithreaded): states (K, n, d), raw weights (K, n)."""

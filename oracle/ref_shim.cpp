@@ -123,6 +123,12 @@ void par_for(std::size_t count, int threads, const std::function<void(std::size_
 
 }  // namespace
 
+namespace dsmc {
+// the reference's gamma_draw (pgibbs.cpp:80-102), compiled from its own source
+// by oracle/Makefile (gamma_draw_ref.cpp)
+double gamma_draw(double shape, double rate, RngStream& stream);
+}  // namespace dsmc
+
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
@@ -475,6 +481,67 @@ int ref_conditional_leaves_all(const dsmc_model_desc* desc, size_t n, uint64_t s
       auto blk = dsmc::conditional_leaf(model, t, n, seed, sweep, star + (size_t)t * d);
       std::memcpy(X + (size_t)t * n * d, blk.paths.data(), sizeof(double) * n * d);
     }
+  });
+}
+
+// gamma_draw (pgibbs.cpp:80-102) from stream {seed, level, node, role}.
+int ref_gamma_draw(double shape, double rate, uint64_t seed, uint32_t level, uint64_t node,
+                   int role, double* out) {
+  return guarded([&] {
+    dsmc::RngStream s(key_of(seed, level, node, role));
+    *out = dsmc::gamma_draw(shape, rate, s);
+  });
+}
+
+// The SV parameter kernel of the batched particle Gibbs (the
+// reference has no SV model), on the reference's RngStream and gamma_draw:
+// sigma2 | rest by the conjugate inverse gamma (gamma_draw of the precision),
+// mu | rest normal, random-walk Metropolis on phi with a flat prior on
+// (-1, 1); stream {seed, 0, sweep, gibbs_param} as pgibbs_sweep keys it
+// (pgibbs.cpp:38). Pins the device kernel's draws (tests/test_gpu_pgibbs.py).
+int ref_sv_param_update(const double* x, int T, const dsmc_sv_prior* pr, uint64_t seed,
+                        uint32_t sweep, double* theta, int* accepted_phi) {
+  return guarded([&] {
+    auto lnp = [](double v, double m, double var) {
+      const double d = v - m;
+      return -0.5 * (1.8378770664093454836 + std::log(var)) - d * d / (2.0 * var);
+    };
+    auto loglik = [&](double mu, double phi, double s2) {
+      double ll = lnp(x[0], mu, s2 / (1.0 - phi * phi));
+      for (int t = 1; t <= T; ++t) ll += lnp(x[t], mu + phi * (x[t - 1] - mu), s2);
+      return ll;
+    };
+    dsmc::RngStream s(key_of(seed, 0, sweep, DSMC_ROLE_GIBBS_PARAM));
+    double mu = theta[0], phi = theta[1], s2 = theta[2];
+    double ss = (1.0 - phi * phi) * (x[0] - mu) * (x[0] - mu);
+    for (int t = 1; t <= T; ++t) {
+      const double e = x[t] - mu - phi * (x[t - 1] - mu);
+      ss += e * e;
+    }
+    const double prec =
+        dsmc::gamma_draw(pr->s2_shape + 0.5 * (double)(T + 1), pr->s2_rate + 0.5 * ss, s);
+    s2 = 1.0 / prec;
+    const double p = 1.0 / pr->mu_var + (1.0 - phi * phi) / s2 +
+                     (double)T * (1.0 - phi) * (1.0 - phi) / s2;
+    double acc = 0.0;
+    for (int t = 1; t <= T; ++t) acc += x[t] - phi * x[t - 1];
+    const double h = pr->mu_mean / pr->mu_var + (1.0 - phi * phi) * x[0] / s2 +
+                     (1.0 - phi) * acc / s2;
+    mu = h / p + std::sqrt(1.0 / p) * s.normal();
+    const double prop = phi + pr->phi_step * s.normal();
+    const double lu = std::log(s.uniform_pos());
+    int a = 0;
+    if (std::fabs(prop) < 1.0) {
+      const double dl = loglik(mu, prop, s2) - loglik(mu, phi, s2);
+      if (lu < dl) {
+        phi = prop;
+        a = 1;
+      }
+    }
+    theta[0] = mu;
+    theta[1] = phi;
+    theta[2] = s2;
+    if (accepted_phi) *accepted_phi = a;
   });
 }
 

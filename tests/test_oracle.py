@@ -167,3 +167,33 @@ def test_oracle_kalman_matches_numpy():
         assert np.allclose(a, b, rtol=1e-10, atol=1e-10) and np.allclose(P, Q, rtol=1e-10,
                                                                            atol=1e-12)
         assert np.isfinite(ll)
+
+
+def test_gamma_draw_pinned_to_the_reference(oracle, reference):
+    """gamma_draw (pgibbs.cpp:80-102) compiled from the reference's own source
+    (oracle/Makefile extracts the function; pgibbs.cpp as a whole needs Eigen)
+    against the oracle's restatement: bitwise over shapes below and above 1,
+    several rates and streams (both use glibc pow/log/sqrt)."""
+    for shape in (0.05, 0.3, 0.999, 1.0, 1.7, 3.0, 12.5, 2049.0):
+        for rate in (0.01, 1.0, 37.0):
+            for node in range(6):
+                key = (99 + node, 0, node, abi.ROLE_GIBBS_PARAM)
+                a = oracle.L.or_gamma_draw(shape, rate, *key)
+                b = reference.gamma_draw(shape, rate, key)
+                assert a == b, (shape, rate, node)
+    with pytest.raises(ValueError):
+        reference.gamma_draw(0.0, 1.0, (1, 0, 0, abi.ROLE_GIBBS_PARAM))
+
+
+def test_sv_param_update_oracle_equals_reference_gamma(oracle, reference):
+    """The SV parameter kernel restated in C (or_sv_param_update) equals the
+    same kernel on the reference's RngStream + gamma_draw, bit for bit."""
+    rng = np.random.default_rng(3)
+    prior = abi.SvPrior(-1.0, 1.0, 2.0, 0.2, 0.05)
+    for T in (0, 7, 511):
+        for seed in (1, 77, 1234):
+            x = -1.0 + 0.4 * rng.standard_normal(T + 1)
+            th = np.array([-1.0, 0.9, 0.1]) + 0.01 * rng.standard_normal(3)
+            a, acc_a = oracle.sv_param_update(x, th, prior, seed, 3)
+            b, acc_b = reference.sv_param_update(x, th, prior, seed, 3)
+            assert np.array_equal(a, b) and acc_a == acc_b
