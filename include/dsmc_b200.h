@@ -448,6 +448,15 @@ DSMC_API int dsmc_kalman_smooth(const dsmc_model_desc* model,
                                 double* smooth_mean, double* smooth_cov,
                                 double* log_likelihood);
 
+/* The same smoother on the device by parallel prefix scans (Sarkka &
+ * Garcia-Fernandez 2021: associative filtering and smoothing elements,
+ * O(log T) span instead of the reference's length-T chain; FP64;
+ * csrc/kalman_scan.cuh). Equal to dsmc_kalman_smooth to rounding
+ * (tests/test_gpu_kalman.py: 1e-9 relative). Host outputs. */
+DSMC_API int dsmc_kalman_smooth_device(dsmc_ctx* ctx, const dsmc_model_desc* model,
+                                       double* smooth_mean, double* smooth_cov,
+                                       double* log_likelihood);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "ffbs.cuh"
+#include "kalman_scan.cuh"
 #include "pair_tc.cuh"
 #include "dsmc_b200.h"
 
@@ -2455,3 +2456,157 @@ extern "C" int dsmc_ffbs_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
 // The reference's piecewise entry points (make_leaf, resample_pairs over a
 // block pair or a caller-evaluated source, index resampling).
 #include "pieces.cuh"
+
+// ------------------------------------------------ device Kalman / RTS
+namespace {
+
+template <class Op>
+int scan_chunked(dsmc_ctx* ctx, typename Op::E* el, int n, int depth) {
+  auto s = ctx->stream;
+  if (n <= kScanChunk) {
+    scan_chunk_apply<Op><<<1, 1, 0, s>>>(el, n, nullptr);
+    LAUNCHED(ctx);
+    return DSMC_OK;
+  }
+  const int nc = (n + kScanChunk - 1) / kScanChunk;
+  void* p;
+  const std::string name = std::string(sizeof(typename Op::E) == sizeof(FiltElem<4>) ? "KFA" : "KSA") +
+                           std::to_string(sizeof(typename Op::E)) + "_" + std::to_string(depth);
+  CU(ctx->arena.get(name.c_str(), (size_t)nc * sizeof(typename Op::E), &p));
+  auto* agg = static_cast<typename Op::E*>(p);
+  scan_chunk_total<Op><<<(nc + 63) / 64, 64, 0, s>>>(el, n, agg);
+  LAUNCHED(ctx);
+  int rc = scan_chunked<Op>(ctx, agg, nc, depth + 1);
+  if (rc) return rc;
+  scan_chunk_apply<Op><<<(nc + 63) / 64, 64, 0, s>>>(el, n, agg);
+  LAUNCHED(ctx);
+  return DSMC_OK;
+}
+
+__global__ void sum_kernel(const double* x, int n, double* out) {
+  __shared__ double sh[1024];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v += x[i];
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+template <int D, int DY>
+int kalman_device(dsmc_ctx* ctx, const KfModel& m, int K, double* d_mean, double* d_cov,
+                  double* d_ll, int* d_bad) {
+  auto s = ctx->stream;
+  void* p;
+  CU(ctx->arena.get("KF_FILT", (size_t)K * sizeof(FiltElem<D>), &p));
+  auto* fe = static_cast<FiltElem<D>*>(p);
+  CU(ctx->arena.get("KF_SMOOTH", (size_t)K * sizeof(SmoothElem<D>), &p));
+  auto* se = static_cast<SmoothElem<D>*>(p);
+  CU(ctx->arena.get("KF_LLT", (size_t)K * sizeof(double), &p));
+  auto* llt = static_cast<double*>(p);
+  const int nb = (K + 127) / 128;
+  kf_filter_elems<D, DY><<<nb, 128, 0, s>>>(m, K, fe, d_bad);
+  LAUNCHED(ctx);
+  int rc = scan_chunked<FiltOp<D>>(ctx, fe, K, 0);
+  if (rc) return rc;
+  kf_smooth_elems<D, DY><<<nb, 128, 0, s>>>(m, K, fe, se, llt, d_bad);
+  LAUNCHED(ctx);
+  rc = scan_chunked<SmoothOp<D>>(ctx, se, K, 0);
+  if (rc) return rc;
+  kf_outputs<D><<<nb, 128, 0, s>>>(K, se, d_mean, d_cov);
+  LAUNCHED(ctx);
+  sum_kernel<<<1, 1024, 0, s>>>(llt, K, d_ll);
+  LAUNCHED(ctx);
+  return cudaGetLastError() == cudaSuccess ? DSMC_OK
+                                           : set_err(ctx, DSMC_E_CUDA, "kalman scan launch failed");
+}
+
+template <int D>
+int kalman_device_dy(dsmc_ctx* ctx, int dy, const KfModel& m, int K, double* a, double* b,
+                     double* c, int* bad) {
+  switch (dy) {
+    case 1: return kalman_device<D, 1>(ctx, m, K, a, b, c, bad);
+    case 2: return kalman_device<D, 2>(ctx, m, K, a, b, c, bad);
+    case 3: return kalman_device<D, 3>(ctx, m, K, a, b, c, bad);
+    default: return kalman_device<D, 4>(ctx, m, K, a, b, c, bad);
+  }
+}
+
+}  // namespace
+
+extern "C" int dsmc_kalman_smooth_device(dsmc_ctx* ctx, const dsmc_model_desc* m,
+                                         double* smooth_mean, double* smooth_cov,
+                                         double* log_likelihood) {
+  if (!ctx || !m || !smooth_mean || !smooth_cov) return DSMC_E_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (m->kind != DSMC_MODEL_LGSSM)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "kalman_smooth: LGSSM descriptor required");
+  const int d = m->state_dim, dy = m->obs_dim, K = m->horizon + 1;
+  if (d < 1 || d > 4 || dy < 1 || dy > 4 || m->horizon < 0)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "kalman_smooth: dims must be 1..4");
+  if (!m->m0 || !m->P0 || !m->H || !m->R || !m->y || (K > 1 && (!m->F || !m->b || !m->Q)))
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                   "kalman_smooth: initial, transition and observation arrays are required");
+  Arena& A = ctx->arena;
+  auto s = ctx->stream;
+  void* p;
+  // model arrays (per-time with stride, 0 = one matrix for all times)
+  auto up = [&](const char* name, const void* src, size_t bytes, const void** dst) -> int {
+    if (!src || !bytes) {
+      *dst = nullptr;
+      return DSMC_OK;
+    }
+    CU(A.get(name, bytes, &p));
+    CU(cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, s));
+    *dst = p;
+    return DSMC_OK;
+  };
+  auto span = [&](int64_t st, size_t per) { return (st ? (size_t)K * st : per) * sizeof(double); };
+  KfModel km{};
+  int rc = 0;
+  const void* q;
+  rc |= up("KF_F", m->F, K > 1 ? span(m->F_stride, (size_t)d * d) : 0, &q); km.F = (const double*)q;
+  rc |= up("KF_b", m->b, K > 1 ? span(m->b_stride, (size_t)d) : 0, &q); km.b = (const double*)q;
+  rc |= up("KF_Q", m->Q, K > 1 ? span(m->Q_stride, (size_t)d * d) : 0, &q); km.Q = (const double*)q;
+  rc |= up("KF_H", m->H, span(m->H_stride, (size_t)dy * d), &q); km.H = (const double*)q;
+  rc |= up("KF_R", m->R, span(m->R_stride, (size_t)dy * dy), &q); km.R = (const double*)q;
+  rc |= up("KF_y", m->y, (size_t)K * dy * sizeof(double), &q); km.y = (const double*)q;
+  rc |= up("KF_m0", m->m0, (size_t)d * sizeof(double), &q); km.m0 = (const double*)q;
+  rc |= up("KF_P0", m->P0, (size_t)d * d * sizeof(double), &q); km.P0 = (const double*)q;
+  rc |= up("KF_obs", m->has_obs, m->has_obs ? (size_t)K : 0, &q); km.has_obs = (const uint8_t*)q;
+  if (rc) return rc;
+  km.Fs = m->F_stride;
+  km.bs = m->b_stride;
+  km.Qs = m->Q_stride;
+  km.Hs = m->H_stride;
+  km.Rs = m->R_stride;
+  CU(A.get("KF_OUT", (size_t)K * d * (d + 1) * sizeof(double) + 16, &p));
+  double* dmean = (double*)p;
+  double* dcov = dmean + (size_t)K * d;
+  CU(A.get("KF_MISC", 64, &p));
+  double* dll = (double*)p;
+  int* dbad = (int*)((char*)p + 16);
+  CU(cudaMemsetAsync(p, 0, 64, s));
+  switch (d) {
+    case 1: rc = kalman_device_dy<1>(ctx, dy, km, K, dmean, dcov, dll, dbad); break;
+    case 2: rc = kalman_device_dy<2>(ctx, dy, km, K, dmean, dcov, dll, dbad); break;
+    case 3: rc = kalman_device_dy<3>(ctx, dy, km, K, dmean, dcov, dll, dbad); break;
+    default: rc = kalman_device_dy<4>(ctx, dy, km, K, dmean, dcov, dll, dbad); break;
+  }
+  if (rc) return rc;
+  int bad = 0;
+  double ll = 0;
+  CU(cudaMemcpyAsync(smooth_mean, dmean, (size_t)K * d * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(smooth_cov, dcov, (size_t)K * d * d * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&ll, dll, sizeof ll, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&bad, dbad, sizeof bad, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (bad)
+    return set_err(ctx, DSMC_E_RUNTIME,
+                   "kalman update: covariance is not positive definite (device scan)");
+  if (log_likelihood) *log_likelihood = ll;
+  return DSMC_OK;
+}

@@ -67,6 +67,7 @@ def load_library():
         "dsmc_cross_combine": (i, [vp, vp, C.POINTER(abi.WindowOpts), i, i, C.c_longlong, vp, vp,
                                    vp, vp, vp, vp, vp, vp]),
         "dsmc_model_upload_window": (i, [vp, C.POINTER(abi.ModelDesc), i, i, C.POINTER(vp)]),
+        "dsmc_kalman_smooth_device": (i, [vp, C.POINTER(abi.ModelDesc), dp, dp, dp]),
         "dsmc_window_remap": (i, [vp, i, vp]),
         "dsmc_window_finish": (i, [vp, vp, vp, vp]),
         "dsmc_ffbs_smooth": (i, [vp, C.POINTER(abi.ModelDesc), C.POINTER(abi.FfbsOpts), dp, dp,
@@ -233,6 +234,14 @@ class Engine:
         ms = (C.c_double * 6)()
         n = self.lib.dsmc_last_timings(self.ctx, ms, 6)
         return list(ms[:n])
+
+    def kalman_smooth(self, model):
+        """Kalman/RTS on the device by parallel scans -> (means, covs, loglik)."""
+        K, d = model.horizon + 1, model.d
+        m, P, ll = np.zeros((K, d)), np.zeros((K, d, d)), C.c_double()
+        self._check(self.lib.dsmc_kalman_smooth_device(self.ctx, C.byref(model.desc), abi.dptr(m),
+                                                       abi.dptr(P), C.byref(ll)))
+        return m, P, ll.value
 
     # ------------------------------------------------- time-sharded stages
     # Device buffers are passed as raw pointers (e.g. torch tensor data_ptr()
