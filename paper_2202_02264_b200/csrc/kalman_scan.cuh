@@ -131,19 +131,22 @@ __device__ inline bool solve(double* M, double* B) {
         B[p * Cc + k] = t;
       }
     }
+    // normalise the pivot row (M and B alike), then clear column c elsewhere
     const double inv = 1.0 / M[c * N + c];
+#pragma unroll
+    for (int k = 0; k < N; ++k) M[c * N + k] *= inv;
+#pragma unroll
+    for (int k = 0; k < Cc; ++k) B[c * Cc + k] *= inv;
 #pragma unroll
     for (int r = 0; r < N; ++r) {
       if (r == c) continue;
-      const double f = M[r * N + c] * inv;
+      const double f = M[r * N + c];
       if (f == 0.0) continue;
 #pragma unroll
       for (int k = 0; k < N; ++k) M[r * N + k] = fma(-f, M[c * N + k], M[r * N + k]);
 #pragma unroll
       for (int k = 0; k < Cc; ++k) B[r * Cc + k] = fma(-f, B[c * Cc + k], B[r * Cc + k]);
     }
-#pragma unroll
-    for (int k = 0; k < Cc; ++k) B[c * Cc + k] *= inv;
   }
   return true;
 }

@@ -194,25 +194,31 @@ def _sharded_smooth(backends, comm, K, N, world):
     virtual = len(backends) > 1
 
     def handoff():
+        # virtual ranks: engines run on their own streams and torch on the
+        # current one; drain both before data crosses between them
         if virtual:
             for be in backends.values():
                 be.sync()
+            if torch.cuda.is_available() and getattr(dev, "type", "cpu") == "cuda":
+                torch.cuda.synchronize(dev)
 
     for g in ranks:
         backends[g].window_run(g * Kloc, Kloc)
     # log Z of every block of the current level (all ranks know all of them)
     lnc = torch.zeros(P, dtype=torch.float64, device=dev)
+    cross = torch.zeros((max(P - 1, 1), 2, N), dtype=torch.int32, device=dev)
+    handoff()
     for g in ranks:
         backends[g].root_lnc(lnc[g:g + 1])
     handoff()
     if comm is not None:
         comm.all_reduce_sum(lnc)
-    cross = torch.zeros((max(P - 1, 1), 2, N), dtype=torch.int32, device=dev)
     cidx = {}
     for lev in range(s + 1, L + 1):
         span, half = 1 << lev, 1 << (lev - 1)
         nblocks = K // span
         new_lnc = torch.zeros(nblocks, dtype=torch.float64, device=dev)
+        handoff()
         geo = []
         for k in range(nblocks):
             a, c, bb = k * span, k * span + half, (k + 1) * span - 1
@@ -246,6 +252,7 @@ def _sharded_smooth(backends, comm, K, N, world):
                 xr, colr = slabs[k]
                 l, r = B.cross(gm["c"], lev, k, xl, xr, colr, lnc[2 * k:2 * k + 1],
                                lnc[2 * k + 1:2 * k + 2], new_lnc[k:k + 1])
+                handoff()
                 cross[cidx[(lev, k)], 0] = l
                 cross[cidx[(lev, k)], 1] = r
                 for side, dst, t in ((0, gm["gA"], l), (1, gm["gB"], r)):
@@ -270,7 +277,7 @@ def _sharded_smooth(backends, comm, K, N, world):
         lnc = new_lnc
     if comm is not None and P > 1:
         comm.all_reduce_sum(cross)
-    out = {}
+    roots = {}
     for g in ranks:
         # the window root's map through the cross levels, on the device
         t0 = g * Kloc
@@ -278,6 +285,8 @@ def _sharded_smooth(backends, comm, K, N, world):
         for lev in range(L, s, -1):
             l, r = cross[cidx[(lev, t0 >> lev)]].long()
             M = l[M] if (t0 % (1 << lev)) < (1 << (lev - 1)) else r[M]
-        out[g] = backends[g].finish(M)
+        roots[g] = M.to(torch.int32).contiguous()
+    handoff()
+    out = {g: backends[g].finish(roots[g]) for g in ranks}
     handoff()
     return out, float(lnc[0])
