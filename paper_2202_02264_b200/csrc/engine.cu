@@ -15,11 +15,13 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "ffbs.cuh"
 #include "kalman_scan.cuh"
 #include "pair_tc.cuh"
+#include "wide.cuh"
 #include "dsmc_b200.h"
 
 using namespace dsmc_dev;
@@ -63,6 +65,8 @@ struct dsmc_model_handle {
   dsmc_model_desc desc{};
   int K = 0, d = 1, dy = 1;
   int t_lo = 0, t_hi = 0;  // prepared times (a window upload: [t0, t0 + len + 1))
+  bool wide = false;       // LGSSM on the wide-state FP32 path (d > 4, wide.cuh)
+  WideBufs wb{};           // its per-time constants (device, owned)
   DevModel* models_dev = nullptr;  // [B]
   TimeConst* tc = nullptr;         // [B][K]
   int* bounded = nullptr;          // [B]
@@ -222,8 +226,11 @@ int validate_desc(dsmc_ctx* ctx, const dsmc_model_desc* m) {
   }
   if (m->kind != DSMC_MODEL_LGSSM)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "unknown model kind");
-  if (m->state_dim < 1 || m->state_dim > 4 || m->obs_dim < 1 || m->obs_dim > 4)
-    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "lgssm descriptor: dims must be 1..4");
+  if (m->state_dim < 1 || m->state_dim > 32 || m->obs_dim < 1 || m->obs_dim > 32)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "lgssm descriptor: dims must be 1..32");
+  if (m->state_dim <= 4 && m->obs_dim > 4)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                   "lgssm descriptor: obs_dim > 4 needs the wide path (state_dim > 4)");
   if (!m->m0 || !m->P0 || !m->prop_mean || !m->prop_cov || !m->H || !m->R ||
       !m->y || (m->horizon >= 1 && (!m->F || !m->b || !m->Q)))
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
@@ -255,6 +262,171 @@ int upload(dsmc_ctx* ctx, dsmc_model_handle* h, const T* src, size_t n,
     CU(cudaMemcpyAsync(p, src, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
   *dst = static_cast<const T*>(p);
   return DSMC_OK;
+}
+
+// ------------------------------------------------ wide-state host prep
+// FP64 per-time constants of the wide path (wide.cuh header): Cholesky
+// factors and whitening of the proposal, transition and observation
+// covariances, computed on the host threads (O(K d^3), the model set-up step)
+// and stored FP32 with the padded dimensions DP / DYP.
+namespace widep {
+bool chol(const double* A, int n, double* L) {
+  for (int i = 0; i < n * n; ++i) L[i] = 0.0;
+  for (int j = 0; j < n; ++j) {
+    double s = A[j * n + j];
+    for (int k = 0; k < j; ++k) s -= L[j * n + k] * L[j * n + k];
+    if (!(s > 0.0)) return false;
+    L[j * n + j] = std::sqrt(s);
+    for (int i = j + 1; i < n; ++i) {
+      double v = A[i * n + j];
+      for (int k = 0; k < j; ++k) v -= L[i * n + k] * L[j * n + k];
+      L[i * n + j] = v / L[j * n + j];
+    }
+  }
+  return true;
+}
+void tri_inv(const double* L, int n, double* W) {  // W = L^-1 (lower)
+  for (int i = 0; i < n * n; ++i) W[i] = 0.0;
+  for (int i = 0; i < n; ++i) {
+    W[i * n + i] = 1.0 / L[i * n + i];
+    for (int j = 0; j < i; ++j) {
+      double s = 0.0;
+      for (int k = j; k < i; ++k) s += L[i * n + k] * W[k * n + j];
+      W[i * n + j] = -s / L[i * n + i];
+    }
+  }
+}
+double logdet(const double* L, int n) {
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s += 2.0 * std::log(L[i * n + i]);
+  return s;
+}
+}  // namespace widep
+
+struct WideHost {
+  std::vector<float> L, G, e, c, W, M, v, WP0, dm0;
+  std::vector<double> m;
+  double p0norm = 0.0;
+};
+
+// returns "" or the error message
+std::string prep_wide(const dsmc_model_desc& md, int DP, int DYP, WideHost& o) {
+  const int K = md.horizon + 1, d = md.state_dim, dy = md.obs_dim;
+  const size_t dd = (size_t)d * d;
+  o.L.assign((size_t)K * DP * DP, 0.f);
+  o.G.assign((size_t)K * DYP * DP, 0.f);
+  o.e.assign((size_t)K * DYP, 0.f);
+  o.c.assign(K, 0.f);
+  o.W.assign((size_t)K * DP * DP, 0.f);
+  o.M.assign((size_t)K * DP * DP, 0.f);
+  o.v.assign((size_t)K * DP, 0.f);
+  o.m.assign(md.prop_mean, md.prop_mean + (size_t)K * d);
+  o.WP0.assign((size_t)DP * DP, 0.f);
+  o.dm0.assign(DP, 0.f);
+  const double s = std::sqrt(kLog2E / 2.0);
+  auto at = [](const double* p, int64_t stride, int t) { return p + stride * t; };
+  {  // prior
+    std::vector<double> Lp(dd), Wp(dd);
+    if (!widep::chol(md.P0, d, Lp.data())) return "lgssm: P0 is not positive definite";
+    widep::tri_inv(Lp.data(), d, Wp.data());
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j) o.WP0[i * DP + j] = (float)Wp[i * d + j];
+    for (int i = 0; i < d; ++i) o.dm0[i] = (float)(md.m0[i] - md.prop_mean[i]);
+    o.p0norm = -0.5 * (d * kLog2Pi + widep::logdet(Lp.data(), d));
+  }
+  std::string err;
+  std::mutex mu;
+  auto work = [&](int t_begin, int t_end) {
+    std::vector<double> Lt(dd), Lr((size_t)dy * dy), Wr((size_t)dy * dy), HL((size_t)dy * d);
+    std::vector<double> Lq(dd), Wq(dd), WF(dd);
+    for (int t = t_begin; t < t_end; ++t) {
+      const double* mt = md.prop_mean + (size_t)t * d;
+      if (!widep::chol(md.prop_cov + (size_t)t * dd, d, Lt.data())) {
+        std::lock_guard<std::mutex> g(mu);
+        err = "lgssm: proposal covariance at time " + std::to_string(t) + " is not positive definite";
+        return;
+      }
+      for (int i = 0; i < d; ++i)
+        for (int j = 0; j <= i; ++j) o.L[(size_t)t * DP * DP + i * DP + j] = (float)Lt[i * d + j];
+      const double p_norm = -0.5 * (d * kLog2Pi + widep::logdet(Lt.data(), d));
+      double o_norm = 0.0;
+      const bool obs = md.has_obs ? md.has_obs[t] != 0 : true;
+      if (obs) {
+        const double* H = at(md.H, md.H_stride, t);
+        const double* R = at(md.R, md.R_stride, t);
+        if (!widep::chol(R, dy, Lr.data())) {
+          std::lock_guard<std::mutex> g(mu);
+          err = "lgssm: R at time " + std::to_string(t) + " is not positive definite";
+          return;
+        }
+        widep::tri_inv(Lr.data(), dy, Wr.data());
+        o_norm = -0.5 * (dy * kLog2Pi + widep::logdet(Lr.data(), dy));
+        for (int a = 0; a < dy; ++a)
+          for (int j = 0; j < d; ++j) {
+            double acc = 0.0;
+            for (int l = 0; l < d; ++l) acc += H[a * d + l] * Lt[l * d + j];
+            HL[a * d + j] = acc;
+          }
+        for (int a = 0; a < dy; ++a) {
+          double ea = 0.0;
+          for (int b2 = 0; b2 <= a; ++b2) {
+            double r = md.y[(size_t)t * dy + b2];
+            for (int l = 0; l < d; ++l) r -= H[b2 * d + l] * mt[l];
+            ea += Wr[a * dy + b2] * r;
+          }
+          o.e[(size_t)t * DYP + a] = (float)ea;
+          for (int j = 0; j < d; ++j) {
+            double g = 0.0;
+            for (int b2 = 0; b2 <= a; ++b2) g += Wr[a * dy + b2] * HL[b2 * d + j];
+            o.G[(size_t)t * DYP * DP + a * DP + j] = (float)g;
+          }
+        }
+      }
+      double t_norm = 0.0;
+      if (t >= 1) {
+        const double* F = at(md.F, md.F_stride, t);
+        const double* bb = at(md.b, md.b_stride, t);
+        const double* Q = at(md.Q, md.Q_stride, t);
+        if (!widep::chol(Q, d, Lq.data())) {
+          std::lock_guard<std::mutex> g(mu);
+          err = "lgssm: Q at time " + std::to_string(t) + " is not positive definite";
+          return;
+        }
+        widep::tri_inv(Lq.data(), d, Wq.data());
+        t_norm = -0.5 * (d * kLog2Pi + widep::logdet(Lq.data(), d));
+        const double* mp = md.prop_mean + (size_t)(t - 1) * d;
+        for (int i = 0; i < d; ++i) {
+          double vi = 0.0;
+          for (int j = 0; j <= i; ++j) {
+            o.W[(size_t)t * DP * DP + i * DP + j] = (float)(s * Wq[i * d + j]);
+            // delta_j = (F m_{t-1} + b - m_t)_j
+            double dj = bb[j] - mt[j];
+            for (int l = 0; l < d; ++l) dj += F[j * d + l] * mp[l];
+            vi += Wq[i * d + j] * dj;
+          }
+          o.v[(size_t)t * DP + i] = (float)(s * vi);
+          for (int j = 0; j < d; ++j) {
+            double acc = 0.0;
+            for (int l = 0; l <= i; ++l) acc += Wq[i * d + l] * F[l * d + j];
+            o.M[(size_t)t * DP * DP + i * DP + j] = (float)(s * acc);
+          }
+        }
+      }
+      o.c[t] = (float)(o_norm - p_norm + t_norm);
+    }
+  };
+  const int nth = std::max(1, std::min<int>(std::thread::hardware_concurrency(), K / 64 + 1));
+  std::vector<std::thread> pool;
+  for (int q = 0; q < nth; ++q)
+    pool.emplace_back(work, (int)((long)K * q / nth), (int)((long)K * (q + 1) / nth));
+  for (auto& th : pool) th.join();
+  return err;
+}
+
+int wide_dp(int d) { return d <= 8 ? 8 : d <= 16 ? 16 : 32; }
+bool force_wide() {
+  const char* f = getenv("DSMC_FORCE_WIDE");
+  return f && f[0] == '1';
 }
 
 // Per-time array restricted to times [lo, hi) (time-sharded windows): only
@@ -395,6 +567,37 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
     if (rc) return DSMC_E_CUDA;
   }
   void* p;
+  // wide-state LGSSM (d > 4, or forced for testing): host-prepared constants
+  if (descs[0].kind == DSMC_MODEL_LGSSM && (d > 4 || force_wide())) {
+    if (B != 1 || window)
+      return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                     "state_dim > 4: one unconditional model on the whole horizon");
+    const int DP = wide_dp(d), DYP = (dy + 3) & ~3;
+    WideHost wh;
+    const std::string e = prep_wide(descs[0], DP, DYP, wh);
+    if (!e.empty()) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, e);
+    auto put = [&](const auto& v, auto** dst) -> int {
+      void* q = nullptr;
+      CU(cudaMallocAsync(&q, std::max<size_t>(1, v.size()) * sizeof(v[0]), ctx->stream));
+      h->owned.push_back(q);
+      CU(cudaMemcpyAsync(q, v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice, ctx->stream));
+      *dst = static_cast<std::remove_reference_t<decltype(*dst)>>(q);
+      return DSMC_OK;
+    };
+    WideBufs& wb = h->wb;
+    wb.d = d;
+    wb.dy = dy;
+    wb.DP = DP;
+    wb.DYP = DYP;
+    wb.p0norm = wh.p0norm;
+    int rcw = put(wh.L, &wb.L) | put(wh.G, &wb.G) | put(wh.e, &wb.e) | put(wh.c, &wb.c) |
+              put(wh.W, &wb.W) | put(wh.M, &wb.M) | put(wh.v, &wb.v) | put(wh.m, &wb.m) |
+              put(wh.WP0, &wb.WP0) | put(wh.dm0, &wb.dm0);
+    if (rcw) return rcw;
+    CU(cudaStreamSynchronize(ctx->stream));  // the host vectors die here
+    h->wide = true;
+    h->defer = false;
+  }
   CU(cudaMallocAsync(&p, sizeof(DevModel) * B, ctx->stream));
   h->owned.push_back(p);
   h->models_dev = static_cast<DevModel*>(p);
@@ -408,7 +611,9 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
   h->bounded = static_cast<int*>(p);
   std::vector<int> ones(B, 3);
   CU(cudaMemcpyAsync(p, ones.data(), sizeof(int) * B, cudaMemcpyHostToDevice, ctx->stream));
-  if (h->deferred.empty()) {
+  if (h->deferred.empty() && d > 4) {
+    h->defer = false;  // the TimeConst per-time constants exist for d <= 4 only
+  } else if (h->deferred.empty()) {
     h->defer = false;
     prep_kernel<<<dim3((w_hi - w_lo + 127) / 128, B), 128, 0, ctx->stream>>>(
         h->models_dev, h->tc, K, h->bounded, w_lo, w_hi);
@@ -584,6 +789,51 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
   return DSMC_OK;
 }
 
+// Wide-state combine chunk: prologue (whitened rows / columns into AUX),
+// pass 1 (register-tiled cross term + sub-block log2-sums), sampler.
+template <int D>
+int launch_wide(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systematic) {
+  const int N = b.N;
+  const int nrt = (N + kWRows - 1) / kWRows, nsub = (N + kSub - 1) / kSub;
+  la.aux_comb = (size_t)2 * N * D + 2 * (size_t)N;
+  {
+    void* p;
+    CU(ctx->arena.get("AUXW", la.aux_comb * sizeof(float) * (size_t)nk * b.B, &p));
+    la.aux = (float*)p;
+  }
+  const int target = 148 * 4;
+  int ncs = 1;
+  while (ncs * 2 <= nsub && (long)nk * b.B * nrt * ncs < target) ncs *= 2;
+  int sb = 1;
+  if ((long)nk * b.B < 148 * 2)
+    sb = std::max(1, std::min((la.n_out + 63) / 64, (int)((148 * 2 + nk * b.B - 1) / (nk * b.B))));
+  la.slots_per_cta = (la.n_out + sb - 1) / sb;
+  const size_t sm1 = sizeof(float) * ((size_t)(kWRows + kSub) * WideK<D>::S + kWRows + kSub);
+  const size_t sm2 = sizeof(double) * (((size_t)N + 1) & ~(size_t)1) + sizeof(float) * (size_t)N;
+  if (sm2 > (size_t)ctx->smem_optin - 1024)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "wide combine: N too large for the sampler");
+  cudaEvent_t* ev = nullptr;
+  if (ctx->time_kernels) {  // pair = prologue + pass 1, sample = sampler
+    while ((int)ctx->kev.size() < ctx->kev_used + 3) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      ctx->kev.push_back(e);
+    }
+    ev = &ctx->kev[ctx->kev_used];
+    ctx->kev_used += 3;
+    CU(rec_event(ev[0], ctx->stream));
+  }
+  prologw_kernel<D><<<dim3((N + 127) / 128, nk, b.B), 128, 0, ctx->stream>>>(b, la);
+  LAUNCHED(ctx);
+  pairw_kernel<D><<<dim3(nrt * ncs, nk, b.B), 256, sm1, ctx->stream>>>(b, la);
+  LAUNCHED(ctx);
+  if (ev) CU(rec_event(ev[1], ctx->stream));
+  samplew_kernel<D><<<dim3(sb, nk, b.B), 256, sm2, ctx->stream>>>(b, la, systematic);
+  LAUNCHED(ctx);
+  if (ev) CU(rec_event(ev[2], ctx->stream));
+  return DSMC_OK;
+}
+
 __global__ void tail_copy_kernel(Bufs b, int idx_prev, int idx_next,
                                  const uint32_t* fp, const uint32_t* lp,
                                  uint32_t* fn, uint32_t* ln,
@@ -694,6 +944,12 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
   const bool fp64 = o.precision == DSMC_FP64_PARITY;
   if (!fp64 && h->desc.kind == DSMC_MODEL_LGSSM && o.inj_x)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "leaf injection needs FP64 parity precision");
+  const bool wide = h->wide;
+  if (wide && (fp64 || o.conditional || B != 1 || o.t0 != 0 || K != h->K ||
+               (o.resampler != DSMC_MULTINOMIAL && o.resampler != DSMC_SYSTEMATIC)))
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                   "state_dim > 4 runs the FP32 dense path (multinomial / systematic, "
+                   "unconditional, whole horizon)");
   const int cap = std::max(1, (K + 1) / 2);
   Bufs b{};
   b.K = K;
@@ -719,6 +975,14 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     b.X64 = (double*)p;
     CU(A.get("LW64", BKN * sizeof(double), &p));
     b.LW64 = (double*)p;
+  } else if (wide) {
+    b.w = h->wb;
+    CU(A.get("XW", BKN * h->wb.DP * sizeof(float), &p));
+    b.w.X = (float*)p;
+    CU(A.get("COL", BKN * sizeof(float), &p));
+    b.COL = (float*)p;
+    CU(A.get("LW32", (size_t)B * N * sizeof(float), &p));
+    b.LW32 = (float*)p;
   } else {
     CU(A.get("X32", BKN * sizeof(float4), &p));
     b.X32 = (float4*)p;
@@ -784,6 +1048,17 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
       leafnorm64_kernel<<<dim3(K, B), 32, 0, ctx->stream>>>(b);
       LAUNCHED(ctx);
     }
+  } else if (wide) {
+    CU(A.get("RAW0", (size_t)B * N * sizeof(double), &p));
+    const dim3 lg(K, B);
+    switch (h->wb.DP) {
+      case 8: leafw_kernel<8><<<lg, 256, 0, ctx->stream>>>(b, (double*)p); break;
+      case 16: leafw_kernel<16><<<lg, 256, 0, ctx->stream>>>(b, (double*)p); break;
+      default: leafw_kernel<32><<<lg, 256, 0, ctx->stream>>>(b, (double*)p); break;
+    }
+    LAUNCHED(ctx);
+    leafnorm32_kernel<<<B, 32, 0, ctx->stream>>>(b, (const double*)p);
+    LAUNCHED(ctx);
   } else {
     CU(A.get("RAW0", (size_t)B * N * sizeof(double), &p));
     const int lt = std::min(256, (N + 31) / 32 * 32);
@@ -837,7 +1112,10 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
   const int nsub = (N + kSub - 1) / kSub;
   const size_t ws_comb = fp64 ? (size_t)N * (5 + nsub) : ((size_t)N * nsub + 1) / 2;
   const size_t ws_budget = (size_t)1 << 30;  // bytes per chunk
-  const int chunk = (int)std::max<size_t>(1, std::min<size_t>(65535, ws_budget / (ws_comb * 8 * B)));
+  // bytes per combine of the chunked scratch (the wide path's AUX dominates)
+  const size_t per_comb = std::max<size_t>(ws_comb * 8 * B,
+                                           wide ? ((size_t)2 * N * h->wb.DP + 2 * N) * 4 * B : 0);
+  const int chunk = (int)std::max<size_t>(1, std::min<size_t>(65535, ws_budget / per_comb));
   double* ws = nullptr;
   if (!lazy && T > 0) {
     const int np1 = K / 2;
@@ -906,6 +1184,10 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
              : d == 2     ? launch_c64<kLGN, 2>(ctx, b, la, nk, sys)
              : d == 3     ? launch_c64<kLGN, 3>(ctx, b, la, nk, sys)
                           : launch_c64<kLGN, 4>(ctx, b, la, nk, sys);
+        } else if (wide) {
+          rc = h->wb.DP == 8    ? launch_wide<8>(ctx, b, la, nk, sys)
+             : h->wb.DP == 16 ? launch_wide<16>(ctx, b, la, nk, sys)
+                              : launch_wide<32>(ctx, b, la, nk, sys);
         } else {
           rc = d == 1 ? launch_c32<1>(ctx, b, la, nk, sys)
              : d == 2 ? launch_c32<2>(ctx, b, la, nk, sys)
@@ -1001,6 +1283,15 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
     if (fp64) {
       gather64_kernel<<<dim3(K, B), 256, 0, ctx->stream>>>(b, Mb[mcur], root ? 1 : 0,
                                                            o.paths, o.mean, o.cov, o.root_map);
+    } else if (wide) {
+      const dim3 gg(K, B);
+      const int r1 = root ? 1 : 0;
+      switch (h->wb.DP) {
+        case 8: gatherw_kernel<8><<<gg, 256, 0, ctx->stream>>>(b, Mb[mcur], r1, o.paths, o.mean, o.cov, o.root_map); break;
+        case 16: gatherw_kernel<16><<<gg, 256, 0, ctx->stream>>>(b, Mb[mcur], r1, o.paths, o.mean, o.cov, o.root_map); break;
+        default: gatherw_kernel<32><<<gg, 256, 0, ctx->stream>>>(b, Mb[mcur], r1, o.paths, o.mean, o.cov, o.root_map); break;
+      }
+      LAUNCHED(ctx);
     } else {
       const uint32_t* M1 = Mb[mcur];
       const int r1 = root ? 1 : 0;
@@ -1095,6 +1386,12 @@ cudaError_t configure_d(int smem) {
   set(ffbs_backward_kernel<D>);
   return e;
 }
+template <int D>
+cudaError_t configure_wide(int smem) {
+  cudaError_t e = set_max_dynamic_smem(pairw_kernel<D>, smem);
+  if (e == cudaSuccess) e = set_max_dynamic_smem(samplew_kernel<D>, smem);
+  return e;
+}
 cudaError_t configure_device(int device, int smem) {
   static std::mutex mu;
   static std::vector<int> done;
@@ -1104,6 +1401,9 @@ cudaError_t configure_device(int device, int smem) {
   if (e == cudaSuccess) e = configure_d<2>(smem);
   if (e == cudaSuccess) e = configure_d<3>(smem);
   if (e == cudaSuccess) e = configure_d<4>(smem);
+  if (e == cudaSuccess) e = configure_wide<8>(smem);
+  if (e == cudaSuccess) e = configure_wide<16>(smem);
+  if (e == cudaSuccess) e = configure_wide<32>(smem);
   for (auto fn : {c64_rows<kLG1, 1>, c64_rows<kSV, 1>, c64_rows<kCOX, 1>, c64_rows<kCRW, 1>,
                   c64_rows<kTHETA, 1>}) {
     if (e != cudaSuccess) break;
@@ -1273,6 +1573,7 @@ int dsmc_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
                                  (model->state_dim + 1) * sizeof(double)
                            : 0;
   const bool defer = opts && opts->precision == DSMC_FP32 && model && big >= (32u << 20) &&
+                     model->state_dim <= 4 && !force_wide() &&
                      host_pinned(model->y) && host_pinned(model->prop_mean) &&
                      host_pinned(model->prop_cov);
   int rc = make_handle(ctx, model, 1, &h, defer);
@@ -2346,6 +2647,8 @@ extern "C" int dsmc_ffbs_smooth(dsmc_ctx* ctx, const dsmc_model_desc* model,
   const int N = (int)opts->n_particles, M = (int)opts->n_draws;
   if (N < 1) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "particle filter: need n >= 1");
   if (M < 1) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "ffbs: need n_draws >= 1");
+  if (model->state_dim > 4 || force_wide())
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "ffbs: state_dim > 4 is not supported");
   if (opts->resampler != DSMC_MULTINOMIAL && opts->resampler != DSMC_SYSTEMATIC)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
                    "particle filter: dense resampling only (multinomial or systematic)");

@@ -48,7 +48,7 @@ struct SmoothElem {
 
 // ---- small dense helpers (row-major, compile-time sizes)
 template <int R, int K, int Cc>
-__device__ inline void mm(const double* A, const double* B, double* C) {  // C = A B
+__host__ __device__ inline void mm(const double* A, const double* B, double* C) {  // C = A B
 #pragma unroll
   for (int i = 0; i < R; ++i)
 #pragma unroll
@@ -60,7 +60,7 @@ __device__ inline void mm(const double* A, const double* B, double* C) {  // C =
     }
 }
 template <int R, int K, int Cc>
-__device__ inline void mmT(const double* A, const double* B, double* C) {  // C = A B'
+__host__ __device__ inline void mmT(const double* A, const double* B, double* C) {  // C = A B'
 #pragma unroll
   for (int i = 0; i < R; ++i)
 #pragma unroll
@@ -72,7 +72,7 @@ __device__ inline void mmT(const double* A, const double* B, double* C) {  // C 
     }
 }
 template <int R, int K, int Cc>
-__device__ inline void mTm(const double* A, const double* B, double* C) {  // C = A' B
+__host__ __device__ inline void mTm(const double* A, const double* B, double* C) {  // C = A' B
 #pragma unroll
   for (int i = 0; i < R; ++i)
 #pragma unroll
@@ -84,7 +84,7 @@ __device__ inline void mTm(const double* A, const double* B, double* C) {  // C 
     }
 }
 template <int R, int Cc>
-__device__ inline void mv(const double* A, const double* x, double* y) {
+__host__ __device__ inline void mv(const double* A, const double* x, double* y) {
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     double s = 0.0;
@@ -94,7 +94,7 @@ __device__ inline void mv(const double* A, const double* x, double* y) {
   }
 }
 template <int R, int Cc>
-__device__ inline void mTv(const double* A, const double* x, double* y) {  // A' x
+__host__ __device__ inline void mTv(const double* A, const double* x, double* y) {  // A' x
 #pragma unroll
   for (int i = 0; i < Cc; ++i) {
     double s = 0.0;
@@ -105,7 +105,7 @@ __device__ inline void mTv(const double* A, const double* x, double* y) {  // A'
 }
 // X := M^-1 B for an n x n M (Gauss-Jordan, partial pivoting); M is destroyed
 template <int N, int Cc>
-__device__ inline bool solve(double* M, double* B) {
+__host__ __device__ inline bool solve(double* M, double* B) {
 #pragma unroll
   for (int c = 0; c < N; ++c) {
     int p = c;
@@ -153,7 +153,7 @@ __device__ inline bool solve(double* M, double* B) {
 
 // ---- associative combines
 template <int D>
-__device__ inline void filt_combine(const FiltElem<D>& ei, const FiltElem<D>& ej,
+__host__ __device__ inline void filt_combine(const FiltElem<D>& ei, const FiltElem<D>& ej,
                                     FiltElem<D>& out) {
   double M[D * D], X[D * (2 * D + 1)];
   // M = I + C_i J_j ; X = [A_i | C_i | b_i + C_i eta_j] -> M^-1 X
@@ -224,7 +224,7 @@ __device__ inline void filt_combine(const FiltElem<D>& ei, const FiltElem<D>& ej
 }
 
 template <int D>
-__device__ inline void smooth_combine(const SmoothElem<D>& ei, const SmoothElem<D>& ej,
+__host__ __device__ inline void smooth_combine(const SmoothElem<D>& ei, const SmoothElem<D>& ej,
                                       SmoothElem<D>& out) {
   SmoothElem<D> o;
   mm<D, D, D>(ei.E, ej.E, o.E);
@@ -245,12 +245,12 @@ __device__ inline void smooth_combine(const SmoothElem<D>& ei, const SmoothElem<
 template <int D>
 struct FiltOp {
   using E = FiltElem<D>;
-  __device__ static void apply(const E& run, const E& next, E& out) { filt_combine<D>(run, next, out); }
+  __host__ __device__ static void apply(const E& run, const E& next, E& out) { filt_combine<D>(run, next, out); }
 };
 template <int D>
 struct SmoothOp {
   using E = SmoothElem<D>;
-  __device__ static void apply(const E& run, const E& next, E& out) {
+  __host__ __device__ static void apply(const E& run, const E& next, E& out) {
     smooth_combine<D>(next, run, out);
   }
 };
@@ -289,12 +289,12 @@ struct KfModel {
   int64_t Fs, bs, Qs, Hs, Rs;
   const uint8_t* has_obs;
 };
-__device__ inline const double* at_t(const double* p, int64_t s, int t) { return p + s * t; }
+__host__ __device__ inline const double* at_t(const double* p, int64_t s, int t) { return p + s * t; }
 
 // x := m + K (y - H m) and the gain of an update with prior (m, P):
 // S = H P H' + R, K = P H' S^-1; returns false if S is singular
 template <int D, int DY>
-__device__ inline bool kf_gain(const double* P, const double* H, const double* R, double* K,
+__host__ __device__ inline bool kf_gain(const double* P, const double* H, const double* R, double* K,
                                double* S) {
   double HP[DY * D];
   mm<DY, D, D>(H, P, HP);
@@ -315,9 +315,16 @@ __device__ inline bool kf_gain(const double* P, const double* H, const double* R
 }
 
 template <int D, int DY>
+__host__ __device__ inline void kf_filter_elem(const KfModel& m, int t, FiltElem<D>* el,
+                                               int* bad);
+template <int D, int DY>
 __global__ void kf_filter_elems(KfModel m, int K, FiltElem<D>* el, int* bad) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= K) return;
+  if (t < K) kf_filter_elem<D, DY>(m, t, el, bad);
+}
+template <int D, int DY>
+__host__ __device__ inline void kf_filter_elem(const KfModel& m, int t, FiltElem<D>* el,
+                                               int* bad) {
   FiltElem<D> e;
 #pragma unroll
   for (int k = 0; k < D * D; ++k) e.A[k] = e.C[k] = e.J[k] = 0.0;
@@ -335,7 +342,7 @@ __global__ void kf_filter_elems(KfModel m, int K, FiltElem<D>* el, int* bad) {
     for (int k = 0; k < D * D; ++k) P[k] = m.P0[k];
     if (obs) {
       double Kg[D * DY], S[DY * DY];
-      if (!kf_gain<D, DY>(P, H, R, Kg, S)) atomicExch(bad, 1);
+      if (!kf_gain<D, DY>(P, H, R, Kg, S)) *bad = 1;
       double Hm[DY], res[DY], KS[D * DY], KSK[D * D], kr[D];
       mv<DY, D>(H, bm, Hm);
 #pragma unroll
@@ -371,7 +378,7 @@ __global__ void kf_filter_elems(KfModel m, int K, FiltElem<D>* el, int* bad) {
     return;
   }
   double Kg[D * DY], S[DY * DY];
-  if (!kf_gain<D, DY>(Q, H, R, Kg, S)) atomicExch(bad, 1);
+  if (!kf_gain<D, DY>(Q, H, R, Kg, S)) *bad = 1;
   double IKH[D * D], KH[D * D];
   mm<D, DY, D>(Kg, H, KH);
 #pragma unroll
@@ -399,7 +406,7 @@ __global__ void kf_filter_elems(KfModel m, int K, FiltElem<D>* el, int* bad) {
     for (int k = 0; k < D; ++k) X[r * (D + 1) + k] = HF[r * D + k];
     X[r * (D + 1) + D] = res[r];
   }
-  if (!solve<DY, D + 1>(Sc, X)) atomicExch(bad, 1);
+  if (!solve<DY, D + 1>(Sc, X)) *bad = 1;
   double SHF[DY * D], Sr[DY];
 #pragma unroll
   for (int r = 0; r < DY; ++r) {
@@ -415,10 +422,35 @@ __global__ void kf_filter_elems(KfModel m, int K, FiltElem<D>* el, int* bad) {
 // filtered (b, C) of the prefix -> smoother elements; per-time log-likelihood
 // terms of the predictive y_t ~ N(H m_pred, H P_pred H' + R)
 template <int D, int DY>
+__host__ __device__ inline void kf_smooth_elem(const KfModel& m, int K, int t,
+                                               const FiltElem<D>* filt, SmoothElem<D>* el,
+                                               double* ll_t, int* bad);
+template <int D, int DY>
 __global__ void kf_smooth_elems(KfModel m, int K, const FiltElem<D>* filt, SmoothElem<D>* el,
                                 double* ll_t, int* bad) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= K) return;
+  if (t < K) kf_smooth_elem<D, DY>(m, K, t, filt, el, ll_t, bad);
+}
+// small Cholesky (d <= 4) usable on both sides
+__host__ __device__ inline bool kchol(const double* A, int d, double* L) {
+  for (int i = 0; i < d * d; ++i) L[i] = 0.0;
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double s = A[i * d + j];
+      for (int k = 0; k < j; ++k) s -= L[i * d + k] * L[j * d + k];
+      if (i == j) {
+        if (!(s > 0.0)) return false;
+        L[i * d + i] = sqrt(s);
+      } else {
+        L[i * d + j] = s / L[j * d + j];
+      }
+    }
+  return true;
+}
+template <int D, int DY>
+__host__ __device__ inline void kf_smooth_elem(const KfModel& m, int K, int t,
+                                               const FiltElem<D>* filt, SmoothElem<D>* el,
+                                               double* ll_t, int* bad) {
   const FiltElem<D>& f = filt[t];
   // predictive of time t from the filtered t - 1 (or the prior at t = 0)
   double mp[D], Pp[D * D];
@@ -454,7 +486,7 @@ __global__ void kf_smooth_elems(KfModel m, int K, const FiltElem<D>* filt, Smoot
     mv<DY, D>(H, mp, Hm);
 #pragma unroll
     for (int k = 0; k < DY; ++k) res[k] = m.y[(size_t)t * DY + k] - Hm[k];
-    if (!dchol(S, DY, L)) atomicExch(bad, 1);
+    if (!kchol(S, DY, L)) *bad = 1;
     double ld = 0.0, q = 0.0, z[DY];
 #pragma unroll
     for (int i = 0; i < DY; ++i) {
@@ -492,7 +524,7 @@ __global__ void kf_smooth_elems(KfModel m, int K, const FiltElem<D>* filt, Smoot
     double X[D * D];  // Pp1^-1 (F P) = G'  (P, Pp1 symmetric)
 #pragma unroll
     for (int k = 0; k < D * D; ++k) X[k] = FP[k];
-    if (!solve<D, D>(Pc, X)) atomicExch(bad, 1);
+    if (!solve<D, D>(Pc, X)) *bad = 1;
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll

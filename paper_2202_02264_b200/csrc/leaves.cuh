@@ -8,6 +8,25 @@
 
 namespace dsmc_dev {
 
+// Wide-state FP32 path (5 <= d <= 32, wide.cuh): per-time constants prepared
+// on the host in FP64 and stored as FP32, indexed by GLOBAL time; D = padded
+// dimension (8, 16, 32), DYP = padded observation dimension.
+struct WideBufs {
+  int d, dy, DP, DYP;
+  const float* L;    // [Kt][DP*DP] lower Cholesky of the proposal covariance
+  const float* G;    // [Kt][DYP*DP] R^-1/2 H L
+  const float* e;    // [Kt][DYP] R^-1/2 (y - H m)
+  const float* c;    // [Kt] o_norm - p_norm + t_norm (t = 0: no t_norm)
+  const float* W;    // [Kt][DP*DP] s W_Q (cut t >= 1; s = sqrt(log2e / 2))
+  const float* M;    // [Kt][DP*DP] s W_Q F
+  const float* v;    // [Kt][DP] s W_Q (F m_{t-1} + b - m_t)
+  const double* m;   // [Kt][d] proposal means (un-centring)
+  const float* WP0;  // [DP*DP] inverse Cholesky of P0
+  const float* dm0;  // [DP] m0 - m_0
+  double p0norm;     // -0.5 (d log 2 pi + log det P0)
+  float* X;          // [B][K][N][DP] centred leaf states (run buffer)
+};
+
 struct Bufs {
   int K, T, N, d, B, cap;  // cap: map capacity (blocks) per chain
   int t0;  // global time of local leaf 0 (time-sharded windows; 0 otherwise)
@@ -38,6 +57,7 @@ struct Bufs {
   const double* star;  // [B][K][d] (conditional)
   int leaf_role;       // FP32 leaf stream role (0 = leaf_proposal; the particle
                        // filter draws with filter_step, baselines.cpp:17-20)
+  WideBufs w;          // wide-state path (d > 4)
 };
 
 // Normal number i of a leaf stream (rng.cpp:74-86 via counter addressing:

@@ -1,0 +1,549 @@
+// Wide-state FP32 path: linear-Gaussian models with state dimension
+// 5 <= d <= 32 (the reference's FeynmanKacModel has no bound on state_dim,
+// fk_model.hpp:38; the float4 path of combine32.cuh stops at 4). Templates
+// over the padded dimension D in {8, 16, 32}.
+//
+// Per time t (host-prepared in FP64, stored FP32, engine.cu prep_wide):
+//   L_t  lower Cholesky of the proposal covariance       (x~ = x - m_t = L z)
+//   G_t = Ro H L, e_t = Ro (y - H m), Ro = R^-1/2         (observation)
+//   c_t  o_norm - p_norm + t_norm                         (column constant)
+//   W_t = s W_Q, M_t = s W_Q F, v_t = s W_Q delta_t       (cut t, s = sqrt(log2e/2))
+// so that, exactly as in combine32.cuh, the pair log-weight in log2 units is
+//   w_ij = A_j + B_i + u_i . y_j,  y_j = W x~_j,  A_j = COL_j - |y_j|^2,
+//   nu_i = M x~_i + v, u_i = 2 nu_i, B_i = lw2_i - |nu_i|^2.
+// The cross term u_i . y_j is a real dense contraction at these d: pass 1
+// computes it per 128-row x 64-column tile from shared-memory staged U / Y
+// (register-tiled FFMA, 4 rows x 8 columns per thread) with the exact
+// per-(row, sub-block) max as the exponent shift, then the usual 64-column
+// sub-block log2-sums feed a sampler with the same row CDF / sub-block walk /
+// 64-weight recompute as c32_sample.
+#pragma once
+
+#include "combine32.cuh"
+
+namespace dsmc_dev {
+
+// rows of the pass-1 tile and the row stride of the staged operands
+constexpr int kWRows = 128;
+template <int D>
+struct WideK {
+  static constexpr int S = D + 4;  // padded smem row (floats), float4-aligned
+};
+
+// ---------------------------------------------------------------- leaves
+template <int D>
+__global__ void __launch_bounds__(256) leafw_kernel(Bufs b, double* raw0) {
+  const int t = blockIdx.x, ch = blockIdx.y;
+  const int gt = b.t0 + t;
+  const WideBufs& w = b.w;
+  const int d = w.d, dy = w.dy, N = b.N;
+  __shared__ float sL[D * D], sG[32 * D], se[32], sWP[D * D], sdm[D];
+  __shared__ float sc;
+  for (int i = threadIdx.x; i < D * D; i += blockDim.x) sL[i] = w.L[(size_t)gt * D * D + i];
+  for (int i = threadIdx.x; i < w.DYP * D; i += blockDim.x) sG[i] = w.G[(size_t)gt * w.DYP * D + i];
+  for (int i = threadIdx.x; i < w.DYP; i += blockDim.x) se[i] = w.e[(size_t)gt * w.DYP + i];
+  if (gt == 0) {
+    for (int i = threadIdx.x; i < D * D; i += blockDim.x) sWP[i] = w.WP0[i];
+    for (int i = threadIdx.x; i < D; i += blockDim.x) sdm[i] = w.dm0[i];
+  }
+  if (threadIdx.x == 0) sc = w.c[gt];
+  __syncthreads();
+  const StreamId id = stream_id(b.seeds[ch], 0, (uint64_t)gt, DSMC_ROLE_LEAF_PROPOSAL, 0);
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    // d normals, counter-addressed Box-Muller pairs (normal i uses u64s
+    // 2(i/2), 2(i/2)+1 of the leaf stream, rng.cpp:74-86), i = n d + k
+    float z[D];
+    U64x4 blk;
+    uint64_t have = ~0ull;
+    float r = 0.f, sn = 0.f, cs = 0.f;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      z[k] = 0.f;
+      if (k < d) {
+        const uint64_t i = (uint64_t)n * d + k;
+        if (k == 0 || !(i & 1)) {
+          const uint64_t q = 2 * (i >> 1);
+          if ((q >> 2) != have) {
+            blk = stream_block(id, q >> 2);
+            have = q >> 2;
+          }
+          const float u1 = ((float)(uint32_t)(pick4(blk, (uint32_t)(q & 3)) >> 40) + 0.5f) * 0x1p-24f;
+          const float u2 = (float)(uint32_t)(pick4(blk, (uint32_t)(q & 3) + 1) >> 40) * 0x1p-24f;
+          r = sqrtf(-2.0f * __logf(u1));
+          sincospif(2.0f * u2, &sn, &cs);
+        }
+        z[k] = (i & 1) ? r * sn : r * cs;
+      }
+    }
+    float x[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      float acc = 0.f;
+#pragma unroll
+      for (int l = 0; l <= k; ++l) acc = fmaf(sL[k * D + l], z[l], acc);
+      x[k] = acc;
+    }
+    float zz = 0.f, rr = 0.f;
+#pragma unroll
+    for (int k = 0; k < D; ++k) zz = fmaf(z[k], z[k], zz);
+    for (int a = 0; a < dy; ++a) {
+      float g = se[a];
+#pragma unroll
+      for (int l = 0; l < D; ++l) g = fmaf(-sG[a * D + l], z[l], g);
+      rr = fmaf(g, g, rr);
+    }
+    const float col = (float)kLog2E * (sc + 0.5f * (zz - rr));
+    const size_t off = ((size_t)ch * b.K + t) * N + n;
+    float4* dst = reinterpret_cast<float4*>(w.X + off * D);
+#pragma unroll
+    for (int q = 0; q < D / 4; ++q) dst[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+    b.COL[off] = col;
+    if (gt == 0) {  // raw leaf-0 weight h0 P0 / q0 (log): col / log2e + log P0(x)
+      double qd = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l <= k; ++l) acc += (double)sWP[k * D + l] * ((double)x[l] - (double)sdm[l]);
+        qd += acc * acc;
+      }
+      raw0[(size_t)ch * N + n] = (double)col * kLn2 + w.p0norm - 0.5 * qd;
+    }
+  }
+  if (threadIdx.x == 0 && gt > 0) {  // q_t = nu_t: uniform leaf
+    const size_t o = (size_t)ch * b.K + t;
+    b.LNC[o] = 0.0;
+    b.UNI[o] = 1;
+    b.LWMAX[o] = -log((double)N);
+  }
+}
+
+// ------------------------------------------------------------- prologue
+// Per combine: whitened columns y_j / A_j and rows u_i / B_i (one index per
+// thread for both), into the combine's AUX slice: Y[N][D], U[N][D], A[N], B[N].
+struct AuxW {
+  float* Y;
+  float* U;
+  float* A;
+  float* B;
+};
+template <int D>
+__device__ __forceinline__ AuxW auxw(const LevelArgs& la, size_t comb, int N) {
+  float* base = la.aux + comb * la.aux_comb;
+  AuxW a;
+  a.Y = base;
+  a.U = base + (size_t)N * D;
+  a.A = base + 2 * (size_t)N * D;
+  a.B = base + 2 * (size_t)N * D + N;
+  return a;
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) prologw_kernel(Bufs b, LevelArgs la) {
+  const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
+  const int N = b.N;
+  Side L, R;
+  CombineGeom g;
+  sides(b, la, k, L, R, g);
+  const int gc = b.t0 + g.c;
+  const WideBufs& w = b.w;
+  __shared__ float sW[D * D], sM[D * D], sv[D];
+  for (int i = threadIdx.x; i < D * D; i += blockDim.x) {
+    sW[i] = w.W[(size_t)gc * D * D + i];
+    sM[i] = w.M[(size_t)gc * D * D + i];
+  }
+  for (int i = threadIdx.x; i < D; i += blockDim.x) sv[i] = w.v[(size_t)gc * D + i];
+  __syncthreads();
+  const size_t cslot = (size_t)blockIdx.z * gridDim.y + blockIdx.y;
+  const AuxW ax = auxw<D>(la, cslot, N);
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= N) return;
+  const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
+  float x[D], y[D];
+  {  // column q: right block's first-leaf state
+    const uint32_t p = map_first(b, la, ch, R, q);
+    const float4* src = reinterpret_cast<const float4*>(w.X + (((size_t)ch * b.K + R.t) * N + p) * D);
+#pragma unroll
+    for (int c = 0; c < D / 4; ++c) {
+      const float4 v = src[c];
+      x[4 * c] = v.x;
+      x[4 * c + 1] = v.y;
+      x[4 * c + 2] = v.z;
+      x[4 * c + 3] = v.w;
+    }
+    float nrm = 0.f;
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      float acc = 0.f;
+#pragma unroll
+      for (int l = 0; l <= r; ++l) acc = fmaf(sW[r * D + l], x[l], acc);
+      y[r] = acc;
+      nrm = fmaf(acc, acc, nrm);
+    }
+    const float col = b.COL[((size_t)ch * b.K + R.t) * N + p];
+    float4* dst = reinterpret_cast<float4*>(ax.Y + (size_t)q * D);
+#pragma unroll
+    for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]);
+    ax.A[q] = col - nrm;
+  }
+  {  // row q: left block's last-leaf state
+    const uint32_t p = map_last(b, la, ch, L, q);
+    const float4* src = reinterpret_cast<const float4*>(w.X + (((size_t)ch * b.K + L.t) * N + p) * D);
+#pragma unroll
+    for (int c = 0; c < D / 4; ++c) {
+      const float4 v = src[c];
+      x[4 * c] = v.x;
+      x[4 * c + 1] = v.y;
+      x[4 * c + 2] = v.z;
+      x[4 * c + 3] = v.w;
+    }
+    float nrm = 0.f;
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      float acc = sv[r];
+#pragma unroll
+      for (int l = 0; l < D; ++l) acc = fmaf(sM[r * D + l], x[l], acc);
+      y[r] = 2.f * acc;
+      nrm = fmaf(acc, acc, nrm);
+    }
+    const float lw2 = lnonuni ? b.LW32[(size_t)ch * N + q] : 0.f;
+    float4* dst = reinterpret_cast<float4*>(ax.U + (size_t)q * D);
+#pragma unroll
+    for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]);
+    ax.B[q] = lw2 - nrm;
+  }
+}
+
+// ---------------------------------------------------------------- pass 1
+// Grid (row tiles x column splits, combines, chains), 256 threads: rows
+// [128 rt, +128) of combine k, sub-blocks [sb0, sb1). Thread (ty, tx) owns
+// rows 4 ty .. 4 ty + 3 and columns tx + 8 c (c < 8) of the staged sub-block.
+template <int D>
+__global__ void __launch_bounds__(256) pairw_kernel(Bufs b, LevelArgs la) {
+  constexpr int S = WideK<D>::S;
+  extern __shared__ float wsm[];
+  float* sU = wsm;                    // [128][S]
+  float* sY = sU + kWRows * S;        // [64][S]
+  float* sB = sY + kSub * S;          // [128]
+  float* sA = sB + kWRows;            // [64]
+  const int N = b.N;
+  const int nsub = (N + kSub - 1) / kSub;
+  const int nrt = (N + kWRows - 1) / kWRows;
+  const int rt = blockIdx.x % nrt, cs = blockIdx.x / nrt, ncs = gridDim.x / nrt;
+  const size_t cslot = (size_t)blockIdx.z * gridDim.y + blockIdx.y;
+  const AuxW ax = auxw<D>(la, cslot, N);
+  float* ws = reinterpret_cast<float*>(la.ws) + cslot * la.ws_comb * 2;
+  const int row0 = rt * kWRows;
+  const int tid = threadIdx.x, ty = tid >> 3, tx = tid & 7;
+  for (int e = tid; e < kWRows * (D / 4); e += blockDim.x) {
+    const int r = e / (D / 4), c = e % (D / 4);
+    const int i = row0 + r;
+    const float4 v = i < N ? reinterpret_cast<const float4*>(ax.U + (size_t)i * D)[c]
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(sU + r * S + 4 * c) = v;
+  }
+  for (int r = tid; r < kWRows; r += blockDim.x)
+    sB[r] = row0 + r < N ? ax.B[row0 + r] : -CUDART_INF_F;
+  const int sb0 = cs * nsub / ncs, sb1 = (cs + 1) * nsub / ncs;
+  for (int s = sb0; s < sb1; ++s) {
+    __syncthreads();  // sU / previous sY consumed
+    for (int e = tid; e < kSub * (D / 4); e += blockDim.x) {
+      const int j = e / (D / 4), c = e % (D / 4);
+      const int col = s * kSub + j;
+      const float4 v = col < N ? reinterpret_cast<const float4*>(ax.Y + (size_t)col * D)[c]
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(sY + j * S + 4 * c) = v;
+    }
+    for (int j = tid; j < kSub; j += blockDim.x)
+      sA[j] = s * kSub + j < N ? ax.A[s * kSub + j] : -CUDART_INF_F;
+    __syncthreads();
+    float acc[4][8];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] = 0.f;
+#pragma unroll 2
+    for (int kk = 0; kk < D; kk += 4) {
+      float4 uv[4], yv[8];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) uv[r] = *reinterpret_cast<const float4*>(sU + (4 * ty + r) * S + kk);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) yv[c] = *reinterpret_cast<const float4*>(sY + (tx + 8 * c) * S + kk);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          float a = acc[r][c];
+          a = fmaf(uv[r].x, yv[c].x, a);
+          a = fmaf(uv[r].y, yv[c].y, a);
+          a = fmaf(uv[r].z, yv[c].z, a);
+          a = fmaf(uv[r].w, yv[c].w, a);
+          acc[r][c] = a;
+        }
+    }
+    // exact per-(row, sub-block) max shift, then the log2 sum (8 lanes share
+    // a row: shuffles over tx)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float Bi = sB[4 * ty + r];
+      float m = -CUDART_INF_F;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        acc[r][c] += sA[tx + 8 * c] + Bi;
+        m = fmaxf(m, acc[r][c]);
+      }
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) m = fmaxf(m, __shfl_xor_sync(~0u, m, o));
+      float sum = 0.f;
+      if (m > -CUDART_INF_F) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) sum += ex2(acc[r][c] - m);
+      }
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) sum += __shfl_xor_sync(~0u, sum, o);
+      const int i = row0 + 4 * ty + r;
+      if (tx == 0 && i < N) ws[(size_t)s * N + i] = sum > 0.f ? m + lg2(sum) : -CUDART_INF_F;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- sampler
+// Grid (slot blocks, combines, chains), 256 threads: row log2-totals from the
+// sub-block sums, FP64 row CDF, then per slot: row search, sub-block walk and
+// the recompute of the chosen sub-block's <= 64 weights (D-term dots against
+// the combine's Y / U), as c32_sample.
+template <int D>
+__global__ void __launch_bounds__(256) samplew_kernel(Bufs b, LevelArgs la, int systematic) {
+  extern __shared__ double wsmem[];
+  __shared__ double sh[32];
+  __shared__ float s_g;
+  const int sb = blockIdx.x;
+  const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
+  const int N = b.N;
+  Side L, R;
+  CombineGeom g;
+  sides(b, la, k, L, R, g);
+  const int nsub = (N + kSub - 1) / kSub;
+  const size_t cslot = (size_t)blockIdx.z * gridDim.y + blockIdx.y;
+  const float* ws = reinterpret_cast<const float*>(la.ws) + cslot * la.ws_comb * 2;
+  const AuxW ax = auxw<D>(la, cslot, N);
+  double* S = wsmem;                                          // [N]
+  float* Lrow = reinterpret_cast<float*>(S + ((N + 1) & ~1));  // [N]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float gm = -CUDART_INF_F;
+  for (int i = tid; i < N; i += blockDim.x) {
+    float m = -CUDART_INF_F, acc = 0.f;
+    for (int q = 0; q < nsub; ++q) {
+      const float v = ws[(size_t)q * N + i];
+      if (v == -CUDART_INF_F) continue;
+      if (v > m) {
+        acc = m == -CUDART_INF_F ? 0.f : acc * ex2(m - v);
+        m = v;
+      }
+      acc += ex2(v - m);
+    }
+    const float La = m == -CUDART_INF_F ? -CUDART_INF_F : m + lg2(acc);
+    Lrow[i] = La;
+    gm = fmaxf(gm, La);
+  }
+  for (int o = 16; o; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(~0u, gm, o));
+  if (lane == 0) sh[warp] = gm;
+  __syncthreads();
+  if (tid == 0) {
+    float v = -CUDART_INF_F;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmaxf(v, (float)sh[w]);
+    s_g = v;
+  }
+  __syncthreads();
+  const float G = s_g;
+  if (G == -CUDART_INF_F) {
+    if (tid == 0 && sb == 0) raise_err(b.err, DSMC_E_RUNTIME, g.c, la.level, kReasonZeroTable);
+    return;
+  }
+  const int per = (N + blockDim.x - 1) / blockDim.x;
+  const int i0 = tid * per, i1 = min(N, i0 + per);
+  double seg = 0.0;
+  for (int i = i0; i < i1; ++i) seg += (double)ex2(Lrow[i] - G);
+  const double incl = block_scan_incl(seg, sh);
+  double run = incl - seg;
+  for (int i = i0; i < i1; ++i) {
+    run += (double)ex2(Lrow[i] - G);
+    S[i] = run;
+  }
+  __syncthreads();
+  const double total = S[N - 1];
+  const size_t gidx = (size_t)ch * b.T + la.cursor + k;
+  if (tid == 0 && sb == 0) b.LMW[gidx] = ((double)G + log2(total)) * kLn2;
+  const uint64_t node = static_cast<uint64_t>(k + la.node_off);
+  const StreamId id = stream_id(b.seeds[ch], la.key_level, node, DSMC_ROLE_PAIR_RESAMPLE, 0);
+  double u0 = 0.0, step = 0.0;
+  if (systematic) {
+    u0 = u64_uniform(stream_u64(id, 0));
+    step = total / (double)la.n_out;
+  }
+  uint32_t* PL = b.PL + gidx * N;
+  uint32_t* PR = b.PR + gidx * N;
+  const size_t nbase = ((size_t)ch * b.cap + k) * N;
+  const int m0 = sb * la.slots_per_cta, m1 = min(la.n_out, m0 + la.slots_per_cta);
+  for (int m = m0 + tid; m < m1; m += blockDim.x) {
+    const double pt = systematic ? (u0 + (double)m) * step : u64_uniform(stream_u64(id, m)) * total;
+    int lo = 0, hi = N;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (pt < S[mid]) hi = mid;
+      else lo = mid + 1;
+    }
+    int i = lo < N ? lo : N - 1;
+    const double before = i > 0 ? S[i - 1] : 0.0;
+    while (i > 0 && !(Lrow[i] > -CUDART_INF_F)) --i;
+    const float Li = Lrow[i];
+    const float local0 = (float)((pt - before) / (double)ex2(Li - G));
+    const float local = local0 >= 0.f ? local0 : 0.f;
+    // sub-block walk (relative to the row total)
+    int s = -1, last_pos = 0;
+    float cum = 0.f, before_s = 0.f, wsel = 0.f, Ls_sel = 0.f;
+    for (int q = 0; q < nsub; ++q) {
+      const float v = ws[(size_t)q * N + i];
+      const float e = ex2(v - Li);
+      const float c2 = cum + e;
+      if (s < 0 && e > 0.f) last_pos = q;
+      if (s < 0 && local < c2) {
+        s = q;
+        before_s = cum;
+        wsel = e;
+        Ls_sel = v;
+      }
+      cum = c2;
+    }
+    if (s < 0) {
+      s = last_pos;
+      Ls_sel = ws[(size_t)s * N + i];
+      wsel = ex2(Ls_sel - Li);
+      before_s = cum - wsel;
+    }
+    float frac = wsel > 0.f ? (local - before_s) / wsel : 0.f;
+    frac = fminf(fmaxf(frac, 0.f), 1.f);
+    // recompute the sub-block's weights relative to its sum: 2^(w_ij - L_is)
+    float u[D];
+    const float4* up = reinterpret_cast<const float4*>(ax.U + (size_t)i * D);
+#pragma unroll
+    for (int c = 0; c < D / 4; ++c) {
+      const float4 v = up[c];
+      u[4 * c] = v.x;
+      u[4 * c + 1] = v.y;
+      u[4 * c + 2] = v.z;
+      u[4 * c + 3] = v.w;
+    }
+    const float sh_i = ax.B[i] - Ls_sel;
+    const int j0 = s * kSub, j1 = min(N, j0 + kSub);
+    float c3 = 0.f;
+    int jl = -1, lastpos = j0;
+    for (int j = j0; j < j1; ++j) {
+      const float4* yp = reinterpret_cast<const float4*>(ax.Y + (size_t)j * D);
+      float t = ax.A[j] + sh_i;
+#pragma unroll
+      for (int c = 0; c < D / 4; ++c) {
+        const float4 yv = yp[c];
+        t = fmaf(u[4 * c], yv.x, t);
+        t = fmaf(u[4 * c + 1], yv.y, t);
+        t = fmaf(u[4 * c + 2], yv.z, t);
+        t = fmaf(u[4 * c + 3], yv.w, t);
+      }
+      const float e = ex2(t);
+      if (e > 0.f) lastpos = j;
+      c3 += e;
+      if (jl < 0 && frac < c3) jl = j;
+    }
+    const int j = jl >= 0 ? jl : lastpos;  // spill (rounding): last positive weight
+    PL[m] = (uint32_t)i;
+    PR[m] = (uint32_t)j;
+    la.first_next[nbase + m] = map_first(b, la, ch, L, (uint32_t)i);
+    la.last_next[nbase + m] = map_last(b, la, ch, R, (uint32_t)j);
+  }
+  if (tid == 0 && sb == 0) {
+    const double logn = log((double)N);
+    const bool luni = !L.leaf || b.UNI[(size_t)ch * b.K + L.t];
+    const bool runi = !R.leaf || b.UNI[(size_t)ch * b.K + R.t];
+    const double shift = (luni ? -logn : 0.0) + (runi ? -logn : 0.0);
+    const double ll = block_lnc(b, la, ch, L, g.a);
+    const double rl = block_lnc(b, la, ch, R, g.c);
+    la.blnc_next[(size_t)ch * b.cap + k] = ll + rl + ((double)G + log2(total)) * kLn2 + shift;
+  }
+}
+
+// ----------------------------------------------------------------- gather
+// Level-1 composition + per-time moments: one CTA per (time, chain); chunks of
+// 64 root slots are gathered into shared memory, threads own entries of the
+// mean / upper covariance and accumulate over the chunk.
+template <int D>
+__global__ void __launch_bounds__(256) gatherw_kernel(Bufs b, const uint32_t* M1, int root1,
+                                                      double* paths, double* mean, double* cov,
+                                                      const uint32_t* root_map) {
+  constexpr int NT = D * (D + 1) / 2;
+  constexpr int CH = 64;
+  const int t = blockIdx.x, ch = blockIdx.y;
+  const int N = b.N, d = b.w.d;
+  const int gt = b.t0 + t;
+  __shared__ float sx[CH][D + 1];
+  __shared__ int sk[NT], sl[NT];
+  for (int e = threadIdx.x; e < NT; e += blockDim.x) {  // entry e -> (k, l), k <= l
+    int k = 0, rem = e;
+    while (rem >= D - k) {
+      rem -= D - k;
+      ++k;
+    }
+    sk[e] = k;
+    sl[e] = k + rem;
+  }
+  float s1 = 0.f, acc[(NT + 255) / 256] = {};
+  const float* X = b.w.X + ((size_t)ch * b.K + t) * N * D;
+  const double* mt = b.w.m + (size_t)gt * d;
+  for (int q0 = 0; q0 < N; q0 += CH) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < CH * D; e += blockDim.x) {
+      const int qq = e / D, k = e % D, q = q0 + qq;
+      float v = 0.f;
+      if (q < N) {
+        const uint32_t sg = leaf_sigma(b, ch, t, q, M1, root1, root_map);
+        v = X[(size_t)sg * D + k];
+        if (paths && k < d) paths[(((size_t)ch * b.K + t) * N + q) * d + k] = (double)v + mt[k];
+      }
+      sx[qq][k] = v;
+    }
+    __syncthreads();
+    const int nq = min(CH, N - q0);
+    if (threadIdx.x < D)
+      for (int qq = 0; qq < nq; ++qq) s1 += sx[qq][threadIdx.x];
+#pragma unroll
+    for (int u = 0; u < (NT + 255) / 256; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      if (e < NT) {
+        const int k = sk[e], l = sl[e];
+        float a = acc[u];
+        for (int qq = 0; qq < nq; ++qq) a = fmaf(sx[qq][k], sx[qq][l], a);
+        acc[u] = a;
+      }
+    }
+  }
+  __shared__ double smu[D];
+  if (threadIdx.x < D) smu[threadIdx.x] = (double)s1 / N;
+  __syncthreads();
+  const size_t o = (size_t)ch * b.K + t;
+  if (mean && threadIdx.x < d) mean[o * d + threadIdx.x] = smu[threadIdx.x] + mt[threadIdx.x];
+  if (cov) {
+#pragma unroll
+    for (int u = 0; u < (NT + 255) / 256; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      if (e < NT) {
+        const int k = sk[e], l = sl[e];
+        if (k < d && l < d) {
+          const double v = (double)acc[u] / N - smu[k] * smu[l];
+          cov[o * d * d + k * d + l] = v;
+          cov[o * d * d + l * d + k] = v;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace dsmc_dev

