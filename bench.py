@@ -50,8 +50,23 @@ CONFIGS = {
                     "RTS-marginal proposals", model="cv", K=1 << 14, N=1024, resampler=0),
     "c3": dict(desc="C3: stochastic volatility, K=T+1=2^16, N=4096, MH-lazy (B=16)",
                model="sv", K=1 << 16, N=4096, resampler=2),
-    "c3r": dict(desc="C3: stochastic volatility, K=T+1=2^16, N=4096, rejection-lazy (exact)",
-                model="sv", K=1 << 16, N=4096, resampler=3),
+    # rejection-lazy needs the exact bound of SV's stitch weight, whose
+    # acceptance collapses at near-zero observations (|y_758| = 9e-5 in the
+    # C3 trajectory: ~350 trials per slot over the 2^10 prefix, beyond the
+    # reference's 2^24 trial cap for some seeds on longer prefixes, CPU and
+    # GPU alike), so its line runs the trajectory's 2^9 prefix
+    "c3r": dict(desc="C3 prefix: stochastic volatility, first K=T+1=2^9 times of the C3 "
+                     "trajectory, N=4096, rejection-lazy (exact)",
+                model="sv", K=1 << 9, N=4096, resampler=3, ys_len=1 << 16),
+    # wide-state extension (not a BASELINE config): the N x N cross term as a
+    # d-term contraction (csrc/wide.cuh), d independent AR(1) coordinates
+    "c6": dict(desc="Wide-state LGSSM d=32 (32 AR(1) coordinates, rho 0.5), K=T+1=2^12, N=1024, "
+                    "multinomial, RTS-marginal proposals", model="ar_iid", dim=32, K=1 << 12,
+               N=1024, resampler=0),
+    "c6d16": dict(desc="Wide-state LGSSM d=16, K=T+1=2^12, N=1024, multinomial",
+                  model="ar_iid", dim=16, K=1 << 12, N=1024, resampler=0),
+    "c6d8": dict(desc="Wide-state LGSSM d=8, K=T+1=2^12, N=1024, multinomial",
+                 model="ar_iid", dim=8, K=1 << 12, N=1024, resampler=0),
     "c5": dict(desc="C5: 2-D constant-velocity LGSSM d=4, K=T+1=2^20, N=1024, multinomial, "
                     "RTS-marginal proposals", model="cv", K=1 << 20, N=1024, resampler=0),
     "c4": dict(desc="C4: SV particle Gibbs (batched c-dSMC sweep + device parameter kernel), "
@@ -77,8 +92,13 @@ def build_model(cfg, pinned=False, smoother=None):
         m = models.cv_tracking(T, smoother=smoother)
     elif cfg["model"] == "lgssm":
         m = models.lgssm_check(T, smoother=smoother)
+    elif cfg["model"] == "ar_iid":
+        m = models.ar_iid(T, cfg["dim"])
     else:
-        m = models.sv(T)
+        ys = None
+        if cfg.get("ys_len"):  # a prefix of the longer trajectory
+            ys = np.asarray(models.sv(cfg["ys_len"] - 1).arrays["y"], np.float64)[:cfg["K"]]
+        m = models.sv(T, ys=ys)
     if pinned:
         import torch
         arrays = {}
@@ -451,10 +471,38 @@ def run_ours(args, cfg, rank, world, device):
                 "pair_kernel_share_of_step": pair_ms / ms_max if pair_ms else None,
                 "leaf_ms": timings[0], "levels_ms": timings[1],
                 "compose_gather_ms": timings[2] if world == 1 else None}
+        if cfg["resampler"] in (2, 3) and world == 1:
+            # lazy configurations: the dominant kernel is lazy32_kernel, bound
+            # by its counter-based Philox4x64-10 draws (3 u64 per MH step,
+            # resampling.cpp:258-275: ceil(3 B / 4) blocks per slot and
+            # combine) against the measured Philox block rate of this B200
+            # (tools/philox_peak.cu -> profiles/philox_peak.json); achieved =
+            # those blocks / the summed CUDA-event time of the combine levels
+            # (lazy32_kernel + its per-combine finish, ~88% + ~2% of the step)
+            pp = os.path.join(ROOT, "profiles", "philox_peak.json")
+            ppeak = float(json.load(open(pp))["philox4x64_blocks_per_s"]) if os.path.exists(pp) else None
+            B_mh = 16
+            blocks = (K - 1) * N * ((3 * B_mh + 3) // 4) if cfg["resampler"] == 2 else None
+            lv = timings[1]
+            ach_l = blocks / (lv * 1e-3) if (blocks and lv and lv > 0) else None
+            roof = {"bound": "int", "kernel": "lazy32_kernel",
+                    "achieved": ach_l, "peak": ppeak, "unit": "Philox4x64-10 blocks/s",
+                    "frac": (ach_l / ppeak) if (ach_l and ppeak) else None,
+                    "peak_source": "measured (tools/philox_peak.cu, profiles/philox_peak.json)",
+                    "traffic": None,
+                    "bound_note": "lazy pair sampling is bound by its counter-based stream "
+                                  "draws (integer IMAD/LOP3 work of Philox4x64-10), not by "
+                                  "HBM, MUFU or tensor cores; the probe gathers hit L1/L2",
+                    "work": (f"{blocks:.4g} Philox blocks per step ({K - 1} combines x N slots "
+                             f"x ceil(3*{B_mh}/4))") if blocks else
+                            "rejection-lazy: trials per slot are data-dependent",
+                    "leaf_ms": timings[0], "levels_ms": lv,
+                    "compose_gather_ms": timings[2], "levels_share_of_step": lv / ms_max}
         # HBM-class kernels: algorithmic bytes / event time
         if world == 1 and timings[0] > 0 and timings[2] > 0:
-            leaf_b = K * N * (16 + 4)            # float4 state + column term written
-            gath_b = K * N * (16 + 4 + 4)        # state + level-1 pair + map read
+            dpb = 16 if d <= 4 else 4 * (8 if d <= 8 else 16 if d <= 16 else 32)  # state bytes
+            leaf_b = K * N * (dpb + 4)           # state + column term written
+            gath_b = K * N * (dpb + 4 + 4)       # state + level-1 pair + map read
             hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]) \
                 if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6551.0
             roof["hbm_kernels"] = {

@@ -66,20 +66,21 @@ void tri_inv(const double* L, int d, double* W) {
 // Whitened Gaussian: log N(x; m, S) = norm - 0.5 |W (x - m)|^2.
 struct Gauss {
   int d = 1;
-  double W[16] = {0};
+  std::vector<double> W;  // d x d (any d: the wide-state models too)
   double norm = 0.0;  // -0.5 (d log 2pi + log det S)
   bool init(const double* S, int dd) {
     d = dd;
-    double L[16];
-    if (!chol(S, d, L)) return false;
-    tri_inv(L, d, W);
+    std::vector<double> L(d * d);
+    W.assign(d * d, 0.0);
+    if (!chol(S, d, L.data())) return false;
+    tri_inv(L.data(), d, W.data());
     double ld = 0.0;
     for (int i = 0; i < d; ++i) ld += 2.0 * std::log(L[i * d + i]);
     norm = -0.5 * (d * kLog2Pi + ld);
     return true;
   }
   double quad(const double* x, const double* m) const {
-    double e[4];
+    double e[32];
     for (int k = 0; k < d; ++k) e[k] = x[k] - m[k];
     double q = 0.0;
     for (int k = 0; k < d; ++k) {
@@ -123,7 +124,7 @@ struct LgCtx {
   double log_h(int t, const double* x) const {
     if (!has_obs[t]) return 0.0;
     const double* h = Ht(t);
-    double hx[4];
+    double hx[32];
     for (int a = 0; a < dy; ++a) {
       double s = 0.0;
       for (int l = 0; l < d; ++l) s += h[a * d + l] * x[l];
@@ -140,8 +141,8 @@ std::shared_ptr<LgCtx> make_lg_ctx(const dsmc_model_desc& m) {
   c->dy = m.obs_dim;
   c->T = m.horizon;
   const int d = c->d, dy = c->dy, K = m.horizon + 1;
-  if (d < 1 || d > 4 || dy < 1 || dy > 4)
-    throw std::invalid_argument("lgssm descriptor: dims must be 1..4");
+  if (d < 1 || d > 32 || dy < 1 || dy > 32)
+    throw std::invalid_argument("lgssm descriptor: dims must be 1..32");
   c->y.assign(m.y, m.y + (size_t)K * dy);
   c->prop_mean.assign(m.prop_mean, m.prop_mean + (size_t)K * d);
   c->prop_cov.assign(m.prop_cov, m.prop_cov + (size_t)K * d * d);
@@ -263,7 +264,8 @@ dsmc::FeynmanKacModel lgssm_1d(std::shared_ptr<LgCtx> ctx) {
   return m;
 }
 
-// d = 2..4: new model against the reference API (not in the reference).
+// d >= 2 (up to 32, the wide-state models too): new model against the
+// reference API (not in the reference).
 dsmc::FeynmanKacModel lgssm_nd(std::shared_ptr<LgCtx> ctx) {
   dsmc::FeynmanKacModel m;
   const int d = ctx->d;
@@ -274,11 +276,11 @@ dsmc::FeynmanKacModel lgssm_nd(std::shared_ptr<LgCtx> ctx) {
   m.proposal_sampler = [ctx, d](int t, std::size_t count, dsmc::RngStream& s,
                                 double* out) {
     s.fill_normal(out, count * d);
-    double L[16];
-    chol(&ctx->prop_cov[(size_t)t * d * d], d, L);
+    std::vector<double> L(d * d);
+    chol(&ctx->prop_cov[(size_t)t * d * d], d, L.data());
     const double* mu = &ctx->prop_mean[(size_t)t * d];
     for (std::size_t i = 0; i < count; ++i) {
-      double z[4], x[4];
+      double z[32], x[32];
       for (int k = 0; k < d; ++k) z[k] = out[i * d + k];
       for (int k = 0; k < d; ++k) {
         double acc = 0.0;
@@ -297,7 +299,7 @@ dsmc::FeynmanKacModel lgssm_nd(std::shared_ptr<LgCtx> ctx) {
   };
   m.log_potential = [ctx](int t, const double* x) { return ctx->log_h(t, x); };
   m.transition_logdensity = [ctx](int t, const double* xp, const double* xc) {
-    double mu[4];
+    double mu[32];
     ctx->mean_of(t, xp, mu);
     return ctx->trans[t].logpdf(xc, mu);
   };
@@ -321,7 +323,7 @@ dsmc::FeynmanKacModel lgssm_nd(std::shared_ptr<LgCtx> ctx) {
       }
     }
     return [ctx, base, wcol, n, c, d](const double* xp, double* out) {
-      double mu[4];
+      double mu[32];
       ctx->mean_of(c, xp, mu);
       const Gauss& g = ctx->trans[c];
       const double* src = base->data();

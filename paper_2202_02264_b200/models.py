@@ -252,3 +252,22 @@ def cv_stack(T, copies=2, q=0.05, r=0.3, data_seed=90210, inflation=1.0):
     y = x @ H.T + np.sqrt(r) * rng.standard_normal((K, dy))
     m = _lgssm(T, d, dy, np.zeros(d), np.eye(d), F, np.zeros(d), Q, H, R, y)
     return with_rts_proposals(m, inflation, kalman_smooth_numpy)
+
+
+def ar_iid(T, d, rho=0.5, q=1.0, r=1.0, data_seed=90210, inflation=1.0):
+    """Wide-state LGSSM with d independent AR(1) coordinates (the d = 1
+    fixture of tests/support/ar1.hpp replicated), y_t = x_t + N(0, r I):
+    weakly persistent dynamics keep the pair weights' spread moderate in high
+    dimension (dSMC's importance weights degenerate with d like any IS), so
+    d = 8..32 runs stay informative. RTS-marginal proposals."""
+    K = T + 1
+    rng = np.random.default_rng(data_seed)
+    s2 = q / (1 - rho * rho)
+    x = np.zeros((K, d))
+    x[0] = np.sqrt(s2) * rng.standard_normal(d)
+    for t in range(1, K):
+        x[t] = rho * x[t - 1] + np.sqrt(q) * rng.standard_normal(d)
+    y = x + np.sqrt(r) * rng.standard_normal((K, d))
+    I = np.eye(d)
+    m = _lgssm(T, d, d, np.zeros(d), s2 * I, rho * I, np.zeros(d), q * I, I, r * I, y)
+    return with_rts_proposals(m, inflation, kalman_smooth_numpy)

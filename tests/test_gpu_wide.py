@@ -1,8 +1,10 @@
 """Wide-state FP32 path (5 <= d <= 32, csrc/wide.cuh): linear-Gaussian
 models beyond the float4 layout (VERDICT r1 missing 3; the reference's
-FeynmanKacModel has no bound on state_dim, fk_model.hpp:38). Stacked 2-D
-constant-velocity trackers (models.cv_stack: d = 8, 16, 32) against the exact
-Kalman/RTS smoother, in the seed-averaged standard-error units of
+FeynmanKacModel has no bound on state_dim, fk_model.hpp:38). d independent
+AR(1) coordinates (models.ar_iid: d = 8, 16, 32; stacked CV trackers make
+every dSMC run, the CPU reference's included, collapse onto one path at
+d = 8) against the exact Kalman/RTS smoother and the compiled CPU
+reference, in the seed-averaged standard-error units of
 test_gpu_stat.py::test_cv_d4_means_match_kalman (test_smoother.cpp:292-341);
 and the wide kernels forced on the d = 4 model (DSMC_FORCE_WIDE) against the
 float4 path."""
@@ -24,9 +26,13 @@ def _seed_avg(engine, m, N, seeds):
     return means.mean(0), means.std(0, ddof=1) / np.sqrt(len(seeds)), runs
 
 
-@pytest.mark.parametrize("copies,T,N", [(2, 127, 1024), (4, 63, 1024), (8, 31, 1024)])
-def test_wide_means_match_kalman(engine, copies, T, N):
-    m = models.cv_stack(T, copies)
+@pytest.mark.parametrize("d", [8, 16, 32])
+def test_wide_means_match_kalman(engine, d):
+    """d independent AR(1) coordinates (models.ar_iid, rho = 0.5): smoothed
+    means in seed-averaged SE units, per-time variances, and log Z against
+    the exact Kalman/RTS answers."""
+    T, N = 127, 1024
+    m = models.ar_iid(T, d)
     km, kP, ll = models.kalman_smooth_numpy(m)
     avg, se, runs = _seed_avg(engine, m, N, range(16))
     z = (avg - km) / np.maximum(se, 1e-12)
@@ -34,19 +40,37 @@ def test_wide_means_match_kalman(engine, copies, T, N):
     assert np.mean(np.abs(z) > 4.0) < 0.01
     assert np.abs(z).max() < 10.0
     r = runs[0]
-    assert r["mean"].shape == (T + 1, 4 * copies) and r["cov"].shape == (T + 1, 4 * copies, 4 * copies)
-    assert np.isfinite(r["cov"]).all()
-    # posterior variances: median ratio to the exact ones near 1 (degeneracy
-    # shrinks single-run variances, as at d = 4)
-    ratio = np.einsum("tii->ti", r["cov"]) / np.einsum("tii->ti", kP)
-    assert 0.5 < np.median(ratio) < 1.2, np.median(ratio)
+    assert r["mean"].shape == (T + 1, d) and r["cov"].shape == (T + 1, d, d)
+    ratio = np.einsum("tii->ti", np.stack([x["cov"] for x in runs]).mean(0)) / np.einsum("tii->ti", kP)
+    assert 0.75 < np.median(ratio) < 1.1, np.median(ratio)
     lz = np.array([x["log_norm_const"] for x in runs])
     lme = np.log(np.mean(np.exp(lz - lz.max()))) + lz.max()
-    assert abs(lme - ll) < 3.0 * copies, (lme, ll)
+    assert abs(lme - ll) < 3.0, (lme, ll)
+
+
+def test_wide_matches_cpu_reference(engine, reference):
+    """The same d = 16 model through the compiled reference's run_smoother
+    (FP64, scalar callbacks + chained gaussian_row fast path, oracle/
+    ref_models.cpp) and the wide FP32 path: 8-seed log Z and per-time
+    mean averages agree within Monte Carlo error."""
+    T, N, d = 63, 1024, 16
+    m = models.ar_iid(T, d)
+    ref = [reference.run_smoother(m, N, abi.MULTINOMIAL, seed=s, threads=8) for s in range(8)]
+    gpu = [engine.smooth(m, N, abi.MULTINOMIAL, seed=100 + s, precision=abi.FP32)
+           for s in range(8)]
+    la = np.array([x["log_norm_const"] for x in ref])
+    lb = np.array([x["log_norm_const"] for x in gpu])
+    se = np.sqrt(la.var(ddof=1) / 8 + lb.var(ddof=1) / 8)
+    assert abs(la.mean() - lb.mean()) < 5 * se + 0.05, (la.mean(), lb.mean(), se)
+    ma = np.stack([x["paths"].mean(1) for x in ref])
+    mb = np.stack([x["mean"] for x in gpu])
+    z = (ma.mean(0) - mb.mean(0)) / np.sqrt(ma.var(0, ddof=1) / 8 + mb.var(0, ddof=1) / 8 + 1e-12)
+    assert np.sqrt(np.mean(z ** 2)) < 2.0
+    assert np.abs(z).max() < 8.0
 
 
 def test_wide_rejects_unsupported_modes(engine):
-    m = models.cv_stack(15, 2)
+    m = models.ar_iid(15, 8)
     for kw in (dict(precision=abi.FP64_PARITY), dict(resampler=abi.MH_LAZY)):
         args = dict(resampler=abi.MULTINOMIAL, precision=abi.FP32)
         args.update(kw)
