@@ -825,7 +825,16 @@ int launch_wide(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemat
   }
   prologw_kernel<D><<<dim3((N + 127) / 128, nk, b.B), 128, 0, ctx->stream>>>(b, la);
   LAUNCHED(ctx);
-  pairw_kernel<D><<<dim3(nrt * ncs, nk, b.B), 256, sm1, ctx->stream>>>(b, la);
+  // the d-term cross term on the tensor cores (tcgen05, 3xTF32) by default;
+  // DSMC_WIDE_PAIR=fma selects the register-tiled CUDA-core kernel
+  static const bool fma_pair = [] {
+    const char* e = getenv("DSMC_WIDE_PAIR");
+    return e && strcmp(e, "fma") == 0;
+  }();
+  if (fma_pair)
+    pairw_kernel<D><<<dim3(nrt * ncs, nk, b.B), 256, sm1, ctx->stream>>>(b, la);
+  else
+    pairw_tc_kernel<D><<<dim3(nrt * ncs, nk, b.B), 128, WideTc<D>::SMEM, ctx->stream>>>(b, la);
   LAUNCHED(ctx);
   if (ev) CU(rec_event(ev[1], ctx->stream));
   samplew_kernel<D><<<dim3(sb, nk, b.B), 256, sm2, ctx->stream>>>(b, la, systematic);
@@ -1390,6 +1399,7 @@ template <int D>
 cudaError_t configure_wide(int smem) {
   cudaError_t e = set_max_dynamic_smem(pairw_kernel<D>, smem);
   if (e == cudaSuccess) e = set_max_dynamic_smem(samplew_kernel<D>, smem);
+  if (e == cudaSuccess) e = set_max_dynamic_smem(pairw_tc_kernel<D>, smem);
   return e;
 }
 cudaError_t configure_device(int device, int smem) {

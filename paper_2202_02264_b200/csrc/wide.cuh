@@ -19,7 +19,7 @@
 // 64-weight recompute as c32_sample.
 #pragma once
 
-#include "combine32.cuh"
+#include "pair_tc.cuh"  // tcgen05 / mbarrier primitives
 
 namespace dsmc_dev {
 
@@ -544,6 +544,186 @@ __global__ void __launch_bounds__(256) gatherw_kernel(Bufs b, const uint32_t* M1
       }
     }
   }
+}
+
+// ------------------------------------------------- pass 1 on tcgen05 (wide)
+// The cross term of a 128-row x 64-column tile as one tcgen05 MMA chain:
+//   D[128 x 64] (TMEM, FP32) = A_rows[128 x 3D] . B_cols[64 x 3D]^T,
+//   A_i = [u_hi, u_lo, u_hi], B_j = [y_hi, y_hi, y_lo]  (3xTF32, kind::tf32,
+// K-major shared-memory operands without swizzle, the layout of pair_tc.cuh),
+// so D_ij = u_i . y_j to ~FP32 accuracy (the dropped u_lo y_lo is ~2^-22
+// relative). One elected thread issues the 3D / 8 MMAs of a sub-block and
+// commits them to an mbarrier; each of the 128 threads then owns one row
+// (TMEM lane): two tcgen05.ld.32x32b.x32 bring its 64 values to registers,
+// and the epilogue adds A_j + B_i and takes the exact-max log2-sum on the SM
+// (MUFU.EX2) — the same sub-block sums as pairw_kernel, with the d-term
+// contraction moved off the FMA pipe. This is the north-star rule: tensor
+// cores once the cross term is a real dense contraction (d >= 8 here).
+template <int D>
+struct WideTc {
+  static constexpr int K = 3 * D;         // 3xTF32
+  static constexpr int KC = K / 4;        // 16-byte chunks per operand row
+  static constexpr int LBO = 128;         // bytes between K-adjacent core matrices
+  static constexpr int SBO = KC * 128;    // bytes between 8-row groups
+  static constexpr int KS = K / 8;        // MMAs per tile (K = 8 per tf32 MMA)
+  static constexpr int A_BYTES = kWRows / 8 * SBO;
+  static constexpr int B_BYTES = kSub / 8 * SBO;
+  static constexpr int SMEM = A_BYTES + B_BYTES + 64 * 4 + 64;  // + A_j + barrier/tmem slot
+};
+
+template <int D>
+__device__ __forceinline__ void wtc_store_row(uint8_t* base, int r, const float* vals) {
+  using L = WideTc<D>;
+  uint8_t* p = base + (r & 7) * 16 + (r >> 3) * L::SBO;
+#pragma unroll
+  for (int c = 0; c < L::KC; ++c)
+    *reinterpret_cast<float4*>(p + c * L::LBO) =
+        make_float4(vals[4 * c], vals[4 * c + 1], vals[4 * c + 2], vals[4 * c + 3]);
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) pairw_tc_kernel(Bufs b, LevelArgs la) {
+  using L = WideTc<D>;
+  extern __shared__ __align__(1024) uint8_t wtc_smem[];
+  uint8_t* sA = wtc_smem;
+  uint8_t* sB = sA + L::A_BYTES;
+  float* sAj = reinterpret_cast<float*>(sB + L::B_BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sAj + 64);
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bar + 1);
+  const int N = b.N;
+  const int nsub = (N + kSub - 1) / kSub;
+  const int nrt = (N + kWRows - 1) / kWRows;
+  const int rt = blockIdx.x % nrt, cs = blockIdx.x / nrt, ncs = gridDim.x / nrt;
+  const size_t cslot = (size_t)blockIdx.z * gridDim.y + blockIdx.y;
+  const AuxW ax = auxw<D>(la, cslot, N);
+  float* ws = reinterpret_cast<float*>(la.ws) + cslot * la.ws_comb * 2;
+  const int row0 = rt * kWRows;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(s_tmem)),
+                 "r"(64));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  // row operand: [u_hi, u_lo, u_hi] of row `tid`
+  const int i = row0 + tid;
+  float Bi = -CUDART_INF_F;
+  {
+    float vals[3 * D];
+    float u[D];
+    if (i < N) {
+      const float4* up = reinterpret_cast<const float4*>(ax.U + (size_t)i * D);
+#pragma unroll
+      for (int c = 0; c < D / 4; ++c) {
+        const float4 v = up[c];
+        u[4 * c] = v.x;
+        u[4 * c + 1] = v.y;
+        u[4 * c + 2] = v.z;
+        u[4 * c + 3] = v.w;
+      }
+      Bi = ax.B[i];
+    } else {
+#pragma unroll
+      for (int c = 0; c < D; ++c) u[c] = 0.f;
+    }
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const float hi = tf32_hi(u[c]);
+      vals[c] = hi;
+      vals[D + c] = u[c] - hi;
+      vals[2 * D + c] = hi;
+    }
+    wtc_store_row<D>(sA, tid, vals);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *s_tmem;
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kSub >> 3) << 17) |
+                         ((uint32_t)(kWRows >> 4) << 24);
+  const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
+  const int sb0 = cs * nsub / ncs, sb1 = (cs + 1) * nsub / ncs;
+  uint32_t phase = 0;
+  for (int s = sb0; s < sb1; ++s) {
+    // column operand: threads 0-63 one column each; 64-127 the A_j
+    if (tid < kSub) {
+      const int j = s * kSub + tid;
+      float y[D], vals[3 * D];
+      if (j < N) {
+        const float4* yp = reinterpret_cast<const float4*>(ax.Y + (size_t)j * D);
+#pragma unroll
+        for (int c = 0; c < D / 4; ++c) {
+          const float4 v = yp[c];
+          y[4 * c] = v.x;
+          y[4 * c + 1] = v.y;
+          y[4 * c + 2] = v.z;
+          y[4 * c + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < D; ++c) y[c] = 0.f;
+      }
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const float hi = tf32_hi(y[c]);
+        vals[c] = hi;
+        vals[D + c] = hi;
+        vals[2 * D + c] = y[c] - hi;
+      }
+      wtc_store_row<D>(sB, tid, vals);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    } else {
+      const int j = s * kSub + (tid - kSub);
+      sAj[tid - kSub] = j < N ? ax.A[j] : -CUDART_INF_F;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (tid == 0) {
+#pragma unroll
+      for (int ks = 0; ks < L::KS; ++ks) {
+        const uint64_t da = umma_sdesc(smem_u32(sA) + ks * 2 * L::LBO, L::LBO, L::SBO);
+        const uint64_t db = umma_sdesc(smem_u32(sB) + ks * 2 * L::LBO, L::LBO, L::SBO);
+        const uint32_t acc = ks > 0;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+              smem_u32(bar)));
+    }
+    mbar_wait(smem_u32(bar), phase);
+    phase ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    float v[64];
+    tmem_ld32(tmem + lane_off, v);
+    tmem_ld32(tmem + lane_off + 32, v + 32);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    float m = -CUDART_INF_F;
+#pragma unroll
+    for (int c = 0; c < 64; ++c) {
+      v[c] += sAj[c] + Bi;
+      m = fmaxf(m, v[c]);
+    }
+    float sum = 0.f;
+    if (m > -CUDART_INF_F) {
+#pragma unroll
+      for (int c = 0; c < 64; ++c) sum += ex2(v[c] - m);
+    }
+    if (i < N) ws[(size_t)s * N + i] = sum > 0.f ? m + lg2(sum) : -CUDART_INF_F;
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();  // TMEM, sB and sAj free for the next sub-block
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
 }
 
 }  // namespace dsmc_dev
