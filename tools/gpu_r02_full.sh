@@ -15,12 +15,19 @@ done
 for c in c6d8 c6d16; do
   timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-fp64 --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err
 done
-DSMC_NO_GRAPH=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
-  --log-file $O/launches_c5.csv python tools/prof_run.py --config c5 --reps 1 > $O/ncu_launch.log 2>&1
-for spec in "c5 c32_pair" "c5 c32_sample" "c5 leaf32_kernel" "c3 lazy32_kernel" "c6 pairw_tc_kernel" "c6 samplew_kernel"; do
-  set -- $spec
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$2 -s 3 -c 1 \
-    -o $O/full_$1_$2 -f python tools/prof_run.py --config $1 --reps 1 > $O/ncu_full_$1_$2.log 2>&1
-  echo "$1 $2 rc=$?" >> $O/ncu_status.txt
-done
+if [ "$NCU" = "1" ]; then
+  # reports stay on the box (/tmp); only summaries travel back (< 64 MiB)
+  R=/tmp/ncu_r02; mkdir -p $R
+  DSMC_NO_GRAPH=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
+    --log-file $O/launches_c5.csv python tools/prof_run.py --config c5 --reps 1 > $O/ncu_launch.log 2>&1
+  python tools/ncu_summary.py launches $O/launches_c5.csv > $O/launches_c5.md 2>&1
+  for spec in "c5 c32_pair" "c5 c32_sample" "c5 leaf32_kernel" "c3 lazy32_kernel" "c6 pairw_tc_kernel" "c6 samplew_kernel"; do
+    set -- $spec
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$2 -s 3 -c 1 \
+      -o $R/full_$1_$2 -f python tools/prof_run.py --config $1 --reps 1 > $O/ncu_full_$1_$2.log 2>&1
+    echo "$1 $2 rc=$?" >> $O/ncu_status.txt
+    python tools/ncu_summary.py report $R/full_$1_$2.ncu-rep > $O/full_$1_$2.md 2>&1
+    ncu -i $R/full_$1_$2.ncu-rep --page raw --csv > $O/full_$1_$2_raw.csv 2>&1
+  done
+fi
 echo done
