@@ -458,7 +458,9 @@ def run_ours(args, cfg, rank, world, device):
         pairs_local = (Kloc - 1) * N * N  # rank 0's local combines (all of them at N=1)
         peak, peak_src = sfu_peak_pairs_per_s(ck.get("sm_max_mhz"))
         ach = pairs_local / (pair_ms * 1e-3) if pair_ms else None
-        roof = {"bound": "sfu", "kernel": "c32_pair", "achieved": ach, "peak": peak,
+        pair_name = ("c32_pair" if d <= 4 else
+                     "prologw_kernel + pairw_tc_kernel (tcgen05 cross term)")
+        roof = {"bound": "sfu", "kernel": pair_name, "achieved": ach, "peak": peak,
                 "unit": "pair-evals/s (1 MUFU.EX2 each)", "frac": ach / peak if ach else None,
                 "peak_source": peak_src, "traffic": None,
                 "bound_note": "the dominant kernel is bound by the special-function unit "

@@ -744,9 +744,17 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
                      sizeof(double) * ((ns + 1) & ~(size_t)1) + 16 * ns + 8 * ns +
                      sizeof(int) * (32 + nsub);
   const bool sample4 = sm2 <= 48 * 1024;
-  if (sm2 > (size_t)ctx->smem_optin - 1024)
+  if (N >= 65536)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
-                   "FP32 dense combine: N too large for the shared-memory sampler (use a lazy "
+                   "FP32 dense combine: N must be < 65536 (use a lazy resampler)");
+  // large N: the column pairs no longer fit next to the row CDF in shared
+  // memory; the sampler then keeps only the CDF (12 N bytes) and reads the
+  // pass-1 hand-off from L2 (samplew_kernel over Aux32)
+  const size_t sm_big = sizeof(double) * (((size_t)N + 1) & ~(size_t)1) + sizeof(float) * (size_t)N;
+  const bool big = sm2 > (size_t)ctx->smem_optin - 1024;
+  if (big && sm_big > (size_t)ctx->smem_optin - 1024)
+    return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                   "FP32 dense combine: N too large for the shared-memory row CDF (use a lazy "
                    "resampler)");
   const bool use_tc = ctx->pair_tc && D >= 2;
   la.aux_comb = ((size_t)10 * N + 3) & ~(size_t)3;
@@ -778,7 +786,10 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
   }
   LAUNCHED(ctx);
   if (ev) CU(rec_event(ev[1], ctx->stream));
-  if (sample4)
+  if (big)
+    samplew_kernel<4, Aux32Recompute<D>><<<dim3(sb, nk, b.B), 256, sm_big, ctx->stream>>>(
+        b, la, systematic);
+  else if (sample4)
     CU(launch_pdl(c32_sample<D, 4>, dim3(sb, nk, b.B), dim3(256), sm2, ctx->stream, b, la,
                   systematic));
   else
@@ -1393,6 +1404,7 @@ cudaError_t configure_d(int smem) {
   set(c64_sample<kLGN, D>);
   set(pf_forward_kernel<D>);
   set(ffbs_backward_kernel<D>);
+  if (e == cudaSuccess) e = set_max_dynamic_smem(samplew_kernel<4, Aux32Recompute<D>>, smem);
   return e;
 }
 template <int D>

@@ -312,7 +312,64 @@ __global__ void __launch_bounds__(256) pairw_kernel(Bufs b, LevelArgs la) {
 // sub-block sums, FP64 row CDF, then per slot: row search, sub-block walk and
 // the recompute of the chosen sub-block's <= 64 weights (D-term dots against
 // the combine's Y / U), as c32_sample.
+// Column / row data of the sampler's recompute: the wide AUX (D floats per
+// row / column) or the float4 path's Aux32 (large N, below).
 template <int D>
+struct WideRecompute {
+  AuxW ax;
+  __device__ WideRecompute(const LevelArgs& la, size_t cslot, int N) : ax(auxw<D>(la, cslot, N)) {}
+  __device__ float B(int i) const { return ax.B[i]; }
+  __device__ void row(int i, float* u) const {
+    const float4* up = reinterpret_cast<const float4*>(ax.U + (size_t)i * D);
+#pragma unroll
+    for (int c = 0; c < D / 4; ++c) {
+      const float4 v = up[c];
+      u[4 * c] = v.x;
+      u[4 * c + 1] = v.y;
+      u[4 * c + 2] = v.z;
+      u[4 * c + 3] = v.w;
+    }
+  }
+  __device__ float weight_exp(int j, const float* u, float sh) const {
+    const float4* yp = reinterpret_cast<const float4*>(ax.Y + (size_t)j * D);
+    float t = ax.A[j] + sh;
+#pragma unroll
+    for (int c = 0; c < D / 4; ++c) {
+      const float4 yv = yp[c];
+      t = fmaf(u[4 * c], yv.x, t);
+      t = fmaf(u[4 * c + 1], yv.y, t);
+      t = fmaf(u[4 * c + 2], yv.z, t);
+      t = fmaf(u[4 * c + 3], yv.w, t);
+    }
+    return ex2(t);
+  }
+};
+// The float4 path's hand-off (pass 1 of c32_pair): d <= 4, pass 1's exact
+// operation order t = A_j + sh; t = fma(u_k, y_k, t).
+template <int D4>
+struct Aux32Recompute {
+  Aux32 ax;
+  __device__ Aux32Recompute(const LevelArgs& la, size_t cslot, int N) : ax(aux32(la, cslot, N)) {}
+  __device__ float B(int i) const { return ax.B[i]; }
+  __device__ void row(int i, float* u) const {
+    const float4 v = ax.u[i];
+    u[0] = v.x;
+    u[1] = v.y;
+    u[2] = v.z;
+    u[3] = v.w;
+  }
+  __device__ float weight_exp(int j, const float* u, float sh) const {
+    const float4 y = ax.y[j];
+    float t = ax.A[j] + sh;
+    t = fmaf(u[0], y.x, t);
+    if (D4 > 1) t = fmaf(u[1], y.y, t);
+    if (D4 > 2) t = fmaf(u[2], y.z, t);
+    if (D4 > 3) t = fmaf(u[3], y.w, t);
+    return ex2(t);
+  }
+};
+
+template <int D, class RC = WideRecompute<D>>
 __global__ void __launch_bounds__(256) samplew_kernel(Bufs b, LevelArgs la, int systematic) {
   extern __shared__ double wsmem[];
   __shared__ double sh[32];
@@ -326,7 +383,7 @@ __global__ void __launch_bounds__(256) samplew_kernel(Bufs b, LevelArgs la, int 
   const int nsub = (N + kSub - 1) / kSub;
   const size_t cslot = (size_t)blockIdx.z * gridDim.y + blockIdx.y;
   const float* ws = reinterpret_cast<const float*>(la.ws) + cslot * la.ws_comb * 2;
-  const AuxW ax = auxw<D>(la, cslot, N);
+  const RC rc(la, cslot, N);
   double* S = wsmem;                                          // [N]
   float* Lrow = reinterpret_cast<float*>(S + ((N + 1) & ~1));  // [N]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -374,7 +431,11 @@ __global__ void __launch_bounds__(256) samplew_kernel(Bufs b, LevelArgs la, int 
   const double total = S[N - 1];
   const size_t gidx = (size_t)ch * b.T + la.cursor + k;
   if (tid == 0 && sb == 0) b.LMW[gidx] = ((double)G + log2(total)) * kLn2;
-  const uint64_t node = static_cast<uint64_t>(k + la.node_off);
+  const int off = b.conditional ? 1 : 0;  // c-dSMC: slot 0 is the reference pair
+  const uint64_t node = b.conditional
+                            ? (static_cast<uint64_t>(static_cast<uint32_t>(k + la.node_off)) |
+                               (static_cast<uint64_t>(b.sweep) << 32))
+                            : static_cast<uint64_t>(k + la.node_off);
   const StreamId id = stream_id(b.seeds[ch], la.key_level, node, DSMC_ROLE_PAIR_RESAMPLE, 0);
   double u0 = 0.0, step = 0.0;
   if (systematic) {
@@ -424,41 +485,29 @@ __global__ void __launch_bounds__(256) samplew_kernel(Bufs b, LevelArgs la, int 
     float frac = wsel > 0.f ? (local - before_s) / wsel : 0.f;
     frac = fminf(fmaxf(frac, 0.f), 1.f);
     // recompute the sub-block's weights relative to its sum: 2^(w_ij - L_is)
-    float u[D];
-    const float4* up = reinterpret_cast<const float4*>(ax.U + (size_t)i * D);
-#pragma unroll
-    for (int c = 0; c < D / 4; ++c) {
-      const float4 v = up[c];
-      u[4 * c] = v.x;
-      u[4 * c + 1] = v.y;
-      u[4 * c + 2] = v.z;
-      u[4 * c + 3] = v.w;
-    }
-    const float sh_i = ax.B[i] - Ls_sel;
+    float u[D < 4 ? 4 : D];
+    rc.row(i, u);
+    const float sh_i = rc.B(i) - Ls_sel;
     const int j0 = s * kSub, j1 = min(N, j0 + kSub);
     float c3 = 0.f;
     int jl = -1, lastpos = j0;
     for (int j = j0; j < j1; ++j) {
-      const float4* yp = reinterpret_cast<const float4*>(ax.Y + (size_t)j * D);
-      float t = ax.A[j] + sh_i;
-#pragma unroll
-      for (int c = 0; c < D / 4; ++c) {
-        const float4 yv = yp[c];
-        t = fmaf(u[4 * c], yv.x, t);
-        t = fmaf(u[4 * c + 1], yv.y, t);
-        t = fmaf(u[4 * c + 2], yv.z, t);
-        t = fmaf(u[4 * c + 3], yv.w, t);
-      }
-      const float e = ex2(t);
+      const float e = rc.weight_exp(j, u, sh_i);
       if (e > 0.f) lastpos = j;
       c3 += e;
       if (jl < 0 && frac < c3) jl = j;
     }
     const int j = jl >= 0 ? jl : lastpos;  // spill (rounding): last positive weight
-    PL[m] = (uint32_t)i;
-    PR[m] = (uint32_t)j;
-    la.first_next[nbase + m] = map_first(b, la, ch, L, (uint32_t)i);
-    la.last_next[nbase + m] = map_last(b, la, ch, R, (uint32_t)j);
+    PL[m + off] = (uint32_t)i;
+    PR[m + off] = (uint32_t)j;
+    la.first_next[nbase + m + off] = map_first(b, la, ch, L, (uint32_t)i);
+    la.last_next[nbase + m + off] = map_last(b, la, ch, R, (uint32_t)j);
+  }
+  if (b.conditional && tid == 0 && sb == 0) {
+    PL[0] = 0;
+    PR[0] = 0;
+    la.first_next[nbase] = map_first(b, la, ch, L, 0);
+    la.last_next[nbase] = map_last(b, la, ch, R, 0);
   }
   if (tid == 0 && sb == 0) {
     const double logn = log((double)N);

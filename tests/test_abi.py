@@ -26,7 +26,9 @@ def test_header_declares_the_boundary():
     syms = declared_symbols()
     for s in ["dsmc_create", "dsmc_smooth", "dsmc_resample_table", "dsmc_conditional_sweep",
               "dsmc_sv_pgibbs_sweep", "dsmc_smooth_resident", "dsmc_kalman_smooth",
-              "dsmc_ffbs_smooth"]:
+              "dsmc_ffbs_smooth", "dsmc_make_leaf", "dsmc_resample_blocks",
+              "dsmc_resample_indices", "dsmc_lazy_begin", "dsmc_lazy_probes", "dsmc_lazy_answer",
+              "dsmc_lazy_finish", "dsmc_kalman_smooth_device", "dsmc_model_upload_window"]:
         assert s in syms
 
 

@@ -15,7 +15,10 @@ def test_host_library_and_tests_are_built():
     assert os.path.exists(HOSTLIB) and os.path.exists(BIN), "make -C paper_2202_02264_b200/csrc"
     out = subprocess.run(["nm", "-DC", "--defined-only", HOSTLIB], capture_output=True, text=True).stdout
     for sym in ["dsmc::run_smoother", "dsmc::run_conditional", "dsmc::pgibbs_sweep",
-                "dsmc::make_lgssm_fk", "dsmc::resample_pairs", "dsmc::kalman_smooth"]:
+                "dsmc::make_lgssm_fk", "dsmc::resample_pairs", "dsmc::kalman_smooth",
+                "dsmc::make_leaf", "dsmc::make_pair_source", "dsmc::combine_blocks",
+                "dsmc::multinomial_indices", "dsmc::mh_lazy_pairs", "dsmc::metrics::snapshot",
+                "dsmc::log_init_weight", "dsmc::make_stitch_row", "dsmc::leaf_weights"]:
         assert sym in out, sym
 
 

@@ -7,6 +7,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > 
 nproc >> $O/smi.txt; lscpu | grep "Model name" >> $O/smi.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; rc=$?; echo "smoke rc=$rc" >> $O/smoke.log
 [ $rc -ne 0 ] && { echo "smoke failed"; exit 1; }
+if [ "$ONLY_NCU" != "1" ]; then
 timeout 2400 python -m pytest tests -m gpu -q --timeout 900 -rs > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench_c5.json 2> $O/bench_c5.err
 for c in c2 c3 c3r c4 c1 c6; do
@@ -15,6 +16,7 @@ done
 for c in c6d8 c6d16; do
   timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-fp64 --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err
 done
+fi
 if [ "$NCU" = "1" ]; then
   # reports stay on the box (/tmp); only summaries travel back (< 64 MiB)
   R=/tmp/ncu_r02; mkdir -p $R
