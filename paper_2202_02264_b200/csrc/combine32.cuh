@@ -755,6 +755,14 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
   }
 }
 
+__device__ __forceinline__ bool lazy_serial_mh() {
+#ifdef DSMC_LAZY_SERIAL
+  return true;
+#else
+  return false;
+#endif
+}
+
 // FP32 lazy samplers: the entry in log2 units in the unexpanded whitened
 // form (accurate for any state), bound in log2 units.
 template <int D>
@@ -805,7 +813,47 @@ __global__ void lazy32_kernel(Bufs b, LevelArgs la, int mh, size_t mh_steps) {
       uint32_t i = (uint32_t)(m % N), j = i;
       float cur = 0.f;
       bool have = false;
-      for (size_t st = 0; st < mh_steps; ++st) {
+      // Each MH step draws exactly 3 u64 (two indices, one uniform;
+      // resampling.cpp:258-275), so 4 steps are 3 whole Philox blocks and
+      // their draws and proposal probes do not depend on the chain state:
+      // generate and probe 4 steps at once (4 independent gather chains in
+      // flight), then apply the 4 accept decisions in order. Bit-identical to
+      // the step-by-step loop below, which finishes any remainder.
+      size_t st = 0;
+      if (!lazy_serial_mh()) {
+        cur = probe(i, j);
+        ++evals;
+        have = true;
+        for (; st + 4 <= mh_steps; st += 4) {
+          const uint64_t b3 = 3 * (st / 4);
+          const U64x4 r0 = stream_block(s.id, b3), r1 = stream_block(s.id, b3 + 1),
+                      r2 = stream_block(s.id, b3 + 2);
+          const uint64_t u[12] = {r0.v[0], r0.v[1], r0.v[2], r0.v[3], r1.v[0], r1.v[1],
+                                  r1.v[2], r1.v[3], r2.v[0], r2.v[1], r2.v[2], r2.v[3]};
+          uint32_t pi[4], pj[4];
+          float lu[4], prop[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            pi[q] = (uint32_t)u64_index(u[3 * q], N);
+            pj[q] = (uint32_t)u64_index(u[3 * q + 1], N);
+            lu[q] = lg2((float)u64_uniform_pos(u[3 * q + 2]));
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) prop[q] = probe(pi[q], pj[q]);
+          evals += 4;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (lu[q] < prop[q] - cur) {
+              i = pi[q];
+              j = pj[q];
+              cur = prop[q];
+            }
+          }
+        }
+        s.blk = 3 * (st / 4);  // the remainder continues the stream
+        s.pos = 4;
+      }
+      for (; st < mh_steps; ++st) {
         const uint32_t pi = (uint32_t)s.index(N), pj = (uint32_t)s.index(N);
         const float lu = lg2((float)s.uniform_pos());  // FP32 path: MUFU, not FP64 log2
         if (!have) {

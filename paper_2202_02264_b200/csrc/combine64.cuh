@@ -73,10 +73,19 @@ __device__ inline double block_lnc(const Bufs& b, const LevelArgs& la, int ch,
 }
 
 // Per-combine column data of the FP64 fill, staged in shared memory.
+// Column j lives at cpad(j): every 64-column sub-block takes 72 slots, so the
+// four 8-lane groups of a warp (four sub-blocks, pass 1's sub-block sums)
+// read disjoint bank halves instead of the same banks; states are stored
+// dimension-major (x[k * ld + cpad(j)]) so consecutive columns are
+// consecutive doubles. The layout only places values: the arithmetic and
+// its order are unchanged.
+__host__ __device__ inline int cpad(int j) { return j + (j >> 6) * 8; }
+__host__ __device__ inline int col_ld(int N) { return (N + 63) / 64 * 72; }
 struct Col64 {
-  double* x;    // N*d
-  double* base; // N
-  double* lwr;  // N or null
+  double* x;    // d * ld
+  double* base; // ld
+  double* lwr;  // ld or null
+  int ld;
 };
 
 // Column base of the stitch-row factory at cut c (per model class).
@@ -157,18 +166,19 @@ __device__ inline double fill64(const DevModel& M, const TimeConst& tc,
                                 double coef, const double* mu, const Col64& C,
                                 int j, double sl, bool has_l) {
   double v;
+  const int cp = cpad(j);
   if (MC == kLGN) {  // d chained gaussian_row passes (ref_models lgssm_nd)
-    v = C.base[j];
+    v = C.base[cp];
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const double t = DSUB(C.x[(size_t)j * D + k], mu[k]);
+      const double t = DSUB(C.x[k * C.ld + cp], mu[k]);
       v = __fma_rn(-0.5, DMUL(t, t), v);
     }
   } else {
-    const double t = DSUB(C.x[j], mu[0]);
-    v = __fma_rn(coef, DMUL(t, t), C.base[j]);
+    const double t = DSUB(C.x[cp], mu[0]);
+    v = __fma_rn(coef, DMUL(t, t), C.base[cp]);
   }
-  if (C.lwr) v = DADD(DADD(v, sl), C.lwr[j]);
+  if (C.lwr) v = DADD(DADD(v, sl), C.lwr[cp]);
   else if (has_l && sl != 0.0) v = DADD(v, sl);
   return v;
 }
@@ -190,29 +200,31 @@ __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
                            const TimeConst& tc, double* smem, Col64& C) {
   const int N = b.N;
   constexpr int d = D;
+  C.ld = col_ld(N);
   C.x = smem;
-  C.base = smem + (size_t)N * d;
+  C.base = smem + (size_t)C.ld * d;
   const bool nonuni = R.leaf && !b.UNI[(size_t)ch * b.K + R.t];
-  C.lwr = nonuni ? C.base + N : nullptr;
+  C.lwr = nonuni ? C.base + C.ld : nullptr;
   const double* X = b.X64 + ((size_t)ch * b.K + R.t) * N * d;
   for (int j = threadIdx.x; j < N; j += blockDim.x) {
     const uint32_t p = map_first(b, la, ch, R, j);
     double x[D];
 #pragma unroll
     for (int k = 0; k < d; ++k) x[k] = X[(size_t)p * d + k];
-    C.base[j] = col_base<MC, D>(M, tc, b.t0 + R.t, x);  // global time (windows)
+    const int cp = cpad(j);
+    C.base[cp] = col_base<MC, D>(M, tc, b.t0 + R.t, x);  // global time (windows)
     if (MC == kLGN) {  // whitened column w = W_Q x
 #pragma unroll
       for (int k = 0; k < d; ++k) {
         double z = 0.0;
 #pragma unroll
         for (int l = 0; l <= k; ++l) z = DADD(z, DMUL(tc.tW[k * d + l], x[l]));
-        C.x[(size_t)j * d + k] = z;
+        C.x[k * C.ld + cp] = z;
       }
     } else {
-      C.x[j] = x[0];
+      C.x[cp] = x[0];
     }
-    if (nonuni) C.lwr[j] = b.LW64[((size_t)ch * b.K + R.t) * N + p];
+    if (nonuni) C.lwr[cp] = b.LW64[((size_t)ch * b.K + R.t) * N + p];
   }
   __syncthreads();
 }
@@ -222,7 +234,7 @@ __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
 // (sequential over sub-blocks) — exp_row_store (kernels.cpp:93-116).
 // ws layout per combine: m[N] raw[N] scale[N] total[N] prefix[N] sub[N*nsub]
 template <int MC, int D>
-__global__ void __launch_bounds__(256) c64_rows(Bufs b, LevelArgs la) {
+__global__ void __launch_bounds__(256, 4) c64_rows(Bufs b, LevelArgs la) {
   extern __shared__ double smem[];
   const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
   const int N = b.N, nsub = (N + kSub - 1) / kSub;

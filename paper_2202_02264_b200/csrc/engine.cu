@@ -264,11 +264,9 @@ int upload(dsmc_ctx* ctx, dsmc_model_handle* h, const T* src, size_t n,
   return DSMC_OK;
 }
 
-// ------------------------------------------------ wide-state host prep
-// FP64 per-time constants of the wide path (wide.cuh header): Cholesky
-// factors and whitening of the proposal, transition and observation
-// covariances, computed on the host threads (O(K d^3), the model set-up step)
-// and stored FP32 with the padded dimensions DP / DYP.
+// ------------------------------------------------ wide-state prior prep
+// Host FP64 helpers for the wide path's prior constants (one P0 factor); the
+// per-time constants are computed on the device (wide.cuh prepw_kernel).
 namespace widep {
 bool chol(const double* A, int n, double* L) {
   for (int i = 0; i < n * n; ++i) L[i] = 0.0;
@@ -303,131 +301,20 @@ double logdet(const double* L, int n) {
 }
 }  // namespace widep
 
-struct WideHost {
-  std::vector<float> L, G, e, c, W, M, v, WP0, dm0;
-  std::vector<double> m;
-  double p0norm = 0.0;
-};
-
-// returns "" or the error message
-std::string prep_wide(const dsmc_model_desc& md, int DP, int DYP, WideHost& o) {
-  const int K = md.horizon + 1, d = md.state_dim, dy = md.obs_dim;
-  const size_t dd = (size_t)d * d;
-  o.L.assign((size_t)K * DP * DP, 0.f);
-  o.G.assign((size_t)K * DYP * DP, 0.f);
-  o.e.assign((size_t)K * DYP, 0.f);
-  o.c.assign(K, 0.f);
-  o.W.assign((size_t)K * DP * DP, 0.f);
-  o.M.assign((size_t)K * DP * DP, 0.f);
-  o.v.assign((size_t)K * DP, 0.f);
-  o.m.assign(md.prop_mean, md.prop_mean + (size_t)K * d);
-  o.WP0.assign((size_t)DP * DP, 0.f);
-  o.dm0.assign(DP, 0.f);
-  const double s = std::sqrt(kLog2E / 2.0);
-  auto at = [](const double* p, int64_t stride, int t) { return p + stride * t; };
-  {  // prior
-    std::vector<double> Lp(dd), Wp(dd);
-    if (!widep::chol(md.P0, d, Lp.data())) return "lgssm: P0 is not positive definite";
-    widep::tri_inv(Lp.data(), d, Wp.data());
-    for (int i = 0; i < d; ++i)
-      for (int j = 0; j < d; ++j) o.WP0[i * DP + j] = (float)Wp[i * d + j];
-    for (int i = 0; i < d; ++i) o.dm0[i] = (float)(md.m0[i] - md.prop_mean[i]);
-    o.p0norm = -0.5 * (d * kLog2Pi + widep::logdet(Lp.data(), d));
-  }
-  std::string err;
-  std::mutex mu;
-  auto work = [&](int t_begin, int t_end) {
-    std::vector<double> Lt(dd), Lr((size_t)dy * dy), Wr((size_t)dy * dy), HL((size_t)dy * d);
-    std::vector<double> Lq(dd), Wq(dd), WF(dd);
-    for (int t = t_begin; t < t_end; ++t) {
-      const double* mt = md.prop_mean + (size_t)t * d;
-      if (!widep::chol(md.prop_cov + (size_t)t * dd, d, Lt.data())) {
-        std::lock_guard<std::mutex> g(mu);
-        err = "lgssm: proposal covariance at time " + std::to_string(t) + " is not positive definite";
-        return;
-      }
-      for (int i = 0; i < d; ++i)
-        for (int j = 0; j <= i; ++j) o.L[(size_t)t * DP * DP + i * DP + j] = (float)Lt[i * d + j];
-      const double p_norm = -0.5 * (d * kLog2Pi + widep::logdet(Lt.data(), d));
-      double o_norm = 0.0;
-      const bool obs = md.has_obs ? md.has_obs[t] != 0 : true;
-      if (obs) {
-        const double* H = at(md.H, md.H_stride, t);
-        const double* R = at(md.R, md.R_stride, t);
-        if (!widep::chol(R, dy, Lr.data())) {
-          std::lock_guard<std::mutex> g(mu);
-          err = "lgssm: R at time " + std::to_string(t) + " is not positive definite";
-          return;
-        }
-        widep::tri_inv(Lr.data(), dy, Wr.data());
-        o_norm = -0.5 * (dy * kLog2Pi + widep::logdet(Lr.data(), dy));
-        for (int a = 0; a < dy; ++a)
-          for (int j = 0; j < d; ++j) {
-            double acc = 0.0;
-            for (int l = 0; l < d; ++l) acc += H[a * d + l] * Lt[l * d + j];
-            HL[a * d + j] = acc;
-          }
-        for (int a = 0; a < dy; ++a) {
-          double ea = 0.0;
-          for (int b2 = 0; b2 <= a; ++b2) {
-            double r = md.y[(size_t)t * dy + b2];
-            for (int l = 0; l < d; ++l) r -= H[b2 * d + l] * mt[l];
-            ea += Wr[a * dy + b2] * r;
-          }
-          o.e[(size_t)t * DYP + a] = (float)ea;
-          for (int j = 0; j < d; ++j) {
-            double g = 0.0;
-            for (int b2 = 0; b2 <= a; ++b2) g += Wr[a * dy + b2] * HL[b2 * d + j];
-            o.G[(size_t)t * DYP * DP + a * DP + j] = (float)g;
-          }
-        }
-      }
-      double t_norm = 0.0;
-      if (t >= 1) {
-        const double* F = at(md.F, md.F_stride, t);
-        const double* bb = at(md.b, md.b_stride, t);
-        const double* Q = at(md.Q, md.Q_stride, t);
-        if (!widep::chol(Q, d, Lq.data())) {
-          std::lock_guard<std::mutex> g(mu);
-          err = "lgssm: Q at time " + std::to_string(t) + " is not positive definite";
-          return;
-        }
-        widep::tri_inv(Lq.data(), d, Wq.data());
-        t_norm = -0.5 * (d * kLog2Pi + widep::logdet(Lq.data(), d));
-        const double* mp = md.prop_mean + (size_t)(t - 1) * d;
-        for (int i = 0; i < d; ++i) {
-          double vi = 0.0;
-          for (int j = 0; j <= i; ++j) {
-            o.W[(size_t)t * DP * DP + i * DP + j] = (float)(s * Wq[i * d + j]);
-            // delta_j = (F m_{t-1} + b - m_t)_j
-            double dj = bb[j] - mt[j];
-            for (int l = 0; l < d; ++l) dj += F[j * d + l] * mp[l];
-            vi += Wq[i * d + j] * dj;
-          }
-          o.v[(size_t)t * DP + i] = (float)(s * vi);
-          for (int j = 0; j < d; ++j) {
-            double acc = 0.0;
-            for (int l = 0; l <= i; ++l) acc += Wq[i * d + l] * F[l * d + j];
-            o.M[(size_t)t * DP * DP + i * DP + j] = (float)(s * acc);
-          }
-        }
-      }
-      o.c[t] = (float)(o_norm - p_norm + t_norm);
-    }
-  };
-  const int nth = std::max(1, std::min<int>(std::thread::hardware_concurrency(), K / 64 + 1));
-  std::vector<std::thread> pool;
-  for (int q = 0; q < nth; ++q)
-    pool.emplace_back(work, (int)((long)K * q / nth), (int)((long)K * (q + 1) / nth));
-  for (auto& th : pool) th.join();
-  return err;
+// Dynamic shared memory of samplew_kernel: row CDF (double) + row totals,
+// then per slot a 16-byte record and a sort index, and the sub-block counts.
+size_t samplew_smem(int N, int slots) {
+  const size_t head = (sizeof(double) * (((size_t)N + 1) & ~(size_t)1) + sizeof(float) * (size_t)N +
+                       15) & ~(size_t)15;
+  return head + (size_t)slots * (16 + 4) + sizeof(int) * (size_t)((N + kSub - 1) / kSub);
 }
 
 int wide_dp(int d) { return d <= 8 ? 8 : d <= 16 ? 16 : 32; }
-bool force_wide() {
-  const char* f = getenv("DSMC_FORCE_WIDE");
+bool getenv_flag(const char* name) {  // A/B switches for tests and tools
+  const char* f = getenv(name);
   return f && f[0] == '1';
 }
+bool force_wide() { return getenv_flag("DSMC_FORCE_WIDE"); }
 
 // Per-time array restricted to times [lo, hi) (time-sharded windows): only
 // those rows are uploaded, and the device pointer is offset so kernels keep
@@ -489,6 +376,7 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
     if (!stride) return upload(ctx, h.get(), src, per, dst);  // one matrix for every time
     return per_time(src, (size_t)stride, dst);
   };
+  const bool wide = descs[0].kind == DSMC_MODEL_LGSSM && (d > 4 || force_wide());
   std::vector<DevModel> dm(B);
   for (int c = 0; c < B; ++c) {
     const dsmc_model_desc& m = descs[c];
@@ -567,34 +455,80 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
     if (rc) return DSMC_E_CUDA;
   }
   void* p;
-  // wide-state LGSSM (d > 4, or forced for testing): host-prepared constants
-  if (descs[0].kind == DSMC_MODEL_LGSSM && (d > 4 || force_wide())) {
+  // wide-state LGSSM (d > 4, or forced for testing): device-prepared constants
+  if (wide) {
     if (B != 1 || window)
       return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
                      "state_dim > 4: one unconditional model on the whole horizon");
     const int DP = wide_dp(d), DYP = (dy + 3) & ~3;
-    WideHost wh;
-    const std::string e = prep_wide(descs[0], DP, DYP, wh);
-    if (!e.empty()) return set_err(ctx, DSMC_E_INVALID_ARGUMENT, e);
-    auto put = [&](const auto& v, auto** dst) -> int {
-      void* q = nullptr;
-      CU(cudaMallocAsync(&q, std::max<size_t>(1, v.size()) * sizeof(v[0]), ctx->stream));
-      h->owned.push_back(q);
-      CU(cudaMemcpyAsync(q, v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice, ctx->stream));
-      *dst = static_cast<std::remove_reference_t<decltype(*dst)>>(q);
-      return DSMC_OK;
-    };
+    const dsmc_model_desc& md = descs[0];
     WideBufs& wb = h->wb;
     wb.d = d;
     wb.dy = dy;
     wb.DP = DP;
     wb.DYP = DYP;
-    wb.p0norm = wh.p0norm;
-    int rcw = put(wh.L, &wb.L) | put(wh.G, &wb.G) | put(wh.e, &wb.e) | put(wh.c, &wb.c) |
-              put(wh.W, &wb.W) | put(wh.M, &wb.M) | put(wh.v, &wb.v) | put(wh.m, &wb.m) |
-              put(wh.WP0, &wb.WP0) | put(wh.dm0, &wb.dm0);
-    if (rcw) return rcw;
-    CU(cudaStreamSynchronize(ctx->stream));  // the host vectors die here
+    {  // prior constants on the host (one matrix)
+      std::vector<double> Lp((size_t)d * d), Wp((size_t)d * d);
+      if (!widep::chol(md.P0, d, Lp.data()))
+        return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "lgssm: P0 is not positive definite");
+      widep::tri_inv(Lp.data(), d, Wp.data());
+      std::vector<float> WP0((size_t)DP * DP, 0.f), dm0(DP, 0.f);
+      for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j) WP0[i * DP + j] = (float)Wp[i * d + j];
+      for (int i = 0; i < d; ++i) dm0[i] = (float)(md.m0[i] - md.prop_mean[i]);
+      wb.p0norm = -0.5 * (d * kLog2Pi + widep::logdet(Lp.data(), d));
+      float* q;
+      CU(cudaMallocAsync((void**)&q, sizeof(float) * ((size_t)DP * DP + DP), ctx->stream));
+      h->owned.push_back(q);
+      CU(cudaMemcpyAsync(q, WP0.data(), sizeof(float) * DP * DP, cudaMemcpyHostToDevice, ctx->stream));
+      CU(cudaMemcpyAsync(q + DP * DP, dm0.data(), sizeof(float) * DP, cudaMemcpyHostToDevice,
+                         ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));  // WP0 / dm0 are local
+      wb.WP0 = q;
+      wb.dm0 = q + DP * DP;
+    }
+    // per-time constants on the device (prepw_kernel), zero-filled padding
+    const size_t nL = (size_t)K * DP * DP, nG = (size_t)K * DYP * DP, ne = (size_t)K * DYP;
+    const size_t nall = 3 * nL + nG + ne + (size_t)K + (size_t)K * DP;
+    float* q;
+    CU(cudaMallocAsync((void**)&q, sizeof(float) * nall + 16, ctx->stream));
+    h->owned.push_back(q);
+    CU(cudaMemsetAsync(q, 0, sizeof(float) * nall, ctx->stream));
+    WidePrep o;
+    o.L = q;
+    o.W = q + nL;
+    o.M = q + 2 * nL;
+    o.G = q + 3 * nL;
+    o.e = o.G + nG;
+    o.c = o.e + ne;
+    o.v = o.c + K;
+    int* errd = reinterpret_cast<int*>(o.v + (size_t)K * DP);  // 16 spare bytes
+    CU(cudaMemsetAsync(errd, 0x7f, 3 * sizeof(int), ctx->stream));
+    o.err = errd;
+    o.d = d;
+    o.dy = dy;
+    o.DP = DP;
+    o.DYP = DYP;
+    o.K = K;
+    prepw_kernel<<<K, 32, 3 * 32 * kPS * sizeof(double), ctx->stream>>>(dm[0], o);
+    LAUNCHED(ctx);
+    int errs[3];
+    CU(cudaMemcpyAsync(errs, errd, sizeof(errs), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    static const char* what[3] = {"proposal covariance", "R", "Q"};
+    for (int q2 = 0; q2 < 3; ++q2)
+      if (errs[q2] < K)
+        return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
+                       std::string("lgssm: ") + what[q2] + " at time " + std::to_string(errs[q2]) +
+                           " is not positive definite");
+    wb.L = o.L;
+    wb.W = o.W;
+    wb.M = o.M;
+    wb.G = o.G;
+    wb.e = o.e;
+    wb.c = o.c;
+    wb.v = o.v;
+    wb.m = dm[0].prop_mean;  // the uploaded FP64 proposal means
     h->wide = true;
     h->defer = false;
   }
@@ -611,8 +545,8 @@ int make_handle(dsmc_ctx* ctx, const dsmc_model_desc* descs, int B,
   h->bounded = static_cast<int*>(p);
   std::vector<int> ones(B, 3);
   CU(cudaMemcpyAsync(p, ones.data(), sizeof(int) * B, cudaMemcpyHostToDevice, ctx->stream));
-  if (h->deferred.empty() && d > 4) {
-    h->defer = false;  // the TimeConst per-time constants exist for d <= 4 only
+  if (h->deferred.empty() && (d > 4 || wide)) {
+    h->defer = false;  // the TimeConst per-time constants exist for d <= 4 only (not wide)
   } else if (h->deferred.empty()) {
     h->defer = false;
     prep_kernel<<<dim3((w_hi - w_lo + 127) / 128, B), 128, 0, ctx->stream>>>(
@@ -682,7 +616,7 @@ struct RunResult {
   double* LW64 = nullptr;
 };
 
-size_t smem_cols64(int N, int d) { return sizeof(double) * (size_t)N * (d + 2); }
+size_t smem_cols64(int N, int d) { return sizeof(double) * (size_t)col_ld(N) * (d + 2); }
 
 template <int MC, int D>
 int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
@@ -691,7 +625,8 @@ int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
   if (sm > (size_t)ctx->smem_optin - 1024)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
                    "FP64 parity combine: N * (d + 2) doubles exceed the shared-memory "
-                   "column stage (N <= " + std::to_string(ctx->smem_optin / (8 * (D + 2))) +
+                   "column stage (N <= " +
+                       std::to_string((ctx->smem_optin - 1024) / (8 * (D + 2)) / 72 * 64) +
                        " at this d); use the FP32 path or a lazy resampler");
   c64_rows<MC, D><<<dim3((b.N + 31) / 32, nk, b.B), 256, sm, ctx->stream>>>(b, la);
   LAUNCHED(ctx);
@@ -750,7 +685,7 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
   // large N: the column pairs no longer fit next to the row CDF in shared
   // memory; the sampler then keeps only the CDF (12 N bytes) and reads the
   // pass-1 hand-off from L2 (samplew_kernel over Aux32)
-  const size_t sm_big = sizeof(double) * (((size_t)N + 1) & ~(size_t)1) + sizeof(float) * (size_t)N;
+  const size_t sm_big = samplew_smem(N, la.slots_per_cta);
   const bool big = sm2 > (size_t)ctx->smem_optin - 1024;
   if (big && sm_big > (size_t)ctx->smem_optin - 1024)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
@@ -818,9 +753,10 @@ int launch_wide(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemat
   int sb = 1;
   if ((long)nk * b.B < 148 * 2)
     sb = std::max(1, std::min((la.n_out + 63) / 64, (int)((148 * 2 + nk * b.B - 1) / (nk * b.B))));
+  sb = std::max(sb, (la.n_out + 1023) / 1024);  // <= 1024 slot records per CTA
   la.slots_per_cta = (la.n_out + sb - 1) / sb;
   const size_t sm1 = sizeof(float) * ((size_t)(kWRows + kSub) * WideK<D>::S + kWRows + kSub);
-  const size_t sm2 = sizeof(double) * (((size_t)N + 1) & ~(size_t)1) + sizeof(float) * (size_t)N;
+  const size_t sm2 = samplew_smem(N, la.slots_per_cta);
   if (sm2 > (size_t)ctx->smem_optin - 1024)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT, "wide combine: N too large for the sampler");
   cudaEvent_t* ev = nullptr;

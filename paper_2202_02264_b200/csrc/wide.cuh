@@ -3,7 +3,7 @@
 // fk_model.hpp:38; the float4 path of combine32.cuh stops at 4). Templates
 // over the padded dimension D in {8, 16, 32}.
 //
-// Per time t (host-prepared in FP64, stored FP32, engine.cu prep_wide):
+// Per time t (prepared in FP64 on the device by prepw_kernel, stored FP32):
 //   L_t  lower Cholesky of the proposal covariance       (x~ = x - m_t = L z)
 //   G_t = Ro H L, e_t = Ro (y - H m), Ro = R^-1/2         (observation)
 //   c_t  o_norm - p_norm + t_norm                         (column constant)
@@ -29,6 +29,156 @@ template <int D>
 struct WideK {
   static constexpr int S = D + 4;  // padded smem row (floats), float4-aligned
 };
+
+// -------------------------------------------------------------- model prep
+// Per-time FP64 constants of the header above, computed on the device: one
+// warp per time t, lane = matrix row, matrices in shared memory (row stride
+// 33 doubles). Same formulas and per-element operation order as the host
+// version it replaced (Cholesky by columns, forward-substituted inverses);
+// outputs are FP32 and the buffers are zero-filled by the caller, so only the
+// live d x d / dy x d entries are written. The prior (P0) constants stay on
+// the host (one matrix). err: the smallest failing time per kind (proposal
+// covariance, R, Q), INT_MAX when none.
+struct WidePrep {
+  float *L, *G, *e, *c, *W, *M, *v;
+  int* err;  // [3]
+  int d, dy, DP, DYP, K;
+};
+
+constexpr int kPS = 33;  // shared row stride (doubles)
+
+// Lower Cholesky of the n x n matrix A (global, row-major) into L (shared).
+// Returns false (warp-uniform) when A is not positive definite.
+__device__ inline bool warp_chol(const double* A, int n, double* L) {
+  const int lane = threadIdx.x & 31;
+  for (int j = 0; j < n; ++j) {
+    double djj = 0.0;
+    if (lane == 0) {
+      double s = A[j * n + j];
+      for (int k = 0; k < j; ++k) s -= L[j * kPS + k] * L[j * kPS + k];
+      djj = s > 0.0 ? sqrt(s) : -1.0;
+      L[j * kPS + j] = djj;
+    }
+    djj = __shfl_sync(~0u, djj, 0);
+    if (!(djj > 0.0)) return false;
+    for (int i = j + 1 + lane; i < n; i += 32) {
+      double v = A[i * n + j];
+      for (int k = 0; k < j; ++k) v -= L[i * kPS + k] * L[j * kPS + k];
+      L[i * kPS + j] = v / djj;
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+// W = L^-1 (lower), column j by lane j.
+__device__ inline void warp_tri_inv(const double* L, int n, double* W) {
+  const int lane = threadIdx.x & 31;
+  for (int j = lane; j < n; j += 32) {
+    W[j * kPS + j] = 1.0 / L[j * kPS + j];
+    for (int i = j + 1; i < n; ++i) {
+      double s = 0.0;
+      for (int k = j; k < i; ++k) s += L[i * kPS + k] * W[k * kPS + j];
+      W[i * kPS + j] = -s / L[i * kPS + i];
+    }
+  }
+  __syncwarp();
+}
+
+__device__ inline double warp_logdet(const double* L, int n) {  // 2 sum log L_jj, lane 0
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s += 2.0 * log(L[i * kPS + i]);
+  return s;
+}
+
+// grid K, 32 threads, 3 * 32 * 33 doubles of dynamic shared memory
+__global__ void __launch_bounds__(32) prepw_kernel(DevModel md, WidePrep o) {
+  extern __shared__ double psm[];
+  double* Lt = psm;                 // proposal Cholesky
+  double* Wm = psm + 32 * kPS;      // R / Q inverse Cholesky
+  double* Tm = psm + 2 * 32 * kPS;  // scratch: R / Q Cholesky, then H L
+  const int t = blockIdx.x, lane = threadIdx.x;
+  const int d = o.d, dy = o.dy, DP = o.DP, DYP = o.DYP;
+  const size_t dd = (size_t)d * d;
+  const double s = sqrt(kLog2E / 2.0);
+  const double* mt = md.prop_mean + (size_t)t * d;
+  if (!warp_chol(md.prop_cov + (size_t)t * dd, d, Lt)) {
+    if (lane == 0) atomicMin(&o.err[0], t);
+    return;
+  }
+  for (int i = lane; i < d; i += 32)
+    for (int j = 0; j <= i; ++j) o.L[(size_t)t * DP * DP + i * DP + j] = (float)Lt[i * kPS + j];
+  const double p_norm = -0.5 * (d * kLog2Pi + warp_logdet(Lt, d));
+  double o_norm = 0.0;
+  const bool obs = md.has_obs ? md.has_obs[t] != 0 : true;
+  if (obs) {
+    const double* H = md.H + md.H_s * t;
+    const double* R = md.R + md.R_s * t;
+    if (!warp_chol(R, dy, Tm)) {
+      if (lane == 0) atomicMin(&o.err[1], t);
+      return;
+    }
+    warp_tri_inv(Tm, dy, Wm);
+    o_norm = -0.5 * (dy * kLog2Pi + warp_logdet(Tm, dy));
+    __syncwarp();
+    for (int a = lane; a < dy; a += 32)  // H L (into Tm; R's factor is done)
+      for (int j = 0; j < d; ++j) {
+        double acc = 0.0;  // L is lower triangular (its upper part is not stored)
+        for (int l = j; l < d; ++l) acc += H[a * d + l] * Lt[l * kPS + j];
+        Tm[a * kPS + j] = acc;
+      }
+    __syncwarp();
+    for (int a = lane; a < dy; a += 32) {
+      double ea = 0.0;
+      for (int b2 = 0; b2 <= a; ++b2) {
+        double r = md.y[(size_t)t * dy + b2];
+        for (int l = 0; l < d; ++l) r -= H[b2 * d + l] * mt[l];
+        ea += Wm[a * kPS + b2] * r;
+      }
+      o.e[(size_t)t * DYP + a] = (float)ea;
+      for (int j = 0; j < d; ++j) {
+        double g = 0.0;
+        for (int b2 = 0; b2 <= a; ++b2) g += Wm[a * kPS + b2] * Tm[b2 * kPS + j];
+        o.G[(size_t)t * DYP * DP + a * DP + j] = (float)g;
+      }
+    }
+    __syncwarp();
+  }
+  double t_norm = 0.0;
+  if (t >= 1) {
+    const double* F = md.F + md.F_s * t;
+    const double* bb = md.b + md.b_s * t;
+    const double* Q = md.Q + md.Q_s * t;
+    if (!warp_chol(Q, d, Tm)) {
+      if (lane == 0) atomicMin(&o.err[2], t);
+      return;
+    }
+    warp_tri_inv(Tm, d, Wm);
+    t_norm = -0.5 * (d * kLog2Pi + warp_logdet(Tm, d));
+    const double* mp = md.prop_mean + (size_t)(t - 1) * d;
+    __syncwarp();
+    for (int j = lane; j < d; j += 32) {  // delta_j = (F m_{t-1} + b - m_t)_j, into Tm row 0
+      double dj = bb[j] - mt[j];
+      for (int l = 0; l < d; ++l) dj += F[j * d + l] * mp[l];
+      Tm[j] = dj;
+    }
+    __syncwarp();
+    for (int i = lane; i < d; i += 32) {
+      double vi = 0.0;
+      for (int j = 0; j <= i; ++j) {
+        o.W[(size_t)t * DP * DP + i * DP + j] = (float)(s * Wm[i * kPS + j]);
+        vi += Wm[i * kPS + j] * Tm[j];
+      }
+      o.v[(size_t)t * DP + i] = (float)(s * vi);
+      for (int j = 0; j < d; ++j) {
+        double acc = 0.0;
+        for (int l = 0; l <= i; ++l) acc += Wm[i * kPS + l] * F[l * d + j];
+        o.M[(size_t)t * DP * DP + i * DP + j] = (float)(s * acc);
+      }
+    }
+  }
+  if (lane == 0) o.c[t] = (float)(o_norm - p_norm + t_norm);
+}
 
 // ---------------------------------------------------------------- leaves
 template <int D>
@@ -446,7 +596,22 @@ __global__ void __launch_bounds__(256) samplew_kernel(Bufs b, LevelArgs la, int 
   uint32_t* PR = b.PR + gidx * N;
   const size_t nbase = ((size_t)ch * b.cap + k) * N;
   const int m0 = sb * la.slots_per_cta, m1 = min(la.n_out, m0 + la.slots_per_cta);
-  for (int m = m0 + tid; m < m1; m += blockDim.x) {
+  const int ns = max(0, m1 - m0);
+  // Two phases with a counting sort by sub-block in between (as c32_sample):
+  // phase 1 (slot order) finds row i, sub-block s and the fraction inside s;
+  // phase 2 (sub-block order) recomputes the chosen sub-block's weights, so a
+  // warp's slots read the same column data (L1 broadcasts instead of 32
+  // scattered D-float rows per load). The order only schedules work: slot m
+  // always uses u64 number m of the stream and writes output m.
+  const size_t ext = ((reinterpret_cast<char*>(Lrow + N) - reinterpret_cast<char*>(wsmem)) + 15) &
+                     ~static_cast<size_t>(15);
+  int4* REC = reinterpret_cast<int4*>(reinterpret_cast<char*>(wsmem) + ext);  // [ns]
+  int* ORD = reinterpret_cast<int*>(REC + ns);                                // [ns]
+  int* CB = ORD + ns;                                                         // [nsub]
+  for (int q = tid; q < nsub; q += blockDim.x) CB[q] = 0;
+  __syncthreads();
+  for (int x = tid; x < ns; x += blockDim.x) {
+    const int m = m0 + x;
     const double pt = systematic ? (u0 + (double)m) * step : u64_uniform(stream_u64(id, m)) * total;
     int lo = 0, hi = N;
     while (lo < hi) {
@@ -484,10 +649,34 @@ __global__ void __launch_bounds__(256) samplew_kernel(Bufs b, LevelArgs la, int 
     }
     float frac = wsel > 0.f ? (local - before_s) / wsel : 0.f;
     frac = fminf(fmaxf(frac, 0.f), 1.f);
+    REC[x] = make_int4(i, s, __float_as_int(frac), __float_as_int(rc.B(i) - Ls_sel));
+    atomicAdd(&CB[s], 1);
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the sub-block counts
+    int carry = 0;
+    for (int c0 = 0; c0 < nsub; c0 += 32) {
+      const int c = c0 + lane < nsub ? CB[c0 + lane] : 0;
+      int v = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(~0u, v, o);
+        if (lane >= o) v += n;
+      }
+      if (c0 + lane < nsub) CB[c0 + lane] = carry + v - c;
+      carry += __shfl_sync(~0u, v, 31);
+    }
+  }
+  __syncthreads();
+  for (int x = tid; x < ns; x += blockDim.x) ORD[atomicAdd(&CB[REC[x].y], 1)] = x;
+  __syncthreads();
+  for (int o = tid; o < ns; o += blockDim.x) {
+    const int x = ORD[o];
+    const int4 rec = REC[x];
+    const int i = rec.x, s = rec.y;
+    const float frac = __int_as_float(rec.z), sh_i = __int_as_float(rec.w);
     // recompute the sub-block's weights relative to its sum: 2^(w_ij - L_is)
     float u[D < 4 ? 4 : D];
     rc.row(i, u);
-    const float sh_i = rc.B(i) - Ls_sel;
     const int j0 = s * kSub, j1 = min(N, j0 + kSub);
     float c3 = 0.f;
     int jl = -1, lastpos = j0;
@@ -498,6 +687,7 @@ __global__ void __launch_bounds__(256) samplew_kernel(Bufs b, LevelArgs la, int 
       if (jl < 0 && frac < c3) jl = j;
     }
     const int j = jl >= 0 ? jl : lastpos;  // spill (rounding): last positive weight
+    const int m = m0 + x;
     PL[m + off] = (uint32_t)i;
     PR[m + off] = (uint32_t)j;
     la.first_next[nbase + m + off] = map_first(b, la, ch, L, (uint32_t)i);

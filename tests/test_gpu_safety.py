@@ -168,3 +168,14 @@ def test_leaf_outputs_fp64_only(engine):
     assert np.allclose(np.log(np.exp(lw - mx).sum(1)) + mx[:, 0], 0.0, atol=1e-12)
     with pytest.raises(ValueError, match="FP64"):
         engine.smooth(m, 16, seed=4, precision=abi.FP32, want_leaf_logw=True)
+
+
+def test_fp64_dense_column_stage_limit(engine):
+    """The FP64 dense combine stages the right block's columns in shared
+    memory; an N beyond it is refused with the bound in the message instead of
+    a raw launch failure."""
+    m = models.cv_tracking(3)
+    with pytest.raises(ValueError, match="column stage"):
+        engine.smooth(m, 8192, abi.MULTINOMIAL, seed=1, precision=abi.FP64_PARITY)
+    r = engine.smooth(m, 2048, abi.MULTINOMIAL, seed=1, precision=abi.FP64_PARITY)
+    assert np.isfinite(r["log_norm_const"])

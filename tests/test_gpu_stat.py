@@ -263,3 +263,26 @@ def test_constrained_rw_rejection_sampling(engine):
         means = np.stack([r["mean"][:, 0] for r in runs])
         z = (means.mean(0) - gm) / np.maximum(means.std(0, ddof=1) / np.sqrt(len(runs)), 1e-12)
         assert np.sqrt(np.mean(z ** 2)) < 2.0, (precision, np.sqrt(np.mean(z ** 2)))
+
+
+def test_fp32_dense_large_n_sampler(engine):
+    """N beyond the shared-memory column staging of c32_sample (N = 8192:
+    the row CDF plus the staged column pairs exceed 227 KB): the sampler
+    keeps only the row CDF in shared memory and reads the pass-1 hand-off
+    from L2 (samplew_kernel over Aux32Recompute). Same bounds as
+    test_lgssm_means_match_kalman (errors shrink with N); N >= 65536 is
+    refused (the packed sub-block index)."""
+    m = models.lgssm_check(127)
+    km, kP, ll = kalman_smooth(m)
+    zs = []
+    for seed in (3, 4, 5, 6):
+        r = engine.smooth(m, 8192, abi.MULTINOMIAL, seed=seed, precision=abi.FP32)
+        zs.append(np.mean(_z(r["mean"], km, kP) ** 2))
+        assert abs(r["log_norm_const"] - ll) < 1.0, (r["log_norm_const"], ll)
+    assert np.sqrt(np.mean(zs)) < 0.1, np.sqrt(np.mean(zs))
+    ratio = r["cov"][:, 0, 0] / kP[:, 0, 0]
+    assert 0.85 < np.median(ratio) < 1.15
+    s = engine.smooth(m, 8192, abi.SYSTEMATIC, seed=9, precision=abi.FP32)
+    assert np.sqrt(np.mean(_z(s["mean"], km, kP) ** 2)) < 0.2
+    with pytest.raises(ValueError, match="65536"):
+        engine.smooth(m, 65536, abi.MULTINOMIAL, seed=1, precision=abi.FP32)

@@ -9,11 +9,13 @@ if sys.argv[1] == "run":
     from paper_2202_02264_b200 import abi, models
     e = D.Engine(0)
     out = {}
-    for name, m, N, rs in [("sv_mh", models.sv(1023), 512, abi.MH_LAZY),
-                           ("cv_mh", models.cv_tracking(511), 256, abi.MH_LAZY),
-                           ("crw_rej", models.constrained_rw(511, 0.3), 256, abi.REJECTION_LAZY),
-                           ("lg_mh", models.lgssm_check(1000), 300, abi.MH_LAZY)]:
-        r = e.smooth(m, N, rs, seed=7, precision=abi.FP32, want_pairs=True, mh_steps=16)
+    for name, m, N, rs, B in [("sv_mh", models.sv(1023), 512, abi.MH_LAZY, 16),
+                              ("cv_mh", models.cv_tracking(511), 256, abi.MH_LAZY, 16),
+                              ("crw_rej", models.constrained_rw(511, 0.3), 256, abi.REJECTION_LAZY, 16),
+                              ("lg_mh", models.lgssm_check(1000), 300, abi.MH_LAZY, 16),
+                              ("sv_mh13", models.sv(255), 200, abi.MH_LAZY, 13),
+                              ("cv_mh2", models.cv_tracking(127), 128, abi.MH_LAZY, 2)]:
+        r = e.smooth(m, N, rs, seed=7, precision=abi.FP32, want_pairs=True, mh_steps=B)
         out[name + "_l"] = r["pair_left"]
         out[name + "_r"] = r["pair_right"]
         out[name + "_ev"] = np.array([r["weight_evals"]])
