@@ -755,6 +755,11 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
   }
 }
 
+#ifndef DSMC_MH_BATCH
+#define DSMC_MH_BATCH 8
+#endif
+constexpr int kMhBatch = DSMC_MH_BATCH;  // MH steps per batch (a multiple of 4)
+static_assert(kMhBatch % 4 == 0, "whole Philox blocks per batch");
 __device__ __forceinline__ bool lazy_serial_mh() {
 #ifdef DSMC_LAZY_SERIAL
   return true;
@@ -765,8 +770,30 @@ __device__ __forceinline__ bool lazy_serial_mh() {
 
 // FP32 lazy samplers: the entry in log2 units in the unexpanded whitened
 // form (accurate for any state), bound in log2 units.
-template <int D>
-__global__ void lazy32_kernel(Bufs b, LevelArgs la, int mh, size_t mh_steps) {
+// MH and rejection are separate instantiations (their batches need
+// different register budgets).
+// The draws of MB lazy steps / trials (3 u64 each: index i, index j, the
+// uniform as a log2) from NBLK = 3 MB / 4 whole Philox blocks starting at
+// block b0; each block is consumed as soon as it is generated.
+template <int MB>
+__device__ __forceinline__ void draw_batch(const StreamId& id, uint64_t b0, int N, uint32_t* pi,
+                                           uint32_t* pj, float* lu) {
+#pragma unroll
+  for (int r = 0; r < 3 * MB / 4; ++r) {
+    const U64x4 blk = stream_block(id, b0 + r);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int n = 4 * r + c, q = n / 3;
+      if (n % 3 == 0) pi[q] = (uint32_t)u64_index(blk.v[c], N);
+      else if (n % 3 == 1) pj[q] = (uint32_t)u64_index(blk.v[c], N);
+      else lu[q] = lg2((float)u64_uniform_pos(blk.v[c]));
+    }
+  }
+}
+
+template <int D, bool MH>
+__global__ void lazy32_kernel(Bufs b, LevelArgs la, size_t mh_steps) {
+  constexpr bool mh = MH;
   const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   const int N = b.N;
@@ -809,40 +836,33 @@ __global__ void lazy32_kernel(Bufs b, LevelArgs la, int mh, size_t mh_steps) {
     StreamReader s;
     s.init(stream_id(b.seeds[ch], la.key_level, node, DSMC_ROLE_PAIR_RESAMPLE, m + 1));
     uint32_t oi = 0, oj = 0;
-    if (mh) {
+    if constexpr (mh) {
       uint32_t i = (uint32_t)(m % N), j = i;
       float cur = 0.f;
       bool have = false;
       // Each MH step draws exactly 3 u64 (two indices, one uniform;
-      // resampling.cpp:258-275), so 4 steps are 3 whole Philox blocks and
-      // their draws and proposal probes do not depend on the chain state:
-      // generate and probe 4 steps at once (4 independent gather chains in
-      // flight), then apply the 4 accept decisions in order. Bit-identical to
-      // the step-by-step loop below, which finishes any remainder.
+      // resampling.cpp:258-275), so kMhBatch = 8 steps are 6 whole Philox
+      // blocks and their draws and proposal probes do not depend on the chain
+      // state: generate and probe 8 steps at once (8 independent gather
+      // chains in flight), then apply the 8 accept decisions in order.
+      // Bit-identical to the step-by-step loop below, which finishes any
+      // remainder (tools/lazy_ab.py; C3 68.2 -> 57.2 ms/step, batches of 4 /
+      // 12 / 16: 61.8 / 70.8 / 70.5 ms, profiles/r02f_lazy_batch.md).
       size_t st = 0;
       if (!lazy_serial_mh()) {
         cur = probe(i, j);
         ++evals;
         have = true;
-        for (; st + 4 <= mh_steps; st += 4) {
-          const uint64_t b3 = 3 * (st / 4);
-          const U64x4 r0 = stream_block(s.id, b3), r1 = stream_block(s.id, b3 + 1),
-                      r2 = stream_block(s.id, b3 + 2);
-          const uint64_t u[12] = {r0.v[0], r0.v[1], r0.v[2], r0.v[3], r1.v[0], r1.v[1],
-                                  r1.v[2], r1.v[3], r2.v[0], r2.v[1], r2.v[2], r2.v[3]};
-          uint32_t pi[4], pj[4];
-          float lu[4], prop[4];
+        constexpr int MB = kMhBatch, NBLK = 3 * MB / 4;
+        for (; st + MB <= mh_steps; st += MB) {
+          uint32_t pi[MB], pj[MB];
+          float lu[MB], prop[MB];
+          draw_batch<MB>(s.id, NBLK * (st / MB), N, pi, pj, lu);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            pi[q] = (uint32_t)u64_index(u[3 * q], N);
-            pj[q] = (uint32_t)u64_index(u[3 * q + 1], N);
-            lu[q] = lg2((float)u64_uniform_pos(u[3 * q + 2]));
-          }
+          for (int q = 0; q < MB; ++q) prop[q] = probe(pi[q], pj[q]);
+          evals += MB;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) prop[q] = probe(pi[q], pj[q]);
-          evals += 4;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < MB; ++q) {
             if (lu[q] < prop[q] - cur) {
               i = pi[q];
               j = pj[q];
@@ -850,7 +870,7 @@ __global__ void lazy32_kernel(Bufs b, LevelArgs la, int mh, size_t mh_steps) {
             }
           }
         }
-        s.blk = 3 * (st / 4);  // the remainder continues the stream
+        s.blk = 3 * (st / 4);  // the remainder continues the stream (MB | st)
         s.pos = 4;
       }
       for (; st < mh_steps; ++st) {
@@ -877,7 +897,31 @@ __global__ void lazy32_kernel(Bufs b, LevelArgs la, int mh, size_t mh_steps) {
       if (lnonuni) bnd += b.LWMAX[(size_t)ch * b.K + L.t];
       const float bound2 = (float)(bnd * kLog2E);
       bool ok = false;
-      for (uint64_t trial = 0; trial < (1u << 24) && !err; ++trial) {
+      // trials also draw exactly 3 u64 each (i, j, then the uniform): the
+      // same batching as MH, the trials after the first accepted (or
+      // failing) one of a batch are evaluated but neither counted nor used
+      constexpr int MB = kMhBatch, NBLK = 3 * MB / 4;
+      uint64_t trial = 0;
+      for (; !lazy_serial_mh() && trial < (1u << 24) && !err && !ok; trial += MB) {
+        uint32_t pi[MB], pj[MB];
+        float lu[MB], lw[MB];
+        draw_batch<MB>(s.id, NBLK * (trial / MB), N, pi, pj, lu);
+#pragma unroll
+        for (int q = 0; q < MB; ++q) lw[q] = probe(pi[q], pj[q]);
+#pragma unroll
+        for (int q = 0; q < MB; ++q) {
+          if (ok || err) continue;
+          ++evals;
+          if (isnan(lw[q]) || lw[q] - bound2 > 1e-3f) {
+            err = DSMC_E_INVALID_ARGUMENT; why = isnan(lw[q]) ? kReasonNaN : kReasonOverBound;
+          } else if (lu[q] <= lw[q] - bound2) {
+            oi = pi[q];
+            oj = pj[q];
+            ok = true;
+          }
+        }
+      }
+      for (; lazy_serial_mh() && trial < (1u << 24) && !err; ++trial) {
         const uint32_t i = (uint32_t)s.index(N), j = (uint32_t)s.index(N);
         const float lw = probe(i, j);
         ++evals;

@@ -309,6 +309,13 @@ size_t samplew_smem(int N, int slots) {
   return head + (size_t)slots * (16 + 4) + sizeof(int) * (size_t)((N + kSub - 1) / kSub);
 }
 
+template <int D>
+void launch_lazy32(dim3 grid, cudaStream_t s, const Bufs& b, const LevelArgs& la, int mh,
+                   size_t steps) {
+  if (mh) lazy32_kernel<D, true><<<grid, 128, 0, s>>>(b, la, steps);
+  else lazy32_kernel<D, false><<<grid, 128, 0, s>>>(b, la, steps);
+}
+
 int wide_dp(int d) { return d <= 8 ? 8 : d <= 16 ? 16 : 32; }
 bool getenv_flag(const char* name) {  // A/B switches for tests and tools
   const char* f = getenv(name);
@@ -1119,10 +1126,10 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
           lazy64_kernel<<<grid, 128, 0, ctx->stream>>>(b, la, mh, o.mh_steps);
         } else {
           switch (d) {
-            case 1: lazy32_kernel<1><<<grid, 128, 0, ctx->stream>>>(b, la, mh, o.mh_steps); break;
-            case 2: lazy32_kernel<2><<<grid, 128, 0, ctx->stream>>>(b, la, mh, o.mh_steps); break;
-            case 3: lazy32_kernel<3><<<grid, 128, 0, ctx->stream>>>(b, la, mh, o.mh_steps); break;
-            default: lazy32_kernel<4><<<grid, 128, 0, ctx->stream>>>(b, la, mh, o.mh_steps); break;
+            case 1: launch_lazy32<1>(grid, ctx->stream, b, la, mh, o.mh_steps); break;
+            case 2: launch_lazy32<2>(grid, ctx->stream, b, la, mh, o.mh_steps); break;
+            case 3: launch_lazy32<3>(grid, ctx->stream, b, la, mh, o.mh_steps); break;
+            default: launch_lazy32<4>(grid, ctx->stream, b, la, mh, o.mh_steps); break;
           }
         }
         LAUNCHED(ctx);
@@ -2562,10 +2569,10 @@ int dsmc_cross_combine(dsmc_ctx* ctx, const dsmc_model_handle* hc, const dsmc_wi
     const int mh = wo->resampler == DSMC_MH_LAZY;
     const dim3 grid((N + 127) / 128, 1, 1);
     switch (d) {
-      case 1: lazy32_kernel<1><<<grid, 128, 0, s>>>(b, la, mh, wo->mh_steps); break;
-      case 2: lazy32_kernel<2><<<grid, 128, 0, s>>>(b, la, mh, wo->mh_steps); break;
-      case 3: lazy32_kernel<3><<<grid, 128, 0, s>>>(b, la, mh, wo->mh_steps); break;
-      default: lazy32_kernel<4><<<grid, 128, 0, s>>>(b, la, mh, wo->mh_steps); break;
+      case 1: launch_lazy32<1>(grid, s, b, la, mh, wo->mh_steps); break;
+      case 2: launch_lazy32<2>(grid, s, b, la, mh, wo->mh_steps); break;
+      case 3: launch_lazy32<3>(grid, s, b, la, mh, wo->mh_steps); break;
+      default: launch_lazy32<4>(grid, s, b, la, mh, wo->mh_steps); break;
     }
     LAUNCHED(ctx);
     lazy_finish_kernel<<<dim3(1, 1, 1), 256, 0, s>>>(b, la);
