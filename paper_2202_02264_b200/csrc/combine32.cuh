@@ -772,25 +772,6 @@ __device__ __forceinline__ bool lazy_serial_mh() {
 // form (accurate for any state), bound in log2 units.
 // MH and rejection are separate instantiations (their batches need
 // different register budgets).
-// The draws of MB lazy steps / trials (3 u64 each: index i, index j, the
-// uniform as a log2) from NBLK = 3 MB / 4 whole Philox blocks starting at
-// block b0; each block is consumed as soon as it is generated.
-template <int MB>
-__device__ __forceinline__ void draw_batch(const StreamId& id, uint64_t b0, int N, uint32_t* pi,
-                                           uint32_t* pj, float* lu) {
-#pragma unroll
-  for (int r = 0; r < 3 * MB / 4; ++r) {
-    const U64x4 blk = stream_block(id, b0 + r);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int n = 4 * r + c, q = n / 3;
-      if (n % 3 == 0) pi[q] = (uint32_t)u64_index(blk.v[c], N);
-      else if (n % 3 == 1) pj[q] = (uint32_t)u64_index(blk.v[c], N);
-      else lu[q] = lg2((float)u64_uniform_pos(blk.v[c]));
-    }
-  }
-}
-
 template <int D, bool MH>
 __global__ void lazy32_kernel(Bufs b, LevelArgs la, size_t mh_steps) {
   constexpr bool mh = MH;
@@ -857,7 +838,8 @@ __global__ void lazy32_kernel(Bufs b, LevelArgs la, size_t mh_steps) {
         for (; st + MB <= mh_steps; st += MB) {
           uint32_t pi[MB], pj[MB];
           float lu[MB], prop[MB];
-          draw_batch<MB>(s.id, NBLK * (st / MB), N, pi, pj, lu);
+          draw_batch<MB>(s.id, NBLK * (st / MB), N, pi, pj, lu,
+                         [](uint64_t v) { return lg2((float)u64_uniform_pos(v)); });
 #pragma unroll
           for (int q = 0; q < MB; ++q) prop[q] = probe(pi[q], pj[q]);
           evals += MB;
@@ -905,7 +887,8 @@ __global__ void lazy32_kernel(Bufs b, LevelArgs la, size_t mh_steps) {
       for (; !lazy_serial_mh() && trial < (1u << 24) && !err && !ok; trial += MB) {
         uint32_t pi[MB], pj[MB];
         float lu[MB], lw[MB];
-        draw_batch<MB>(s.id, NBLK * (trial / MB), N, pi, pj, lu);
+        draw_batch<MB>(s.id, NBLK * (trial / MB), N, pi, pj, lu,
+                       [](uint64_t v) { return lg2((float)u64_uniform_pos(v)); });
 #pragma unroll
         for (int q = 0; q < MB; ++q) lw[q] = probe(pi[q], pj[q]);
 #pragma unroll

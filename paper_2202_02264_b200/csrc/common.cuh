@@ -165,6 +165,27 @@ struct StreamReader {
   }
 };
 
+// The draws of MB lazy steps / trials (3 u64 each: index i, index j, then the
+// uniform through `lu_of` -- log2 in FP32, log in FP64) from 3 MB / 4 whole
+// Philox blocks starting at block b0; each block is consumed as soon as it is
+// generated, so only the converted values stay live.
+template <int MB, class T, class F>
+__device__ __forceinline__ void draw_batch(const StreamId& id, uint64_t b0, int N, uint32_t* pi,
+                                           uint32_t* pj, T* lu, F lu_of) {
+  static_assert(MB % 4 == 0, "whole Philox blocks per batch");
+#pragma unroll
+  for (int r = 0; r < 3 * MB / 4; ++r) {
+    const U64x4 blk = stream_block(id, b0 + r);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int n = 4 * r + c, q = n / 3;
+      if (n % 3 == 0) pi[q] = (uint32_t)u64_index(blk.v[c], N);
+      else if (n % 3 == 1) pj[q] = (uint32_t)u64_index(blk.v[c], N);
+      else lu[q] = lu_of(blk.v[c]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ exp_w
 __device__ __forceinline__ double exp_w(double x) {
   if (isnan(x)) return x;
