@@ -830,11 +830,11 @@ __global__ void lazy32_kernel(Bufs b, LevelArgs la, size_t mh_steps) {
       // remainder (tools/lazy_ab.py; C3 68.2 -> 57.2 ms/step, batches of 4 /
       // 12 / 16: 61.8 / 70.8 / 70.5 ms, profiles/r02f_lazy_batch.md).
       size_t st = 0;
-      if (!lazy_serial_mh()) {
+      constexpr int MB = kMhBatch, NBLK = 3 * MB / 4;
+      if (!lazy_serial_mh() && mh_steps >= (size_t)MB) {  // (0 steps: no probe at all)
         cur = probe(i, j);
         ++evals;
         have = true;
-        constexpr int MB = kMhBatch, NBLK = 3 * MB / 4;
         for (; st + MB <= mh_steps; st += MB) {
           uint32_t pi[MB], pj[MB];
           float lu[MB], prop[MB];

@@ -187,32 +187,34 @@ __device__ __forceinline__ void draw_batch(const StreamId& id, uint64_t b0, int 
 }
 
 // ------------------------------------------------------------------ exp_w
+// The FP64 constants live in constant memory so DMUL / DFMA take them as
+// c[][] operands (as immediates each costs two UMOVs per use, ~14% of the
+// FP64 pass's instructions), and the special cases are selects around one
+// straight-line evaluation instead of branches. Same operations, same order,
+// same results as the branchy form.
+__constant__ double kExpW[16] = {
+    1.4426950408889634074,  -6.93147180369123816490e-01, -1.90821492927058770002e-10,
+    1.0 / 6227020800.0,     1.0 / 479001600,              1.0 / 39916800,
+    1.0 / 3628800,          1.0 / 362880,                 1.0 / 40320,
+    1.0 / 5040,             1.0 / 720,                    1.0 / 120,
+    1.0 / 24,               1.0 / 6,                      1.0 / 2,
+    1.0};
 __device__ __forceinline__ double exp_w(double x) {
-  if (isnan(x)) return x;
-  if (x <= -708.0) return 0.0;
-  const double xc = x > 710.0 ? 710.0 : x;
-  const double k = rint(__dmul_rn(xc, 1.4426950408889634074));
-  double r = __fma_rn(k, -6.93147180369123816490e-01, xc);
-  r = __fma_rn(k, -1.90821492927058770002e-10, r);
-  double p = 1.0 / 6227020800.0;
-  p = __fma_rn(p, r, 1.0 / 479001600);
-  p = __fma_rn(p, r, 1.0 / 39916800);
-  p = __fma_rn(p, r, 1.0 / 3628800);
-  p = __fma_rn(p, r, 1.0 / 362880);
-  p = __fma_rn(p, r, 1.0 / 40320);
-  p = __fma_rn(p, r, 1.0 / 5040);
-  p = __fma_rn(p, r, 1.0 / 720);
-  p = __fma_rn(p, r, 1.0 / 120);
-  p = __fma_rn(p, r, 1.0 / 24);
-  p = __fma_rn(p, r, 1.0 / 6);
-  p = __fma_rn(p, r, 1.0 / 2);
-  p = __fma_rn(p, r, 1.0);
-  p = __fma_rn(p, r, 1.0);
+  const bool nan = isnan(x), low = x <= -708.0;
+  const double xc = (nan || low) ? 0.0 : (x > 710.0 ? 710.0 : x);
+  const double k = rint(__dmul_rn(xc, kExpW[0]));
+  double r = __fma_rn(k, kExpW[1], xc);
+  r = __fma_rn(k, kExpW[2], r);
+  double p = kExpW[3];
+#pragma unroll
+  for (int q = 4; q < 16; ++q) p = __fma_rn(p, r, kExpW[q]);
+  p = __fma_rn(p, r, kExpW[15]);
   const long long ki = static_cast<long long>(k);
   const double scale =
       __longlong_as_double(static_cast<long long>(
           static_cast<unsigned long long>(ki + 1023) << 52));
-  return __dmul_rn(p, scale);
+  const double v = __dmul_rn(p, scale);
+  return nan ? x : (low ? 0.0 : v);
 }
 
 // b[l] = a[l] + a[l+4]; (b0 + b2) + (b1 + b3).
