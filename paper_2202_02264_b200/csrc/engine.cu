@@ -1074,7 +1074,12 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
   const bool lazy = o.resampler == DSMC_MH_LAZY || o.resampler == DSMC_REJECTION_LAZY;
   const int nsub = (N + kSub - 1) / kSub;
   const size_t ws_comb = fp64 ? (size_t)N * (5 + nsub) : ((size_t)N * nsub + 1) / 2;
-  const size_t ws_budget = (size_t)1 << 30;  // bytes per chunk
+  // bytes of pass-1 scratch per chunk: 4 GB = up to 65535 combines per
+  // launch (C5: 412.6 vs 415.3 ms/step at 1 GB; smaller chunks that would
+  // keep a chunk's sums in L2 lose more to wave tails: 507 ms at 32 MB;
+  // tools/gpu_chunk_ab.sh)
+  size_t ws_budget = (size_t)4 << 30;
+  if (const char* e = getenv("DSMC_WS_BUDGET_MB")) ws_budget = (size_t)atol(e) << 20;  // A/B
   // bytes per combine of the chunked scratch (the wide path's AUX dominates)
   const size_t per_comb = std::max<size_t>(ws_comb * 8 * B,
                                            wide ? ((size_t)2 * N * h->wb.DP + 2 * N) * 4 * B : 0);
