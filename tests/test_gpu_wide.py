@@ -112,3 +112,39 @@ def test_forced_wide_matches_float4_path(engine, tmp_path):
     lzw = np.array(json.loads(r.stdout.strip().splitlines()[-1]))
     lzf = np.array([x["log_norm_const"] for x in runs])
     assert abs(np.median(lzw) - np.median(lzf)) < 2.0
+
+
+def test_wide_systematic_matches_kalman(engine):
+    """The wide sampler's systematic branch (one shared uniform, sorted
+    points) against the exact smoother, same units as above."""
+    T, N, d = 63, 1024, 8
+    m = models.ar_iid(T, d)
+    km, kP, _ = models.kalman_smooth_numpy(m)
+    runs = [engine.smooth(m, N, abi.SYSTEMATIC, seed=s, precision=abi.FP32) for s in range(8)]
+    means = np.stack([r["mean"] for r in runs])
+    z = (means.mean(0) - km) / np.maximum(means.std(0, ddof=1) / np.sqrt(8), 1e-12)
+    assert np.sqrt(np.mean(z ** 2)) < 2.0, np.sqrt(np.mean(z ** 2))
+    ratio = np.einsum("tii->ti", runs[0]["cov"]) / np.einsum("tii->ti", kP)
+    assert 0.7 < np.median(ratio) < 1.2
+
+
+@pytest.mark.parametrize("which,msg", [("prop_cov", "proposal covariance at time 5"),
+                                       ("R", "R at time 9"), ("Q", "Q at time 7")])
+def test_wide_prep_reports_the_failing_time(engine, which, msg):
+    """The device model prep (prepw_kernel) factors every per-time matrix;
+    a non-positive-definite one is reported with its kind and time, as the
+    host prep did (the smallest failing time wins)."""
+    T, d = 15, 8
+    m = models.ar_iid(T, d)
+    A = dict(m.arrays)
+    K = T + 1
+    t = {"prop_cov": 5, "R": 9, "Q": 7}[which]
+    if which != "prop_cov":  # make the matrix time-varying first
+        A[which] = np.tile(np.asarray(A[which]).reshape(d, d), (K, 1, 1))
+    bad = np.array(A[which], dtype=np.float64).reshape(K, d, d).copy()
+    bad[t] = -np.eye(d)
+    bad[t + 3] = -np.eye(d)
+    A[which] = bad
+    m2 = abi.Model(m.kind, m.horizon, m.d, m.dy, **A)
+    with pytest.raises(ValueError, match=msg):
+        engine.smooth(m2, 64, abi.MULTINOMIAL, seed=1, precision=abi.FP32)
