@@ -181,13 +181,16 @@ __global__ void __launch_bounds__(32) prepw_kernel(DevModel md, WidePrep o) {
 }
 
 // ---------------------------------------------------------------- leaves
+#ifndef LEAFW_MINB
+#define LEAFW_MINB 2
+#endif
 template <int D>
-__global__ void __launch_bounds__(256) leafw_kernel(Bufs b, double* raw0) {
+__global__ void __launch_bounds__(256, LEAFW_MINB) leafw_kernel(Bufs b, double* raw0) {
   const int t = blockIdx.x, ch = blockIdx.y;
   const int gt = b.t0 + t;
   const WideBufs& w = b.w;
   const int d = w.d, dy = w.dy, N = b.N;
-  __shared__ float sL[D * D], sG[32 * D], se[32], sWP[D * D], sdm[D];
+  __shared__ __align__(16) float sL[D * D], sG[32 * D], se[32], sWP[D * D], sdm[D];
   __shared__ float sc;
   for (int i = threadIdx.x; i < D * D; i += blockDim.x) sL[i] = w.L[(size_t)gt * D * D + i];
   for (int i = threadIdx.x; i < w.DYP * D; i += blockDim.x) sG[i] = w.G[(size_t)gt * w.DYP * D + i];
@@ -225,13 +228,29 @@ __global__ void __launch_bounds__(256) leafw_kernel(Bufs b, double* raw0) {
         z[k] = (i & 1) ? r * sn : r * cs;
       }
     }
-    float x[D];
+    // x = L z and g = e - G z from broadcast 16-byte shared loads (4 entries
+    // each); L's upper triangle is stored as zeros, and fma(0, z, acc) = acc,
+    // so the row loops over whole float4s give the l <= k sums bit for bit
+    const size_t off = ((size_t)ch * b.K + t) * N + n;
+    float4* dst = reinterpret_cast<float4*>(w.X + off * D);
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      float acc = 0.f;
+    for (int q = 0; q < D / 4; ++q) {  // four rows of x at a time, stored at once
+      float xv[4];
 #pragma unroll
-      for (int l = 0; l <= k; ++l) acc = fmaf(sL[k * D + l], z[l], acc);
-      x[k] = acc;
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = 4 * q + kk;
+        float acc = 0.f;
+#pragma unroll
+        for (int l4 = 0; l4 <= k; l4 += 4) {
+          const float4 Lv = *reinterpret_cast<const float4*>(sL + k * D + l4);
+          acc = fmaf(Lv.x, z[l4], acc);
+          acc = fmaf(Lv.y, z[l4 + 1], acc);
+          acc = fmaf(Lv.z, z[l4 + 2], acc);
+          acc = fmaf(Lv.w, z[l4 + 3], acc);
+        }
+        xv[kk] = acc;
+      }
+      dst[q] = make_float4(xv[0], xv[1], xv[2], xv[3]);
     }
     float zz = 0.f, rr = 0.f;
 #pragma unroll
@@ -239,21 +258,22 @@ __global__ void __launch_bounds__(256) leafw_kernel(Bufs b, double* raw0) {
     for (int a = 0; a < dy; ++a) {
       float g = se[a];
 #pragma unroll
-      for (int l = 0; l < D; ++l) g = fmaf(-sG[a * D + l], z[l], g);
+      for (int l4 = 0; l4 < D; l4 += 4) {
+        const float4 Gv = *reinterpret_cast<const float4*>(sG + a * D + l4);
+        g = fmaf(-Gv.x, z[l4], g);
+        g = fmaf(-Gv.y, z[l4 + 1], g);
+        g = fmaf(-Gv.z, z[l4 + 2], g);
+        g = fmaf(-Gv.w, z[l4 + 3], g);
+      }
       rr = fmaf(g, g, rr);
     }
     const float col = (float)kLog2E * (sc + 0.5f * (zz - rr));
-    const size_t off = ((size_t)ch * b.K + t) * N + n;
-    float4* dst = reinterpret_cast<float4*>(w.X + off * D);
-#pragma unroll
-    for (int q = 0; q < D / 4; ++q) dst[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
     b.COL[off] = col;
     if (gt == 0) {  // raw leaf-0 weight h0 P0 / q0 (log): col / log2e + log P0(x)
+      const float* x = w.X + off * D;  // this thread's own stores, read back
       double qd = 0.0;
-#pragma unroll
       for (int k = 0; k < D; ++k) {
         double acc = 0.0;
-#pragma unroll
         for (int l = 0; l <= k; ++l) acc += (double)sWP[k * D + l] * ((double)x[l] - (double)sdm[l]);
         qd += acc * acc;
       }
@@ -480,18 +500,21 @@ struct WideRecompute {
       u[4 * c + 3] = v.w;
     }
   }
+  // four independent FMA chains (components k mod 4) instead of one chain of
+  // D: the recompute loop is latency-bound on this chain (one column at a
+  // time per slot), not on issue
   __device__ float weight_exp(int j, const float* u, float sh) const {
     const float4* yp = reinterpret_cast<const float4*>(ax.Y + (size_t)j * D);
-    float t = ax.A[j] + sh;
+    float t0 = ax.A[j] + sh, t1 = 0.f, t2 = 0.f, t3 = 0.f;
 #pragma unroll
     for (int c = 0; c < D / 4; ++c) {
       const float4 yv = yp[c];
-      t = fmaf(u[4 * c], yv.x, t);
-      t = fmaf(u[4 * c + 1], yv.y, t);
-      t = fmaf(u[4 * c + 2], yv.z, t);
-      t = fmaf(u[4 * c + 3], yv.w, t);
+      t0 = fmaf(u[4 * c], yv.x, t0);
+      t1 = fmaf(u[4 * c + 1], yv.y, t1);
+      t2 = fmaf(u[4 * c + 2], yv.z, t2);
+      t3 = fmaf(u[4 * c + 3], yv.w, t3);
     }
-    return ex2(t);
+    return ex2((t0 + t1) + (t2 + t3));
   }
 };
 // The float4 path's hand-off (pass 1 of c32_pair): d <= 4, pass 1's exact
@@ -539,15 +562,22 @@ __global__ void __launch_bounds__(256) samplew_kernel(Bufs b, LevelArgs la, int 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float gm = -CUDART_INF_F;
   for (int i = tid; i < N; i += blockDim.x) {
+    // online LSE over the row's sub-block sums, 16 loads in flight per round
     float m = -CUDART_INF_F, acc = 0.f;
-    for (int q = 0; q < nsub; ++q) {
-      const float v = ws[(size_t)q * N + i];
-      if (v == -CUDART_INF_F) continue;
-      if (v > m) {
-        acc = m == -CUDART_INF_F ? 0.f : acc * ex2(m - v);
-        m = v;
+    for (int s0 = 0; s0 < nsub; s0 += 16) {
+      float v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = s0 + q < nsub ? ws[(size_t)(s0 + q) * N + i] : -CUDART_INF_F;
+      float cm = v[0];
+#pragma unroll
+      for (int q = 1; q < 16; ++q) cm = fmaxf(cm, v[q]);
+      if (cm == -CUDART_INF_F) continue;
+      if (cm > m) {
+        acc = m == -CUDART_INF_F ? 0.f : acc * ex2(m - cm);
+        m = cm;
       }
-      acc += ex2(v - m);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc += ex2(v[q] - m);
     }
     const float La = m == -CUDART_INF_F ? -CUDART_INF_F : m + lg2(acc);
     Lrow[i] = La;
