@@ -35,6 +35,7 @@ struct LevelArgs {
   size_t aux_comb;    // floats per combine in aux
   int tc_ncs;         // tensor-core pass 1: column splits per 128-row tile
   int tc_nk;          // ... and combines in this chunk (persistent work list)
+  int wide_tiles;     // wide path: the prologue also writes pass 1's column tiles
 };
 
 // Block meta derived from the schedule geometry.

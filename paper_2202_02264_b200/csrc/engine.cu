@@ -316,6 +316,12 @@ void launch_lazy32(dim3 grid, cudaStream_t s, const Bufs& b, const LevelArgs& la
   else lazy32_kernel<D, false><<<grid, 128, 0, s>>>(b, la, steps);
 }
 
+// floats per combine of the wide AUX (wide.cuh auxw): Y, U, A, B and the
+// column tiles of the pipelined pass 1 (64 columns x K = 3 D + 8 per tile)
+size_t wide_aux_floats(int N, int D) {
+  return auxw_yt_off(N, D) + (size_t)((N + kSub - 1) / kSub) * kSub * (3 * D + 8);
+}
+
 int wide_dp(int d) { return d <= 8 ? 8 : d <= 16 ? 16 : 32; }
 bool getenv_flag(const char* name) {  // A/B switches for tests and tools
   const char* f = getenv(name);
@@ -748,7 +754,15 @@ template <int D>
 int launch_wide(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systematic) {
   const int N = b.N;
   const int nrt = (N + kWRows - 1) / kWRows, nsub = (N + kSub - 1) / kSub;
-  la.aux_comb = (size_t)2 * N * D + 2 * (size_t)N;
+  // pass-1 kernel: the pipelined tcgen05 kernel (default), the first
+  // tcgen05 kernel (DSMC_WIDE_PAIR=tc1) or the register-tiled CUDA-core one
+  // (DSMC_WIDE_PAIR=fma)
+  static const int pair_kind = [] {
+    const char* e = getenv("DSMC_WIDE_PAIR");
+    return !e ? 2 : strcmp(e, "fma") == 0 ? 0 : strcmp(e, "tc1") == 0 ? 1 : 2;
+  }();
+  la.wide_tiles = pair_kind == 2;
+  la.aux_comb = wide_aux_floats(N, D);
   {
     void* p;
     CU(ctx->arena.get("AUXW", la.aux_comb * sizeof(float) * (size_t)nk * b.B, &p));
@@ -779,16 +793,12 @@ int launch_wide(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemat
   }
   prologw_kernel<D><<<dim3((N + 127) / 128, nk, b.B), 128, 0, ctx->stream>>>(b, la);
   LAUNCHED(ctx);
-  // the d-term cross term on the tensor cores (tcgen05, 3xTF32) by default;
-  // DSMC_WIDE_PAIR=fma selects the register-tiled CUDA-core kernel
-  static const bool fma_pair = [] {
-    const char* e = getenv("DSMC_WIDE_PAIR");
-    return e && strcmp(e, "fma") == 0;
-  }();
-  if (fma_pair)
+  if (pair_kind == 0)
     pairw_kernel<D><<<dim3(nrt * ncs, nk, b.B), 256, sm1, ctx->stream>>>(b, la);
-  else
+  else if (pair_kind == 1)
     pairw_tc_kernel<D><<<dim3(nrt * ncs, nk, b.B), 128, WideTc<D>::SMEM, ctx->stream>>>(b, la);
+  else
+    pairw_tc2_kernel<D><<<dim3(nrt * ncs, nk, b.B), 256, WideTc2<D>::SMEM, ctx->stream>>>(b, la);
   LAUNCHED(ctx);
   if (ev) CU(rec_event(ev[1], ctx->stream));
   samplew_kernel<D><<<dim3(sb, nk, b.B), 256, sm2, ctx->stream>>>(b, la, systematic);
@@ -1082,7 +1092,7 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
   if (const char* e = getenv("DSMC_WS_BUDGET_MB")) ws_budget = (size_t)atol(e) << 20;  // A/B
   // bytes per combine of the chunked scratch (the wide path's AUX dominates)
   const size_t per_comb = std::max<size_t>(ws_comb * 8 * B,
-                                           wide ? ((size_t)2 * N * h->wb.DP + 2 * N) * 4 * B : 0);
+                                           wide ? wide_aux_floats(N, h->wb.DP) * 4 * B : 0);
   const int chunk = (int)std::max<size_t>(1, std::min<size_t>(65535, ws_budget / per_comb));
   double* ws = nullptr;
   if (!lazy && T > 0) {
@@ -1360,6 +1370,7 @@ cudaError_t configure_wide(int smem) {
   cudaError_t e = set_max_dynamic_smem(pairw_kernel<D>, smem);
   if (e == cudaSuccess) e = set_max_dynamic_smem(samplew_kernel<D>, smem);
   if (e == cudaSuccess) e = set_max_dynamic_smem(pairw_tc_kernel<D>, smem);
+  if (e == cudaSuccess) e = set_max_dynamic_smem(pairw_tc2_kernel<D>, smem);
   return e;
 }
 cudaError_t configure_device(int device, int smem) {

@@ -296,7 +296,13 @@ struct AuxW {
   float* U;
   float* A;
   float* B;
+  float* YT;  // pass 1's column operand, one K-major core-matrix tile per sub-block
 };
+// floats per combine of the wide AUX: Y, U (N x D), A, B (N), then the
+// 256-byte aligned column tiles (nsub x WideTc2<D>::B_BYTES)
+__host__ __device__ inline size_t auxw_yt_off(int N, int D) {
+  return ((size_t)2 * N * D + 2 * (size_t)N + 63) & ~(size_t)63;
+}
 template <int D>
 __device__ __forceinline__ AuxW auxw(const LevelArgs& la, size_t comb, int N) {
   float* base = la.aux + comb * la.aux_comb;
@@ -305,7 +311,60 @@ __device__ __forceinline__ AuxW auxw(const LevelArgs& la, size_t comb, int N) {
   a.U = base + (size_t)N * D;
   a.A = base + 2 * (size_t)N * D;
   a.B = base + 2 * (size_t)N * D + N;
+  a.YT = base + auxw_yt_off(N, D);
   return a;
+}
+
+// Pipelined tensor-core pass 1 (pairw_tc2_kernel): K-major operands with the
+// column and row terms folded into the contraction,
+//   A_i = [u_hi(D), u_lo(D), u_hi(D), 1, 1, 1, b_hi, b_mid, b_lo, 0...]
+//   B_j = [y_hi(D), y_hi(D), y_lo(D), a_hi, a_mid, a_lo, 1, 1, 1, 0...]
+// so D_ij = u_i . y_j + A_j + B_i = w_ij (3xTF32, three-way splits of A_j
+// and B_i); dead columns / rows carry a finite stand-in (kDeadColW).
+constexpr float kDeadColW = -1e30f;
+template <int D>
+struct WideTc2 {
+  static constexpr int K = 3 * D + 8;
+  static constexpr int KC = K / 4;         // 16-byte chunks per operand row
+  static constexpr int LBO = 128;          // bytes between K-adjacent core matrices
+  static constexpr int SBO = KC * 128;     // bytes between 8-row groups
+  static constexpr int KS = K / 8;         // MMAs per tile (K = 8 per tf32 MMA)
+  static constexpr int A_BYTES = kWRows / 8 * SBO;
+  static constexpr int B_BYTES = kSub / 8 * SBO;
+  static constexpr int SMEM = A_BYTES + 2 * B_BYTES + 64 + 2 * kWRows * 8;  // + barriers, halves
+};
+template <int D>
+__device__ __forceinline__ void wtc2_store_row(uint8_t* base, int r, const float* vals) {
+  using L = WideTc2<D>;
+  uint8_t* p = base + (r & 7) * 16 + (r >> 3) * L::SBO;
+#pragma unroll
+  for (int c = 0; c < L::KC; ++c)
+    *reinterpret_cast<float4*>(p + c * L::LBO) =
+        make_float4(vals[4 * c], vals[4 * c + 1], vals[4 * c + 2], vals[4 * c + 3]);
+}
+// column q's row of its sub-block tile (the prologue writes them; padding
+// columns q >= N get y = 0 and the dead stand-in)
+template <int D>
+__device__ __forceinline__ void wtc2_store_col(const AuxW& ax, int q, const float* y, float a) {
+  using L = WideTc2<D>;
+  float vals[L::K];
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const float hi = tf32_hi(y[c]);
+    vals[c] = hi;
+    vals[D + c] = hi;
+    vals[2 * D + c] = y[c] - hi;
+  }
+  const float av = a > kDeadColW ? a : kDeadColW;
+  const float ah = tf32_hi(av), r1 = av - ah, am = tf32_hi(r1);
+  vals[3 * D] = ah;
+  vals[3 * D + 1] = am;
+  vals[3 * D + 2] = r1 - am;
+  vals[3 * D + 3] = vals[3 * D + 4] = vals[3 * D + 5] = 1.f;  // x the row's B_i split
+#pragma unroll
+  for (int c = 3 * D + 6; c < L::K; ++c) vals[c] = 0.f;
+  uint8_t* tile = reinterpret_cast<uint8_t*>(ax.YT) + (size_t)(q / kSub) * L::B_BYTES;
+  wtc2_store_row<D>(tile, q % kSub, vals);
 }
 
 template <int D>
@@ -327,7 +386,15 @@ __global__ void __launch_bounds__(128) prologw_kernel(Bufs b, LevelArgs la) {
   const size_t cslot = (size_t)blockIdx.z * gridDim.y + blockIdx.y;
   const AuxW ax = auxw<D>(la, cslot, N);
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= N) return;
+  if (q >= N) {
+    if (la.wide_tiles && q < (N + kSub - 1) / kSub * kSub) {  // padding column of the last tile
+      float y0[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) y0[c] = 0.f;
+      wtc2_store_col<D>(ax, q, y0, -CUDART_INF_F);
+    }
+    return;
+  }
   const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
   float x[D], y[D];
   {  // column q: right block's first-leaf state
@@ -355,6 +422,7 @@ __global__ void __launch_bounds__(128) prologw_kernel(Bufs b, LevelArgs la) {
 #pragma unroll
     for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]);
     ax.A[q] = col - nrm;
+    if (la.wide_tiles) wtc2_store_col<D>(ax, q, y, col - nrm);
   }
   {  // row q: left block's last-leaf state
     const uint32_t p = map_last(b, la, ch, L, q);
@@ -993,6 +1061,171 @@ __global__ void __launch_bounds__(128) pairw_tc_kernel(Bufs b, LevelArgs la) {
   }
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
+}
+
+// Pipelined pass 1 (default): the column operand tiles come from the
+// prologue through bulk copies (cp.async.bulk, TMA engine) into two shared
+// stages, the row operand is built once per CTA, and two TMEM accumulators
+// (2 x 64 columns) let sub-block s+1's MMAs run while the CTA's threads
+// take the exponentials of sub-block s. Per (row = TMEM lane, sub-block):
+// the exact-max log2-sum of the 64 values D_ij + B_i, as pairw_tc_kernel.
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) pairw_tc2_kernel(Bufs b, LevelArgs la) {
+  using L = WideTc2<D>;
+  extern __shared__ __align__(1024) uint8_t wtc2_smem[];
+  uint8_t* sA = wtc2_smem;
+  uint8_t* sB = sA + L::A_BYTES;  // stage q at sB + q * B_BYTES
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + 2 * L::B_BYTES);  // [2] tile landed
+  uint64_t* mmad = full + 2;                                          // [2] MMAs done
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(mmad + 2);
+  float2* part = reinterpret_cast<float2*>(sB + 2 * L::B_BYTES + 64);  // [2 acc][128 rows]
+  const int N = b.N;
+  const int nsub = (N + kSub - 1) / kSub;
+  const int nrt = (N + kWRows - 1) / kWRows;
+  const int rt = blockIdx.x % nrt, cs = blockIdx.x / nrt, ncs = gridDim.x / nrt;
+  const size_t cslot = (size_t)blockIdx.z * gridDim.y + blockIdx.y;
+  const AuxW ax = auxw<D>(la, cslot, N);
+  float* ws = reinterpret_cast<float*>(la.ws) + cslot * la.ws_comb * 2;
+  const int row0 = rt * kWRows;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int sb0 = cs * nsub / ncs, sb1 = (cs + 1) * nsub / ncs, nit = sb1 - sb0;
+  const uint8_t* YT = reinterpret_cast<const uint8_t*>(ax.YT);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(s_tmem)),
+                 "r"(128));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int q = 0; q < 4; ++q) mbar_init(full + q, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    for (int q = 0; q < 2 && q < nit; ++q)
+      tma_bulk_g2s(sB + q * L::B_BYTES, YT + (size_t)(sb0 + q) * L::B_BYTES, L::B_BYTES, full + q);
+  }
+  // row operand of row `tid` (built while the first tiles are in flight)
+  const int i = row0 + tid;
+  float Bi = -CUDART_INF_F;
+  if (tid < kWRows) {
+    float vals[L::K];
+    float u[D];
+    if (i < N) {
+      const float4* up = reinterpret_cast<const float4*>(ax.U + (size_t)i * D);
+#pragma unroll
+      for (int c = 0; c < D / 4; ++c) {
+        const float4 v = up[c];
+        u[4 * c] = v.x;
+        u[4 * c + 1] = v.y;
+        u[4 * c + 2] = v.z;
+        u[4 * c + 3] = v.w;
+      }
+      Bi = ax.B[i];
+    } else {
+#pragma unroll
+      for (int c = 0; c < D; ++c) u[c] = 0.f;
+    }
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const float hi = tf32_hi(u[c]);
+      vals[c] = hi;
+      vals[D + c] = u[c] - hi;
+      vals[2 * D + c] = hi;
+    }
+    vals[3 * D] = vals[3 * D + 1] = vals[3 * D + 2] = 1.f;
+    const float bv = Bi > kDeadColW ? Bi : kDeadColW;
+    const float bh = tf32_hi(bv), r1 = bv - bh, bm = tf32_hi(r1);
+    vals[3 * D + 3] = bh;
+    vals[3 * D + 4] = bm;
+    vals[3 * D + 5] = r1 - bm;
+#pragma unroll
+    for (int c = 3 * D + 6; c < L::K; ++c) vals[c] = 0.f;
+    wtc2_store_row<D>(sA, tid, vals);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *s_tmem;
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kSub >> 3) << 17) |
+                         ((uint32_t)(kWRows >> 4) << 24);
+  // epilogue: warp w reads TMEM lanes 32 (w & 3).. (its rows) and columns
+  // 32 (w >> 2).. of the accumulator; the two column halves meet in `part`
+  const int quad = warp & 3, half = warp >> 2;
+  const int erow = 32 * quad + (tid & 31), ei = row0 + erow;
+  const uint32_t lane_off = ((uint32_t)(32 * quad) << 16) + 32 * half;
+  for (int it = 0; it <= nit; ++it) {
+    if (it < nit && tid == 0) {  // MMAs of sub-block sb0 + it into accumulator it & 1
+      const int q = it & 1;
+      mbar_wait(smem_u32(full + q), (it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      uint8_t* tB = sB + q * L::B_BYTES;
+#pragma unroll
+      for (int ks = 0; ks < L::KS; ++ks) {
+        const uint64_t da = umma_sdesc(smem_u32(sA) + ks * 2 * L::LBO, L::LBO, L::SBO);
+        const uint64_t db = umma_sdesc(smem_u32(tB) + ks * 2 * L::LBO, L::LBO, L::SBO);
+        const uint32_t acc = ks > 0;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + q * 64),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+              smem_u32(mmad + q)));
+    }
+    if (it > 0) {  // epilogue of sub-block sb0 + it - 1
+      const int p = (it - 1) & 1;
+      mbar_wait(smem_u32(mmad + p), ((it - 1) >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (tid == 0 && it + 1 < nit)  // stage p is free: fetch sub-block sb0 + it + 1
+        tma_bulk_g2s(sB + p * L::B_BYTES, YT + (size_t)(sb0 + it + 1) * L::B_BYTES, L::B_BYTES,
+                     full + p);
+      float v[32];
+      tmem_ld32(tmem + p * 64 + lane_off, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      // max and sum of the half as 8 independent chains
+      float mc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) mc[c] = v[c];
+#pragma unroll
+      for (int c = 8; c < 32; ++c) mc[c & 7] = fmaxf(mc[c & 7], v[c]);
+      const float m = fmaxf(fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3])),
+                            fmaxf(fmaxf(mc[4], mc[5]), fmaxf(mc[6], mc[7])));
+      float sum = 0.f;
+      if (m > -1e29f) {
+        float sc[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) sc[c] = ex2(v[c] - m);
+#pragma unroll
+        for (int c = 8; c < 32; ++c) sc[c & 7] += ex2(v[c] - m);
+        sum = ((sc[0] + sc[1]) + (sc[2] + sc[3])) + ((sc[4] + sc[5]) + (sc[6] + sc[7]));
+      }
+      if (half == 1) part[p * kWRows + erow] = make_float2(m, sum);
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();  // accumulator p read by every warp before MMA(it + 1) reuses it
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (half == 0 && ei < N) {  // combine the halves (part[p] is rewritten two
+        const float2 o = part[p * kWRows + erow];  // iterations later, after a barrier)
+        const float M = fmaxf(m, o.x);
+        float S = 0.f;
+        if (M > -1e29f) S = (m > -1e29f ? sum * ex2(m - M) : 0.f) + (o.x > -1e29f ? o.y * ex2(o.x - M) : 0.f);
+        ws[(size_t)(sb0 + it - 1) * N + ei] = S > 0.f ? M + lg2(S) : -CUDART_INF_F;
+      }
+    }
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
 }
 
 }  // namespace dsmc_dev
