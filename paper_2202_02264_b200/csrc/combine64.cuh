@@ -87,7 +87,22 @@ struct Col64 {
   double* base; // ld
   double* lwr;  // ld or null
   int ld;
+  // FP32 copies for pass 1's row-max screen (c64_rows with fast = 1): the
+  // column states centred on column 0's (x - cen: float4 per column, d > 1;
+  // float, d = 1), bases and leaf weights, plus the largest finite magnitudes
+  // of each (cm: base, lwr, x_k - cen_k) and the centre itself (FP64)
+  float* xf;
+  float* bf;
+  float* lf;
+  float* cm;
+  double* cen;
 };
+// Shared-memory bytes of the column stage: the FP64 columns, plus the FP32
+// screen copies and their magnitude maxima when `fast`.
+__host__ __device__ inline size_t cols64_bytes(int N, int d, bool fast) {
+  const size_t ld = col_ld(N);
+  return sizeof(double) * ld * (d + 2) + (fast ? ld * ((d == 1 ? 4 : 16) + 8) + 64 : 0);
+}
 
 // Column base of the stitch-row factory at cut c (per model class).
 template <int MC, int D>
@@ -162,12 +177,13 @@ __device__ inline void row_mean(const DevModel& M, const TimeConst& tc, int c, c
 }
 
 // One table entry (fill_row of make_pair_source, smoother.cpp:153-161).
-template <int MC, int D>
-__device__ inline double fill64(const DevModel& M, const TimeConst& tc,
-                                double coef, const double* mu, const Col64& C,
-                                int j, double sl, bool has_l) {
+// MODE selects the leaf-weight terms: 0 none, 1 the left leaf's own weight
+// (v + sl), 2 both leaves' weights ((v + sl) + lwr_j) — the three cases of
+// fill64, hoisted out of the entry loops of pass 1.
+template <int MC, int D, int MODE>
+__device__ __forceinline__ double fill64m(double coef, const double* mu, const Col64& C, int cp,
+                                          double sl) {
   double v;
-  const int cp = cpad(j);
   if (MC == kLGN) {  // d chained gaussian_row passes (ref_models lgssm_nd)
     v = C.base[cp];
 #pragma unroll
@@ -179,9 +195,45 @@ __device__ inline double fill64(const DevModel& M, const TimeConst& tc,
     const double t = DSUB(C.x[cp], mu[0]);
     v = __fma_rn(coef, DMUL(t, t), C.base[cp]);
   }
-  if (C.lwr) v = DADD(DADD(v, sl), C.lwr[cp]);
-  else if (has_l && sl != 0.0) v = DADD(v, sl);
+  if (MODE == 2) v = DADD(DADD(v, sl), C.lwr[cp]);
+  else if (MODE == 1) v = DADD(v, sl);
   return v;
+}
+template <int MC, int D>
+__device__ inline double fill64(const DevModel& M, const TimeConst& tc,
+                                double coef, const double* mu, const Col64& C,
+                                int j, double sl, bool has_l) {
+  const int cp = cpad(j);
+  if (C.lwr) return fill64m<MC, D, 2>(coef, mu, C, cp, sl);
+  if (has_l && sl != 0.0) return fill64m<MC, D, 1>(coef, mu, C, cp, sl);
+  return fill64m<MC, D, 0>(coef, mu, C, cp, sl);
+}
+
+// FP32 estimate of fill64m from the screen copies (|error| <= E, c64_row):
+// base - 0.5 sum_k t_k^2 (coef t^2 for the d = 1 model classes).
+template <int MC, int D, int MODE>
+__device__ __forceinline__ float fill32_est(const float* muf, float coeff, const Col64& C,
+                                            int cp) {
+  float q;
+  if (MC == kLGN && D > 1) {
+    const float4 x = reinterpret_cast<const float4*>(C.xf)[cp];
+    const float t0 = x.x - muf[0], t1 = x.y - muf[1];
+    q = fmaf(t1, t1, t0 * t0);
+    if (D > 2) {
+      const float t2 = x.z - muf[2];
+      q = fmaf(t2, t2, q);
+    }
+    if (D > 3) {
+      const float t3 = x.w - muf[3];
+      q = fmaf(t3, t3, q);
+    }
+  } else {
+    const float t = C.xf[cp] - muf[0];
+    q = t * t;
+  }
+  float a = fmaf(MC == kLGN ? -0.5f : coeff, q, C.bf[cp]);
+  if (MODE == 2) a += C.lf[cp];
+  return a;
 }
 
 template <int MC>
@@ -195,10 +247,15 @@ __device__ inline double row_coef(const DevModel& M, int c) {
 }
 
 // Stage the combine's right boundary slab + column bases in shared memory.
+__device__ __forceinline__ float finite_abs(double v) {
+  const float a = fabsf((float)v);
+  return a < CUDART_INF_F ? a : 0.f;
+}
 template <int MC, int D>
 __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
                            const Side& R, const DevModel& M,
-                           const TimeConst& tc, double* smem, Col64& C) {
+                           const TimeConst& tc, double* smem, Col64& C,
+                           bool fast = false) {
   const int N = b.N;
   constexpr int d = D;
   C.ld = col_ld(N);
@@ -206,7 +263,47 @@ __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
   C.base = smem + (size_t)C.ld * d;
   const bool nonuni = R.leaf && !b.UNI[(size_t)ch * b.K + R.t];
   C.lwr = nonuni ? C.base + C.ld : nullptr;
+  C.xf = C.bf = C.lf = C.cm = nullptr;
+  C.cen = nullptr;
+  float mb = 0.f, ml = 0.f, mxk[4] = {0.f, 0.f, 0.f, 0.f};
   const double* X = b.X64 + ((size_t)ch * b.K + R.t) * N * d;
+  // the fill's column coordinates: whitened w = W_Q x (LGSSM d > 1) or x
+  auto coords = [&](int j, double* z) {
+    const uint32_t p = map_first(b, la, ch, R, j);
+    double x[D];
+#pragma unroll
+    for (int k = 0; k < d; ++k) x[k] = X[(size_t)p * d + k];
+    if (MC == kLGN) {
+#pragma unroll
+      for (int k = 0; k < d; ++k) {
+        double v = 0.0;
+#pragma unroll
+        for (int l = 0; l <= k; ++l) v = DADD(v, DMUL(tc.tW[k * d + l], x[l]));
+        z[k] = v;
+      }
+    } else {
+      z[0] = x[0];
+    }
+  };
+  if (fast) {
+    double cen[D];
+    C.xf = reinterpret_cast<float*>(smem + (size_t)C.ld * (d + 2));
+    C.bf = C.xf + (size_t)C.ld * (d == 1 ? 1 : 4);
+    C.lf = C.bf + C.ld;
+    C.cm = C.lf + C.ld;
+    C.cen = reinterpret_cast<double*>(C.cm + 8);
+    // centre the FP32 copies on column 0 (the fill's coordinates drift with
+    // time, e.g. positions of the constant-velocity model; centred, the
+    // screen's rounding scales with the particle spread, not the position)
+    coords(0, cen);
+#pragma unroll
+    for (int k = 0; k < d; ++k) cen[k] = isfinite(cen[k]) ? cen[k] : 0.0;
+    if (threadIdx.x < 8) C.cm[threadIdx.x] = 0.f;
+#pragma unroll
+    for (int k = 0; k < d; ++k)
+      if (threadIdx.x == k) C.cen[k] = cen[k];
+    __syncthreads();
+  }
   for (int j = threadIdx.x; j < N; j += blockDim.x) {
     const uint32_t p = map_first(b, la, ch, R, j);
     double x[D];
@@ -226,6 +323,44 @@ __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
       C.x[cp] = x[0];
     }
     if (nonuni) C.lwr[cp] = b.LW64[((size_t)ch * b.K + R.t) * N + p];
+    if (fast) {
+      const double bs = C.base[cp];
+      C.bf[cp] = (float)bs;
+      mb = fmaxf(mb, finite_abs(bs));
+      const double lw = nonuni ? C.lwr[cp] : 0.0;
+      C.lf[cp] = (float)lw;
+      ml = fmaxf(ml, finite_abs(lw));
+      if (d == 1) {
+        const double xc = DSUB(C.x[cp], C.cen[0]);
+        C.xf[cp] = (float)xc;
+        mxk[0] = fmaxf(mxk[0], finite_abs(xc));
+      } else {
+        float xs[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int k = 0; k < d && k < 4; ++k) {
+          const double xc = DSUB(C.x[k * C.ld + cp], C.cen[k]);
+          xs[k] = (float)xc;
+          mxk[k] = fmaxf(mxk[k], finite_abs(xc));
+        }
+        reinterpret_cast<float4*>(C.xf)[cp] = make_float4(xs[0], xs[1], xs[2], xs[3]);
+      }
+    }
+  }
+  if (fast) {  // block maxima of the finite magnitudes (non-negative: int order)
+    const int lane = threadIdx.x & 31;
+    for (int o = 16; o; o >>= 1) {
+      mb = fmaxf(mb, __shfl_xor_sync(~0u, mb, o));
+      ml = fmaxf(ml, __shfl_xor_sync(~0u, ml, o));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mxk[k] = fmaxf(mxk[k], __shfl_xor_sync(~0u, mxk[k], o));
+    }
+    if (lane == 0) {
+      int* cmi = reinterpret_cast<int*>(C.cm);
+      atomicMax(cmi + 0, __float_as_int(mb));
+      atomicMax(cmi + 1, __float_as_int(ml));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) atomicMax(cmi + 2 + k, __float_as_int(mxk[k]));
+    }
   }
   __syncthreads();
 }
@@ -234,40 +369,88 @@ __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
 // contract per sub-block, sequential tail) and the raw row total
 // (sequential over sub-blocks) — exp_row_store (kernels.cpp:93-116).
 // ws layout per combine: m[N] raw[N] scale[N] total[N] prefix[N] sub[N*nsub]
-template <int MC, int D>
-__global__ void __launch_bounds__(256, 4) c64_rows(Bufs b, LevelArgs la) {
-  extern __shared__ double smem[];
-  const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
+//
+// Row max (fast = 1): an FP32 screen first. Every entry's FP32 estimate a_j
+// (fill32_est) is within E of the FP64 fill, E = 2^-18 (max|base| + |sl| +
+// max|lwr| + sum_k (max|x_k - c_k| + |mu_k - c_k|)^2), c = column 0's
+// coordinates (the FP32 copies are centred on it; the centring subtractions
+// are FP64, their rounding ~2^-53 |x| is far below E) — 8x the worst-case rounding of the
+// estimate's d + 2 FP32 operations on operands of those magnitudes (|coef|
+// scales the square for d = 1 models). Only entries with a_j >= max a - 3E
+// can hold the FP64 maximum; they are evaluated in FP64 (usually one per
+// row), so the row max is the same double as the full FP64 scan's at a
+// fraction of its instructions. Rows whose screen saw a NaN / +inf estimate,
+// or only -inf, run the full FP64 scan (with the NaN check). The sum pass
+// then evaluates every entry in FP64 exactly as before (exp_w_le0 = exp_w
+// on its domain x <= 0).
+template <int MC, int D, int MODE>
+__device__ __forceinline__ void c64_row(const Bufs& b, const LevelArgs& la, const Col64& C,
+                                        const double* mu, double coef, double sl, int i, int c,
+                                        bool fast, double* wm, double* wraw, double* wsub) {
   const int N = b.N, nsub = (N + kSub - 1) / kSub;
-  constexpr int d = D;
-  Side L, R;
-  CombineGeom g;
-  sides(b, la, k, L, R, g);
-  const DevModel& M = b.models[ch];
-  const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + g.c];
-  Col64 C;
-  stage_cols<MC, D>(b, la, ch, R, M, tc, smem, C);
-  // per (chain, combine of the chunk) workspace
-  double* ws = la.ws + ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * la.ws_comb;
-  double *wm = ws, *wraw = ws + N, *wsub = ws + 5 * (size_t)N;
-  const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
-  const double coef = row_coef<MC>(M, b.t0 + g.c);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rows_per_cta = 32;
-  const double* XL = b.X64 + ((size_t)ch * b.K + L.t) * N * d;
-  for (int r = warp; r < rows_per_cta; r += 8) {
-    const int i = blockIdx.x * rows_per_cta + r;
-    if (i >= N) break;
-    const uint32_t p = map_last(b, la, ch, L, i);
-    double xl[D], mu[D];
-    for (int q = 0; q < d; ++q) xl[q] = XL[(size_t)p * d + q];
-    row_mean<MC, D>(M, tc, b.t0 + g.c, xl, mu);
-    const double sl = lnonuni ? b.LW64[((size_t)ch * b.K + L.t) * N + i] : 0.0;
-    // max (reduce_max, kernels.cpp:26-36)
-    double mx = -CUDART_INF;
+  const int lane = threadIdx.x & 31;
+  double mx = -CUDART_INF;
+  bool full = !fast;
+  if (fast) {
+    float muf[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < D && k < 4; ++k) muf[k] = (float)DSUB(mu[k], C.cen[k]);
+    const float coeff = (float)coef;
+    float es = C.cm[0] + fabsf((float)sl) + (MODE == 2 ? C.cm[1] : 0.f);
+    if (MC == kLGN) {
+#pragma unroll
+      for (int k = 0; k < D && k < 4; ++k) {
+        const float s = C.cm[2 + k] + fabsf(muf[k]);
+        es += s * s;
+      }
+    } else {
+      const float s = C.cm[2] + fabsf(muf[0]);
+      es += fabsf(coeff) * s * s;
+    }
+    const float E = es * 0x1p-18f;
+    float b1 = -CUDART_INF_F, b2 = -CUDART_INF_F;
+    int i1 = 0;
+    bool bad = false;
+    auto screen = [&](float a, int j) {
+      bad |= (a != a) | (a == CUDART_INF_F);  // NaN or +inf
+      const bool up = a > b1;
+      b2 = fmaxf(b2, fminf(a, b1));
+      i1 = up ? j : i1;
+      b1 = fmaxf(b1, a);
+    };
+    const int nfull = N / kSub;
+    for (int s = 0; s < nfull; ++s) {  // two columns per lane and sub-block
+      const int cp = 72 * s + lane;
+      const float a0 = fill32_est<MC, D, MODE>(muf, coeff, C, cp);
+      const float a1 = fill32_est<MC, D, MODE>(muf, coeff, C, cp + 32);
+      screen(a0, kSub * s + lane);
+      screen(a1, kSub * s + 32 + lane);
+    }
+    for (int j = nfull * kSub + lane; j < N; j += 32)
+      screen(fill32_est<MC, D, MODE>(muf, coeff, C, cpad(j)), j);
+    float M = b1;
+    for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(~0u, M, o));
+    bad = __any_sync(~0u, bad) || M == -CUDART_INF_F || !(E < CUDART_INF_F);
+    if (bad) {
+      full = true;
+    } else {
+      const float thr = M - 3.f * E;
+      double e = -CUDART_INF;
+      if (b2 >= thr) {  // several candidates on this lane (near-ties): rescan
+        for (int j = lane; j < N; j += 32)
+          if (fill32_est<MC, D, MODE>(muf, coeff, C, cpad(j)) >= thr)
+            e = fmax(e, fill64m<MC, D, MODE>(coef, mu, C, cpad(j), sl));
+      } else if (b1 >= thr) {
+        e = fill64m<MC, D, MODE>(coef, mu, C, cpad(i1), sl);
+      }
+      for (int o = 16; o; o >>= 1) e = fmax(e, __shfl_xor_sync(~0u, e, o));
+      mx = e;
+    }
+  }
+  if (full) {  // max (reduce_max, kernels.cpp:26-36)
     int nan = 0;
     for (int j = lane; j < N; j += 32) {
-      const double v = fill64<MC, D>(M, tc, coef, mu, C, j, sl, lnonuni);
+      const double v = fill64m<MC, D, MODE>(coef, mu, C, cpad(j), sl);
       nan |= isnan(v);
       mx = fmax(mx, v);
     }
@@ -276,43 +459,89 @@ __global__ void __launch_bounds__(256, 4) c64_rows(Bufs b, LevelArgs la) {
       nan |= __shfl_xor_sync(~0u, nan, o);
     }
     if (nan) {
-      if (lane == 0) raise_err(b.err, DSMC_E_DOMAIN, g.c, la.level, kReasonNaN);
+      if (lane == 0) raise_err(b.err, DSMC_E_DOMAIN, c, la.level, kReasonNaN);
       mx = -CUDART_INF;
     }
-    if (lane == 0) wm[i] = mx;
-    double* srow = wsub + (size_t)i * nsub;
-    if (mx == -CUDART_INF) {  // dead row: zero total, never selected
-      for (int s = lane; s < nsub; s += 32) srow[s] = 0.0;
-      if (lane == 0) wraw[i] = 0.0;
-      continue;
+  }
+  if (lane == 0) wm[i] = mx;
+  double* srow = wsub + (size_t)i * nsub;
+  if (mx == -CUDART_INF) {  // dead row: zero total, never selected
+    for (int s = lane; s < nsub; s += 32) srow[s] = 0.0;
+    if (lane == 0) wraw[i] = 0.0;
+    return;
+  }
+  const int grp = lane >> 3, l8 = lane & 7;
+  for (int s0 = 0; s0 < nsub; s0 += 4) {
+    const int s = s0 + grp;
+    const bool act = s < nsub;
+    const int j0 = s * kSub;
+    const int len = act ? min(kSub, N - j0) : 0;
+    const int len8 = len & ~7;
+    const int cp0 = s * 72 + l8;  // cpad(j0 + l8)
+    double acc = 0.0;
+    if (len8 == kSub) {
+#pragma unroll
+      for (int q = 0; q < kSub; q += 8)
+        acc = DADD(acc, exp_w_le0(DSUB(fill64m<MC, D, MODE>(coef, mu, C, cp0 + q, sl), mx)));
+    } else {
+      for (int q = 0; q < len8; q += 8)
+        acc = DADD(acc, exp_w_le0(DSUB(fill64m<MC, D, MODE>(coef, mu, C, cp0 + q, sl), mx)));
     }
-    const int grp = lane >> 3, l8 = lane & 7;
-    for (int s0 = 0; s0 < nsub; s0 += 4) {
-      const int s = s0 + grp;
-      const bool act = s < nsub;
-      const int j0 = s * kSub;
-      const int len = act ? min(kSub, N - j0) : 0;
-      const int len8 = len & ~7;
-      double acc = 0.0;
-      for (int q = 0; q < len8; q += 8) {
-        const int j = j0 + q + l8;
-        acc = DADD(acc, exp_w(DSUB(fill64<MC, D>(M, tc, coef, mu, C, j, sl, lnonuni), mx)));
-      }
-      double a8[8];
-      for (int l = 0; l < 8; ++l) a8[l] = __shfl_sync(~0u, acc, (lane & ~7) + l);
-      if (act && l8 == 0) {
-        double bs = combine8(a8);
-        for (int j = j0 + len8; j < j0 + len; ++j)
-          bs = DADD(bs, exp_w(DSUB(fill64<MC, D>(M, tc, coef, mu, C, j, sl, lnonuni), mx)));
-        srow[s] = bs;
-      }
+    double a8[8];
+#pragma unroll
+    for (int l = 0; l < 8; ++l) a8[l] = __shfl_sync(~0u, acc, (lane & ~7) + l);
+    if (act && l8 == 0) {
+      double bs = combine8(a8);
+      for (int j = j0 + len8; j < j0 + len; ++j)
+        bs = DADD(bs, exp_w_le0(DSUB(fill64m<MC, D, MODE>(coef, mu, C, cpad(j), sl), mx)));
+      srow[s] = bs;
     }
-    __syncwarp();
-    if (lane == 0) {
-      double tot = 0.0;
-      for (int s = 0; s < nsub; ++s) tot = DADD(tot, srow[s]);
-      wraw[i] = tot;
-    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double tot = 0.0;
+    for (int s = 0; s < nsub; ++s) tot = DADD(tot, srow[s]);
+    wraw[i] = tot;
+  }
+}
+
+constexpr int kC64Threads = 512;   // 16 warps, one row at a time each
+constexpr int kC64Rows = 64;       // rows per CTA (the column stage is shared)
+template <int MC, int D>
+__global__ void __launch_bounds__(kC64Threads, 2) c64_rows(Bufs b, LevelArgs la, int fast) {
+  extern __shared__ double smem[];
+  const int k = la.k0 + blockIdx.y, ch = blockIdx.z;
+  const int N = b.N;
+  constexpr int d = D;
+  Side L, R;
+  CombineGeom g;
+  sides(b, la, k, L, R, g);
+  const DevModel& M = b.models[ch];
+  const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + g.c];
+  Col64 C;
+  stage_cols<MC, D>(b, la, ch, R, M, tc, smem, C, fast != 0);
+  // per (chain, combine of the chunk) workspace
+  double* ws = la.ws + ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * la.ws_comb;
+  double *wm = ws, *wraw = ws + N, *wsub = ws + 5 * (size_t)N;
+  const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
+  const double coef = row_coef<MC>(M, b.t0 + g.c);
+  const int warp = threadIdx.x >> 5;
+  const double* XL = b.X64 + ((size_t)ch * b.K + L.t) * N * d;
+  for (int r = warp; r < kC64Rows; r += kC64Threads / 32) {
+    const int i = blockIdx.x * kC64Rows + r;
+    if (i >= N) break;
+    const uint32_t p = map_last(b, la, ch, L, i);
+    double xl[D], mu[D];
+    for (int q = 0; q < d; ++q) xl[q] = XL[(size_t)p * d + q];
+    row_mean<MC, D>(M, tc, b.t0 + g.c, xl, mu);
+    const double sl = lnonuni ? b.LW64[((size_t)ch * b.K + L.t) * N + i] : 0.0;
+    // the leaf-weight case of fill64 (uniform over the row)
+    if (C.lwr)
+      c64_row<MC, D, 2>(b, la, C, mu, coef, sl, i, g.c, fast != 0, wm, wraw, wsub);
+    else if (lnonuni && sl != 0.0)
+      c64_row<MC, D, 1>(b, la, C, mu, coef, sl, i, g.c, fast != 0, wm, wraw, wsub);
+    else
+      c64_row<MC, D, 0>(b, la, C, mu, coef, sl, i, g.c, fast != 0, wm, wraw, wsub);
   }
 }
 
@@ -358,7 +587,7 @@ __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
     return;
   }
   for (int i = tid; i < N; i += blockDim.x) {
-    const double sc = exp_w(DSUB(wm[i], gmax));
+    const double sc = exp_w_le0(DSUB(wm[i], gmax));  // wm[i] <= gmax
     wscale[i] = sc;
     wtot[i] = DMUL(sc, wraw[i]);
   }
@@ -437,7 +666,7 @@ __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
     double c3 = c2b;
     int j = j0;
     for (; j < j1; ++j) {
-      c3 = DADD(c3, exp_w(DSUB(fill64<MC, D>(M, tc, coef, mu, C, j, sl, lnonuni), mrow)));
+      c3 = DADD(c3, exp_w_le0(DSUB(fill64<MC, D>(M, tc, coef, mu, C, j, sl, lnonuni), mrow)));
       if (local < c3) break;
     }
     if (j == j1) {  // spill: clamp to the last positive entry

@@ -216,6 +216,26 @@ __device__ __forceinline__ double exp_w(double x) {
   const double v = __dmul_rn(p, scale);
   return nan ? x : (low ? 0.0 : v);
 }
+// exp_w on its pass-1 domain: x = v - (row max) <= 0 or -inf, never NaN (a
+// NaN row is reported and skipped before its sum pass). Same operations and
+// results as exp_w there, without the NaN and overflow selects.
+__device__ __forceinline__ double exp_w_le0(double x) {
+  const bool low = x <= -708.0;
+  const double xc = low ? 0.0 : x;
+  const double k = rint(__dmul_rn(xc, kExpW[0]));
+  double r = __fma_rn(k, kExpW[1], xc);
+  r = __fma_rn(k, kExpW[2], r);
+  double p = kExpW[3];
+#pragma unroll
+  for (int q = 4; q < 16; ++q) p = __fma_rn(p, r, kExpW[q]);
+  p = __fma_rn(p, r, kExpW[15]);
+  const long long ki = static_cast<long long>(k);
+  const double scale =
+      __longlong_as_double(static_cast<long long>(
+          static_cast<unsigned long long>(ki + 1023) << 52));
+  const double v = __dmul_rn(p, scale);
+  return low ? 0.0 : v;
+}
 
 // b[l] = a[l] + a[l+4]; (b0 + b2) + (b1 + b3).
 __device__ __forceinline__ double combine8(const double a[8]) {

@@ -629,19 +629,25 @@ struct RunResult {
   double* LW64 = nullptr;
 };
 
-size_t smem_cols64(int N, int d) { return sizeof(double) * (size_t)col_ld(N) * (d + 2); }
-
 template <int MC, int D>
 int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
                int systematic) {
-  const size_t sm = smem_cols64(b.N, D);
-  if (sm > (size_t)ctx->smem_optin - 1024)
+  const size_t lim = (size_t)ctx->smem_optin - 1024;
+  const size_t sm = cols64_bytes(b.N, D, false);
+  if (sm > lim)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
                    "FP64 parity combine: N * (d + 2) doubles exceed the shared-memory "
                    "column stage (N <= " +
                        std::to_string((ctx->smem_optin - 1024) / (8 * (D + 2)) / 72 * 64) +
                        " at this d); use the FP32 path or a lazy resampler");
-  c64_rows<MC, D><<<dim3((b.N + 31) / 32, nk, b.B), 256, sm, ctx->stream>>>(b, la);
+  // pass 1 screens each row's max in FP32 when the screen copies fit too
+  // (DSMC_C64_SCREEN=0 forces the full FP64 max scan)
+  const bool screen_env =
+      !(getenv("DSMC_C64_SCREEN") && atoi(getenv("DSMC_C64_SCREEN")) == 0);
+  const size_t smf = cols64_bytes(b.N, D, true);
+  const int fast = screen_env && smf <= lim;
+  c64_rows<MC, D><<<dim3((b.N + kC64Rows - 1) / kC64Rows, nk, b.B), kC64Threads,
+                    fast ? smf : sm, ctx->stream>>>(b, la, fast);
   LAUNCHED(ctx);
   c64_sample<MC, D><<<dim3(nk, 1, b.B), 256, sm, ctx->stream>>>(b, la, systematic);
   LAUNCHED(ctx);
