@@ -73,35 +73,41 @@ __device__ inline double block_lnc(const Bufs& b, const LevelArgs& la, int ch,
   return la.blnc_prev[(size_t)ch * b.cap + s.idx];
 }
 
-// Per-combine column data of the FP64 fill, staged in shared memory.
-// Column j lives at cpad(j): every 64-column sub-block takes 72 slots, so the
+// Per-combine column data of the FP64 fill, staged in shared memory as one
+// record per column: x_0..x_{d-1}, base, leaf weight (+ pad to 16 bytes), so
+// an entry is two or three 16-byte loads at immediate offsets. Column j's
+// record sits at cpad(j): every 64-column sub-block takes 72 records, so the
 // four 8-lane groups of a warp (four sub-blocks, pass 1's sub-block sums)
-// read disjoint bank halves instead of the same banks; states are stored
-// dimension-major (x[k * ld + cpad(j)]) so consecutive columns are
-// consecutive doubles. The layout only places values: the arithmetic and
-// its order are unchanged.
+// start at different banks. The layout only places values: the arithmetic
+// and its order are unchanged.
 __host__ __device__ inline int cpad(int j) { return j + (j >> 6) * 8; }
 __host__ __device__ inline int col_ld(int N) { return (N + 63) / 64 * 72; }
+__host__ __device__ constexpr int rec_len(int d) { return (d + 3) & ~1; }  // d + 2, even
 struct Col64 {
-  double* x;    // d * ld
-  double* base; // ld
-  double* lwr;  // ld or null
+  double* rec;  // ld records of rec_len(d) doubles
   int ld;
-  // FP32 copies for pass 1's row-max screen (c64_rows with fast = 1): the
-  // column states centred on column 0's (x - cen: float4 per column, d > 1;
-  // float, d = 1), bases and leaf weights, plus the largest finite magnitudes
-  // of each (cm: base, lwr, x_k - cen_k) and the centre itself (FP64)
-  float* xf;
-  float* bf;
-  float* lf;
+  int has_lwr;  // the right block is a non-uniform leaf (weights in the records)
+  // FP32 screen copies (c64_rows with fast = 1), in column PAIRS: pair
+  // p = 32 s + l holds columns 64 s + l and 64 s + 32 + l (sub-block s, lane
+  // l), so a lane screens both with packed FADD2 / FFMA2. States are centred
+  // on column 0's (x - cen) in two planes (first / second column of each pair:
+  // float4 for d > 1, float for d = 1), bases and leaf weights as float2 pairs; dead padding columns carry
+  // base -inf. cm: the largest finite |base|, |lwr|, |x_k - cen_k|, and
+  // (as an int) whether every column is clean (finite states, no NaN or +inf
+  // base / weight); cen: the centre (FP64).
+  float* xs;    // [2][npair] (first / second column of each pair)
+  int npair;
+  float2* bf2;
+  float2* lf2;
   float* cm;
   double* cen;
 };
-// Shared-memory bytes of the column stage: the FP64 columns, plus the FP32
-// screen copies and their magnitude maxima when `fast`.
+// Shared-memory bytes of the column stage: the FP64 records, plus the FP32
+// screen pairs and their magnitude maxima when `fast`.
 __host__ __device__ inline size_t cols64_bytes(int N, int d, bool fast) {
-  const size_t ld = col_ld(N);
-  return sizeof(double) * ld * (d + 2) + (fast ? ld * ((d == 1 ? 4 : 16) + 8) + 64 : 0);
+  const size_t ld = col_ld(N), npair = (size_t)(N + 63) / 64 * 32;
+  return sizeof(double) * ld * rec_len(d) +
+         (fast ? npair * ((d == 1 ? 8 : 32) + 16) + 64 : 0);
 }
 
 // Column base of the stitch-row factory at cut c (per model class).
@@ -183,19 +189,28 @@ __device__ inline void row_mean(const DevModel& M, const TimeConst& tc, int c, c
 template <int MC, int D, int MODE>
 __device__ __forceinline__ double fill64m(double coef, const double* mu, const Col64& C, int cp,
                                           double sl) {
+  constexpr int RL = rec_len(D);
+  const double2* r = reinterpret_cast<const double2*>(C.rec) + (size_t)cp * (RL / 2);
+  double f[RL];
+#pragma unroll
+  for (int q = 0; q < RL / 2; ++q) {
+    const double2 v = r[q];
+    f[2 * q] = v.x;
+    f[2 * q + 1] = v.y;
+  }
   double v;
   if (MC == kLGN) {  // d chained gaussian_row passes (ref_models lgssm_nd)
-    v = C.base[cp];
+    v = f[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const double t = DSUB(C.x[k * C.ld + cp], mu[k]);
+      const double t = DSUB(f[k], mu[k]);
       v = __fma_rn(-0.5, DMUL(t, t), v);
     }
   } else {
-    const double t = DSUB(C.x[cp], mu[0]);
-    v = __fma_rn(coef, DMUL(t, t), C.base[cp]);
+    const double t = DSUB(f[0], mu[0]);
+    v = __fma_rn(coef, DMUL(t, t), f[D]);
   }
-  if (MODE == 2) v = DADD(DADD(v, sl), C.lwr[cp]);
+  if (MODE == 2) v = DADD(DADD(v, sl), f[D + 1]);
   else if (MODE == 1) v = DADD(v, sl);
   return v;
 }
@@ -204,35 +219,37 @@ __device__ inline double fill64(const DevModel& M, const TimeConst& tc,
                                 double coef, const double* mu, const Col64& C,
                                 int j, double sl, bool has_l) {
   const int cp = cpad(j);
-  if (C.lwr) return fill64m<MC, D, 2>(coef, mu, C, cp, sl);
+  if (C.has_lwr) return fill64m<MC, D, 2>(coef, mu, C, cp, sl);
   if (has_l && sl != 0.0) return fill64m<MC, D, 1>(coef, mu, C, cp, sl);
   return fill64m<MC, D, 0>(coef, mu, C, cp, sl);
 }
 
-// FP32 estimate of fill64m from the screen copies (|error| <= E, c64_row):
-// base - 0.5 sum_k t_k^2 (coef t^2 for the d = 1 model classes).
+// FP32 estimates of fill64m for screen pair p (|error| <= E, c64_row):
+// base - 0.5 sum_k t_k^2 (coef t^2 for the d = 1 model classes), both
+// columns of the pair in packed FADD2 / FFMA2; nmu = -(mu - cen) per dim.
 template <int MC, int D, int MODE>
-__device__ __forceinline__ float fill32_est(const float* muf, float coeff, const Col64& C,
-                                            int cp) {
-  float q;
+__device__ __forceinline__ float2 est32_pair(const float2* nmu, float2 cf, const Col64& C, int p) {
+  float2 q;
   if (MC == kLGN && D > 1) {
-    const float4 x = reinterpret_cast<const float4*>(C.xf)[cp];
-    const float t0 = x.x - muf[0], t1 = x.y - muf[1];
-    q = fmaf(t1, t1, t0 * t0);
+    const float4 xa = reinterpret_cast<const float4*>(C.xs)[p];
+    const float4 xb = reinterpret_cast<const float4*>(C.xs)[C.npair + p];
+    const float2 t0 = __fadd2_rn(make_float2(xa.x, xb.x), nmu[0]);
+    const float2 t1 = __fadd2_rn(make_float2(xa.y, xb.y), nmu[1]);
+    q = __ffma2_rn(t1, t1, __fmul2_rn(t0, t0));
     if (D > 2) {
-      const float t2 = x.z - muf[2];
-      q = fmaf(t2, t2, q);
+      const float2 t2 = __fadd2_rn(make_float2(xa.z, xb.z), nmu[2]);
+      q = __ffma2_rn(t2, t2, q);
     }
     if (D > 3) {
-      const float t3 = x.w - muf[3];
-      q = fmaf(t3, t3, q);
+      const float2 t3 = __fadd2_rn(make_float2(xa.w, xb.w), nmu[3]);
+      q = __ffma2_rn(t3, t3, q);
     }
   } else {
-    const float t = C.xf[cp] - muf[0];
-    q = t * t;
+    const float2 t = __fadd2_rn(make_float2(C.xs[p], C.xs[C.npair + p]), nmu[0]);
+    q = __fmul2_rn(t, t);
   }
-  float a = fmaf(MC == kLGN ? -0.5f : coeff, q, C.bf[cp]);
-  if (MODE == 2) a += C.lf[cp];
+  float2 a = __ffma2_rn(cf, q, C.bf2[p]);
+  if (MODE == 2) a = __fadd2_rn(a, C.lf2[p]);
   return a;
 }
 
@@ -257,22 +274,18 @@ __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
                            const TimeConst& tc, double* smem, Col64& C,
                            bool fast = false) {
   const int N = b.N;
-  constexpr int d = D;
+  constexpr int d = D, RL = rec_len(D);
   C.ld = col_ld(N);
-  C.x = smem;
-  C.base = smem + (size_t)C.ld * d;
+  C.rec = smem;
   const bool nonuni = R.leaf && !b.UNI[(size_t)ch * b.K + R.t];
-  C.lwr = nonuni ? C.base + C.ld : nullptr;
-  C.xf = C.bf = C.lf = C.cm = nullptr;
+  C.has_lwr = nonuni;
+  C.xs = nullptr;
+  C.bf2 = C.lf2 = nullptr;
+  C.cm = nullptr;
   C.cen = nullptr;
-  float mb = 0.f, ml = 0.f, mxk[4] = {0.f, 0.f, 0.f, 0.f};
   const double* X = b.X64 + ((size_t)ch * b.K + R.t) * N * d;
   // the fill's column coordinates: whitened w = W_Q x (LGSSM d > 1) or x
-  auto coords = [&](int j, double* z) {
-    const uint32_t p = map_first(b, la, ch, R, j);
-    double x[D];
-#pragma unroll
-    for (int k = 0; k < d; ++k) x[k] = X[(size_t)p * d + k];
+  auto coords = [&](const double* x, double* z) {
     if (MC == kLGN) {
 #pragma unroll
       for (int k = 0; k < d; ++k) {
@@ -285,65 +298,71 @@ __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
       z[0] = x[0];
     }
   };
+  const int nsub = (N + kSub - 1) / kSub, npair = nsub * 32;
   if (fast) {
-    double cen[D];
-    C.xf = reinterpret_cast<float*>(smem + (size_t)C.ld * (d + 2));
-    C.bf = C.xf + (size_t)C.ld * (d == 1 ? 1 : 4);
-    C.lf = C.bf + C.ld;
-    C.cm = C.lf + C.ld;
+    C.xs = reinterpret_cast<float*>(smem + (size_t)C.ld * RL);
+    C.npair = npair;
+    C.bf2 = reinterpret_cast<float2*>(C.xs + (size_t)npair * (d == 1 ? 2 : 8));
+    C.lf2 = C.bf2 + npair;
+    C.cm = reinterpret_cast<float*>(C.lf2 + npair);
     C.cen = reinterpret_cast<double*>(C.cm + 8);
     // centre the FP32 copies on column 0 (the fill's coordinates drift with
     // time, e.g. positions of the constant-velocity model; centred, the
     // screen's rounding scales with the particle spread, not the position)
-    coords(0, cen);
+    double x0[D], cen[D];
+    const uint32_t p0 = map_first(b, la, ch, R, 0);
 #pragma unroll
-    for (int k = 0; k < d; ++k) cen[k] = isfinite(cen[k]) ? cen[k] : 0.0;
-    if (threadIdx.x < 8) C.cm[threadIdx.x] = 0.f;
+    for (int k = 0; k < d; ++k) x0[k] = X[(size_t)p0 * d + k];
+    coords(x0, cen);
+    if (threadIdx.x < 8) C.cm[threadIdx.x] = threadIdx.x == 6 ? __int_as_float(1) : 0.f;
 #pragma unroll
     for (int k = 0; k < d; ++k)
-      if (threadIdx.x == k) C.cen[k] = cen[k];
+      if (threadIdx.x == k) C.cen[k] = isfinite(cen[k]) ? cen[k] : 0.0;
     __syncthreads();
   }
-  for (int j = threadIdx.x; j < N; j += blockDim.x) {
-    const uint32_t p = map_first(b, la, ch, R, j);
-    double x[D];
+  float mb = 0.f, ml = 0.f, mxk[4] = {0.f, 0.f, 0.f, 0.f};
+  int clean = 1;
+  const int jend = fast ? nsub * kSub : N;  // the screen also fills the padding columns
+  for (int j = threadIdx.x; j < jend; j += blockDim.x) {
+    double z[D], bs = -CUDART_INF, lw = 0.0;
+    const bool live = j < N;
+    if (live) {
+      const uint32_t p = map_first(b, la, ch, R, j);
+      double x[D];
 #pragma unroll
-    for (int k = 0; k < d; ++k) x[k] = X[(size_t)p * d + k];
-    const int cp = cpad(j);
-    C.base[cp] = col_base<MC, D>(M, tc, b.t0 + R.t, x);  // global time (windows)
-    if (MC == kLGN) {  // whitened column w = W_Q x
+      for (int k = 0; k < d; ++k) x[k] = X[(size_t)p * d + k];
+      bs = col_base<MC, D>(M, tc, b.t0 + R.t, x);  // global time (windows)
+      coords(x, z);
+      double* r = C.rec + (size_t)cpad(j) * RL;
 #pragma unroll
-      for (int k = 0; k < d; ++k) {
-        double z = 0.0;
-#pragma unroll
-        for (int l = 0; l <= k; ++l) z = DADD(z, DMUL(tc.tW[k * d + l], x[l]));
-        C.x[k * C.ld + cp] = z;
+      for (int k = 0; k < d; ++k) r[k] = z[k];
+      r[d] = bs;
+      if (nonuni) {
+        lw = b.LW64[((size_t)ch * b.K + R.t) * N + p];
+        r[d + 1] = lw;
       }
-    } else {
-      C.x[cp] = x[0];
     }
-    if (nonuni) C.lwr[cp] = b.LW64[((size_t)ch * b.K + R.t) * N + p];
     if (fast) {
-      const double bs = C.base[cp];
-      C.bf[cp] = (float)bs;
-      mb = fmaxf(mb, finite_abs(bs));
-      const double lw = nonuni ? C.lwr[cp] : 0.0;
-      C.lf[cp] = (float)lw;
-      ml = fmaxf(ml, finite_abs(lw));
-      if (d == 1) {
-        const double xc = DSUB(C.x[cp], C.cen[0]);
-        C.xf[cp] = (float)xc;
-        mxk[0] = fmaxf(mxk[0], finite_abs(xc));
-      } else {
-        float xs[4] = {0.f, 0.f, 0.f, 0.f};
+      const int pr = (j >> 6) * 32 + (j & 31), h = (j >> 5) & 1;  // screen pair, half
+      reinterpret_cast<float*>(C.bf2)[2 * pr + h] = (float)bs;
+      reinterpret_cast<float*>(C.lf2)[2 * pr + h] = (float)lw;
+      float xs[4] = {0.f, 0.f, 0.f, 0.f};
+      if (live) {
+        mb = fmaxf(mb, finite_abs(bs));
+        ml = fmaxf(ml, finite_abs(lw));
+        clean &= !isnan(bs) && bs != CUDART_INF && !isnan(lw) && lw != CUDART_INF;
 #pragma unroll
         for (int k = 0; k < d && k < 4; ++k) {
-          const double xc = DSUB(C.x[k * C.ld + cp], C.cen[k]);
+          const double xc = DSUB(z[k], C.cen[k]);
           xs[k] = (float)xc;
           mxk[k] = fmaxf(mxk[k], finite_abs(xc));
+          clean &= isfinite(z[k]) && isfinite(xs[k]);
         }
-        reinterpret_cast<float4*>(C.xf)[cp] = make_float4(xs[0], xs[1], xs[2], xs[3]);
       }
+      if (d == 1)
+        C.xs[h * npair + pr] = xs[0];
+      else
+        reinterpret_cast<float4*>(C.xs)[h * npair + pr] = make_float4(xs[0], xs[1], xs[2], xs[3]);
     }
   }
   if (fast) {  // block maxima of the finite magnitudes (non-negative: int order)
@@ -354,12 +373,14 @@ __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
 #pragma unroll
       for (int k = 0; k < 4; ++k) mxk[k] = fmaxf(mxk[k], __shfl_xor_sync(~0u, mxk[k], o));
     }
+    clean = __all_sync(~0u, clean);
     if (lane == 0) {
       int* cmi = reinterpret_cast<int*>(C.cm);
       atomicMax(cmi + 0, __float_as_int(mb));
       atomicMax(cmi + 1, __float_as_int(ml));
 #pragma unroll
       for (int k = 0; k < 4; ++k) atomicMax(cmi + 2 + k, __float_as_int(mxk[k]));
+      if (!clean) atomicAnd(cmi + 6, 0);
     }
   }
   __syncthreads();
@@ -371,18 +392,20 @@ __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
 // ws layout per combine: m[N] raw[N] scale[N] total[N] prefix[N] sub[N*nsub]
 //
 // Row max (fast = 1): an FP32 screen first. Every entry's FP32 estimate a_j
-// (fill32_est) is within E of the FP64 fill, E = 2^-18 (max|base| + |sl| +
+// (est32_pair) is within E of the FP64 fill, E = 2^-18 (max|base| + |sl| +
 // max|lwr| + sum_k (max|x_k - c_k| + |mu_k - c_k|)^2), c = column 0's
 // coordinates (the FP32 copies are centred on it; the centring subtractions
-// are FP64, their rounding ~2^-53 |x| is far below E) — 8x the worst-case rounding of the
-// estimate's d + 2 FP32 operations on operands of those magnitudes (|coef|
-// scales the square for d = 1 models). Only entries with a_j >= max a - 3E
-// can hold the FP64 maximum; they are evaluated in FP64 (usually one per
-// row), so the row max is the same double as the full FP64 scan's at a
-// fraction of its instructions. Rows whose screen saw a NaN / +inf estimate,
-// or only -inf, run the full FP64 scan (with the NaN check). The sum pass
-// then evaluates every entry in FP64 exactly as before (exp_w_le0 = exp_w
-// on its domain x <= 0).
+// are FP64, their rounding ~2^-53 |x| is far below E) — 8x the worst-case
+// rounding of the estimate's FP32 operations on operands of those magnitudes
+// (|coef| scales the square for the d = 1 model classes). Only entries with
+// a_j >= max a - 3E can hold the FP64 maximum; they are evaluated in FP64
+// (usually one per row), so the row max is the same double as the full FP64
+// scan's at a fraction of its instructions. The screen runs only when the
+// inputs are clean (finite states and row mean, finite left weight, no NaN
+// or +inf base / right weight): then no FP64 entry can be NaN, and no
+// estimate NaN or +inf. Other rows run the full FP64 scan with its NaN
+// check. The sum pass then evaluates every entry in FP64 exactly as before
+// (exp_w_le0 = exp_w on its domain x <= 0).
 template <int MC, int D, int MODE>
 __device__ __forceinline__ void c64_row(const Bufs& b, const LevelArgs& la, const Col64& C,
                                         const double* mu, double coef, double sl, int i, int c,
@@ -392,59 +415,67 @@ __device__ __forceinline__ void c64_row(const Bufs& b, const LevelArgs& la, cons
   double mx = -CUDART_INF;
   bool full = !fast;
   if (fast) {
-    float muf[4] = {0.f, 0.f, 0.f, 0.f};
+    bool clean = __float_as_int(C.cm[6]) != 0 && isfinite(sl);
+    float2 nmu[4];
 #pragma unroll
-    for (int k = 0; k < D && k < 4; ++k) muf[k] = (float)DSUB(mu[k], C.cen[k]);
+    for (int k = 0; k < 4; ++k) nmu[k] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < D && k < 4; ++k) {
+      const float m = (float)DSUB(mu[k], C.cen[k]);
+      clean &= isfinite(mu[k]) && isfinite(m);
+      nmu[k] = make_float2(-m, -m);
+    }
     const float coeff = (float)coef;
     float es = C.cm[0] + fabsf((float)sl) + (MODE == 2 ? C.cm[1] : 0.f);
     if (MC == kLGN) {
 #pragma unroll
       for (int k = 0; k < D && k < 4; ++k) {
-        const float s = C.cm[2 + k] + fabsf(muf[k]);
+        const float s = C.cm[2 + k] + fabsf(nmu[k].x);
         es += s * s;
       }
     } else {
-      const float s = C.cm[2] + fabsf(muf[0]);
+      const float s = C.cm[2] + fabsf(nmu[0].x);
       es += fabsf(coeff) * s * s;
     }
     const float E = es * 0x1p-18f;
-    float b1 = -CUDART_INF_F, b2 = -CUDART_INF_F;
-    int i1 = 0;
-    bool bad = false;
-    auto screen = [&](float a, int j) {
-      bad |= (a != a) | (a == CUDART_INF_F);  // NaN or +inf
-      const bool up = a > b1;
-      b2 = fmaxf(b2, fminf(a, b1));
-      i1 = up ? j : i1;
-      b1 = fmaxf(b1, a);
-    };
-    const int nfull = N / kSub;
-    for (int s = 0; s < nfull; ++s) {  // two columns per lane and sub-block
-      const int cp = 72 * s + lane;
-      const float a0 = fill32_est<MC, D, MODE>(muf, coeff, C, cp);
-      const float a1 = fill32_est<MC, D, MODE>(muf, coeff, C, cp + 32);
-      screen(a0, kSub * s + lane);
-      screen(a1, kSub * s + 32 + lane);
-    }
-    for (int j = nfull * kSub + lane; j < N; j += 32)
-      screen(fill32_est<MC, D, MODE>(muf, coeff, C, cpad(j)), j);
-    float M = b1;
-    for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(~0u, M, o));
-    bad = __any_sync(~0u, bad) || M == -CUDART_INF_F || !(E < CUDART_INF_F);
-    if (bad) {
+    const float cfv = MC == kLGN ? -0.5f : coeff;
+    const float2 cf = make_float2(cfv, cfv);
+    if (!clean || !(E < CUDART_INF_F)) {
       full = true;
     } else {
-      const float thr = M - 3.f * E;
-      double e = -CUDART_INF;
-      if (b2 >= thr) {  // several candidates on this lane (near-ties): rescan
-        for (int j = lane; j < N; j += 32)
-          if (fill32_est<MC, D, MODE>(muf, coeff, C, cpad(j)) >= thr)
-            e = fmax(e, fill64m<MC, D, MODE>(coef, mu, C, cpad(j), sl));
-      } else if (b1 >= thr) {
-        e = fill64m<MC, D, MODE>(coef, mu, C, cpad(i1), sl);
+      float b1 = -CUDART_INF_F, b2 = -CUDART_INF_F;
+      int i1 = 0;
+      auto upd = [&](float a, int j) {
+        const bool up = a > b1;
+        b2 = fmaxf(b2, fminf(a, b1));
+        i1 = up ? j : i1;
+        b1 = fmaxf(b1, a);
+      };
+      for (int s = 0; s < nsub; ++s) {  // pair 32 s + lane: columns 64 s + lane, + 32
+        const float2 a = est32_pair<MC, D, MODE>(nmu, cf, C, 32 * s + lane);
+        upd(a.x, kSub * s + lane);
+        upd(a.y, kSub * s + 32 + lane);
       }
-      for (int o = 16; o; o >>= 1) e = fmax(e, __shfl_xor_sync(~0u, e, o));
-      mx = e;
+      float M = b1;
+      for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(~0u, M, o));
+      if (M == -CUDART_INF_F) {
+        full = true;  // every estimate -inf: let the FP64 scan decide
+      } else {
+        const float thr = M - 3.f * E;
+        double e = -CUDART_INF;
+        if (b2 >= thr) {  // several candidates on this lane (near-ties): rescan
+          for (int s = 0; s < nsub; ++s) {
+            const float2 a = est32_pair<MC, D, MODE>(nmu, cf, C, 32 * s + lane);
+            if (a.x >= thr) e = fmax(e, fill64m<MC, D, MODE>(coef, mu, C, cpad(kSub * s + lane), sl));
+            if (a.y >= thr)
+              e = fmax(e, fill64m<MC, D, MODE>(coef, mu, C, cpad(kSub * s + 32 + lane), sl));
+          }
+        } else if (b1 >= thr) {
+          e = fill64m<MC, D, MODE>(coef, mu, C, cpad(i1), sl);
+        }
+        for (int o = 16; o; o >>= 1) e = fmax(e, __shfl_xor_sync(~0u, e, o));
+        mx = e;
+      }
     }
   }
   if (full) {  // max (reduce_max, kernels.cpp:26-36)
@@ -506,7 +537,7 @@ __device__ __forceinline__ void c64_row(const Bufs& b, const LevelArgs& la, cons
 }
 
 constexpr int kC64Threads = 512;   // 16 warps, one row at a time each
-constexpr int kC64Rows = 64;       // rows per CTA (the column stage is shared)
+constexpr int kC64Rows = 128;      // rows per CTA (the column stage is shared)
 template <int MC, int D>
 __global__ void __launch_bounds__(kC64Threads, 2) c64_rows(Bufs b, LevelArgs la, int fast) {
   extern __shared__ double smem[];
@@ -536,7 +567,7 @@ __global__ void __launch_bounds__(kC64Threads, 2) c64_rows(Bufs b, LevelArgs la,
     row_mean<MC, D>(M, tc, b.t0 + g.c, xl, mu);
     const double sl = lnonuni ? b.LW64[((size_t)ch * b.K + L.t) * N + i] : 0.0;
     // the leaf-weight case of fill64 (uniform over the row)
-    if (C.lwr)
+    if (C.has_lwr)
       c64_row<MC, D, 2>(b, la, C, mu, coef, sl, i, g.c, fast != 0, wm, wraw, wsub);
     else if (lnonuni && sl != 0.0)
       c64_row<MC, D, 1>(b, la, C, mu, coef, sl, i, g.c, fast != 0, wm, wraw, wsub);
@@ -545,18 +576,76 @@ __global__ void __launch_bounds__(kC64Threads, 2) c64_rows(Bufs b, LevelArgs la,
   }
 }
 
-// Pass 2: one CTA per combine. Cross-row combination (resampling.cpp:92-102),
-// per-slot inversion (Appendix A), ancestor maps, block log Z.
+// Cross-row combination of the pair table (resampling.cpp:92-102), one warp
+// per combine (any number of combines per CTA): g = max_i m_i, per-row scale
+// exp_w(m_i - g) and total scale_i raw_i, the grand total under the 8-lane
+// contract and the sequential inclusive prefix of the totals (the walk's
+// cum), log mean weight. The prefix is one dependent chain of N additions per
+// combine; running it here, one warp per combine with many combines in flight
+// per SM, keeps it off the sampler CTAs. ws extras: [5N + N nsub] = g,
+// [+1] = grand total.
+__global__ void __launch_bounds__(256) c64_cdf(Bufs b, LevelArgs la, int nk) {
+  const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= nk * b.B) return;
+  const int kk = w % nk, ch = w / nk;  // ws slot of (chain, combine) as c64_rows
+  const int k = la.k0 + kk;
+  const int N = b.N, nsub = (N + kSub - 1) / kSub;
+  double* ws = la.ws + (size_t)w * la.ws_comb;
+  double *wm = ws, *wraw = ws + N, *wscale = ws + 2 * (size_t)N, *wtot = ws + 3 * (size_t)N,
+         *wpre = ws + 4 * (size_t)N, *wx = ws + (size_t)N * (5 + nsub);
+  double mx = -CUDART_INF;
+  for (int i = lane; i < N; i += 32) mx = fmax(mx, wm[i]);
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(~0u, mx, o));
+  if (lane == 0) wx[0] = mx;
+  if (mx == -CUDART_INF) {
+    if (lane == 0) {
+      CombineGeom g = combine_geom(la.level, k, b.K);
+      raise_err(b.err, DSMC_E_RUNTIME, g.c, la.level, kReasonZeroTable);
+    }
+    return;
+  }
+  for (int i = lane; i < N; i += 32) {
+    const double sc = exp_w_le0(DSUB(wm[i], mx));  // wm[i] <= g
+    wscale[i] = sc;
+    wtot[i] = DMUL(sc, wraw[i]);
+  }
+  __syncwarp();
+  // grand = reduce_sum(row_total) (8-lane contract)
+  const int n8 = N & ~7;
+  double acc = 0.0;
+  if (lane < 8)
+    for (int i = lane; i < n8; i += 8) acc = DADD(acc, wtot[i]);
+  double a8[8];
+#pragma unroll
+  for (int l = 0; l < 8; ++l) a8[l] = __shfl_sync(~0u, acc, l);
+  if (lane == 0) {
+    double tot = combine8(a8);
+    for (int i = n8; i < N; ++i) tot = DADD(tot, wtot[i]);
+    wx[1] = tot;
+    double cum = 0.0;  // sequential inclusive prefix (the walk's cum)
+#pragma unroll 8
+    for (int i = 0; i < N; ++i) {
+      cum = DADD(cum, wtot[i]);
+      wpre[i] = cum;
+    }
+    b.LMW[(size_t)ch * b.T + la.cursor + k] = DADD(mx, log(tot));
+  }
+}
+
+// Pass 2: one CTA per combine: per-slot inversion over the prefix c64_cdf
+// left in ws (Appendix A), ancestor maps, block log Z.
 template <int MC, int D>
 __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
                                                   int systematic) {
   extern __shared__ double smem[];
-  __shared__ double red[32];
-  __shared__ double s_g, s_grand;
-  __shared__ double a8s[8];
   const int k = la.k0 + blockIdx.x, ch = blockIdx.z;
   const int N = b.N, nsub = (N + kSub - 1) / kSub;
   constexpr int d = D;
+  double* ws = la.ws + ((size_t)blockIdx.z * gridDim.x + blockIdx.x) * la.ws_comb;
+  double *wm = ws, *wscale = ws + 2 * (size_t)N, *wtot = ws + 3 * (size_t)N,
+         *wpre = ws + 4 * (size_t)N, *wsub = ws + 5 * (size_t)N;
+  const double* wx = ws + (size_t)N * (5 + nsub);
+  if (wx[0] == -CUDART_INF) return;  // zero table: c64_cdf raised the error
   Side L, R;
   CombineGeom g;
   sides(b, la, k, L, R, g);
@@ -564,57 +653,8 @@ __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
   const TimeConst& tc = b.tc[(size_t)ch * b.Kt + b.t0 + g.c];
   Col64 C;
   stage_cols<MC, D>(b, la, ch, R, M, tc, smem, C);
-  double* ws = la.ws + ((size_t)blockIdx.z * gridDim.x + blockIdx.x) * la.ws_comb;
-  double *wm = ws, *wraw = ws + N, *wscale = ws + 2 * (size_t)N,
-         *wtot = ws + 3 * (size_t)N, *wpre = ws + 4 * (size_t)N,
-         *wsub = ws + 5 * (size_t)N;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // g = max_i m_i
-  double mx = -CUDART_INF;
-  for (int i = tid; i < N; i += blockDim.x) mx = fmax(mx, wm[i]);
-  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(~0u, mx, o));
-  if (lane == 0) red[warp] = mx;
-  __syncthreads();
-  if (tid == 0) {
-    double v = -CUDART_INF;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
-    s_g = v;
-  }
-  __syncthreads();
-  const double gmax = s_g;
-  if (gmax == -CUDART_INF) {
-    if (tid == 0) raise_err(b.err, DSMC_E_RUNTIME, g.c, la.level, kReasonZeroTable);
-    return;
-  }
-  for (int i = tid; i < N; i += blockDim.x) {
-    const double sc = exp_w_le0(DSUB(wm[i], gmax));  // wm[i] <= gmax
-    wscale[i] = sc;
-    wtot[i] = DMUL(sc, wraw[i]);
-  }
-  __syncthreads();
-  // grand = reduce_sum(row_total) (8-lane contract)
-  const int n8 = N & ~7;
-  if (tid < 8) {
-    double acc = 0.0;
-    for (int i = tid; i < n8; i += 8) acc = DADD(acc, wtot[i]);
-    a8s[tid] = acc;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double a8[8];
-    for (int l = 0; l < 8; ++l) a8[l] = a8s[l];
-    double tot = combine8(a8);
-    for (int i = n8; i < N; ++i) tot = DADD(tot, wtot[i]);
-    s_grand = tot;
-    double cum = 0.0;  // sequential inclusive prefix (the walk's cum)
-    for (int i = 0; i < N; ++i) {
-      cum = DADD(cum, wtot[i]);
-      wpre[i] = cum;
-    }
-    b.LMW[(size_t)ch * b.T + la.cursor + k] = DADD(gmax, log(tot));
-  }
-  __syncthreads();
-  const double grand = s_grand;
+  const int tid = threadIdx.x;
+  const double grand = wx[1];
   const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
   const double coef = row_coef<MC>(M, b.t0 + g.c);
   const int off = b.conditional ? 1 : 0;

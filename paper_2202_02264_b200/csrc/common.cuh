@@ -221,7 +221,7 @@ __device__ __forceinline__ double exp_w(double x) {
 // results as exp_w there, without the NaN and overflow selects.
 __device__ __forceinline__ double exp_w_le0(double x) {
   const bool low = x <= -708.0;
-  const double xc = low ? 0.0 : x;
+  const double xc = x;  // a low x (-inf included) evaluates garbage the final select drops
   const double k = rint(__dmul_rn(xc, kExpW[0]));
   double r = __fma_rn(k, kExpW[1], xc);
   r = __fma_rn(k, kExpW[2], r);

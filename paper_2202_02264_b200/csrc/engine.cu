@@ -649,6 +649,8 @@ int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
   c64_rows<MC, D><<<dim3((b.N + kC64Rows - 1) / kC64Rows, nk, b.B), kC64Threads,
                     fast ? smf : sm, ctx->stream>>>(b, la, fast);
   LAUNCHED(ctx);
+  c64_cdf<<<(nk * b.B + 7) / 8, 256, 0, ctx->stream>>>(b, la, nk);
+  LAUNCHED(ctx);
   c64_sample<MC, D><<<dim3(nk, 1, b.B), 256, sm, ctx->stream>>>(b, la, systematic);
   LAUNCHED(ctx);
   return DSMC_OK;
@@ -1089,7 +1091,7 @@ int run_tree(dsmc_ctx* ctx, dsmc_model_handle* h, const RunOpts& o, RunResult* r
   // ---------------------------------------------------------------- levels
   const bool lazy = o.resampler == DSMC_MH_LAZY || o.resampler == DSMC_REJECTION_LAZY;
   const int nsub = (N + kSub - 1) / kSub;
-  const size_t ws_comb = fp64 ? (size_t)N * (5 + nsub) : ((size_t)N * nsub + 1) / 2;
+  const size_t ws_comb = fp64 ? (size_t)N * (5 + nsub) + 2 : ((size_t)N * nsub + 1) / 2;
   // bytes of pass-1 scratch per chunk: 4 GB = up to 65535 combines per
   // launch (C5: 412.6 vs 415.3 ms/step at 1 GB; smaller chunks that would
   // keep a chunk's sums in L2 lose more to wave tails: 507 ms at 32 MB;
