@@ -90,12 +90,12 @@ struct Col64 {
   // FP32 screen copies (c64_rows with fast = 1), in column PAIRS: pair
   // p = 32 s + l holds columns 64 s + l and 64 s + 32 + l (sub-block s, lane
   // l), so a lane screens both with packed FADD2 / FFMA2. States are centred
-  // on column 0's (x - cen) in two planes (first / second column of each pair:
-  // float4 for d > 1, float for d = 1), bases and leaf weights as float2 pairs; dead padding columns carry
-  // base -inf. cm: the largest finite |base|, |lwr|, |x_k - cen_k|, and
+  // on column 0's (x - cen), interleaved so a lane's packed operands are one
+  // 16-byte load; bases and leaf weights as float2 pairs; dead padding
+  // columns carry base -inf. cm: the largest finite |base|, |lwr|, |x_k - cen_k|, and
   // (as an int) whether every column is clean (finite states, no NaN or +inf
   // base / weight); cen: the centre (FP64).
-  float* xs;    // [2][npair] (first / second column of each pair)
+  float* xs;    // d > 1: planes [2][npair] float4 (x0, x0', x1, x1'), (x2, x2', x3, x3'); d = 1: float2 (x, x')
   int npair;
   float2* bf2;
   float2* lf2;
@@ -231,21 +231,21 @@ template <int MC, int D, int MODE>
 __device__ __forceinline__ float2 est32_pair(const float2* nmu, float2 cf, const Col64& C, int p) {
   float2 q;
   if (MC == kLGN && D > 1) {
-    const float4 xa = reinterpret_cast<const float4*>(C.xs)[p];
-    const float4 xb = reinterpret_cast<const float4*>(C.xs)[C.npair + p];
-    const float2 t0 = __fadd2_rn(make_float2(xa.x, xb.x), nmu[0]);
-    const float2 t1 = __fadd2_rn(make_float2(xa.y, xb.y), nmu[1]);
+    const float4 a = reinterpret_cast<const float4*>(C.xs)[p];  // (x0, x0', x1, x1')
+    const float2 t0 = __fadd2_rn(make_float2(a.x, a.y), nmu[0]);
+    const float2 t1 = __fadd2_rn(make_float2(a.z, a.w), nmu[1]);
     q = __ffma2_rn(t1, t1, __fmul2_rn(t0, t0));
     if (D > 2) {
-      const float2 t2 = __fadd2_rn(make_float2(xa.z, xb.z), nmu[2]);
+      const float4 c = reinterpret_cast<const float4*>(C.xs)[C.npair + p];  // (x2, x2', x3, x3')
+      const float2 t2 = __fadd2_rn(make_float2(c.x, c.y), nmu[2]);
       q = __ffma2_rn(t2, t2, q);
-    }
-    if (D > 3) {
-      const float2 t3 = __fadd2_rn(make_float2(xa.w, xb.w), nmu[3]);
-      q = __ffma2_rn(t3, t3, q);
+      if (D > 3) {
+        const float2 t3 = __fadd2_rn(make_float2(c.z, c.w), nmu[3]);
+        q = __ffma2_rn(t3, t3, q);
+      }
     }
   } else {
-    const float2 t = __fadd2_rn(make_float2(C.xs[p], C.xs[C.npair + p]), nmu[0]);
+    const float2 t = __fadd2_rn(reinterpret_cast<const float2*>(C.xs)[p], nmu[0]);
     q = __fmul2_rn(t, t);
   }
   float2 a = __ffma2_rn(cf, q, C.bf2[p]);
@@ -359,10 +359,16 @@ __device__ void stage_cols(const Bufs& b, const LevelArgs& la, int ch,
           clean &= isfinite(z[k]) && isfinite(xs[k]);
         }
       }
-      if (d == 1)
-        C.xs[h * npair + pr] = xs[0];
-      else
-        reinterpret_cast<float4*>(C.xs)[h * npair + pr] = make_float4(xs[0], xs[1], xs[2], xs[3]);
+      if (d == 1) {
+        C.xs[2 * pr + h] = xs[0];
+      } else {  // planes (x0, x0', x1, x1') and (x2, x2', x3, x3') per pair
+        C.xs[4 * pr + h] = xs[0];
+        C.xs[4 * pr + 2 + h] = xs[1];
+        if (d > 2) {
+          C.xs[4 * (npair + pr) + h] = xs[2];
+          C.xs[4 * (npair + pr) + 2 + h] = xs[3];
+        }
+      }
     }
   }
   if (fast) {  // block maxima of the finite magnitudes (non-negative: int order)
@@ -502,6 +508,7 @@ __device__ __forceinline__ void c64_row(const Bufs& b, const LevelArgs& la, cons
     return;
   }
   const int grp = lane >> 3, l8 = lane & 7;
+  double tot = 0.0;
   for (int s0 = 0; s0 < nsub; s0 += 4) {
     const int s = s0 + grp;
     const bool act = s < nsub;
@@ -521,19 +528,21 @@ __device__ __forceinline__ void c64_row(const Bufs& b, const LevelArgs& la, cons
     double a8[8];
 #pragma unroll
     for (int l = 0; l < 8; ++l) a8[l] = __shfl_sync(~0u, acc, (lane & ~7) + l);
+    double bs = 0.0;
     if (act && l8 == 0) {
-      double bs = combine8(a8);
+      bs = combine8(a8);
       for (int j = j0 + len8; j < j0 + len; ++j)
         bs = DADD(bs, exp_w_le0(DSUB(fill64m<MC, D, MODE>(coef, mu, C, cpad(j), sl), mx)));
       srow[s] = bs;
     }
+    // raw row total: sequential over sub-blocks, in lane 0
+#pragma unroll
+    for (int g4 = 0; g4 < 4; ++g4) {
+      const double v = __shfl_sync(~0u, bs, 8 * g4);
+      if (s0 + g4 < nsub) tot = DADD(tot, v);
+    }
   }
-  __syncwarp();
-  if (lane == 0) {
-    double tot = 0.0;
-    for (int s = 0; s < nsub; ++s) tot = DADD(tot, srow[s]);
-    wraw[i] = tot;
-  }
+  if (lane == 0) wraw[i] = tot;
 }
 
 constexpr int kC64Threads = 512;   // 16 warps, one row at a time each
@@ -558,14 +567,30 @@ __global__ void __launch_bounds__(kC64Threads, 2) c64_rows(Bufs b, LevelArgs la,
   const double coef = row_coef<MC>(M, b.t0 + g.c);
   const int warp = threadIdx.x >> 5;
   const double* XL = b.X64 + ((size_t)ch * b.K + L.t) * N * d;
-  for (int r = warp; r < kC64Rows; r += kC64Threads / 32) {
+  // the CTA's row means and left weights, one thread per row (a warp per row
+  // would evaluate each 32 times over)
+  double* MU = smem + cols64_bytes(N, D, fast != 0) / sizeof(double);  // [kC64Rows][D]
+  double* SL = MU + kC64Rows * D;                                        // [kC64Rows]
+  for (int r = threadIdx.x; r < kC64Rows; r += kC64Threads) {
     const int i = blockIdx.x * kC64Rows + r;
     if (i >= N) break;
     const uint32_t p = map_last(b, la, ch, L, i);
     double xl[D], mu[D];
+#pragma unroll
     for (int q = 0; q < d; ++q) xl[q] = XL[(size_t)p * d + q];
     row_mean<MC, D>(M, tc, b.t0 + g.c, xl, mu);
-    const double sl = lnonuni ? b.LW64[((size_t)ch * b.K + L.t) * N + i] : 0.0;
+#pragma unroll
+    for (int q = 0; q < d; ++q) MU[r * D + q] = mu[q];
+    SL[r] = lnonuni ? b.LW64[((size_t)ch * b.K + L.t) * N + i] : 0.0;
+  }
+  __syncthreads();
+  for (int r = warp; r < kC64Rows; r += kC64Threads / 32) {
+    const int i = blockIdx.x * kC64Rows + r;
+    if (i >= N) break;
+    double mu[D];
+#pragma unroll
+    for (int q = 0; q < d; ++q) mu[q] = MU[r * D + q];
+    const double sl = SL[r];
     // the leaf-weight case of fill64 (uniform over the row)
     if (C.has_lwr)
       c64_row<MC, D, 2>(b, la, C, mu, coef, sl, i, g.c, fast != 0, wm, wraw, wsub);

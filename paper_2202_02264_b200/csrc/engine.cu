@@ -634,7 +634,8 @@ int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
                int systematic) {
   const size_t lim = (size_t)ctx->smem_optin - 1024;
   const size_t sm = cols64_bytes(b.N, D, false);
-  if (sm > lim)
+  const size_t rows = sizeof(double) * kC64Rows * (D + 1);  // pass 1's row means + weights
+  if (sm + rows > lim)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
                    "FP64 parity combine: N * (d + 2) doubles exceed the shared-memory "
                    "column stage (N <= " +
@@ -645,9 +646,9 @@ int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
   const bool screen_env =
       !(getenv("DSMC_C64_SCREEN") && atoi(getenv("DSMC_C64_SCREEN")) == 0);
   const size_t smf = cols64_bytes(b.N, D, true);
-  const int fast = screen_env && smf <= lim;
+  const int fast = screen_env && smf + rows <= lim;
   c64_rows<MC, D><<<dim3((b.N + kC64Rows - 1) / kC64Rows, nk, b.B), kC64Threads,
-                    fast ? smf : sm, ctx->stream>>>(b, la, fast);
+                    (fast ? smf : sm) + rows, ctx->stream>>>(b, la, fast);
   LAUNCHED(ctx);
   c64_cdf<<<(nk * b.B + 7) / 8, 256, 0, ctx->stream>>>(b, la, nk);
   LAUNCHED(ctx);
