@@ -22,6 +22,7 @@
 #include "kalman_scan.cuh"
 #include "pair_tc.cuh"
 #include "wide.cuh"
+#include "pair_tc2.cuh"
 #include "dsmc_b200.h"
 
 using namespace dsmc_dev;
@@ -100,6 +101,9 @@ struct dsmc_ctx {
   // FP32 pass 1: the CUDA-core kernel c32_pair (default, faster today) or
   // the tcgen05 kernel c32_pair_tc (DSMC_PAIR_KERNEL=tc)
   bool pair_tc = false;
+  // the streaming tcgen05 pass 1 c32_pair_tc2 with its column prologue
+  // (DSMC_PAIR_KERNEL=tc2; pair_tc2.cuh)
+  bool pair_tc2 = false;
   int num_sms = 148;
   int smem_optin = 227 * 1024;  // max dynamic shared memory per CTA (opt-in)
   cudaStream_t copy_stream = nullptr;  // device->host copies overlapping the gather
@@ -731,7 +735,33 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
     ctx->kev_used += 3;
     CU(rec_event(ev[0], ctx->stream));
   }
-  if (use_tc) {
+  const int nrt_tc2 = (N + kTcRows - 1) / kTcRows;
+  // (levels with fewer CTAs than two per SM stay on c32_pair; DSMC_TC2_MIN
+  // overrides the threshold, e.g. 0 in tests)
+  const long tc2_min = getenv("DSMC_TC2_MIN") ? atol(getenv("DSMC_TC2_MIN")) : 2 * 148;
+  const bool use_tc2 = ctx->pair_tc2 && D >= 2 && b.B == 1 && (long)nk * nrt_tc2 >= tc2_min;
+  if (use_tc2) {
+    // streaming tensor-core pass 1: per sub-chunk of <= kTc2Sub combines the
+    // prologue writes the column tiles (kept in L2), then one CTA per 128-row
+    // tile consumes them
+    using T = Tc2L<D>;
+    const size_t cb = tc2_comb_bytes(nsubb, T::TILE);
+    void* tp;
+    CU(ctx->arena.get("TILE32", cb * (size_t)std::min(nk, kTc2Sub), &tp));
+    for (int s0 = 0; s0 < nk; s0 += kTc2Sub) {
+      const int m = std::min(kTc2Sub, nk - s0);
+      LevelArgs l2 = la;
+      l2.k0 = la.k0 + s0;
+      l2.ws = la.ws + (size_t)s0 * la.ws_comb;
+      l2.aux = la.aux + (size_t)s0 * la.aux_comb;
+      c32_prol<D><<<dim3((nsubb * kSub + 127) / 128, m, 1), 128, 0, ctx->stream>>>(
+          b, l2, static_cast<uint8_t*>(tp));
+      LAUNCHED(ctx);
+      c32_pair_tc2<D><<<dim3(nrt_tc2, m, 1), kTc2Threads, 0, ctx->stream>>>(
+          b, l2, static_cast<const uint8_t*>(tp));
+      if (s0 + kTc2Sub < nk) LAUNCHED(ctx);
+    }
+  } else if (use_tc) {
     // tensor-core pass 1: 128-row tiles, 4 CTAs per SM (128 TMEM columns each)
     const int nrt_tc = (N + kTcRows - 1) / kTcRows;
     int ncs_tc = 1;
@@ -1420,7 +1450,10 @@ int dsmc_create(int device, dsmc_ctx** out) {
     return DSMC_E_NO_DEVICE;
   auto* ctx = new dsmc_ctx();
   ctx->device = device;
-  if (const char* pk = getenv("DSMC_PAIR_KERNEL")) ctx->pair_tc = strcmp(pk, "tc") == 0;
+  if (const char* pk = getenv("DSMC_PAIR_KERNEL")) {
+    ctx->pair_tc = strcmp(pk, "tc") == 0;
+    ctx->pair_tc2 = strcmp(pk, "tc2") == 0;
+  }
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (cudaSetDevice(device) != cudaSuccess ||

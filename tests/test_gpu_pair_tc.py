@@ -15,16 +15,17 @@ pytestmark = pytest.mark.gpu
 
 
 def _run(kernel, out):
-    env = dict(os.environ, DSMC_PAIR_KERNEL=kernel)
+    env = dict(os.environ, DSMC_PAIR_KERNEL=kernel, DSMC_TC2_MIN="0")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "tc_lmw.py"), "run", out],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "failed" not in r.stdout, r.stdout
 
 
-def test_tc_level1_weights_match_the_cuda_core_kernel(tmp_path):
+@pytest.mark.parametrize("kernel", ["tc", "tc2"])
+def test_tc_level1_weights_match_the_cuda_core_kernel(tmp_path, kernel):
     a, b = str(tmp_path / "tc.npz"), str(tmp_path / "fma.npz")
-    _run("tc", a)
+    _run(kernel, a)
     _run("fma", b)
     A, B = np.load(a), np.load(b)
     assert set(A.files) == set(B.files) and len(A.files) == 7
@@ -36,7 +37,8 @@ def test_tc_level1_weights_match_the_cuda_core_kernel(tmp_path):
         assert np.max(np.abs(A[k] - B[k])) < tol, (k, np.max(np.abs(A[k] - B[k])))
 
 
-def test_tc_smoothing_tracks_kalman():
+@pytest.mark.parametrize("kernel", ["tc", "tc2"])
+def test_tc_smoothing_tracks_kalman(kernel):
     code = r"""
 import numpy as np
 from paper_2202_02264_b200 import abi, models
@@ -59,7 +61,7 @@ for N in (100, 300):
     assert float(np.sqrt(np.mean(np.mean(zs, 0) ** 2))) < 0.6, N
 print(float(np.sqrt(np.mean(z ** 2))))
 """
-    env = dict(os.environ, DSMC_PAIR_KERNEL="tc", PYTHONPATH=ROOT)
+    env = dict(os.environ, DSMC_PAIR_KERNEL=kernel, DSMC_TC2_MIN="0", PYTHONPATH=ROOT)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
