@@ -86,21 +86,32 @@ __global__ void __launch_bounds__(128) c32_prol(Bufs b, LevelArgs la, uint8_t* t
   __shared__ CutConst32 s_cc;
   __shared__ float s_cm[4];
   if (threadIdx.x == 0) load_cut32<D>(b.tc[(size_t)ch * b.Kt + b.t0 + g.c], s_cc);
-  __syncthreads();
-  const CutConst32& cc = s_cc;
+  const CutConst32& cc = s_cc;  // read after the barrier below
   const size_t cslot = (size_t)blockIdx.z * gridDim.y + blockIdx.y;
   const Aux32 ax = aux32(la, cslot, N);
   uint8_t* ct = tiles + cslot * tc2_comb_bytes(nsub, T::TILE);
   float* cmax = reinterpret_cast<float*>(ct + (size_t)nsub * T::TILE);
   const int q = blockIdx.x * 128 + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // both gather chains (column q and row q) issued before any arithmetic
+  const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
+  float4 xc = make_float4(0.f, 0.f, 0.f, 0.f), xl = xc;
+  float col = -CUDART_INF_F, lwr = 0.f;
+  if (q < N) {
+    const uint32_t pc = map_first(b, la, ch, R, q);
+    const uint32_t pr = map_last(b, la, ch, L, q);
+    const size_t offc = ((size_t)ch * b.K + R.t) * N + pc;
+    xc = b.X32[offc];
+    col = b.COL[offc];
+    xl = b.X32[((size_t)ch * b.K + L.t) * N + pr];
+    if (lnonuni) lwr = b.LW32[(size_t)ch * N + q];
+  }
+  __syncthreads();  // s_cc
   float y[4] = {0.f, 0.f, 0.f, 0.f};
   float A = -CUDART_INF_F, cv = -CUDART_INF_F;
   if (q < N) {
-    const uint32_t p = map_first(b, la, ch, R, q);
-    const size_t off = ((size_t)ch * b.K + R.t) * N + p;
-    cv = b.COL[off];
-    col32<D>(cc, b.X32[off], cv, y, A);
+    cv = col;
+    col32<D>(cc, xc, cv, y, A);
     ax.y[q] = make_float4(y[0], y[1], y[2], y[3]);
     ax.A[q] = A;
   }
@@ -141,9 +152,6 @@ __global__ void __launch_bounds__(128) c32_prol(Bufs b, LevelArgs la, uint8_t* t
     tc_store_row<D>(ct + (size_t)s * T::TILE, q & (kSub - 1), vals);
   }
   if (q < N) {  // row q: the left block's last-leaf state
-    const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
-    const float4 xl = b.X32[((size_t)ch * b.K + L.t) * N + map_last(b, la, ch, L, q)];
-    const float lwr = lnonuni ? b.LW32[(size_t)ch * N + q] : 0.f;
     float u[4] = {0.f, 0.f, 0.f, 0.f}, Bv;
     row32<D>(cc, xl, lwr, u, Bv);
     ax.u[q] = make_float4(u[0], u[1], u[2], u[3]);
