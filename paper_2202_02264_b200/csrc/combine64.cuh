@@ -601,6 +601,30 @@ __global__ void __launch_bounds__(kC64Threads, 2) c64_rows(Bufs b, LevelArgs la,
   }
 }
 
+// Inversion inside a sub-block (select_sorted, resampling.cpp:109-153 /
+// Appendix A): the first j in [j0, j1) whose running sum c3 (from c3 = c2b)
+// exceeds `local`; past the end, the last positive entry (rounding spill).
+template <int MC, int D, int MODE>
+__device__ __forceinline__ int walk64(double coef, const double* mu, const Col64& C, double sl,
+                                      double mrow, double c3, double local, int j0, int j1) {
+  for (int jb = j0; jb < j1; jb += 8) {
+    double e[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      e[q] = jb + q < j1 ? exp_w_le0(DSUB(fill64m<MC, D, MODE>(coef, mu, C, cpad(jb + q), sl), mrow))
+                         : 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (jb + q >= j1) break;
+      c3 = DADD(c3, e[q]);
+      if (local < c3) return jb + q;
+    }
+  }
+  int j = j1 - 1;  // spill: clamp to the last positive entry
+  while (j > 0 && !(exp_w(DSUB(fill64m<MC, D, MODE>(coef, mu, C, cpad(j), sl), mrow)) > 0.0)) --j;
+  return j;
+}
+
 // Cross-row combination of the pair table (resampling.cpp:92-102), one warp
 // per combine (any number of combines per CTA): g = max_i m_i, per-row scale
 // exp_w(m_i - g) and total scale_i raw_i, the grand total under the 8-lane
@@ -659,9 +683,18 @@ __global__ void __launch_bounds__(256) c64_cdf(Bufs b, LevelArgs la, int nk) {
 
 // Pass 2: one CTA per combine: per-slot inversion over the prefix c64_cdf
 // left in ws (Appendix A), ancestor maps, block log Z.
+#ifndef DSMC_C64S_MINB
+#define DSMC_C64S_MINB 2
+#endif
+// shared memory of c64_sample beyond the column stage: the row prefix, and in
+// sorted mode the slot records, order and sub-block counts
+__host__ __device__ inline size_t c64s_extra(int N, bool sorted) {
+  const int nsub = (N + kSub - 1) / kSub;
+  return sizeof(double) * (size_t)N + (sorted ? (size_t)N * (16 + 8 + 4) + 4 * (size_t)nsub : 0);
+}
 template <int MC, int D>
-__global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
-                                                  int systematic) {
+__global__ void __launch_bounds__(256, DSMC_C64S_MINB) c64_sample(Bufs b, LevelArgs la,
+                                                  int systematic, int sorted) {
   extern __shared__ double smem[];
   const int k = la.k0 + blockIdx.x, ch = blockIdx.z;
   const int N = b.N, nsub = (N + kSub - 1) / kSub;
@@ -680,6 +713,9 @@ __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
   stage_cols<MC, D>(b, la, ch, R, M, tc, smem, C);
   const int tid = threadIdx.x;
   const double grand = wx[1];
+  double* spre = smem + cols64_bytes(N, D, false) / sizeof(double);  // [N] row prefix
+  for (int q = tid; q < N; q += blockDim.x) spre[q] = wpre[q];
+  __syncthreads();
   const bool lnonuni = L.leaf && !b.UNI[(size_t)ch * b.K + L.t];
   const double coef = row_coef<MC>(M, b.t0 + g.c);
   const int off = b.conditional ? 1 : 0;
@@ -698,29 +734,11 @@ __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
   uint32_t* PL = b.PL + gidx * N;
   uint32_t* PR = b.PR + gidx * N;
   const double* XL = b.X64 + ((size_t)ch * b.K + L.t) * N * d;
-  for (int m = tid; m < la.n_out; m += blockDim.x) {
-    const double pt = systematic ? DMUL(DADD(u0, (double)m), step)
-                                 : DMUL(u64_uniform(stream_u64(id, m)), grand);
-    int lo = 0, hi = N;  // first i with pt < S_i
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (pt < wpre[mid]) hi = mid;
-      else lo = mid + 1;
-    }
-    const int i = lo < N ? lo : N - 1;
-    const double before = i > 0 ? wpre[i - 1] : 0.0;
-    int row = i;
-    while (row > 0 && wtot[row] <= 0.0) --row;
-    double local = DDIV(DSUB(pt, before), wscale[row]);
-    if (!(local >= 0.0)) local = 0.0;
-    const double* srow = wsub + (size_t)row * nsub;
-    int s = 0;
-    double c2b = 0.0, c2 = srow[0];
-    while (!(local < c2) && s + 1 < nsub) {
-      c2b = c2;
-      ++s;
-      c2 = DADD(c2, srow[s]);
-    }
+  // the column of slot m in row `row`, sub-block s: first j with local < c3,
+  // c3 the running sum from c2b (the reference's sequential walk); the
+  // weights of 8 entries are evaluated together (independent exp_w chains),
+  // the sum and the test stay in order
+  auto finish = [&](int m, int row, int s, double local, double c2b) {
     const uint32_t pl = map_last(b, la, ch, L, row);
     double xl[D], mu[D];
     for (int q = 0; q < d; ++q) xl[q] = XL[(size_t)pl * d + q];
@@ -728,18 +746,107 @@ __global__ void __launch_bounds__(256) c64_sample(Bufs b, LevelArgs la,
     const double sl = lnonuni ? b.LW64[((size_t)ch * b.K + L.t) * N + row] : 0.0;
     const double mrow = wm[row];
     const int j0 = s * kSub, j1 = min(j0 + kSub, N);
-    double c3 = c2b;
-    int j = j0;
-    for (; j < j1; ++j) {
-      c3 = DADD(c3, exp_w_le0(DSUB(fill64<MC, D>(M, tc, coef, mu, C, j, sl, lnonuni), mrow)));
-      if (local < c3) break;
-    }
-    if (j == j1) {  // spill: clamp to the last positive entry
-      j = j1 - 1;
-      while (j > 0 && !(exp_w(DSUB(fill64<MC, D>(M, tc, coef, mu, C, j, sl, lnonuni), mrow)) > 0.0)) --j;
-    }
+    const int j = C.has_lwr ? walk64<MC, D, 2>(coef, mu, C, sl, mrow, c2b, local, j0, j1)
+                  : (lnonuni && sl != 0.0)
+                      ? walk64<MC, D, 1>(coef, mu, C, sl, mrow, c2b, local, j0, j1)
+                      : walk64<MC, D, 0>(coef, mu, C, sl, mrow, c2b, local, j0, j1);
     PL[m + off] = (uint32_t)row;
     PR[m + off] = (uint32_t)j;
+  };
+  // sorted mode: per-slot records (local, c2b | row, s), sub-block counts, order
+  double* RLC = spre + N;                                    // [2 n_out]
+  int2* RRS = reinterpret_cast<int2*>(RLC + 2 * (size_t)N);  // [n_out]
+  int* ORD = reinterpret_cast<int*>(RRS + N);                // [n_out]
+  int* CNT = ORD + N;                                        // [nsub]
+  if (sorted) {
+    for (int q = tid; q < nsub; q += blockDim.x) CNT[q] = 0;
+    __syncthreads();
+  }
+  // each thread takes 4 consecutive slots: one Philox block gives their
+  // uniforms (slot m <-> u64 number m of the stream, rng.cpp:45-68)
+  for (int q0 = 4 * tid; q0 < la.n_out; q0 += 4 * blockDim.x) {
+    U64x4 blk;
+    if (!systematic) blk = stream_block(id, (uint64_t)q0 >> 2);
+#pragma unroll 1
+    for (int qq = 0; qq < 4; ++qq) {
+      const int m = q0 + qq;
+      if (m >= la.n_out) break;
+      const double pt = systematic ? DMUL(DADD(u0, (double)m), step)
+                                   : DMUL(u64_uniform(blk.v[qq]), grand);
+      int lo = 0, hi = N;  // first i with pt < S_i (prefix staged in shared memory)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (pt < spre[mid]) hi = mid;
+        else lo = mid + 1;
+      }
+      const int i = lo < N ? lo : N - 1;
+      const double before = i > 0 ? spre[i - 1] : 0.0;
+      int row = i;
+      while (row > 0 && wtot[row] <= 0.0) --row;
+      double local = DDIV(DSUB(pt, before), wscale[row]);
+      if (!(local >= 0.0)) local = 0.0;
+      const double* srow = wsub + (size_t)row * nsub;
+      int s = 0;
+      double c2b = 0.0, c2;
+      {  // the sub-block walk; its loads issued 16 at a time ahead of the
+         // sequential sum
+        double sv[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) sv[q] = q < nsub ? srow[q] : 0.0;
+        c2 = sv[0];
+        bool done = local < c2 || nsub == 1;
+#pragma unroll
+        for (int q = 1; q < 16; ++q) {
+          if (!done) {
+            c2b = c2;
+            s = q;
+            c2 = DADD(c2, sv[q]);
+            done = local < c2 || q + 1 >= nsub;
+          }
+        }
+        while (!done) {  // nsub > 16
+          c2b = c2;
+          ++s;
+          c2 = DADD(c2, srow[s]);
+          done = local < c2 || s + 1 >= nsub;
+        }
+      }
+      if (sorted) {
+        RLC[2 * m] = local;
+        RLC[2 * m + 1] = c2b;
+        RRS[m] = make_int2(row, s);
+        atomicAdd(&CNT[s], 1);
+      } else {
+        finish(m, row, s, local, c2b);
+      }
+    }
+  }
+  if (sorted) {
+    // slots re-ordered by sub-block (CTA counting sort) so that a warp's
+    // lanes recompute the same sub-block's records (shared-memory broadcasts
+    // instead of bank conflicts); every slot's arithmetic is unchanged
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of the sub-block counts
+      int carry = 0;
+      for (int c0 = 0; c0 < nsub; c0 += 32) {
+        const int c = c0 + tid < nsub ? CNT[c0 + tid] : 0;
+        int v = c;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int n = __shfl_up_sync(~0u, v, o);
+          if (tid >= o) v += n;
+        }
+        if (c0 + tid < nsub) CNT[c0 + tid] = carry + v - c;
+        carry += __shfl_sync(~0u, v, 31);
+      }
+    }
+    __syncthreads();
+    for (int m = tid; m < la.n_out; m += blockDim.x) ORD[atomicAdd(&CNT[RRS[m].y], 1)] = m;
+    __syncthreads();
+    for (int o = tid; o < la.n_out; o += blockDim.x) {
+      const int m = ORD[o];
+      const int2 rs = RRS[m];
+      finish(m, rs.x, rs.y, RLC[2 * m], RLC[2 * m + 1]);
+    }
   }
   if (b.conditional && tid == 0) {
     PL[0] = 0;

@@ -639,7 +639,7 @@ int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
   const size_t lim = (size_t)ctx->smem_optin - 1024;
   const size_t sm = cols64_bytes(b.N, D, false);
   const size_t rows = sizeof(double) * kC64Rows * (D + 1);  // pass 1's row means + weights
-  if (sm + rows > lim)
+  if (sm + rows > lim || sm + c64s_extra(b.N, false) > lim)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
                    "FP64 parity combine: N * (d + 2) doubles exceed the shared-memory "
                    "column stage (N <= " +
@@ -656,7 +656,10 @@ int launch_c64(dsmc_ctx* ctx, const Bufs& b, const LevelArgs& la, int nk,
   LAUNCHED(ctx);
   c64_cdf<<<(nk * b.B + 7) / 8, 256, 0, ctx->stream>>>(b, la, nk);
   LAUNCHED(ctx);
-  c64_sample<MC, D><<<dim3(nk, 1, b.B), 256, sm, ctx->stream>>>(b, la, systematic);
+  // the sampler sorts its slots by sub-block when the records fit
+  const int sorted = sm + c64s_extra(b.N, true) <= lim;
+  c64_sample<MC, D><<<dim3(nk, 1, b.B), 256, sm + c64s_extra(b.N, sorted), ctx->stream>>>(
+      b, la, systematic, sorted);
   LAUNCHED(ctx);
   return DSMC_OK;
 }
