@@ -458,8 +458,12 @@ def run_ours(args, cfg, rank, world, device):
         pairs_local = (Kloc - 1) * N * N  # rank 0's local combines (all of them at N=1)
         peak, peak_src = sfu_peak_pairs_per_s(ck.get("sm_max_mhz"))
         ach = pairs_local / (pair_ms * 1e-3) if pair_ms else None
-        pair_name = ("c32_pair" if d <= 4 else
-                     "prologw_kernel + pairw_tc_kernel (tcgen05 cross term)")
+        pk = os.environ.get("DSMC_PAIR_KERNEL", "")
+        wk = os.environ.get("DSMC_WIDE_PAIR", "")
+        pair_name = (("c32_prol + c32_pair_tc2 (tcgen05, opt-in)" if pk == "tc2" else
+                      "c32_pair_tc (tcgen05, opt-in)" if pk == "tc" else "c32_pair") if d <= 4 else
+                     "prologw_kernel + " + {"tc1": "pairw_tc_kernel", "fma": "pairw_kernel"}.get(
+                         wk, "pairw_tc2_kernel") + " (tcgen05 cross term)")
         roof = {"bound": "sfu", "kernel": pair_name, "achieved": ach, "peak": peak,
                 "unit": "pair-evals/s (1 MUFU.EX2 each)", "frac": ach / peak if ach else None,
                 "peak_source": peak_src, "traffic": None,

@@ -25,8 +25,9 @@ if [ "$NCU" = "1" ]; then
   DSMC_NO_GRAPH=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
     --log-file $O/launches_c5.csv python tools/prof_run.py --config c5 --reps 1 > $O/ncu_launch.log 2>&1
   python tools/ncu_summary.py launches $O/launches_c5.csv > $O/launches_c5.md 2>&1
-  for spec in ${NCU_SPECS:-"c5 c32_pair" "c5 c32_sample" "c3 lazy32_kernel" "c6 pairw_tc_kernel" "c6 samplew_kernel"}; do
-    set -- $spec
+  # NCU_SPECS: space-separated config:kernel pairs
+  for spec in ${NCU_SPECS:-c5:c32_pair c5:c32_sample c3:lazy32_kernel c6:pairw_tc2_kernel c6:samplew_kernel}; do
+    set -- ${spec/:/ }
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$2 -s 3 -c 1 \
       -o $R/full_$1_$2 -f python tools/prof_run.py --config $1 --reps 1 > $O/ncu_full_$1_$2.log 2>&1
     echo "$1 $2 rc=$?" >> $O/ncu_status.txt
