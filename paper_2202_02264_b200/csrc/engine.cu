@@ -23,6 +23,7 @@
 #include "pair_tc.cuh"
 #include "wide.cuh"
 #include "pair_tc2.cuh"
+#include "small32.cuh"
 #include "dsmc_b200.h"
 
 using namespace dsmc_dev;
@@ -737,6 +738,19 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
     ev = &ctx->kev[ctx->kev_used];
     ctx->kev_used += 3;
     CU(rec_event(ev[0], ctx->stream));
+  }
+  // small N: pass 1 and pass 2 fused in one CTA per combine (c32_small;
+  // DSMC_SMALL=0 keeps the two-kernel path)
+  const bool small_env = !(getenv("DSMC_SMALL") && atoi(getenv("DSMC_SMALL")) == 0);
+  if (small_env && N <= kSmallN && !use_tc && !ctx->pair_tc2) {
+    CU(launch_pdl(c32_small<D>, dim3(nk, 1, b.B), dim3(kSmallN), 0, ctx->stream, b, la,
+                  systematic));
+    LAUNCHED(ctx);
+    if (ev) {
+      CU(rec_event(ev[1], ctx->stream));
+      CU(rec_event(ev[2], ctx->stream));
+    }
+    return DSMC_OK;
   }
   const int nrt_tc2 = (N + kTcRows - 1) / kTcRows;
   // (levels with fewer CTAs than two per SM stay on c32_pair; DSMC_TC2_MIN
