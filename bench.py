@@ -508,7 +508,10 @@ def run_ours(args, cfg, rank, world, device):
         if world == 1 and timings[0] > 0 and timings[2] > 0:
             dpb = 16 if d <= 4 else 4 * (8 if d <= 8 else 16 if d <= 16 else 32)  # state bytes
             leaf_b = K * N * (dpb + 4)           # state + column term written
-            gath_b = K * N * (dpb + 4 + 4)       # state + level-1 pair + map read
+            # gather: state + level-1 pair index + level-1 map (one 4-byte entry per
+            # two leaves); top-down composition over levels >= 2 (sum of blocks
+            # ~K/2, N entries each): map read 4 + two pair reads 8 + two writes 8
+            gath_b = K * N * (dpb + 4 + 2) + (K // 2) * N * 20
             hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]) \
                 if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6551.0
             roof["hbm_kernels"] = {

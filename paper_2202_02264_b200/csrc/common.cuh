@@ -107,6 +107,15 @@ __device__ __forceinline__ uint64_t stream_u64(const StreamId& s, uint64_t q) {
 }
 
 // rng.cpp:66-72.
+// FP32 uniforms from the top 23 bits of a u64 without an int -> float
+// conversion (I2F issues on the XU pipe, which the leaf kernels' MUFU work
+// already saturates): the bits fill the mantissa of a float in [1, 2).
+__device__ __forceinline__ float u01_open23(uint64_t v) {  // (0, 1): (2m + 1) 2^-24
+  return __uint_as_float(0x3F800000u | (uint32_t)(v >> 41)) - (1.0f - 0x1p-24f);
+}
+__device__ __forceinline__ float u01_23(uint64_t v) {  // [0, 1): m 2^-23
+  return __uint_as_float(0x3F800000u | (uint32_t)(v >> 41)) - 1.0f;
+}
 __device__ __forceinline__ double u64_uniform(uint64_t v) {
   return __dmul_rn(static_cast<double>(v >> 11), 0x1.0p-53);
 }

@@ -326,9 +326,9 @@ __global__ void __launch_bounds__(256, 3) leaf32_kernel(Bufs b, double* raw0, in
             blk = stream_block(id, q >> 2);
             have = q >> 2;
           }
-          const float u1 = ((float)(uint32_t)(pick4(blk, (uint32_t)(q & 3)) >> 40) + 0.5f) * 0x1p-24f;
-          const float u2 = (float)(uint32_t)(pick4(blk, (uint32_t)(q & 3) + 1) >> 40) * 0x1p-24f;
-          r = sqrtf(-2.0f * __logf(u1));
+          const float u1 = u01_open23(pick4(blk, (uint32_t)(q & 3)));
+          const float u2 = u01_23(pick4(blk, (uint32_t)(q & 3) + 1));
+          { const float a2 = -2.0f * __logf(u1); r = a2 * rsqrtf(a2); }  // a2 in (0, 34]
           sincospif(2.0f * u2, &sn, &cs);
         }
         z[k] = (i & 1) ? r * sn : r * cs;
@@ -400,9 +400,9 @@ __global__ void __launch_bounds__(256, 3) leaf32_kernel(Bufs b, double* raw0, in
             have = q >> 2;
           }
           // uniform_pos / uniform at 24-bit resolution: (0,1) and [0,1)
-          const float u1 = ((float)(uint32_t)(pick4(blk, (uint32_t)(q & 3)) >> 40) + 0.5f) * 0x1p-24f;
-          const float u2 = (float)(uint32_t)(pick4(blk, (uint32_t)(q & 3) + 1) >> 40) * 0x1p-24f;
-          r = sqrtf(-2.0f * __logf(u1));
+          const float u1 = u01_open23(pick4(blk, (uint32_t)(q & 3)));
+          const float u2 = u01_23(pick4(blk, (uint32_t)(q & 3) + 1));
+          { const float a2 = -2.0f * __logf(u1); r = a2 * rsqrtf(a2); }  // a2 in (0, 34]
           sincospif(2.0f * u2, &sn, &cs);
         }
         z[k] = (i & 1) ? r * sn : r * cs;
