@@ -459,13 +459,24 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
   for (int i = tid; i < N; i += 2 * blockDim.x) {
     const int i2 = i + blockDim.x;
     float m[2] = {-CUDART_INF_F, -CUDART_INF_F}, acc[2] = {0.f, 0.f};
+    // (a missing second row re-reads the first; its result is discarded)
+    const float* w0 = ws + i;
+    const float* w1 = ws + (i2 < N ? i2 : i);
     for (int s0 = 0; s0 < nsub; s0 += 16) {
       float v[2][16];
+      if (s0 + 16 <= nsub) {  // whole round: unguarded loads, 32-bit offsets
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const bool in = s0 + q < nsub;
-        v[0][q] = in ? ws[(size_t)(s0 + q) * N + i] : -CUDART_INF_F;
-        v[1][q] = in && i2 < N ? ws[(size_t)(s0 + q) * N + i2] : -CUDART_INF_F;
+        for (int q = 0; q < 16; ++q) {
+          v[0][q] = w0[(s0 + q) * N];
+          v[1][q] = w1[(s0 + q) * N];
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const bool in = s0 + q < nsub;
+          v[0][q] = in ? w0[(s0 + q) * N] : -CUDART_INF_F;
+          v[1][q] = in ? w1[(s0 + q) * N] : -CUDART_INF_F;
+        }
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -611,8 +622,13 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
     float cum = 0.f, before_s = 0.f, wsel = 0.f, Ls_sel = 0.f;
     for (int s0 = 0; s0 < nsub; s0 += 16) {
       float v[16];
+      if (s0 + 16 <= nsub) {  // whole round: unguarded loads, 32-bit offsets
 #pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = (s0 + q < nsub) ? w[(size_t)(s0 + q) * N] : -CUDART_INF_F;
+        for (int q = 0; q < 16; ++q) v[q] = w[(s0 + q) * N];
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = (s0 + q < nsub) ? w[(s0 + q) * N] : -CUDART_INF_F;
+      }
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const float e = (s0 + q < nsub) ? ex2(v[q] - Li) : 0.f;
