@@ -238,7 +238,7 @@ __device__ __forceinline__ double exp_w_le0(double x) {
 #pragma unroll
   for (int q = 4; q < 16; ++q) p = __fma_rn(p, r, kExpW[q]);
   p = __fma_rn(p, r, kExpW[15]);
-  const long long ki = static_cast<long long>(k);
+  const long long ki = __double2ll_rz(k);  // k is integral; a low x's inf saturates (result dropped)
   const double scale =
       __longlong_as_double(static_cast<long long>(
           static_cast<unsigned long long>(ki + 1023) << 52));
