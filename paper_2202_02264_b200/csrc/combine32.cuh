@@ -554,12 +554,17 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
   // offsets from the shared-memory base keep the compiler on LDS/STS
   const size_t ext = ((reinterpret_cast<char*>(Lrow + N) - reinterpret_cast<char*>(smem)) + 15) &
                      ~static_cast<size_t>(15);
+  // slot records: key i | s << 16 and (frac, shift); slot orders as 16-bit
+  // indices (ns <= 1024), the phase-C order over PT (dead after phase B) —
+  // small enough for 4 CTAs per SM at N = 1024
+  const int ns2 = (ns + 1) & ~1;
   double* PT = reinterpret_cast<double*>(reinterpret_cast<char*>(smem) + ext);  // [ns]
-  int4* REC = reinterpret_cast<int4*>(PT + ((ns + 1) & ~1));                     // [ns]
-  int* ORD1 = reinterpret_cast<int*>(REC + ns);                                   // [ns]
-  int* ORD2 = ORD1 + ns;                                                          // [ns]
-  int* CA = ORD2 + ns;                                                            // [NBA]
-  int* CB = CA + NBA;                                                             // [nsub]
+  int* RKEY = reinterpret_cast<int*>(PT + ns2);                                  // [ns]
+  float2* RFS = reinterpret_cast<float2*>(RKEY + ns2);                          // [ns]
+  uint16_t* ORD1 = reinterpret_cast<uint16_t*>(RFS + ns);                       // [ns]
+  uint16_t* ORD2 = reinterpret_cast<uint16_t*>(PT);                             // [ns]
+  int* CA = reinterpret_cast<int*>(ORD1 + ns2);                                 // [NBA]
+  int* CB = CA + NBA;                                                           // [nsub]
   for (int q = tid; q < NBA; q += blockDim.x) CA[q] = 0;
   for (int q = tid; q < nsub; q += blockDim.x) CB[q] = 0;
   __syncthreads();
@@ -589,7 +594,7 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
   }
   __syncthreads();
   for (int x = tid; x < ns; x += blockDim.x)
-    ORD1[atomicAdd(&CA[min(NBA - 1, (int)(PT[x] * bscale))], 1)] = x;
+    ORD1[atomicAdd(&CA[min(NBA - 1, (int)(PT[x] * bscale))], 1)] = (uint16_t)x;
   __syncthreads();
   // phase B
   int steps = 0;
@@ -652,8 +657,8 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
     frac = fminf(fmaxf(frac, 0.f), 1.f);
     // (i | s << 16, -, frac, shift); N < 2^16. The left block's first map at
     // i is read in phase C, where its latency hides under the recompute.
-    REC[x] = make_int4(i | (s << 16), 0,
-                       __float_as_int(frac), __float_as_int(Brow - Ls_sel));
+    RKEY[x] = i | (s << 16);
+    RFS[x] = make_float2(frac, Brow - Ls_sel);
     atomicAdd(&CB[s], 1);
   }
   __syncthreads();
@@ -671,7 +676,7 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
     }
   }
   __syncthreads();
-  for (int x = tid; x < ns; x += blockDim.x) ORD2[atomicAdd(&CB[REC[x].x >> 16], 1)] = x;
+  for (int x = tid; x < ns; x += blockDim.x) ORD2[atomicAdd(&CB[RKEY[x] >> 16], 1)] = (uint16_t)x;
   __syncthreads();
   // phase C: recompute the sub-block's 64 weights with pass 1's pair
   // arithmetic, two columns per FFMA2 / FADD2 (padding columns give 0); the
@@ -683,27 +688,29 @@ __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
   uint32_t pend_src = 0;
   bool pend = false;
   // (the next slot's record and row vector are prefetched a slot ahead)
-  int x_n = 0;
-  int4 rc_n = make_int4(0, 0, 0, 0);
+  int x_n = 0, key_n = 0;
+  float2 fs_n = make_float2(0.f, 0.f);
   float4 u_n = make_float4(0.f, 0.f, 0.f, 0.f);
   if (tid < ns) {
     x_n = ORD2[tid];
-    rc_n = REC[x_n];
-    u_n = ax.u[rc_n.x & 0xffff];
+    key_n = RKEY[x_n];
+    fs_n = RFS[x_n];
+    u_n = ax.u[key_n & 0xffff];
   }
   for (int o = tid; o < ns; o += blockDim.x) {
-    const int x = x_n;
-    const int4 rc = rc_n;
+    const int x = x_n, key = key_n;
+    const float2 fs = fs_n;
     const float4 urow = u_n;
     if (o + (int)blockDim.x < ns) {
       x_n = ORD2[o + blockDim.x];
-      rc_n = REC[x_n];
-      u_n = ax.u[rc_n.x & 0xffff];
+      key_n = RKEY[x_n];
+      fs_n = RFS[x_n];
+      u_n = ax.u[key_n & 0xffff];
     }
-    const int i = rc.x & 0xffff, s = rc.x >> 16;
+    const int i = key & 0xffff, s = key >> 16;
     const uint32_t first_i = map_first(b, la, ch, L, (uint32_t)i);  // used at the end
-    const float frac = __int_as_float(rc.z);
-    const float sh = __int_as_float(rc.w);
+    const float frac = fs.x;
+    const float sh = fs.y;
     const float2 nsh = make_float2(sh, sh);
     const float2 uu0 = make_float2(urow.x, urow.x), uu1 = make_float2(urow.y, urow.y);
     const float2 uu2 = make_float2(urow.z, urow.z), uu3 = make_float2(urow.w, urow.w);

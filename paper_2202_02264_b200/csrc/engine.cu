@@ -107,6 +107,7 @@ struct dsmc_ctx {
   bool pair_tc2 = false;
   int num_sms = 148;
   int smem_optin = 227 * 1024;  // max dynamic shared memory per CTA (opt-in)
+  int smem_sm = 228 * 1024;     // shared memory per SM
   cudaStream_t copy_stream = nullptr;  // device->host copies overlapping the gather
   static constexpr int kGatherChunks = 8;
   cudaEvent_t gather_ev[kGatherChunks] = {};
@@ -705,10 +706,12 @@ int launch_c32(dsmc_ctx* ctx, const Bufs& b, LevelArgs la, int nk, int systemati
   const size_t NP = (N + 63) / 64 * 64;
   const size_t NPS = NP / 2 + NP / 64;  // column pairs, one skew pad per sub-block
   const size_t ns = la.slots_per_cta, nsub = (N + 63) / 64;
+  const size_t ns2 = (ns + 1) & ~(size_t)1;
   const size_t sm2 = sizeof(double) * (N + 1) + NPS * (16 + 16 + 8) + sizeof(float) * N + 16 +
-                     sizeof(double) * ((ns + 1) & ~(size_t)1) + 16 * ns + 8 * ns +
-                     sizeof(int) * (32 + nsub);
-  const bool sample4 = sm2 <= 48 * 1024;
+                     sizeof(double) * ns2 + 4 * ns2 + 8 * ns + 2 * ns2 + sizeof(int) * (32 + nsub);
+  // the 64-register instantiation where 4 CTAs per SM fit (dynamic + 1 KB
+  // static + 1 KB reserved per CTA)
+  const bool sample4 = 4 * (sm2 + 2048) <= (size_t)ctx->smem_sm;
   if (N >= 65536)
     return set_err(ctx, DSMC_E_INVALID_ARGUMENT,
                    "FP32 dense combine: N must be < 65536 (use a lazy resampler)");
@@ -1473,6 +1476,7 @@ int dsmc_create(int device, dsmc_ctx** out) {
   }
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  cudaDeviceGetAttribute(&ctx->smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
