@@ -409,8 +409,9 @@ __device__ inline double block_scan_incl(double v, double* sh) {
 // search over the row CDF in shared memory, a walk over the row's sub-block
 // sums, and a recomputation of the chosen sub-block's <= 64 weights with
 // pass 1's FP32 pair arithmetic (two columns per FFMA2 / FADD2).
-// MINB: 3 CTAs/SM when N ~ 1024 fills shared memory, 4 (64 registers) for
-// smaller N where the occupancy gain wins (C4 N = 512: 35.1 -> 34.1 ms/sweep)
+// MINB: 4 (64 registers) wherever 4 CTAs fit in shared memory — N <= 1024
+// since the slot records were compacted (C5 sampler 83.1 -> 77.4 ms; C4
+// N = 512: 35.1 -> 34.1 ms/sweep) — else 3
 template <int D, int MINB>
 __global__ void __launch_bounds__(256, MINB) c32_sample(Bufs b, LevelArgs la,
                                                      int systematic) {
