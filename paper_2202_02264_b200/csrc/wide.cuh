@@ -611,7 +611,10 @@ struct Aux32Recompute {
 };
 
 template <int D, class RC = WideRecompute<D>>
-__global__ void __launch_bounds__(256) samplew_kernel(Bufs b, LevelArgs la, int systematic) {
+#ifndef DSMC_SAMPLEW_MINB
+#define DSMC_SAMPLEW_MINB 4  // 64 registers: 4 CTAs per SM (C6 d = 32 sampler ~2x)
+#endif
+__global__ void __launch_bounds__(256, DSMC_SAMPLEW_MINB) samplew_kernel(Bufs b, LevelArgs la, int systematic) {
   extern __shared__ double wsmem[];
   __shared__ double sh[32];
   __shared__ float s_g;
