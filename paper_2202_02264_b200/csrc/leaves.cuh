@@ -268,7 +268,11 @@ __device__ __noinline__ double leaf0_raw_weight(const DevModel& M, const TimeCon
 // top 24 bits of the reference stream's u64s (same Philox4x64-10 stream and
 // counter layout as the FP64 path, rng.cpp:45-86; FP32 rounding only).
 template <int D>
-__global__ void __launch_bounds__(256, 3) leaf32_kernel(Bufs b, double* raw0, int t_off = 0) {
+#ifndef DSMC_LEAF32_MINB
+#define DSMC_LEAF32_MINB 4  // 64 registers: 4 CTAs per SM (C5 leaves 16.6 -> 16.1 ms)
+#endif
+__global__ void __launch_bounds__(256, DSMC_LEAF32_MINB) leaf32_kernel(Bufs b, double* raw0,
+                                                                       int t_off = 0) {
   const int t = t_off + blockIdx.x, ch = blockIdx.y;
   const int gt = b.t0 + t;  // global time (stream key, model data)
   const DevModel& M = b.models[ch];
