@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(32) prepw_kernel(DevModel md, WidePrep o) {
 
 // ---------------------------------------------------------------- leaves
 #ifndef LEAFW_MINB
-#define LEAFW_MINB 2
+#define LEAFW_MINB 3  // C6 d = 32 leaves 1.28 -> 1.16 ms (at 2: 128 registers)
 #endif
 template <int D>
 __global__ void __launch_bounds__(256, LEAFW_MINB) leafw_kernel(Bufs b, double* raw0) {
